@@ -1,0 +1,200 @@
+"""MoE application of the static batching framework — fp64 oracle.
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+Definitions followed (P:n = PAPER.md line n):
+* token-index buckets: "a token index array for every expert, containing the
+  indices of the tokens routed to the expert"; canonical order within a
+  bucket is ascending token id (reading R3 — the paper's atomic
+  scatter P:336 leaves it unspecified).
+* experts as tasks, tile count nu = ceil(m/BM) * ceil(N/BN) per task
+  (K is not split, R4), sigma over non-empty tasks.
+* intra-task tile order: row-tile fastest, rt = l mod R, ct = l div R with
+  R = ceil(rows/BM) (R5; the paper leaves it open, "tile
+  swizzle").
+* expert GEMM: Y[row_off[e] + r, :] = X[token_idx_e[r], :] @ W[e] — the unbatched
+  per-expert loop of P:100-101 evaluated in fp64 (numpy matmul is the library
+  primitive for each expert's product).
+* expert parallelism: experts [g*E/G, (g+1)*E/G) live on rank g;
+  tokens [g*T/G, (g+1)*T/G) are owned by rank g (R8).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import mapping
+
+
+# ---------------------------------------------------------------------------
+# c1 — buckets
+# ---------------------------------------------------------------------------
+def buckets(topk_ids: np.ndarray, E: int):
+    """Returns (counts[E], row_off[E+1], token_idx[sum counts], slot[sum counts]).
+
+    token_idx[row_off[e] + r] is the r-th smallest token routed to expert e;
+    slot[...] is the top-k position j with topk_ids[t, j] == e.  Raises
+    ValueError for ids outside [0, E) or a token listing one expert twice."""
+    topk_ids = np.asarray(topk_ids)
+    T, k = topk_ids.shape
+    lists: list[list[tuple[int, int]]] = [[] for _ in range(E)]
+    for t in range(T):
+        seen = set()
+        for j in range(k):
+            e = int(topk_ids[t, j])
+            if e < 0 or e >= E:
+                raise ValueError(f"expert id {e} out of range")
+            if e in seen:
+                raise ValueError(f"token {t} routes to expert {e} twice")
+            seen.add(e)
+            lists[e].append((t, j))          # t visited in ascending order
+    counts = np.array([len(b) for b in lists], dtype=np.int64)
+    row_off = np.zeros(E + 1, dtype=np.int64)
+    for e in range(E):
+        row_off[e + 1] = row_off[e] + counts[e]
+    token_idx = np.array([t for b in lists for (t, _) in b], dtype=np.int64)
+    slot = np.array([j for b in lists for (_, j) in b], dtype=np.int64)
+    return counts, row_off, token_idx, slot
+
+
+# ---------------------------------------------------------------------------
+# c2 — plan: experts as tasks, Alg. 1 + Alg. 4's non-empty stage
+# ---------------------------------------------------------------------------
+def ceil_div(a: int, b: int) -> int:
+    return -(-a // b)
+
+
+def tiles_of(rows: int, N: int, bm: int, bn: int) -> int:
+    """nu(T) = ceil(m/BM) * ceil(N/BN); 0 iff m == 0 (SPEC tile_count)."""
+    if rows == 0:
+        return 0
+    return ceil_div(rows, bm) * ceil_div(N, bn)
+
+
+def make_tasks(counts, bm: int, bn: int) -> list[dict]:
+    """One task per expert, kind 0 with tile bm x bn."""
+    return [dict(expert=e, row_begin=0, rows=int(m), bm=bm, bn=bn, kind=0) for e, m in enumerate(counts)]
+
+
+def plan(counts, N: int, bm: int, bn: int, pad_mode: str = "max", warp_size: int = 32,
+         tasks: list[dict] | None = None) -> dict:
+    """Host-side plan: nu per task, sigma (non-empty tasks, natural order), TilePrefix
+    (Alg. 1 over eta), padded per P:203."""
+    if tasks is None:
+        tasks = make_tasks(counts, bm, bn)
+    nu = [tiles_of(t["rows"], N, t["bm"], t["bn"]) for t in tasks]
+    sigma, prefix = mapping.nonempty_stage(nu)
+    padded = mapping.pad_tile_prefix(prefix, warp_size, pad_mode) if prefix else []
+    return dict(tasks=tasks, nu=nu, sigma=sigma, prefix=prefix, padded=padded,
+                M=len(sigma), total=mapping.total_tiles(prefix), N=N, warp_size=warp_size)
+
+
+# ---------------------------------------------------------------------------
+# c3 — decode one virtual tile (block index) into its GEMM tile
+# ---------------------------------------------------------------------------
+def decode(pl: dict, row_off, B: int) -> dict:
+    """Alg. 4 then the intra-task tile split (R5)."""
+    if not (0 <= B < pl["total"]):
+        raise ValueError("block index out of range")
+    h, j, l = mapping.mapping_extended(pl["padded"], pl["sigma"], B, pl["warp_size"])
+    task = pl["tasks"][j]
+    R = ceil_div(task["rows"], task["bm"])
+    rt = l % R
+    ct = l // R
+    e = task["expert"]
+    r0 = int(row_off[e]) + task["row_begin"] + rt * task["bm"]
+    r1 = int(row_off[e]) + task["row_begin"] + min((rt + 1) * task["bm"], task["rows"])
+    c0 = ct * task["bn"]
+    c1 = min(c0 + task["bn"], pl["N"])
+    return dict(h=h, task=j, expert=e, l=l, rt=rt, ct=ct, rows=(r0, r1), cols=(c0, c1), kind=task["kind"])
+
+
+def tile_cover(pl: dict, row_off, n_rows: int) -> np.ndarray:
+    """Write-count shadow buffer: how many tiles cover each Y element."""
+    cover = np.zeros((n_rows, pl["N"]), dtype=np.int64)
+    for B in range(pl["total"]):
+        d = decode(pl, row_off, B)
+        cover[d["rows"][0]:d["rows"][1], d["cols"][0]:d["cols"][1]] += 1
+    return cover
+
+
+# ---------------------------------------------------------------------------
+# c4 — the expert GEMM, unbatched, fp64
+# ---------------------------------------------------------------------------
+def expert_gemm(X: np.ndarray, W: np.ndarray, token_idx, row_off) -> np.ndarray:
+    """Y[row_off[e]+r, :] = X[token_idx[row_off[e]+r], :] @ W[e] for e = 0..E-1."""
+    E = W.shape[0]
+    Y = np.zeros((int(row_off[E]), W.shape[2]), dtype=np.float64)
+    for e in range(E):
+        a, b = int(row_off[e]), int(row_off[e + 1])
+        if b > a:
+            Y[a:b] = X[np.asarray(token_idx[a:b], dtype=np.int64)].astype(np.float64) @ W[e].astype(np.float64)
+    return Y
+
+
+def expert_gemm_entries(x_row, w_cols, token_idx, row_off, rows, cols) -> np.ndarray:
+    """Sampled entries of the same product: out[i, c] = sum_h X[t_i, h] * W[e_i, h, cols[c]]
+    for CSR rows ``rows`` (t_i = token_idx[row], e_i = the expert owning that row).
+
+    ``x_row(t) -> [H]`` and ``w_cols(e, cols) -> [H, len(cols)]`` fetch inputs on
+    demand so full-size parity never materialises W on the host."""
+    E = len(row_off) - 1
+    out = np.zeros((len(rows), len(cols)))
+    for i, r in enumerate(rows):
+        e = 0
+        while not (row_off[e] <= r < row_off[e + 1]):
+            e += 1
+            if e >= E:
+                raise ValueError("row outside the CSR")
+        t = int(token_idx[r])
+        out[i] = np.asarray(x_row(t), dtype=np.float64) @ np.asarray(w_cols(e, cols), dtype=np.float64)
+    return out
+
+
+# ---------------------------------------------------------------------------
+# combine order and expert parallelism
+# ---------------------------------------------------------------------------
+def per_slot_outputs(topk_ids, X, W) -> np.ndarray:
+    """Definition used by EP checks: out[t*k + j] = X[t] @ W[topk[t, j]]."""
+    T, k = topk_ids.shape
+    out = np.zeros((T * k, W.shape[2]))
+    for t in range(T):
+        for j in range(k):
+            out[t * k + j] = X[t].astype(np.float64) @ W[int(topk_ids[t, j])].astype(np.float64)
+    return out
+
+
+def ep_simulate(topk_ids: np.ndarray, X: np.ndarray, W: np.ndarray, G: int) -> dict:
+    """In-process expert-parallel simulation.
+
+    Rank g owns experts [g*E/G, (g+1)*E/G) and tokens [g*T/G, (g+1)*T/G).
+    Dispatch sends each owned token once to every rank hosting >= 1 of its
+    experts (dedup per destination); the receiving rank buckets the received rows
+    per local expert (ascending global token id), multiplies, and returns each
+    (t, slot) row to the token's owner, which places it at t_local*k + slot."""
+    T, k = topk_ids.shape
+    E = W.shape[0]
+    if E % G or T % G:
+        raise ValueError("E and T must be divisible by G")
+    El, Tl = E // G, T // G
+    owner_of_expert = [e // El for e in range(E)]
+    sent_rows = np.zeros((G, G), dtype=np.int64)       # [src, dst]
+    recv: list[list[int]] = [[] for _ in range(G)]     # global token ids received by rank d
+    for g in range(G):
+        for d in range(G):
+            for t in range(g * Tl, (g + 1) * Tl):
+                if any(owner_of_expert[int(e)] == d for e in topk_ids[t]):
+                    recv[d].append(t)
+                    sent_rows[g, d] += 1
+    out = [np.zeros((Tl * k, W.shape[2])) for _ in range(G)]
+    local_counts = np.zeros((G, El), dtype=np.int64)
+    for d in range(G):
+        rows = recv[d]                                  # ascending global token ids
+        for el in range(El):
+            e = d * El + el
+            members = [(i, t) for i, t in enumerate(rows) if e in set(int(x) for x in topk_ids[t])]
+            local_counts[d, el] = len(members)
+            for (i, t) in members:
+                y = X[t].astype(np.float64) @ W[e].astype(np.float64)
+                j = [int(x) for x in topk_ids[t]].index(e)
+                g = t // Tl
+                out[g][(t - g * Tl) * k + j] = y
+    return dict(out=out, sent_rows=sent_rows, local_counts=local_counts, recv=recv)
