@@ -1,0 +1,183 @@
+/*
+ * moe_sm100.h — C ABI of the single-launch, statically batched MoE expert GEMM
+ * for NVIDIA B200 (sm_100a).  Method: arXiv 2501.16103 ("P:n" = line n of the
+ * paper's LaTeX source, /root/reference/PAPER.md; see DESIGN.md for readings).
+ *
+ *   moe_route      tokens' top-k expert ids -> per-expert token-index arrays
+ *                  (CSR).
+ *   moe_plan_*     expert token counts + tile shape -> the compressed mapping:
+ *                  TilePrefix over non-empty tasks (Alg. 1; Alg. 4's
+ *                  extra stage) plus sigma and task parameters p_i.
+ *   moe_gemm       ONE kernel launch computing every (expert, output-tile) task:
+ *                  each CTA decodes (task, tile) on device with the warp
+ *                  vote/popcount algorithm (Alg. 2), gathers its
+ *                  token rows through the token-index array and
+ *                  multiplies them by that expert's weight slice.
+ *   moe_decode_debug  the device decode alone, for bit-exact parity tests.
+ *
+ * Conventions (all entry points):
+ *   - Plain pointers and sizes only.  "_dev" = device memory, "_host" = host
+ *     memory.  All tensors are caller-owned; the library never frees them.
+ *   - `stream` is a cudaStream_t (passed as void*).  Device work is enqueued
+ *     on it; no entry point synchronises the stream.
+ *   - Return codes: moe_status below.  No C++ exception crosses the ABI.  On a
+ *     non-OK status nothing has been enqueued and moe_last_error() returns a
+ *     thread-local message.  Asynchronous CUDA faults surface at the caller's
+ *     next synchronisation, as for any CUDA library.
+ *   - Indices are 0-based (reading R1).  Rows of the token-index
+ *     array are grouped by expert in ascending expert id; within an expert they
+ *     are in ascending token id (reading R3).
+ */
+#ifndef MOE_SM100_H_
+#define MOE_SM100_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t moe_status;
+#define MOE_OK               0   /* success                                                     */
+#define MOE_OK_EMPTY         1   /* success, nothing to compute (every expert empty): no launch */
+#define MOE_ERR_INVALID     (-1) /* bad argument, shape, null or misaligned pointer             */
+#define MOE_ERR_UNSUPPORTED (-2) /* H%8, N%8 (TMA needs 16-byte strides), tile shape, non-sm_100 */
+#define MOE_ERR_CAPACITY    (-3) /* int32 overflow of rows / tiles, too many tasks, buffer small */
+#define MOE_ERR_CUDA        (-4) /* a CUDA runtime/driver call failed (message has the name)     */
+#define MOE_ERR_NCCL        (-5) /* reserved for the expert-parallel layer                       */
+
+/* Output element types of moe_gemm. */
+#define MOE_DTYPE_BF16 0
+#define MOE_DTYPE_F32  1
+
+/* Plan flags. */
+#define MOE_PAD_MAX     0u  /* pad TilePrefix with INT32_MAX ("the maximum possible value") */
+#define MOE_PAD_REPEAT  1u  /* pad TilePrefix by repeating its last element                */
+
+/* ---- the compressed mapping ("plan blob"), int32 words -------------------
+ * Built on the host by moe_plan_build (no GPU needed) and copied once to the
+ * device by moe_plan_create ("pre-computed on the host and then copied to the
+ * device").  Layout:
+ *   [0]  MOE_PLAN_MAGIC          [1] M  = number of non-empty tasks (|eta|)
+ *   [2]  total virtual tiles     [3] M_pad = M rounded up to a multiple of 32 (>= 32)
+ *   [4]  E (experts)             [5] N (expert output width)   [6] H (hidden = GEMM K)
+ *   [7]  BM (tile rows)          [8] BN (tile cols)            [9] n_tasks (tasks incl. empty)
+ *   [10] flags                   [11..15] reserved (0)
+ *   [16 .. 16+M_pad)               TilePrefix: inclusive prefix of nu over the
+ *                                  non-empty tasks (Alg. 1), padded
+ *   [16+M_pad .. 16+2*M_pad)       sigma: non-empty index -> task index,
+ *                                  padded with 0
+ *   [16+2*M_pad .. +8*n_tasks)     task parameters p_i, 8 words per
+ *                                  task i: {expert, row0, rows, kind, bm, bn,
+ *                                  row_tiles, col_tiles}; row0 = first CSR row of
+ *                                  the task (= row_off[expert] + offset in expert)
+ *   [.. +E+1)                      row_off: exclusive prefix of counts (CSR offsets)
+ * nu(task) = row_tiles * col_tiles, row_tiles = ceil(rows/BM), col_tiles = ceil(N/BN).
+ * Intra-task tile order: row tile fastest, rt = l mod row_tiles, ct = l div
+ * row_tiles (reading R5).
+ */
+#define MOE_PLAN_MAGIC      0x4d4f4531  /* "MOE1" */
+#define MOE_PLAN_HEADER     16
+#define MOE_PLAN_TASK_WORDS 8
+
+/* Number of int32 words moe_plan_build needs for E experts (upper bound). */
+int64_t moe_plan_blob_words(int32_t E);
+
+/*
+ * Build the compressed mapping on the host.
+ *   counts_host [E]  tokens routed to each expert (m_e >= 0), host memory.
+ *   H, N             GEMM K and expert output width; both must be multiples of 8.
+ *   bm, bn           tile shape.  bm must be 128 (tcgen05 M=128); bn % 16 == 0,
+ *                    16 <= bn <= 256.
+ *   flags            MOE_PAD_MAX | MOE_PAD_REPEAT.
+ *   blob, blob_cap   caller buffer of blob_cap int32 words (see moe_plan_blob_words).
+ *   blob_len         out: words written.
+ * Returns MOE_OK, MOE_OK_EMPTY (all experts empty: M = 0, total = 0),
+ * MOE_ERR_INVALID, MOE_ERR_UNSUPPORTED or MOE_ERR_CAPACITY (sum of counts or
+ * total tiles >= 2^31, blob_cap too small).  Pure host code: never touches CUDA.
+ */
+moe_status moe_plan_build(const int32_t* counts_host, int32_t E, int64_t H, int64_t N,
+                          int32_t bm, int32_t bn, uint32_t flags,
+                          int32_t* blob, int64_t blob_cap, int64_t* blob_len);
+
+/* Opaque plan: the host blob plus its device copy (library-owned). */
+typedef struct moe_plan moe_plan;
+
+/*
+ * moe_plan_build + one stream-ordered H2D copy of the blob into a device buffer
+ * owned by the plan (the copy is "very small" — its length is the
+ * number of tasks, not the number of blocks).  The plan is bound to `stream`:
+ * moe_gemm / moe_decode_debug must be enqueued on the same stream (or after an
+ * event on it).  On MOE_OK_EMPTY a valid plan with total = 0 is returned.
+ */
+moe_status moe_plan_create(const int32_t* counts_host, int32_t E, int64_t H, int64_t N,
+                           int32_t bm, int32_t bn, uint32_t flags, void* stream, moe_plan** out);
+
+/* Re-plan in place for new counts (same E, H, N, bm, bn, flags); reuses the device buffer. */
+moe_status moe_plan_update(moe_plan* plan, const int32_t* counts_host, void* stream);
+
+/* Scalars of a plan (any pointer may be NULL). */
+moe_status moe_plan_query(const moe_plan* plan, int32_t* M, int32_t* total_tiles, int32_t* M_pad);
+
+/* Copy of the host blob into a caller buffer of cap words; *len = blob words. */
+moe_status moe_plan_blob(const moe_plan* plan, int32_t* out, int64_t cap, int64_t* len);
+
+/* Device address of the plan blob (same layout), for debugging and tests. */
+const int32_t* moe_plan_device_blob(const moe_plan* plan);
+
+/* Stream-ordered release of the device buffer (safe while work using it is in flight). */
+void moe_plan_destroy(moe_plan* plan);
+
+/*
+ * Token-index buckets on device, stable: token_idx[row_off[e] + r]
+ * is the r-th smallest token id t with e in topk_ids[t, :].
+ *   topk_ids_dev [T, k] int32 row-major, expert ids in [0, E); no token may list
+ *                an expert twice.
+ *   counts_dev   [E]   out: m_e.
+ *   row_off_dev  [E+1] out: exclusive prefix of counts.
+ *   token_idx_dev[T*k] out.
+ *   slot_dev     [T*k] out (nullable): the top-k position j of each row.
+ *   status_dev   [1]   out (nullable): set to 0, or to 1 if an id was out of range
+ *                      or duplicated in a token (those entries are dropped).
+ * Two kernel launches on `stream`; T*k < 2^31, 1 <= k <= 32, 1 <= E <= 1024.
+ */
+moe_status moe_route(const int32_t* topk_ids_dev, int64_t T, int32_t k, int32_t E,
+                     int32_t* counts_dev, int32_t* row_off_dev, int32_t* token_idx_dev,
+                     int32_t* slot_dev, int32_t* status_dev, void* stream);
+
+/*
+ * The hot path: Y[row0 + r, n] = sum_h X[token_idx[row0 + r], h] * W[e, h, n]
+ * for every task of the plan, in ONE persistent kernel launch (sm_100a: TMA
+ * gather4 of token rows, TMA tiles of W, tcgen05.mma with fp32 accumulation in
+ * TMEM, warp-specialised pipeline).
+ *   X_dev         [T, H] bf16 row-major (token activations), 16-byte aligned.
+ *   token_idx_dev [sum m_e] int32, the CSR of moe_route, consistent with the
+ *                 plan's counts (not re-checked on device).
+ *   W_dev         [E, H, N] bf16 row-major (expert weights), 16-byte aligned.
+ *   Y_dev         [sum m_e, N] of y_dtype (MOE_DTYPE_BF16: fp32 accumulate, RNE
+ *                 to bf16; MOE_DTYPE_F32: the fp32 accumulator), 16-byte aligned.
+ * Returns MOE_OK_EMPTY without launching when the plan has no tiles.
+ */
+moe_status moe_gemm(const moe_plan* plan, const void* X_dev, int64_t T, const int32_t* token_idx_dev,
+                    const void* W_dev, void* Y_dev, int32_t y_dtype, void* stream);
+
+/*
+ * Device decode of every virtual tile B in [0, total) with the same device
+ * function moe_gemm uses: out_dev[5*B .. 5*B+5) = {h, task, l, rt, ct}
+ * (h = non-empty task index, task = sigma(h), l = tile index in the task).
+ */
+moe_status moe_decode_debug(const moe_plan* plan, int32_t* out_dev, void* stream);
+
+/* Number of SMs of the current device, and a check that it is sm_100 (MOE_OK) or not. */
+moe_status moe_device_info(int32_t* sm_count, int32_t* cc_major, int32_t* cc_minor);
+
+/* Thread-local message describing the last non-OK status ("" if none). */
+const char* moe_last_error(void);
+
+/* Library version string. */
+const char* moe_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MOE_SM100_H_ */

@@ -1,0 +1,256 @@
+"""Thin Python binding over libmoe_sm100.so (C ABI in include/moe_sm100.h).
+
+Argument marshalling only: every step of the path (routing buckets, the
+compressed mapping decode, the gathered tcgen05 GEMM) runs in the library's
+CUDA kernels; the host planner runs in the library's C++ code.  PyTorch is used
+for device memory and streams.  There is no CPU fallback: if the library is
+missing or the device is not sm_100, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libmoe_sm100.so")
+
+MOE_OK, MOE_OK_EMPTY = 0, 1
+MOE_ERR = {-1: "INVALID", -2: "UNSUPPORTED", -3: "CAPACITY", -4: "CUDA", -5: "NCCL"}
+MOE_DTYPE_BF16, MOE_DTYPE_F32 = 0, 1
+MOE_PAD_MAX, MOE_PAD_REPEAT = 0, 1
+MOE_PLAN_MAGIC = 0x4D4F4531
+MOE_PLAN_HEADER = 16
+MOE_PLAN_TASK_WORDS = 8
+
+# Public symbols of include/moe_sm100.h and include/moe_sm100_debug.h.
+EXPORTED = (
+    "moe_plan_blob_words", "moe_plan_build", "moe_plan_create", "moe_plan_update", "moe_plan_query",
+    "moe_plan_blob", "moe_plan_device_blob", "moe_plan_destroy", "moe_route", "moe_gemm",
+    "moe_decode_debug", "moe_device_info", "moe_last_error", "moe_version", "moe_probe_gather4",
+)
+
+
+class MoeError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"moe status {status} ({MOE_ERR.get(status, '?')}): {msg}")
+        self.status = status
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load the in-tree library (raises if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} missing: run `python -m paper_2501_16103_b200.build` "
+                           "(or __graft_entry__.build()) — there is no fallback path")
+    L = ctypes.CDLL(LIB_PATH)
+    c_i32p = ctypes.POINTER(ctypes.c_int32)
+    c_i64p = ctypes.POINTER(ctypes.c_int64)
+    vp = ctypes.c_void_p
+    sig = {
+        "moe_plan_blob_words": (ctypes.c_int64, [ctypes.c_int32]),
+        "moe_plan_build": (ctypes.c_int32, [c_i32p, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32,
+                                            ctypes.c_int32, ctypes.c_uint32, c_i32p, ctypes.c_int64, c_i64p]),
+        "moe_plan_create": (ctypes.c_int32, [c_i32p, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32,
+                                             ctypes.c_int32, ctypes.c_uint32, vp, ctypes.POINTER(vp)]),
+        "moe_plan_update": (ctypes.c_int32, [vp, c_i32p, vp]),
+        "moe_plan_query": (ctypes.c_int32, [vp, c_i32p, c_i32p, c_i32p]),
+        "moe_plan_blob": (ctypes.c_int32, [vp, c_i32p, ctypes.c_int64, c_i64p]),
+        "moe_plan_device_blob": (vp, [vp]),
+        "moe_plan_destroy": (None, [vp]),
+        "moe_route": (ctypes.c_int32, [vp, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, vp, vp, vp, vp, vp, vp]),
+        "moe_gemm": (ctypes.c_int32, [vp, vp, ctypes.c_int64, vp, vp, vp, ctypes.c_int32, vp]),
+        "moe_decode_debug": (ctypes.c_int32, [vp, vp, vp]),
+        "moe_device_info": (ctypes.c_int32, [c_i32p, c_i32p, c_i32p]),
+        "moe_last_error": (ctypes.c_char_p, []),
+        "moe_version": (ctypes.c_char_p, []),
+        "moe_probe_gather4": (ctypes.c_int32, [vp, ctypes.c_int64, ctypes.c_int64, vp, ctypes.c_int32, vp, vp]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = L
+    return L
+
+
+def _check(status: int) -> int:
+    if status < 0:
+        raise MoeError(status, lib().moe_last_error().decode())
+    return status
+
+
+def _i32ptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+
+
+# ---------------------------------------------------------------------------
+# plan (host, no GPU needed)
+# ---------------------------------------------------------------------------
+def moe_plan_build(counts, H: int, N: int, bm: int = 128, bn: int = 256, flags: int = MOE_PAD_MAX) -> np.ndarray:
+    """The compressed mapping blob (int32 words, layout in include/moe_sm100.h)."""
+    c = np.ascontiguousarray(np.asarray(counts, dtype=np.int32))
+    E = int(c.shape[0])
+    L = lib()
+    cap = int(L.moe_plan_blob_words(E)) if E > 0 else 64
+    blob = np.zeros(max(cap, 16), dtype=np.int32)
+    n = ctypes.c_int64(0)
+    _check(L.moe_plan_build(_i32ptr(c), E, H, N, bm, bn, flags, _i32ptr(blob), blob.size, ctypes.byref(n)))
+    return blob[: n.value].copy()
+
+
+def parse_plan_blob(blob: np.ndarray) -> dict:
+    """Split a blob into named arrays (layout of include/moe_sm100.h)."""
+    b = np.asarray(blob)
+    if int(b[0]) != MOE_PLAN_MAGIC:
+        raise ValueError("not a plan blob")
+    M, total, M_pad, E, N, H, bm, bn, n_tasks, flags = (int(x) for x in b[1:11])
+    o = MOE_PLAN_HEADER
+    prefix = b[o:o + M_pad]
+    sigma = b[o + M_pad:o + 2 * M_pad]
+    po = o + 2 * M_pad
+    params = b[po:po + MOE_PLAN_TASK_WORDS * n_tasks].reshape(n_tasks, MOE_PLAN_TASK_WORDS)
+    row_off = b[po + MOE_PLAN_TASK_WORDS * n_tasks: po + MOE_PLAN_TASK_WORDS * n_tasks + E + 1]
+    return dict(M=M, total=total, M_pad=M_pad, E=E, N=N, H=H, bm=bm, bn=bn, n_tasks=n_tasks, flags=flags,
+                prefix=prefix, sigma=sigma, params=params, row_off=row_off)
+
+
+def _stream(stream=None) -> int:
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+class Plan:
+    """Device-resident plan (moe_plan_create / moe_plan_update / moe_plan_destroy)."""
+
+    def __init__(self, counts, H: int, N: int, bm: int = 128, bn: int = 256, flags: int = MOE_PAD_MAX,
+                 stream=None):
+        c = np.ascontiguousarray(np.asarray(counts, dtype=np.int32))
+        self.E, self.H, self.N, self.bm, self.bn, self.flags = int(c.shape[0]), H, N, bm, bn, flags
+        self._h = ctypes.c_void_p()
+        self.status = _check(lib().moe_plan_create(_i32ptr(c), self.E, H, N, bm, bn, flags, _stream(stream),
+                                                   ctypes.byref(self._h)))
+
+    def update(self, counts, stream=None) -> int:
+        c = np.ascontiguousarray(np.asarray(counts, dtype=np.int32))
+        self.status = _check(lib().moe_plan_update(self._h, _i32ptr(c), _stream(stream)))
+        return self.status
+
+    def query(self) -> tuple[int, int, int]:
+        M, total, M_pad = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+        _check(lib().moe_plan_query(self._h, ctypes.byref(M), ctypes.byref(total), ctypes.byref(M_pad)))
+        return M.value, total.value, M_pad.value
+
+    @property
+    def total_tiles(self) -> int:
+        return self.query()[1]
+
+    def blob(self) -> np.ndarray:
+        n = ctypes.c_int64()
+        _check(lib().moe_plan_blob(self._h, None, 0, ctypes.byref(n)))
+        out = np.zeros(n.value, dtype=np.int32)
+        _check(lib().moe_plan_blob(self._h, _i32ptr(out), out.size, ctypes.byref(n)))
+        return out
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if self._h:
+            lib().moe_plan_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ---------------------------------------------------------------------------
+# device entry points
+# ---------------------------------------------------------------------------
+def moe_device_info() -> tuple[int, int, int]:
+    n, ma, mi = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    _check(lib().moe_device_info(ctypes.byref(n), ctypes.byref(ma), ctypes.byref(mi)))
+    return n.value, ma.value, mi.value
+
+
+def moe_route(topk_ids, E: int, with_slot: bool = True, stream=None):
+    """topk_ids: int32 CUDA tensor [T, k] -> (counts[E], row_off[E+1], token_idx[T*k], slot, status)."""
+    import torch
+
+    assert topk_ids.is_cuda and topk_ids.dtype == torch.int32 and topk_ids.is_contiguous()
+    T, k = topk_ids.shape
+    dev = topk_ids.device
+    counts = torch.empty(E, dtype=torch.int32, device=dev)
+    row_off = torch.empty(E + 1, dtype=torch.int32, device=dev)
+    token_idx = torch.empty(max(T * k, 1), dtype=torch.int32, device=dev)
+    slot = torch.empty(max(T * k, 1), dtype=torch.int32, device=dev) if with_slot else None
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    _check(lib().moe_route(topk_ids.data_ptr(), T, k, E, counts.data_ptr(), row_off.data_ptr(),
+                           token_idx.data_ptr(), slot.data_ptr() if slot is not None else None,
+                           status.data_ptr(), _stream(stream)))
+    return counts, row_off, token_idx[: T * k], (slot[: T * k] if slot is not None else None), status
+
+
+def moe_gemm(plan: Plan, X, token_idx, W, Y=None, out_dtype=None, stream=None):
+    """Y[sum m_e, N] = per-expert X[token_idx] @ W[e] in one launch."""
+    import torch
+
+    out_dtype = out_dtype or torch.bfloat16
+    assert X.is_cuda and X.dtype == torch.bfloat16 and X.is_contiguous()
+    assert W.is_cuda and W.dtype == torch.bfloat16 and W.is_contiguous()
+    assert token_idx.dtype == torch.int32 and token_idx.is_contiguous()
+    rows = int(token_idx.numel())
+    if Y is None:
+        Y = torch.empty((rows, plan.N), dtype=out_dtype, device=X.device)
+    yd = MOE_DTYPE_F32 if Y.dtype == torch.float32 else MOE_DTYPE_BF16
+    _check(lib().moe_gemm(plan.handle, X.data_ptr(), X.shape[0], token_idx.data_ptr(), W.data_ptr(),
+                          Y.data_ptr(), yd, _stream(stream)))
+    return Y
+
+
+def moe_decode_debug(plan: Plan, stream=None):
+    import torch
+
+    total = plan.total_tiles
+    out = torch.full((max(total, 1), 5), -1, dtype=torch.int32, device="cuda")
+    _check(lib().moe_decode_debug(plan.handle, out.data_ptr(), _stream(stream)))
+    return out[:total]
+
+
+def moe_probe_gather4(X, rows, col0: int, stream=None):
+    import torch
+
+    out = torch.zeros(16384, dtype=torch.uint8, device=X.device)
+    _check(lib().moe_probe_gather4(X.data_ptr(), X.shape[0], X.shape[1], rows.data_ptr(), col0, out.data_ptr(),
+                                   _stream(stream)))
+    return out
+
+
+def moe_forward(topk_ids, X, W, E: int, bm: int = 128, bn: int = 256, out_dtype=None, plan: Plan | None = None,
+                stream=None):
+    """One MoE expert-GEMM step on device: route -> counts D2H -> host plan -> single-launch GEMM.
+
+    Returns (Y, counts_host, row_off, token_idx, slot, plan)."""
+    import torch
+
+    counts, row_off, token_idx, slot, _ = moe_route(topk_ids, E, stream=stream)
+    counts_h = counts.cpu().numpy()            # the planner runs on the host
+    H, N = int(X.shape[1]), int(W.shape[2])
+    if plan is None:
+        plan = Plan(counts_h, H, N, bm, bn, stream=stream)
+    else:
+        plan.update(counts_h, stream=stream)
+    Y = moe_gemm(plan, X, token_idx, W, out_dtype=out_dtype or torch.bfloat16, stream=stream)
+    return Y, counts_h, row_off, token_idx, slot, plan

@@ -1,0 +1,33 @@
+// Internal helpers shared by the library's translation units (not part of the ABI).
+#pragma once
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include "moe_sm100.h"
+
+namespace moe {
+
+void set_error(const char* fmt, ...);
+void clear_error();
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Host-side view of a plan blob (offsets into the int32 word array).
+struct BlobView {
+  int32_t M, total, M_pad, E, N, H, bm, bn, n_tasks;
+  uint32_t flags;
+  int64_t off_prefix, off_sigma, off_params, off_row_off, words;
+};
+bool blob_view(const int32_t* blob, int64_t len, BlobView* v);
+
+struct moe_plan_impl;
+
+}  // namespace moe
+
+#define MOE_FAIL(status, ...)        \
+  do {                               \
+    ::moe::set_error(__VA_ARGS__);   \
+    return (status);                 \
+  } while (0)

@@ -1,0 +1,507 @@
+// Single-launch statically batched MoE expert GEMM for sm_100a (B200).
+//
+// One persistent, warp-specialised kernel executes every (expert, output-tile)
+// task of a plan (arXiv 2501.16103, Alg. 3/4):
+//   * every role warp decodes its virtual tile v with the warp vote/popcount
+//     mapping over TilePrefix (Alg. 2 + chunk loop) and sigma (Alg. 4
+//     line 289) — "let all warps execute the algorithm";
+//   * warp 0 (producer) stages, per 64-wide K block, the tile's token rows with
+//     TMA tile::gather4 straight from X through the token-index array (P:334-335,
+//     no gathered copy) and the expert's W block with 3-D TMA tile loads, into a
+//     4-stage SW128 shared-memory ring guarded by mbarriers (deepened);
+//   * warp 1 issues tcgen05.mma (M=128, N=BN, K=16, bf16 x bf16 -> fp32) into a
+//     double-buffered TMEM accumulator (P:351's WGMMA, Blackwell-native);
+//   * warps 2-5 drain TMEM with tcgen05.ld, convert and store Y rows, masked to
+//     the task's rows and to N, overlapping the next tile's main loop.
+// Static batching: CTA b processes v = b, b + grid, b + 2*grid, ... (no
+// dynamic scheduler, no atomics).  Within a task, tiles are ordered row-tile
+// fastest (R5), so CTAs of one wave share W column blocks in L2
+// (the paper's "tile swizzle").
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <mutex>
+
+#include "common.h"
+#include "moe_sm100_debug.h"
+#include "sm100_ptx.cuh"
+
+namespace moe {
+const int32_t* plan_blob_host(const moe_plan* p, int64_t* words);
+const int32_t* plan_blob_dev(const moe_plan* p);
+}  // namespace moe
+
+namespace {
+
+using namespace moe::ptx;
+
+constexpr int kBM = 128;                        // tile rows = tcgen05 M
+constexpr int kBK = 64;                         // K block: 64 bf16 = one 128-byte swizzle row
+constexpr int kStages = 4;
+constexpr int kABytes = kBM * kBK * 2;          // 16 KB: 128 gathered rows x 64
+constexpr int kBBoxBytes = 64 * kBK * 2;        // 8 KB: one TMA box of W (64 N x 64 K)
+constexpr int kBStageBytes = 4 * kBBoxBytes;    // up to BN = 256
+constexpr int kEpiWarps = 4;
+constexpr int kThreads = 32 * (2 + kEpiWarps);  // producer, MMA, 4 epilogue warps
+constexpr uint32_t kTmemCols = 512;             // 2 accumulators x 256 fp32 columns
+constexpr uint32_t kAccCols = 256;
+constexpr int kMaxMPad = 1024;
+constexpr int kBarBytes = 128;
+constexpr size_t kSmemFixed = 1024 /*align slack*/ + (size_t)kStages * (kABytes + kBStageBytes) + kBarBytes;
+
+struct GemmArgs {
+  const int32_t* plan;       // device plan blob
+  const int32_t* token_idx;  // CSR token-index array
+  void* Y;
+  int32_t y_f32;
+  int32_t N;
+  int32_t num_kb;
+  int32_t total;
+  int32_t M_pad;
+  int32_t off_params;
+};
+
+// ---------------------------------------------------------------------------
+// Alg. 2 with the chunk loop and Alg. 4's sigma.
+// Executed by a full warp; v must be warp-uniform and < total.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void map_tile(const int32_t* prefix, const int32_t* sigma, int M_pad, int v,
+                                         int& h, int& task, int& l) {
+  const int lane = threadIdx.x & 31;
+  int hh = 0;
+  for (int c = 0; c < M_pad; c += 32) {
+    const bool p = v >= prefix[c + lane];                  // p <- B >= TilePrefix[t]
+    const unsigned mask = __ballot_sync(0xffffffffu, p);   // warp vote
+    const int cnt = __popc(mask);                          // population count
+    hh += cnt;
+    if (cnt < 32) break;
+  }
+  const int base = hh > 0 ? prefix[hh - 1] : 0;            // k <- TilePrefix[h-1] (or 0)
+  h = hh;
+  l = v - base;                                            // l <- B - k
+  task = sigma[hh];                                        // h~ <- sigma(h)
+}
+
+struct Tile {
+  int expert, row0, rows, bn, rt, ct;
+};
+
+__device__ __forceinline__ Tile load_tile(const int32_t* params, int task, int l) {
+  const int4 pa = __ldg(reinterpret_cast<const int4*>(params + task * MOE_PLAN_TASK_WORDS));
+  const int4 pb = __ldg(reinterpret_cast<const int4*>(params + task * MOE_PLAN_TASK_WORDS + 4));
+  Tile t;
+  t.expert = pa.x;
+  t.row0 = pa.y;
+  t.rows = pa.z;
+  t.bn = pb.y;
+  t.rt = l % pb.z;   // row tile fastest (R5)
+  t.ct = l / pb.z;
+  return t;
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(uint32_t lo, uint32_t hi) {
+  __nv_bfloat162 b = __floats2bfloat162_rn(__uint_as_float(lo), __uint_as_float(hi));
+  return *reinterpret_cast<uint32_t*>(&b);
+}
+
+// Store 32 consecutive fp32 accumulator columns [col0, col0+32) of one Y row,
+// masked to col < col_end (col_end is a multiple of 8).
+__device__ __forceinline__ void store_chunk(const GemmArgs& a, int64_t yrow, int col0, int col_end,
+                                            const uint32_t (&v)[32]) {
+  if (a.y_f32) {
+    float* y = reinterpret_cast<float*>(a.Y) + yrow * a.N;
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+      const int c = col0 + 4 * g;
+      if (c + 4 <= col_end) {
+        uint4 q = make_uint4(v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3]);
+        *reinterpret_cast<uint4*>(y + c) = q;
+      }
+    }
+  } else {
+    __nv_bfloat16* y = reinterpret_cast<__nv_bfloat16*>(a.Y) + yrow * a.N;
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      const int c = col0 + 8 * g;
+      if (c + 8 <= col_end) {
+        uint4 q = make_uint4(pack_bf16(v[8 * g], v[8 * g + 1]), pack_bf16(v[8 * g + 2], v[8 * g + 3]),
+                             pack_bf16(v[8 * g + 4], v[8 * g + 5]), pack_bf16(v[8 * g + 6], v[8 * g + 7]));
+        *reinterpret_cast<uint4*>(y + c) = q;
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    moe_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
+                    const GemmArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;            // SW128 atoms need 1024-byte alignment
+  uint8_t* smem = smem_raw + (base - raw);
+  const uint32_t sA = base;
+  const uint32_t sB = sA + kStages * kABytes;
+  const uint32_t sBar = sB + kStages * kBStageBytes;
+  auto full_bar = [&](int s) { return sBar + 8u * s; };
+  auto empty_bar = [&](int s) { return sBar + 8u * (kStages + s); };
+  auto tfull_bar = [&](int i) { return sBar + 8u * (2 * kStages + i); };
+  auto tempty_bar = [&](int i) { return sBar + 8u * (2 * kStages + 2 + i); };
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + (sBar - base) + 8 * (2 * kStages + 4));
+  int32_t* s_prefix = reinterpret_cast<int32_t*>(smem + (sBar - base) + kBarBytes);
+  int32_t* s_sigma = s_prefix + a.M_pad;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  // TilePrefix and sigma are adjacent in the blob: one copy into shared memory.
+  for (int i = threadIdx.x; i < 2 * a.M_pad; i += blockDim.x) s_prefix[i] = a.plan[MOE_PLAN_HEADER + i];
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(full_bar(s), 1);
+      mbar_init(empty_bar(s), 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(tfull_bar(i), 1);
+      mbar_init(tempty_bar(i), kEpiWarps);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmX);
+    prefetch_tmap(&tmW);
+  }
+  if (warp == 1) tmem_alloc<kTmemCols>(smem_u32(tmem_holder));
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+  const int32_t* params = a.plan + a.off_params;
+
+  if (warp == 0) {
+    // ===================== producer: TMA gather4 (X rows) + TMA tiles (W) =====================
+    const uint64_t pol_x = policy_evict_last();    // X_e is re-read by every column tile of the task
+    const uint64_t pol_w = policy_evict_normal();
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int v = blockIdx.x; v < a.total; v += gridDim.x) {
+      int h, task, l;
+      map_tile(s_prefix, s_sigma, a.M_pad, v, h, task, l);
+      const Tile t = load_tile(params, task, l);
+      const int rbeg = t.rt * kBM;
+      const int nvalid = min(kBM, t.rows - rbeg);
+      // Lane i gathers tile rows 4i..4i+3; rows past the task's end repeat its last
+      // valid token (their results are never stored).
+      const int32_t* idx = a.token_idx + t.row0 + rbeg;
+      const int r0 = __ldg(idx + min(4 * lane + 0, nvalid - 1));
+      const int r1 = __ldg(idx + min(4 * lane + 1, nvalid - 1));
+      const int r2 = __ldg(idx + min(4 * lane + 2, nvalid - 1));
+      const int r3 = __ldg(idx + min(4 * lane + 3, nvalid - 1));
+      const int n0 = t.ct * t.bn;
+      const int nbox = (t.bn + 63) >> 6;
+      const uint32_t tx = kABytes + nbox * kBBoxBytes;
+      for (int kb = 0; kb < a.num_kb; ++kb) {
+        mbar_wait(empty_bar(stage), phase ^ 1u);
+        if (lane == 0) mbar_arrive_expect_tx(full_bar(stage), tx);
+        __syncwarp();
+        tma_gather4(&tmX, full_bar(stage), sA + stage * kABytes + lane * 512, kb * kBK, r0, r1, r2, r3, pol_x);
+        if (lane < nbox)
+          tma_load_3d(&tmW, full_bar(stage), sB + stage * kBStageBytes + lane * kBBoxBytes, n0 + lane * 64,
+                      kb * kBK, t.expert, pol_w);
+        if (++stage == kStages) {
+          stage = 0;
+          phase ^= 1u;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer: one thread drives tcgen05 =====================
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int v = blockIdx.x; v < a.total; v += gridDim.x) {
+      int h, task, l;
+      map_tile(s_prefix, s_sigma, a.M_pad, v, h, task, l);
+      const int bn = __ldg(params + task * MOE_PLAN_TASK_WORDS + 5);
+      const uint32_t idesc = idesc_bf16_f32(kBM, bn, /*A K-major*/ 0, /*B MN-major*/ 1);
+      mbar_wait(tempty_bar(acc), acc_phase ^ 1u);            // epilogue drained this accumulator
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * kAccCols;
+      for (int kb = 0; kb < a.num_kb; ++kb) {
+        mbar_wait(full_bar(stage), phase);                    // TMA bytes landed
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t a0 = sA + stage * kABytes;
+          const uint32_t b0 = sB + stage * kBStageBytes;
+#pragma unroll
+          for (int kk = 0; kk < kBK / 16; ++kk) {
+            // A: K-major SW128, 8-row groups 1024 B apart; K step of 16 = +32 B in the row.
+            const uint64_t ad = smem_desc_sw128(a0 + kk * 32, 16, 1024);
+            // B: MN-major SW128; 64-wide N chunks 8 KB apart (LBO), 8-row K groups 1 KB apart
+            // (SBO); K step of 16 rows = +2 KB.
+            const uint64_t bd = smem_desc_sw128(b0 + kk * 2048, kBBoxBytes, 1024);
+            mma_bf16(d_tmem, ad, bd, idesc, (kb | kk) != 0);
+          }
+          mma_commit(empty_bar(stage));                       // frees the smem slot when done
+        }
+        __syncwarp();
+        if (++stage == kStages) {
+          stage = 0;
+          phase ^= 1u;
+        }
+      }
+      if (lane == 0) mma_commit(tfull_bar(acc));              // accumulator ready
+      __syncwarp();
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1u;
+      }
+    }
+  } else {
+    // ===================== epilogue: TMEM -> registers -> Y =====================
+    const int q = warp & 3;                                   // TMEM lane quarter of this warp
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int v = blockIdx.x; v < a.total; v += gridDim.x) {
+      int h, task, l;
+      map_tile(s_prefix, s_sigma, a.M_pad, v, h, task, l);
+      const Tile t = load_tile(params, task, l);
+      mbar_wait(tfull_bar(acc), acc_phase);
+      tc_fence_after();
+      const int grow = t.rt * kBM + q * 32 + lane;            // row within the task
+      const bool valid = grow < t.rows;
+      const int64_t yrow = (int64_t)t.row0 + grow;
+      const int n0 = t.ct * t.bn;
+      const int col_end = min(n0 + t.bn, a.N);
+      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * kAccCols;
+      for (int c = 0; c < t.bn; c += 32) {
+        uint32_t r[32];
+        tmem_ld32(taddr + c, r);
+        tmem_wait_ld();
+        if (valid) store_chunk(a, yrow, n0 + c, col_end, r);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty_bar(acc));
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1u;
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<kTmemCols>(tmem_base);
+  }
+}
+
+// Decode every virtual tile with the same device function as the GEMM.
+__global__ void decode_debug_kernel(const int32_t* plan, int total, int M_pad, int off_params, int32_t* out) {
+  extern __shared__ int32_t s_pre[];
+  for (int i = threadIdx.x; i < 2 * M_pad; i += blockDim.x) s_pre[i] = plan[MOE_PLAN_HEADER + i];
+  __syncthreads();
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int v = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < total; v += warps) {
+    int h, task, l;
+    map_tile(s_pre, s_pre + M_pad, M_pad, v, h, task, l);
+    const Tile t = load_tile(plan + off_params, task, l);
+    if ((threadIdx.x & 31) == 0) {
+      int32_t* o = out + 5 * (int64_t)v;
+      o[0] = h;
+      o[1] = task;
+      o[2] = l;
+      o[3] = t.rt;
+      o[4] = t.ct;
+    }
+  }
+}
+
+// Probe: one CTA gathers 128 rows x 64 columns with tile::gather4 into a SW128
+// buffer and dumps the raw 16 KB of shared memory.
+__global__ void probe_gather4_kernel(const __grid_constant__ CUtensorMap tmX, const int32_t* rows, int col0,
+                                     uint8_t* out) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  uint8_t* smem = smem_raw + (base - raw);
+  const uint32_t bar = base + kABytes;
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    if (lane == 0) mbar_arrive_expect_tx(bar, kABytes);
+    __syncwarp();
+    tma_gather4(&tmX, bar, base + lane * 512, col0, rows[4 * lane], rows[4 * lane + 1], rows[4 * lane + 2],
+                rows[4 * lane + 3], policy_evict_normal());
+  }
+  mbar_wait(bar, 0);
+  for (int i = threadIdx.x; i < kABytes / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(out)[i] = reinterpret_cast<const uint4*>(smem)[i];
+}
+
+// ---------------------------------------------------------------------------
+// Host side
+// ---------------------------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+moe_status make_x_map(CUtensorMap* m, const void* X, int64_t T, int64_t H) {
+  auto fn = encode_fn();
+  if (!fn) MOE_FAIL(MOE_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
+  const cuuint64_t dims[2] = {(cuuint64_t)H, (cuuint64_t)T};
+  const cuuint64_t strides[1] = {(cuuint64_t)H * 2};
+  const cuuint32_t box[2] = {(cuuint32_t)kBK, 1};   // gather4: 4 rows of one box row each
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(X), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) MOE_FAIL(MOE_ERR_CUDA, "cuTensorMapEncodeTiled(X) failed: %d", (int)r);
+  return MOE_OK;
+}
+
+moe_status make_w_map(CUtensorMap* m, const void* W, int64_t E, int64_t H, int64_t N) {
+  auto fn = encode_fn();
+  if (!fn) MOE_FAIL(MOE_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
+  const cuuint64_t dims[3] = {(cuuint64_t)N, (cuuint64_t)H, (cuuint64_t)E};
+  const cuuint64_t strides[2] = {(cuuint64_t)N * 2, (cuuint64_t)H * N * 2};
+  const cuuint32_t box[3] = {64, (cuuint32_t)kBK, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(W), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) MOE_FAIL(MOE_ERR_CUDA, "cuTensorMapEncodeTiled(W) failed: %d", (int)r);
+  return MOE_OK;
+}
+
+int sm_count_cached() {
+  static int n = 0;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  });
+  return n;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+}  // namespace
+
+extern "C" {
+
+moe_status moe_device_info(int32_t* sm_count, int32_t* cc_major, int32_t* cc_minor) {
+  moe::clear_error();
+  int dev = 0, maj = 0, min = 0, n = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) MOE_FAIL(MOE_ERR_CUDA, "cudaGetDevice: %s", cudaGetErrorString(e));
+  cudaDeviceGetAttribute(&maj, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&min, cudaDevAttrComputeCapabilityMinor, dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  if (sm_count) *sm_count = n;
+  if (cc_major) *cc_major = maj;
+  if (cc_minor) *cc_minor = min;
+  if (maj != 10 || min != 0) MOE_FAIL(MOE_ERR_UNSUPPORTED, "device is sm_%d%d; this library is built for sm_100a", maj, min);
+  return MOE_OK;
+}
+
+moe_status moe_gemm(const moe_plan* plan, const void* X, int64_t T, const int32_t* token_idx, const void* W,
+                    void* Y, int32_t y_dtype, void* stream) {
+  moe::clear_error();
+  if (!plan) MOE_FAIL(MOE_ERR_INVALID, "moe_gemm: null plan");
+  int64_t words = 0;
+  const int32_t* blob = moe::plan_blob_host(plan, &words);
+  moe::BlobView v;
+  if (!moe::blob_view(blob, words, &v)) MOE_FAIL(MOE_ERR_INVALID, "moe_gemm: corrupt plan");
+  if (v.total == 0) return MOE_OK_EMPTY;
+  if (!X || !token_idx || !W || !Y) MOE_FAIL(MOE_ERR_INVALID, "moe_gemm: null tensor pointer");
+  if (!aligned16(X) || !aligned16(W) || !aligned16(Y))
+    MOE_FAIL(MOE_ERR_INVALID, "moe_gemm: X, W and Y must be 16-byte aligned");
+  if (T < 1 || T >= INT_MAX) MOE_FAIL(MOE_ERR_INVALID, "moe_gemm: T=%lld outside [1, 2^31)", (long long)T);
+  if (y_dtype != MOE_DTYPE_BF16 && y_dtype != MOE_DTYPE_F32) MOE_FAIL(MOE_ERR_INVALID, "moe_gemm: y_dtype=%d", y_dtype);
+  if (v.M_pad > kMaxMPad) MOE_FAIL(MOE_ERR_CAPACITY, "moe_gemm: %d tasks exceed %d", v.M_pad, kMaxMPad);
+
+  CUtensorMap tmX, tmW;
+  moe_status st = make_x_map(&tmX, X, T, v.H);
+  if (st != MOE_OK) return st;
+  st = make_w_map(&tmW, W, v.E, v.H, v.N);
+  if (st != MOE_OK) return st;
+
+  GemmArgs a;
+  a.plan = moe::plan_blob_dev(plan);
+  a.token_idx = token_idx;
+  a.Y = Y;
+  a.y_f32 = y_dtype == MOE_DTYPE_F32;
+  a.N = v.N;
+  a.num_kb = (int32_t)moe::ceil_div(v.H, kBK);
+  a.total = v.total;
+  a.M_pad = v.M_pad;
+  a.off_params = (int32_t)v.off_params;
+
+  const size_t smem = kSmemFixed + 8 * (size_t)v.M_pad;
+  static std::once_flag attr_once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(attr_once, [] {
+    attr_err = cudaFuncSetAttribute(moe_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)(kSmemFixed + 8 * kMaxMPad));
+  });
+  if (attr_err != cudaSuccess) MOE_FAIL(MOE_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(attr_err));
+  const int grid = std::min(v.total, sm_count_cached());
+  moe_gemm_kernel<<<grid, kThreads, smem, (cudaStream_t)stream>>>(tmX, tmW, a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) MOE_FAIL(MOE_ERR_CUDA, "moe_gemm launch: %s", cudaGetErrorString(e));
+  return MOE_OK;
+}
+
+moe_status moe_decode_debug(const moe_plan* plan, int32_t* out, void* stream) {
+  moe::clear_error();
+  if (!plan || !out) MOE_FAIL(MOE_ERR_INVALID, "moe_decode_debug: null argument");
+  int64_t words = 0;
+  const int32_t* blob = moe::plan_blob_host(plan, &words);
+  moe::BlobView v;
+  if (!moe::blob_view(blob, words, &v)) MOE_FAIL(MOE_ERR_INVALID, "moe_decode_debug: corrupt plan");
+  if (v.total == 0) return MOE_OK_EMPTY;
+  const int threads = 256;
+  const int grid = (int)std::min<int64_t>(moe::ceil_div(v.total, threads / 32), 4 * 148);
+  decode_debug_kernel<<<grid, threads, 8 * v.M_pad, (cudaStream_t)stream>>>(moe::plan_blob_dev(plan), v.total,
+                                                                          v.M_pad, (int)v.off_params, out);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) MOE_FAIL(MOE_ERR_CUDA, "moe_decode_debug launch: %s", cudaGetErrorString(e));
+  return MOE_OK;
+}
+
+moe_status moe_probe_gather4(const void* X, int64_t T, int64_t H, const int32_t* rows_dev, int32_t col0,
+                             void* out_dev, void* stream) {
+  moe::clear_error();
+  if (!X || !rows_dev || !out_dev) MOE_FAIL(MOE_ERR_INVALID, "moe_probe_gather4: null argument");
+  if (H % 8) MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_probe_gather4: H %% 8 != 0");
+  CUtensorMap tmX;
+  moe_status st = make_x_map(&tmX, X, T, H);
+  if (st != MOE_OK) return st;
+  const int smem = kABytes + 1024 + 64;
+  probe_gather4_kernel<<<1, 128, smem, (cudaStream_t)stream>>>(tmX, rows_dev, col0, (uint8_t*)out_dev);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) MOE_FAIL(MOE_ERR_CUDA, "moe_probe_gather4 launch: %s", cudaGetErrorString(e));
+  return MOE_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,270 @@
+// Host planner: expert token counts + tile shape -> the compressed mapping.
+//
+// Paper passages (P:n = line of PAPER.md):
+//   Alg. 1  TilePrefix[i] = sum_{j<=i} nu(T_j)
+//   P:203               pad TilePrefix to the warp size (INT32_MAX or repeat-last)
+//   P:262-271, Alg. 4   TilePrefix only over the M non-empty tasks; sigma: [M] -> [N]
+//   P:298-301           each expert is a task; p_i holds the expert's parameters
+// The blob layout is documented in include/moe_sm100.h.
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.h"
+
+namespace moe {
+
+static thread_local std::string g_last_error;
+
+void set_error(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+}
+
+void clear_error() { g_last_error.clear(); }
+
+static int32_t pad32(int64_t m) { return (int32_t)(m <= 32 ? 32 : ceil_div(m, 32) * 32); }
+
+bool blob_view(const int32_t* blob, int64_t len, BlobView* v) {
+  if (!blob || len < MOE_PLAN_HEADER || blob[0] != MOE_PLAN_MAGIC) return false;
+  v->M = blob[1];
+  v->total = blob[2];
+  v->M_pad = blob[3];
+  v->E = blob[4];
+  v->N = blob[5];
+  v->H = blob[6];
+  v->bm = blob[7];
+  v->bn = blob[8];
+  v->n_tasks = blob[9];
+  v->flags = (uint32_t)blob[10];
+  v->off_prefix = MOE_PLAN_HEADER;
+  v->off_sigma = v->off_prefix + v->M_pad;
+  v->off_params = v->off_sigma + v->M_pad;
+  v->off_row_off = v->off_params + (int64_t)MOE_PLAN_TASK_WORDS * v->n_tasks;
+  v->words = v->off_row_off + v->E + 1;
+  return v->words <= len;
+}
+
+}  // namespace moe
+
+using moe::ceil_div;
+
+extern "C" {
+
+int64_t moe_plan_blob_words(int32_t E) {
+  if (E < 1) return 0;
+  const int64_t m_pad = moe::pad32(E);
+  return MOE_PLAN_HEADER + 2 * m_pad + (int64_t)MOE_PLAN_TASK_WORDS * E + E + 1;
+}
+
+moe_status moe_plan_build(const int32_t* counts, int32_t E, int64_t H, int64_t N, int32_t bm,
+                          int32_t bn, uint32_t flags, int32_t* blob, int64_t blob_cap,
+                          int64_t* blob_len) {
+  moe::clear_error();
+  if (!counts || !blob) MOE_FAIL(MOE_ERR_INVALID, "moe_plan_build: null counts or blob");
+  if (E < 1 || E > 4096) MOE_FAIL(MOE_ERR_INVALID, "moe_plan_build: E=%d outside [1, 4096]", E);
+  if (H <= 0 || N <= 0) MOE_FAIL(MOE_ERR_INVALID, "moe_plan_build: H=%lld N=%lld must be > 0", (long long)H, (long long)N);
+  if (H % 8 || N % 8)
+    MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_plan_build: H=%lld and N=%lld must be multiples of 8 (16-byte TMA strides)",
+             (long long)H, (long long)N);
+  if (H >= INT_MAX || N >= INT_MAX) MOE_FAIL(MOE_ERR_CAPACITY, "moe_plan_build: H or N >= 2^31");
+  if (bm != 128) MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_plan_build: bm=%d unsupported (tcgen05 M=128 tiles)", bm);
+  if (bn < 16 || bn > 256 || bn % 16)
+    MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_plan_build: bn=%d must be a multiple of 16 in [16, 256]", bn);
+  if (flags & ~MOE_PAD_REPEAT) MOE_FAIL(MOE_ERR_INVALID, "moe_plan_build: unknown flags 0x%x", flags);
+
+  // CSR row offsets: exclusive prefix of counts in expert-id order.
+  std::vector<int64_t> row_off(E + 1, 0);
+  for (int32_t e = 0; e < E; ++e) {
+    if (counts[e] < 0) MOE_FAIL(MOE_ERR_INVALID, "moe_plan_build: counts[%d]=%d < 0", e, counts[e]);
+    row_off[e + 1] = row_off[e] + counts[e];
+  }
+  if (row_off[E] >= INT_MAX) MOE_FAIL(MOE_ERR_CAPACITY, "moe_plan_build: sum of counts >= 2^31");
+
+  // Tasks = experts.  nu = ceil(m/BM) * ceil(N/BN); K is not split.
+  const int32_t n_tasks = E;
+  const int64_t col_tiles = ceil_div(N, bn);
+  std::vector<int64_t> nu(n_tasks);
+  for (int32_t i = 0; i < n_tasks; ++i) nu[i] = counts[i] == 0 ? 0 : ceil_div(counts[i], bm) * col_tiles;
+
+  // Non-empty stage: sigma in natural order, then Alg. 1 over eta.
+  std::vector<int32_t> sigma;
+  std::vector<int64_t> prefix;
+  int64_t acc = 0;
+  for (int32_t i = 0; i < n_tasks; ++i) {
+    if (nu[i] == 0) continue;
+    sigma.push_back(i);
+    acc += nu[i];
+    prefix.push_back(acc);
+  }
+  if (acc >= INT_MAX) MOE_FAIL(MOE_ERR_CAPACITY, "moe_plan_build: %lld tiles >= 2^31", (long long)acc);
+  const int32_t M = (int32_t)sigma.size();
+  const int32_t M_pad = moe::pad32(M);
+  const int64_t words = MOE_PLAN_HEADER + 2 * (int64_t)M_pad + (int64_t)MOE_PLAN_TASK_WORDS * n_tasks + E + 1;
+  if (blob_cap < words)
+    MOE_FAIL(MOE_ERR_CAPACITY, "moe_plan_build: blob needs %lld words, cap %lld", (long long)words, (long long)blob_cap);
+
+  std::memset(blob, 0, sizeof(int32_t) * words);
+  blob[0] = MOE_PLAN_MAGIC;
+  blob[1] = M;
+  blob[2] = (int32_t)acc;
+  blob[3] = M_pad;
+  blob[4] = E;
+  blob[5] = (int32_t)N;
+  blob[6] = (int32_t)H;
+  blob[7] = bm;
+  blob[8] = bn;
+  blob[9] = n_tasks;
+  blob[10] = (int32_t)flags;
+  int32_t* pre = blob + MOE_PLAN_HEADER;
+  int32_t* sig = pre + M_pad;
+  int32_t* par = sig + M_pad;
+  int32_t* roff = par + (int64_t)MOE_PLAN_TASK_WORDS * n_tasks;
+  for (int32_t h = 0; h < M_pad; ++h) {
+    if (h < M) {
+      pre[h] = (int32_t)prefix[h];
+      sig[h] = sigma[h];
+    } else {
+      // P:203 padding: "repeating its last element or padding with the maximum possible value".
+      pre[h] = (flags & MOE_PAD_REPEAT) && M > 0 ? (int32_t)prefix[M - 1] : INT_MAX;
+      sig[h] = 0;
+    }
+  }
+  for (int32_t i = 0; i < n_tasks; ++i) {
+    int32_t* p = par + (int64_t)MOE_PLAN_TASK_WORDS * i;
+    p[0] = i;                                   // expert
+    p[1] = (int32_t)row_off[i];                 // first CSR row of the task
+    p[2] = counts[i];                           // rows
+    p[3] = 0;                                   // kind (one tiling strategy in this build)
+    p[4] = bm;
+    p[5] = bn;
+    p[6] = (int32_t)ceil_div(counts[i], bm);    // row tiles
+    p[7] = (int32_t)col_tiles;                  // col tiles
+  }
+  for (int32_t e = 0; e <= E; ++e) roff[e] = (int32_t)row_off[e];
+  if (blob_len) *blob_len = words;
+  return M == 0 ? MOE_OK_EMPTY : MOE_OK;
+}
+
+const char* moe_last_error(void) { return moe::g_last_error.c_str(); }
+
+const char* moe_version(void) { return "moe_sm100 0.1 (sm_100a)"; }
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Device-resident plan
+// ---------------------------------------------------------------------------
+struct moe_plan {
+  std::vector<int32_t> blob;
+  int64_t words = 0;
+  int32_t* dev = nullptr;
+  int64_t dev_words = 0;
+  cudaStream_t stream = nullptr;
+  int32_t E = 0;
+  int64_t H = 0, N = 0;
+  int32_t bm = 0, bn = 0;
+  uint32_t flags = 0;
+};
+
+namespace moe {
+const int32_t* plan_blob_host(const moe_plan* p, int64_t* words) {
+  if (words) *words = p->words;
+  return p->blob.data();
+}
+const int32_t* plan_blob_dev(const moe_plan* p) { return p->dev; }
+cudaStream_t plan_stream(const moe_plan* p) { return p->stream; }
+}  // namespace moe
+
+extern "C" {
+
+static moe_status upload(moe_plan* p, cudaStream_t s) {
+  cudaError_t err = cudaMemcpyAsync(p->dev, p->blob.data(), sizeof(int32_t) * p->words,
+                                    cudaMemcpyHostToDevice, s);
+  if (err != cudaSuccess) MOE_FAIL(MOE_ERR_CUDA, "cudaMemcpyAsync(plan blob): %s", cudaGetErrorString(err));
+  return MOE_OK;
+}
+
+moe_status moe_plan_create(const int32_t* counts, int32_t E, int64_t H, int64_t N, int32_t bm,
+                           int32_t bn, uint32_t flags, void* stream, moe_plan** out) {
+  moe::clear_error();
+  if (!out) MOE_FAIL(MOE_ERR_INVALID, "moe_plan_create: null out");
+  *out = nullptr;
+  if (E < 1) MOE_FAIL(MOE_ERR_INVALID, "moe_plan_create: E=%d", E);
+  auto* p = new moe_plan();
+  p->blob.resize(moe_plan_blob_words(E));
+  moe_status st = moe_plan_build(counts, E, H, N, bm, bn, flags, p->blob.data(), (int64_t)p->blob.size(), &p->words);
+  if (st < 0) {
+    delete p;
+    return st;
+  }
+  p->stream = (cudaStream_t)stream;
+  p->E = E;
+  p->H = H;
+  p->N = N;
+  p->bm = bm;
+  p->bn = bn;
+  p->flags = flags;
+  p->dev_words = (int64_t)p->blob.size();
+  cudaError_t err = cudaMallocAsync((void**)&p->dev, sizeof(int32_t) * p->dev_words, p->stream);
+  if (err != cudaSuccess) {
+    delete p;
+    MOE_FAIL(MOE_ERR_CUDA, "cudaMallocAsync(plan): %s", cudaGetErrorString(err));
+  }
+  moe_status up = upload(p, p->stream);
+  if (up != MOE_OK) {
+    cudaFreeAsync(p->dev, p->stream);
+    delete p;
+    return up;
+  }
+  *out = p;
+  return st;
+}
+
+moe_status moe_plan_update(moe_plan* p, const int32_t* counts, void* stream) {
+  moe::clear_error();
+  if (!p) MOE_FAIL(MOE_ERR_INVALID, "moe_plan_update: null plan");
+  int64_t words = 0;
+  moe_status st = moe_plan_build(counts, p->E, p->H, p->N, p->bm, p->bn, p->flags, p->blob.data(),
+                                 (int64_t)p->blob.size(), &words);
+  if (st < 0) return st;
+  p->words = words;
+  if (stream) p->stream = (cudaStream_t)stream;
+  moe_status up = upload(p, p->stream);
+  return up != MOE_OK ? up : st;
+}
+
+moe_status moe_plan_query(const moe_plan* p, int32_t* M, int32_t* total, int32_t* M_pad) {
+  if (!p) MOE_FAIL(MOE_ERR_INVALID, "moe_plan_query: null plan");
+  if (M) *M = p->blob[1];
+  if (total) *total = p->blob[2];
+  if (M_pad) *M_pad = p->blob[3];
+  return MOE_OK;
+}
+
+moe_status moe_plan_blob(const moe_plan* p, int32_t* out, int64_t cap, int64_t* len) {
+  if (!p) MOE_FAIL(MOE_ERR_INVALID, "moe_plan_blob: null plan");
+  if (len) *len = p->words;
+  if (out) {
+    if (cap < p->words) MOE_FAIL(MOE_ERR_CAPACITY, "moe_plan_blob: cap %lld < %lld", (long long)cap, (long long)p->words);
+    std::memcpy(out, p->blob.data(), sizeof(int32_t) * p->words);
+  }
+  return MOE_OK;
+}
+
+const int32_t* moe_plan_device_blob(const moe_plan* p) { return p ? p->dev : nullptr; }
+
+void moe_plan_destroy(moe_plan* p) {
+  if (!p) return;
+  if (p->dev) cudaFreeAsync(p->dev, p->stream);
+  delete p;
+}
+
+}  // extern "C"

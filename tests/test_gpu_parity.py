@@ -1,0 +1,280 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle.
+
+Bar (north star): mapping / indexing bit-exact; Y within
+max|d| <= 1e-2 * (|ref| + 1) and relative Frobenius <= 2e-3 for bf16 inputs
+with fp32 accumulation; integer-valued inputs with fp32 output bit-exact.
+"""
+import numpy as np
+import pytest
+import torch
+
+import paper_2501_16103_b200 as M
+import synth
+from oracle import moe as omoe
+from synth import workloads as wl
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def device():
+    from paper_2501_16103_b200 import build
+    build.build()
+    n, ma, mi = M.moe_device_info()
+    assert (ma, mi) == (10, 0), "needs sm_100"
+    return n
+
+
+def tol_check(Y, ref, tag=""):
+    Y = Y.double()
+    ref = torch.as_tensor(ref, dtype=torch.float64)
+    d = (Y - ref).abs()
+    bound = 1e-2 * (ref.abs() + 1)
+    worst = (d / bound).max().item() if d.numel() else 0.0
+    rel = ((Y - ref).norm() / ref.norm().clamp_min(1e-30)).item() if d.numel() else 0.0
+    assert worst <= 1.0, f"{tag}: max |d| / (1e-2 (|ref|+1)) = {worst}"
+    assert rel <= 2e-3, f"{tag}: rel Frobenius {rel}"
+    return worst, rel
+
+
+def _inputs(T, E, k, H, N, seed, mode="normal", routing=None):
+    ids = routing if routing is not None else synth.route_gumbel(seed, T, E, k)
+    X = synth.make_x(seed, T, H, mode)
+    W = synth.make_w(seed, E, H, N, mode)
+    Xd = torch.from_numpy(X).to(torch.bfloat16).cuda()
+    Wd = torch.from_numpy(W).to(torch.bfloat16).cuda()
+    return ids, X, W, Xd, Wd
+
+
+def run_path(ids, Xd, Wd, E, bn=256, out_dtype=torch.float32, pad=M.MOE_PAD_MAX):
+    topk = torch.from_numpy(np.ascontiguousarray(ids, dtype=np.int32)).cuda()
+    counts, row_off, tok, slot, status = M.moe_route(topk, E)
+    counts_h = counts.cpu().numpy()
+    plan = M.Plan(counts_h, Xd.shape[1], Wd.shape[2], 128, bn, pad)
+    Y = torch.full((tok.numel(), Wd.shape[2]), float("nan"), dtype=out_dtype, device="cuda")
+    M.moe_gemm(plan, Xd, tok, Wd, Y=Y)
+    torch.cuda.synchronize()
+    return Y, counts_h, row_off, tok, slot, plan, status
+
+
+# ---------------------------------------------------------------------------- gather4 probe
+def _expected_swizzled(X, rows, col0, H):
+    out = np.zeros((128, 64), dtype=np.uint16)
+    xb = torch.from_numpy(X).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+    for r in range(128):
+        for c in range(64):
+            if col0 + c < H:
+                out[r, c] = xb[rows[r], col0 + c]
+    # 16-byte chunk c of row r lands at chunk position c ^ (r % 8)
+    sw = np.zeros_like(out)
+    for r in range(128):
+        for ch in range(8):
+            sw[r, 8 * (ch ^ (r % 8)): 8 * (ch ^ (r % 8)) + 8] = out[r, 8 * ch: 8 * ch + 8]
+    return sw.view(np.uint8).reshape(-1)
+
+
+@pytest.mark.parametrize("H,col0", [(128, 0), (128, 64), (72, 64)])
+def test_probe_gather4_swizzle(H, col0):
+    T = 300
+    X = synth.make_x(1, T, H)
+    rng = np.random.default_rng(H + col0)
+    rows = rng.integers(0, T, size=128).astype(np.int32)
+    rows[5] = rows[4]                                             # repeated rows are legal
+    Xd = torch.from_numpy(X).to(torch.bfloat16).cuda()
+    got = M.moe_probe_gather4(Xd, torch.from_numpy(rows).cuda(), col0).cpu().numpy()
+    assert np.array_equal(got, _expected_swizzled(X, rows, col0, H))
+
+
+# ---------------------------------------------------------------------------- decode (bit-exact)
+def _decode_ref(counts, N, bn, pad="max"):
+    pl = omoe.plan(counts, N, 128, bn, pad_mode=pad)
+    row_off = np.concatenate([[0], np.cumsum(counts)])
+    out = []
+    for B in range(pl["total"]):
+        d = omoe.decode(pl, row_off, B)
+        out.append((d["h"], d["task"], d["l"], d["rt"], d["ct"]))
+    return np.array(out, dtype=np.int64).reshape(-1, 5)
+
+
+@pytest.mark.parametrize("case", ["tiny_a", "mix", "ds", "worst", "random_many"])
+@pytest.mark.parametrize("pad", ["max", "repeat"])
+def test_decode_debug_bit_exact(case, pad):
+    if case == "tiny_a":
+        counts, N, bn = np.array([11, 0, 11, 10]), 128, 128
+    elif case == "random_many":
+        rng = np.random.default_rng(7)
+        counts = np.where(rng.random(300) < 0.3, 0, rng.integers(1, 700, size=300))
+        N, bn = 1024, 64
+    else:
+        c = synth.CONFIGS[{"mix": "mix", "ds": "ds", "worst": "paper_worst"}[case]]
+        counts = np.bincount(synth.route(c, 0).ravel(), minlength=c.E)
+        N, bn = c.N, 256 if case != "ds" else 128
+    plan = M.Plan(counts, 64, N, 128, bn, M.MOE_PAD_REPEAT if pad == "repeat" else 0)
+    got = M.moe_decode_debug(plan).cpu().numpy()
+    ref = _decode_ref(counts, N, bn, pad)
+    assert got.shape == ref.shape
+    assert np.array_equal(got, ref)
+
+
+def test_decode_large_total():
+    """~10^6 virtual tiles across 3 chunks of TilePrefix."""
+    rng = np.random.default_rng(8)
+    counts = rng.integers(0, 40000, size=70)
+    counts[::9] = 0
+    plan = M.Plan(counts, 64, 4096, 128, 16)
+    got = M.moe_decode_debug(plan).cpu().numpy()
+    pl = M.parse_plan_blob(plan.blob())
+    # independent enumeration of the lattice (sigma order, rt fastest)
+    ref = []
+    h = 0
+    for e in range(70):
+        if counts[e] == 0:
+            continue
+        R, C = -(-counts[e] // 128), 4096 // 16
+        l = np.arange(R * C)
+        ref.append(np.stack([np.full(R * C, h), np.full(R * C, e), l, l % R, l // R], axis=1))
+        h += 1
+    ref = np.concatenate(ref)
+    assert pl["total"] == len(ref) and len(ref) > 900_000
+    assert np.array_equal(got, ref)
+
+
+# ---------------------------------------------------------------------------- route (bit-exact)
+@pytest.mark.parametrize("cfg", ["tiny", "mix", "ds", "paper_worst", "dec1", "ep"])
+def test_route_bit_exact(cfg):
+    c = synth.CONFIGS[cfg]
+    ids = synth.route(c, 0)
+    counts, row_off, tok, slot, status = M.moe_route(torch.from_numpy(ids).cuda(), c.E)
+    rc, rr, rt, rs = omoe.buckets(ids, c.E)
+    assert counts.cpu().numpy().tolist() == rc.tolist()
+    assert row_off.cpu().numpy().tolist() == rr.tolist()
+    assert tok.cpu().numpy().tolist() == rt.tolist()
+    assert slot.cpu().numpy().tolist() == rs.tolist()
+    assert status.item() == 0
+
+
+def test_route_flags_bad_ids_and_empty():
+    ids = np.array([[0, 1], [2, 2], [5, 1]], dtype=np.int32)          # duplicate and out-of-range
+    counts, row_off, tok, slot, status = M.moe_route(torch.from_numpy(ids).cuda(), 4)
+    assert status.item() == 1
+    assert counts.cpu().tolist() == [1, 2, 1, 0]
+    assert tok.cpu().tolist()[:4] == [0, 0, 2, 1]
+    ids = np.zeros((0, 2), dtype=np.int32)
+    counts, row_off, tok, slot, status = M.moe_route(torch.zeros((0, 2), dtype=torch.int32, device="cuda"), 4)
+    assert counts.cpu().tolist() == [0, 0, 0, 0] and row_off.cpu().tolist() == [0] * 5
+
+
+# ---------------------------------------------------------------------------- GEMM
+def test_gemm_tiny_a_integer_bit_exact():
+    c = synth.CONFIGS["tiny"]
+    ids = synth.route(c, 0)
+    _, X, W, Xd, Wd = _inputs(c.T, c.E, c.k, c.H, c.N, 0, "int", routing=ids)
+    Y, counts, row_off, tok, slot, plan, _ = run_path(ids, Xd, Wd, c.E, bn=128)
+    rc, rr, rt, rs = omoe.buckets(ids, c.E)
+    ref = omoe.expert_gemm(X, W, rt, rr)
+    assert counts.tolist() == [11, 0, 11, 10]
+    assert np.array_equal(Y.cpu().double().numpy(), ref)
+
+
+@pytest.mark.parametrize("out_dtype", [torch.float32, torch.bfloat16])
+def test_gemm_tiny_b_random(out_dtype):
+    c = synth.CONFIGS["tiny_b"]
+    ids = synth.route(c, 3)
+    _, X, W, Xd, Wd = _inputs(c.T, c.E, c.k, c.H, c.N, 3, routing=ids)
+    Y, *_ = run_path(ids, Xd, Wd, c.E, bn=128, out_dtype=out_dtype)
+    rc, rr, rt, rs = omoe.buckets(ids, c.E)
+    tol_check(Y.cpu(), omoe.expert_gemm(X, W, rt, rr), "tiny_b")
+
+
+def test_gemm_identity_weights_bf16_exact():
+    """W[e] = (e+1) I => Y row = (e+1) X[token] exactly, even with bf16 output."""
+    T, E, k, H = 200, 4, 2, 128
+    ids = synth.route_gumbel(2, T, E, k)
+    X = synth.make_x(2, T, H, "int")
+    Xd = torch.from_numpy(X).to(torch.bfloat16).cuda()
+    Wd = synth.make_w_torch(0, E, H, H, "identity", device="cuda")
+    Y, counts, row_off, tok, *_ = run_path(ids, Xd, Wd, E, bn=128, out_dtype=torch.bfloat16)
+    tok_h = tok.cpu().numpy()
+    ro = row_off.cpu().numpy()
+    exp = np.zeros((len(tok_h), H))
+    for e in range(E):
+        exp[ro[e]:ro[e + 1]] = (e + 1) * X[tok_h[ro[e]:ro[e + 1]]]
+    assert np.array_equal(Y.cpu().double().numpy(), exp)
+
+
+@pytest.mark.parametrize("T,E,k,H,N,bn", [
+    (300, 5, 2, 200, 136, 128),     # K tail (200 = 3*64 + 8), N tail, ragged row tiles
+    (513, 7, 3, 256, 512, 256),     # several row tiles per expert, exact N tiles
+    (64, 16, 4, 128, 176, 176),     # bn not a multiple of 64 (3 W boxes, 176 used)
+    (1, 8, 2, 4096, 1024, 256),     # decode: one token
+    (2000, 3, 1, 64, 8, 16),        # smallest N tile
+])
+@pytest.mark.parametrize("mode", ["int", "normal"])
+def test_gemm_ragged(T, E, k, H, N, bn, mode):
+    ids, X, W, Xd, Wd = _inputs(T, E, k, H, N, T + E, mode)
+    Y, counts, row_off, tok, *_ = run_path(ids, Xd, Wd, E, bn=bn)
+    rc, rr, rt, rs = omoe.buckets(ids, E)
+    ref = omoe.expert_gemm(X, W, rt, rr)
+    Yh = Y.cpu().double().numpy()
+    assert not np.isnan(Yh).any(), "some Y element was never written"
+    if mode == "int":
+        assert np.array_equal(Yh, ref)
+    else:
+        tol_check(torch.from_numpy(Yh), ref, f"ragged {T},{E},{k},{H},{N},{bn}")
+
+
+def test_gemm_empty_plan_no_launch():
+    Xd = torch.zeros((4, 64), dtype=torch.bfloat16, device="cuda")
+    Wd = torch.zeros((3, 64, 128), dtype=torch.bfloat16, device="cuda")
+    plan = M.Plan([0, 0, 0], 64, 128, 128, 128)
+    assert plan.status == M.MOE_OK_EMPTY
+    tok = torch.zeros(1, dtype=torch.int32, device="cuda")
+    st = M.lib().moe_gemm(plan.handle, Xd.data_ptr(), 4, tok.data_ptr(), Wd.data_ptr(), Xd.data_ptr(), 0,
+                          M._stream())
+    assert st == M.MOE_OK_EMPTY
+
+
+def test_gemm_misaligned_rejected():
+    Xd = torch.zeros((4, 72), dtype=torch.bfloat16, device="cuda")
+    Wd = torch.zeros((3, 64, 128), dtype=torch.bfloat16, device="cuda")
+    plan = M.Plan([1, 0, 0], 64, 128, 128, 128)
+    tok = torch.zeros(1, dtype=torch.int32, device="cuda")
+    Y = torch.zeros((1, 129), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(M.MoeError):
+        M.moe_gemm(plan, Xd[:, 1:].contiguous()[:, :64].contiguous(), tok, Wd, Y=Y[:, 1:])
+
+
+# ---------------------------------------------------------------------------- full-size sampled parity
+def _sample_rows(row_off, counts, rng, per_expert=6):
+    rows = []
+    for e in range(len(counts)):
+        if counts[e] == 0:
+            continue
+        a, b = int(row_off[e]), int(row_off[e + 1])
+        cand = {a, b - 1, min(a + 127, b - 1), min(a + 128, b - 1)}
+        cand |= set(rng.integers(a, b, size=per_expert).tolist())
+        rows += sorted(cand)
+    return np.array(rows)
+
+
+@pytest.mark.parametrize("cfg,bn", [("mix", 256), ("ds", 128), ("dec16", 256), ("paper_worst", 256)])
+def test_gemm_full_size_sampled(cfg, bn):
+    """BASELINE.json sizes, the launch configuration bench.py times; sampled outputs vs fp64."""
+    c = synth.CONFIGS[cfg]
+    seed = 0
+    ids = synth.route(c, seed)
+    Xd = synth.make_x_torch(seed, c.T, c.H, device="cuda")
+    Wd = synth.make_w_torch(seed, c.E, c.H, c.N, device="cuda")
+    Y, counts, row_off, tok, *_ = run_path(ids, Xd, Wd, c.E, bn=bn, out_dtype=torch.bfloat16)
+    rc, rr, rt, rs = omoe.buckets(ids, c.E)
+    assert np.array_equal(tok.cpu().numpy(), rt)
+    rng = np.random.default_rng(1)
+    rows = _sample_rows(rr, rc, rng)
+    cols = np.unique(np.concatenate([rng.integers(0, c.N, 40), [0, c.N - 1, bn - 1, bn]]))
+    ref = omoe.expert_gemm_entries(lambda t: wl.x_rows(seed, c.T, c.H, [t])[0],
+                                   lambda e, cs: wl.w_columns(seed, c.E, c.H, c.N, e, cs),
+                                   rt, rr, rows, cols)
+    got = Y[torch.from_numpy(rows).cuda()][:, torch.from_numpy(cols).cuda()].cpu()
+    tol_check(got, ref, cfg)
+    # every row written (NaN sentinel) — the exactly-once cover follows from the bit-exact decode
+    assert not torch.isnan(Y.float()).any().item()

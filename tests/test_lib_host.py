@@ -1,0 +1,133 @@
+"""C-ABI library on the host (no GPU): it loads, exports every declared symbol, and
+its planner (moe_plan_build) matches the oracle plan bit-exactly."""
+import ctypes
+import os
+import random
+import re
+
+import numpy as np
+import pytest
+
+import paper_2501_16103_b200 as moe_lib
+import synth
+from oracle import mapping as om
+from oracle import moe as omoe
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    from paper_2501_16103_b200 import build
+    build.build()
+
+
+def _declared_functions():
+    names = set()
+    for h in os.listdir(os.path.join(ROOT, "include")):
+        if h.endswith(".h"):
+            src = open(os.path.join(ROOT, "include", h)).read()
+            src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+            names |= set(re.findall(r"\b(moe_[a-z0-9_]+)\s*\(", src))
+    return names
+
+
+def test_library_exports_every_declared_symbol():
+    L = moe_lib.lib()
+    declared = _declared_functions()
+    assert "moe_gemm" in declared and "moe_plan_build" in declared and "moe_route" in declared
+    for name in declared:
+        assert hasattr(L, name), name
+    assert set(moe_lib.EXPORTED) == declared
+    assert b"sm_100a" in L.moe_version()
+
+
+def _compare(counts, N, bm, bn, pad):
+    blob = moe_lib.moe_plan_build(counts, 64, N, bm, bn, moe_lib.MOE_PAD_REPEAT if pad == "repeat" else 0)
+    p = moe_lib.parse_plan_blob(blob)
+    ref = omoe.plan(counts, N, bm, bn, pad_mode=pad)
+    assert p["M"] == ref["M"] and p["total"] == ref["total"]
+    if ref["M"] == 0:
+        return
+    assert p["prefix"].tolist() == ref["padded"]
+    assert p["sigma"][: p["M"]].tolist() == ref["sigma"]
+    row_off = np.concatenate([[0], np.cumsum(counts)])
+    assert p["row_off"].tolist() == row_off.tolist()
+    for i, t in enumerate(ref["tasks"]):
+        q = p["params"][i]
+        assert q[0] == t["expert"] and q[1] == row_off[t["expert"]] + t["row_begin"] and q[2] == t["rows"]
+        assert q[4] == t["bm"] and q[5] == t["bn"]
+        assert q[6] * q[7] == ref["nu"][i]
+        assert q[6] == -(-t["rows"] // bm)
+
+
+def test_planner_matches_oracle_configs():
+    _compare(np.array([11, 0, 11, 10]), 128, 128, 128, "max")          # tiny-A
+    c = synth.CONFIGS["mix"]
+    _compare(np.bincount(synth.route(c, 0).ravel(), minlength=8), c.N, 128, 256, "max")
+    c = synth.CONFIGS["ds"]
+    counts = np.bincount(synth.route(c, 0).ravel(), minlength=64)
+    for bn in (128, 176, 256):
+        _compare(counts, c.N, 128, bn, "max")
+        _compare(counts, c.N, 128, bn, "repeat")
+    c = synth.CONFIGS["paper_worst"]
+    _compare(np.bincount(synth.route(c).ravel(), minlength=64), c.N, 128, 256, "max")
+
+
+def test_planner_matches_oracle_random_corpus():
+    rng = random.Random(11)
+    for _ in range(300):
+        E = rng.randint(1, 300)
+        counts = np.array([0 if rng.random() < 0.4 else rng.randint(1, 3000) for _ in range(E)])
+        N = 8 * rng.randint(1, 2500)
+        bn = 16 * rng.randint(1, 16)
+        _compare(counts, N, 128, bn, rng.choice(["max", "repeat"]))
+
+
+def test_planner_decode_bijection_through_blob():
+    """Decode every block of a library-built blob with the oracle's Alg. 2 and check the lattice."""
+    counts = np.array([300, 0, 5, 129, 0, 1000, 1])
+    blob = moe_lib.parse_plan_blob(moe_lib.moe_plan_build(counts, 64, 200, 128, 64))
+    seen = set()
+    for B in range(blob["total"]):
+        h, l = om.mapping_chunked(blob["prefix"].tolist(), B)
+        task = int(blob["sigma"][h])
+        q = blob["params"][task]
+        rt, ct = l % q[6], l // q[6]
+        assert 0 <= ct < q[7]
+        seen.add((task, rt, ct))
+    assert len(seen) == blob["total"]
+
+
+def test_planner_errors():
+    L = moe_lib.lib()
+    with pytest.raises(moe_lib.MoeError) as e:
+        moe_lib.moe_plan_build([1, 2], 63, 128)
+    assert e.value.status == -2
+    with pytest.raises(moe_lib.MoeError) as e:
+        moe_lib.moe_plan_build([1, 2], 64, 128, bm=64)
+    assert e.value.status == -2
+    with pytest.raises(moe_lib.MoeError) as e:
+        moe_lib.moe_plan_build([1, 2], 64, 128, bn=24)
+    assert e.value.status == -2
+    with pytest.raises(moe_lib.MoeError) as e:
+        moe_lib.moe_plan_build([1, -2], 64, 128)
+    assert e.value.status == -1
+    with pytest.raises(moe_lib.MoeError) as e:
+        moe_lib.moe_plan_build([2**31 - 1, 5], 64, 128)
+    assert e.value.status == -3
+    assert b"2^31" in L.moe_last_error()
+    blob = moe_lib.moe_plan_build([0, 0, 0], 64, 128)
+    p = moe_lib.parse_plan_blob(blob)
+    assert p["M"] == 0 and p["total"] == 0
+    # total tiles overflow int32
+    with pytest.raises(moe_lib.MoeError) as e:
+        moe_lib.moe_plan_build([2**30] * 1, 64, 8 * 200000, bn=16)
+    assert e.value.status == -3
+    # status code of an all-empty build is MOE_OK_EMPTY
+    c = np.zeros(3, dtype=np.int32)
+    blob = np.zeros(4096, dtype=np.int32)
+    n = ctypes.c_int64()
+    st = L.moe_plan_build(c.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), 3, 64, 128, 128, 256, 0,
+                          blob.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), blob.size, ctypes.byref(n))
+    assert st == moe_lib.MOE_OK_EMPTY
