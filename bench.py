@@ -1,0 +1,362 @@
+#!/usr/bin/env python
+"""Benchmark of the statically batched MoE expert GEMM (arXiv 2501.16103) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config mix]
+
+A step = one pass of the whole hot path over one batch of synthetic input
+(SURVEY §8(a)): moe_route (device buckets) -> counts D2H -> host plan (Alg. 1 +
+sigma) + blob H2D -> moe_gemm (one tcgen05 launch over every expert tile).
+`value` = useful FLOPs (2 * sum m_e * H * N) / device step time, inputs resident
+in HBM; `e2e` = the same metric with X / top-k ids copied from pinned host memory
+and Y copied back inside the timed region.  L2 is flushed (256 MiB memset)
+before every timed step.  `--impl reference` times the fp64 CPU oracle on a
+bounded sample of the same workload (the tier's reference arm).
+
+Multi-GPU (torchrun, N > 1): see DESIGN.md §Multi-GPU; each rank runs the
+expert-parallel shard of the `ep` workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+METRIC = "MoE GEMM TFLOPS and % of B200 BF16 tensor peak at 1/2/4/8 GPUs"
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured (MEASURED_PEAKS.json)"
+    return dict(FALLBACK_PEAKS), "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons via NVML during the timed region."""
+
+    REASONS = {
+        "sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
+        "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
+    }
+
+    def __init__(self, index: int, period_s: float = 0.005):
+        self.samples, self.reasons, self.ok = [], set(), False
+        self.period = period_s
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = repr(e)
+            self.max_mhz = None
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                fn = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                    nv.nvmlDeviceGetCurrentClocksThrottleReasons
+                r = fn(self.h)
+                for name, bit in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self._t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def load_traffic(workload: str):
+    """dram bytes per launch of moe_gemm_kernel from the committed ncu --set full summary."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        v = d.get(workload)
+        if v:
+            return v.get("dram_bytes_per_launch"), v.get("source")
+    return None, None
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle timing (cpu_baseline leg / reference arm)
+# ---------------------------------------------------------------------------
+def oracle_sample(cfg, seed: int, budget_s: float, cache: dict | None = None):
+    """Times oracle.moe.expert_gemm expert by expert on the workload until budget_s of
+    CPU work has been spent (input generation excluded).  Returns (flops, seconds, sample, cores)."""
+    from oracle import moe as omoe
+    try:
+        from threadpoolctl import threadpool_info
+        cores = sum(int(i.get("num_threads", 1)) for i in threadpool_info() if i.get("user_api") == "blas") or 1
+    except Exception:  # pragma: no cover
+        cores = os.cpu_count()
+    cache = {} if cache is None else cache
+    if "inputs" not in cache:
+        ids = synth.route(cfg, seed)
+        cache["inputs"] = (omoe.buckets(ids, cfg.E), synth.make_x(seed, cfg.T, cfg.H))
+    (counts, row_off, tok, _), X = cache["inputs"]
+    flops, secs, done = 0, 0.0, []
+    for e in range(cfg.E):
+        if counts[e] == 0:
+            continue
+        if e not in cache:                                               # generation is not timed
+            cache[e] = synth.make_w(seed, cfg.E, cfg.H, cfg.N, experts=[e])   # [1, H, N]
+        W = cache[e]
+        a, b = int(row_off[e]), int(row_off[e + 1])
+        sub_tok = tok[a:b]
+        t0 = time.perf_counter()
+        omoe.expert_gemm(X, W, sub_tok, np.array([0, b - a]))
+        secs += time.perf_counter() - t0
+        flops += 2 * (b - a) * cfg.H * cfg.N
+        done.append(e)
+        if secs >= budget_s:
+            break
+    sample = (f"{cfg.name} seed {seed}: experts {done} ({int(sum(counts[e] for e in done))} of "
+              f"{int(counts.sum())} rows, full H x N), fp64 numpy/OpenBLAS")
+    return flops, secs, sample, cores
+
+
+def run_reference(args, cfg):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    # warm-up: one small expert product so BLAS threads exist
+    from oracle import moe as omoe
+    omoe.expert_gemm(np.ones((8, 64)), np.ones((1, 64, 64)), np.arange(8), np.array([0, 8]))
+    per_step = max(1.0, 60.0 / max(args.steps + args.warmup, 1))
+    vals, ms = [], []
+    info = None
+    cache = {}
+    for i in range(args.warmup + args.steps):
+        f, s, sample, cores = oracle_sample(cfg, args.seed, per_step, cache)
+        if i >= args.warmup:
+            vals.append(f / s / 1e12)
+            ms.append(s * 1e3)
+            info = (sample, cores)
+    v = float(statistics.median(vals))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "TFLOP/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(statistics.mean(ms)),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": config_dict(cfg, args),
+        "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": info[1], "kind": "oracle", "sample": info[0]},
+        "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(cfg, args):
+    return {"workload": f"{cfg.name}: E={cfg.E} top-{cfg.k} T={cfg.T} H={cfg.H} N={cfg.N} "
+                        f"routing={cfg.routing} seed={args.seed}",
+            "tile": f"128x{args.bn}", "out_dtype": args.out_dtype, "global_batch": cfg.T,
+            "l2": "flushed before every timed step (256 MiB memset); W alone exceeds L2",
+            "parallelism": f"ep{args.gpus}" if args.gpus > 1 else "1 GPU"}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args, cfg):
+    import torch
+
+    import paper_2501_16103_b200 as M
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    M.moe_device_info()
+    peaks, peak_src = load_peaks()
+    out_dtype = torch.bfloat16 if args.out_dtype == "bf16" else torch.float32
+
+    ids = synth.route(cfg, args.seed)
+    topk_d = torch.from_numpy(ids).to(dev)
+    Xd = synth.make_x_torch(args.seed, cfg.T, cfg.H, device=dev)
+    Wd = synth.make_w_torch(args.seed, cfg.E, cfg.H, cfg.N, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flops = cfg.flops
+    stream = torch.cuda.current_stream()
+
+    plan = None
+
+    def step(Y=None):
+        nonlocal plan
+        counts, row_off, tok, slot, _ = M.moe_route(topk_d, cfg.E, with_slot=False)
+        counts_h = counts.cpu().numpy()
+        if plan is None:
+            plan = M.Plan(counts_h, cfg.H, cfg.N, 128, args.bn)
+        else:
+            plan.update(counts_h)
+        g0 = torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        Y = M.moe_gemm(plan, Xd, tok, Wd, Y=Y, out_dtype=out_dtype)
+        return Y, g0
+
+    Y0, _ = step()
+    Ybuf = torch.empty_like(Y0)
+    for _ in range(args.warmup):
+        step(Ybuf)
+    torch.cuda.synchronize()
+
+    step_ms, gemm_ms = [], []
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            _, g0 = step(Ybuf)
+            s1.record(stream)
+            s1.synchronize()
+            step_ms.append(s0.elapsed_time(s1))
+            gemm_ms.append(g0.elapsed_time(s1))
+    torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    t_total = sum(step_ms)
+    if ws > 1:
+        t = torch.tensor([t_total], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        t_total = float(t.item())
+    value = flops * ws * args.steps / (t_total * 1e-3) / 1e12
+    gemm_avg = statistics.mean(gemm_ms)
+    achieved = flops / (gemm_avg * 1e-3) / 1e12
+    peak = float(peaks["bf16_tflops"])
+    traffic, tsrc = load_traffic(cfg.name)
+
+    # ---- e2e through the public API with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        X_h = synth.make_x_torch(args.seed, cfg.T, cfg.H).pin_memory()
+        ids_h = torch.from_numpy(ids).pin_memory()
+        Y_h = torch.empty(Y0.shape, dtype=Y0.dtype).pin_memory()
+        Xe = torch.empty_like(Xd)
+        te = torch.empty_like(topk_d)
+
+        def e2e_step():
+            Xe.copy_(X_h, non_blocking=True)
+            te.copy_(ids_h, non_blocking=True)
+            Y, counts_h, _, _, _, _ = M.moe_forward(te, Xe, Wd, cfg.E, bn=args.bn, out_dtype=out_dtype, plan=plan)
+            Y_h.copy_(Y, non_blocking=True)
+            return counts_h
+
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        e_ms = []
+        for _ in range(max(3, min(args.steps, 10))):
+            flush.zero_()
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            e2e_step()
+            s1.record(stream)
+            s1.synchronize()
+            e_ms.append(s0.elapsed_time(s1))
+        h2d = X_h.numel() * X_h.element_size() + ids_h.numel() * 4 + 4 * plan.blob().size
+        d2h = Y_h.numel() * Y_h.element_size() + 4 * cfg.E
+        e2e = {"value": flops / (statistics.mean(e_ms) * 1e-3) / 1e12, "unit": "TFLOP/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": statistics.mean(e_ms)}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        f, s, sample, cores = oracle_sample(cfg, args.seed, args.cpu_budget)
+        cpu = {"value": f / s / 1e12, "unit": "TFLOP/s", "cores": cores, "kind": "oracle", "sample": sample,
+               "seconds": s}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": statistics.mean(step_ms), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": config_dict(cfg, args),
+            "pct_of_peak": value / peak,
+            "kernel": {"name": "moe_gemm_kernel", "ms_per_launch": gemm_avg, "tflops": achieved,
+                       "pct_of_measured_burst_peak": achieved / peak,
+                       "pct_of_measured_sustained_peak": achieved / float(peaks["bf16_tflops_sustained"]),
+                       "pct_of_datasheet_2250": achieved / 2250.0},
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "peak_source": f"{peak_src} bf16_tflops (burst; kernel timed per launch)",
+                         "algorithmic_flops_per_launch": flops, "traffic_source": tsrc},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": 3 * args.steps,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="mix")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--bn", type=int, default=256)
+    ap.add_argument("--out-dtype", choices=["bf16", "f32"], default="bf16")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=10.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        raise SystemExit("--warmup must be >= 3")
+    cfg = synth.CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -5,13 +5,15 @@
 //   * every role warp decodes its virtual tile v with the warp vote/popcount
 //     mapping over TilePrefix (Alg. 2 + chunk loop) and sigma (Alg. 4
 //     line 289) — "let all warps execute the algorithm";
-//   * warp 0 (producer) stages, per 64-wide K block, the tile's token rows with
-//     TMA tile::gather4 straight from X through the token-index array (P:334-335,
-//     no gathered copy) and the expert's W block with 3-D TMA tile loads, into a
-//     4-stage SW128 shared-memory ring guarded by mbarriers (deepened);
-//   * warp 1 issues tcgen05.mma (M=128, N=BN, K=16, bf16 x bf16 -> fp32) into a
+//   * warps 0-3 (producers) stage, per 64-wide K block, the tile's 128 token rows
+//     with TMA tile::gather4 straight from X through the token-index array
+//     (no gathered copy; 8 gather4 per warp, since TMA issue is
+//     serialised within a warp) and warp 0 the expert's W block with one 4-D TMA
+//     tile load, into a 4-stage SW128 shared-memory ring guarded by mbarriers
+//     (deepened);
+//   * warp 4 issues tcgen05.mma (M=128, N=BN, K=16, bf16 x bf16 -> fp32) into a
 //     double-buffered TMEM accumulator (P:351's WGMMA, Blackwell-native);
-//   * warps 2-5 drain TMEM with tcgen05.ld, convert and store Y rows, masked to
+//   * warps 5-8 drain TMEM with tcgen05.ld, convert and store Y rows, masked to
 //     the task's rows and to N, overlapping the next tile's main loop.
 // Static batching: CTA b processes v = b, b + grid, b + 2*grid, ... (no
 // dynamic scheduler, no atomics).  Within a task, tiles are ordered row-tile
@@ -44,8 +46,10 @@ constexpr int kStages = 4;
 constexpr int kABytes = kBM * kBK * 2;          // 16 KB: 128 gathered rows x 64
 constexpr int kBBoxBytes = 64 * kBK * 2;        // 8 KB: one TMA box of W (64 N x 64 K)
 constexpr int kBStageBytes = 4 * kBBoxBytes;    // up to BN = 256
+constexpr int kProdWarps = 4;                   // gather4 issue is serialised per warp: spread it
+constexpr int kMmaWarp = kProdWarps;
 constexpr int kEpiWarps = 4;
-constexpr int kThreads = 32 * (2 + kEpiWarps);  // producer, MMA, 4 epilogue warps
+constexpr int kThreads = 32 * (kProdWarps + 1 + kEpiWarps);
 constexpr uint32_t kTmemCols = 512;             // 2 accumulators x 256 fp32 columns
 constexpr uint32_t kAccCols = 256;
 constexpr int kMaxMPad = 1024;
@@ -62,6 +66,7 @@ struct GemmArgs {
   int32_t total;
   int32_t M_pad;
   int32_t off_params;
+  int32_t w4d;               // W map is 4-D {64, H, N/64, E}: one TMA per B stage
 };
 
 // ---------------------------------------------------------------------------
@@ -160,7 +165,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   for (int i = threadIdx.x; i < 2 * a.M_pad; i += blockDim.x) s_prefix[i] = a.plan[MOE_PLAN_HEADER + i];
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
-      mbar_init(full_bar(s), 1);
+      mbar_init(full_bar(s), kProdWarps);
       mbar_init(empty_bar(s), 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -173,17 +178,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     prefetch_tmap(&tmX);
     prefetch_tmap(&tmW);
   }
-  if (warp == 1) tmem_alloc<kTmemCols>(smem_u32(tmem_holder));
+  if (warp == kMmaWarp) tmem_alloc<kTmemCols>(smem_u32(tmem_holder));
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
   const int32_t* params = a.plan + a.off_params;
 
-  if (warp == 0) {
-    // ===================== producer: TMA gather4 (X rows) + TMA tiles (W) =====================
+  if (warp < kProdWarps) {
+    // ===================== producers: TMA gather4 (X rows) + TMA tiles (W) =====================
+    // Producer warp p stages tile rows [32p, 32p+32): lanes 0..7 each gather 4 rows.
+    // Warp 0 also stages the W block.  Each warp arms the full barrier with its own bytes.
     const uint64_t pol_x = policy_evict_last();    // X_e is re-read by every column tile of the task
     const uint64_t pol_w = policy_evict_normal();
+    const int p = warp;
     int stage = 0;
     uint32_t phase = 0;
     for (int v = blockIdx.x; v < a.total; v += gridDim.x) {
@@ -192,31 +200,38 @@ __global__ void __launch_bounds__(kThreads, 1)
       const Tile t = load_tile(params, task, l);
       const int rbeg = t.rt * kBM;
       const int nvalid = min(kBM, t.rows - rbeg);
-      // Lane i gathers tile rows 4i..4i+3; rows past the task's end repeat its last
-      // valid token (their results are never stored).
+      // Rows past the task's end repeat its last valid token (their results are never stored).
       const int32_t* idx = a.token_idx + t.row0 + rbeg;
-      const int r0 = __ldg(idx + min(4 * lane + 0, nvalid - 1));
-      const int r1 = __ldg(idx + min(4 * lane + 1, nvalid - 1));
-      const int r2 = __ldg(idx + min(4 * lane + 2, nvalid - 1));
-      const int r3 = __ldg(idx + min(4 * lane + 3, nvalid - 1));
+      const int rr = 32 * p + 4 * (lane & 7);
+      const int r0 = __ldg(idx + min(rr + 0, nvalid - 1));
+      const int r1 = __ldg(idx + min(rr + 1, nvalid - 1));
+      const int r2 = __ldg(idx + min(rr + 2, nvalid - 1));
+      const int r3 = __ldg(idx + min(rr + 3, nvalid - 1));
       const int n0 = t.ct * t.bn;
       const int nbox = (t.bn + 63) >> 6;
-      const uint32_t tx = kABytes + nbox * kBBoxBytes;
+      const uint32_t tx = kABytes / kProdWarps + (p == 0 ? nbox * kBBoxBytes : 0);
       for (int kb = 0; kb < a.num_kb; ++kb) {
         mbar_wait(empty_bar(stage), phase ^ 1u);
         if (lane == 0) mbar_arrive_expect_tx(full_bar(stage), tx);
         __syncwarp();
-        tma_gather4(&tmX, full_bar(stage), sA + stage * kABytes + lane * 512, kb * kBK, r0, r1, r2, r3, pol_x);
-        if (lane < nbox)
-          tma_load_3d(&tmW, full_bar(stage), sB + stage * kBStageBytes + lane * kBBoxBytes, n0 + lane * 64,
-                      kb * kBK, t.expert, pol_w);
+        if (lane < 8)
+          tma_gather4(&tmX, full_bar(stage), sA + stage * kABytes + rr * 128, kb * kBK, r0, r1, r2, r3, pol_x);
+        if (p == 0) {
+          const uint32_t dstB = sB + stage * kBStageBytes;
+          if (a.w4d) {
+            if (lane == 8) tma_load_4d(&tmW, full_bar(stage), dstB, 0, kb * kBK, n0 >> 6, t.expert, pol_w);
+          } else if (lane >= 8 && lane < 8 + nbox) {
+            const int j = lane - 8;
+            tma_load_3d(&tmW, full_bar(stage), dstB + j * kBBoxBytes, n0 + j * 64, kb * kBK, t.expert, pol_w);
+          }
+        }
         if (++stage == kStages) {
           stage = 0;
           phase ^= 1u;
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == kMmaWarp) {
     // ===================== MMA issuer: one thread drives tcgen05 =====================
     int stage = 0;
     uint32_t phase = 0;
@@ -295,7 +310,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) {
+  if (warp == kMmaWarp) {
     tc_fence_after();
     tmem_dealloc<kTmemCols>(tmem_base);
   }
@@ -378,16 +393,29 @@ moe_status make_x_map(CUtensorMap* m, const void* X, int64_t T, int64_t H) {
   return MOE_OK;
 }
 
-moe_status make_w_map(CUtensorMap* m, const void* W, int64_t E, int64_t H, int64_t N) {
+moe_status make_w_map(CUtensorMap* m, const void* W, int64_t E, int64_t H, int64_t N, int bn, bool w4d) {
   auto fn = encode_fn();
   if (!fn) MOE_FAIL(MOE_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
-  const cuuint64_t dims[3] = {(cuuint64_t)N, (cuuint64_t)H, (cuuint64_t)E};
-  const cuuint64_t strides[2] = {(cuuint64_t)N * 2, (cuuint64_t)H * N * 2};
-  const cuuint32_t box[3] = {64, (cuuint32_t)kBK, 1};
-  const cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(W), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r;
+  if (w4d) {
+    // W viewed as {64 (n within chunk), H, N/64 (chunk), E}: one box = the whole B stage,
+    // laid out chunk-major, then k, then n — the MN-major SW128 canonical layout.
+    const cuuint64_t dims[4] = {64, (cuuint64_t)H, (cuuint64_t)(N / 64), (cuuint64_t)E};
+    const cuuint64_t strides[3] = {(cuuint64_t)N * 2, 128, (cuuint64_t)H * N * 2};
+    const cuuint32_t box[4] = {64, (cuuint32_t)kBK, (cuuint32_t)((bn + 63) / 64), 1};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(W), dims, strides, box, estr,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else {
+    const cuuint64_t dims[3] = {(cuuint64_t)N, (cuuint64_t)H, (cuuint64_t)E};
+    const cuuint64_t strides[2] = {(cuuint64_t)N * 2, (cuuint64_t)H * N * 2};
+    const cuuint32_t box[3] = {64, (cuuint32_t)kBK, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(W), dims, strides, box, estr,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
   if (r != CUDA_SUCCESS) MOE_FAIL(MOE_ERR_CUDA, "cuTensorMapEncodeTiled(W) failed: %d", (int)r);
   return MOE_OK;
 }
@@ -443,7 +471,8 @@ moe_status moe_gemm(const moe_plan* plan, const void* X, int64_t T, const int32_
   CUtensorMap tmX, tmW;
   moe_status st = make_x_map(&tmX, X, T, v.H);
   if (st != MOE_OK) return st;
-  st = make_w_map(&tmW, W, v.E, v.H, v.N);
+  const bool w4d = (v.N % 64) == 0;
+  st = make_w_map(&tmW, W, v.E, v.H, v.N, v.bn, w4d);
   if (st != MOE_OK) return st;
 
   GemmArgs a;
@@ -456,6 +485,7 @@ moe_status moe_gemm(const moe_plan* plan, const void* X, int64_t T, const int32_
   a.total = v.total;
   a.M_pad = v.M_pad;
   a.off_params = (int32_t)v.off_params;
+  a.w4d = w4d ? 1 : 0;
 
   const size_t smem = kSmemFixed + 8 * (size_t)v.M_pad;
   static std::once_flag attr_once;

@@ -60,6 +60,14 @@ __device__ __forceinline__ void tma_load_3d(const void* tmap, uint32_t bar, uint
       "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "l"(policy)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_4d(const void* tmap, uint32_t bar, uint32_t dst, int32_t c0, int32_t c1,
+                                            int32_t c2, int32_t c3, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2], %7;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "l"(policy)
+      : "memory");
+}
 // 2-D gather of four rows (r0..r3) of a box {inner, 1} at column c0: 4 x inner elements.
 __device__ __forceinline__ void tma_gather4(const void* tmap, uint32_t bar, uint32_t dst, int32_t c0, int32_t r0,
                                             int32_t r1, int32_t r2, int32_t r3, uint64_t policy) {
