@@ -23,6 +23,23 @@ extern "C" {
 moe_status moe_probe_gather4(const void* X_dev, int64_t T, int64_t H, const int32_t* rows_dev, int32_t col0,
                              void* out_dev, void* stream);
 
+/*
+ * moe_gemm with per-CTA cycle counters (an instrumented build of the same
+ * kernel; clock64() around every mbarrier wait).  prof_dev: device int64 array of
+ * grid * 8 words, grid = min(total tiles, SM count); per CTA:
+ *   [0] MMA warp cycles waiting for a free TMEM accumulator (epilogue-bound time)
+ *   [1] MMA warp cycles waiting for TMA bytes (load-bound time)
+ *   [2] MMA warp cycles in its tile loop
+ *   [3] producer warp 0 cycles waiting for a free stage
+ *   [4] epilogue warp (TMEM lanes 0-31) cycles waiting for an accumulator
+ *   [5] the same warp's cycles draining TMEM and storing Y
+ *   [6] tiles processed by the CTA
+ *   [7] producer warp 0 cycles in its tile loop
+ * Results (Y) are identical to moe_gemm.
+ */
+moe_status moe_gemm_profile(const moe_plan* plan, const void* X_dev, int64_t T, const int32_t* token_idx_dev,
+                            const void* W_dev, void* Y_dev, int32_t y_dtype, long long* prof_dev, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

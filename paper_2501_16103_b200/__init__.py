@@ -29,6 +29,7 @@ EXPORTED = (
     "moe_plan_blob_words", "moe_plan_build", "moe_plan_create", "moe_plan_update", "moe_plan_query",
     "moe_plan_blob", "moe_plan_device_blob", "moe_plan_destroy", "moe_route", "moe_gemm",
     "moe_decode_debug", "moe_device_info", "moe_last_error", "moe_version", "moe_probe_gather4",
+    "moe_gemm_profile",
 )
 
 
@@ -71,6 +72,7 @@ def lib() -> ctypes.CDLL:
         "moe_last_error": (ctypes.c_char_p, []),
         "moe_version": (ctypes.c_char_p, []),
         "moe_probe_gather4": (ctypes.c_int32, [vp, ctypes.c_int64, ctypes.c_int64, vp, ctypes.c_int32, vp, vp]),
+        "moe_gemm_profile": (ctypes.c_int32, [vp, vp, ctypes.c_int64, vp, vp, vp, ctypes.c_int32, vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -218,6 +220,23 @@ def moe_gemm(plan: Plan, X, token_idx, W, Y=None, out_dtype=None, stream=None):
     _check(lib().moe_gemm(plan.handle, X.data_ptr(), X.shape[0], token_idx.data_ptr(), W.data_ptr(),
                           Y.data_ptr(), yd, _stream(stream)))
     return Y
+
+
+PROF_SLOTS = ("mma_wait_tmem", "mma_wait_full", "mma_total", "prod_wait_empty", "epi_wait_full", "epi_work",
+              "tiles", "prod_total")
+
+
+def moe_gemm_profile(plan: Plan, X, token_idx, W, Y, stream=None):
+    """Instrumented moe_gemm: returns Y and per-CTA cycle counters [grid, 8] (see moe_sm100_debug.h)."""
+    import torch
+
+    n_sm = moe_device_info()[0]
+    grid = min(plan.total_tiles, n_sm)
+    prof = torch.zeros((max(grid, 1), len(PROF_SLOTS)), dtype=torch.int64, device=X.device)
+    yd = MOE_DTYPE_F32 if Y.dtype == torch.float32 else MOE_DTYPE_BF16
+    _check(lib().moe_gemm_profile(plan.handle, X.data_ptr(), X.shape[0], token_idx.data_ptr(), W.data_ptr(),
+                                  Y.data_ptr(), yd, prof.data_ptr(), _stream(stream)))
+    return Y, prof[:grid]
 
 
 def moe_decode_debug(plan: Plan, stream=None):

@@ -5,15 +5,17 @@
 //   * every role warp decodes its virtual tile v with the warp vote/popcount
 //     mapping over TilePrefix (Alg. 2 + chunk loop) and sigma (Alg. 4
 //     line 289) — "let all warps execute the algorithm";
-//   * warps 0-3 (producers) stage, per 64-wide K block, the tile's 128 token rows
-//     with TMA tile::gather4 straight from X through the token-index array
-//     (no gathered copy; 8 gather4 per warp, since TMA issue is
-//     serialised within a warp) and warp 0 the expert's W block with one 4-D TMA
-//     tile load, into a 4-stage SW128 shared-memory ring guarded by mbarriers
-//     (deepened);
-//   * warp 4 issues tcgen05.mma (M=128, N=BN, K=16, bf16 x bf16 -> fp32) into a
+//   * warps 0-3 (A producers) stage, per 64-wide K block, the tile's 128 token
+//     rows straight from X through the token-index array (no gathered
+//     copy): either with TMA tile::gather4 or with cp.async on the LSU path (the
+//     default: gather4 is issue-rate bound at ~17-21 B/clk/SM, below the 32 B/clk
+//     a 128x256 tile consumes; DESIGN.md §A staging);
+//   * warp 4 (B producer) stages the expert's W block with one 4-D TMA tile load;
+//     both feed a 4-stage SW128 shared-memory ring guarded by mbarriers
+//     (P:352-353's two-stage prefetch, deepened);
+//   * warp 5 issues tcgen05.mma (M=128, N=BN, K=16, bf16 x bf16 -> fp32) into a
 //     double-buffered TMEM accumulator (P:351's WGMMA, Blackwell-native);
-//   * warps 5-8 drain TMEM with tcgen05.ld, convert and store Y rows, masked to
+//   * warps 6-9 drain TMEM with tcgen05.ld, convert and store Y rows, masked to
 //     the task's rows and to N, overlapping the next tile's main loop.
 // Static batching: CTA b processes v = b, b + grid, b + 2*grid, ... (no
 // dynamic scheduler, no atomics).  Within a task, tiles are ordered row-tile
@@ -25,6 +27,7 @@
 #include <cuda_runtime.h>
 
 #include <climits>
+#include <cstdlib>
 #include <mutex>
 
 #include "common.h"
@@ -46,10 +49,13 @@ constexpr int kStages = 4;
 constexpr int kABytes = kBM * kBK * 2;          // 16 KB: 128 gathered rows x 64
 constexpr int kBBoxBytes = 64 * kBK * 2;        // 8 KB: one TMA box of W (64 N x 64 K)
 constexpr int kBStageBytes = 4 * kBBoxBytes;    // up to BN = 256
-constexpr int kProdWarps = 4;                   // gather4 issue is serialised per warp: spread it
-constexpr int kMmaWarp = kProdWarps;
-constexpr int kEpiWarps = 4;
-constexpr int kThreads = 32 * (kProdWarps + 1 + kEpiWarps);
+constexpr int kAWarps = 4;                      // A producers (token rows): warps 0-3
+constexpr int kBWarp = kAWarps;                 // B producer (W block, TMA): warp 4
+constexpr int kMmaWarp = kAWarps + 1;           // tcgen05 issuer: warp 5
+constexpr int kEpiWarps = 4;                    // epilogue: warps 6-9 (TMEM lane quarters 2,3,0,1)
+constexpr int kThreads = 32 * (kAWarps + 2 + kEpiWarps);
+constexpr int kALag = 2;
+constexpr int kDefaultAMode = 1;                        // cp.async path: stages in flight before a thread signals
 constexpr uint32_t kTmemCols = 512;             // 2 accumulators x 256 fp32 columns
 constexpr uint32_t kAccCols = 256;
 constexpr int kMaxMPad = 1024;
@@ -66,7 +72,25 @@ struct GemmArgs {
   int32_t total;
   int32_t M_pad;
   int32_t off_params;
+  int32_t T;
   int32_t w4d;               // W map is 4-D {64, H, N/64, E}: one TMA per B stage
+  long long* prof;           // kProf builds only: per-CTA cycle counters (moe_gemm_profile)
+  int32_t a_mode;            // A staging: 0 = TMA tile::gather4, 1 = cp.async (LSU path), see DESIGN.md
+  int32_t H;
+  const __nv_bfloat16* X;
+};
+
+// Per-CTA counters written by the instrumented build (kProf = true).
+enum ProfSlot {
+  kProfMmaWaitTmem = 0,   // MMA warp: cycles waiting for the epilogue to free an accumulator
+  kProfMmaWaitFull,       // MMA warp: cycles waiting for TMA bytes
+  kProfMmaTotal,          // MMA warp: cycles in its tile loop
+  kProfProdWaitEmpty,     // producer warp 0: cycles waiting for a free stage
+  kProfEpiWaitFull,       // epilogue warp (quarter 0): cycles waiting for an accumulator
+  kProfEpiWork,           // epilogue warp (quarter 0): cycles draining + storing
+  kProfTiles,             // tiles processed by the CTA
+  kProfProdTotal,         // producer warp 0: cycles in its tile loop
+  kProfSlots
 };
 
 // ---------------------------------------------------------------------------
@@ -140,6 +164,18 @@ __device__ __forceinline__ void store_chunk(const GemmArgs& a, int64_t yrow, int
   }
 }
 
+template <bool kProf>
+__device__ __forceinline__ void wait_timed(uint32_t bar, uint32_t parity, long long& acc) {
+  if constexpr (kProf) {
+    const long long t0 = clock64();
+    mbar_wait(bar, parity);
+    acc += clock64() - t0;
+  } else {
+    mbar_wait(bar, parity);
+  }
+}
+
+template <bool kProf>
 __global__ void __launch_bounds__(kThreads, 1)
     moe_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
                     const GemmArgs a) {
@@ -165,7 +201,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   for (int i = threadIdx.x; i < 2 * a.M_pad; i += blockDim.x) s_prefix[i] = a.plan[MOE_PLAN_HEADER + i];
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
-      mbar_init(full_bar(s), kProdWarps);
+      mbar_init(full_bar(s), kAWarps + 1);        // one arrival per A warp + the B warp
       mbar_init(empty_bar(s), 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -185,50 +221,110 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem_base = *tmem_holder;
   const int32_t* params = a.plan + a.off_params;
 
-  if (warp < kProdWarps) {
-    // ===================== producers: TMA gather4 (X rows) + TMA tiles (W) =====================
-    // Producer warp p stages tile rows [32p, 32p+32): lanes 0..7 each gather 4 rows.
-    // Warp 0 also stages the W block.  Each warp arms the full barrier with its own bytes.
+  if (warp < kAWarps) {
+    // ===================== A producers: the tile's 128 token rows, 64 columns per stage =====================
+    // Gathered straight from X through the token-index array: no gathered copy of X.
+    // a_mode 0: TMA tile::gather4 — warp p stages rows [32p, 32p+32), lanes 0..7 four rows each.
+    // a_mode 1: cp.async 16 B per thread, 8 threads per 128-byte row (coalesced), SW128 swizzle
+    //           applied by hand; rows past the task's end (and columns past H) are zero-filled
+    //           without a read.  Completion: each thread waits for its copies kALag stages later,
+    //           fences them into the async proxy (tcgen05 reads smem through it) and the warp arrives.
     const uint64_t pol_x = policy_evict_last();    // X_e is re-read by every column tile of the task
-    const uint64_t pol_w = policy_evict_normal();
     const int p = warp;
-    int stage = 0;
-    uint32_t phase = 0;
+    uint32_t g = 0;                                 // stages issued by this warp, over all tiles
+    long long c_wait = 0, c_t0 = kProf ? clock64() : 0;
+    const int ch = threadIdx.x & 7;                 // cp.async: 16-byte chunk of the 128-byte row
+    const int rsub = threadIdx.x >> 3;              // cp.async: row within a 16-row group
+    const uint32_t dst_off = rsub * 128 + ((ch ^ (rsub & 7)) << 4);
     for (int v = blockIdx.x; v < a.total; v += gridDim.x) {
       int h, task, l;
       map_tile(s_prefix, s_sigma, a.M_pad, v, h, task, l);
       const Tile t = load_tile(params, task, l);
       const int rbeg = t.rt * kBM;
       const int nvalid = min(kBM, t.rows - rbeg);
-      // Rows past the task's end repeat its last valid token (their results are never stored).
       const int32_t* idx = a.token_idx + t.row0 + rbeg;
-      const int rr = 32 * p + 4 * (lane & 7);
-      const int r0 = __ldg(idx + min(rr + 0, nvalid - 1));
-      const int r1 = __ldg(idx + min(rr + 1, nvalid - 1));
-      const int r2 = __ldg(idx + min(rr + 2, nvalid - 1));
-      const int r3 = __ldg(idx + min(rr + 3, nvalid - 1));
-      const int n0 = t.ct * t.bn;
-      const int nbox = (t.bn + 63) >> 6;
-      const uint32_t tx = kABytes / kProdWarps + (p == 0 ? nbox * kBBoxBytes : 0);
-      for (int kb = 0; kb < a.num_kb; ++kb) {
-        mbar_wait(empty_bar(stage), phase ^ 1u);
-        if (lane == 0) mbar_arrive_expect_tx(full_bar(stage), tx);
-        __syncwarp();
-        if (lane < 8)
-          tma_gather4(&tmX, full_bar(stage), sA + stage * kABytes + rr * 128, kb * kBK, r0, r1, r2, r3, pol_x);
-        if (p == 0) {
-          const uint32_t dstB = sB + stage * kBStageBytes;
-          if (a.w4d) {
-            if (lane == 8) tma_load_4d(&tmW, full_bar(stage), dstB, 0, kb * kBK, n0 >> 6, t.expert, pol_w);
-          } else if (lane >= 8 && lane < 8 + nbox) {
-            const int j = lane - 8;
-            tma_load_3d(&tmW, full_bar(stage), dstB + j * kBBoxBytes, n0 + j * 64, kb * kBK, t.expert, pol_w);
+      if (a.a_mode == 0) {
+        // Rows past the task's end repeat its last valid token (their results are never stored).
+        const int rr = 32 * p + 4 * (lane & 7);
+        const int r0 = __ldg(idx + min(rr + 0, nvalid - 1));
+        const int r1 = __ldg(idx + min(rr + 1, nvalid - 1));
+        const int r2 = __ldg(idx + min(rr + 2, nvalid - 1));
+        const int r3 = __ldg(idx + min(rr + 3, nvalid - 1));
+        for (int kb = 0; kb < a.num_kb; ++kb, ++g) {
+          const int s = g % kStages;
+          wait_timed<kProf>(empty_bar(s), ((g / kStages) & 1u) ^ 1u, c_wait);
+          if (lane == 0) mbar_arrive_expect_tx(full_bar(s), kABytes / kAWarps);
+          __syncwarp();
+          if (lane < 8) tma_gather4(&tmX, full_bar(s), sA + s * kABytes + rr * 128, kb * kBK, r0, r1, r2, r3, pol_x);
+        }
+      } else {
+        const __nv_bfloat16* src[8];
+        uint32_t rowok = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int r = rsub + 16 * j;
+          const int tok = __ldg(idx + min(r, nvalid - 1));
+          src[j] = a.X + (int64_t)tok * a.H + ch * 8;
+          rowok |= (r < nvalid ? 1u : 0u) << j;
+        }
+        for (int kb = 0; kb < a.num_kb; ++kb, ++g) {
+          const int s = g % kStages;
+          wait_timed<kProf>(empty_bar(s), ((g / kStages) & 1u) ^ 1u, c_wait);
+          const int kcol = kb * kBK;
+          const bool colok = kcol + ch * 8 < a.H;
+          const uint32_t dst = sA + s * kABytes + dst_off;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const bool ok = colok && ((rowok >> j) & 1u);
+            cp_async_16(dst + j * 16 * 128, ok ? src[j] + kcol : a.X, ok ? 16u : 0u);
+          }
+          cp_async_commit();
+          if (g >= (uint32_t)kALag) {
+            cp_async_wait<kALag>();
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(full_bar((g - kALag) % kStages));
           }
         }
-        if (++stage == kStages) {
-          stage = 0;
-          phase ^= 1u;
+      }
+    }
+    if (a.a_mode == 1) {                            // drain the last kALag stages
+      cp_async_wait<0>();
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0)
+        for (uint32_t i = g > (uint32_t)kALag ? g - kALag : 0; i < g; ++i) mbar_arrive(full_bar(i % kStages));
+    }
+    if constexpr (kProf) {
+      if (p == 0 && lane == 0) {
+        a.prof[blockIdx.x * kProfSlots + kProfProdWaitEmpty] = c_wait;
+        a.prof[blockIdx.x * kProfSlots + kProfProdTotal] = clock64() - c_t0;
+      }
+    }
+  } else if (warp == kBWarp) {
+    // ===================== B producer: the expert's W block, one TMA per stage =====================
+    const uint64_t pol_w = policy_evict_normal();
+    uint32_t g = 0;
+    for (int v = blockIdx.x; v < a.total; v += gridDim.x) {
+      int h, task, l;
+      map_tile(s_prefix, s_sigma, a.M_pad, v, h, task, l);
+      const Tile t = load_tile(params, task, l);
+      const int n0 = t.ct * t.bn;
+      const int nbox = (t.bn + 63) >> 6;
+      for (int kb = 0; kb < a.num_kb; ++kb, ++g) {
+        const int s = g % kStages;
+        mbar_wait(empty_bar(s), ((g / kStages) & 1u) ^ 1u);
+        if (lane == 0) {
+          mbar_arrive_expect_tx(full_bar(s), nbox * kBBoxBytes);
+          const uint32_t dstB = sB + s * kBStageBytes;
+          if (a.w4d) {
+            tma_load_4d(&tmW, full_bar(s), dstB, 0, kb * kBK, n0 >> 6, t.expert, pol_w);
+          } else {
+            for (int j = 0; j < nbox; ++j)
+              tma_load_3d(&tmW, full_bar(s), dstB + j * kBBoxBytes, n0 + j * 64, kb * kBK, t.expert, pol_w);
+          }
         }
+        __syncwarp();
       }
     }
   } else if (warp == kMmaWarp) {
@@ -237,16 +333,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
+    long long c_tmem = 0, c_full = 0, c_t0 = kProf ? clock64() : 0;
+    int n_tiles = 0;
     for (int v = blockIdx.x; v < a.total; v += gridDim.x) {
+      ++n_tiles;
       int h, task, l;
       map_tile(s_prefix, s_sigma, a.M_pad, v, h, task, l);
       const int bn = __ldg(params + task * MOE_PLAN_TASK_WORDS + 5);
       const uint32_t idesc = idesc_bf16_f32(kBM, bn, /*A K-major*/ 0, /*B MN-major*/ 1);
-      mbar_wait(tempty_bar(acc), acc_phase ^ 1u);            // epilogue drained this accumulator
+      wait_timed<kProf>(tempty_bar(acc), acc_phase ^ 1u, c_tmem);   // epilogue drained this accumulator
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * kAccCols;
       for (int kb = 0; kb < a.num_kb; ++kb) {
-        mbar_wait(full_bar(stage), phase);                    // TMA bytes landed
+        wait_timed<kProf>(full_bar(stage), phase, c_full);             // TMA bytes landed
         tc_fence_after();
         if (lane == 0) {
           const uint32_t a0 = sA + stage * kABytes;
@@ -275,16 +374,27 @@ __global__ void __launch_bounds__(kThreads, 1)
         acc_phase ^= 1u;
       }
     }
+    if constexpr (kProf) {
+      if (lane == 0) {
+        long long* o = a.prof + blockIdx.x * kProfSlots;
+        o[kProfMmaWaitTmem] = c_tmem;
+        o[kProfMmaWaitFull] = c_full;
+        o[kProfMmaTotal] = clock64() - c_t0;
+        o[kProfTiles] = n_tiles;
+      }
+    }
   } else {
     // ===================== epilogue: TMEM -> registers -> Y =====================
     const int q = warp & 3;                                   // TMEM lane quarter of this warp
     int acc = 0;
     uint32_t acc_phase = 0;
+    long long c_wait = 0, c_work = 0;
     for (int v = blockIdx.x; v < a.total; v += gridDim.x) {
       int h, task, l;
       map_tile(s_prefix, s_sigma, a.M_pad, v, h, task, l);
       const Tile t = load_tile(params, task, l);
-      mbar_wait(tfull_bar(acc), acc_phase);
+      wait_timed<kProf>(tfull_bar(acc), acc_phase, c_wait);
+      const long long w0 = kProf ? clock64() : 0;
       tc_fence_after();
       const int grow = t.rt * kBM + q * 32 + lane;            // row within the task
       const bool valid = grow < t.rows;
@@ -301,9 +411,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(tempty_bar(acc));
+      if constexpr (kProf) c_work += clock64() - w0;
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1u;
+      }
+    }
+    if constexpr (kProf) {
+      if (q == 0 && lane == 0) {
+        a.prof[blockIdx.x * kProfSlots + kProfEpiWaitFull] = c_wait;
+        a.prof[blockIdx.x * kProfSlots + kProfEpiWork] = c_work;
       }
     }
   }
@@ -435,9 +552,7 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 
 }  // namespace
 
-extern "C" {
-
-moe_status moe_device_info(int32_t* sm_count, int32_t* cc_major, int32_t* cc_minor) {
+extern "C" moe_status moe_device_info(int32_t* sm_count, int32_t* cc_major, int32_t* cc_minor) {
   moe::clear_error();
   int dev = 0, maj = 0, min = 0, n = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -452,8 +567,10 @@ moe_status moe_device_info(int32_t* sm_count, int32_t* cc_major, int32_t* cc_min
   return MOE_OK;
 }
 
-moe_status moe_gemm(const moe_plan* plan, const void* X, int64_t T, const int32_t* token_idx, const void* W,
-                    void* Y, int32_t y_dtype, void* stream) {
+namespace {
+
+static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, const int32_t* token_idx,
+                              const void* W, void* Y, int32_t y_dtype, void* stream, long long* prof) {
   moe::clear_error();
   if (!plan) MOE_FAIL(MOE_ERR_INVALID, "moe_gemm: null plan");
   int64_t words = 0;
@@ -486,20 +603,49 @@ moe_status moe_gemm(const moe_plan* plan, const void* X, int64_t T, const int32_
   a.M_pad = v.M_pad;
   a.off_params = (int32_t)v.off_params;
   a.w4d = w4d ? 1 : 0;
+  a.prof = prof;
+  a.T = (int32_t)T;
+  a.H = v.H;
+  a.X = reinterpret_cast<const __nv_bfloat16*>(X);
+  {
+    const char* am = getenv("MOE_A_PATH");       // timing studies: force the A staging path
+    a.a_mode = am ? atoi(am) : kDefaultAMode;
+  }
 
   const size_t smem = kSmemFixed + 8 * (size_t)v.M_pad;
   static std::once_flag attr_once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(attr_once, [] {
-    attr_err = cudaFuncSetAttribute(moe_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    attr_err = cudaFuncSetAttribute(moe_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)(kSmemFixed + 8 * kMaxMPad));
+    if (attr_err == cudaSuccess)
+      attr_err = cudaFuncSetAttribute(moe_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)(kSmemFixed + 8 * kMaxMPad));
   });
   if (attr_err != cudaSuccess) MOE_FAIL(MOE_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(attr_err));
   const int grid = std::min(v.total, sm_count_cached());
-  moe_gemm_kernel<<<grid, kThreads, smem, (cudaStream_t)stream>>>(tmX, tmW, a);
+  if (prof)
+    moe_gemm_kernel<true><<<grid, kThreads, smem, (cudaStream_t)stream>>>(tmX, tmW, a);
+  else
+    moe_gemm_kernel<false><<<grid, kThreads, smem, (cudaStream_t)stream>>>(tmX, tmW, a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) MOE_FAIL(MOE_ERR_CUDA, "moe_gemm launch: %s", cudaGetErrorString(e));
   return MOE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+moe_status moe_gemm(const moe_plan* plan, const void* X, int64_t T, const int32_t* token_idx, const void* W,
+                    void* Y, int32_t y_dtype, void* stream) {
+  return gemm_launch(plan, X, T, token_idx, W, Y, y_dtype, stream, nullptr);
+}
+
+moe_status moe_gemm_profile(const moe_plan* plan, const void* X, int64_t T, const int32_t* token_idx,
+                            const void* W, void* Y, int32_t y_dtype, long long* prof_dev, void* stream) {
+  if (!prof_dev) MOE_FAIL(MOE_ERR_INVALID, "moe_gemm_profile: null prof_dev");
+  return gemm_launch(plan, X, T, token_idx, W, Y, y_dtype, stream, prof_dev);
 }
 
 moe_status moe_decode_debug(const moe_plan* plan, int32_t* out, void* stream) {

@@ -1,0 +1,64 @@
+"""Per-role cycle breakdown of moe_gemm from the instrumented build (moe_gemm_profile).
+
+    python scripts/gemm_breakdown.py [config] [bn]
+Prints one JSON line: fractions of the MMA warp's loop time spent waiting for TMA
+bytes vs for a free TMEM accumulator, producer / epilogue figures, and the
+kernel time of the plain build for comparison."""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import paper_2501_16103_b200 as M  # noqa: E402
+import synth  # noqa: E402
+
+
+def main():
+    name = sys.argv[1] if len(sys.argv) > 1 else "mix"
+    bn = int(sys.argv[2]) if len(sys.argv) > 2 else 256
+    c = synth.CONFIGS[name]
+    ids = torch.from_numpy(synth.route(c, 0)).cuda()
+    X = synth.make_x_torch(0, c.T, c.H, device="cuda")
+    W = synth.make_w_torch(0, c.E, c.H, c.N, device="cuda")
+    counts, row_off, tok, _, _ = M.moe_route(ids, c.E)
+    plan = M.Plan(counts.cpu().numpy(), c.H, c.N, 128, bn)
+    Y = torch.empty((tok.numel(), c.N), dtype=torch.bfloat16, device="cuda")
+    for _ in range(3):
+        M.moe_gemm(plan, X, tok, W, Y=Y)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ev[0].record()
+    for _ in range(10):
+        M.moe_gemm(plan, X, tok, W, Y=Y)
+    ev[1].record()
+    torch.cuda.synchronize()
+    t_plain = ev[0].elapsed_time(ev[1]) / 10
+    Y2 = torch.empty_like(Y)
+    M.moe_gemm_profile(plan, X, tok, W, Y2)
+    ev[0].record()
+    _, prof = M.moe_gemm_profile(plan, X, tok, W, Y2)
+    ev[1].record()
+    torch.cuda.synchronize()
+    t_prof = ev[0].elapsed_time(ev[1])
+    p = prof.double()
+    tot = p[:, 2]
+    out = {
+        "config": name, "bn": bn, "tiles": plan.total_tiles, "ms_plain": t_plain, "ms_instrumented": t_prof,
+        "tflops_plain": c.flops / t_plain / 1e9,
+        "identical_Y": bool(torch.equal(Y, Y2)),
+        "mma_wait_full_frac": float((p[:, 1] / tot).mean()),
+        "mma_wait_tmem_frac": float((p[:, 0] / tot).mean()),
+        "prod_wait_empty_frac": float((p[:, 3] / p[:, 7]).mean()),
+        "epi_work_per_tile_cycles": float((p[:, 5] / p[:, 6]).mean()),
+        "mma_cycles_per_tile": float((tot / p[:, 6]).mean()),
+        "mma_loop_cycles_max": float(tot.max()), "mma_loop_cycles_min": float(tot.min()),
+        "tiles_per_cta_min": int(p[:, 6].min()), "tiles_per_cta_max": int(p[:, 6].max()),
+    }
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()

@@ -210,7 +210,9 @@ def test_gemm_identity_weights_bf16_exact():
     (2000, 3, 1, 64, 8, 16),        # smallest N tile
 ])
 @pytest.mark.parametrize("mode", ["int", "normal"])
-def test_gemm_ragged(T, E, k, H, N, bn, mode):
+@pytest.mark.parametrize("a_path", ["0", "1"])
+def test_gemm_ragged(T, E, k, H, N, bn, mode, a_path, monkeypatch):
+    monkeypatch.setenv("MOE_A_PATH", a_path)          # both A staging paths (gather4 / cp.async)
     ids, X, W, Xd, Wd = _inputs(T, E, k, H, N, T + E, mode)
     Y, counts, row_off, tok, *_ = run_path(ids, Xd, Wd, E, bn=bn)
     rc, rr, rt, rs = omoe.buckets(ids, E)
@@ -257,7 +259,7 @@ def _sample_rows(row_off, counts, rng, per_expert=6):
     return np.array(rows)
 
 
-@pytest.mark.parametrize("cfg,bn", [("mix", 256), ("ds", 128), ("dec16", 256), ("paper_worst", 256)])
+@pytest.mark.parametrize("cfg,bn", [("mix", 256), ("ds", 128), ("ds", 256), ("dec16", 256), ("paper_worst", 256)])
 def test_gemm_full_size_sampled(cfg, bn):
     """BASELINE.json sizes, the launch configuration bench.py times; sampled outputs vs fp64."""
     c = synth.CONFIGS[cfg]
