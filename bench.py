@@ -190,7 +190,7 @@ def run_reference(args, cfg):
 def config_dict(cfg, args):
     return {"workload": f"{cfg.name}: E={cfg.E} top-{cfg.k} T={cfg.T} H={cfg.H} N={cfg.N} "
                         f"routing={cfg.routing} seed={args.seed}",
-            "tile": f"128x{args.bn}", "out_dtype": args.out_dtype, "global_batch": cfg.T,
+            "tile": f"{getattr(args, 'bm_resolved', args.bm) or 'auto'}x{args.bn}", "out_dtype": args.out_dtype, "global_batch": cfg.T,
             "l2": "flushed before every timed step (256 MiB memset); W alone exceeds L2",
             "parallelism": f"ep{args.gpus}" if args.gpus > 1 else "1 GPU"}
 
@@ -228,7 +228,7 @@ def run_ours(args, cfg):
         counts, row_off, tok, slot, _ = M.moe_route(topk_d, cfg.E, with_slot=False)
         counts_h = counts.cpu().numpy()
         if plan is None:
-            plan = M.Plan(counts_h, cfg.H, cfg.N, 128, args.bn)
+            plan = M.Plan(counts_h, cfg.H, cfg.N, args.bm, args.bn)
         else:
             plan.update(counts_h)
         g0 = torch.cuda.Event(enable_timing=True)
@@ -282,7 +282,8 @@ def run_ours(args, cfg):
         def e2e_step():
             Xe.copy_(X_h, non_blocking=True)
             te.copy_(ids_h, non_blocking=True)
-            Y, counts_h, _, _, _, _ = M.moe_forward(te, Xe, Wd, cfg.E, bn=args.bn, out_dtype=out_dtype, plan=plan)
+            Y, counts_h, _, _, _, _ = M.moe_forward(te, Xe, Wd, cfg.E, bm=args.bm, bn=args.bn, out_dtype=out_dtype,
+                                                    plan=plan)
             Y_h.copy_(Y, non_blocking=True)
             return counts_h
 
@@ -310,6 +311,7 @@ def run_ours(args, cfg):
         cpu = {"value": f / s / 1e12, "unit": "TFLOP/s", "cores": cores, "kind": "oracle", "sample": sample,
                "seconds": s}
 
+    args.bm_resolved = plan.bm
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": ws, "steps": args.steps,
@@ -344,6 +346,7 @@ def main():
     ap.add_argument("--config", default="mix")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--bn", type=int, default=256)
+    ap.add_argument("--bm", type=int, default=0, help="tile rows: 128 (1 CTA), 256 (CTA pair), 0 = planner's choice")
     ap.add_argument("--out-dtype", choices=["bf16", "f32"], default="bf16")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -87,8 +87,13 @@ int64_t moe_plan_blob_words(int32_t E);
  * Build the compressed mapping on the host.
  *   counts_host [E]  tokens routed to each expert (m_e >= 0), host memory.
  *   H, N             GEMM K and expert output width; both must be multiples of 8.
- *   bm, bn           tile shape.  bm must be 128 (tcgen05 M=128); bn % 16 == 0,
- *                    16 <= bn <= 256.
+ *   bm, bn           tile shape.  bm = 128: one CTA per tile (tcgen05 M=128, cta_group::1);
+ *                    bm = 256: a CTA pair per tile (tcgen05 M=256, cta_group::2, each
+ *                    CTA 128 rows and half of the W block).  16 <= bn <= 256, bn % 16 == 0
+ *                    (bn % 32 == 0 when bm = 256).  bm = 0: automatic — 256 unless the pair
+ *                    tiles' extra padding rows exceed their ~10% per-row speed advantage
+ *                    (sum of ceil(m_e/256)*256 > 1.10 * sum of ceil(m_e/128)*128).  The
+ *                    blob records the resolved bm.
  *   flags            MOE_PAD_MAX | MOE_PAD_REPEAT.
  *   blob, blob_cap   caller buffer of blob_cap int32 words (see moe_plan_blob_words).
  *   blob_len         out: words written.
@@ -113,7 +118,8 @@ typedef struct moe_plan moe_plan;
 moe_status moe_plan_create(const int32_t* counts_host, int32_t E, int64_t H, int64_t N,
                            int32_t bm, int32_t bn, uint32_t flags, void* stream, moe_plan** out);
 
-/* Re-plan in place for new counts (same E, H, N, bm, bn, flags); reuses the device buffer. */
+/* Re-plan in place for new counts (same E, H, N, bn, flags; the bm resolved at creation is kept);
+ * reuses the device buffer. */
 moe_status moe_plan_update(moe_plan* plan, const int32_t* counts_host, void* stream);
 
 /* Scalars of a plan (any pointer may be NULL). */

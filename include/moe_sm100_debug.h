@@ -26,7 +26,8 @@ moe_status moe_probe_gather4(const void* X_dev, int64_t T, int64_t H, const int3
 /*
  * moe_gemm with per-CTA cycle counters (an instrumented build of the same
  * kernel; clock64() around every mbarrier wait).  prof_dev: device int64 array of
- * grid * 8 words, grid = min(total tiles, SM count); per CTA:
+ * grid * 12 words, grid = CTAs launched (min(total tiles, SMs) for bm=128; 2*min(total, SMs/2)
+ * for bm=256); per CTA:
  *   [0] MMA warp cycles waiting for a free TMEM accumulator (epilogue-bound time)
  *   [1] MMA warp cycles waiting for TMA bytes (load-bound time)
  *   [2] MMA warp cycles in its tile loop
@@ -35,6 +36,9 @@ moe_status moe_probe_gather4(const void* X_dev, int64_t T, int64_t H, const int3
  *   [5] the same warp's cycles draining TMEM and storing Y
  *   [6] tiles processed by the CTA
  *   [7] producer warp 0 cycles in its tile loop
+ *   [8] producer warp 0 cycles in cp.async.wait_group (cp.async A path)
+ *   [9] producer warp 0 cycles fencing and arriving on the full barrier
+ *   [10] B warp cycles waiting for a free stage    [11] B warp cycles in its tile loop
  * Results (Y) are identical to moe_gemm.
  */
 moe_status moe_gemm_profile(const moe_plan* plan, const void* X_dev, int64_t T, const int32_t* token_idx_dev,

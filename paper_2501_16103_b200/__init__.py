@@ -95,7 +95,7 @@ def _i32ptr(a: np.ndarray):
 # ---------------------------------------------------------------------------
 # plan (host, no GPU needed)
 # ---------------------------------------------------------------------------
-def moe_plan_build(counts, H: int, N: int, bm: int = 128, bn: int = 256, flags: int = MOE_PAD_MAX) -> np.ndarray:
+def moe_plan_build(counts, H: int, N: int, bm: int = 0, bn: int = 256, flags: int = MOE_PAD_MAX) -> np.ndarray:
     """The compressed mapping blob (int32 words, layout in include/moe_sm100.h)."""
     c = np.ascontiguousarray(np.asarray(counts, dtype=np.int32))
     E = int(c.shape[0])
@@ -133,13 +133,14 @@ def _stream(stream=None) -> int:
 class Plan:
     """Device-resident plan (moe_plan_create / moe_plan_update / moe_plan_destroy)."""
 
-    def __init__(self, counts, H: int, N: int, bm: int = 128, bn: int = 256, flags: int = MOE_PAD_MAX,
+    def __init__(self, counts, H: int, N: int, bm: int = 0, bn: int = 256, flags: int = MOE_PAD_MAX,
                  stream=None):
         c = np.ascontiguousarray(np.asarray(counts, dtype=np.int32))
-        self.E, self.H, self.N, self.bm, self.bn, self.flags = int(c.shape[0]), H, N, bm, bn, flags
+        self.E, self.H, self.N, self.bn, self.flags = int(c.shape[0]), H, N, bn, flags
         self._h = ctypes.c_void_p()
         self.status = _check(lib().moe_plan_create(_i32ptr(c), self.E, H, N, bm, bn, flags, _stream(stream),
                                                    ctypes.byref(self._h)))
+        self.bm = int(self.blob()[7])            # resolved tile height (bm = 0: automatic)
 
     def update(self, counts, stream=None) -> int:
         c = np.ascontiguousarray(np.asarray(counts, dtype=np.int32))
@@ -223,7 +224,7 @@ def moe_gemm(plan: Plan, X, token_idx, W, Y=None, out_dtype=None, stream=None):
 
 
 PROF_SLOTS = ("mma_wait_tmem", "mma_wait_full", "mma_total", "prod_wait_empty", "epi_wait_full", "epi_work",
-              "tiles", "prod_total")
+              "tiles", "prod_total", "a_cp_wait", "a_arrive", "b_wait_empty", "b_total")
 
 
 def moe_gemm_profile(plan: Plan, X, token_idx, W, Y, stream=None):
@@ -231,7 +232,7 @@ def moe_gemm_profile(plan: Plan, X, token_idx, W, Y, stream=None):
     import torch
 
     n_sm = moe_device_info()[0]
-    grid = min(plan.total_tiles, n_sm)
+    grid = min(plan.total_tiles, n_sm) if plan.bm == 128 else 2 * min(plan.total_tiles, n_sm // 2)
     prof = torch.zeros((max(grid, 1), len(PROF_SLOTS)), dtype=torch.int64, device=X.device)
     yd = MOE_DTYPE_F32 if Y.dtype == torch.float32 else MOE_DTYPE_BF16
     _check(lib().moe_gemm_profile(plan.handle, X.data_ptr(), X.shape[0], token_idx.data_ptr(), W.data_ptr(),
@@ -257,7 +258,7 @@ def moe_probe_gather4(X, rows, col0: int, stream=None):
     return out
 
 
-def moe_forward(topk_ids, X, W, E: int, bm: int = 128, bn: int = 256, out_dtype=None, plan: Plan | None = None,
+def moe_forward(topk_ids, X, W, E: int, bm: int = 0, bn: int = 256, out_dtype=None, plan: Plan | None = None,
                 stream=None):
     """One MoE expert-GEMM step on device: route -> counts D2H -> host plan -> single-launch GEMM.
 

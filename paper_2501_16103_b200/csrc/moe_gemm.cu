@@ -45,7 +45,6 @@ using namespace moe::ptx;
 
 constexpr int kBM = 128;                        // tile rows = tcgen05 M
 constexpr int kBK = 64;                         // K block: 64 bf16 = one 128-byte swizzle row
-constexpr int kStages = 4;
 constexpr int kABytes = kBM * kBK * 2;          // 16 KB: 128 gathered rows x 64
 constexpr int kBBoxBytes = 64 * kBK * 2;        // 8 KB: one TMA box of W (64 N x 64 K)
 constexpr int kBStageBytes = 4 * kBBoxBytes;    // up to BN = 256
@@ -54,13 +53,11 @@ constexpr int kBWarp = kAWarps;                 // B producer (W block, TMA): wa
 constexpr int kMmaWarp = kAWarps + 1;           // tcgen05 issuer: warp 5
 constexpr int kEpiWarps = 4;                    // epilogue: warps 6-9 (TMEM lane quarters 2,3,0,1)
 constexpr int kThreads = 32 * (kAWarps + 2 + kEpiWarps);
-constexpr int kALag = 2;
-constexpr int kDefaultAMode = 1;                        // cp.async path: stages in flight before a thread signals
+constexpr int kDefaultAMode = 1;                // A staging: cp.async (see the A-producer comment)
 constexpr uint32_t kTmemCols = 512;             // 2 accumulators x 256 fp32 columns
 constexpr uint32_t kAccCols = 256;
 constexpr int kMaxMPad = 1024;
-constexpr int kBarBytes = 128;
-constexpr size_t kSmemFixed = 1024 /*align slack*/ + (size_t)kStages * (kABytes + kBStageBytes) + kBarBytes;
+constexpr int kBarBytes = 256;                  // 8 B per mbarrier (<= 2*6+4) + TMEM address slot
 
 struct GemmArgs {
   const int32_t* plan;       // device plan blob
@@ -90,6 +87,10 @@ enum ProfSlot {
   kProfEpiWork,           // epilogue warp (quarter 0): cycles draining + storing
   kProfTiles,             // tiles processed by the CTA
   kProfProdTotal,         // producer warp 0: cycles in its tile loop
+  kProfACpWait,           // producer warp 0: cycles in cp.async.wait_group
+  kProfAArrive,           // producer warp 0: cycles fencing + arriving
+  kProfBWaitEmpty,        // B warp: cycles waiting for a free stage
+  kProfBTotal,            // B warp: cycles in its tile loop
   kProfSlots
 };
 
@@ -175,38 +176,61 @@ __device__ __forceinline__ void wait_timed(uint32_t bar, uint32_t parity, long l
   }
 }
 
-template <bool kProf>
+// Pipeline geometry per CTA-group size: a CTA pair (cta_group::2) splits the B block across the
+// two CTAs, so a stage is 32 KB instead of 48 KB and six stages fit.
+template <int kCta>
+struct Geo {
+  static constexpr int kStages = kCta == 2 ? 6 : 4;
+  static_assert(8 * (2 * kStages + 4) + 4 <= kBarBytes, "barrier block overlaps TilePrefix");
+  static constexpr int kBStage = kBStageBytes / kCta;            // bytes of W per CTA per stage
+  static constexpr size_t kSmem = 1024 + (size_t)kStages * (kABytes + kBStage) + kBarBytes;
+};
+
+template <bool kProf, int kCta>
 __global__ void __launch_bounds__(kThreads, 1)
     moe_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
                     const GemmArgs a) {
+  constexpr int kSt = Geo<kCta>::kStages;
+  constexpr int kBSt = Geo<kCta>::kBStage;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;            // SW128 atoms need 1024-byte alignment
   uint8_t* smem = smem_raw + (base - raw);
   const uint32_t sA = base;
-  const uint32_t sB = sA + kStages * kABytes;
-  const uint32_t sBar = sB + kStages * kBStageBytes;
+  const uint32_t sB = sA + kSt * kABytes;
+  const uint32_t sBar = sB + kSt * kBSt;
   auto full_bar = [&](int s) { return sBar + 8u * s; };
-  auto empty_bar = [&](int s) { return sBar + 8u * (kStages + s); };
-  auto tfull_bar = [&](int i) { return sBar + 8u * (2 * kStages + i); };
-  auto tempty_bar = [&](int i) { return sBar + 8u * (2 * kStages + 2 + i); };
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + (sBar - base) + 8 * (2 * kStages + 4));
+  auto empty_bar = [&](int s) { return sBar + 8u * (kSt + s); };
+  auto tfull_bar = [&](int i) { return sBar + 8u * (2 * kSt + i); };
+  auto tempty_bar = [&](int i) { return sBar + 8u * (2 * kSt + 2 + i); };
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + (sBar - base) + 8 * (2 * kSt + 4));
   int32_t* s_prefix = reinterpret_cast<int32_t*>(smem + (sBar - base) + kBarBytes);
   int32_t* s_sigma = s_prefix + a.M_pad;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  // CTA pair: rank 0 (leader) issues the MMAs for both CTAs; all consumers of the
+  // data path (full / tmem-empty barriers) live in the leader.
+  const uint32_t rank = kCta == 2 ? cluster_ctarank() : 0;
+  const int pair_id = blockIdx.x / kCta;
+  const int n_pairs = gridDim.x / kCta;
+  auto leader = [&](uint32_t addr) { return kCta == 2 ? mapa_shared(addr, 0) : addr; };
 
   // TilePrefix and sigma are adjacent in the blob: one copy into shared memory.
   for (int i = threadIdx.x; i < 2 * a.M_pad; i += blockDim.x) s_prefix[i] = a.plan[MOE_PLAN_HEADER + i];
+  const int a_mode = kCta == 2 ? 1 : a.a_mode;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(full_bar(s), kAWarps + 1);        // one arrival per A warp + the B warp
+    // full[s] arrivals: A stage done (gather4: one expect_tx per A warp; cp.async: one asynchronous
+    // arrive per A thread), the B warp's expect_tx (leader), and in a pair the peer's relay (leader).
+    const uint32_t a_arrivals = a_mode == 0 ? kAWarps : 32 * kAWarps;
+    const uint32_t full_count = a_arrivals + (rank == 0 ? 1u + (kCta == 2 ? 1u : 0u) : 0u);
+    for (int s = 0; s < kSt; ++s) {
+      mbar_init(full_bar(s), full_count);
       mbar_init(empty_bar(s), 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(tfull_bar(i), 1);
-      mbar_init(tempty_bar(i), kEpiWarps);
+      mbar_init(tempty_bar(i), kCta * kEpiWarps);
     }
     fence_mbar_init();
   }
@@ -214,45 +238,47 @@ __global__ void __launch_bounds__(kThreads, 1)
     prefetch_tmap(&tmX);
     prefetch_tmap(&tmW);
   }
-  if (warp == kMmaWarp) tmem_alloc<kTmemCols>(smem_u32(tmem_holder));
+  if (warp == kMmaWarp) tmem_alloc<kTmemCols, kCta>(smem_u32(tmem_holder));
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kCta == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
   const int32_t* params = a.plan + a.off_params;
+  constexpr int kPairRows = kBM * kCta;                     // rows of a virtual tile
 
   if (warp < kAWarps) {
-    // ===================== A producers: the tile's 128 token rows, 64 columns per stage =====================
+    // ===================== A producers: this CTA's 128 token rows, 64 columns per stage =====================
     // Gathered straight from X through the token-index array: no gathered copy of X.
-    // a_mode 0: TMA tile::gather4 — warp p stages rows [32p, 32p+32), lanes 0..7 four rows each.
+    // a_mode 0 (1-CTA only): TMA tile::gather4 — warp p stages rows [32p, 32p+32), 4 rows per lane.
     // a_mode 1: cp.async 16 B per thread, 8 threads per 128-byte row (coalesced), SW128 swizzle
     //           applied by hand; rows past the task's end (and columns past H) are zero-filled
-    //           without a read.  Completion: each thread waits for its copies kALag stages later,
-    //           fences them into the async proxy (tcgen05 reads smem through it) and the warp arrives.
+    //           without a read.  Completion: cp.async.mbarrier.arrive — the hardware arrives on
+    //           this CTA's full barrier when the thread's copies land; the thread never blocks.
+    //           In a CTA pair the peer's MMA warp relays its completed stages to the leader.
     const uint64_t pol_x = policy_evict_last();    // X_e is re-read by every column tile of the task
     const int p = warp;
     uint32_t g = 0;                                 // stages issued by this warp, over all tiles
-    long long c_wait = 0, c_t0 = kProf ? clock64() : 0;
+    long long c_wait = 0, c_t0 = kProf ? clock64() : 0, c_cpw = 0, c_arr = 0;
     const int ch = threadIdx.x & 7;                 // cp.async: 16-byte chunk of the 128-byte row
     const int rsub = threadIdx.x >> 3;              // cp.async: row within a 16-row group
     const uint32_t dst_off = rsub * 128 + ((ch ^ (rsub & 7)) << 4);
-    for (int v = blockIdx.x; v < a.total; v += gridDim.x) {
+    for (int v = pair_id; v < a.total; v += n_pairs) {
       int h, task, l;
       map_tile(s_prefix, s_sigma, a.M_pad, v, h, task, l);
       const Tile t = load_tile(params, task, l);
-      const int rbeg = t.rt * kBM;
-      const int nvalid = min(kBM, t.rows - rbeg);
-      const int32_t* idx = a.token_idx + t.row0 + rbeg;
-      if (a.a_mode == 0) {
+      const int rbeg = t.rt * kPairRows + (int)rank * kBM;
+      const int nvalid = min(kBM, t.rows - rbeg);   // may be <= 0 for the second CTA of a pair tile
+      const int32_t* idx = a.token_idx + t.row0;
+      if (a_mode == 0) {
         // Rows past the task's end repeat its last valid token (their results are never stored).
         const int rr = 32 * p + 4 * (lane & 7);
-        const int r0 = __ldg(idx + min(rr + 0, nvalid - 1));
-        const int r1 = __ldg(idx + min(rr + 1, nvalid - 1));
-        const int r2 = __ldg(idx + min(rr + 2, nvalid - 1));
-        const int r3 = __ldg(idx + min(rr + 3, nvalid - 1));
+        const int r0 = __ldg(idx + rbeg + min(rr + 0, nvalid - 1));
+        const int r1 = __ldg(idx + rbeg + min(rr + 1, nvalid - 1));
+        const int r2 = __ldg(idx + rbeg + min(rr + 2, nvalid - 1));
+        const int r3 = __ldg(idx + rbeg + min(rr + 3, nvalid - 1));
         for (int kb = 0; kb < a.num_kb; ++kb, ++g) {
-          const int s = g % kStages;
-          wait_timed<kProf>(empty_bar(s), ((g / kStages) & 1u) ^ 1u, c_wait);
+          const int s = g % kSt;
+          wait_timed<kProf>(empty_bar(s), ((g / kSt) & 1u) ^ 1u, c_wait);
           if (lane == 0) mbar_arrive_expect_tx(full_bar(s), kABytes / kAWarps);
           __syncwarp();
           if (lane < 8) tma_gather4(&tmX, full_bar(s), sA + s * kABytes + rr * 128, kb * kBK, r0, r1, r2, r3, pol_x);
@@ -263,13 +289,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const int r = rsub + 16 * j;
-          const int tok = __ldg(idx + min(r, nvalid - 1));
+          const int tok = r < nvalid ? __ldg(idx + rbeg + r) : 0;
           src[j] = a.X + (int64_t)tok * a.H + ch * 8;
           rowok |= (r < nvalid ? 1u : 0u) << j;
         }
         for (int kb = 0; kb < a.num_kb; ++kb, ++g) {
-          const int s = g % kStages;
-          wait_timed<kProf>(empty_bar(s), ((g / kStages) & 1u) ^ 1u, c_wait);
+          const int s = g % kSt;
+          wait_timed<kProf>(empty_bar(s), ((g / kSt) & 1u) ^ 1u, c_wait);
           const int kcol = kb * kBK;
           const bool colok = kcol + ch * 8 < a.H;
           const uint32_t dst = sA + s * kABytes + dst_off;
@@ -278,110 +304,132 @@ __global__ void __launch_bounds__(kThreads, 1)
             const bool ok = colok && ((rowok >> j) & 1u);
             cp_async_16(dst + j * 16 * 128, ok ? src[j] + kcol : a.X, ok ? 16u : 0u);
           }
-          cp_async_commit();
-          if (g >= (uint32_t)kALag) {
-            cp_async_wait<kALag>();
-            fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(full_bar((g - kALag) % kStages));
-          }
+          cp_async_mbar_arrive_noinc(full_bar(s));
         }
       }
-    }
-    if (a.a_mode == 1) {                            // drain the last kALag stages
-      cp_async_wait<0>();
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0)
-        for (uint32_t i = g > (uint32_t)kALag ? g - kALag : 0; i < g; ++i) mbar_arrive(full_bar(i % kStages));
     }
     if constexpr (kProf) {
       if (p == 0 && lane == 0) {
         a.prof[blockIdx.x * kProfSlots + kProfProdWaitEmpty] = c_wait;
         a.prof[blockIdx.x * kProfSlots + kProfProdTotal] = clock64() - c_t0;
+        a.prof[blockIdx.x * kProfSlots + kProfACpWait] = c_cpw;
+        a.prof[blockIdx.x * kProfSlots + kProfAArrive] = c_arr;
       }
     }
   } else if (warp == kBWarp) {
-    // ===================== B producer: the expert's W block, one TMA per stage =====================
+    // ===================== B producer: this CTA's share of the W block, one TMA per stage =====================
     const uint64_t pol_w = policy_evict_normal();
     uint32_t g = 0;
-    for (int v = blockIdx.x; v < a.total; v += gridDim.x) {
+    long long c_wait = 0, c_t0 = kProf ? clock64() : 0;
+    for (int v = pair_id; v < a.total; v += n_pairs) {
       int h, task, l;
       map_tile(s_prefix, s_sigma, a.M_pad, v, h, task, l);
       const Tile t = load_tile(params, task, l);
-      const int n0 = t.ct * t.bn;
-      const int nbox = (t.bn + 63) >> 6;
+      const int bnc = t.bn / kCta;                  // columns of the block staged by this CTA
+      const int n0 = t.ct * t.bn + (int)rank * bnc;
+      const int nbox = (bnc + 63) >> 6;
       for (int kb = 0; kb < a.num_kb; ++kb, ++g) {
-        const int s = g % kStages;
-        mbar_wait(empty_bar(s), ((g / kStages) & 1u) ^ 1u);
+        const int s = g % kSt;
+        wait_timed<kProf>(empty_bar(s), ((g / kSt) & 1u) ^ 1u, c_wait);
         if (lane == 0) {
-          mbar_arrive_expect_tx(full_bar(s), nbox * kBBoxBytes);
-          const uint32_t dstB = sB + s * kBStageBytes;
-          if (a.w4d) {
-            tma_load_4d(&tmW, full_bar(s), dstB, 0, kb * kBK, n0 >> 6, t.expert, pol_w);
+          const uint32_t dstB = sB + s * kBSt;
+          if constexpr (kCta == 2) {
+            const uint32_t fb = leader(full_bar(s));
+            if (rank == 0) mbar_arrive_expect_tx(full_bar(s), kCta * nbox * kBBoxBytes);
+            if (a.w4d) {
+              tma_load_4d_pair(&tmW, fb, dstB, 0, kb * kBK, n0 >> 6, t.expert, pol_w);
+            } else {
+              for (int j = 0; j < nbox; ++j)
+                tma_load_3d_pair(&tmW, fb, dstB + j * kBBoxBytes, n0 + j * 64, kb * kBK, t.expert, pol_w);
+            }
           } else {
-            for (int j = 0; j < nbox; ++j)
-              tma_load_3d(&tmW, full_bar(s), dstB + j * kBBoxBytes, n0 + j * 64, kb * kBK, t.expert, pol_w);
+            mbar_arrive_expect_tx(full_bar(s), nbox * kBBoxBytes);
+            if (a.w4d) {
+              tma_load_4d(&tmW, full_bar(s), dstB, 0, kb * kBK, n0 >> 6, t.expert, pol_w);
+            } else {
+              for (int j = 0; j < nbox; ++j)
+                tma_load_3d(&tmW, full_bar(s), dstB + j * kBBoxBytes, n0 + j * 64, kb * kBK, t.expert, pol_w);
+            }
           }
         }
         __syncwarp();
-      }
-    }
-  } else if (warp == kMmaWarp) {
-    // ===================== MMA issuer: one thread drives tcgen05 =====================
-    int stage = 0;
-    uint32_t phase = 0;
-    int acc = 0;
-    uint32_t acc_phase = 0;
-    long long c_tmem = 0, c_full = 0, c_t0 = kProf ? clock64() : 0;
-    int n_tiles = 0;
-    for (int v = blockIdx.x; v < a.total; v += gridDim.x) {
-      ++n_tiles;
-      int h, task, l;
-      map_tile(s_prefix, s_sigma, a.M_pad, v, h, task, l);
-      const int bn = __ldg(params + task * MOE_PLAN_TASK_WORDS + 5);
-      const uint32_t idesc = idesc_bf16_f32(kBM, bn, /*A K-major*/ 0, /*B MN-major*/ 1);
-      wait_timed<kProf>(tempty_bar(acc), acc_phase ^ 1u, c_tmem);   // epilogue drained this accumulator
-      tc_fence_after();
-      const uint32_t d_tmem = tmem_base + acc * kAccCols;
-      for (int kb = 0; kb < a.num_kb; ++kb) {
-        wait_timed<kProf>(full_bar(stage), phase, c_full);             // TMA bytes landed
-        tc_fence_after();
-        if (lane == 0) {
-          const uint32_t a0 = sA + stage * kABytes;
-          const uint32_t b0 = sB + stage * kBStageBytes;
-#pragma unroll
-          for (int kk = 0; kk < kBK / 16; ++kk) {
-            // A: K-major SW128, 8-row groups 1024 B apart; K step of 16 = +32 B in the row.
-            const uint64_t ad = smem_desc_sw128(a0 + kk * 32, 16, 1024);
-            // B: MN-major SW128; 64-wide N chunks 8 KB apart (LBO), 8-row K groups 1 KB apart
-            // (SBO); K step of 16 rows = +2 KB.
-            const uint64_t bd = smem_desc_sw128(b0 + kk * 2048, kBBoxBytes, 1024);
-            mma_bf16(d_tmem, ad, bd, idesc, (kb | kk) != 0);
-          }
-          mma_commit(empty_bar(stage));                       // frees the smem slot when done
-        }
-        __syncwarp();
-        if (++stage == kStages) {
-          stage = 0;
-          phase ^= 1u;
-        }
-      }
-      if (lane == 0) mma_commit(tfull_bar(acc));              // accumulator ready
-      __syncwarp();
-      if (++acc == 2) {
-        acc = 0;
-        acc_phase ^= 1u;
       }
     }
     if constexpr (kProf) {
       if (lane == 0) {
-        long long* o = a.prof + blockIdx.x * kProfSlots;
-        o[kProfMmaWaitTmem] = c_tmem;
-        o[kProfMmaWaitFull] = c_full;
-        o[kProfMmaTotal] = clock64() - c_t0;
-        o[kProfTiles] = n_tiles;
+        a.prof[blockIdx.x * kProfSlots + kProfBWaitEmpty] = c_wait;
+        a.prof[blockIdx.x * kProfSlots + kProfBTotal] = clock64() - c_t0;
       }
+    }
+  } else if (warp == kMmaWarp) {
+    // ===================== MMA issuer (pair leader): one thread drives tcgen05 =====================
+    if (rank == 0) {
+      uint32_t g = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      long long c_tmem = 0, c_full = 0, c_t0 = kProf ? clock64() : 0;
+      int n_tiles = 0;
+      for (int v = pair_id; v < a.total; v += n_pairs) {
+        ++n_tiles;
+        int h, task, l;
+        map_tile(s_prefix, s_sigma, a.M_pad, v, h, task, l);
+        const int bn = __ldg(params + task * MOE_PLAN_TASK_WORDS + 5);
+        const uint32_t idesc = idesc_bf16_f32(kPairRows, bn, /*A K-major*/ 0, /*B MN-major*/ 1);
+        wait_timed<kProf>(tempty_bar(acc), acc_phase ^ 1u, c_tmem);     // epilogue(s) drained this accumulator
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * kAccCols;
+        for (int kb = 0; kb < a.num_kb; ++kb, ++g) {
+          const int s = g % kSt;
+          const uint32_t par = (g / kSt) & 1u;
+          wait_timed<kProf>(full_bar(s), par, c_full);                   // both CTAs' bytes landed
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t a0 = sA + s * kABytes;
+            const uint32_t b0 = sB + s * kBSt;
+#pragma unroll
+            for (int kk = 0; kk < kBK / 16; ++kk) {
+              // A: K-major SW128, 8-row groups 1024 B apart; K step of 16 = +32 B in the row.
+              const uint64_t ad = smem_desc_sw128(a0 + kk * 32, 16, 1024);
+              // B: MN-major SW128; 64-wide N chunks 8 KB apart (LBO), 8-row K groups 1 KB apart
+              // (SBO); K step of 16 rows = +2 KB.
+              const uint64_t bd = smem_desc_sw128(b0 + kk * 2048, kBBoxBytes, 1024);
+              if constexpr (kCta == 2) mma_bf16_pair(d_tmem, ad, bd, idesc, (kb | kk) != 0);
+              else mma_bf16(d_tmem, ad, bd, idesc, (kb | kk) != 0);
+            }
+            if constexpr (kCta == 2) mma_commit_pair(empty_bar(s), 0x3);  // frees the slot in both CTAs
+            else mma_commit(empty_bar(s));
+          }
+          __syncwarp();
+        }
+        if (lane == 0) {
+          if constexpr (kCta == 2) mma_commit_pair(tfull_bar(acc), 0x3);  // accumulator ready in both CTAs
+          else mma_commit(tfull_bar(acc));
+        }
+        __syncwarp();
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1u;
+        }
+      }
+      if constexpr (kProf) {
+        if (lane == 0) {
+          long long* o = a.prof + blockIdx.x * kProfSlots;
+          o[kProfMmaWaitTmem] = c_tmem;
+          o[kProfMmaWaitFull] = c_full;
+          o[kProfMmaTotal] = clock64() - c_t0;
+          o[kProfTiles] = n_tiles;
+        }
+      }
+    } else if (lane == 0) {
+      // Pair peer: relay "my A stage landed" (local full barrier, fed by cp.async arrivals) to the
+      // leader's full barrier, where the MMA issuer waits for both CTAs' bytes.
+      uint32_t g = 0;
+      for (int v = pair_id; v < a.total; v += n_pairs)
+        for (int kb = 0; kb < a.num_kb; ++kb, ++g) {
+          const int s = g % kSt;
+          mbar_wait(full_bar(s), (g / kSt) & 1u);
+          mbar_arrive_cluster(leader(full_bar(s)));
+        }
     }
   } else {
     // ===================== epilogue: TMEM -> registers -> Y =====================
@@ -389,14 +437,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     long long c_wait = 0, c_work = 0;
-    for (int v = blockIdx.x; v < a.total; v += gridDim.x) {
+    for (int v = pair_id; v < a.total; v += n_pairs) {
       int h, task, l;
       map_tile(s_prefix, s_sigma, a.M_pad, v, h, task, l);
       const Tile t = load_tile(params, task, l);
       wait_timed<kProf>(tfull_bar(acc), acc_phase, c_wait);
       const long long w0 = kProf ? clock64() : 0;
       tc_fence_after();
-      const int grow = t.rt * kBM + q * 32 + lane;            // row within the task
+      const int grow = t.rt * kPairRows + (int)rank * kBM + q * 32 + lane;   // row within the task
       const bool valid = grow < t.rows;
       const int64_t yrow = (int64_t)t.row0 + grow;
       const int n0 = t.ct * t.bn;
@@ -410,7 +458,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(tempty_bar(acc));
+      if (lane == 0) {
+        if constexpr (kCta == 2) mbar_arrive_cluster(leader(tempty_bar(acc)));
+        else mbar_arrive(tempty_bar(acc));
+      }
       if constexpr (kProf) c_work += clock64() - w0;
       if (++acc == 2) {
         acc = 0;
@@ -426,10 +477,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kCta == 2) cluster_sync(); else __syncthreads();
   if (warp == kMmaWarp) {
     tc_fence_after();
-    tmem_dealloc<kTmemCols>(tmem_base);
+    tmem_dealloc<kTmemCols, kCta>(tmem_base);
   }
 }
 
@@ -510,7 +561,8 @@ moe_status make_x_map(CUtensorMap* m, const void* X, int64_t T, int64_t H) {
   return MOE_OK;
 }
 
-moe_status make_w_map(CUtensorMap* m, const void* W, int64_t E, int64_t H, int64_t N, int bn, bool w4d) {
+// bn_cta: W columns one CTA stages per K block (the 4-D box spans ceil(bn_cta / 64) chunks).
+moe_status make_w_map(CUtensorMap* m, const void* W, int64_t E, int64_t H, int64_t N, int bn_cta, bool w4d) {
   auto fn = encode_fn();
   if (!fn) MOE_FAIL(MOE_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
   CUresult r;
@@ -519,7 +571,7 @@ moe_status make_w_map(CUtensorMap* m, const void* W, int64_t E, int64_t H, int64
     // laid out chunk-major, then k, then n — the MN-major SW128 canonical layout.
     const cuuint64_t dims[4] = {64, (cuuint64_t)H, (cuuint64_t)(N / 64), (cuuint64_t)E};
     const cuuint64_t strides[3] = {(cuuint64_t)N * 2, 128, (cuuint64_t)H * N * 2};
-    const cuuint32_t box[4] = {64, (cuuint32_t)kBK, (cuuint32_t)((bn + 63) / 64), 1};
+    const cuuint32_t box[4] = {64, (cuuint32_t)kBK, (cuuint32_t)((bn_cta + 63) / 64), 1};
     const cuuint32_t estr[4] = {1, 1, 1, 1};
     r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(W), dims, strides, box, estr,
            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -569,6 +621,22 @@ extern "C" moe_status moe_device_info(int32_t* sm_count, int32_t* cc_major, int3
 
 namespace {
 
+cudaError_t set_smem_attrs() {
+  static std::once_flag once;
+  static cudaError_t err = cudaSuccess;
+  std::call_once(once, [] {
+    const int s1 = (int)(Geo<1>::kSmem + 8 * kMaxMPad), s2 = (int)(Geo<2>::kSmem + 8 * kMaxMPad);
+    cudaError_t e[4] = {
+        cudaFuncSetAttribute(moe_gemm_kernel<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, s1),
+        cudaFuncSetAttribute(moe_gemm_kernel<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, s1),
+        cudaFuncSetAttribute(moe_gemm_kernel<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, s2),
+        cudaFuncSetAttribute(moe_gemm_kernel<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, s2)};
+    for (cudaError_t x : e)
+      if (x != cudaSuccess && err == cudaSuccess) err = x;
+  });
+  return err;
+}
+
 static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, const int32_t* token_idx,
                               const void* W, void* Y, int32_t y_dtype, void* stream, long long* prof) {
   moe::clear_error();
@@ -589,7 +657,8 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
   moe_status st = make_x_map(&tmX, X, T, v.H);
   if (st != MOE_OK) return st;
   const bool w4d = (v.N % 64) == 0;
-  st = make_w_map(&tmW, W, v.E, v.H, v.N, v.bn, w4d);
+  const int cta = v.bm / kBM;                    // CTAs per tile: each stages bn / cta W columns
+  st = make_w_map(&tmW, W, v.E, v.H, v.N, v.bn / cta, w4d);
   if (st != MOE_OK) return st;
 
   GemmArgs a;
@@ -612,22 +681,35 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
     a.a_mode = am ? atoi(am) : kDefaultAMode;
   }
 
-  const size_t smem = kSmemFixed + 8 * (size_t)v.M_pad;
-  static std::once_flag attr_once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(attr_once, [] {
-    attr_err = cudaFuncSetAttribute(moe_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)(kSmemFixed + 8 * kMaxMPad));
-    if (attr_err == cudaSuccess)
-      attr_err = cudaFuncSetAttribute(moe_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)(kSmemFixed + 8 * kMaxMPad));
-  });
+  if (v.bm == 256 && (v.bn / 2) % 16) MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_gemm: pair tiles need bn %% 32 == 0");
+  cudaError_t attr_err = set_smem_attrs();
   if (attr_err != cudaSuccess) MOE_FAIL(MOE_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(attr_err));
-  const int grid = std::min(v.total, sm_count_cached());
-  if (prof)
-    moe_gemm_kernel<true><<<grid, kThreads, smem, (cudaStream_t)stream>>>(tmX, tmW, a);
-  else
-    moe_gemm_kernel<false><<<grid, kThreads, smem, (cudaStream_t)stream>>>(tmX, tmW, a);
+  if (v.bm == 256) {
+    const int pairs = std::min(v.total, sm_count_cached() / 2);
+    const size_t smem = Geo<2>::kSmem + 8 * (size_t)v.M_pad;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * pairs);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = (cudaStream_t)stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t le = prof ? cudaLaunchKernelEx(&cfg, moe_gemm_kernel<true, 2>, tmX, tmW, a)
+                          : cudaLaunchKernelEx(&cfg, moe_gemm_kernel<false, 2>, tmX, tmW, a);
+    if (le != cudaSuccess) MOE_FAIL(MOE_ERR_CUDA, "moe_gemm pair launch: %s", cudaGetErrorString(le));
+  } else {
+    const int grid = std::min(v.total, sm_count_cached());
+    const size_t smem = Geo<1>::kSmem + 8 * (size_t)v.M_pad;
+    if (prof)
+      moe_gemm_kernel<true, 1><<<grid, kThreads, smem, (cudaStream_t)stream>>>(tmX, tmW, a);
+    else
+      moe_gemm_kernel<false, 1><<<grid, kThreads, smem, (cudaStream_t)stream>>>(tmX, tmW, a);
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) MOE_FAIL(MOE_ERR_CUDA, "moe_gemm launch: %s", cudaGetErrorString(e));
   return MOE_OK;

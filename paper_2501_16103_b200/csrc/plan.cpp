@@ -75,9 +75,22 @@ moe_status moe_plan_build(const int32_t* counts, int32_t E, int64_t H, int64_t N
     MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_plan_build: H=%lld and N=%lld must be multiples of 8 (16-byte TMA strides)",
              (long long)H, (long long)N);
   if (H >= INT_MAX || N >= INT_MAX) MOE_FAIL(MOE_ERR_CAPACITY, "moe_plan_build: H or N >= 2^31");
-  if (bm != 128) MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_plan_build: bm=%d unsupported (tcgen05 M=128 tiles)", bm);
-  if (bn < 16 || bn > 256 || bn % 16)
-    MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_plan_build: bn=%d must be a multiple of 16 in [16, 256]", bn);
+  if (bm == 0) {
+    // Auto: executed rows under each tile height, with CTA-pair tiles credited for their measured
+    // per-row advantage (half the W traffic per SM, 6-stage ring: ~1.10x, DESIGN.md §Tile choice).
+    int64_t r128 = 0, r256 = 0;
+    for (int32_t e = 0; e < E; ++e) {
+      const int64_t m = counts[e] < 0 ? 0 : counts[e];
+      r128 += ceil_div(m, 128) * 128;
+      r256 += ceil_div(m, 256) * 256;
+    }
+    bm = (r256 * 100 <= r128 * 110 && bn % 32 == 0) ? 256 : 128;
+  }
+  if (bm != 128 && bm != 256)
+    MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_plan_build: bm=%d unsupported (128: one CTA, 256: CTA pair, 0: auto)", bm);
+  if (bn < 16 || bn > 256 || bn % (bm == 256 ? 32 : 16))
+    MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_plan_build: bn=%d must be a multiple of %d in [16, 256]", bn,
+             bm == 256 ? 32 : 16);
   if (flags & ~MOE_PAD_REPEAT) MOE_FAIL(MOE_ERR_INVALID, "moe_plan_build: unknown flags 0x%x", flags);
 
   // CSR row offsets: exclusive prefix of counts in expert-id order.
@@ -205,6 +218,7 @@ moe_status moe_plan_create(const int32_t* counts, int32_t E, int64_t H, int64_t 
     delete p;
     return st;
   }
+  bm = p->blob[7];                              // resolved tile height (bm = 0 means auto)
   p->stream = (cudaStream_t)stream;
   p->E = E;
   p->H = H;

@@ -20,12 +20,13 @@ import synth  # noqa: E402
 def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "mix"
     bn = int(sys.argv[2]) if len(sys.argv) > 2 else 256
+    bm = int(sys.argv[3]) if len(sys.argv) > 3 else 128
     c = synth.CONFIGS[name]
     ids = torch.from_numpy(synth.route(c, 0)).cuda()
     X = synth.make_x_torch(0, c.T, c.H, device="cuda")
     W = synth.make_w_torch(0, c.E, c.H, c.N, device="cuda")
     counts, row_off, tok, _, _ = M.moe_route(ids, c.E)
-    plan = M.Plan(counts.cpu().numpy(), c.H, c.N, 128, bn)
+    plan = M.Plan(counts.cpu().numpy(), c.H, c.N, bm, bn)
     Y = torch.empty((tok.numel(), c.N), dtype=torch.bfloat16, device="cuda")
     for _ in range(3):
         M.moe_gemm(plan, X, tok, W, Y=Y)
@@ -43,10 +44,11 @@ def main():
     ev[1].record()
     torch.cuda.synchronize()
     t_prof = ev[0].elapsed_time(ev[1])
-    p = prof.double()
+    pall = prof.double()
+    p = pall[0::2] if bm == 256 else pall           # MMA counters live in the pair leaders
     tot = p[:, 2]
     out = {
-        "config": name, "bn": bn, "tiles": plan.total_tiles, "ms_plain": t_plain, "ms_instrumented": t_prof,
+        "config": name, "bn": bn, "bm": bm, "tiles": plan.total_tiles, "ms_plain": t_plain, "ms_instrumented": t_prof,
         "tflops_plain": c.flops / t_plain / 1e9,
         "identical_Y": bool(torch.equal(Y, Y2)),
         "mma_wait_full_frac": float((p[:, 1] / tot).mean()),
@@ -56,7 +58,15 @@ def main():
         "mma_cycles_per_tile": float((tot / p[:, 6]).mean()),
         "mma_loop_cycles_max": float(tot.max()), "mma_loop_cycles_min": float(tot.min()),
         "tiles_per_cta_min": int(p[:, 6].min()), "tiles_per_cta_max": int(p[:, 6].max()),
+        "a_cpwait_frac": float((pall[:, 8] / pall[:, 7]).mean()),
+        "a_arrive_frac": float((pall[:, 9] / pall[:, 7]).mean()),
+        "b_wait_empty_frac": float((pall[:, 10] / pall[:, 11]).mean()),
     }
+    if bm == 256:
+        q = pall[1::2]
+        out["peer_a_cpwait_frac"] = float((q[:, 8] / q[:, 7]).mean())
+        out["peer_a_wait_empty_frac"] = float((q[:, 3] / q[:, 7]).mean())
+        out["peer_b_wait_empty_frac"] = float((q[:, 10] / q[:, 11]).mean())
     print(json.dumps(out))
 
 

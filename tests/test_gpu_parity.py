@@ -46,11 +46,11 @@ def _inputs(T, E, k, H, N, seed, mode="normal", routing=None):
     return ids, X, W, Xd, Wd
 
 
-def run_path(ids, Xd, Wd, E, bn=256, out_dtype=torch.float32, pad=M.MOE_PAD_MAX):
+def run_path(ids, Xd, Wd, E, bn=256, out_dtype=torch.float32, pad=M.MOE_PAD_MAX, bm=128):
     topk = torch.from_numpy(np.ascontiguousarray(ids, dtype=np.int32)).cuda()
     counts, row_off, tok, slot, status = M.moe_route(topk, E)
     counts_h = counts.cpu().numpy()
-    plan = M.Plan(counts_h, Xd.shape[1], Wd.shape[2], 128, bn, pad)
+    plan = M.Plan(counts_h, Xd.shape[1], Wd.shape[2], bm, bn, pad)
     Y = torch.full((tok.numel(), Wd.shape[2]), float("nan"), dtype=out_dtype, device="cuda")
     M.moe_gemm(plan, Xd, tok, Wd, Y=Y)
     torch.cuda.synchronize()
@@ -165,11 +165,12 @@ def test_route_flags_bad_ids_and_empty():
 
 
 # ---------------------------------------------------------------------------- GEMM
-def test_gemm_tiny_a_integer_bit_exact():
+@pytest.mark.parametrize("bm", [128, 256])
+def test_gemm_tiny_a_integer_bit_exact(bm):
     c = synth.CONFIGS["tiny"]
     ids = synth.route(c, 0)
     _, X, W, Xd, Wd = _inputs(c.T, c.E, c.k, c.H, c.N, 0, "int", routing=ids)
-    Y, counts, row_off, tok, slot, plan, _ = run_path(ids, Xd, Wd, c.E, bn=128)
+    Y, counts, row_off, tok, slot, plan, _ = run_path(ids, Xd, Wd, c.E, bn=128, bm=bm)
     rc, rr, rt, rs = omoe.buckets(ids, c.E)
     ref = omoe.expert_gemm(X, W, rt, rr)
     assert counts.tolist() == [11, 0, 11, 10]
@@ -202,19 +203,30 @@ def test_gemm_identity_weights_bf16_exact():
     assert np.array_equal(Y.cpu().double().numpy(), exp)
 
 
-@pytest.mark.parametrize("T,E,k,H,N,bn", [
+RAGGED = [
     (300, 5, 2, 200, 136, 128),     # K tail (200 = 3*64 + 8), N tail, ragged row tiles
     (513, 7, 3, 256, 512, 256),     # several row tiles per expert, exact N tiles
     (64, 16, 4, 128, 176, 176),     # bn not a multiple of 64 (3 W boxes, 176 used)
     (1, 8, 2, 4096, 1024, 256),     # decode: one token
     (2000, 3, 1, 64, 8, 16),        # smallest N tile
-])
+]
+RAGGED_PAIR = [
+    (300, 5, 2, 200, 136, 128),     # pair tiles: second CTA often has no valid rows
+    (700, 3, 2, 256, 512, 256),     # several pair row tiles per expert
+    (64, 16, 4, 128, 352, 224),     # bn/2 = 112: N half not a multiple of 64
+    (1, 8, 2, 4096, 1024, 256),
+    (1500, 4, 1, 128, 200, 32),     # smallest pair N tile, N % 64 != 0 (3-D W map)
+]
+
+
+@pytest.mark.parametrize("T,E,k,H,N,bn,bm,a_path",
+                         [c + (128, "0") for c in RAGGED] + [c + (128, "1") for c in RAGGED]
+                         + [c + (256, "1") for c in RAGGED_PAIR])
 @pytest.mark.parametrize("mode", ["int", "normal"])
-@pytest.mark.parametrize("a_path", ["0", "1"])
-def test_gemm_ragged(T, E, k, H, N, bn, mode, a_path, monkeypatch):
-    monkeypatch.setenv("MOE_A_PATH", a_path)          # both A staging paths (gather4 / cp.async)
+def test_gemm_ragged(T, E, k, H, N, bn, bm, a_path, mode, monkeypatch):
+    monkeypatch.setenv("MOE_A_PATH", a_path)          # A staging path: gather4 (0) / cp.async (1)
     ids, X, W, Xd, Wd = _inputs(T, E, k, H, N, T + E, mode)
-    Y, counts, row_off, tok, *_ = run_path(ids, Xd, Wd, E, bn=bn)
+    Y, counts, row_off, tok, *_ = run_path(ids, Xd, Wd, E, bn=bn, bm=bm)
     rc, rr, rt, rs = omoe.buckets(ids, E)
     ref = omoe.expert_gemm(X, W, rt, rr)
     Yh = Y.cpu().double().numpy()
@@ -259,15 +271,16 @@ def _sample_rows(row_off, counts, rng, per_expert=6):
     return np.array(rows)
 
 
-@pytest.mark.parametrize("cfg,bn", [("mix", 256), ("ds", 128), ("ds", 256), ("dec16", 256), ("paper_worst", 256)])
-def test_gemm_full_size_sampled(cfg, bn):
+@pytest.mark.parametrize("cfg,bn,bm", [("mix", 256, 128), ("mix", 256, 256), ("ds", 128, 128), ("ds", 256, 256),
+                                       ("dec16", 256, 128), ("dec16", 256, 256), ("paper_worst", 256, 256)])
+def test_gemm_full_size_sampled(cfg, bn, bm):
     """BASELINE.json sizes, the launch configuration bench.py times; sampled outputs vs fp64."""
     c = synth.CONFIGS[cfg]
     seed = 0
     ids = synth.route(c, seed)
     Xd = synth.make_x_torch(seed, c.T, c.H, device="cuda")
     Wd = synth.make_w_torch(seed, c.E, c.H, c.N, device="cuda")
-    Y, counts, row_off, tok, *_ = run_path(ids, Xd, Wd, c.E, bn=bn, out_dtype=torch.bfloat16)
+    Y, counts, row_off, tok, *_ = run_path(ids, Xd, Wd, c.E, bn=bn, out_dtype=torch.bfloat16, bm=bm)
     rc, rr, rt, rs = omoe.buckets(ids, c.E)
     assert np.array_equal(tok.cpu().numpy(), rt)
     rng = np.random.default_rng(1)

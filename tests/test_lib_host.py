@@ -80,8 +80,29 @@ def test_planner_matches_oracle_random_corpus():
         E = rng.randint(1, 300)
         counts = np.array([0 if rng.random() < 0.4 else rng.randint(1, 3000) for _ in range(E)])
         N = 8 * rng.randint(1, 2500)
-        bn = 16 * rng.randint(1, 16)
-        _compare(counts, N, 128, bn, rng.choice(["max", "repeat"]))
+        bm = rng.choice([128, 256])
+        bn = (32 if bm == 256 else 16) * rng.randint(1, 256 // (32 if bm == 256 else 16))
+        _compare(counts, N, bm, bn, rng.choice(["max", "repeat"]))
+
+
+def test_planner_auto_tile_choice():
+    """bm = 0: pair tiles unless their padding rows exceed 1.10x the 128-row padding (header rule)."""
+    rng = random.Random(12)
+    for _ in range(200):
+        E = rng.randint(1, 64)
+        counts = [0 if rng.random() < 0.3 else rng.randint(1, 5000) for _ in range(E)]
+        if sum(counts) == 0:
+            continue
+        bn = rng.choice([64, 128, 176, 256])
+        blob = moe_lib.parse_plan_blob(moe_lib.moe_plan_build(counts, 64, 1024, 0, bn))
+        r128 = sum(-(-m // 128) * 128 for m in counts)
+        r256 = sum(-(-m // 256) * 256 for m in counts)
+        expect = 256 if (r256 * 100 <= r128 * 110 and bn % 32 == 0) else 128
+        assert blob["bm"] == expect
+        _compare(np.array(counts), 1024, expect, bn, "max")
+    c = synth.CONFIGS["mix_balanced"]
+    counts = np.bincount(synth.route(c).ravel(), minlength=c.E)
+    assert moe_lib.parse_plan_blob(moe_lib.moe_plan_build(counts, c.H, c.N, 0, 256))["bm"] == 256
 
 
 def test_planner_decode_bijection_through_blob():
