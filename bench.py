@@ -190,7 +190,8 @@ def run_reference(args, cfg):
 def config_dict(cfg, args):
     return {"workload": f"{cfg.name}: E={cfg.E} top-{cfg.k} T={cfg.T} H={cfg.H} N={cfg.N} "
                         f"routing={cfg.routing} seed={args.seed}",
-            "tile": f"{getattr(args, 'bm_resolved', args.bm) or 'auto'}x{args.bn}", "out_dtype": args.out_dtype, "global_batch": cfg.T,
+            "tile": f"{getattr(args, 'bm_resolved', args.bm) or 'auto'}x{args.bn}", "out_dtype": args.out_dtype,
+            "planner": "host (counts D2H + moe_plan_update)" if args.host_plan else "device (moe_plan_device)", "global_batch": cfg.T,
             "l2": "flushed before every timed step (256 MiB memset); W alone exceeds L2",
             "parallelism": f"ep{args.gpus}" if args.gpus > 1 else "1 GPU"}
 
@@ -226,11 +227,16 @@ def run_ours(args, cfg):
     def step(Y=None):
         nonlocal plan
         counts, row_off, tok, slot, _ = M.moe_route(topk_d, cfg.E, with_slot=False)
-        counts_h = counts.cpu().numpy()
-        if plan is None:
-            plan = M.Plan(counts_h, cfg.H, cfg.N, args.bm, args.bn)
-        else:
-            plan.update(counts_h)
+        if args.host_plan:                         # P:142 option 1: counts D2H, plan on the host
+            counts_h = counts.cpu().numpy()
+            if plan is None:
+                plan = M.Plan(counts_h, cfg.H, cfg.N, args.bm, args.bn)
+            else:
+                plan.update(counts_h)
+        else:                                      # P:142 option 2: plan generated on the device
+            if plan is None:
+                plan = M.Plan(None, cfg.H, cfg.N, args.bm, args.bn, E=cfg.E)
+            plan.update_device(counts)
         g0 = torch.cuda.Event(enable_timing=True)
         g0.record(stream)
         Y = M.moe_gemm(plan, Xd, tok, Wd, Y=Y, out_dtype=out_dtype)
@@ -268,6 +274,14 @@ def run_ours(args, cfg):
     gemm_avg = statistics.mean(gemm_ms)
     achieved = flops / (gemm_avg * 1e-3) / 1e12
     peak = float(peaks["bf16_tflops"])
+    # Algorithmic HBM bytes of one moe_gemm launch: W of active experts, the token
+    # rows routed anywhere, Y (out dtype) and the token-index array.
+    counts_np = np.bincount(ids.ravel(), minlength=cfg.E)
+    ybytes = 2 if out_dtype == torch.bfloat16 else 4
+    alg_bytes = (int((counts_np > 0).sum()) * cfg.H * cfg.N * 2 + len(np.unique(ids)) * cfg.H * 2
+                 + int(counts_np.sum()) * (cfg.N * ybytes + 4))
+    hbm = float(peaks["hbm_gbs"])
+    mem_bound = flops / alg_bytes < peak * 1e12 / (hbm * 1e9)
     traffic, tsrc = load_traffic(cfg.name)
 
     # ---- e2e through the public API with pinned host buffers
@@ -282,10 +296,10 @@ def run_ours(args, cfg):
         def e2e_step():
             Xe.copy_(X_h, non_blocking=True)
             te.copy_(ids_h, non_blocking=True)
-            Y, counts_h, _, _, _, _ = M.moe_forward(te, Xe, Wd, cfg.E, bm=args.bm, bn=args.bn, out_dtype=out_dtype,
-                                                    plan=plan)
+            Y, counts, _, _, _, _ = M.moe_forward(te, Xe, Wd, cfg.E, bm=args.bm, bn=args.bn, out_dtype=out_dtype,
+                                                  plan=plan, device_plan=not args.host_plan, Y=Ybuf)
             Y_h.copy_(Y, non_blocking=True)
-            return counts_h
+            return counts
 
         for _ in range(2):
             e2e_step()
@@ -299,8 +313,11 @@ def run_ours(args, cfg):
             s1.record(stream)
             s1.synchronize()
             e_ms.append(s0.elapsed_time(s1))
-        h2d = X_h.numel() * X_h.element_size() + ids_h.numel() * 4 + 4 * plan.blob().size
-        d2h = Y_h.numel() * Y_h.element_size() + 4 * cfg.E
+        h2d = X_h.numel() * X_h.element_size() + ids_h.numel() * 4
+        d2h = Y_h.numel() * Y_h.element_size()
+        if args.host_plan:
+            h2d += 4 * plan.blob().size            # plan blob upload
+            d2h += 4 * cfg.E                       # counts read back for the host planner
         e2e = {"value": flops / (statistics.mean(e_ms) * 1e-3) / 1e12, "unit": "TFLOP/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "ms_per_step": statistics.mean(e_ms)}
@@ -323,13 +340,19 @@ def run_ours(args, cfg):
                        "pct_of_measured_burst_peak": achieved / peak,
                        "pct_of_measured_sustained_peak": achieved / float(peaks["bf16_tflops_sustained"]),
                        "pct_of_datasheet_2250": achieved / 2250.0},
-            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "peak_source": f"{peak_src} bf16_tflops (burst; kernel timed per launch)",
-                         "algorithmic_flops_per_launch": flops, "traffic_source": tsrc},
+            "roofline": ({"bound": "hbm", "achieved": alg_bytes / (gemm_avg * 1e-3) / 1e9, "peak": hbm,
+                          "unit": "GB/s", "frac": alg_bytes / (gemm_avg * 1e-3) / 1e9 / hbm, "traffic": traffic,
+                          "peak_source": f"{peak_src} hbm_gbs", "algorithmic_bytes_per_launch": alg_bytes,
+                          "algorithmic_flops_per_launch": flops, "traffic_source": tsrc}
+                         if mem_bound else
+                         {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                          "frac": achieved / peak, "traffic": traffic,
+                          "peak_source": f"{peak_src} bf16_tflops (burst; kernel timed per launch)",
+                          "algorithmic_flops_per_launch": flops, "algorithmic_bytes_per_launch": alg_bytes,
+                          "traffic_source": tsrc}),
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": 3 * args.steps,
+            "gpu_launches": (3 if args.host_plan else 4) * args.steps,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -349,6 +372,7 @@ def main():
     ap.add_argument("--bm", type=int, default=0, help="tile rows: 128 (1 CTA), 256 (CTA pair), 0 = planner's choice")
     ap.add_argument("--out-dtype", choices=["bf16", "f32"], default="bf16")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--host-plan", action="store_true", help="plan on the host (counts D2H) instead of on the device")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     args = ap.parse_args()

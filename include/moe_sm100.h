@@ -115,12 +115,31 @@ typedef struct moe_plan moe_plan;
  * moe_gemm / moe_decode_debug must be enqueued on the same stream (or after an
  * event on it).  On MOE_OK_EMPTY a valid plan with total = 0 is returned.
  */
-moe_status moe_plan_create(const int32_t* counts_host, int32_t E, int64_t H, int64_t N,
+moe_status moe_plan_create(const int32_t* counts_host /* NULL: all zero, for moe_plan_device */,
+                           int32_t E, int64_t H, int64_t N,
                            int32_t bm, int32_t bn, uint32_t flags, void* stream, moe_plan** out);
 
 /* Re-plan in place for new counts (same E, H, N, bn, flags; the bm resolved at creation is kept);
  * reuses the device buffer. */
 moe_status moe_plan_update(moe_plan* plan, const int32_t* counts_host, void* stream);
+
+/*
+ * Device-side planner ("or directly generated on the device", P:144 parallel prefix
+ * sum): one single-block kernel on `stream` rebuilds the plan's device blob from
+ * device-resident counts (e.g. moe_route's counts_dev) — no host synchronisation, so
+ * route -> plan -> moe_gemm can be enqueued (and graph-captured) back to back.  Same
+ * arithmetic and layout as moe_plan_build except M_pad = pad32(E) (count-independent).
+ * The plan keeps the E, H, N, bm, bn, flags of moe_plan_create (counts_host may be NULL
+ * there; bm = 0 then resolves to 256 when bn % 32 == 0).  Requires E <= 1024.  Afterwards
+ * the host copy is stale: moe_plan_query / moe_plan_blob / moe_decode_debug return
+ * MOE_ERR_INVALID until moe_plan_sync; moe_gemm launches one CTA (pair) per SM and reads
+ * the tile count from the device blob.  If the counts overflow int32 rows or tiles the
+ * device blob gets total = 0 and header word 11 = 3 (reported by moe_plan_sync).
+ */
+moe_status moe_plan_device(moe_plan* plan, const int32_t* counts_dev, void* stream);
+
+/* Copy a device-planned blob back to the host (synchronises `stream`; NULL = plan's stream). */
+moe_status moe_plan_sync(moe_plan* plan, void* stream);
 
 /* Scalars of a plan (any pointer may be NULL). */
 moe_status moe_plan_query(const moe_plan* plan, int32_t* M, int32_t* total_tiles, int32_t* M_pad);

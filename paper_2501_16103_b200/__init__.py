@@ -29,7 +29,7 @@ EXPORTED = (
     "moe_plan_blob_words", "moe_plan_build", "moe_plan_create", "moe_plan_update", "moe_plan_query",
     "moe_plan_blob", "moe_plan_device_blob", "moe_plan_destroy", "moe_route", "moe_gemm",
     "moe_decode_debug", "moe_device_info", "moe_last_error", "moe_version", "moe_probe_gather4",
-    "moe_gemm_profile",
+    "moe_gemm_profile", "moe_plan_device", "moe_plan_sync",
 )
 
 
@@ -73,6 +73,8 @@ def lib() -> ctypes.CDLL:
         "moe_version": (ctypes.c_char_p, []),
         "moe_probe_gather4": (ctypes.c_int32, [vp, ctypes.c_int64, ctypes.c_int64, vp, ctypes.c_int32, vp, vp]),
         "moe_gemm_profile": (ctypes.c_int32, [vp, vp, ctypes.c_int64, vp, vp, vp, ctypes.c_int32, vp, vp]),
+        "moe_plan_device": (ctypes.c_int32, [vp, vp, vp]),
+        "moe_plan_sync": (ctypes.c_int32, [vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -134,17 +136,37 @@ class Plan:
     """Device-resident plan (moe_plan_create / moe_plan_update / moe_plan_destroy)."""
 
     def __init__(self, counts, H: int, N: int, bm: int = 0, bn: int = 256, flags: int = MOE_PAD_MAX,
-                 stream=None):
-        c = np.ascontiguousarray(np.asarray(counts, dtype=np.int32))
-        self.E, self.H, self.N, self.bn, self.flags = int(c.shape[0]), H, N, bn, flags
+                 stream=None, E: int | None = None):
+        """counts: host int array [E], or None (with E=...) for a plan filled by update_device()."""
+        if counts is None:
+            c, cp = None, None
+            self.E = int(E)
+        else:
+            c = np.ascontiguousarray(np.asarray(counts, dtype=np.int32))
+            cp = _i32ptr(c)
+            self.E = int(c.shape[0])
+        self.H, self.N, self.bn, self.flags = H, N, bn, flags
         self._h = ctypes.c_void_p()
-        self.status = _check(lib().moe_plan_create(_i32ptr(c), self.E, H, N, bm, bn, flags, _stream(stream),
+        self.status = _check(lib().moe_plan_create(cp, self.E, H, N, bm, bn, flags, _stream(stream),
                                                    ctypes.byref(self._h)))
         self.bm = int(self.blob()[7])            # resolved tile height (bm = 0: automatic)
+        self.device_resident = False
+
+    def update_device(self, counts_dev, stream=None):
+        """Re-plan on the device from device counts (no host synchronisation)."""
+        _check(lib().moe_plan_device(self._h, counts_dev.data_ptr(), _stream(stream)))
+        self.device_resident = True
+
+    def sync(self, stream=None) -> int:
+        """Copy a device-built plan back to the host (synchronises the stream)."""
+        self.status = _check(lib().moe_plan_sync(self._h, _stream(stream)))
+        self.device_resident = False
+        return self.status
 
     def update(self, counts, stream=None) -> int:
         c = np.ascontiguousarray(np.asarray(counts, dtype=np.int32))
         self.status = _check(lib().moe_plan_update(self._h, _i32ptr(c), _stream(stream)))
+        self.device_resident = False
         return self.status
 
     def query(self) -> tuple[int, int, int]:
@@ -232,7 +254,8 @@ def moe_gemm_profile(plan: Plan, X, token_idx, W, Y, stream=None):
     import torch
 
     n_sm = moe_device_info()[0]
-    grid = min(plan.total_tiles, n_sm) if plan.bm == 128 else 2 * min(plan.total_tiles, n_sm // 2)
+    total = n_sm if plan.device_resident else plan.total_tiles
+    grid = min(total, n_sm) if plan.bm == 128 else 2 * min(total, n_sm // 2)
     prof = torch.zeros((max(grid, 1), len(PROF_SLOTS)), dtype=torch.int64, device=X.device)
     yd = MOE_DTYPE_F32 if Y.dtype == torch.float32 else MOE_DTYPE_BF16
     _check(lib().moe_gemm_profile(plan.handle, X.data_ptr(), X.shape[0], token_idx.data_ptr(), W.data_ptr(),
@@ -259,18 +282,27 @@ def moe_probe_gather4(X, rows, col0: int, stream=None):
 
 
 def moe_forward(topk_ids, X, W, E: int, bm: int = 0, bn: int = 256, out_dtype=None, plan: Plan | None = None,
-                stream=None):
-    """One MoE expert-GEMM step on device: route -> counts D2H -> host plan -> single-launch GEMM.
+                stream=None, device_plan: bool = True, Y=None):
+    """One MoE expert-GEMM step: route -> plan -> single-launch GEMM.
 
-    Returns (Y, counts_host, row_off, token_idx, slot, plan)."""
+    device_plan=True: the plan is built on the device from the route's counts (moe_plan_device),
+    no host synchronisation; counts are returned as a device tensor.  device_plan=False: counts
+    are copied to the host and planned there (moe_plan_update; P:142's first option).
+    Returns (Y, counts, row_off, token_idx, slot, plan)."""
     import torch
 
     counts, row_off, token_idx, slot, _ = moe_route(topk_ids, E, stream=stream)
-    counts_h = counts.cpu().numpy()            # the planner runs on the host (P:142)
     H, N = int(X.shape[1]), int(W.shape[2])
-    if plan is None:
-        plan = Plan(counts_h, H, N, bm, bn, stream=stream)
+    if device_plan:
+        if plan is None:
+            plan = Plan(None, H, N, bm, bn, stream=stream, E=E)
+        plan.update_device(counts, stream=stream)
+        counts_out = counts
     else:
-        plan.update(counts_h, stream=stream)
-    Y = moe_gemm(plan, X, token_idx, W, out_dtype=out_dtype or torch.bfloat16, stream=stream)
-    return Y, counts_h, row_off, token_idx, slot, plan
+        counts_out = counts.cpu().numpy()
+        if plan is None:
+            plan = Plan(counts_out, H, N, bm, bn, stream=stream)
+        else:
+            plan.update(counts_out, stream=stream)
+    Y = moe_gemm(plan, X, token_idx, W, Y=Y, out_dtype=out_dtype or torch.bfloat16, stream=stream)
+    return Y, counts_out, row_off, token_idx, slot, plan

@@ -37,6 +37,8 @@
 namespace moe {
 const int32_t* plan_blob_host(const moe_plan* p, int64_t* words);
 const int32_t* plan_blob_dev(const moe_plan* p);
+bool plan_device_mode(const moe_plan* p);
+void plan_shape(const moe_plan* p, int32_t* E, int32_t* H, int32_t* N, int32_t* bm, int32_t* bn, uint32_t* flags);
 }  // namespace moe
 
 namespace {
@@ -66,7 +68,7 @@ struct GemmArgs {
   int32_t y_f32;
   int32_t N;
   int32_t num_kb;
-  int32_t total;
+  int32_t total;             // < 0: device-planned, read the tile count from the blob header
   int32_t M_pad;
   int32_t off_params;
   int32_t T;
@@ -209,6 +211,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const int total = a.total >= 0 ? a.total : __ldg(a.plan + 2);
   // CTA pair: rank 0 (leader) issues the MMAs for both CTAs; all consumers of the
   // data path (full / tmem-empty barriers) live in the leader.
   const uint32_t rank = kCta == 2 ? cluster_ctarank() : 0;
@@ -262,7 +265,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int ch = threadIdx.x & 7;                 // cp.async: 16-byte chunk of the 128-byte row
     const int rsub = threadIdx.x >> 3;              // cp.async: row within a 16-row group
     const uint32_t dst_off = rsub * 128 + ((ch ^ (rsub & 7)) << 4);
-    for (int v = pair_id; v < a.total; v += n_pairs) {
+    for (int v = pair_id; v < total; v += n_pairs) {
       int h, task, l;
       map_tile(s_prefix, s_sigma, a.M_pad, v, h, task, l);
       const Tile t = load_tile(params, task, l);
@@ -321,7 +324,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint64_t pol_w = policy_evict_normal();
     uint32_t g = 0;
     long long c_wait = 0, c_t0 = kProf ? clock64() : 0;
-    for (int v = pair_id; v < a.total; v += n_pairs) {
+    for (int v = pair_id; v < total; v += n_pairs) {
       int h, task, l;
       map_tile(s_prefix, s_sigma, a.M_pad, v, h, task, l);
       const Tile t = load_tile(params, task, l);
@@ -369,7 +372,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t acc_phase = 0;
       long long c_tmem = 0, c_full = 0, c_t0 = kProf ? clock64() : 0;
       int n_tiles = 0;
-      for (int v = pair_id; v < a.total; v += n_pairs) {
+      for (int v = pair_id; v < total; v += n_pairs) {
         ++n_tiles;
         int h, task, l;
         map_tile(s_prefix, s_sigma, a.M_pad, v, h, task, l);
@@ -424,7 +427,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // Pair peer: relay "my A stage landed" (local full barrier, fed by cp.async arrivals) to the
       // leader's full barrier, where the MMA issuer waits for both CTAs' bytes.
       uint32_t g = 0;
-      for (int v = pair_id; v < a.total; v += n_pairs)
+      for (int v = pair_id; v < total; v += n_pairs)
         for (int kb = 0; kb < a.num_kb; ++kb, ++g) {
           const int s = g % kSt;
           mbar_wait(full_bar(s), (g / kSt) & 1u);
@@ -437,7 +440,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     long long c_wait = 0, c_work = 0;
-    for (int v = pair_id; v < a.total; v += n_pairs) {
+    for (int v = pair_id; v < total; v += n_pairs) {
       int h, task, l;
       map_tile(s_prefix, s_sigma, a.M_pad, v, h, task, l);
       const Tile t = load_tile(params, task, l);
@@ -641,11 +644,26 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
                               const void* W, void* Y, int32_t y_dtype, void* stream, long long* prof) {
   moe::clear_error();
   if (!plan) MOE_FAIL(MOE_ERR_INVALID, "moe_gemm: null plan");
-  int64_t words = 0;
-  const int32_t* blob = moe::plan_blob_host(plan, &words);
   moe::BlobView v;
-  if (!moe::blob_view(blob, words, &v)) MOE_FAIL(MOE_ERR_INVALID, "moe_gemm: corrupt plan");
-  if (v.total == 0) return MOE_OK_EMPTY;
+  const bool dev_planned = moe::plan_device_mode(plan);
+  if (dev_planned) {
+    // Counts live on the device (moe_plan_device): fixed-layout blob, tile count read in-kernel.
+    int32_t E, H, N, bm, bn;
+    uint32_t flags;
+    moe::plan_shape(plan, &E, &H, &N, &bm, &bn, &flags);
+    v.E = E; v.H = H; v.N = N; v.bm = bm; v.bn = bn; v.flags = flags; v.n_tasks = E;
+    v.M_pad = E <= 32 ? 32 : (E + 31) / 32 * 32;
+    v.M = -1;
+    v.total = -1;
+    v.off_prefix = MOE_PLAN_HEADER;
+    v.off_sigma = v.off_prefix + v.M_pad;
+    v.off_params = v.off_sigma + v.M_pad;
+  } else {
+    int64_t words = 0;
+    const int32_t* blob = moe::plan_blob_host(plan, &words);
+    if (!moe::blob_view(blob, words, &v)) MOE_FAIL(MOE_ERR_INVALID, "moe_gemm: corrupt plan");
+    if (v.total == 0) return MOE_OK_EMPTY;
+  }
   if (!X || !token_idx || !W || !Y) MOE_FAIL(MOE_ERR_INVALID, "moe_gemm: null tensor pointer");
   if (!aligned16(X) || !aligned16(W) || !aligned16(Y))
     MOE_FAIL(MOE_ERR_INVALID, "moe_gemm: X, W and Y must be 16-byte aligned");
@@ -685,7 +703,7 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
   cudaError_t attr_err = set_smem_attrs();
   if (attr_err != cudaSuccess) MOE_FAIL(MOE_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(attr_err));
   if (v.bm == 256) {
-    const int pairs = std::min(v.total, sm_count_cached() / 2);
+    const int pairs = v.total < 0 ? sm_count_cached() / 2 : std::min(v.total, sm_count_cached() / 2);
     const size_t smem = Geo<2>::kSmem + 8 * (size_t)v.M_pad;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * pairs);
@@ -703,7 +721,7 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
                           : cudaLaunchKernelEx(&cfg, moe_gemm_kernel<false, 2>, tmX, tmW, a);
     if (le != cudaSuccess) MOE_FAIL(MOE_ERR_CUDA, "moe_gemm pair launch: %s", cudaGetErrorString(le));
   } else {
-    const int grid = std::min(v.total, sm_count_cached());
+    const int grid = v.total < 0 ? sm_count_cached() : std::min(v.total, sm_count_cached());
     const size_t smem = Geo<1>::kSmem + 8 * (size_t)v.M_pad;
     if (prof)
       moe_gemm_kernel<true, 1><<<grid, kThreads, smem, (cudaStream_t)stream>>>(tmX, tmW, a);
@@ -733,6 +751,7 @@ moe_status moe_gemm_profile(const moe_plan* plan, const void* X, int64_t T, cons
 moe_status moe_decode_debug(const moe_plan* plan, int32_t* out, void* stream) {
   moe::clear_error();
   if (!plan || !out) MOE_FAIL(MOE_ERR_INVALID, "moe_decode_debug: null argument");
+  if (moe::plan_device_mode(plan)) MOE_FAIL(MOE_ERR_INVALID, "moe_decode_debug: device-resident plan (call moe_plan_sync)");
   int64_t words = 0;
   const int32_t* blob = moe::plan_blob_host(plan, &words);
   moe::BlobView v;

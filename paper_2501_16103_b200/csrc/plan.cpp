@@ -185,6 +185,7 @@ struct moe_plan {
   int64_t H = 0, N = 0;
   int32_t bm = 0, bn = 0;
   uint32_t flags = 0;
+  bool device_mode = false;   // device blob written by moe_plan_device; host blob stale
 };
 
 namespace moe {
@@ -194,6 +195,17 @@ const int32_t* plan_blob_host(const moe_plan* p, int64_t* words) {
 }
 const int32_t* plan_blob_dev(const moe_plan* p) { return p->dev; }
 cudaStream_t plan_stream(const moe_plan* p) { return p->stream; }
+bool plan_device_mode(const moe_plan* p) { return p->device_mode; }
+void plan_set_device_mode(moe_plan* p, bool on) { p->device_mode = on; }
+void plan_shape(const moe_plan* p, int32_t* E, int32_t* H, int32_t* N, int32_t* bm, int32_t* bn, uint32_t* flags) {
+  *E = p->E;
+  *H = (int32_t)p->H;
+  *N = (int32_t)p->N;
+  *bm = p->bm;
+  *bn = p->bn;
+  *flags = p->flags;
+}
+int32_t* plan_blob_dev_mut(moe_plan* p) { return p->dev; }
 }  // namespace moe
 
 extern "C" {
@@ -213,6 +225,11 @@ moe_status moe_plan_create(const int32_t* counts, int32_t E, int64_t H, int64_t 
   if (E < 1) MOE_FAIL(MOE_ERR_INVALID, "moe_plan_create: E=%d", E);
   auto* p = new moe_plan();
   p->blob.resize(moe_plan_blob_words(E));
+  std::vector<int32_t> zeros;
+  if (!counts) {                                // plan to be filled on the device (moe_plan_device)
+    zeros.assign(E, 0);
+    counts = zeros.data();
+  }
   moe_status st = moe_plan_build(counts, E, H, N, bm, bn, flags, p->blob.data(), (int64_t)p->blob.size(), &p->words);
   if (st < 0) {
     delete p;
@@ -250,13 +267,32 @@ moe_status moe_plan_update(moe_plan* p, const int32_t* counts, void* stream) {
                                  (int64_t)p->blob.size(), &words);
   if (st < 0) return st;
   p->words = words;
+  p->device_mode = false;
   if (stream) p->stream = (cudaStream_t)stream;
   moe_status up = upload(p, p->stream);
   return up != MOE_OK ? up : st;
 }
 
+moe_status moe_plan_sync(moe_plan* p, void* stream) {
+  moe::clear_error();
+  if (!p) MOE_FAIL(MOE_ERR_INVALID, "moe_plan_sync: null plan");
+  if (!p->device_mode) return MOE_OK;
+  cudaStream_t s = stream ? (cudaStream_t)stream : p->stream;
+  cudaError_t e = cudaMemcpyAsync(p->blob.data(), p->dev, sizeof(int32_t) * p->dev_words, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) MOE_FAIL(MOE_ERR_CUDA, "moe_plan_sync: %s", cudaGetErrorString(e));
+  moe::BlobView v;
+  if (!moe::blob_view(p->blob.data(), (int64_t)p->blob.size(), &v)) MOE_FAIL(MOE_ERR_INVALID, "moe_plan_sync: corrupt device blob");
+  p->words = v.words;
+  p->device_mode = false;
+  if (p->blob[11] != 0)
+    MOE_FAIL(MOE_ERR_CAPACITY, "moe_plan_device: rows or tiles >= 2^31 (device planner status %d)", p->blob[11]);
+  return p->blob[1] == 0 ? MOE_OK_EMPTY : MOE_OK;
+}
+
 moe_status moe_plan_query(const moe_plan* p, int32_t* M, int32_t* total, int32_t* M_pad) {
   if (!p) MOE_FAIL(MOE_ERR_INVALID, "moe_plan_query: null plan");
+  if (p->device_mode) MOE_FAIL(MOE_ERR_INVALID, "moe_plan_query: plan is device-resident (call moe_plan_sync)");
   if (M) *M = p->blob[1];
   if (total) *total = p->blob[2];
   if (M_pad) *M_pad = p->blob[3];
@@ -265,6 +301,7 @@ moe_status moe_plan_query(const moe_plan* p, int32_t* M, int32_t* total, int32_t
 
 moe_status moe_plan_blob(const moe_plan* p, int32_t* out, int64_t cap, int64_t* len) {
   if (!p) MOE_FAIL(MOE_ERR_INVALID, "moe_plan_blob: null plan");
+  if (p->device_mode) MOE_FAIL(MOE_ERR_INVALID, "moe_plan_blob: plan is device-resident (call moe_plan_sync)");
   if (len) *len = p->words;
   if (out) {
     if (cap < p->words) MOE_FAIL(MOE_ERR_CAPACITY, "moe_plan_blob: cap %lld < %lld", (long long)cap, (long long)p->words);

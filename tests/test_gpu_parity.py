@@ -293,3 +293,76 @@ def test_gemm_full_size_sampled(cfg, bn, bm):
     tol_check(got, ref, cfg)
     # every row written (NaN sentinel) — the exactly-once cover follows from the bit-exact decode
     assert not torch.isnan(Y.float()).any().item()
+
+
+# ---------------------------------------------------------------------------- device-side planner
+def _device_plan_blob(counts, N, bm, bn, pad, H=64):
+    E = len(counts)
+    plan = M.Plan(None, H, N, bm, bn, M.MOE_PAD_REPEAT if pad == "repeat" else 0, E=E)
+    plan.update_device(torch.tensor(np.asarray(counts), dtype=torch.int32, device="cuda"))
+    st = plan.sync()
+    return plan, st, M.parse_plan_blob(plan.blob())
+
+
+@pytest.mark.parametrize("pad", ["max", "repeat"])
+@pytest.mark.parametrize("bm,bn", [(128, 256), (256, 256), (128, 48), (256, 96)])
+def test_plan_device_bit_exact(pad, bm, bn):
+    rng = np.random.default_rng(bm + bn)
+    cases = [np.array([11, 0, 11, 10]), np.zeros(5, dtype=np.int64), np.array([1]),
+             np.where(rng.random(1024) < 0.3, 0, rng.integers(1, 3000, size=1024)),
+             np.bincount(synth.route(synth.CONFIGS["ds"], 0).ravel(), minlength=64)]
+    for counts in cases:
+        N = 1408
+        plan, st, b = _device_plan_blob(counts, N, bm, bn, pad)
+        ref = omoe.plan(counts, N, bm, bn, pad_mode=pad)
+        E = len(counts)
+        assert b["M"] == ref["M"] and b["total"] == ref["total"]
+        assert st == (M.MOE_OK_EMPTY if ref["M"] == 0 else M.MOE_OK)
+        assert b["M_pad"] == (32 if E <= 32 else -(-E // 32) * 32)
+        assert b["prefix"][: ref["M"]].tolist() == ref["prefix"]
+        padv = (ref["prefix"][-1] if ref["M"] else 2**31 - 1) if pad == "repeat" else 2**31 - 1
+        assert (b["prefix"][ref["M"]:] == padv).all()
+        assert b["sigma"][: ref["M"]].tolist() == ref["sigma"]
+        assert b["row_off"].tolist() == np.concatenate([[0], np.cumsum(counts)]).tolist()
+        host = M.parse_plan_blob(M.moe_plan_build(counts, 64, N, bm, bn, M.MOE_PAD_REPEAT if pad == "repeat" else 0))
+        assert np.array_equal(b["params"], host["params"])
+
+
+def test_plan_device_overflow_reported():
+    plan, _, _ = None, None, None
+    p = M.Plan(None, 64, 1 << 20, 128, 16, E=3)
+    p.update_device(torch.tensor([2**30, 2**30, 5], dtype=torch.int32, device="cuda"))
+    with pytest.raises(M.MoeError) as e:
+        p.sync()
+    assert e.value.status == -3
+
+
+@pytest.mark.parametrize("bm", [128, 256])
+@pytest.mark.parametrize("T,E,k,H,N,bn", [(300, 5, 2, 200, 136, 128), (513, 7, 3, 256, 512, 256), (1, 8, 2, 4096, 1024, 256)])
+def test_gemm_device_planned(T, E, k, H, N, bn, bm):
+    ids, X, W, Xd, Wd = _inputs(T, E, k, H, N, T + E + 1, "int")
+    topk = torch.from_numpy(ids).cuda()
+    Yout = torch.full((T * k, N), float("nan"), dtype=torch.float32, device="cuda")
+    Y, counts, row_off, tok, slot, plan = M.moe_forward(topk, Xd, Wd, E, bm=bm, bn=bn, Y=Yout, device_plan=True)
+    torch.cuda.synchronize()
+    rc, rr, rt, rs = omoe.buckets(ids, E)
+    assert np.array_equal(Y.cpu().double().numpy(), omoe.expert_gemm(X, W, rt, rr))
+    # a second step on the same plan object with different routing
+    ids2 = synth.route_gumbel(99, T, E, k)
+    Y2, *_ = M.moe_forward(torch.from_numpy(ids2).cuda(), Xd, Wd, E, plan=plan, out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    rc, rr, rt, rs = omoe.buckets(ids2, E)
+    assert np.array_equal(Y2.cpu().double().numpy(), omoe.expert_gemm(X, W, rt, rr))
+
+
+def test_gemm_device_planned_all_empty():
+    """A rank that receives no rows: the device plan has total 0 and the launch does nothing."""
+    Xd = torch.zeros((4, 64), dtype=torch.bfloat16, device="cuda")
+    Wd = torch.zeros((3, 64, 128), dtype=torch.bfloat16, device="cuda")
+    plan = M.Plan(None, 64, 128, 128, 128, E=3)
+    plan.update_device(torch.zeros(3, dtype=torch.int32, device="cuda"))
+    tok = torch.zeros(1, dtype=torch.int32, device="cuda")
+    Y = torch.full((1, 128), 7.0, dtype=torch.float32, device="cuda")
+    M.moe_gemm(plan, Xd, tok, Wd, Y=Y)
+    torch.cuda.synchronize()
+    assert (Y == 7.0).all()
