@@ -157,13 +157,14 @@ void moe_plan_destroy(moe_plan* plan);
  * Token-index buckets on device, stable: token_idx[row_off[e] + r]
  * is the r-th smallest token id t with e in topk_ids[t, :].
  *   topk_ids_dev [T, k] int32 row-major, expert ids in [0, E); no token may list
- *                an expert twice.
+ *                an expert twice.  A negative id marks a masked slot (skipped silently;
+ *                used by expert parallelism for slots owned by another rank).
  *   counts_dev   [E]   out: m_e.
  *   row_off_dev  [E+1] out: exclusive prefix of counts.
  *   token_idx_dev[T*k] out.
  *   slot_dev     [T*k] out (nullable): the top-k position j of each row.
- *   status_dev   [1]   out (nullable): set to 0, or to 1 if an id was out of range
- *                      or duplicated in a token (those entries are dropped).
+ *   status_dev   [1]   out (nullable): set to 0, or to 1 if an id was >= E or
+ *                      duplicated in a token (those entries are dropped).
  * Two kernel launches on `stream`; T*k < 2^31, 1 <= k <= 32, 1 <= E <= 1024.
  */
 moe_status moe_route(const int32_t* topk_ids_dev, int64_t T, int32_t k, int32_t E,
@@ -185,6 +186,15 @@ moe_status moe_route(const int32_t* topk_ids_dev, int64_t T, int32_t k, int32_t 
  */
 moe_status moe_gemm(const moe_plan* plan, const void* X_dev, int64_t T, const int32_t* token_idx_dev,
                     const void* W_dev, void* Y_dev, int32_t y_dtype, void* stream);
+
+/*
+ * moe_gemm with the output rows scattered: the result row of CSR row i is written to
+ * Y_dev[y_row_map_dev[i]] (Y_dev has at least max(map)+1 rows of N).  Used by expert
+ * parallelism to write results straight into the combine send buffer (no Y gather copy).
+ */
+moe_status moe_gemm_rowmap(const moe_plan* plan, const void* X_dev, int64_t T, const int32_t* token_idx_dev,
+                           const void* W_dev, void* Y_dev, int32_t y_dtype, const int32_t* y_row_map_dev,
+                           void* stream);
 
 /*
  * Device decode of every virtual tile B in [0, total) with the same device

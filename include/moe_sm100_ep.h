@@ -1,0 +1,68 @@
+/*
+ * moe_sm100_ep.h — expert-parallel (EP) bookkeeping kernels of libmoe_sm100.
+ *
+ * Expert parallelism is background in the paper ("a subset of experts reside on
+ * each GPU"; the per-GPU work remains an irregular batch).  Sharding (R8): G ranks,
+ * rank g owns experts [g*E/G, (g+1)*E/G) and its own tokens.  One EP step:
+ *   1. moe_ep_dispatch_plan  per destination d: the owned tokens with >= 1 expert on d
+ *                            (deduplicated, ascending token), their d-local expert ids;
+ *   2. NCCL all-to-all of the counts (caller), moe_gather_rows + all-to-all of the rows;
+ *   3. on every rank: moe_route over the received rows' local ids (-1 = masked slot),
+ *      moe_plan_device, moe_gemm_rowmap writing each result row straight into the combine
+ *      send buffer at the position moe_ep_combine_map chose;
+ *   4. all-to-all of the result rows back (caller), moe_ep_unpack into (token, slot) order.
+ * Same conventions as moe_sm100.h (device pointers, void* stream, no synchronisation).
+ */
+#ifndef MOE_SM100_EP_H_
+#define MOE_SM100_EP_H_
+
+#include "moe_sm100.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/*
+ * topk_dev [T, k] int32 global expert ids of this rank's tokens (negative = masked), E % G == 0.
+ * Out (device):
+ *   counts2_dev [G][2]   {rows sent to d, result rows d will return} — exchanged by the caller
+ *                        with one all-to-all of 2 ints per peer;
+ *   send_off_dev [G+1]   exclusive prefix of rows sent per destination;
+ *   send_tok_dev [<= G*T] local token index of each send row (destination-major, ascending t);
+ *   send_meta_dev [<= G*T, k] the row's k ids mapped to destination-local expert ids, -1 where
+ *                        another rank owns the slot.
+ * Two kernel launches.
+ */
+moe_status moe_ep_dispatch_plan(const int32_t* topk_dev, int64_t T, int32_t k, int32_t E, int32_t G,
+                                int32_t* counts2_dev, int32_t* send_off_dev, int32_t* send_tok_dev,
+                                int32_t* send_meta_dev, void* stream);
+
+/* dst_dev[i, :] = src_dev[idx_dev[i], :] for n rows of row_bytes (a multiple of 16, 16-byte aligned). */
+moe_status moe_gather_rows(const void* src_dev, const int32_t* idx_dev, int64_t n, int64_t row_bytes,
+                           void* dst_dev, void* stream);
+
+/*
+ * Expert side.  For the n CSR rows of moe_route over the received rows (token_idx_dev: received
+ * row r, slot_dev: top-k slot j), recv_off_dev [G+1]: segment of received rows per source,
+ * ret_off_dev [G+1]: segment of the combine send buffer per source.  Out: row_map_dev[i] =
+ * position of CSR row i in the combine send buffer (any order within a source's segment;
+ * pass it to moe_gemm_rowmap), ret_meta_dev[pos] = (r - recv_off[s]) * k + j.  cursor_dev:
+ * [G] int32 scratch.
+ */
+moe_status moe_ep_combine_map(const int32_t* token_idx_dev, const int32_t* slot_dev, int64_t n,
+                              const int32_t* recv_off_dev, const int32_t* ret_off_dev, int32_t G, int32_t k,
+                              int32_t* cursor_dev, int32_t* row_map_dev, int32_t* ret_meta_dev, void* stream);
+
+/*
+ * Source side.  rows_dev: n returned result rows (segment per destination given by
+ * ret_off_dev [G+1]) with their ret_meta_dev; send_off_dev / send_tok_dev from
+ * moe_ep_dispatch_plan.  out_dev[t * k + j, :] = the returned row of (token t, slot j).
+ */
+moe_status moe_ep_unpack(const void* rows_dev, const int32_t* ret_meta_dev, int64_t n, const int32_t* ret_off_dev,
+                         const int32_t* send_off_dev, const int32_t* send_tok_dev, int32_t G, int32_t k,
+                         int64_t row_bytes, void* out_dev, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MOE_SM100_EP_H_ */

@@ -29,7 +29,8 @@ EXPORTED = (
     "moe_plan_blob_words", "moe_plan_build", "moe_plan_create", "moe_plan_update", "moe_plan_query",
     "moe_plan_blob", "moe_plan_device_blob", "moe_plan_destroy", "moe_route", "moe_gemm",
     "moe_decode_debug", "moe_device_info", "moe_last_error", "moe_version", "moe_probe_gather4",
-    "moe_gemm_profile", "moe_plan_device", "moe_plan_sync",
+    "moe_gemm_profile", "moe_plan_device", "moe_plan_sync", "moe_gemm_rowmap",
+    "moe_ep_dispatch_plan", "moe_gather_rows", "moe_ep_combine_map", "moe_ep_unpack",
 )
 
 
@@ -75,6 +76,14 @@ def lib() -> ctypes.CDLL:
         "moe_gemm_profile": (ctypes.c_int32, [vp, vp, ctypes.c_int64, vp, vp, vp, ctypes.c_int32, vp, vp]),
         "moe_plan_device": (ctypes.c_int32, [vp, vp, vp]),
         "moe_plan_sync": (ctypes.c_int32, [vp, vp]),
+        "moe_gemm_rowmap": (ctypes.c_int32, [vp, vp, ctypes.c_int64, vp, vp, vp, ctypes.c_int32, vp, vp]),
+        "moe_ep_dispatch_plan": (ctypes.c_int32, [vp, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
+                                                  ctypes.c_int32, vp, vp, vp, vp, vp]),
+        "moe_gather_rows": (ctypes.c_int32, [vp, vp, ctypes.c_int64, ctypes.c_int64, vp, vp]),
+        "moe_ep_combine_map": (ctypes.c_int32, [vp, vp, ctypes.c_int64, vp, vp, ctypes.c_int32, ctypes.c_int32,
+                                                vp, vp, vp, vp]),
+        "moe_ep_unpack": (ctypes.c_int32, [vp, vp, ctypes.c_int64, vp, vp, vp, ctypes.c_int32, ctypes.c_int32,
+                                           ctypes.c_int64, vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -211,7 +220,10 @@ def moe_device_info() -> tuple[int, int, int]:
 
 
 def moe_route(topk_ids, E: int, with_slot: bool = True, stream=None):
-    """topk_ids: int32 CUDA tensor [T, k] -> (counts[E], row_off[E+1], token_idx[T*k], slot, status)."""
+    """topk_ids: int32 CUDA tensor [T, k] -> (counts[E], row_off[E+1], token_idx[T*k], slot, status).
+
+    With masked (negative) or invalid ids only the first sum(counts) = row_off[E] entries of
+    token_idx / slot are meaningful (the length is not read back, to avoid a host sync)."""
     import torch
 
     assert topk_ids.is_cuda and topk_ids.dtype == torch.int32 and topk_ids.is_contiguous()
@@ -228,8 +240,8 @@ def moe_route(topk_ids, E: int, with_slot: bool = True, stream=None):
     return counts, row_off, token_idx[: T * k], (slot[: T * k] if slot is not None else None), status
 
 
-def moe_gemm(plan: Plan, X, token_idx, W, Y=None, out_dtype=None, stream=None):
-    """Y[sum m_e, N] = per-expert X[token_idx] @ W[e] in one launch."""
+def moe_gemm(plan: Plan, X, token_idx, W, Y=None, out_dtype=None, stream=None, row_map=None):
+    """Y[sum m_e, N] = per-expert X[token_idx] @ W[e] in one launch (row_map: Y row of CSR row i)."""
     import torch
 
     out_dtype = out_dtype or torch.bfloat16
@@ -240,8 +252,13 @@ def moe_gemm(plan: Plan, X, token_idx, W, Y=None, out_dtype=None, stream=None):
     if Y is None:
         Y = torch.empty((rows, plan.N), dtype=out_dtype, device=X.device)
     yd = MOE_DTYPE_F32 if Y.dtype == torch.float32 else MOE_DTYPE_BF16
-    _check(lib().moe_gemm(plan.handle, X.data_ptr(), X.shape[0], token_idx.data_ptr(), W.data_ptr(),
-                          Y.data_ptr(), yd, _stream(stream)))
+    if row_map is None:
+        _check(lib().moe_gemm(plan.handle, X.data_ptr(), X.shape[0], token_idx.data_ptr(), W.data_ptr(),
+                              Y.data_ptr(), yd, _stream(stream)))
+    else:
+        assert row_map.dtype == torch.int32 and row_map.is_contiguous()
+        _check(lib().moe_gemm_rowmap(plan.handle, X.data_ptr(), X.shape[0], token_idx.data_ptr(), W.data_ptr(),
+                                     Y.data_ptr(), yd, row_map.data_ptr(), _stream(stream)))
     return Y
 
 
@@ -261,6 +278,59 @@ def moe_gemm_profile(plan: Plan, X, token_idx, W, Y, stream=None):
     _check(lib().moe_gemm_profile(plan.handle, X.data_ptr(), X.shape[0], token_idx.data_ptr(), W.data_ptr(),
                                   Y.data_ptr(), yd, prof.data_ptr(), _stream(stream)))
     return Y, prof[:grid]
+
+
+# ---------------------------------------------------------------------------
+# expert-parallel bookkeeping kernels (include/moe_sm100_ep.h)
+# ---------------------------------------------------------------------------
+def moe_ep_dispatch_plan(topk_ids, E: int, G: int, stream=None):
+    """-> counts2 [G, 2] (rows sent to d, result rows d returns), send_off [G+1], send_tok [G*T],
+    send_meta [G*T, k] (device; only the first send_off[G] rows are meaningful)."""
+    import torch
+
+    T, k = topk_ids.shape
+    dev = topk_ids.device
+    counts2 = torch.empty((G, 2), dtype=torch.int32, device=dev)
+    send_off = torch.empty(G + 1, dtype=torch.int32, device=dev)
+    cap = max(G * T, 1)
+    send_tok = torch.empty(cap, dtype=torch.int32, device=dev)
+    send_meta = torch.empty((cap, k), dtype=torch.int32, device=dev)
+    _check(lib().moe_ep_dispatch_plan(topk_ids.data_ptr(), T, k, E, G, counts2.data_ptr(), send_off.data_ptr(),
+                                      send_tok.data_ptr(), send_meta.data_ptr(), _stream(stream)))
+    return counts2, send_off, send_tok, send_meta
+
+
+def moe_gather_rows(src, idx, out=None, stream=None):
+    import torch
+
+    n = int(idx.numel())
+    if out is None:
+        out = torch.empty((n,) + tuple(src.shape[1:]), dtype=src.dtype, device=src.device)
+    row_bytes = src[0].numel() * src.element_size() if src.shape[0] else 16
+    _check(lib().moe_gather_rows(src.data_ptr(), idx.data_ptr(), n, row_bytes, out.data_ptr(), _stream(stream)))
+    return out
+
+
+def moe_ep_combine_map(token_idx, slot, recv_off, ret_off, G: int, k: int, stream=None):
+    import torch
+
+    n = int(token_idx.numel())
+    dev = token_idx.device
+    cursor = torch.empty(G, dtype=torch.int32, device=dev)
+    row_map = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    ret_meta = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    _check(lib().moe_ep_combine_map(token_idx.data_ptr(), slot.data_ptr(), n, recv_off.data_ptr(),
+                                    ret_off.data_ptr(), G, k, cursor.data_ptr(), row_map.data_ptr(),
+                                    ret_meta.data_ptr(), _stream(stream)))
+    return row_map[:n], ret_meta[:n]
+
+
+def moe_ep_unpack(rows, ret_meta, ret_off, send_off, send_tok, G: int, k: int, out, stream=None):
+    n = int(rows.shape[0])
+    row_bytes = rows[0].numel() * rows.element_size() if n else 16
+    _check(lib().moe_ep_unpack(rows.data_ptr(), ret_meta.data_ptr(), n, ret_off.data_ptr(), send_off.data_ptr(),
+                               send_tok.data_ptr(), G, k, row_bytes, out.data_ptr(), _stream(stream)))
+    return out
 
 
 def moe_decode_debug(plan: Plan, stream=None):

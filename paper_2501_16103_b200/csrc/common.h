@@ -6,6 +6,7 @@
 #include <string>
 
 #include "moe_sm100.h"
+#include "moe_sm100_ep.h"
 
 namespace moe {
 

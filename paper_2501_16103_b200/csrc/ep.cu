@@ -1,0 +1,230 @@
+// Expert-parallel (EP) bookkeeping kernels: dispatch of token rows to the ranks that own
+// their experts, and combine of expert outputs back to the tokens' owners.
+//
+// The paper gives EP only as background ("a subset of experts reside on each
+// GPU"; per-GPU work stays irregular).  Sharding (R8): G ranks, rank g owns
+// experts [g*El, (g+1)*El) and its own tokens.  A token is sent ONCE to every rank that
+// owns at least one of its experts (deduplicated per destination — the token-copy
+// argument of §4.3 applied across GPUs); the receiving rank runs the ordinary single-launch
+// GEMM over its local experts; each (token, slot) result row returns to the token's owner.
+// The collectives themselves are NCCL all-to-alls issued by the caller (torch.distributed);
+// these kernels produce and consume the packed, variable-split buffers.
+#include <cuda_runtime.h>
+
+#include <climits>
+
+#include "common.h"
+
+namespace {
+
+constexpr int kThreads = 1024;
+
+__device__ __forceinline__ bool owns(int e, int d, int El) { return e >= 0 && e / El == d; }
+
+// Block d: rows to send to d (tokens with >= 1 slot owned by d) and result rows d returns
+// (slots owned by d).
+__global__ void __launch_bounds__(kThreads)
+    ep_count_kernel(const int32_t* __restrict__ topk, int T, int k, int El, int32_t* __restrict__ counts2) {
+  const int d = blockIdx.x;
+  int rows = 0, slots = 0;
+  for (int t = threadIdx.x; t < T; t += blockDim.x) {
+    int n = 0;
+    for (int j = 0; j < k; ++j) n += owns(topk[(int64_t)t * k + j], d, El);
+    rows += n > 0;
+    slots += n;
+  }
+  __shared__ int s_r[32], s_s[32];
+  for (int o = 16; o > 0; o >>= 1) {
+    rows += __shfl_xor_sync(0xffffffffu, rows, o);
+    slots += __shfl_xor_sync(0xffffffffu, slots, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    s_r[threadIdx.x >> 5] = rows;
+    s_s[threadIdx.x >> 5] = slots;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int a = 0, b = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      a += s_r[w];
+      b += s_s[w];
+    }
+    counts2[2 * d] = a;       // send rows to d
+    counts2[2 * d + 1] = b;   // result rows d returns to me
+  }
+}
+
+// Block d: stable (ascending t) compaction of the tokens sent to d into the send segment
+// [send_off[d], send_off[d+1]); send_meta row = the token's k ids mapped to d-local expert
+// ids (or -1 where another rank owns the slot).
+__global__ void __launch_bounds__(kThreads)
+    ep_scatter_kernel(const int32_t* __restrict__ topk, int T, int k, int El, int G,
+                      const int32_t* __restrict__ counts2, int32_t* __restrict__ send_off,
+                      int32_t* __restrict__ send_tok, int32_t* __restrict__ send_meta) {
+  const int d = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  __shared__ int s_base;
+  __shared__ int s_warp[32];
+  if (threadIdx.x == 0) {
+    int b = 0;
+    for (int i = 0; i < d; ++i) b += counts2[2 * i];
+    s_base = b;
+    send_off[d] = b;
+    if (d == G - 1) send_off[G] = b + counts2[2 * d];
+  }
+  __syncthreads();
+  int base = s_base;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int t0 = 0; t0 < T; t0 += blockDim.x) {
+    const int t = t0 + threadIdx.x;
+    bool hit = false;
+    if (t < T)
+      for (int j = 0; j < k; ++j) hit |= owns(topk[(int64_t)t * k + j], d, El);
+    const unsigned m = __ballot_sync(0xffffffffu, hit);
+    if (lane == 0) s_warp[warp] = __popc(m);
+    __syncthreads();
+    int woff = 0, tot = 0;
+    for (int w = 0; w < nwarps; ++w) {
+      woff += w < warp ? s_warp[w] : 0;
+      tot += s_warp[w];
+    }
+    if (hit) {
+      const int pos = base + woff + __popc(m & lt);
+      send_tok[pos] = t;
+      for (int j = 0; j < k; ++j) {
+        const int e = topk[(int64_t)t * k + j];
+        send_meta[(int64_t)pos * k + j] = owns(e, d, El) ? e - d * El : -1;
+      }
+    }
+    base += tot;
+    __syncthreads();
+  }
+}
+
+// dst[i] = src[idx[i]] for rows of row_bytes (multiple of 16), one warp per row.
+__global__ void gather_rows_kernel(const uint4* __restrict__ src, const int32_t* __restrict__ idx, int n,
+                                   int row_vec, uint4* __restrict__ dst) {
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += warps) {
+    const uint4* s = src + (int64_t)idx[i] * row_vec;
+    uint4* o = dst + (int64_t)i * row_vec;
+    for (int c = threadIdx.x & 31; c < row_vec; c += 32) o[c] = s[c];
+  }
+}
+
+__device__ __forceinline__ int segment_of(const int32_t* off, int G, int r) {
+  int s = 0;
+  while (s + 1 < G && off[s + 1] <= r) ++s;
+  return s;
+}
+
+// Expert side: CSR row i (received row r = token_idx[i], slot j = slot[i]) returns to the
+// source s owning r's segment of the receive buffer.  Position in the combine send buffer:
+// ret_off[s] + (running count within s, any order); meta = (r - recv_off[s]) * k + j lets the
+// source put the row back at (token, slot) whatever the order.
+__global__ void ep_combine_map_kernel(const int32_t* __restrict__ token_idx, const int32_t* __restrict__ slot,
+                                      int n, const int32_t* __restrict__ recv_off, const int32_t* __restrict__ ret_off,
+                                      int G, int k, int32_t* __restrict__ cursor, int32_t* __restrict__ row_map,
+                                      int32_t* __restrict__ ret_meta) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int r = token_idx[i];
+    const int s = segment_of(recv_off, G, r);
+    const int pos = ret_off[s] + atomicAdd(cursor + s, 1);
+    row_map[i] = pos;
+    ret_meta[pos] = (r - recv_off[s]) * k + slot[i];
+  }
+}
+
+// Source side: returned row i (from destination d = segment of i in ret_off) goes to
+// out[t * k + j] with t = send_tok[send_off[d] + meta / k], j = meta % k.  One warp per row.
+__global__ void ep_unpack_kernel(const uint4* __restrict__ rows, const int32_t* __restrict__ ret_meta, int n,
+                                 const int32_t* __restrict__ ret_off, const int32_t* __restrict__ send_off,
+                                 const int32_t* __restrict__ send_tok, int G, int k, int row_vec,
+                                 uint4* __restrict__ out) {
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += warps) {
+    const int d = segment_of(ret_off, G, i);
+    const int m = ret_meta[i];
+    const int t = send_tok[send_off[d] + m / k];
+    const uint4* s = rows + (int64_t)i * row_vec;
+    uint4* o = out + ((int64_t)t * k + m % k) * row_vec;
+    for (int c = threadIdx.x & 31; c < row_vec; c += 32) o[c] = s[c];
+  }
+}
+
+int grid_for(int64_t warps_needed) {
+  const int64_t b = (warps_needed + 7) / 8;
+  return (int)(b < 1 ? 1 : (b > 4 * 148 ? 4 * 148 : b));
+}
+
+}  // namespace
+
+extern "C" {
+
+moe_status moe_ep_dispatch_plan(const int32_t* topk, int64_t T, int32_t k, int32_t E, int32_t G,
+                                int32_t* counts2, int32_t* send_off, int32_t* send_tok, int32_t* send_meta,
+                                void* stream) {
+  moe::clear_error();
+  if (G < 1 || E < 1 || E % G || k < 1 || k > 32 || T < 0 || T * k >= INT_MAX)
+    MOE_FAIL(MOE_ERR_INVALID, "moe_ep_dispatch_plan: E=%d G=%d k=%d T=%lld", E, G, k, (long long)T);
+  if (!counts2 || !send_off || (T > 0 && (!topk || !send_tok || !send_meta)))
+    MOE_FAIL(MOE_ERR_INVALID, "moe_ep_dispatch_plan: null pointer");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int El = E / G;
+  ep_count_kernel<<<G, kThreads, 0, s>>>(topk, (int)T, k, El, counts2);
+  ep_scatter_kernel<<<G, kThreads, 0, s>>>(topk, (int)T, k, El, G, counts2, send_off, send_tok, send_meta);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) MOE_FAIL(MOE_ERR_CUDA, "moe_ep_dispatch_plan launch: %s", cudaGetErrorString(e));
+  return MOE_OK;
+}
+
+moe_status moe_gather_rows(const void* src, const int32_t* idx, int64_t n, int64_t row_bytes, void* dst,
+                           void* stream) {
+  moe::clear_error();
+  if (n == 0) return MOE_OK;
+  if (!src || !idx || !dst || n < 0 || n >= INT_MAX) MOE_FAIL(MOE_ERR_INVALID, "moe_gather_rows: bad argument");
+  if (row_bytes <= 0 || row_bytes % 16 || (reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15)
+    MOE_FAIL(MOE_ERR_INVALID, "moe_gather_rows: rows and pointers must be 16-byte multiples/aligned");
+  gather_rows_kernel<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(
+      (const uint4*)src, idx, (int)n, (int)(row_bytes / 16), (uint4*)dst);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) MOE_FAIL(MOE_ERR_CUDA, "moe_gather_rows launch: %s", cudaGetErrorString(e));
+  return MOE_OK;
+}
+
+moe_status moe_ep_combine_map(const int32_t* token_idx, const int32_t* slot, int64_t n, const int32_t* recv_off,
+                              const int32_t* ret_off, int32_t G, int32_t k, int32_t* cursor, int32_t* row_map,
+                              int32_t* ret_meta, void* stream) {
+  moe::clear_error();
+  if (n == 0) return MOE_OK;
+  if (!token_idx || !slot || !recv_off || !ret_off || !cursor || !row_map || !ret_meta || G < 1 || k < 1 ||
+      n < 0 || n >= INT_MAX)
+    MOE_FAIL(MOE_ERR_INVALID, "moe_ep_combine_map: bad argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(cursor, 0, sizeof(int32_t) * G, s);
+  if (e != cudaSuccess) MOE_FAIL(MOE_ERR_CUDA, "moe_ep_combine_map memset: %s", cudaGetErrorString(e));
+  const int blocks = (int)std::min<int64_t>((n + 255) / 256, 4 * 148);
+  ep_combine_map_kernel<<<blocks, 256, 0, s>>>(token_idx, slot, (int)n, recv_off, ret_off, G, k, cursor, row_map,
+                                               ret_meta);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) MOE_FAIL(MOE_ERR_CUDA, "moe_ep_combine_map launch: %s", cudaGetErrorString(e));
+  return MOE_OK;
+}
+
+moe_status moe_ep_unpack(const void* rows, const int32_t* ret_meta, int64_t n, const int32_t* ret_off,
+                         const int32_t* send_off, const int32_t* send_tok, int32_t G, int32_t k, int64_t row_bytes,
+                         void* out, void* stream) {
+  moe::clear_error();
+  if (n == 0) return MOE_OK;
+  if (!rows || !ret_meta || !ret_off || !send_off || !send_tok || !out || G < 1 || k < 1 || n < 0 || n >= INT_MAX)
+    MOE_FAIL(MOE_ERR_INVALID, "moe_ep_unpack: bad argument");
+  if (row_bytes <= 0 || row_bytes % 16 || (reinterpret_cast<uintptr_t>(rows) | reinterpret_cast<uintptr_t>(out)) & 15)
+    MOE_FAIL(MOE_ERR_INVALID, "moe_ep_unpack: rows and pointers must be 16-byte multiples/aligned");
+  ep_unpack_kernel<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(
+      (const uint4*)rows, ret_meta, (int)n, ret_off, send_off, send_tok, G, k, (int)(row_bytes / 16), (uint4*)out);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) MOE_FAIL(MOE_ERR_CUDA, "moe_ep_unpack launch: %s", cudaGetErrorString(e));
+  return MOE_OK;
+}
+
+}  // extern "C"

@@ -77,6 +77,7 @@ struct GemmArgs {
   int32_t a_mode;            // A staging: 0 = TMA tile::gather4, 1 = cp.async (LSU path), see DESIGN.md
   int32_t H;
   const __nv_bfloat16* X;
+  const int32_t* y_row_map;  // nullable: Y row of CSR row i is y_row_map[i] (EP combine buffer)
 };
 
 // Per-CTA counters written by the instrumented build (kProf = true).
@@ -449,7 +450,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const int grow = t.rt * kPairRows + (int)rank * kBM + q * 32 + lane;   // row within the task
       const bool valid = grow < t.rows;
-      const int64_t yrow = (int64_t)t.row0 + grow;
+      const int64_t yrow = a.y_row_map ? (int64_t)__ldg(a.y_row_map + t.row0 + min(grow, t.rows - 1))
+                                       : (int64_t)t.row0 + grow;
       const int n0 = t.ct * t.bn;
       const int col_end = min(n0 + t.bn, a.N);
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * kAccCols;
@@ -641,7 +643,8 @@ cudaError_t set_smem_attrs() {
 }
 
 static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, const int32_t* token_idx,
-                              const void* W, void* Y, int32_t y_dtype, void* stream, long long* prof) {
+                              const void* W, void* Y, int32_t y_dtype, void* stream, long long* prof,
+                              const int32_t* y_row_map = nullptr) {
   moe::clear_error();
   if (!plan) MOE_FAIL(MOE_ERR_INVALID, "moe_gemm: null plan");
   moe::BlobView v;
@@ -691,6 +694,7 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
   a.off_params = (int32_t)v.off_params;
   a.w4d = w4d ? 1 : 0;
   a.prof = prof;
+  a.y_row_map = y_row_map;
   a.T = (int32_t)T;
   a.H = v.H;
   a.X = reinterpret_cast<const __nv_bfloat16*>(X);
@@ -740,6 +744,12 @@ extern "C" {
 moe_status moe_gemm(const moe_plan* plan, const void* X, int64_t T, const int32_t* token_idx, const void* W,
                     void* Y, int32_t y_dtype, void* stream) {
   return gemm_launch(plan, X, T, token_idx, W, Y, y_dtype, stream, nullptr);
+}
+
+moe_status moe_gemm_rowmap(const moe_plan* plan, const void* X, int64_t T, const int32_t* token_idx,
+                           const void* W, void* Y, int32_t y_dtype, const int32_t* y_row_map, void* stream) {
+  if (!y_row_map) MOE_FAIL(MOE_ERR_INVALID, "moe_gemm_rowmap: null y_row_map");
+  return gemm_launch(plan, X, T, token_idx, W, Y, y_dtype, stream, nullptr, y_row_map);
 }
 
 moe_status moe_gemm_profile(const moe_plan* plan, const void* X, int64_t T, const int32_t* token_idx,

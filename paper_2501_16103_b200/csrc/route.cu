@@ -8,7 +8,8 @@
 //   kernel 2 (grid E): row_off[e] = sum_{e' < e} counts[e'];
 //                      token_idx[row_off[e] + r] = r-th token routed to e,
 //                      ranks from a block-wide ballot/popcount scan over t.
-// Invalid entries (id outside [0, E), or an id repeated later in the same
+// Negative ids are masked slots (e.g. slots owned by another rank in expert parallelism)
+// and are skipped silently.  Invalid entries (id >= E, or an id repeated later in the same
 // token's list) are dropped by both kernels and reported in *status.
 #include <cuda_runtime.h>
 
@@ -21,13 +22,16 @@ namespace {
 constexpr int kCountThreads = 512;
 constexpr int kScatterThreads = 1024;
 
-__device__ __forceinline__ bool entry_valid(const int32_t* row, int j, int E) {
+// 1: a valid slot; 0: a masked slot (negative id); -1: invalid (id >= E or a duplicate).
+__device__ __forceinline__ int classify(const int32_t* row, int j, int E) {
   const int x = row[j];
-  if (x < 0 || x >= E) return false;
+  if (x < 0) return 0;
+  if (x >= E) return -1;
   for (int i = 0; i < j; ++i)
-    if (row[i] == x) return false;
-  return true;
+    if (row[i] == x) return -1;
+  return 1;
 }
+__device__ __forceinline__ bool entry_valid(const int32_t* row, int j, int E) { return classify(row, j, E) == 1; }
 
 __global__ void __launch_bounds__(kCountThreads) route_count_kernel(const int32_t* __restrict__ topk, int T, int k,
                                                                     int E, int32_t* __restrict__ counts,
@@ -38,9 +42,9 @@ __global__ void __launch_bounds__(kCountThreads) route_count_kernel(const int32_
   for (int t = threadIdx.x; t < T; t += blockDim.x) {
     const int32_t* row = topk + (int64_t)t * k;
     for (int j = 0; j < k; ++j) {
-      const bool ok = entry_valid(row, j, E);
-      c += ok && row[j] == e;
-      bad |= !ok;
+      const int cl = classify(row, j, E);
+      c += cl == 1 && row[j] == e;
+      bad |= cl < 0;
     }
   }
   // block reduction

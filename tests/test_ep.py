@@ -1,0 +1,141 @@
+"""Expert-parallel path: exchange logic over gloo (CPU, world size 2, real torch.distributed),
+G virtual ranks in one process, and the CUDA kernels on one GPU (virtual ranks and a
+world-size-1 NCCL group).  Reference: the P:90 per-(token, slot) definition in the oracle."""
+import os
+import socket
+import threading
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+import synth
+from oracle import moe as omoe
+from paper_2501_16103_b200.ep import ExpertParallelMoE, ThreadComm, TorchComm
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _problem(G, E=8, k=2, T_l=12, H=16, N=24, seed=0):
+    T = G * T_l
+    ids = synth.route_gumbel(seed, T, E, k)
+    X = synth.make_x(seed, T, H, "int")
+    W = synth.make_w(seed, E, H, N, "int")
+    return ids, X, W, omoe.per_slot_outputs(ids, X, W)
+
+
+def _cpu_kernels():
+    import sys
+    sys.path.insert(0, HERE)
+    from ep_doubles import CpuKernels
+    return CpuKernels()
+
+
+def _gloo_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ids, X, W, ref = _problem(world)
+        T_l, El = ids.shape[0] // world, W.shape[0] // world
+        sl = slice(rank * T_l, (rank + 1) * T_l)
+        moe = ExpertParallelMoE(W.shape[0], torch.from_numpy(W[rank * El:(rank + 1) * El]).float(), TorchComm(),
+                                out_dtype=torch.float32, kernels=_cpu_kernels())
+        out = moe.forward(torch.from_numpy(ids[sl]), torch.from_numpy(X[sl]).float())
+        q.put((rank, bool(np.array_equal(out.double().numpy(), ref[rank * T_l * 2:(rank + 1) * T_l * 2])),
+               moe.last))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_ep_exchange_gloo_world2():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok, _ in res), res
+    # conservation: rows sent by one rank are the rows received by the other
+    last = {r: l for r, _, l in res}
+    assert last[0]["send_rows"][1] == last[1]["recv_rows"][0]
+    assert last[0]["ret_rows"] == [last[g]["back_rows"][0] for g in range(2)]
+
+
+def _run_virtual(G, kernels_fn, device, out_dtype, E=8, k=2, T_l=12, H=16, N=24, seed=0):
+    ids, X, W, ref = _problem(G, E, k, T_l, H, N, seed)
+    El = E // G
+    comm = ThreadComm(G)
+    outs, errs = [None] * G, []
+
+    def body(r):
+        try:
+            comm.bind(r)
+            Wl = torch.from_numpy(W[r * El:(r + 1) * El])
+            Xl = torch.from_numpy(X[r * T_l:(r + 1) * T_l])
+            if device == "cuda":
+                Wl, Xl = Wl.to(torch.bfloat16).cuda(), Xl.to(torch.bfloat16).cuda()
+            else:
+                Wl, Xl = Wl.float(), Xl.float()
+            moe = ExpertParallelMoE(E, Wl, comm, out_dtype=out_dtype, kernels=kernels_fn())
+            outs[r] = moe.forward(torch.from_numpy(ids[r * T_l:(r + 1) * T_l]).to(device), Xl).cpu()
+        except Exception as e:  # pragma: no cover
+            errs.append(repr(e))
+            comm._bar.abort()
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(G)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    assert not errs, errs
+    got = torch.cat(outs).double().numpy()
+    return got, ref
+
+
+@pytest.mark.parametrize("G", [1, 2, 4])
+def test_ep_exchange_virtual_ranks_cpu(G):
+    got, ref = _run_virtual(G, _cpu_kernels, "cpu", torch.float32)
+    assert np.array_equal(got, ref)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("G", [1, 2, 4, 8])
+def test_ep_cuda_kernels_virtual_ranks(G):
+    from paper_2501_16103_b200.ep import CudaKernels
+    got, ref = _run_virtual(G, CudaKernels, "cuda", torch.float32, E=8, k=2, T_l=40, H=64, N=136)
+    assert np.array_equal(got, ref)
+
+
+@pytest.mark.gpu
+def test_ep_cuda_skewed_and_large():
+    """Zipf routing with empty experts: some ranks receive nothing for some experts."""
+    from paper_2501_16103_b200.ep import CudaKernels
+    got, ref = _run_virtual(4, CudaKernels, "cuda", torch.float32, E=16, k=4, T_l=300, H=128, N=256, seed=3)
+    assert np.array_equal(got, ref)
+
+
+@pytest.mark.gpu
+def test_ep_nccl_world1():
+    """The real NCCL collective path (a world of one rank on one GPU)."""
+    import torch.distributed as dist
+    from paper_2501_16103_b200.ep import CudaKernels
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        ids, X, W, ref = _problem(1, E=8, k=2, T_l=64, H=64, N=128)
+        moe = ExpertParallelMoE(8, torch.from_numpy(W).to(torch.bfloat16).cuda(), TorchComm(),
+                                out_dtype=torch.float32, kernels=CudaKernels())
+        out = moe.forward(torch.from_numpy(ids).cuda(), torch.from_numpy(X).to(torch.bfloat16).cuda())
+        assert np.array_equal(out.cpu().double().numpy(), ref)
+    finally:
+        dist.destroy_process_group()
