@@ -360,6 +360,123 @@ def run_ours(args, cfg):
         torch.distributed.destroy_process_group()
 
 
+# ---------------------------------------------------------------------------
+# multi-GPU: expert parallelism (one process per GPU, NCCL all-to-all dispatch / combine)
+# ---------------------------------------------------------------------------
+def run_ep(args, base):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2501_16103_b200 as M
+    from paper_2501_16103_b200.ep import ExpertParallelMoE, TorchComm
+
+    for k_, v_ in (("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", "29531"), ("RANK", "0"), ("WORLD_SIZE", "1")):
+        os.environ.setdefault(k_, v_)                 # `--ep` on one GPU without torchrun
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    M.moe_device_info()
+    peaks, peak_src = load_peaks()
+    out_dtype = torch.bfloat16 if args.out_dtype == "bf16" else torch.float32
+    strong = base.name == "ep"                      # BASELINE configs[4]: total T fixed across N
+    T_total = base.T if strong else base.T * ws     # otherwise weak scaling: T per GPU fixed
+    if base.E % ws or T_total % ws:
+        raise SystemExit(f"E={base.E} and T={T_total} must be divisible by {ws} ranks")
+    cfg = synth.Config(f"{base.name}-ep{ws}", E=base.E, k=base.k, T=T_total, H=base.H, N=base.N,
+                       routing=base.routing, zipf_s=base.zipf_s, n_empty=base.n_empty)
+    ids = synth.route(cfg, args.seed)               # the global batch (identical on every rank)
+    T_l, El = T_total // ws, cfg.E // ws
+    topk_l = torch.from_numpy(np.ascontiguousarray(ids[rank * T_l:(rank + 1) * T_l])).to(dev)
+    X_l = synth.counter_values_torch(args.seed, synth.workloads.STREAM_X, rank * T_l * cfg.H, T_l * cfg.H,
+                                     "normal", 6, dev).reshape(T_l, cfg.H)
+    W_l = synth.make_w_torch(args.seed, cfg.E, cfg.H, cfg.N, device=dev, experts=range(rank * El, (rank + 1) * El))
+    moe = ExpertParallelMoE(cfg.E, W_l, TorchComm(), bm=args.bm, bn=args.bn, out_dtype=out_dtype)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        moe.forward(topk_l, X_l)
+    torch.cuda.synchronize()
+    moe.time_gemm = True
+    step_ms, gemm_ms, local_rows = [], [], []
+    dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            moe.forward(topk_l, X_l)
+            s1.record(stream)
+            s1.synchronize()
+            step_ms.append(s0.elapsed_time(s1))
+            gemm_ms.append(moe.gemm_events[0].elapsed_time(moe.gemm_events[1]))
+            local_rows.append(moe.last["local_rows"])
+    torch.cuda.synchronize()
+    dist.barrier()
+    t = torch.tensor([sum(step_ms)], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    value = cfg.flops * args.steps / (float(t.item()) * 1e-3) / 1e12
+    gemm_avg = statistics.mean(gemm_ms)
+    flops_l = 2 * local_rows[-1] * cfg.H * cfg.N
+    achieved = flops_l / (gemm_avg * 1e-3) / 1e12
+    peak = float(peaks["bf16_tflops"])
+    per_rank = torch.tensor([statistics.mean(step_ms), gemm_avg, achieved], device=dev)
+    gathered = [torch.zeros_like(per_rank) for _ in range(ws)]
+    dist.all_gather(gathered, per_rank)
+    # e2e: the rank's X / top-k ids from pinned host memory, result rows back to the host
+    e2e = None
+    if not args.no_e2e:
+        X_h = X_l.cpu().pin_memory()
+        ids_h = topk_l.cpu().pin_memory()
+        out0 = moe.forward(topk_l, X_l)
+        out_h = torch.empty(out0.shape, dtype=out0.dtype).pin_memory()
+        Xe, te = torch.empty_like(X_l), torch.empty_like(topk_l)
+        e_ms = []
+        for i in range(2 + max(3, min(args.steps, 10))):
+            flush.zero_()
+            dist.barrier()
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            Xe.copy_(X_h, non_blocking=True)
+            te.copy_(ids_h, non_blocking=True)
+            out_h.copy_(moe.forward(te, Xe), non_blocking=True)
+            s1.record(stream)
+            s1.synchronize()
+            if i >= 2:
+                e_ms.append(s0.elapsed_time(s1))
+        te_max = torch.tensor([sum(e_ms)], device=dev)
+        dist.all_reduce(te_max, op=dist.ReduceOp.MAX)
+        e2e = {"value": cfg.flops * len(e_ms) / (float(te_max.item()) * 1e-3) / 1e12, "unit": "TFLOP/s",
+               "h2d_bytes_per_step": int(X_h.numel() * 2 + ids_h.numel() * 4) * ws,
+               "d2h_bytes_per_step": int(out_h.numel() * out_h.element_size()) * ws}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": float(t.item()) / args.steps, "higher_is_better": True,
+            "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"{cfg.name}: E={cfg.E} top-{cfg.k} T={cfg.T} ({T_l}/rank) H={cfg.H} N={cfg.N} "
+                                   f"routing={cfg.routing} seed={args.seed}",
+                       "tile": f"{moe.kernels._plans[('ep', args.bm, args.bn)].bm}x{args.bn}",
+                       "out_dtype": args.out_dtype, "global_batch": cfg.T, "parallelism": f"ep{ws}",
+                       "collectives": "NCCL all_to_all_single (torch.distributed): counts, dispatch rows, "
+                                      "combine rows", "l2": "flushed before every timed step"},
+            "pct_of_peak": value / (peak * ws),
+            "per_rank": [{"ms_per_step": float(g[0]), "gemm_ms": float(g[1]), "gemm_tflops": float(g[2])}
+                         for g in gathered],
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "peak_source": f"{peak_src} bf16_tflops (rank 0's GEMM launch)",
+                         "algorithmic_flops_per_launch": flops_l},
+            "cpu_baseline": None,
+            "e2e": e2e,
+            "gpu_launches": 9 * args.steps,   # dispatch 2, gather 1, route 2, plan 1, combine map 1, GEMM 1, unpack 1
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -373,14 +490,18 @@ def main():
     ap.add_argument("--out-dtype", choices=["bf16", "f32"], default="bf16")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--host-plan", action="store_true", help="plan on the host (counts D2H) instead of on the device")
+    ap.add_argument("--ep", action="store_true", help="run the expert-parallel path even on one GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")
     cfg = synth.CONFIGS[args.config]
+    ws = dist_env()[0]
     if args.impl == "reference":
         run_reference(args, cfg)
+    elif ws > 1 or args.ep:
+        run_ep(args, cfg)
     else:
         run_ours(args, cfg)
 

@@ -122,6 +122,8 @@ class ExpertParallelMoE:
         self.bm, self.bn, self.out_dtype = bm, bn, out_dtype
         self.kernels = kernels if kernels is not None else CudaKernels()
         self.last = {}
+        self.time_gemm = False        # bench: record CUDA events around the GEMM launch
+        self.gemm_events = None
 
     def forward(self, topk_local, X_local):
         """topk_local [T_l, k] int32 global expert ids, X_local [T_l, H] bf16 -> out [T_l * k, N]."""
@@ -149,7 +151,13 @@ class ExpertParallelMoE:
         ret_off = _excl(recv2[:, 1])
         row_map, ret_meta = K.combine_map(tok_l, slot_l, recv_off, ret_off, G, k)
         Ysend = torch.empty((Rr, N), dtype=self.out_dtype, device=dev)
+        if self.time_gemm:
+            ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            ev[0].record()
         K.gemm(("ep", self.bm, self.bn), counts_l, Xr, tok_l, self.W, Ysend, row_map, self.bm, self.bn)
+        if self.time_gemm:
+            ev[1].record()
+            self.gemm_events = ev
         # combine
         Yb = torch.empty((B, N), dtype=self.out_dtype, device=dev)
         Mb = torch.empty(B, dtype=torch.int32, device=dev)

@@ -263,17 +263,20 @@ def make_x_torch(seed: int, T: int, H: int, mode: str = "normal", device="cpu"):
     return counter_values_torch(seed, STREAM_X, 0, T * H, mode, _shift_x(), device).reshape(T, H)
 
 
-def make_w_torch(seed: int, E: int, H: int, N: int, mode: str = "normal", device="cpu", chunk=1 << 26):
+def make_w_torch(seed: int, E: int, H: int, N: int, mode: str = "normal", device="cpu", chunk=1 << 26,
+                 experts: range | None = None):
+    """W [E, H, N] (or the contiguous expert range `experts` of it, e.g. one EP rank's share)."""
     import torch
 
+    ex = range(E) if experts is None else experts
     if mode == "identity":
         if H != N:
             raise ValueError("identity mode needs H == N")
         eye = torch.eye(H, device=device, dtype=torch.float32)
-        return torch.stack([(e + 1) * eye for e in range(E)]).to(torch.bfloat16)
-    total = E * H * N
+        return torch.stack([(e + 1) * eye for e in ex]).to(torch.bfloat16)
+    start, total = ex.start * H * N, len(ex) * H * N
     out = torch.empty(total, dtype=torch.bfloat16, device=device)
     for s in range(0, total, chunk):
         n = min(chunk, total - s)
-        out[s:s + n] = counter_values_torch(seed, STREAM_W, s, n, mode, _shift_w(H), device)
-    return out.reshape(E, H, N)
+        out[s:s + n] = counter_values_torch(seed, STREAM_W, start + s, n, mode, _shift_w(H), device)
+    return out.reshape(len(ex), H, N)

@@ -47,6 +47,7 @@ def test_numpy_torch_twins_identical(mode):
     w = synth.make_w(7, 3, 64, 40, mode)
     wt = synth.make_w_torch(7, 3, 64, 40, mode, chunk=1000)
     assert np.array_equal(w, wt.double().numpy())
+    assert np.array_equal(synth.make_w_torch(7, 3, 64, 40, mode, experts=range(1, 3)).double().numpy(), w[1:3])
     # column/row fetchers agree with the full arrays
     assert np.array_equal(wl.w_columns(7, 3, 64, 40, 2, np.array([0, 39]), mode), w[2][:, [0, 39]])
     assert np.array_equal(wl.x_rows(7, 33, 64, [5, 32], mode), x[[5, 32]])
