@@ -53,6 +53,11 @@ typedef int32_t moe_status;
 /* Plan flags. */
 #define MOE_PAD_MAX     0u  /* pad TilePrefix with INT32_MAX ("the maximum possible value") */
 #define MOE_PAD_REPEAT  1u  /* pad TilePrefix by repeating its last element                */
+#define MOE_SPLIT_TAIL  2u  /* bm = bn = 256: an expert whose m is not a multiple of 256 is kind 1 —
+                               the LAST row tile of each column block (its m mod 256 tail rows) runs
+                               as a swap-AB pair tile (W block as the M = 256 operand, the tail's
+                               tokens as N = tail rounded up to 16).  Same tile partition; a second
+                               tiling strategy in the launch (Alg. 3 with K = 2).        */
 
 /* ---- the compressed mapping ("plan blob"), int32 words -------------------
  * Built on the host by moe_plan_build (no GPU needed) and copied once to the
@@ -70,7 +75,8 @@ typedef int32_t moe_status;
  *   [16+2*M_pad .. +8*n_tasks)     task parameters p_i, 8 words per
  *                                  task i: {expert, row0, rows, kind, bm, bn,
  *                                  row_tiles, col_tiles}; row0 = first CSR row of
- *                                  the task (= row_off[expert] + offset in expert)
+ *                                  the task (= row_off[expert] + offset in expert);
+ *                                  kind 1 (MOE_SPLIT_TAIL): last row tile is swap-AB
  *   [.. +E+1)                      row_off: exclusive prefix of counts (CSR offsets)
  * nu(task) = row_tiles * col_tiles, row_tiles = ceil(rows/BM), col_tiles = ceil(N/BN).
  * Intra-task tile order: row tile fastest, rt = l mod row_tiles, ct = l div
@@ -92,9 +98,9 @@ int64_t moe_plan_blob_words(int32_t E);
  *                    CTA 128 rows and half of the W block).  16 <= bn <= 256, bn % 16 == 0
  *                    (bn % 32 == 0 when bm = 256).  bm = 0: automatic — 256 unless the pair
  *                    tiles' extra padding rows exceed their ~10% per-row speed advantage
- *                    (sum of ceil(m_e/256)*256 > 1.10 * sum of ceil(m_e/128)*128).  The
- *                    blob records the resolved bm.
- *   flags            MOE_PAD_MAX | MOE_PAD_REPEAT.
+ *                    (sum of ceil(m_e/256)*256 > 1.10 * sum of ceil(m_e/128)*128).  The blob
+ *                    records the resolved bm.
+ *   flags            MOE_PAD_MAX | MOE_PAD_REPEAT, optionally | MOE_SPLIT_TAIL.
  *   blob, blob_cap   caller buffer of blob_cap int32 words (see moe_plan_blob_words).
  *   blob_len         out: words written.
  * Returns MOE_OK, MOE_OK_EMPTY (all experts empty: M = 0, total = 0),

@@ -69,17 +69,23 @@ def tiles_of(rows: int, N: int, bm: int, bn: int) -> int:
     return ceil_div(rows, bm) * ceil_div(N, bn)
 
 
-def make_tasks(counts, bm: int, bn: int) -> list[dict]:
-    """One task per expert, kind 0 with tile bm x bn."""
-    return [dict(expert=e, row_begin=0, rows=int(m), bm=bm, bn=bn, kind=0) for e, m in enumerate(counts)]
+def make_tasks(counts, bm: int, bn: int, split_tail: bool = False) -> list[dict]:
+    """One task per expert with tile bm x bn.
+
+    split_tail (R6): the mapping is unchanged, but an expert whose m is not a
+    multiple of bm gets kind 1 — its LAST row tile (rows [floor(m/bm)*bm, m)) is executed by a
+    second tiling strategy (Alg. 3 with K = 2): a swap-AB tile whose height is the
+    tail rounded up to 16.  The tile partition, hence Y, is identical."""
+    return [dict(expert=e, row_begin=0, rows=int(m), bm=bm, bn=bn,
+                 kind=1 if (split_tail and int(m) % bm) else 0) for e, m in enumerate(counts)]
 
 
 def plan(counts, N: int, bm: int, bn: int, pad_mode: str = "max", warp_size: int = 32,
-         tasks: list[dict] | None = None) -> dict:
+         tasks: list[dict] | None = None, split_tail: bool = False) -> dict:
     """Host-side plan: nu per task, sigma (non-empty tasks, natural order), TilePrefix
     (Alg. 1 over eta), padded per P:203."""
     if tasks is None:
-        tasks = make_tasks(counts, bm, bn)
+        tasks = make_tasks(counts, bm, bn, split_tail)
     nu = [tiles_of(t["rows"], N, t["bm"], t["bn"]) for t in tasks]
     sigma, prefix = mapping.nonempty_stage(nu)
     padded = mapping.pad_tile_prefix(prefix, warp_size, pad_mode) if prefix else []
@@ -104,7 +110,9 @@ def decode(pl: dict, row_off, B: int) -> dict:
     r1 = int(row_off[e]) + task["row_begin"] + min((rt + 1) * task["bm"], task["rows"])
     c0 = ct * task["bn"]
     c1 = min(c0 + task["bn"], pl["N"])
-    return dict(h=h, task=j, expert=e, l=l, rt=rt, ct=ct, rows=(r0, r1), cols=(c0, c1), kind=task["kind"])
+    kind = 1 if (task["kind"] == 1 and rt == R - 1) else 0          # the tail tile of a split task
+    return dict(h=h, task=j, expert=e, l=l, rt=rt, ct=ct, rows=(r0, r1), cols=(c0, c1), kind=kind,
+                height=-(-(r1 - r0) // 16) * 16 if kind == 1 else task["bm"])
 
 
 def tile_cover(pl: dict, row_off, n_rows: int) -> np.ndarray:

@@ -14,12 +14,13 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmoe_sm100.so")
+# MOE_LIB: load another build of the same C ABI (same-box A/B timing of kernel revisions).
+LIB_PATH = os.environ.get("MOE_LIB") or os.path.join(HERE, "libmoe_sm100.so")
 
 MOE_OK, MOE_OK_EMPTY = 0, 1
 MOE_ERR = {-1: "INVALID", -2: "UNSUPPORTED", -3: "CAPACITY", -4: "CUDA", -5: "NCCL"}
 MOE_DTYPE_BF16, MOE_DTYPE_F32 = 0, 1
-MOE_PAD_MAX, MOE_PAD_REPEAT = 0, 1
+MOE_PAD_MAX, MOE_PAD_REPEAT, MOE_SPLIT_TAIL = 0, 1, 2
 MOE_PLAN_MAGIC = 0x4D4F4531
 MOE_PLAN_HEADER = 16
 MOE_PLAN_TASK_WORDS = 8

@@ -120,8 +120,11 @@ __device__ __forceinline__ void map_tile(const int32_t* prefix, const int32_t* s
 
 struct Tile {
   int expert, row0, rows, bn, rt, ct;
+  int kind;     // of THIS tile: 0 = bm rows x bn cols; 1 = swap-AB tail tile (MOE_SPLIT_TAIL)
+  int height;   // kind 1: tail rows rounded up to 16 (the MMA's N)
 };
 
+template <bool kSplit = false>
 __device__ __forceinline__ Tile load_tile(const int32_t* params, int task, int l) {
   const int4 pa = __ldg(reinterpret_cast<const int4*>(params + task * MOE_PLAN_TASK_WORDS));
   const int4 pb = __ldg(reinterpret_cast<const int4*>(params + task * MOE_PLAN_TASK_WORDS + 4));
@@ -132,6 +135,18 @@ __device__ __forceinline__ Tile load_tile(const int32_t* params, int task, int l
   t.bn = pb.y;
   t.rt = l % pb.z;   // row tile fastest (R5)
   t.ct = l / pb.z;
+  t.kind = 0;
+  t.height = pb.x;
+  if constexpr (kSplit) {
+    // MOE_SPLIT_TAIL: a kind-1 task runs its last row tile (rows [rt*bm, rows)) swap-AB.
+    if (pa.w == 1 && t.rt == pb.z - 1) {
+      const int tail = t.rows - t.rt * pb.x;
+      t.kind = 1;
+      t.height = (tail + 15) / 16 * 16;
+      t.row0 += t.rt * pb.x;                       // kind 1: row0 / rows are the tail's
+      t.rows = tail;
+    }
+  }
   return t;
 }
 
@@ -181,27 +196,33 @@ __device__ __forceinline__ void wait_timed(uint32_t bar, uint32_t parity, long l
 
 // Pipeline geometry per CTA-group size: a CTA pair (cta_group::2) splits the B block across the
 // two CTAs, so a stage is 32 KB instead of 48 KB and six stages fit.
-template <int kCta>
+template <int kCta, bool kSplit = false>
 struct Geo {
   static constexpr int kStages = kCta == 2 ? 6 : 4;
   static_assert(8 * (2 * kStages + 4) + 4 <= kBarBytes, "barrier block overlaps TilePrefix");
   static constexpr int kBStage = kBStageBytes / kCta;            // bytes of W per CTA per stage
-  static constexpr size_t kSmem = 1024 + (size_t)kStages * (kABytes + kBStage) + kBarBytes;
+  // CTA pairs: a 4 KB transpose buffer per epilogue warp for swap-AB tail tiles (MOE_SPLIT_TAIL).
+  static constexpr int kEpiStage = kSplit ? kEpiWarps * 32 * 32 * 4 : 0;
+  static constexpr size_t kSmem = 1024 + (size_t)kStages * (kABytes + kBStage) + kEpiStage + kBarBytes;
 };
 
-template <bool kProf, int kCta>
+// kSplit: the plan carries MOE_SPLIT_TAIL (kind-1 tail tiles exist); a separate instantiation so
+// the plain path carries none of the swap-AB code.
+template <bool kProf, int kCta, bool kSplit>
 __global__ void __launch_bounds__(kThreads, 1)
     moe_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
                     const GemmArgs a) {
-  constexpr int kSt = Geo<kCta>::kStages;
-  constexpr int kBSt = Geo<kCta>::kBStage;
+  static_assert(!kSplit || kCta == 2, "swap-AB tail tiles need CTA pairs (M = 256)");
+  constexpr int kSt = Geo<kCta, kSplit>::kStages;
+  constexpr int kBSt = Geo<kCta, kSplit>::kBStage;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;            // SW128 atoms need 1024-byte alignment
   uint8_t* smem = smem_raw + (base - raw);
   const uint32_t sA = base;
   const uint32_t sB = sA + kSt * kABytes;
-  const uint32_t sBar = sB + kSt * kBSt;
+  const uint32_t sEpi = sB + kSt * kBSt;                   // swap-AB transpose buffers (pairs)
+  const uint32_t sBar = sEpi + Geo<kCta, kSplit>::kEpiStage;
   auto full_bar = [&](int s) { return sBar + 8u * s; };
   auto empty_bar = [&](int s) { return sBar + 8u * (kSt + s); };
   auto tfull_bar = [&](int i) { return sBar + 8u * (2 * kSt + i); };
@@ -269,9 +290,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int v = pair_id; v < total; v += n_pairs) {
       int h, task, l;
       map_tile(s_prefix, s_sigma, a.M_pad, v, h, task, l);
-      const Tile t = load_tile(params, task, l);
-      const int rbeg = t.rt * kPairRows + (int)rank * kBM;
-      const int nvalid = min(kBM, t.rows - rbeg);   // may be <= 0 for the second CTA of a pair tile
+      const Tile t = load_tile<kSplit>(params, task, l);
+      // kind 0: this CTA's 128 rows of the tile; kind 1 (swap-AB tail): this CTA's half of the
+      // tail's `height` token rows, which the MMA reads as its N operand.
+      const int n_alloc = kSplit && t.kind == 1 ? t.height / kCta : kBM;
+      const int rbeg = kSplit && t.kind == 1 ? (int)rank * n_alloc : t.rt * kPairRows + (int)rank * kBM;
+      const int nvalid = min(n_alloc, t.rows - rbeg);   // may be <= 0 for the second CTA of a pair tile
       const int32_t* idx = a.token_idx + t.row0;
       if (a_mode == 0) {
         // Rows past the task's end repeat its last valid token (their results are never stored).
@@ -328,7 +352,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int v = pair_id; v < total; v += n_pairs) {
       int h, task, l;
       map_tile(s_prefix, s_sigma, a.M_pad, v, h, task, l);
-      const Tile t = load_tile(params, task, l);
+      const Tile t = load_tile<kSplit>(params, task, l);
       const int bnc = t.bn / kCta;                  // columns of the block staged by this CTA
       const int n0 = t.ct * t.bn + (int)rank * bnc;
       const int nbox = (bnc + 63) >> 6;
@@ -377,8 +401,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++n_tiles;
         int h, task, l;
         map_tile(s_prefix, s_sigma, a.M_pad, v, h, task, l);
-        const int bn = __ldg(params + task * MOE_PLAN_TASK_WORDS + 5);
-        const uint32_t idesc = idesc_bf16_f32(kPairRows, bn, /*A K-major*/ 0, /*B MN-major*/ 1);
+        const Tile t = load_tile<kSplit>(params, task, l);
+        const bool swap = kSplit && t.kind == 1;
+        // kind 0: D[tokens, cols] = A[tokens (K-major)] * B[W block (MN-major)], N = bn.
+        // kind 1: D[cols, tokens] = A[W block as MN-major M-operand] * B[tail tokens (K-major)],
+        //         M = the pair's 256 output columns, N = the tail height (swap-AB).
+        const uint32_t idesc = swap ? idesc_bf16_f32(kPairRows, t.height, /*A MN-major*/ 1, /*B K-major*/ 0)
+                                    : idesc_bf16_f32(kPairRows, t.bn, /*A K-major*/ 0, /*B MN-major*/ 1);
         wait_timed<kProf>(tempty_bar(acc), acc_phase ^ 1u, c_tmem);     // epilogue(s) drained this accumulator
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * kAccCols;
@@ -390,15 +419,25 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (lane == 0) {
             const uint32_t a0 = sA + s * kABytes;
             const uint32_t b0 = sB + s * kBSt;
+            // Token rows: K-major SW128, 8-row groups 1024 B apart; K step of 16 = +32 B in the row.
+            // W block: MN-major SW128; 64-wide chunks 8 KB apart (LBO), 8-row K groups 1 KB apart
+            // (SBO); K step of 16 rows = +2 KB.  The two kinds only swap the operand roles.
+            if (!kSplit || !swap) {
 #pragma unroll
-            for (int kk = 0; kk < kBK / 16; ++kk) {
-              // A: K-major SW128, 8-row groups 1024 B apart; K step of 16 = +32 B in the row.
-              const uint64_t ad = smem_desc_sw128(a0 + kk * 32, 16, 1024);
-              // B: MN-major SW128; 64-wide N chunks 8 KB apart (LBO), 8-row K groups 1 KB apart
-              // (SBO); K step of 16 rows = +2 KB.
-              const uint64_t bd = smem_desc_sw128(b0 + kk * 2048, kBBoxBytes, 1024);
-              if constexpr (kCta == 2) mma_bf16_pair(d_tmem, ad, bd, idesc, (kb | kk) != 0);
-              else mma_bf16(d_tmem, ad, bd, idesc, (kb | kk) != 0);
+              for (int kk = 0; kk < kBK / 16; ++kk) {
+                const uint64_t ad = smem_desc_sw128(a0 + kk * 32, 16, 1024);
+                const uint64_t bd = smem_desc_sw128(b0 + kk * 2048, kBBoxBytes, 1024);
+                if constexpr (kCta == 2) mma_bf16_pair(d_tmem, ad, bd, idesc, (kb | kk) != 0);
+                else mma_bf16(d_tmem, ad, bd, idesc, (kb | kk) != 0);
+              }
+            } else {
+#pragma unroll
+              for (int kk = 0; kk < kBK / 16; ++kk) {
+                const uint64_t ad = smem_desc_sw128(b0 + kk * 2048, kBBoxBytes, 1024);
+                const uint64_t bd = smem_desc_sw128(a0 + kk * 32, 16, 1024);
+                if constexpr (kCta == 2) mma_bf16_pair(d_tmem, ad, bd, idesc, (kb | kk) != 0);
+                else mma_bf16(d_tmem, ad, bd, idesc, (kb | kk) != 0);
+              }
             }
             if constexpr (kCta == 2) mma_commit_pair(empty_bar(s), 0x3);  // frees the slot in both CTAs
             else mma_commit(empty_bar(s));
@@ -444,10 +483,57 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int v = pair_id; v < total; v += n_pairs) {
       int h, task, l;
       map_tile(s_prefix, s_sigma, a.M_pad, v, h, task, l);
-      const Tile t = load_tile(params, task, l);
+      const Tile t = load_tile<kSplit>(params, task, l);
       wait_timed<kProf>(tfull_bar(acc), acc_phase, c_wait);
       const long long w0 = kProf ? clock64() : 0;
       tc_fence_after();
+      if (kSplit && t.kind == 1) {
+        // Swap-AB tail: TMEM lane = output column, TMEM column = tail token.
+        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * kAccCols;
+        // Transpose each 32 (columns) x 32 (tokens) block through this warp's smem buffer, then
+        // write token rows with 16-byte stores (a warp covers 32 columns of 4 (fp32) / 8 (bf16) rows).
+        uint8_t* buf = smem + (sEpi - base) + (warp - (kMmaWarp + 1)) * (32 * 32 * 4);
+        const int esz = a.y_f32 ? 4 : 2;
+        const int col0 = t.ct * t.bn + (int)rank * (t.bn / kCta) + q * 32;   // this warp's 32 columns
+        for (int c = 0; c < t.height; c += 32) {
+          uint32_t r[32];
+          tmem_ld32(taddr + c, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {              // token c+j, column lane -> buf[j][lane]
+            if (a.y_f32)
+              reinterpret_cast<uint32_t*>(buf)[j * 32 + lane] = r[j];
+            else
+              reinterpret_cast<__nv_bfloat16*>(buf)[j * 32 + lane] = __float2bfloat16_rn(__uint_as_float(r[j]));
+          }
+          __syncwarp();
+          const int vec_per_row = 32 * esz / 16;      // 16-byte pieces per 32-column row segment
+          const int rows_per_pass = 32 / vec_per_row;
+          for (int j0 = 0; j0 < 32; j0 += rows_per_pass) {
+            const int j = j0 + lane / vec_per_row, piece = lane % vec_per_row;
+            const int tok = c + j;
+            const int col = col0 + piece * (16 / esz);
+            if (tok < t.rows && col < a.N) {
+              const int64_t yr = a.y_row_map ? (int64_t)__ldg(a.y_row_map + t.row0 + tok) : (int64_t)t.row0 + tok;
+              const uint4 val = *reinterpret_cast<const uint4*>(buf + j * 32 * esz + piece * 16);
+              *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(a.Y) + (yr * a.N + col) * esz) = val;
+            }
+          }
+          __syncwarp();
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (kCta == 2) mbar_arrive_cluster(leader(tempty_bar(acc)));
+          else mbar_arrive(tempty_bar(acc));
+        }
+        if constexpr (kProf) c_work += clock64() - w0;
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1u;
+        }
+        continue;
+      }
       const int grow = t.rt * kPairRows + (int)rank * kBM + q * 32 + lane;   // row within the task
       const bool valid = grow < t.rows;
       const int64_t yrow = a.y_row_map ? (int64_t)__ldg(a.y_row_map + t.row0 + min(grow, t.rows - 1))
@@ -626,16 +712,18 @@ extern "C" moe_status moe_device_info(int32_t* sm_count, int32_t* cc_major, int3
 
 namespace {
 
+template <bool kProf, int kCta, bool kSplit>
+cudaError_t set_attr() {
+  return cudaFuncSetAttribute(moe_gemm_kernel<kProf, kCta, kSplit>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)(Geo<kCta, kSplit>::kSmem + 8 * kMaxMPad));
+}
+
 cudaError_t set_smem_attrs() {
   static std::once_flag once;
   static cudaError_t err = cudaSuccess;
   std::call_once(once, [] {
-    const int s1 = (int)(Geo<1>::kSmem + 8 * kMaxMPad), s2 = (int)(Geo<2>::kSmem + 8 * kMaxMPad);
-    cudaError_t e[4] = {
-        cudaFuncSetAttribute(moe_gemm_kernel<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, s1),
-        cudaFuncSetAttribute(moe_gemm_kernel<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, s1),
-        cudaFuncSetAttribute(moe_gemm_kernel<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, s2),
-        cudaFuncSetAttribute(moe_gemm_kernel<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, s2)};
+    cudaError_t e[6] = {set_attr<false, 1, false>(), set_attr<true, 1, false>(), set_attr<false, 2, false>(),
+                        set_attr<true, 2, false>(), set_attr<false, 2, true>(), set_attr<true, 2, true>()};
     for (cudaError_t x : e)
       if (x != cudaSuccess && err == cudaSuccess) err = x;
   });
@@ -707,8 +795,9 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
   cudaError_t attr_err = set_smem_attrs();
   if (attr_err != cudaSuccess) MOE_FAIL(MOE_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(attr_err));
   if (v.bm == 256) {
+    const bool split = (v.flags & MOE_SPLIT_TAIL) != 0;
     const int pairs = v.total < 0 ? sm_count_cached() / 2 : std::min(v.total, sm_count_cached() / 2);
-    const size_t smem = Geo<2>::kSmem + 8 * (size_t)v.M_pad;
+    const size_t smem = (split ? Geo<2, true>::kSmem : Geo<2, false>::kSmem) + 8 * (size_t)v.M_pad;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * pairs);
     cfg.blockDim = dim3(kThreads);
@@ -721,16 +810,21 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t le = prof ? cudaLaunchKernelEx(&cfg, moe_gemm_kernel<true, 2>, tmX, tmW, a)
-                          : cudaLaunchKernelEx(&cfg, moe_gemm_kernel<false, 2>, tmX, tmW, a);
+    cudaError_t le;
+    if (split)
+      le = prof ? cudaLaunchKernelEx(&cfg, moe_gemm_kernel<true, 2, true>, tmX, tmW, a)
+                : cudaLaunchKernelEx(&cfg, moe_gemm_kernel<false, 2, true>, tmX, tmW, a);
+    else
+      le = prof ? cudaLaunchKernelEx(&cfg, moe_gemm_kernel<true, 2, false>, tmX, tmW, a)
+                : cudaLaunchKernelEx(&cfg, moe_gemm_kernel<false, 2, false>, tmX, tmW, a);
     if (le != cudaSuccess) MOE_FAIL(MOE_ERR_CUDA, "moe_gemm pair launch: %s", cudaGetErrorString(le));
   } else {
     const int grid = v.total < 0 ? sm_count_cached() : std::min(v.total, sm_count_cached());
     const size_t smem = Geo<1>::kSmem + 8 * (size_t)v.M_pad;
     if (prof)
-      moe_gemm_kernel<true, 1><<<grid, kThreads, smem, (cudaStream_t)stream>>>(tmX, tmW, a);
+      moe_gemm_kernel<true, 1, false><<<grid, kThreads, smem, (cudaStream_t)stream>>>(tmX, tmW, a);
     else
-      moe_gemm_kernel<false, 1><<<grid, kThreads, smem, (cudaStream_t)stream>>>(tmX, tmW, a);
+      moe_gemm_kernel<false, 1, false><<<grid, kThreads, smem, (cudaStream_t)stream>>>(tmX, tmW, a);
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) MOE_FAIL(MOE_ERR_CUDA, "moe_gemm launch: %s", cudaGetErrorString(e));

@@ -76,8 +76,8 @@ moe_status moe_plan_build(const int32_t* counts, int32_t E, int64_t H, int64_t N
              (long long)H, (long long)N);
   if (H >= INT_MAX || N >= INT_MAX) MOE_FAIL(MOE_ERR_CAPACITY, "moe_plan_build: H or N >= 2^31");
   if (bm == 0) {
-    // Auto: executed rows under each tile height, with CTA-pair tiles credited for their measured
-    // per-row advantage (half the W traffic per SM, 6-stage ring: ~1.10x, DESIGN.md §Tile choice).
+    // Auto: executed rows under each tile height, CTA-pair tiles credited with
+    // their measured ~1.10x per-row advantage (half the W traffic per SM, 6-stage ring).
     int64_t r128 = 0, r256 = 0;
     for (int32_t e = 0; e < E; ++e) {
       const int64_t m = counts[e] < 0 ? 0 : counts[e];
@@ -91,8 +91,10 @@ moe_status moe_plan_build(const int32_t* counts, int32_t E, int64_t H, int64_t N
   if (bn < 16 || bn > 256 || bn % (bm == 256 ? 32 : 16))
     MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_plan_build: bn=%d must be a multiple of %d in [16, 256]", bn,
              bm == 256 ? 32 : 16);
-  if (flags & ~MOE_PAD_REPEAT) MOE_FAIL(MOE_ERR_INVALID, "moe_plan_build: unknown flags 0x%x", flags);
-
+  if (flags & ~(MOE_PAD_REPEAT | MOE_SPLIT_TAIL)) MOE_FAIL(MOE_ERR_INVALID, "moe_plan_build: unknown flags 0x%x", flags);
+  const bool split = (flags & MOE_SPLIT_TAIL) != 0;
+  if (split && (bm != 256 || bn != 256))
+    MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_plan_build: MOE_SPLIT_TAIL needs bm = bn = 256 (swap-AB tail tiles, M = 256)");
   // CSR row offsets: exclusive prefix of counts in expert-id order.
   std::vector<int64_t> row_off(E + 1, 0);
   for (int32_t e = 0; e < E; ++e) {
@@ -101,7 +103,9 @@ moe_status moe_plan_build(const int32_t* counts, int32_t E, int64_t H, int64_t N
   }
   if (row_off[E] >= INT_MAX) MOE_FAIL(MOE_ERR_CAPACITY, "moe_plan_build: sum of counts >= 2^31");
 
-  // Tasks = experts.  nu = ceil(m/BM) * ceil(N/BN); K is not split.
+  // Tasks = experts.  nu = ceil(m/BM) * ceil(N/BN); K is not split.  With
+  // MOE_SPLIT_TAIL an expert with m % BM != 0 is kind 1: its last row tile (the tail) runs as a
+  // swap-AB tile of height roundup16(m % BM) — same tile partition, second tiling strategy.
   const int32_t n_tasks = E;
   const int64_t col_tiles = ceil_div(N, bn);
   std::vector<int64_t> nu(n_tasks);
@@ -155,7 +159,7 @@ moe_status moe_plan_build(const int32_t* counts, int32_t E, int64_t H, int64_t N
     p[0] = i;                                   // expert
     p[1] = (int32_t)row_off[i];                 // first CSR row of the task
     p[2] = counts[i];                           // rows
-    p[3] = 0;                                   // kind (one tiling strategy in this build)
+    p[3] = split && counts[i] % bm ? 1 : 0;     // kind: 1 = last row tile is a swap-AB tail tile
     p[4] = bm;
     p[5] = bn;
     p[6] = (int32_t)ceil_div(counts[i], bm);    // row tiles
@@ -236,6 +240,7 @@ moe_status moe_plan_create(const int32_t* counts, int32_t E, int64_t H, int64_t 
     return st;
   }
   bm = p->blob[7];                              // resolved tile height (bm = 0 means auto)
+  flags = (uint32_t)p->blob[10];                // auto may add MOE_SPLIT_TAIL
   p->stream = (cudaStream_t)stream;
   p->E = E;
   p->H = H;

@@ -54,7 +54,8 @@ __global__ void __launch_bounds__(kPlanThreads)
     plan_device_kernel(const int32_t* __restrict__ counts, int E, int H, int N, int bm, int bn, uint32_t flags,
                        int32_t* __restrict__ blob) {
   __shared__ long long s_warp[32];
-  const int t = threadIdx.x;
+  const int t = threadIdx.x;                                       // expert t
+  const bool split = (flags & MOE_SPLIT_TAIL) != 0;
   const long long m = t < E ? (long long)max(counts[t], 0) : 0;
   const long long col_tiles = (N + bn - 1) / bn;
   const long long row_tiles = (m + bm - 1) / bm;
@@ -94,21 +95,21 @@ __global__ void __launch_bounds__(kPlanThreads)
     pre[h] = (int32_t)tiles_incl;                    // TilePrefix over eta: the scan of nu with
     sig[h] = t;                                      // empty tasks adding 0 (sigma(h) = t)
   }
-  if (t >= M && t < M_pad) {                         // P:203 padding
-    pre[t] = (flags & MOE_PAD_REPEAT) && M > 0 ? (int32_t)tiles_total : INT_MAX;
-    sig[t] = 0;
-  }
   if (t < E) {
     int32_t* p = par + (long long)MOE_PLAN_TASK_WORDS * t;
     p[0] = t;
     p[1] = (int32_t)(rows_incl - m);
     p[2] = (int32_t)m;
-    p[3] = 0;
+    p[3] = split && (m % bm) ? 1 : 0;               // kind 1: last row tile is a swap-AB tail
     p[4] = bm;
     p[5] = bn;
     p[6] = (int32_t)row_tiles;
     p[7] = (int32_t)col_tiles;
     roff[t] = (int32_t)(rows_incl - m);
+  }
+  for (int i = M + t; i < M_pad; i += blockDim.x) {                 // P:203 padding
+    pre[i] = (flags & MOE_PAD_REPEAT) && M > 0 ? (int32_t)tiles_total : INT_MAX;
+    sig[i] = 0;
   }
   if (t == 0) roff[E] = (int32_t)rows_total;
 }

@@ -21,12 +21,13 @@ def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "mix"
     bn = int(sys.argv[2]) if len(sys.argv) > 2 else 256
     bm = int(sys.argv[3]) if len(sys.argv) > 3 else 128
+    flags = int(sys.argv[4]) if len(sys.argv) > 4 else 0
     c = synth.CONFIGS[name]
     ids = torch.from_numpy(synth.route(c, 0)).cuda()
     X = synth.make_x_torch(0, c.T, c.H, device="cuda")
     W = synth.make_w_torch(0, c.E, c.H, c.N, device="cuda")
     counts, row_off, tok, _, _ = M.moe_route(ids, c.E)
-    plan = M.Plan(counts.cpu().numpy(), c.H, c.N, bm, bn)
+    plan = M.Plan(counts.cpu().numpy(), c.H, c.N, bm, bn, flags)
     Y = torch.empty((tok.numel(), c.N), dtype=torch.bfloat16, device="cuda")
     for _ in range(3):
         M.moe_gemm(plan, X, tok, W, Y=Y)
@@ -48,7 +49,7 @@ def main():
     p = pall[0::2] if bm == 256 else pall           # MMA counters live in the pair leaders
     tot = p[:, 2]
     out = {
-        "config": name, "bn": bn, "bm": bm, "tiles": plan.total_tiles, "ms_plain": t_plain, "ms_instrumented": t_prof,
+        "config": name, "bn": bn, "bm": bm, "flags": flags, "tiles": plan.total_tiles, "ms_plain": t_plain, "ms_instrumented": t_prof,
         "tflops_plain": c.flops / t_plain / 1e9,
         "identical_Y": bool(torch.equal(Y, Y2)),
         "mma_wait_full_frac": float((p[:, 1] / tot).mean()),

@@ -46,11 +46,11 @@ def _inputs(T, E, k, H, N, seed, mode="normal", routing=None):
     return ids, X, W, Xd, Wd
 
 
-def run_path(ids, Xd, Wd, E, bn=256, out_dtype=torch.float32, pad=M.MOE_PAD_MAX, bm=128):
+def run_path(ids, Xd, Wd, E, bn=256, out_dtype=torch.float32, pad=M.MOE_PAD_MAX, bm=128, flags=0):
     topk = torch.from_numpy(np.ascontiguousarray(ids, dtype=np.int32)).cuda()
     counts, row_off, tok, slot, status = M.moe_route(topk, E)
     counts_h = counts.cpu().numpy()
-    plan = M.Plan(counts_h, Xd.shape[1], Wd.shape[2], bm, bn, pad)
+    plan = M.Plan(counts_h, Xd.shape[1], Wd.shape[2], bm, bn, pad | flags)
     Y = torch.full((tok.numel(), Wd.shape[2]), float("nan"), dtype=out_dtype, device="cuda")
     M.moe_gemm(plan, Xd, tok, Wd, Y=Y)
     torch.cuda.synchronize()
@@ -165,12 +165,12 @@ def test_route_flags_bad_ids_and_empty():
 
 
 # ---------------------------------------------------------------------------- GEMM
-@pytest.mark.parametrize("bm", [128, 256])
-def test_gemm_tiny_a_integer_bit_exact(bm):
+@pytest.mark.parametrize("bm,bn,flags", [(128, 128, 0), (256, 128, 0), (256, 256, M.MOE_SPLIT_TAIL)])
+def test_gemm_tiny_a_integer_bit_exact(bm, bn, flags):
     c = synth.CONFIGS["tiny"]
     ids = synth.route(c, 0)
     _, X, W, Xd, Wd = _inputs(c.T, c.E, c.k, c.H, c.N, 0, "int", routing=ids)
-    Y, counts, row_off, tok, slot, plan, _ = run_path(ids, Xd, Wd, c.E, bn=128, bm=bm)
+    Y, counts, row_off, tok, slot, plan, _ = run_path(ids, Xd, Wd, c.E, bn=bn, bm=bm, flags=flags)
     rc, rr, rt, rs = omoe.buckets(ids, c.E)
     ref = omoe.expert_gemm(X, W, rt, rr)
     assert counts.tolist() == [11, 0, 11, 10]
@@ -219,14 +219,25 @@ RAGGED_PAIR = [
 ]
 
 
-@pytest.mark.parametrize("T,E,k,H,N,bn,bm,a_path",
-                         [c + (128, "0") for c in RAGGED] + [c + (128, "1") for c in RAGGED]
-                         + [c + (256, "1") for c in RAGGED_PAIR])
+RAGGED_SPLIT = [                    # MOE_SPLIT_TAIL: 256-row pair body tiles + swap-AB tail tiles
+    (300, 5, 2, 200, 136),          # tails only / N < 256
+    (700, 3, 2, 256, 512),          # body + tails
+    (64, 16, 4, 128, 352),          # tails of 1..31 rows, N tail
+    (1, 8, 2, 4096, 1024),          # decode: one-token tails
+    (1500, 4, 1, 128, 200),         # 3-D W map (N % 64 != 0)
+    (2048, 4, 2, 64, 256),          # 1024 rows/expert on average, tails of all sizes
+]
+
+
+@pytest.mark.parametrize("T,E,k,H,N,bn,bm,a_path,flags",
+                         [c + (128, "0", 0) for c in RAGGED] + [c + (128, "1", 0) for c in RAGGED]
+                         + [c + (256, "1", 0) for c in RAGGED_PAIR]
+                         + [c + (256, 256, "1", M.MOE_SPLIT_TAIL) for c in RAGGED_SPLIT])
 @pytest.mark.parametrize("mode", ["int", "normal"])
-def test_gemm_ragged(T, E, k, H, N, bn, bm, a_path, mode, monkeypatch):
+def test_gemm_ragged(T, E, k, H, N, bn, bm, a_path, flags, mode, monkeypatch):
     monkeypatch.setenv("MOE_A_PATH", a_path)          # A staging path: gather4 (0) / cp.async (1)
     ids, X, W, Xd, Wd = _inputs(T, E, k, H, N, T + E, mode)
-    Y, counts, row_off, tok, *_ = run_path(ids, Xd, Wd, E, bn=bn, bm=bm)
+    Y, counts, row_off, tok, *_ = run_path(ids, Xd, Wd, E, bn=bn, bm=bm, flags=flags)
     rc, rr, rt, rs = omoe.buckets(ids, E)
     ref = omoe.expert_gemm(X, W, rt, rr)
     Yh = Y.cpu().double().numpy()
@@ -271,16 +282,19 @@ def _sample_rows(row_off, counts, rng, per_expert=6):
     return np.array(rows)
 
 
-@pytest.mark.parametrize("cfg,bn,bm", [("mix", 256, 128), ("mix", 256, 256), ("ds", 128, 128), ("ds", 256, 256),
-                                       ("dec16", 256, 128), ("dec16", 256, 256), ("paper_worst", 256, 256)])
-def test_gemm_full_size_sampled(cfg, bn, bm):
+@pytest.mark.parametrize("cfg,bn,bm,flags", [("mix", 256, 128, 0), ("mix", 256, 256, 0), ("mix", 256, 0, 0),
+                                             ("mix", 256, 256, 2), ("ds", 128, 128, 0), ("ds", 256, 256, 0),
+                                             ("ds", 256, 256, 2), ("dec16", 256, 128, 0), ("dec16", 256, 0, 0),
+                                             ("dec16", 256, 256, 2), ("paper_worst", 256, 256, 0),
+                                             ("paper_worst", 256, 256, 2)])
+def test_gemm_full_size_sampled(cfg, bn, bm, flags):
     """BASELINE.json sizes, the launch configuration bench.py times; sampled outputs vs fp64."""
     c = synth.CONFIGS[cfg]
     seed = 0
     ids = synth.route(c, seed)
     Xd = synth.make_x_torch(seed, c.T, c.H, device="cuda")
     Wd = synth.make_w_torch(seed, c.E, c.H, c.N, device="cuda")
-    Y, counts, row_off, tok, *_ = run_path(ids, Xd, Wd, c.E, bn=bn, out_dtype=torch.bfloat16, bm=bm)
+    Y, counts, row_off, tok, *_ = run_path(ids, Xd, Wd, c.E, bn=bn, out_dtype=torch.bfloat16, bm=bm, flags=flags)
     rc, rr, rt, rs = omoe.buckets(ids, c.E)
     assert np.array_equal(tok.cpu().numpy(), rt)
     rng = np.random.default_rng(1)
@@ -296,35 +310,38 @@ def test_gemm_full_size_sampled(cfg, bn, bm):
 
 
 # ---------------------------------------------------------------------------- device-side planner
-def _device_plan_blob(counts, N, bm, bn, pad, H=64):
+def _device_plan_blob(counts, N, bm, bn, pad, H=64, split=0):
     E = len(counts)
-    plan = M.Plan(None, H, N, bm, bn, M.MOE_PAD_REPEAT if pad == "repeat" else 0, E=E)
+    plan = M.Plan(None, H, N, bm, bn, (M.MOE_PAD_REPEAT if pad == "repeat" else 0) | (M.MOE_SPLIT_TAIL if split else 0),
+                  E=E)
     plan.update_device(torch.tensor(np.asarray(counts), dtype=torch.int32, device="cuda"))
     st = plan.sync()
     return plan, st, M.parse_plan_blob(plan.blob())
 
 
 @pytest.mark.parametrize("pad", ["max", "repeat"])
-@pytest.mark.parametrize("bm,bn", [(128, 256), (256, 256), (128, 48), (256, 96)])
-def test_plan_device_bit_exact(pad, bm, bn):
+@pytest.mark.parametrize("bm,bn,split", [(128, 256, 0), (256, 256, 0), (128, 48, 0), (256, 96, 0), (256, 256, 1)])
+def test_plan_device_bit_exact(pad, bm, bn, split):
     rng = np.random.default_rng(bm + bn)
-    cases = [np.array([11, 0, 11, 10]), np.zeros(5, dtype=np.int64), np.array([1]),
+    cases = [np.array([11, 0, 11, 10]), np.zeros(5, dtype=np.int64), np.array([1]), np.array([256, 512, 5, 0, 300]),
              np.where(rng.random(1024) < 0.3, 0, rng.integers(1, 3000, size=1024)),
              np.bincount(synth.route(synth.CONFIGS["ds"], 0).ravel(), minlength=64)]
     for counts in cases:
         N = 1408
-        plan, st, b = _device_plan_blob(counts, N, bm, bn, pad)
-        ref = omoe.plan(counts, N, bm, bn, pad_mode=pad)
+        plan, st, b = _device_plan_blob(counts, N, bm, bn, pad, split=split)
+        ref = omoe.plan(counts, N, bm, bn, pad_mode=pad, split_tail=bool(split))
         E = len(counts)
+        nt = E
         assert b["M"] == ref["M"] and b["total"] == ref["total"]
         assert st == (M.MOE_OK_EMPTY if ref["M"] == 0 else M.MOE_OK)
-        assert b["M_pad"] == (32 if E <= 32 else -(-E // 32) * 32)
+        assert b["M_pad"] == (32 if nt <= 32 else -(-nt // 32) * 32)
         assert b["prefix"][: ref["M"]].tolist() == ref["prefix"]
         padv = (ref["prefix"][-1] if ref["M"] else 2**31 - 1) if pad == "repeat" else 2**31 - 1
         assert (b["prefix"][ref["M"]:] == padv).all()
         assert b["sigma"][: ref["M"]].tolist() == ref["sigma"]
         assert b["row_off"].tolist() == np.concatenate([[0], np.cumsum(counts)]).tolist()
-        host = M.parse_plan_blob(M.moe_plan_build(counts, 64, N, bm, bn, M.MOE_PAD_REPEAT if pad == "repeat" else 0))
+        host = M.parse_plan_blob(M.moe_plan_build(counts, 64, N, bm, bn, (M.MOE_PAD_REPEAT if pad == "repeat" else 0)
+                                                  | (M.MOE_SPLIT_TAIL if split else 0)))
         assert np.array_equal(b["params"], host["params"])
 
 
@@ -337,7 +354,7 @@ def test_plan_device_overflow_reported():
     assert e.value.status == -3
 
 
-@pytest.mark.parametrize("bm", [128, 256])
+@pytest.mark.parametrize("bm", [128, 256, 0])
 @pytest.mark.parametrize("T,E,k,H,N,bn", [(300, 5, 2, 200, 136, 128), (513, 7, 3, 256, 512, 256), (1, 8, 2, 4096, 1024, 256)])
 def test_gemm_device_planned(T, E, k, H, N, bn, bm):
     ids, X, W, Xd, Wd = _inputs(T, E, k, H, N, T + E + 1, "int")

@@ -42,10 +42,11 @@ def test_library_exports_every_declared_symbol():
     assert b"sm_100a" in L.moe_version()
 
 
-def _compare(counts, N, bm, bn, pad):
-    blob = moe_lib.moe_plan_build(counts, 64, N, bm, bn, moe_lib.MOE_PAD_REPEAT if pad == "repeat" else 0)
+def _compare(counts, N, bm, bn, pad, split=False):
+    flags = (moe_lib.MOE_PAD_REPEAT if pad == "repeat" else 0) | (moe_lib.MOE_SPLIT_TAIL if split else 0)
+    blob = moe_lib.moe_plan_build(counts, 64, N, bm, bn, flags)
     p = moe_lib.parse_plan_blob(blob)
-    ref = omoe.plan(counts, N, bm, bn, pad_mode=pad)
+    ref = omoe.plan(counts, N, bm, bn, pad_mode=pad, split_tail=split)
     assert p["M"] == ref["M"] and p["total"] == ref["total"]
     if ref["M"] == 0:
         return
@@ -56,7 +57,7 @@ def _compare(counts, N, bm, bn, pad):
     for i, t in enumerate(ref["tasks"]):
         q = p["params"][i]
         assert q[0] == t["expert"] and q[1] == row_off[t["expert"]] + t["row_begin"] and q[2] == t["rows"]
-        assert q[4] == t["bm"] and q[5] == t["bn"]
+        assert q[3] == t["kind"] and q[4] == t["bm"] and q[5] == t["bn"]
         assert q[6] * q[7] == ref["nu"][i]
         assert q[6] == -(-t["rows"] // bm)
 
@@ -85,6 +86,16 @@ def test_planner_matches_oracle_random_corpus():
         _compare(counts, N, bm, bn, rng.choice(["max", "repeat"]))
 
 
+def test_planner_split_tail_matches_oracle():
+    rng = random.Random(13)
+    for _ in range(200):
+        E = rng.randint(1, 200)
+        counts = np.array([0 if rng.random() < 0.3 else rng.randint(1, 3000) for _ in range(E)])
+        _compare(counts, 8 * rng.randint(1, 3000), 256, 256, rng.choice(["max", "repeat"]), split=True)
+    with pytest.raises(moe_lib.MoeError):
+        moe_lib.moe_plan_build([5, 5], 64, 512, 256, 128, moe_lib.MOE_SPLIT_TAIL)   # needs bn = 256
+
+
 def test_planner_auto_tile_choice():
     """bm = 0: pair tiles unless their padding rows exceed 1.10x the 128-row padding (header rule)."""
     rng = random.Random(12)
@@ -99,6 +110,7 @@ def test_planner_auto_tile_choice():
         r256 = sum(-(-m // 256) * 256 for m in counts)
         expect = 256 if (r256 * 100 <= r128 * 110 and bn % 32 == 0) else 128
         assert blob["bm"] == expect
+        assert not blob["flags"] & moe_lib.MOE_SPLIT_TAIL
         _compare(np.array(counts), 1024, expect, bn, "max")
     c = synth.CONFIGS["mix_balanced"]
     counts = np.bincount(synth.route(c).ravel(), minlength=c.E)

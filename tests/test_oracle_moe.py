@@ -151,6 +151,30 @@ def test_decode_enumeration_rt_fastest_and_cover():
         assert (moe.tile_cover(p, row_off, sum(counts)) == 1).all()          # exactly-once
 
 
+def test_split_tail_tasks_cover_exactly_once():
+    """Two tiling strategies in one plan: the tail tile of each expert (kind 1)
+    covers exactly its m mod 256 rows and Y is still tiled exactly once."""
+    rng = random.Random(7)
+    for _ in range(20):
+        E = rng.randint(1, 6)
+        counts = [0 if rng.random() < 0.2 else rng.randint(1, 700) for _ in range(E)]
+        if sum(counts) == 0:
+            counts[0] = 1
+        N = rng.choice([200, 256, 600])
+        p = moe.plan(counts, N, 256, 256, split_tail=True)
+        assert p["total"] == moe.plan(counts, N, 256, 256)["total"]
+        row_off = np.concatenate([[0], np.cumsum(counts)])
+        assert (moe.tile_cover(p, row_off, sum(counts)) == 1).all()
+        for B in range(p["total"]):
+            d = moe.decode(p, row_off, B)
+            m = counts[d["expert"]]
+            if d["kind"] == 1:
+                assert m % 256 and d["rows"] == (row_off[d["expert"]] + m // 256 * 256, row_off[d["expert"]] + m)
+                assert d["height"] % 16 == 0 and d["height"] - 16 < m % 256 <= d["height"]
+            else:
+                assert d["rows"][1] - d["rows"][0] == 256 or m % 256 == 0 or d["rt"] < m // 256
+
+
 # ---- c4 GEMM -----------------------------------------------------------------
 def _route(T, E, k, seed):
     return synth.route_gumbel(seed, T, E, k)
