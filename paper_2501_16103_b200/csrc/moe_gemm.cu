@@ -77,6 +77,7 @@ struct GemmArgs {
   int32_t a_mode;            // A staging: 0 = TMA tile::gather4, 1 = cp.async (LSU path), see DESIGN.md
   int32_t H;
   const __nv_bfloat16* X;
+  int32_t experiment;        // MOE_EXPERIMENTS builds only (timing studies, wrong Y): 1 = no A reads, 2 = no B loads
   const int32_t* y_row_map;  // nullable: Y row of CSR row i is y_row_map[i] (EP combine buffer)
 };
 
@@ -198,7 +199,7 @@ __device__ __forceinline__ void wait_timed(uint32_t bar, uint32_t parity, long l
 // two CTAs, so a stage is 32 KB instead of 48 KB and six stages fit.
 template <int kCta, bool kSplit = false>
 struct Geo {
-  static constexpr int kStages = kCta == 2 ? 6 : 4;
+  static constexpr int kStages = kCta == 2 ? 6 : 4;     // a 7th pair stage measured no gain (NOTES)
   static_assert(8 * (2 * kStages + 4) + 4 <= kBarBytes, "barrier block overlaps TilePrefix");
   static constexpr int kBStage = kBStageBytes / kCta;            // bytes of W per CTA per stage
   // CTA pairs: a 4 KB transpose buffer per epilogue warp for swap-AB tail tiles (MOE_SPLIT_TAIL).
@@ -329,7 +330,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t dst = sA + s * kABytes + dst_off;
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
+#ifdef MOE_EXPERIMENTS
+            const bool ok = a.experiment != 1 && colok && ((rowok >> j) & 1u);
+#else
             const bool ok = colok && ((rowok >> j) & 1u);
+#endif
             cp_async_16(dst + j * 16 * 128, ok ? src[j] + kcol : a.X, ok ? 16u : 0u);
           }
           cp_async_mbar_arrive_noinc(full_bar(s));
@@ -359,6 +364,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int kb = 0; kb < a.num_kb; ++kb, ++g) {
         const int s = g % kSt;
         wait_timed<kProf>(empty_bar(s), ((g / kSt) & 1u) ^ 1u, c_wait);
+#ifdef MOE_EXPERIMENTS
+        if (a.experiment == 2) {
+          if (lane == 0 && rank == 0) mbar_arrive(full_bar(s));
+          __syncwarp();
+          continue;
+        }
+#endif
         if (lane == 0) {
           const uint32_t dstB = sB + s * kBSt;
           if constexpr (kCta == 2) {
@@ -786,6 +798,10 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
   a.T = (int32_t)T;
   a.H = v.H;
   a.X = reinterpret_cast<const __nv_bfloat16*>(X);
+  {
+    const char* ex = getenv("MOE_GEMM_EXPERIMENT");
+    a.experiment = ex ? atoi(ex) : 0;
+  }
   {
     const char* am = getenv("MOE_A_PATH");       // timing studies: force the A staging path
     a.a_mode = am ? atoi(am) : kDefaultAMode;
