@@ -46,6 +46,12 @@ typedef int32_t moe_status;
 #define MOE_ERR_CUDA        (-4) /* a CUDA runtime/driver call failed (message has the name)     */
 #define MOE_ERR_NCCL        (-5) /* reserved for the expert-parallel layer                       */
 
+/* Expert (task) ordering of sigma, §4.2, plan flags; results never depend on it. */
+#define MOE_ORDER_ALTERNATING    4u  /* sort non-empty tasks by load (desc, ties: lower id), interleave
+                                        the busiest half with the rest: b1, s1, b2, s2, ...          */
+#define MOE_ORDER_HALF_INTERVAL  8u  /* same sort; the i-th busiest task takes the i-th slot of the
+                                        bit-reversal (van der Corput) sequence over the slots        */
+
 /* Output element types of moe_gemm. */
 #define MOE_DTYPE_BF16 0
 #define MOE_DTYPE_F32  1
@@ -100,7 +106,8 @@ int64_t moe_plan_blob_words(int32_t E);
  *                    tiles' extra padding rows exceed their ~10% per-row speed advantage
  *                    (sum of ceil(m_e/256)*256 > 1.10 * sum of ceil(m_e/128)*128).  The blob
  *                    records the resolved bm.
- *   flags            MOE_PAD_MAX | MOE_PAD_REPEAT, optionally | MOE_SPLIT_TAIL.
+ *   flags            MOE_PAD_MAX | MOE_PAD_REPEAT, optionally | MOE_SPLIT_TAIL and one of
+ *                    MOE_ORDER_ALTERNATING / MOE_ORDER_HALF_INTERVAL (sigma order, §4.2).
  *   blob, blob_cap   caller buffer of blob_cap int32 words (see moe_plan_blob_words).
  *   blob_len         out: words written.
  * Returns MOE_OK, MOE_OK_EMPTY (all experts empty: M = 0, total = 0),

@@ -36,13 +36,14 @@ def pad_tile_prefix(prefix: list[int], warp_size: int = 32, mode: str = "max") -
 # ---------------------------------------------------------------------------
 # Algorithm 4's extra stage — sigma over non-empty tasks
 # ---------------------------------------------------------------------------
-def nonempty_stage(nu: list[int]) -> tuple[list[int], list[int]]:
+def nonempty_stage(nu: list[int], order: list[int] | None = None) -> tuple[list[int], list[int]]:
     """Returns (sigma, TilePrefix over the non-empty tasks).
 
     eta = {S_1..S_M} = tasks with nu > 0 (P:268); sigma: [M] -> [N] with
-    S_i = T_sigma(i), taken in the natural (increasing) order; TilePrefix
-    is built "only ... for non-empty tasks" (P:271)."""
-    sigma = [j for j in range(len(nu)) if nu[j] > 0]
+    S_i = T_sigma(i), taken in the natural (increasing) order unless ``order``
+    (a permutation of the non-empty task ids, §4.2) is given; TilePrefix is built
+    "only ... for non-empty tasks", in sigma's order."""
+    sigma = [j for j in range(len(nu)) if nu[j] > 0] if order is None else list(order)
     prefix = build_tile_prefix([nu[j] for j in sigma])
     return sigma, prefix
 

@@ -80,14 +80,50 @@ def make_tasks(counts, bm: int, bn: int, split_tail: bool = False) -> list[dict]
                  kind=1 if (split_tail and int(m) % bm) else 0) for e, m in enumerate(counts)]
 
 
+def order_tasks(loads: list[int], strategy: str) -> list[int]:
+    """§4.2 expert ordering over the NON-EMPTY tasks, as SPEC formalises it
+    (S:341-346): sort by load descending, ties by lower id; 'alternating' interleaves the
+    busiest half with the rest (b1, s1, b2, s2, ...); 'half_interval' puts the i-th busiest
+    at the i-th slot of the bit-reversal (van der Corput) sequence over the slot range."""
+    ids = [j for j in range(len(loads)) if loads[j] > 0]
+    if strategy == "natural":
+        return ids
+    desc = sorted(ids, key=lambda j: (-loads[j], j))
+    n = len(desc)
+    if strategy == "alternating":
+        h = (n + 1) // 2
+        busy, rest = desc[:h], desc[h:]
+        out = []
+        for i in range(h):
+            out.append(busy[i])
+            if i < len(rest):
+                out.append(rest[i])
+        return out
+    if strategy == "half_interval":
+        w = 0
+        while (1 << w) < n:
+            w += 1
+        slots = []
+        for i in range(1 << w):
+            r = int(format(i, f"0{w}b")[::-1], 2) if w else 0
+            if r < n:
+                slots.append(r)
+        out = [None] * n
+        for i, j in enumerate(desc):
+            out[slots[i]] = j
+        return out
+    raise ValueError(strategy)
+
+
 def plan(counts, N: int, bm: int, bn: int, pad_mode: str = "max", warp_size: int = 32,
-         tasks: list[dict] | None = None, split_tail: bool = False) -> dict:
-    """Host-side plan: nu per task, sigma (non-empty tasks, natural order), TilePrefix
-    (Alg. 1 over eta), padded per P:203."""
+         tasks: list[dict] | None = None, split_tail: bool = False, order: str = "natural") -> dict:
+    """Host-side plan: nu per task, sigma (non-empty tasks, natural order or a §4.2
+    ordering), TilePrefix (Alg. 1 over eta in sigma's order), padded per P:203."""
     if tasks is None:
         tasks = make_tasks(counts, bm, bn, split_tail)
     nu = [tiles_of(t["rows"], N, t["bm"], t["bn"]) for t in tasks]
-    sigma, prefix = mapping.nonempty_stage(nu)
+    sigma, prefix = mapping.nonempty_stage(nu, order_tasks([t["rows"] for t in tasks], order)
+                                           if order != "natural" else None)
     padded = mapping.pad_tile_prefix(prefix, warp_size, pad_mode) if prefix else []
     return dict(tasks=tasks, nu=nu, sigma=sigma, prefix=prefix, padded=padded,
                 M=len(sigma), total=mapping.total_tiles(prefix), N=N, warp_size=warp_size)

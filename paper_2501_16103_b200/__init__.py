@@ -21,6 +21,7 @@ MOE_OK, MOE_OK_EMPTY = 0, 1
 MOE_ERR = {-1: "INVALID", -2: "UNSUPPORTED", -3: "CAPACITY", -4: "CUDA", -5: "NCCL"}
 MOE_DTYPE_BF16, MOE_DTYPE_F32 = 0, 1
 MOE_PAD_MAX, MOE_PAD_REPEAT, MOE_SPLIT_TAIL = 0, 1, 2
+MOE_ORDER_ALTERNATING, MOE_ORDER_HALF_INTERVAL = 4, 8
 MOE_PLAN_MAGIC = 0x4D4F4531
 MOE_PLAN_HEADER = 16
 MOE_PLAN_TASK_WORDS = 8

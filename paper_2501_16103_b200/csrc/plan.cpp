@@ -8,6 +8,7 @@
 // The blob layout is documented in include/moe_sm100.h.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <climits>
 #include <cstring>
 #include <string>
@@ -91,7 +92,10 @@ moe_status moe_plan_build(const int32_t* counts, int32_t E, int64_t H, int64_t N
   if (bn < 16 || bn > 256 || bn % (bm == 256 ? 32 : 16))
     MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_plan_build: bn=%d must be a multiple of %d in [16, 256]", bn,
              bm == 256 ? 32 : 16);
-  if (flags & ~(MOE_PAD_REPEAT | MOE_SPLIT_TAIL)) MOE_FAIL(MOE_ERR_INVALID, "moe_plan_build: unknown flags 0x%x", flags);
+  if (flags & ~(MOE_PAD_REPEAT | MOE_SPLIT_TAIL | MOE_ORDER_ALTERNATING | MOE_ORDER_HALF_INTERVAL))
+    MOE_FAIL(MOE_ERR_INVALID, "moe_plan_build: unknown flags 0x%x", flags);
+  if ((flags & MOE_ORDER_ALTERNATING) && (flags & MOE_ORDER_HALF_INTERVAL))
+    MOE_FAIL(MOE_ERR_INVALID, "moe_plan_build: choose one expert ordering");
   const bool split = (flags & MOE_SPLIT_TAIL) != 0;
   if (split && (bm != 256 || bn != 256))
     MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_plan_build: MOE_SPLIT_TAIL needs bm = bn = 256 (swap-AB tail tiles, M = 256)");
@@ -113,11 +117,36 @@ moe_status moe_plan_build(const int32_t* counts, int32_t E, int64_t H, int64_t N
 
   // Non-empty stage: sigma in natural order, then Alg. 1 over eta.
   std::vector<int32_t> sigma;
+  for (int32_t i = 0; i < n_tasks; ++i)
+    if (nu[i] > 0) sigma.push_back(i);
+  if (flags & (MOE_ORDER_ALTERNATING | MOE_ORDER_HALF_INTERVAL)) {
+    // §4.2 expert ordering: busy (compute-bound) and non-busy (memory-bound)
+    // experts interleaved so a wave of CTAs mixes both.  sigma stays an injection.
+    std::vector<int32_t> desc = sigma;
+    std::stable_sort(desc.begin(), desc.end(), [&](int32_t x, int32_t y) { return counts[x] > counts[y]; });
+    const int32_t n = (int32_t)desc.size();
+    if (flags & MOE_ORDER_ALTERNATING) {
+      const int32_t h = (n + 1) / 2;
+      sigma.clear();
+      for (int32_t i = 0; i < h; ++i) {
+        sigma.push_back(desc[i]);
+        if (h + i < n) sigma.push_back(desc[h + i]);
+      }
+    } else {
+      int32_t w = 0;
+      while ((1 << w) < n) ++w;
+      std::vector<int32_t> slots;
+      for (int32_t i = 0; i < (1 << w); ++i) {
+        int32_t r = 0;
+        for (int32_t b = 0; b < w; ++b) r |= ((i >> b) & 1) << (w - 1 - b);
+        if (r < n) slots.push_back(r);
+      }
+      for (int32_t i = 0; i < n; ++i) sigma[slots[i]] = desc[i];
+    }
+  }
   std::vector<int64_t> prefix;
   int64_t acc = 0;
-  for (int32_t i = 0; i < n_tasks; ++i) {
-    if (nu[i] == 0) continue;
-    sigma.push_back(i);
+  for (int32_t i : sigma) {
     acc += nu[i];
     prefix.push_back(acc);
   }

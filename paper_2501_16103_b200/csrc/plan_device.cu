@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(kPlanThreads)
   const long long nu = m > 0 ? row_tiles * col_tiles : 0;         // nu(T_t)
   long long rows_total, tiles_total, ne_total;
   const long long rows_incl = block_scan_incl(m, s_warp, &rows_total);
-  const long long tiles_incl = block_scan_incl(nu, s_warp, &tiles_total);   // Alg. 1 over all tasks
+  block_scan_incl(nu, s_warp, &tiles_total);                       // total tiles
   const long long ne_incl = block_scan_incl(nu > 0 ? 1 : 0, s_warp, &ne_total);
   const int M = (int)ne_total;                                      // |eta|
   const int M_pad = E <= 32 ? 32 : (E + 31) / 32 * 32;
@@ -90,10 +90,49 @@ __global__ void __launch_bounds__(kPlanThreads)
     }
     blob[t] = w;
   }
+  // sigma: natural order (slot = non-empty index), or a §4.2 ordering over the non-empty tasks
+  // (rank by load descending, ties lower id first; then the alternating / bit-reversal slot).
+  __shared__ int s_m[kPlanThreads];
+  __shared__ long long s_nu[kPlanThreads];
+  __shared__ int s_sig[kPlanThreads];
+  s_m[t] = nu > 0 ? (int)m : -1;
+  __syncthreads();
   if (t < E && nu > 0) {
-    const int h = (int)(ne_incl - 1);                // non-empty index of task t
-    pre[h] = (int32_t)tiles_incl;                    // TilePrefix over eta: the scan of nu with
-    sig[h] = t;                                      // empty tasks adding 0 (sigma(h) = t)
+    int slot = (int)(ne_incl - 1);
+    if (flags & (MOE_ORDER_ALTERNATING | MOE_ORDER_HALF_INTERVAL)) {
+      int r = 0;                                     // rank in descending load order
+      for (int j = 0; j < E; ++j) {
+        const int mj = s_m[j];
+        r += mj > (int)m || (mj == (int)m && j < t);
+      }
+      if (flags & MOE_ORDER_ALTERNATING) {
+        const int h = (M + 1) / 2;
+        slot = r < h ? 2 * r : 2 * (r - h) + 1;
+      } else {
+        int w = 0;
+        while ((1 << w) < M) ++w;
+        int seen = 0;
+        for (int i = 0; i < (1 << w); ++i) {         // r-th element of the bit-reversal sequence < M
+          const int rev = (int)(__brev((unsigned)i) >> (32 - w));
+          if (w == 0 || rev < M) {
+            if (seen == r) {
+              slot = w == 0 ? 0 : rev;
+              break;
+            }
+            ++seen;
+          }
+        }
+      }
+    }
+    s_nu[slot] = nu;
+    s_sig[slot] = t;
+  }
+  __syncthreads();
+  long long scan_total;
+  const long long pre_incl = block_scan_incl(t < M ? s_nu[t] : 0, s_warp, &scan_total);   // Alg. 1 in sigma order
+  if (t < M) {
+    pre[t] = (int32_t)pre_incl;
+    sig[t] = s_sig[t];
   }
   if (t < E) {
     int32_t* p = par + (long long)MOE_PLAN_TASK_WORDS * t;

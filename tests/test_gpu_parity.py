@@ -310,26 +310,31 @@ def test_gemm_full_size_sampled(cfg, bn, bm, flags):
 
 
 # ---------------------------------------------------------------------------- device-side planner
-def _device_plan_blob(counts, N, bm, bn, pad, H=64, split=0):
+ORDER_FLAG = {"natural": 0, "alternating": M.MOE_ORDER_ALTERNATING, "half_interval": M.MOE_ORDER_HALF_INTERVAL}
+
+
+def _device_plan_blob(counts, N, bm, bn, pad, H=64, split=0, order="natural"):
     E = len(counts)
-    plan = M.Plan(None, H, N, bm, bn, (M.MOE_PAD_REPEAT if pad == "repeat" else 0) | (M.MOE_SPLIT_TAIL if split else 0),
-                  E=E)
+    plan = M.Plan(None, H, N, bm, bn, (M.MOE_PAD_REPEAT if pad == "repeat" else 0) | (M.MOE_SPLIT_TAIL if split else 0)
+                  | ORDER_FLAG[order], E=E)
     plan.update_device(torch.tensor(np.asarray(counts), dtype=torch.int32, device="cuda"))
     st = plan.sync()
     return plan, st, M.parse_plan_blob(plan.blob())
 
 
 @pytest.mark.parametrize("pad", ["max", "repeat"])
-@pytest.mark.parametrize("bm,bn,split", [(128, 256, 0), (256, 256, 0), (128, 48, 0), (256, 96, 0), (256, 256, 1)])
-def test_plan_device_bit_exact(pad, bm, bn, split):
+@pytest.mark.parametrize("bm,bn,split,order", [(128, 256, 0, "natural"), (256, 256, 0, "natural"), (128, 48, 0, "natural"),
+                                               (256, 96, 0, "natural"), (256, 256, 1, "natural"),
+                                               (128, 256, 0, "alternating"), (256, 256, 0, "half_interval")])
+def test_plan_device_bit_exact(pad, bm, bn, split, order):
     rng = np.random.default_rng(bm + bn)
     cases = [np.array([11, 0, 11, 10]), np.zeros(5, dtype=np.int64), np.array([1]), np.array([256, 512, 5, 0, 300]),
              np.where(rng.random(1024) < 0.3, 0, rng.integers(1, 3000, size=1024)),
              np.bincount(synth.route(synth.CONFIGS["ds"], 0).ravel(), minlength=64)]
     for counts in cases:
         N = 1408
-        plan, st, b = _device_plan_blob(counts, N, bm, bn, pad, split=split)
-        ref = omoe.plan(counts, N, bm, bn, pad_mode=pad, split_tail=bool(split))
+        plan, st, b = _device_plan_blob(counts, N, bm, bn, pad, split=split, order=order)
+        ref = omoe.plan(counts, N, bm, bn, pad_mode=pad, split_tail=bool(split), order=order)
         E = len(counts)
         nt = E
         assert b["M"] == ref["M"] and b["total"] == ref["total"]
@@ -341,7 +346,7 @@ def test_plan_device_bit_exact(pad, bm, bn, split):
         assert b["sigma"][: ref["M"]].tolist() == ref["sigma"]
         assert b["row_off"].tolist() == np.concatenate([[0], np.cumsum(counts)]).tolist()
         host = M.parse_plan_blob(M.moe_plan_build(counts, 64, N, bm, bn, (M.MOE_PAD_REPEAT if pad == "repeat" else 0)
-                                                  | (M.MOE_SPLIT_TAIL if split else 0)))
+                                                  | (M.MOE_SPLIT_TAIL if split else 0) | ORDER_FLAG[order]))
         assert np.array_equal(b["params"], host["params"])
 
 
@@ -370,6 +375,24 @@ def test_gemm_device_planned(T, E, k, H, N, bn, bm):
     torch.cuda.synchronize()
     rc, rr, rt, rs = omoe.buckets(ids2, E)
     assert np.array_equal(Y2.cpu().double().numpy(), omoe.expert_gemm(X, W, rt, rr))
+
+
+@pytest.mark.parametrize("order", ["alternating", "half_interval"])
+def test_gemm_ordering_invariance(order):
+    """Y is bit-identical under every §4.2 ordering (paper worst case, integer data)."""
+    c = synth.CONFIGS["paper_worst"]
+    ids = synth.route(c)
+    T, H, N = 512, 256, 512                                  # the routing pattern at a smaller width
+    ids = np.ascontiguousarray(ids[:T])
+    X = synth.make_x(4, T, H, "int")
+    W = synth.make_w(4, c.E, H, N, "int")
+    Xd = torch.from_numpy(X).to(torch.bfloat16).cuda()
+    Wd = torch.from_numpy(W).to(torch.bfloat16).cuda()
+    Y0, *_ = run_path(ids, Xd, Wd, c.E, bn=256, bm=256)
+    Y1, *_ = run_path(ids, Xd, Wd, c.E, bn=256, bm=256, flags=ORDER_FLAG[order])
+    assert torch.equal(Y0, Y1)
+    rc, rr, rt, rs = omoe.buckets(ids, c.E)
+    assert np.array_equal(Y1.cpu().double().numpy(), omoe.expert_gemm(X, W, rt, rr))
 
 
 def test_gemm_device_planned_all_empty():

@@ -42,11 +42,14 @@ def test_library_exports_every_declared_symbol():
     assert b"sm_100a" in L.moe_version()
 
 
-def _compare(counts, N, bm, bn, pad, split=False):
+ORDER_FLAG = {"natural": 0, "alternating": 4, "half_interval": 8}
+
+
+def _compare(counts, N, bm, bn, pad, split=False, order="natural"):
     flags = (moe_lib.MOE_PAD_REPEAT if pad == "repeat" else 0) | (moe_lib.MOE_SPLIT_TAIL if split else 0)
-    blob = moe_lib.moe_plan_build(counts, 64, N, bm, bn, flags)
+    blob = moe_lib.moe_plan_build(counts, 64, N, bm, bn, flags | ORDER_FLAG[order])
     p = moe_lib.parse_plan_blob(blob)
-    ref = omoe.plan(counts, N, bm, bn, pad_mode=pad, split_tail=split)
+    ref = omoe.plan(counts, N, bm, bn, pad_mode=pad, split_tail=split, order=order)
     assert p["M"] == ref["M"] and p["total"] == ref["total"]
     if ref["M"] == 0:
         return
@@ -84,6 +87,21 @@ def test_planner_matches_oracle_random_corpus():
         bm = rng.choice([128, 256])
         bn = (32 if bm == 256 else 16) * rng.randint(1, 256 // (32 if bm == 256 else 16))
         _compare(counts, N, bm, bn, rng.choice(["max", "repeat"]))
+
+
+def test_planner_expert_ordering_matches_oracle():
+    rng = random.Random(14)
+    for _ in range(200):
+        E = rng.randint(1, 300)
+        counts = np.array([0 if rng.random() < 0.3 else rng.randint(1, 3000) for _ in range(E)])
+        counts[rng.randrange(E)] = counts[rng.randrange(E)]          # ties
+        _compare(counts, 8 * rng.randint(1, 800), 128, 256, "max", order=rng.choice(["alternating", "half_interval"]))
+    c = synth.CONFIGS["paper_worst"]
+    counts = np.bincount(synth.route(c).ravel(), minlength=c.E)
+    for order in ("alternating", "half_interval"):
+        _compare(counts, c.N, 256, 256, "max", order=order)
+    with pytest.raises(moe_lib.MoeError):
+        moe_lib.moe_plan_build([1, 2], 64, 128, 128, 128, 4 | 8)
 
 
 def test_planner_split_tail_matches_oracle():

@@ -123,6 +123,35 @@ def test_paper_best_case_empty_extension():
     assert p["total"] == sum(moe.plan([m], c.N, 128, 256)["total"] for m in counts[:8])
 
 
+def test_expert_ordering_spec_examples():
+    assert moe.order_tasks([9, 1, 8, 2], "alternating") == [0, 3, 2, 1]            # S:345 (a, d, c, b)
+    # 8 experts, loads 8..1 -> busiest at slots {0, 4, 2, 6, 1, 5, 3, 7}
+    order = moe.order_tasks([8, 7, 6, 5, 4, 3, 2, 1], "half_interval")
+    assert [order.index(j) for j in range(8)] == [0, 4, 2, 6, 1, 5, 3, 7]
+    assert moe.order_tasks([3, 3, 3], "natural") == [0, 1, 2]
+    rng = random.Random(8)
+    for _ in range(100):
+        loads = [0 if rng.random() < 0.3 else rng.randint(1, 50) for _ in range(rng.randint(1, 70))]
+        for st in ("natural", "alternating", "half_interval"):
+            o = moe.order_tasks(loads, st)
+            assert sorted(o) == [j for j in range(len(loads)) if loads[j] > 0]     # a permutation of eta
+
+
+def test_ordering_keeps_the_tile_partition():
+    """ordering changes only the tile order, never the partition (hence never Y)."""
+    counts = [4096] * 7 + [4096 - 56] + [1] * 56
+    row_off = np.concatenate([[0], np.cumsum(counts)])
+    for st in ("alternating", "half_interval"):
+        p = moe.plan(counts, 2560, 128, 256, order=st)
+        assert sorted(p["sigma"]) == list(range(64))
+        cover = np.zeros((sum(counts), 2560), dtype=np.int8)
+        seen = set()
+        for B in range(p["total"]):
+            d = moe.decode(p, row_off, B)
+            seen.add((d["expert"], d["rt"], d["ct"]))
+        assert len(seen) == p["total"] == moe.plan(counts, 2560, 128, 256)["total"]
+
+
 # ---- c3 decode ---------------------------------------------------------------
 def test_decode_enumeration_rt_fastest_and_cover():
     rng = random.Random(6)
