@@ -226,17 +226,17 @@ def run_ours(args, cfg):
 
     def step(Y=None):
         nonlocal plan
-        counts, row_off, tok, slot, _ = M.moe_route(topk_d, cfg.E, with_slot=False)
         if args.host_plan:                         # P:142 option 1: counts D2H, plan on the host
+            counts, row_off, tok, slot, _ = M.moe_route(topk_d, cfg.E, with_slot=False)
             counts_h = counts.cpu().numpy()
             if plan is None:
                 plan = M.Plan(counts_h, cfg.H, cfg.N, args.bm, args.bn)
             else:
                 plan.update(counts_h)
-        else:                                      # P:142 option 2: plan generated on the device
-            if plan is None:
+        else:                                      # P:142 option 2: plan generated on the device,
+            if plan is None:                       # fused into the routing scan (moe_route_plan)
                 plan = M.Plan(None, cfg.H, cfg.N, args.bm, args.bn, E=cfg.E)
-            plan.update_device(counts)
+            counts, row_off, tok, slot, _ = M.moe_route(topk_d, cfg.E, with_slot=False, plan=plan)
         g0 = torch.cuda.Event(enable_timing=True)
         g0.record(stream)
         Y = M.moe_gemm(plan, Xd, tok, Wd, Y=Y, out_dtype=out_dtype)
@@ -248,7 +248,33 @@ def run_ours(args, cfg):
         step(Ybuf)
     torch.cuda.synchronize()
 
-    step_ms, gemm_ms = [], []
+    # (1) eager steps: per-launch GEMM time on the launching stream (the roofline's kernel time)
+    step_ms_eager, gemm_ms = [], []
+    for _ in range(args.steps):
+        flush.zero_()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        _, g0 = step(Ybuf)
+        s1.record(stream)
+        s1.synchronize()
+        step_ms_eager.append(s0.elapsed_time(s1))
+        gemm_ms.append(g0.elapsed_time(s1))
+    # (2) the step as one CUDA graph (route + device plan + GEMM, no host synchronisation inside)
+    graph = None
+    if args.graph and not args.host_plan:
+        side = torch.cuda.Stream()
+        side.wait_stream(stream)
+        with torch.cuda.stream(side):
+            step(Ybuf)                                   # warm the capture stream
+        stream.wait_stream(side)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            _, _, tok_g, _, _ = M.moe_route(topk_d, cfg.E, with_slot=False, plan=plan)
+            M.moe_gemm(plan, Xd, tok_g, Wd, Y=Ybuf, out_dtype=out_dtype)
+        for _ in range(3):
+            graph.replay()
+        torch.cuda.synchronize()
+    step_ms = []
     if ws > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
@@ -257,11 +283,13 @@ def run_ours(args, cfg):
             flush.zero_()
             s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s0.record(stream)
-            _, g0 = step(Ybuf)
+            if graph is not None:
+                graph.replay()
+            else:
+                step(Ybuf)
             s1.record(stream)
             s1.synchronize()
             step_ms.append(s0.elapsed_time(s1))
-            gemm_ms.append(g0.elapsed_time(s1))
     torch.cuda.synchronize()
     if ws > 1:
         torch.distributed.barrier()
@@ -294,6 +322,12 @@ def run_ours(args, cfg):
         te = torch.empty_like(topk_d)
 
         def e2e_step():
+            if graph is not None:                  # the captured step reads Xd / topk_d
+                Xd.copy_(X_h, non_blocking=True)
+                topk_d.copy_(ids_h, non_blocking=True)
+                graph.replay()
+                Y_h.copy_(Ybuf, non_blocking=True)
+                return None
             Xe.copy_(X_h, non_blocking=True)
             te.copy_(ids_h, non_blocking=True)
             Y, counts, _, _, _, _ = M.moe_forward(te, Xe, Wd, cfg.E, bm=args.bm, bn=args.bn, out_dtype=out_dtype,
@@ -333,6 +367,8 @@ def run_ours(args, cfg):
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": statistics.mean(step_ms), "higher_is_better": True,
+            "ms_per_step_eager": statistics.mean(step_ms_eager),
+            "cuda_graph": graph is not None,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": config_dict(cfg, args),
             "pct_of_peak": value / peak,
@@ -352,7 +388,7 @@ def run_ours(args, cfg):
                           "traffic_source": tsrc}),
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": (3 if args.host_plan else 4) * args.steps,
+            "gpu_launches": 4 * args.steps,   # route hist / scan(+plan) / scatter, GEMM
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -491,6 +527,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--host-plan", action="store_true", help="plan on the host (counts D2H) instead of on the device")
     ap.add_argument("--ep", action="store_true", help="run the expert-parallel path even on one GPU")
+    ap.add_argument("--no-graph", dest="graph", action="store_false",
+                    help="time eager launches instead of one CUDA graph per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     args = ap.parse_args()

@@ -178,11 +178,22 @@ void moe_plan_destroy(moe_plan* plan);
  *   slot_dev     [T*k] out (nullable): the top-k position j of each row.
  *   status_dev   [1]   out (nullable): set to 0, or to 1 if an id was >= E or
  *                      duplicated in a token (those entries are dropped).
- * Two kernel launches on `stream`; T*k < 2^31, 1 <= k <= 32, 1 <= E <= 1024.
+ * Three kernel launches on `stream` (chunk histograms, one scan block, chunk x expert stable
+ * compaction) plus a stream-ordered scratch allocation (cudaMallocAsync, n_chunks * E int32);
+ * T*k < 2^31, 1 <= k <= 32, 1 <= E <= 1024.
  */
 moe_status moe_route(const int32_t* topk_ids_dev, int64_t T, int32_t k, int32_t E,
                      int32_t* counts_dev, int32_t* row_off_dev, int32_t* token_idx_dev,
                      int32_t* slot_dev, int32_t* status_dev, void* stream);
+
+/*
+ * moe_route fused with moe_plan_device: the scan block that produces counts / row_off also
+ * writes `plan`'s device blob (same kernels, no extra launch, no host synchronisation).
+ * plan must have been created for the same E (counts_host may have been NULL).
+ */
+moe_status moe_route_plan(const int32_t* topk_ids_dev, int64_t T, int32_t k, int32_t E,
+                          int32_t* counts_dev, int32_t* row_off_dev, int32_t* token_idx_dev,
+                          int32_t* slot_dev, int32_t* status_dev, moe_plan* plan, void* stream);
 
 /*
  * The hot path: Y[row0 + r, n] = sum_h X[token_idx[row0 + r], h] * W[e, h, n]

@@ -32,7 +32,7 @@ EXPORTED = (
     "moe_plan_blob", "moe_plan_device_blob", "moe_plan_destroy", "moe_route", "moe_gemm",
     "moe_decode_debug", "moe_device_info", "moe_last_error", "moe_version", "moe_probe_gather4",
     "moe_gemm_profile", "moe_plan_device", "moe_plan_sync", "moe_gemm_rowmap",
-    "moe_ep_dispatch_plan", "moe_gather_rows", "moe_ep_combine_map", "moe_ep_unpack",
+    "moe_ep_dispatch_plan", "moe_gather_rows", "moe_ep_combine_map", "moe_ep_unpack", "moe_route_plan",
 )
 
 
@@ -69,6 +69,8 @@ def lib() -> ctypes.CDLL:
         "moe_plan_device_blob": (vp, [vp]),
         "moe_plan_destroy": (None, [vp]),
         "moe_route": (ctypes.c_int32, [vp, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, vp, vp, vp, vp, vp, vp]),
+        "moe_route_plan": (ctypes.c_int32, [vp, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, vp, vp, vp, vp, vp,
+                                            vp, vp]),
         "moe_gemm": (ctypes.c_int32, [vp, vp, ctypes.c_int64, vp, vp, vp, ctypes.c_int32, vp]),
         "moe_decode_debug": (ctypes.c_int32, [vp, vp, vp]),
         "moe_device_info": (ctypes.c_int32, [c_i32p, c_i32p, c_i32p]),
@@ -221,7 +223,7 @@ def moe_device_info() -> tuple[int, int, int]:
     return n.value, ma.value, mi.value
 
 
-def moe_route(topk_ids, E: int, with_slot: bool = True, stream=None):
+def moe_route(topk_ids, E: int, with_slot: bool = True, stream=None, plan: "Plan | None" = None):
     """topk_ids: int32 CUDA tensor [T, k] -> (counts[E], row_off[E+1], token_idx[T*k], slot, status).
 
     With masked (negative) or invalid ids only the first sum(counts) = row_off[E] entries of
@@ -236,9 +238,13 @@ def moe_route(topk_ids, E: int, with_slot: bool = True, stream=None):
     token_idx = torch.empty(max(T * k, 1), dtype=torch.int32, device=dev)
     slot = torch.empty(max(T * k, 1), dtype=torch.int32, device=dev) if with_slot else None
     status = torch.zeros(1, dtype=torch.int32, device=dev)
-    _check(lib().moe_route(topk_ids.data_ptr(), T, k, E, counts.data_ptr(), row_off.data_ptr(),
-                           token_idx.data_ptr(), slot.data_ptr() if slot is not None else None,
-                           status.data_ptr(), _stream(stream)))
+    args = (topk_ids.data_ptr(), T, k, E, counts.data_ptr(), row_off.data_ptr(), token_idx.data_ptr(),
+            slot.data_ptr() if slot is not None else None, status.data_ptr())
+    if plan is None:
+        _check(lib().moe_route(*args, _stream(stream)))
+    else:                                        # fused with the device planner (moe_route_plan)
+        _check(lib().moe_route_plan(*args, plan.handle, _stream(stream)))
+        plan.device_resident = True
     return counts, row_off, token_idx[: T * k], (slot[: T * k] if slot is not None else None), status
 
 
@@ -363,14 +369,14 @@ def moe_forward(topk_ids, X, W, E: int, bm: int = 0, bn: int = 256, out_dtype=No
     Returns (Y, counts, row_off, token_idx, slot, plan)."""
     import torch
 
-    counts, row_off, token_idx, slot, _ = moe_route(topk_ids, E, stream=stream)
     H, N = int(X.shape[1]), int(W.shape[2])
     if device_plan:
         if plan is None:
             plan = Plan(None, H, N, bm, bn, stream=stream, E=E)
-        plan.update_device(counts, stream=stream)
+        counts, row_off, token_idx, slot, _ = moe_route(topk_ids, E, stream=stream, plan=plan)
         counts_out = counts
     else:
+        counts, row_off, token_idx, slot, _ = moe_route(topk_ids, E, stream=stream)
         counts_out = counts.cpu().numpy()
         if plan is None:
             plan = Plan(counts_out, H, N, bm, bn, stream=stream)

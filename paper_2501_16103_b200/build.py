@@ -21,7 +21,7 @@ NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_SOURCES = ["moe_gemm.cu", "route.cu", "plan_device.cu", "ep.cu"]
 CPP_SOURCES = ["plan.cpp"]
-HEADERS = ["common.h", "sm100_ptx.cuh"]
+HEADERS = ["common.h", "sm100_ptx.cuh", "plan_body.cuh"]
 
 
 def _newer(target: str, deps: list[str]) -> bool:

@@ -234,7 +234,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int total = a.total >= 0 ? a.total : __ldg(a.plan + 2);
+  // Everything up to the TMEM allocation overlaps the previous kernel (PDL); the plan, the
+  // token-index array and X are only touched after griddepcontrol.wait.
+  int total = a.total;
   // CTA pair: rank 0 (leader) issues the MMAs for both CTAs; all consumers of the
   // data path (full / tmem-empty barriers) live in the leader.
   const uint32_t rank = kCta == 2 ? cluster_ctarank() : 0;
@@ -242,8 +244,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int n_pairs = gridDim.x / kCta;
   auto leader = [&](uint32_t addr) { return kCta == 2 ? mapa_shared(addr, 0) : addr; };
 
-  // TilePrefix and sigma are adjacent in the blob: one copy into shared memory.
-  for (int i = threadIdx.x; i < 2 * a.M_pad; i += blockDim.x) s_prefix[i] = a.plan[MOE_PLAN_HEADER + i];
   const int a_mode = kCta == 2 ? 1 : a.a_mode;
   if (threadIdx.x == 0) {
     // full[s] arrivals: A stage done (gather4: one expect_tx per A warp; cp.async: one asynchronous
@@ -265,6 +265,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     prefetch_tmap(&tmW);
   }
   if (warp == kMmaWarp) tmem_alloc<kTmemCols, kCta>(smem_u32(tmem_holder));
+  pdl_wait();                                        // routing / plan of this step are complete
+  // TilePrefix and sigma are adjacent in the blob: one copy into shared memory.
+  for (int i = threadIdx.x; i < 2 * a.M_pad; i += blockDim.x) s_prefix[i] = a.plan[MOE_PLAN_HEADER + i];
+  if (total < 0) total = __ldg(a.plan + 2);
   tc_fence_before();
   if constexpr (kCta == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
@@ -819,13 +823,15 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = (cudaStream_t)stream;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 2;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // PDL: overlap the prologue
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     cudaError_t le;
     if (split)
       le = prof ? cudaLaunchKernelEx(&cfg, moe_gemm_kernel<true, 2, true>, tmX, tmW, a)
@@ -836,11 +842,19 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
     if (le != cudaSuccess) MOE_FAIL(MOE_ERR_CUDA, "moe_gemm pair launch: %s", cudaGetErrorString(le));
   } else {
     const int grid = v.total < 0 ? sm_count_cached() : std::min(v.total, sm_count_cached());
-    const size_t smem = Geo<1>::kSmem + 8 * (size_t)v.M_pad;
-    if (prof)
-      moe_gemm_kernel<true, 1, false><<<grid, kThreads, smem, (cudaStream_t)stream>>>(tmX, tmW, a);
-    else
-      moe_gemm_kernel<false, 1, false><<<grid, kThreads, smem, (cudaStream_t)stream>>>(tmX, tmW, a);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = Geo<1>::kSmem + 8 * (size_t)v.M_pad;
+    cfg.stream = (cudaStream_t)stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t le = prof ? cudaLaunchKernelEx(&cfg, moe_gemm_kernel<true, 1, false>, tmX, tmW, a)
+                          : cudaLaunchKernelEx(&cfg, moe_gemm_kernel<false, 1, false>, tmX, tmW, a);
+    if (le != cudaSuccess) MOE_FAIL(MOE_ERR_CUDA, "moe_gemm launch: %s", cudaGetErrorString(le));
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) MOE_FAIL(MOE_ERR_CUDA, "moe_gemm launch: %s", cudaGetErrorString(e));

@@ -406,3 +406,40 @@ def test_gemm_device_planned_all_empty():
     M.moe_gemm(plan, Xd, tok, Wd, Y=Y)
     torch.cuda.synchronize()
     assert (Y == 7.0).all()
+
+
+@pytest.mark.parametrize("cfg", ["tiny", "mix", "ds", "paper_worst", "dec1", "ep"])
+def test_route_plan_fused_matches_separate(cfg):
+    """moe_route_plan = moe_route + moe_plan_device, bit for bit (and both = the oracle)."""
+    c = synth.CONFIGS[cfg]
+    ids = torch.from_numpy(synth.route(c, 0)).cuda()
+    plan_a = M.Plan(None, c.H, c.N, 0, 256, E=c.E)
+    counts_a, row_off_a, tok_a, slot_a, st_a = M.moe_route(ids, c.E, plan=plan_a)
+    counts_b, row_off_b, tok_b, slot_b, st_b = M.moe_route(ids, c.E)
+    plan_b = M.Plan(None, c.H, c.N, 0, 256, E=c.E)
+    plan_b.update_device(counts_b)
+    plan_a.sync()
+    plan_b.sync()
+    assert torch.equal(counts_a, counts_b) and torch.equal(tok_a, tok_b) and torch.equal(slot_a, slot_b)
+    assert np.array_equal(plan_a.blob(), plan_b.blob())
+    rc, rr, rt, rs = omoe.buckets(synth.route(c, 0), c.E)
+    assert tok_a.cpu().numpy().tolist() == rt.tolist()
+    ref = omoe.plan(rc, c.N, plan_a.bm, 256)
+    b = M.parse_plan_blob(plan_a.blob())
+    assert b["total"] == ref["total"] and b["prefix"][: ref["M"]].tolist() == ref["prefix"]
+
+
+def test_route_many_chunks_and_masked_slots():
+    """> 1 chunk per expert, masked (negative) slots skipped, status only for real errors."""
+    rng = np.random.default_rng(5)
+    T, E, k = 5000, 37, 4
+    ids = np.stack([rng.permutation(E)[:k] for _ in range(T)]).astype(np.int32)
+    ids[rng.random((T, k)) < 0.2] = -1
+    counts, row_off, tok, slot, status = M.moe_route(torch.from_numpy(ids).cuda(), E)
+    assert status.item() == 0
+    n = int(counts.sum().item())
+    for e in range(E):
+        a, b = int(row_off[e]), int(row_off[e + 1])
+        got = tok[a:b].cpu().numpy().tolist()
+        assert got == [t for t in range(T) if e in ids[t]]
+    assert n == int((ids >= 0).sum())
