@@ -89,9 +89,16 @@ def main():
             f.write(f"| {m} | {v['value']:.6g} | {v['unit']} |\n")
         f.write(f"\nDRAM traffic per launch: {dram / 1e9:.4f} GB\n")
         if lc:
-            f.write("\n## launch list (ncu gpu__time_duration, cold-cache, serialised)\n\n| kernel | launches | mean us |\n|---|---|---|\n")
+            f.write("\n## launch list (ncu gpu__time_duration, cold-cache, serialised)\n\nThe library's kernels "
+                    "(one step = route kernels + moe_gemm):\n\n| kernel | launches | mean us |\n|---|---|---|\n")
+            others = 0
             for n, v in sorted(summary["launch_list"].items(), key=lambda kv: -kv[1]["mean_us"]):
-                f.write(f"| `{n}` | {v['launches']} | {v['mean_us']:.1f} |\n")
+                if "moe_gemm" in n or "route_" in n or "plan_" in n:
+                    f.write(f"| `{n}` | {v['launches']} | {v['mean_us']:.1f} |\n")
+                else:
+                    others += v["launches"]
+            f.write(f"\n({others} other launches in the same process: synthetic input generation and the L2 flush "
+                    "memset, outside the timed step.)\n")
             if "gemm_share_of_step_kernels" in summary:
                 f.write(f"\nmoe_gemm share of the step's own kernels: {summary['gemm_share_of_step_kernels']:.3f}\n")
     tp = os.path.join(ROOT, "profiles", "traffic.json")
