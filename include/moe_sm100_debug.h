@@ -26,7 +26,7 @@ moe_status moe_probe_gather4(const void* X_dev, int64_t T, int64_t H, const int3
 /*
  * moe_gemm with per-CTA cycle counters (an instrumented build of the same
  * kernel; clock64() around every mbarrier wait).  prof_dev: device int64 array of
- * grid * 12 words, grid = CTAs launched (min(total tiles, SMs) for bm=128; 2*min(total, SMs/2)
+ * grid * 16 words, grid = CTAs launched (min(total tiles, SMs) for bm=128; 2*min(total, SMs/2)
  * for bm=256); per CTA:
  *   [0] MMA warp cycles waiting for a free TMEM accumulator (epilogue-bound time)
  *   [1] MMA warp cycles waiting for TMA bytes (load-bound time)
@@ -39,6 +39,10 @@ moe_status moe_probe_gather4(const void* X_dev, int64_t T, int64_t H, const int3
  *   [8] producer warp 0 cycles in cp.async.wait_group (cp.async A path)
  *   [9] producer warp 0 cycles fencing and arriving on the full barrier
  *   [10] B warp cycles waiting for a free stage    [11] B warp cycles in its tile loop
+ *   [12] sum over stages of (MMA warp sees the stage full) - (B warp issued its TMA)
+ *   [13] the same from A warp 0's issue of its row copies
+ *   [14] sum over stages of (B warp re-issues into a slot) - (MMA committed that slot)
+ *   [15] stages counted by the MMA warp
  * Results (Y) are identical to moe_gemm.
  */
 moe_status moe_gemm_profile(const moe_plan* plan, const void* X_dev, int64_t T, const int32_t* token_idx_dev,

@@ -59,7 +59,8 @@ constexpr int kDefaultAMode = 1;                // A staging: cp.async (see the 
 constexpr uint32_t kTmemCols = 512;             // 2 accumulators x 256 fp32 columns
 constexpr uint32_t kAccCols = 256;
 constexpr int kMaxMPad = 1024;
-constexpr int kBarBytes = 256;                  // 8 B per mbarrier (<= 2*6+4) + TMEM address slot
+constexpr int kBarBytes = 512;                  // 8 B per mbarrier (<= 2*6+4) + TMEM address slot [0,256);
+                                                // kProf stage timestamps [256,512)
 
 struct GemmArgs {
   const int32_t* plan;       // device plan blob
@@ -95,6 +96,10 @@ enum ProfSlot {
   kProfAArrive,           // producer warp 0: cycles fencing + arriving
   kProfBWaitEmpty,        // B warp: cycles waiting for a free stage
   kProfBTotal,            // B warp: cycles in its tile loop
+  kProfLatB,              // sum over stages: MMA sees `full` - B warp issued the W TMA (this CTA)
+  kProfLatA,              // sum over stages: MMA sees `full` - A warp 0 issued its row copies
+  kProfRelease,           // sum over stages: B warp re-issues into a slot - MMA committed that slot
+  kProfStages,            // stages counted
   kProfSlots
 };
 
@@ -230,6 +235,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto tempty_bar = [&](int i) { return sBar + 8u * (2 * kSt + 2 + i); };
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + (sBar - base) + 8 * (2 * kSt + 4));
   int32_t* s_prefix = reinterpret_cast<int32_t*>(smem + (sBar - base) + kBarBytes);
+  long long* s_ts = reinterpret_cast<long long*>(smem + (sBar - base) + 256);   // kProf: [3][kSt] stamps
   int32_t* s_sigma = s_prefix + a.M_pad;
 
   const int warp = threadIdx.x >> 5;
@@ -329,6 +335,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < a.num_kb; ++kb, ++g) {
           const int s = g % kSt;
           wait_timed<kProf>(empty_bar(s), ((g / kSt) & 1u) ^ 1u, c_wait);
+          if constexpr (kProf) {
+            if (p == 0 && lane == 0) s_ts[kSt + s] = clock64();
+          }
           const int kcol = kb * kBK;
           const bool colok = kcol + ch * 8 < a.H;
           const uint32_t dst = sA + s * kABytes + dst_off;
@@ -357,7 +366,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ===================== B producer: this CTA's share of the W block, one TMA per stage =====================
     const uint64_t pol_w = policy_evict_normal();
     uint32_t g = 0;
-    long long c_wait = 0, c_t0 = kProf ? clock64() : 0;
+    long long c_wait = 0, c_t0 = kProf ? clock64() : 0, c_rel = 0;
     for (int v = pair_id; v < total; v += n_pairs) {
       int h, task, l;
       map_tile(s_prefix, s_sigma, a.M_pad, v, h, task, l);
@@ -368,6 +377,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int kb = 0; kb < a.num_kb; ++kb, ++g) {
         const int s = g % kSt;
         wait_timed<kProf>(empty_bar(s), ((g / kSt) & 1u) ^ 1u, c_wait);
+        if constexpr (kProf) {
+          if (lane == 0) {
+            const long long now = clock64();
+            if (g >= (uint32_t)kSt) c_rel += now - s_ts[2 * kSt + s];   // slot's previous commit
+            s_ts[s] = now;
+          }
+        }
 #ifdef MOE_EXPERIMENTS
         if (a.experiment == 2) {
           if (lane == 0 && rank == 0) mbar_arrive(full_bar(s));
@@ -403,6 +419,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) {
         a.prof[blockIdx.x * kProfSlots + kProfBWaitEmpty] = c_wait;
         a.prof[blockIdx.x * kProfSlots + kProfBTotal] = clock64() - c_t0;
+        a.prof[blockIdx.x * kProfSlots + kProfRelease] = c_rel;
       }
     }
   } else if (warp == kMmaWarp) {
@@ -411,7 +428,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t g = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      long long c_tmem = 0, c_full = 0, c_t0 = kProf ? clock64() : 0;
+      long long c_tmem = 0, c_full = 0, c_t0 = kProf ? clock64() : 0, c_lb = 0, c_la = 0, c_ns = 0;
       int n_tiles = 0;
       for (int v = pair_id; v < total; v += n_pairs) {
         ++n_tiles;
@@ -431,6 +448,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int s = g % kSt;
           const uint32_t par = (g / kSt) & 1u;
           wait_timed<kProf>(full_bar(s), par, c_full);                   // both CTAs' bytes landed
+          if constexpr (kProf) {
+            const long long now = clock64();
+            c_lb += now - s_ts[s];
+            c_la += now - s_ts[kSt + s];
+            ++c_ns;
+          }
           tc_fence_after();
           if (lane == 0) {
             const uint32_t a0 = sA + s * kABytes;
@@ -455,6 +478,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 else mma_bf16(d_tmem, ad, bd, idesc, (kb | kk) != 0);
               }
             }
+            if constexpr (kProf) s_ts[2 * kSt + s] = clock64();
             if constexpr (kCta == 2) mma_commit_pair(empty_bar(s), 0x3);  // frees the slot in both CTAs
             else mma_commit(empty_bar(s));
           }
@@ -477,6 +501,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           o[kProfMmaWaitFull] = c_full;
           o[kProfMmaTotal] = clock64() - c_t0;
           o[kProfTiles] = n_tiles;
+          o[kProfLatB] = c_lb;
+          o[kProfLatA] = c_la;
+          o[kProfStages] = c_ns;
         }
       }
     } else if (lane == 0) {

@@ -62,6 +62,10 @@ def main():
         "a_cpwait_frac": float((pall[:, 8] / pall[:, 7]).mean()),
         "a_arrive_frac": float((pall[:, 9] / pall[:, 7]).mean()),
         "b_wait_empty_frac": float((pall[:, 10] / pall[:, 11]).mean()),
+        "fill_latency_b_cycles": float((p[:, 12] / p[:, 15]).mean()),
+        "fill_latency_a_cycles": float((p[:, 13] / p[:, 15]).mean()),
+        "release_to_reissue_cycles": float((p[:, 14] / p[:, 15]).mean()),
+        "mma_cycles_per_stage": float((tot / p[:, 15]).mean()),
     }
     if bm == 256:
         q = pall[1::2]
