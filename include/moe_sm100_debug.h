@@ -27,7 +27,7 @@ moe_status moe_probe_gather4(const void* X_dev, int64_t T, int64_t H, const int3
  * moe_gemm with per-CTA cycle counters (an instrumented build of the same
  * kernel; clock64() around every mbarrier wait).  prof_dev: device int64 array of
  * grid * 16 words, grid = CTAs launched (min(total tiles, SMs) for bm=128; 2*min(total, SMs/2)
- * for bm=256); per CTA:
+ * for bm=256; 4*min(total, SMs/4) for bm=256, bn=512); per CTA:
  *   [0] MMA warp cycles waiting for a free TMEM accumulator (epilogue-bound time)
  *   [1] MMA warp cycles waiting for TMA bytes (load-bound time)
  *   [2] MMA warp cycles in its tile loop
@@ -36,8 +36,8 @@ moe_status moe_probe_gather4(const void* X_dev, int64_t T, int64_t H, const int3
  *   [5] the same warp's cycles draining TMEM and storing Y
  *   [6] tiles processed by the CTA
  *   [7] producer warp 0 cycles in its tile loop
- *   [8] producer warp 0 cycles in cp.async.wait_group (cp.async A path)
- *   [9] producer warp 0 cycles fencing and arriving on the full barrier
+ *   [8] MMA warp cycles from "stage full" observed to the stage's commit issued
+ *   [9] MMA warp cycles between tiles (decode + waiting for the accumulator)
  *   [10] B warp cycles waiting for a free stage    [11] B warp cycles in its tile loop
  *   [12] sum over stages of (MMA warp sees the stage full) - (B warp issued its TMA)
  *   [13] the same from A warp 0's issue of its row copies

@@ -271,7 +271,7 @@ def moe_gemm(plan: Plan, X, token_idx, W, Y=None, out_dtype=None, stream=None, r
 
 
 PROF_SLOTS = ("mma_wait_tmem", "mma_wait_full", "mma_total", "prod_wait_empty", "epi_wait_full", "epi_work",
-              "tiles", "prod_total", "a_cp_wait", "a_arrive", "b_wait_empty", "b_total", "lat_b", "lat_a",
+              "tiles", "prod_total", "mma_issue", "mma_tile_gap", "b_wait_empty", "b_total", "lat_b", "lat_a",
               "release", "stages")
 
 

@@ -28,6 +28,7 @@
 
 #include <climits>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 
 #include "common.h"
@@ -78,8 +79,10 @@ struct GemmArgs {
   int32_t a_mode;            // A staging: 0 = TMA tile::gather4, 1 = cp.async (LSU path), see DESIGN.md
   int32_t H;
   const __nv_bfloat16* X;
-  int32_t experiment;        // MOE_EXPERIMENTS builds only (timing studies, wrong Y): 1 = no A reads, 2 = no B loads
+  int32_t experiment;        // MOE_EXPERIMENTS builds only (timing studies, wrong Y), bit mask: 1 = no A reads,
+                             // 2 = no B loads, 4 = A as contiguous tile TMA (pairs), 8 = no Y stores
   const int32_t* y_row_map;  // nullable: Y row of CSR row i is y_row_map[i] (EP combine buffer)
+  int32_t tma_store;         // bf16 Y in CSR row order: full 32-row quarters leave through TMA tile stores
 };
 
 // Per-CTA counters written by the instrumented build (kProf = true).
@@ -92,8 +95,8 @@ enum ProfSlot {
   kProfEpiWork,           // epilogue warp (quarter 0): cycles draining + storing
   kProfTiles,             // tiles processed by the CTA
   kProfProdTotal,         // producer warp 0: cycles in its tile loop
-  kProfACpWait,           // producer warp 0: cycles in cp.async.wait_group
-  kProfAArrive,           // producer warp 0: cycles fencing + arriving
+  kProfMmaIssue,          // MMA warp: cycles from `full` observed to the stage's commit issued
+  kProfMmaTileGap,        // MMA warp: cycles between tiles (decode + accumulator hand-off)
   kProfBWaitEmpty,        // B warp: cycles waiting for a free stage
   kProfBTotal,            // B warp: cycles in its tile loop
   kProfLatB,              // sum over stages: MMA sees `full` - B warp issued the W TMA (this CTA)
@@ -207,18 +210,25 @@ struct Geo {
   static constexpr int kStages = kCta == 2 ? 6 : 4;     // a 7th pair stage measured no gain (NOTES)
   static_assert(8 * (2 * kStages + 4) + 4 <= kBarBytes, "barrier block overlaps TilePrefix");
   static constexpr int kBStage = kBStageBytes / kCta;            // bytes of W per CTA per stage
-  // CTA pairs: a 4 KB transpose buffer per epilogue warp for swap-AB tail tiles (MOE_SPLIT_TAIL).
-  static constexpr int kEpiStage = kSplit ? kEpiWarps * 32 * 32 * 4 : 0;
+  // 4 KB per epilogue warp: two 2 KB bf16 staging buffers for the TMA-store epilogue, or the
+  // transpose buffer of swap-AB tail tiles (MOE_SPLIT_TAIL).
+  static constexpr int kEpiStage = kEpiWarps * 32 * 32 * 4;
   static constexpr size_t kSmem = 1024 + (size_t)kStages * (kABytes + kBStage) + kEpiStage + kBarBytes;
 };
 
 // kSplit: the plan carries MOE_SPLIT_TAIL (kind-1 tail tiles exist); a separate instantiation so
 // the plain path carries none of the swap-AB code.
-template <bool kProf, int kCta, bool kSplit>
+// kMc: cluster tiles (bm = 256, bn = 512): a cluster of four CTAs = two CTA pairs side by side in N.
+// Both pairs need the same 256 token rows; each CTA gathers half of its 128 rows with tile::gather4
+// and multicasts them to itself and to its twin in the other pair (crank ^ 2), so every token row
+// crosses L2 -> SM once per cluster instead of once per pair.
+template <bool kProf, int kCta, bool kSplit, bool kMc = false>
 __global__ void __launch_bounds__(kThreads, 1)
     moe_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
-                    const GemmArgs a) {
+                    const __grid_constant__ CUtensorMap tmY, const GemmArgs a) {
   static_assert(!kSplit || kCta == 2, "swap-AB tail tiles need CTA pairs (M = 256)");
+  static_assert(!kMc || (kCta == 2 && !kSplit), "cluster tiles are built from CTA pairs");
+  constexpr int kCl = kMc ? 4 : kCta;                      // CTAs per cluster (one scheduling unit)
   constexpr int kSt = Geo<kCta, kSplit>::kStages;
   constexpr int kBSt = Geo<kCta, kSplit>::kBStage;
   extern __shared__ uint8_t smem_raw[];
@@ -245,20 +255,25 @@ __global__ void __launch_bounds__(kThreads, 1)
   int total = a.total;
   // CTA pair: rank 0 (leader) issues the MMAs for both CTAs; all consumers of the
   // data path (full / tmem-empty barriers) live in the leader.
-  const uint32_t rank = kCta == 2 ? cluster_ctarank() : 0;
-  const int pair_id = blockIdx.x / kCta;
-  const int n_pairs = gridDim.x / kCta;
-  auto leader = [&](uint32_t addr) { return kCta == 2 ? mapa_shared(addr, 0) : addr; };
+  const uint32_t crank = kCta == 2 ? cluster_ctarank() : 0;   // rank in the cluster
+  const uint32_t rank = crank & 1u;                            // rank in the CTA pair (0 = leader)
+  const uint32_t pr = crank >> 1;                              // kMc: the pair's column half of the tile
+  const int pair_id = blockIdx.x / kCl;                        // scheduling unit (CTA, pair or cluster)
+  const int n_pairs = gridDim.x / kCl;
+  auto leader = [&](uint32_t addr) { return kCta == 2 ? mapa_shared(addr, crank & ~1u) : addr; };
 
-  const int a_mode = kCta == 2 ? 1 : a.a_mode;
+  const int a_mode = kMc ? 0 : kCta == 2 ? 1 : a.a_mode;
   if (threadIdx.x == 0) {
     // full[s] arrivals: A stage done (gather4: one expect_tx per A warp; cp.async: one asynchronous
     // arrive per A thread), the B warp's expect_tx (leader), and in a pair the peer's relay (leader).
-    const uint32_t a_arrivals = a_mode == 0 ? kAWarps : 32 * kAWarps;
-    const uint32_t full_count = a_arrivals + (rank == 0 ? 1u + (kCta == 2 ? 1u : 0u) : 0u);
+    // kMc: every CTA's B warp registers the A and B bytes of its stage (A arrives partly from the
+    // twin CTA's multicast), plus the peer's relay in the leader.
+    const uint32_t a_arrivals = kMc ? 0u : a_mode == 0 ? kAWarps : 32 * kAWarps;
+    const uint32_t full_count =
+        kMc ? 1u + (rank == 0 ? 1u : 0u) : a_arrivals + (rank == 0 ? 1u + (kCta == 2 ? 1u : 0u) : 0u);
     for (int s = 0; s < kSt; ++s) {
       mbar_init(full_bar(s), full_count);
-      mbar_init(empty_bar(s), 1);
+      mbar_init(empty_bar(s), kMc ? 2 : 1);   // kMc: a slot is free once BOTH pairs consumed it
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(tfull_bar(i), 1);
@@ -269,6 +284,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmX);
     prefetch_tmap(&tmW);
+    if (a.tma_store) prefetch_tmap(&tmY);
   }
   if (warp == kMmaWarp) tmem_alloc<kTmemCols, kCta>(smem_u32(tmem_holder));
   pdl_wait();                                        // routing / plan of this step are complete
@@ -294,7 +310,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint64_t pol_x = policy_evict_last();    // X_e is re-read by every column tile of the task
     const int p = warp;
     uint32_t g = 0;                                 // stages issued by this warp, over all tiles
-    long long c_wait = 0, c_t0 = kProf ? clock64() : 0, c_cpw = 0, c_arr = 0;
+    long long c_wait = 0, c_t0 = kProf ? clock64() : 0;
     const int ch = threadIdx.x & 7;                 // cp.async: 16-byte chunk of the 128-byte row
     const int rsub = threadIdx.x >> 3;              // cp.async: row within a 16-row group
     const uint32_t dst_off = rsub * 128 + ((ch ^ (rsub & 7)) << 4);
@@ -308,7 +324,27 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int rbeg = kSplit && t.kind == 1 ? (int)rank * n_alloc : t.rt * kPairRows + (int)rank * kBM;
       const int nvalid = min(n_alloc, t.rows - rbeg);   // may be <= 0 for the second CTA of a pair tile
       const int32_t* idx = a.token_idx + t.row0;
-      if (a_mode == 0) {
+      if constexpr (kMc) {
+        // Rows [64 pr, 64 pr + 64) of this CTA's 128: warp p gathers 16 rows (lanes 0-3, 4 rows each)
+        // and multicasts them to this CTA and its twin; rows past the task's end repeat its last
+        // valid token (never stored).
+        const uint16_t mask = (uint16_t)((1u << crank) | (1u << (crank ^ 2u)));
+        const int rr = 64 * (int)pr + 16 * p + 4 * (lane & 3);
+        const int r0 = __ldg(idx + rbeg + min(rr + 0, nvalid - 1));
+        const int r1 = __ldg(idx + rbeg + min(rr + 1, nvalid - 1));
+        const int r2 = __ldg(idx + rbeg + min(rr + 2, nvalid - 1));
+        const int r3 = __ldg(idx + rbeg + min(rr + 3, nvalid - 1));
+        for (int kb = 0; kb < a.num_kb; ++kb, ++g) {
+          const int s = g % kSt;
+          wait_timed<kProf>(empty_bar(s), ((g / kSt) & 1u) ^ 1u, c_wait);
+          if constexpr (kProf) {
+            if (p == 0 && lane == 0) s_ts[kSt + s] = clock64();
+          }
+          if (lane < 4)
+            tma_gather4_mc(&tmX, full_bar(s), sA + s * kABytes + rr * 128, kb * kBK, r0, r1, r2, r3, mask, pol_x);
+          __syncwarp();
+        }
+      } else if (a_mode == 0) {
         // Rows past the task's end repeat its last valid token (their results are never stored).
         const int rr = 32 * p + 4 * (lane & 7);
         const int r0 = __ldg(idx + rbeg + min(rr + 0, nvalid - 1));
@@ -338,13 +374,30 @@ __global__ void __launch_bounds__(kThreads, 1)
           if constexpr (kProf) {
             if (p == 0 && lane == 0) s_ts[kSt + s] = clock64();
           }
+#ifdef MOE_EXPERIMENTS
+          if (kCta == 2 && (a.experiment & 4)) {
+            // 128 CONTIGUOUS X rows by one tile TMA into the leader's barrier (wrong Y: timing only).
+            if (p == 0 && lane == 0) {
+              const int xr = (t.row0 + rbeg) % max(1, a.T - kBM);
+              tma_load_2d_pair(&tmX, leader(full_bar(s)), sA + s * kABytes, kb * kBK, xr, pol_x);
+            }
+            mbar_arrive(full_bar(s));
+            continue;
+          }
+#endif
+#ifdef MOE_EXPERIMENTS
+          if (a.experiment & 32) {   // no cp.async at all: plain arrivals (timing only)
+            mbar_arrive(full_bar(s));
+            continue;
+          }
+#endif
           const int kcol = kb * kBK;
           const bool colok = kcol + ch * 8 < a.H;
           const uint32_t dst = sA + s * kABytes + dst_off;
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
 #ifdef MOE_EXPERIMENTS
-            const bool ok = a.experiment != 1 && colok && ((rowok >> j) & 1u);
+            const bool ok = !(a.experiment & 1) && colok && ((rowok >> j) & 1u);
 #else
             const bool ok = colok && ((rowok >> j) & 1u);
 #endif
@@ -358,8 +411,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (p == 0 && lane == 0) {
         a.prof[blockIdx.x * kProfSlots + kProfProdWaitEmpty] = c_wait;
         a.prof[blockIdx.x * kProfSlots + kProfProdTotal] = clock64() - c_t0;
-        a.prof[blockIdx.x * kProfSlots + kProfACpWait] = c_cpw;
-        a.prof[blockIdx.x * kProfSlots + kProfAArrive] = c_arr;
       }
     }
   } else if (warp == kBWarp) {
@@ -371,8 +422,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       int h, task, l;
       map_tile(s_prefix, s_sigma, a.M_pad, v, h, task, l);
       const Tile t = load_tile<kSplit>(params, task, l);
-      const int bnc = t.bn / kCta;                  // columns of the block staged by this CTA
-      const int n0 = t.ct * t.bn + (int)rank * bnc;
+      const int bnp = kMc ? t.bn / 2 : t.bn;         // columns of the pair's MMA
+      const int bnc = bnp / kCta;                   // columns of the block staged by this CTA
+      const int n0 = t.ct * t.bn + (int)pr * bnp + (int)rank * bnc;
       const int nbox = (bnc + 63) >> 6;
       for (int kb = 0; kb < a.num_kb; ++kb, ++g) {
         const int s = g % kSt;
@@ -385,7 +437,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
 #ifdef MOE_EXPERIMENTS
-        if (a.experiment == 2) {
+        if (a.experiment & 2) {
           if (lane == 0 && rank == 0) mbar_arrive(full_bar(s));
           __syncwarp();
           continue;
@@ -393,9 +445,22 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
         if (lane == 0) {
           const uint32_t dstB = sB + s * kBSt;
-          if constexpr (kCta == 2) {
+          if constexpr (kMc) {
+            // Own full barrier: this stage's A bytes (own + twin's multicast) and this CTA's W share.
+            mbar_arrive_expect_tx(full_bar(s), kABytes + nbox * kBBoxBytes);
+            if (a.w4d) {
+              tma_load_4d(&tmW, full_bar(s), dstB, 0, kb * kBK, n0 >> 6, t.expert, pol_w);
+            } else {
+              for (int j = 0; j < nbox; ++j)
+                tma_load_3d(&tmW, full_bar(s), dstB + j * kBBoxBytes, n0 + j * 64, kb * kBK, t.expert, pol_w);
+            }
+          } else if constexpr (kCta == 2) {
             const uint32_t fb = leader(full_bar(s));
+#ifdef MOE_EXPERIMENTS
+            if (rank == 0) mbar_arrive_expect_tx(full_bar(s), kCta * nbox * kBBoxBytes + ((a.experiment & 4) ? kCta * kABytes : 0));
+#else
             if (rank == 0) mbar_arrive_expect_tx(full_bar(s), kCta * nbox * kBBoxBytes);
+#endif
             if (a.w4d) {
               tma_load_4d_pair(&tmW, fb, dstB, 0, kb * kBK, n0 >> 6, t.expert, pol_w);
             } else {
@@ -429,6 +494,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       long long c_tmem = 0, c_full = 0, c_t0 = kProf ? clock64() : 0, c_lb = 0, c_la = 0, c_ns = 0;
+      long long c_issue = 0, c_gap = 0, t_end = 0;
       int n_tiles = 0;
       for (int v = pair_id; v < total; v += n_pairs) {
         ++n_tiles;
@@ -440,19 +506,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         // kind 1: D[cols, tokens] = A[W block as MN-major M-operand] * B[tail tokens (K-major)],
         //         M = the pair's 256 output columns, N = the tail height (swap-AB).
         const uint32_t idesc = swap ? idesc_bf16_f32(kPairRows, t.height, /*A MN-major*/ 1, /*B K-major*/ 0)
-                                    : idesc_bf16_f32(kPairRows, t.bn, /*A K-major*/ 0, /*B MN-major*/ 1);
+                                    : idesc_bf16_f32(kPairRows, kMc ? t.bn / 2 : t.bn, /*A K-major*/ 0,
+                                                     /*B MN-major*/ 1);
         wait_timed<kProf>(tempty_bar(acc), acc_phase ^ 1u, c_tmem);     // epilogue(s) drained this accumulator
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * kAccCols;
         for (int kb = 0; kb < a.num_kb; ++kb, ++g) {
           const int s = g % kSt;
           const uint32_t par = (g / kSt) & 1u;
+          if constexpr (kProf) {
+            if (kb == 0 && n_tiles > 1) c_gap += clock64() - t_end;   // decode + accumulator hand-off
+          }
           wait_timed<kProf>(full_bar(s), par, c_full);                   // both CTAs' bytes landed
+          long long t_i = 0;
           if constexpr (kProf) {
             const long long now = clock64();
             c_lb += now - s_ts[s];
             c_la += now - s_ts[kSt + s];
             ++c_ns;
+            t_i = now;
           }
           tc_fence_after();
           if (lane == 0) {
@@ -461,6 +533,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             // Token rows: K-major SW128, 8-row groups 1024 B apart; K step of 16 = +32 B in the row.
             // W block: MN-major SW128; 64-wide chunks 8 KB apart (LBO), 8-row K groups 1 KB apart
             // (SBO); K step of 16 rows = +2 KB.  The two kinds only swap the operand roles.
+#ifdef MOE_EXPERIMENTS
+            if (a.experiment & 16) {   // B read as K-major (wrong Y): is the MN-major B operand slower?
+              const uint32_t idk = idesc_bf16_f32(kPairRows, kMc ? t.bn / 2 : t.bn, 0, 0);
+#pragma unroll
+              for (int kk = 0; kk < kBK / 16; ++kk) {
+                const uint64_t ad = smem_desc_sw128(a0 + kk * 32, 16, 1024);
+                const uint64_t bd = smem_desc_sw128(b0 + kk * 32, 16, 1024);
+                if constexpr (kCta == 2) mma_bf16_pair(d_tmem, ad, bd, idk, (kb | kk) != 0);
+                else mma_bf16(d_tmem, ad, bd, idk, (kb | kk) != 0);
+              }
+            } else
+#endif
             if (!kSplit || !swap) {
 #pragma unroll
               for (int kk = 0; kk < kBK / 16; ++kk) {
@@ -479,13 +563,17 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
             if constexpr (kProf) s_ts[2 * kSt + s] = clock64();
-            if constexpr (kCta == 2) mma_commit_pair(empty_bar(s), 0x3);  // frees the slot in both CTAs
+            if constexpr (kMc) mma_commit_pair(empty_bar(s), 0xF);        // all four CTAs (A is shared)
+            else if constexpr (kCta == 2) mma_commit_pair(empty_bar(s), 0x3);  // frees the slot in both CTAs
             else mma_commit(empty_bar(s));
           }
           __syncwarp();
+          if constexpr (kProf) c_issue += clock64() - t_i;
         }
+        if constexpr (kProf) t_end = clock64();
         if (lane == 0) {
-          if constexpr (kCta == 2) mma_commit_pair(tfull_bar(acc), 0x3);  // accumulator ready in both CTAs
+          if constexpr (kCta == 2)   // accumulator ready in both CTAs of this pair
+            mma_commit_pair(tfull_bar(acc), (uint16_t)(0x3u << (crank & 2u)));
           else mma_commit(tfull_bar(acc));
         }
         __syncwarp();
@@ -504,6 +592,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           o[kProfLatB] = c_lb;
           o[kProfLatA] = c_la;
           o[kProfStages] = c_ns;
+          o[kProfMmaIssue] = c_issue;
+          o[kProfMmaTileGap] = c_gap;
         }
       }
     } else if (lane == 0) {
@@ -522,6 +612,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q = warp & 3;                                   // TMEM lane quarter of this warp
     int acc = 0;
     uint32_t acc_phase = 0;
+    uint32_t n_chunk = 0;                                     // TMA-store chunks issued by this warp
+    const uint32_t ebuf = sEpi + (uint32_t)(warp - (kMmaWarp + 1)) * 4096u;
     long long c_wait = 0, c_work = 0;
     for (int v = pair_id; v < total; v += n_pairs) {
       int h, task, l;
@@ -581,14 +673,50 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool valid = grow < t.rows;
       const int64_t yrow = a.y_row_map ? (int64_t)__ldg(a.y_row_map + t.row0 + min(grow, t.rows - 1))
                                        : (int64_t)t.row0 + grow;
-      const int n0 = t.ct * t.bn;
-      const int col_end = min(n0 + t.bn, a.N);
+      const int bnp = kMc ? t.bn / 2 : t.bn;        // this pair's columns of the tile
+      const int n0 = t.ct * t.bn + (int)pr * bnp;
+      const int col_end = min(n0 + bnp, a.N);
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * kAccCols;
-      for (int c = 0; c < t.bn; c += 32) {
-        uint32_t r[32];
-        tmem_ld32(taddr + c, r);
-        tmem_wait_ld();
-        if (valid) store_chunk(a, yrow, n0 + c, col_end, r);
+      const int wrow0 = grow - lane;                          // first task row of this warp's quarter
+      if (!kSplit && a.tma_store && wrow0 + 32 <= t.rows) {
+        // All 32 rows belong to the task: convert to bf16 into a 64B-swizzled 32 x 32 staging buffer
+        // (conflict-free 16-byte st.shared) and let TMA write the block; two buffers alternate, so
+        // the conversion of chunk i+1 overlaps the store of chunk i.  Partial quarters (the task's
+        // last rows) take the masked register path below: a box must not touch the next task's rows.
+        const uint32_t xr = (uint32_t)((lane >> 1) & 3);
+        for (int c = 0; c < bnp && n0 + c < a.N; c += 32) {
+          uint32_t r[32];
+          tmem_ld32(taddr + c, r);
+          tmem_wait_ld();
+          const uint32_t buf = ebuf + (n_chunk & 1u) * 2048u;
+          if (lane == 0) bulk_wait_group_read<1>();         // the store issued two chunks ago has read buf
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            st_shared_v4(buf + lane * 64 + ((j ^ xr) << 4), pack_bf16(r[8 * j], r[8 * j + 1]),
+                         pack_bf16(r[8 * j + 2], r[8 * j + 3]), pack_bf16(r[8 * j + 4], r[8 * j + 5]),
+                         pack_bf16(r[8 * j + 6], r[8 * j + 7]));
+          fence_proxy_async_smem();
+          __syncwarp();
+#ifdef MOE_EXPERIMENTS
+          if (!(a.experiment & 8))
+#endif
+          if (lane == 0) {
+            tma_store_2d(&tmY, buf, n0 + c, t.row0 + wrow0);
+            bulk_commit_group();
+          }
+          ++n_chunk;
+        }
+      } else {
+        for (int c = 0; c < bnp; c += 32) {
+          uint32_t r[32];
+          tmem_ld32(taddr + c, r);
+          tmem_wait_ld();
+#ifdef MOE_EXPERIMENTS
+          if (a.experiment & 8) continue;
+#endif
+          if (valid) store_chunk(a, yrow, n0 + c, col_end, r);
+        }
       }
       tc_fence_before();
       __syncwarp();
@@ -602,6 +730,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         acc_phase ^= 1u;
       }
     }
+    if (lane == 0) bulk_wait_group<0>();                      // TMA stores complete before exit
     if constexpr (kProf) {
       if (q == 0 && lane == 0) {
         a.prof[blockIdx.x * kProfSlots + kProfEpiWaitFull] = c_wait;
@@ -681,17 +810,31 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-moe_status make_x_map(CUtensorMap* m, const void* X, int64_t T, int64_t H) {
+moe_status make_x_map(CUtensorMap* m, const void* X, int64_t T, int64_t H, int box_rows = 1) {
   auto fn = encode_fn();
   if (!fn) MOE_FAIL(MOE_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
   const cuuint64_t dims[2] = {(cuuint64_t)H, (cuuint64_t)T};
   const cuuint64_t strides[1] = {(cuuint64_t)H * 2};
-  const cuuint32_t box[2] = {(cuuint32_t)kBK, 1};   // gather4: 4 rows of one box row each
+  const cuuint32_t box[2] = {(cuuint32_t)kBK, (cuuint32_t)box_rows};   // gather4: box_rows = 1
   const cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(X), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) MOE_FAIL(MOE_ERR_CUDA, "cuTensorMapEncodeTiled(X) failed: %d", (int)r);
+  return MOE_OK;
+}
+
+// Y viewed as {N, R} bf16 rows; box 32 x 32 with the 64-byte swizzle (the epilogue's staging layout).
+moe_status make_y_map(CUtensorMap* m, void* Y, int64_t R, int64_t N) {
+  auto fn = encode_fn();
+  if (!fn) MOE_FAIL(MOE_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
+  const cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)R};
+  const cuuint64_t strides[1] = {(cuuint64_t)N * 2};
+  const cuuint32_t box[2] = {32, 32};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Y, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) MOE_FAIL(MOE_ERR_CUDA, "cuTensorMapEncodeTiled(Y) failed: %d", (int)r);
   return MOE_OK;
 }
 
@@ -755,18 +898,20 @@ extern "C" moe_status moe_device_info(int32_t* sm_count, int32_t* cc_major, int3
 
 namespace {
 
-template <bool kProf, int kCta, bool kSplit>
+template <bool kProf, int kCta, bool kSplit, bool kMc = false>
 cudaError_t set_attr() {
-  return cudaFuncSetAttribute(moe_gemm_kernel<kProf, kCta, kSplit>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)(Geo<kCta, kSplit>::kSmem + 8 * kMaxMPad));
+  return cudaFuncSetAttribute(moe_gemm_kernel<kProf, kCta, kSplit, kMc>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(Geo<kCta, kSplit>::kSmem + 8 * kMaxMPad));
 }
 
 cudaError_t set_smem_attrs() {
   static std::once_flag once;
   static cudaError_t err = cudaSuccess;
   std::call_once(once, [] {
-    cudaError_t e[6] = {set_attr<false, 1, false>(), set_attr<true, 1, false>(), set_attr<false, 2, false>(),
-                        set_attr<true, 2, false>(), set_attr<false, 2, true>(), set_attr<true, 2, true>()};
+    cudaError_t e[8] = {set_attr<false, 1, false>(),      set_attr<true, 1, false>(),
+                        set_attr<false, 2, false>(),      set_attr<true, 2, false>(),
+                        set_attr<false, 2, true>(),       set_attr<true, 2, true>(),
+                        set_attr<false, 2, false, true>(), set_attr<true, 2, false, true>()};
     for (cudaError_t x : e)
       if (x != cudaSuccess && err == cudaSuccess) err = x;
   });
@@ -806,12 +951,41 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
   if (v.M_pad > kMaxMPad) MOE_FAIL(MOE_ERR_CAPACITY, "moe_gemm: %d tasks exceed %d", v.M_pad, kMaxMPad);
 
   CUtensorMap tmX, tmW;
-  moe_status st = make_x_map(&tmX, X, T, v.H);
+  int experiment = 0;
+#ifdef MOE_EXPERIMENTS
+  {
+    const char* ex = getenv("MOE_GEMM_EXPERIMENT");
+    experiment = ex ? atoi(ex) : 0;
+  }
+#endif
+  moe_status st = make_x_map(&tmX, X, T, v.H, (experiment & 4) ? kBM : 1);
   if (st != MOE_OK) return st;
   const bool w4d = (v.N % 64) == 0;
-  const int cta = v.bm / kBM;                    // CTAs per tile: each stages bn / cta W columns
+  const bool mc = v.bm == 256 && v.bn > 256;      // cluster tile: two CTA pairs, A multicast
+  const int cta = (v.bm / kBM) * (mc ? 2 : 1);    // CTAs per tile: each stages bn / cta W columns
   st = make_w_map(&tmW, W, v.E, v.H, v.N, v.bn / cta, w4d);
   if (st != MOE_OK) return st;
+
+  // TMA-store epilogue: bf16 Y in CSR row order (the EP combine path scatters rows: register stores).
+  CUtensorMap tmY;
+  std::memset(&tmY, 0, sizeof(tmY));
+  bool tma_store = y_dtype == MOE_DTYPE_BF16 && !y_row_map;
+  {
+    const char* ep = getenv("MOE_EPI_TMA");        // timing studies: 0 = register stores only
+    if (ep && atoi(ep) == 0) tma_store = false;
+  }
+  if (tma_store) {
+    // Rows of Y: the plan's total (host plan); a device plan's count is on the device, so the
+    // map spans 2^31-1 rows — every box the kernel stores lies inside one task's rows.
+    int64_t R = INT_MAX;
+    if (!dev_planned) {
+      int64_t words = 0;
+      const int32_t* blob = moe::plan_blob_host(plan, &words);
+      R = blob[v.off_row_off + v.E];
+    }
+    st = make_y_map(&tmY, Y, R, v.N);
+    if (st != MOE_OK) return st;
+  }
 
   GemmArgs a;
   a.plan = moe::plan_blob_dev(plan);
@@ -826,13 +1000,11 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
   a.w4d = w4d ? 1 : 0;
   a.prof = prof;
   a.y_row_map = y_row_map;
+  a.tma_store = tma_store ? 1 : 0;
   a.T = (int32_t)T;
   a.H = v.H;
   a.X = reinterpret_cast<const __nv_bfloat16*>(X);
-  {
-    const char* ex = getenv("MOE_GEMM_EXPERIMENT");
-    a.experiment = ex ? atoi(ex) : 0;
-  }
+  a.experiment = experiment;
   {
     const char* am = getenv("MOE_A_PATH");       // timing studies: force the A staging path
     a.a_mode = am ? atoi(am) : kDefaultAMode;
@@ -843,16 +1015,17 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
   if (attr_err != cudaSuccess) MOE_FAIL(MOE_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(attr_err));
   if (v.bm == 256) {
     const bool split = (v.flags & MOE_SPLIT_TAIL) != 0;
-    const int pairs = v.total < 0 ? sm_count_cached() / 2 : std::min(v.total, sm_count_cached() / 2);
+    const int ncl = mc ? 4 : 2;                    // CTAs per scheduling unit
+    const int units = v.total < 0 ? sm_count_cached() / ncl : std::min(v.total, sm_count_cached() / ncl);
     const size_t smem = (split ? Geo<2, true>::kSmem : Geo<2, false>::kSmem) + 8 * (size_t)v.M_pad;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(2 * pairs);
+    cfg.gridDim = dim3(ncl * units);
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = (cudaStream_t)stream;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.x = ncl;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // PDL: overlap the prologue
@@ -860,12 +1033,15 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
     cfg.attrs = attr;
     cfg.numAttrs = 2;
     cudaError_t le;
-    if (split)
-      le = prof ? cudaLaunchKernelEx(&cfg, moe_gemm_kernel<true, 2, true>, tmX, tmW, a)
-                : cudaLaunchKernelEx(&cfg, moe_gemm_kernel<false, 2, true>, tmX, tmW, a);
+    if (mc)
+      le = prof ? cudaLaunchKernelEx(&cfg, moe_gemm_kernel<true, 2, false, true>, tmX, tmW, tmY, a)
+                : cudaLaunchKernelEx(&cfg, moe_gemm_kernel<false, 2, false, true>, tmX, tmW, tmY, a);
+    else if (split)
+      le = prof ? cudaLaunchKernelEx(&cfg, moe_gemm_kernel<true, 2, true>, tmX, tmW, tmY, a)
+                : cudaLaunchKernelEx(&cfg, moe_gemm_kernel<false, 2, true>, tmX, tmW, tmY, a);
     else
-      le = prof ? cudaLaunchKernelEx(&cfg, moe_gemm_kernel<true, 2, false>, tmX, tmW, a)
-                : cudaLaunchKernelEx(&cfg, moe_gemm_kernel<false, 2, false>, tmX, tmW, a);
+      le = prof ? cudaLaunchKernelEx(&cfg, moe_gemm_kernel<true, 2, false>, tmX, tmW, tmY, a)
+                : cudaLaunchKernelEx(&cfg, moe_gemm_kernel<false, 2, false>, tmX, tmW, tmY, a);
     if (le != cudaSuccess) MOE_FAIL(MOE_ERR_CUDA, "moe_gemm pair launch: %s", cudaGetErrorString(le));
   } else {
     const int grid = v.total < 0 ? sm_count_cached() : std::min(v.total, sm_count_cached());
@@ -879,8 +1055,8 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t le = prof ? cudaLaunchKernelEx(&cfg, moe_gemm_kernel<true, 1, false>, tmX, tmW, a)
-                          : cudaLaunchKernelEx(&cfg, moe_gemm_kernel<false, 1, false>, tmX, tmW, a);
+    cudaError_t le = prof ? cudaLaunchKernelEx(&cfg, moe_gemm_kernel<true, 1, false>, tmX, tmW, tmY, a)
+                          : cudaLaunchKernelEx(&cfg, moe_gemm_kernel<false, 1, false>, tmX, tmW, tmY, a);
     if (le != cudaSuccess) MOE_FAIL(MOE_ERR_CUDA, "moe_gemm launch: %s", cudaGetErrorString(le));
   }
   cudaError_t e = cudaGetLastError();

@@ -85,13 +85,15 @@ moe_status moe_plan_build(const int32_t* counts, int32_t E, int64_t H, int64_t N
       r128 += ceil_div(m, 128) * 128;
       r256 += ceil_div(m, 256) * 256;
     }
-    bm = (r256 * 100 <= r128 * 110 && bn % 32 == 0) ? 256 : 128;
+    bm = bn == 512 || (r256 * 100 <= r128 * 110 && bn % 32 == 0) ? 256 : 128;
   }
   if (bm != 128 && bm != 256)
     MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_plan_build: bm=%d unsupported (128: one CTA, 256: CTA pair, 0: auto)", bm);
-  if (bn < 16 || bn > 256 || bn % (bm == 256 ? 32 : 16))
-    MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_plan_build: bn=%d must be a multiple of %d in [16, 256]", bn,
-             bm == 256 ? 32 : 16);
+  // bm = 256, bn = 512: cluster tile (two CTA pairs sharing the tile's token rows by multicast).
+  const bool cluster_tile = bm == 256 && bn == 512;
+  if (!cluster_tile && (bn < 16 || bn > 256 || bn % (bm == 256 ? 32 : 16)))
+    MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_plan_build: bn=%d must be a multiple of %d in [16, 256] (or 512 with bm=256)",
+             bn, bm == 256 ? 32 : 16);
   if (flags & ~(MOE_PAD_REPEAT | MOE_SPLIT_TAIL | MOE_ORDER_ALTERNATING | MOE_ORDER_HALF_INTERVAL))
     MOE_FAIL(MOE_ERR_INVALID, "moe_plan_build: unknown flags 0x%x", flags);
   if ((flags & MOE_ORDER_ALTERNATING) && (flags & MOE_ORDER_HALF_INTERVAL))

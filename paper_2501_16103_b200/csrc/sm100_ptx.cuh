@@ -132,6 +132,14 @@ __device__ __forceinline__ void tma_load_4d_pair(const void* tmap, uint32_t bar_
       "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "l"(policy)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_2d_pair(const void* tmap, uint32_t bar_cluster, uint32_t dst, int32_t c0,
+                                                 int32_t c1, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar_cluster), "r"(c0), "r"(c1), "l"(policy)
+      : "memory");
+}
 __device__ __forceinline__ void tma_load_3d_pair(const void* tmap, uint32_t bar_cluster, uint32_t dst, int32_t c0,
                                                  int32_t c1, int32_t c2, uint64_t policy) {
   asm volatile(
@@ -147,6 +155,17 @@ __device__ __forceinline__ void tma_gather4(const void* tmap, uint32_t bar, uint
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes.L2::cache_hint"
       " [%0], [%1, {%3, %4, %5, %6, %7}], [%2], %8;" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "l"(policy)
+      : "memory");
+}
+// gather4 multicast: the four rows land at the same offset in every CTA of ctaMask, each
+// destination's mbarrier (same offset) receiving the complete_tx.
+__device__ __forceinline__ void tma_gather4_mc(const void* tmap, uint32_t bar, uint32_t dst, int32_t c0, int32_t r0,
+                                               int32_t r1, int32_t r2, int32_t r3, uint16_t mask, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes.multicast::cluster"
+      ".L2::cache_hint [%0], [%1, {%3, %4, %5, %6, %7}], [%2], %8, %9;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "h"(mask),
+      "l"(policy)
       : "memory");
 }
 __device__ __forceinline__ uint64_t policy_evict_last() {
@@ -174,6 +193,26 @@ __device__ __forceinline__ void cp_async_wait() {
 // (.noinc: the arrival counts against the barrier's expected count).  The thread does not block.
 __device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint32_t bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
+}
+// TMA tile store (shared::cta -> global) in a bulk group; wait_group_read<N>: at most N groups
+// may still be reading their shared-memory source.
+__device__ __forceinline__ void tma_store_2d(const void* tmap, uint32_t src, int32_t c0, int32_t c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(tmap)),
+               "r"(src), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit_group() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_group_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_group() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
 // Make this thread's generic-proxy shared-memory writes visible to the async proxy (tcgen05 / TMA).
 __device__ __forceinline__ void fence_proxy_async_smem() {

@@ -38,6 +38,31 @@ def main():
     ev[1].record()
     torch.cuda.synchronize()
     t_plain = ev[0].elapsed_time(ev[1]) / 10
+    # SM clock under this load: NVML sample in the middle of ~300 ms of back-to-back launches.
+    sm_mhz = None
+    try:
+        import threading
+        import time
+        import pynvml
+        pynvml.nvmlInit()
+        hnd = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
+        samples = []
+
+        def sample():
+            time.sleep(0.15)
+            for _ in range(5):
+                samples.append(pynvml.nvmlDeviceGetClockInfo(hnd, pynvml.NVML_CLOCK_SM))
+                time.sleep(0.02)
+        n_launch = max(1, int(300 / max(t_plain, 1e-3)))
+        th = threading.Thread(target=sample)
+        th.start()
+        for _ in range(n_launch):
+            M.moe_gemm(plan, X, tok, W, Y=Y)
+        torch.cuda.synchronize()
+        th.join()
+        sm_mhz = sorted(samples)[len(samples) // 2] if samples else None
+    except Exception:  # pragma: no cover - NVML missing
+        pass
     Y2 = torch.empty_like(Y)
     M.moe_gemm_profile(plan, X, tok, W, Y2)
     ev[0].record()
@@ -50,7 +75,8 @@ def main():
     tot = p[:, 2]
     out = {
         "config": name, "bn": bn, "bm": bm, "flags": flags, "tiles": plan.total_tiles, "ms_plain": t_plain, "ms_instrumented": t_prof,
-        "tflops_plain": c.flops / t_plain / 1e9,
+        "tflops_plain": c.flops / t_plain / 1e9, "sm_mhz_plain": sm_mhz,
+        "tensor_frac_at_clock": (c.flops / t_plain / 1e9) / (148 * 8192 * sm_mhz * 1e-6) if sm_mhz else None,
         "identical_Y": bool(torch.equal(Y, Y2)),
         "mma_wait_full_frac": float((p[:, 1] / tot).mean()),
         "mma_wait_tmem_frac": float((p[:, 0] / tot).mean()),
@@ -59,8 +85,8 @@ def main():
         "mma_cycles_per_tile": float((tot / p[:, 6]).mean()),
         "mma_loop_cycles_max": float(tot.max()), "mma_loop_cycles_min": float(tot.min()),
         "tiles_per_cta_min": int(p[:, 6].min()), "tiles_per_cta_max": int(p[:, 6].max()),
-        "a_cpwait_frac": float((pall[:, 8] / pall[:, 7]).mean()),
-        "a_arrive_frac": float((pall[:, 9] / pall[:, 7]).mean()),
+        "mma_issue_frac": float((p[:, 8] / tot).mean()),
+        "mma_tile_gap_frac": float((p[:, 9] / tot).mean()),
         "b_wait_empty_frac": float((pall[:, 10] / pall[:, 11]).mean()),
         "fill_latency_b_cycles": float((p[:, 12] / p[:, 15]).mean()),
         "fill_latency_a_cycles": float((p[:, 13] / p[:, 15]).mean()),
@@ -69,7 +95,6 @@ def main():
     }
     if bm == 256:
         q = pall[1::2]
-        out["peer_a_cpwait_frac"] = float((q[:, 8] / q[:, 7]).mean())
         out["peer_a_wait_empty_frac"] = float((q[:, 3] / q[:, 7]).mean())
         out["peer_b_wait_empty_frac"] = float((q[:, 10] / q[:, 11]).mean())
     print(json.dumps(out))
