@@ -190,7 +190,7 @@ def run_reference(args, cfg):
 def config_dict(cfg, args):
     return {"workload": f"{cfg.name}: E={cfg.E} top-{cfg.k} T={cfg.T} H={cfg.H} N={cfg.N} "
                         f"routing={cfg.routing} seed={args.seed}",
-            "tile": f"{getattr(args, 'bm_resolved', args.bm) or 'auto'}x{args.bn}", "out_dtype": args.out_dtype,
+            "tile": f"{getattr(args, 'bm_resolved', args.bm) or 'auto'}x{getattr(args, 'bn_resolved', args.bn) or 'auto'}", "out_dtype": args.out_dtype,
             "planner": "host (counts D2H + moe_plan_update)" if args.host_plan else "device (moe_plan_device)", "global_batch": cfg.T,
             "l2": "flushed before every timed step (256 MiB memset); W alone exceeds L2",
             "parallelism": f"ep{args.gpus}" if args.gpus > 1 else "1 GPU"}
@@ -362,7 +362,7 @@ def run_ours(args, cfg):
         cpu = {"value": f / s / 1e12, "unit": "TFLOP/s", "cores": cores, "kind": "oracle", "sample": sample,
                "seconds": s}
 
-    args.bm_resolved = plan.bm
+    args.bm_resolved, args.bn_resolved = plan.bm, plan.bn
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": ws, "steps": args.steps,
@@ -493,7 +493,7 @@ def run_ep(args, base):
             "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": f"{cfg.name}: E={cfg.E} top-{cfg.k} T={cfg.T} ({T_l}/rank) H={cfg.H} N={cfg.N} "
                                    f"routing={cfg.routing} seed={args.seed}",
-                       "tile": f"{moe.kernels._plans[('ep', args.bm, args.bn)].bm}x{args.bn}",
+                       "tile": f"{moe.kernels._plans[('ep', args.bm, args.bn)].bm}x{moe.kernels._plans[('ep', args.bm, args.bn)].bn}",
                        "out_dtype": args.out_dtype, "global_batch": cfg.T, "parallelism": f"ep{ws}",
                        "collectives": "NCCL all_to_all_single (torch.distributed): counts, dispatch rows, "
                                       "combine rows", "l2": "flushed before every timed step"},
@@ -521,7 +521,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="mix")
     ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--bn", type=int, default=256)
+    ap.add_argument("--bn", type=int, default=0)
     ap.add_argument("--bm", type=int, default=0, help="tile rows: 128 (1 CTA), 256 (CTA pair), 0 = planner's choice")
     ap.add_argument("--out-dtype", choices=["bf16", "f32"], default="bf16")
     ap.add_argument("--no-e2e", action="store_true")

@@ -102,10 +102,13 @@ int64_t moe_plan_blob_words(int32_t E);
  *   bm, bn           tile shape.  bm = 128: one CTA per tile (tcgen05 M=128, cta_group::1);
  *                    bm = 256: a CTA pair per tile (tcgen05 M=256, cta_group::2, each
  *                    CTA 128 rows and half of the W block).  16 <= bn <= 256, bn % 16 == 0
- *                    (bn % 32 == 0 when bm = 256).  bm = 0: automatic — 256 unless the pair
- *                    tiles' extra padding rows exceed their ~10% per-row speed advantage
- *                    (sum of ceil(m_e/256)*256 > 1.10 * sum of ceil(m_e/128)*128).  The blob
- *                    records the resolved bm.
+ *                    (bn % 32 == 0 when bm = 256), or bn = 512 with bm = 256: a wide pair
+ *                    tile (two N = 256 MMA blocks per staged K block, both TMEM accumulators).
+ *                    bm = 0: automatic — 256 unless the pair tiles' extra padding rows exceed
+ *                    their ~10% per-row speed advantage (sum of ceil(m_e/256)*256 > 1.10 *
+ *                    sum of ceil(m_e/128)*128).  bn = 0: automatic — 512 when bm resolves to
+ *                    256, N >= 512 and MOE_SPLIT_TAIL is off, else 256.  The blob records
+ *                    the resolved bm and bn.
  *   flags            MOE_PAD_MAX | MOE_PAD_REPEAT, optionally | MOE_SPLIT_TAIL and one of
  *                    MOE_ORDER_ALTERNATING / MOE_ORDER_HALF_INTERVAL (sigma order, §4.2).
  *   blob, blob_cap   caller buffer of blob_cap int32 words (see moe_plan_blob_words).
@@ -132,7 +135,7 @@ moe_status moe_plan_create(const int32_t* counts_host /* NULL: all zero, for moe
                            int32_t E, int64_t H, int64_t N,
                            int32_t bm, int32_t bn, uint32_t flags, void* stream, moe_plan** out);
 
-/* Re-plan in place for new counts (same E, H, N, bn, flags; the bm resolved at creation is kept);
+/* Re-plan in place for new counts (same E, H, N, flags; the bm, bn resolved at creation are kept);
  * reuses the device buffer. */
 moe_status moe_plan_update(moe_plan* plan, const int32_t* counts_host, void* stream);
 
@@ -143,7 +146,7 @@ moe_status moe_plan_update(moe_plan* plan, const int32_t* counts_host, void* str
  * route -> plan -> moe_gemm can be enqueued (and graph-captured) back to back.  Same
  * arithmetic and layout as moe_plan_build except M_pad = pad32(E) (count-independent).
  * The plan keeps the E, H, N, bm, bn, flags of moe_plan_create (counts_host may be NULL
- * there; bm = 0 then resolves to 256 when bn % 32 == 0).  Requires E <= 1024.  Afterwards
+ * there; bm = 0 then resolves to 256 when bn % 32 == 0, bn = 0 to 512 when N >= 512).  Requires E <= 1024.  Afterwards
  * the host copy is stale: moe_plan_query / moe_plan_blob / moe_decode_debug return
  * MOE_ERR_INVALID until moe_plan_sync; moe_gemm launches one CTA (pair) per SM and reads
  * the tile count from the device blob.  If the counts overflow int32 rows or tiles the

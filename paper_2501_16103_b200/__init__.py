@@ -110,7 +110,7 @@ def _i32ptr(a: np.ndarray):
 # ---------------------------------------------------------------------------
 # plan (host, no GPU needed)
 # ---------------------------------------------------------------------------
-def moe_plan_build(counts, H: int, N: int, bm: int = 0, bn: int = 256, flags: int = MOE_PAD_MAX) -> np.ndarray:
+def moe_plan_build(counts, H: int, N: int, bm: int = 0, bn: int = 0, flags: int = MOE_PAD_MAX) -> np.ndarray:
     """The compressed mapping blob (int32 words, layout in include/moe_sm100.h)."""
     c = np.ascontiguousarray(np.asarray(counts, dtype=np.int32))
     E = int(c.shape[0])
@@ -148,7 +148,7 @@ def _stream(stream=None) -> int:
 class Plan:
     """Device-resident plan (moe_plan_create / moe_plan_update / moe_plan_destroy)."""
 
-    def __init__(self, counts, H: int, N: int, bm: int = 0, bn: int = 256, flags: int = MOE_PAD_MAX,
+    def __init__(self, counts, H: int, N: int, bm: int = 0, bn: int = 0, flags: int = MOE_PAD_MAX,
                  stream=None, E: int | None = None):
         """counts: host int array [E], or None (with E=...) for a plan filled by update_device()."""
         if counts is None:
@@ -162,7 +162,8 @@ class Plan:
         self._h = ctypes.c_void_p()
         self.status = _check(lib().moe_plan_create(cp, self.E, H, N, bm, bn, flags, _stream(stream),
                                                    ctypes.byref(self._h)))
-        self.bm = int(self.blob()[7])            # resolved tile height (bm = 0: automatic)
+        b = self.blob()
+        self.bm, self.bn = int(b[7]), int(b[8])  # resolved tile shape (0: automatic)
         self.device_resident = False
 
     def update_device(self, counts_dev, stream=None):
@@ -360,7 +361,7 @@ def moe_probe_gather4(X, rows, col0: int, stream=None):
     return out
 
 
-def moe_forward(topk_ids, X, W, E: int, bm: int = 0, bn: int = 256, out_dtype=None, plan: Plan | None = None,
+def moe_forward(topk_ids, X, W, E: int, bm: int = 0, bn: int = 0, out_dtype=None, plan: Plan | None = None,
                 stream=None, device_plan: bool = True, Y=None):
     """One MoE expert-GEMM step: route -> plan -> single-launch GEMM.
 

@@ -204,12 +204,13 @@ __device__ __forceinline__ void wait_timed(uint32_t bar, uint32_t parity, long l
 }
 
 // Pipeline geometry per CTA-group size: a CTA pair (cta_group::2) splits the B block across the
-// two CTAs, so a stage is 32 KB instead of 48 KB and six stages fit.
-template <int kCta, bool kSplit = false>
+// two CTAs, so a stage is 32 KB instead of 48 KB and six stages fit.  A wide pair tile (256 x 512,
+// kWide) stages 128 rows + 256 W columns per CTA: 48 KB, four stages.
+template <int kCta, bool kSplit = false, bool kWide = false>
 struct Geo {
-  static constexpr int kStages = kCta == 2 ? 6 : 4;     // a 7th pair stage measured no gain (NOTES)
+  static constexpr int kStages = kWide ? 4 : kCta == 2 ? 6 : 4;   // a 7th pair stage measured no gain (NOTES)
   static_assert(8 * (2 * kStages + 4) + 4 <= kBarBytes, "barrier block overlaps TilePrefix");
-  static constexpr int kBStage = kBStageBytes / kCta;            // bytes of W per CTA per stage
+  static constexpr int kBStage = (kWide ? 2 : 1) * kBStageBytes / kCta;   // bytes of W per CTA per stage
   // 4 KB per epilogue warp: two 2 KB bf16 staging buffers for the TMA-store epilogue, or the
   // transpose buffer of swap-AB tail tiles (MOE_SPLIT_TAIL).
   static constexpr int kEpiStage = kEpiWarps * 32 * 32 * 4;
@@ -218,19 +219,21 @@ struct Geo {
 
 // kSplit: the plan carries MOE_SPLIT_TAIL (kind-1 tail tiles exist); a separate instantiation so
 // the plain path carries none of the swap-AB code.
-// kMc: cluster tiles (bm = 256, bn = 512): a cluster of four CTAs = two CTA pairs side by side in N.
-// Both pairs need the same 256 token rows; each CTA gathers half of its 128 rows with tile::gather4
-// and multicasts them to itself and to its twin in the other pair (crank ^ 2), so every token row
-// crosses L2 -> SM once per cluster instead of once per pair.
-template <bool kProf, int kCta, bool kSplit, bool kMc = false>
+// kWide: wide pair tiles (bm = 256, bn = 512).  Each K block feeds two N = 256 MMAs into the two
+// TMEM accumulators (columns 0-255 and 256-511): every staged token row serves 512 output columns,
+// so per FLOP the tile stages 3/4 of the bytes of a 256 x 256 tile (fewer L2 -> SM bytes, fewer
+// shared-memory fills, half the barrier round trips).  The accumulator is not double-buffered: the
+// MMA waits for the epilogue to drain half 0 before the next tile's first MMAs, half 1 before the
+// next tile's first half-1 MMAs.
+template <bool kProf, int kCta, bool kSplit, bool kWide = false>
 __global__ void __launch_bounds__(kThreads, 1)
     moe_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
                     const __grid_constant__ CUtensorMap tmY, const GemmArgs a) {
   static_assert(!kSplit || kCta == 2, "swap-AB tail tiles need CTA pairs (M = 256)");
-  static_assert(!kMc || (kCta == 2 && !kSplit), "cluster tiles are built from CTA pairs");
-  constexpr int kCl = kMc ? 4 : kCta;                      // CTAs per cluster (one scheduling unit)
-  constexpr int kSt = Geo<kCta, kSplit>::kStages;
-  constexpr int kBSt = Geo<kCta, kSplit>::kBStage;
+  static_assert(!kWide || (kCta == 2 && !kSplit), "wide tiles are CTA-pair tiles");
+  constexpr int kSt = Geo<kCta, kSplit, kWide>::kStages;
+  constexpr int kBSt = Geo<kCta, kSplit, kWide>::kBStage;
+  constexpr int kHalves = kWide ? 2 : 1;                   // N = 256 MMA blocks per tile
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;            // SW128 atoms need 1024-byte alignment
@@ -238,7 +241,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t sA = base;
   const uint32_t sB = sA + kSt * kABytes;
   const uint32_t sEpi = sB + kSt * kBSt;                   // swap-AB transpose buffers (pairs)
-  const uint32_t sBar = sEpi + Geo<kCta, kSplit>::kEpiStage;
+  const uint32_t sBar = sEpi + Geo<kCta, kSplit, kWide>::kEpiStage;
   auto full_bar = [&](int s) { return sBar + 8u * s; };
   auto empty_bar = [&](int s) { return sBar + 8u * (kSt + s); };
   auto tfull_bar = [&](int i) { return sBar + 8u * (2 * kSt + i); };
@@ -255,25 +258,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   int total = a.total;
   // CTA pair: rank 0 (leader) issues the MMAs for both CTAs; all consumers of the
   // data path (full / tmem-empty barriers) live in the leader.
-  const uint32_t crank = kCta == 2 ? cluster_ctarank() : 0;   // rank in the cluster
-  const uint32_t rank = crank & 1u;                            // rank in the CTA pair (0 = leader)
-  const uint32_t pr = crank >> 1;                              // kMc: the pair's column half of the tile
-  const int pair_id = blockIdx.x / kCl;                        // scheduling unit (CTA, pair or cluster)
-  const int n_pairs = gridDim.x / kCl;
-  auto leader = [&](uint32_t addr) { return kCta == 2 ? mapa_shared(addr, crank & ~1u) : addr; };
+  const uint32_t rank = kCta == 2 ? cluster_ctarank() : 0;
+  const int pair_id = blockIdx.x / kCta;
+  const int n_pairs = gridDim.x / kCta;
+  auto leader = [&](uint32_t addr) { return kCta == 2 ? mapa_shared(addr, 0) : addr; };
 
-  const int a_mode = kMc ? 0 : kCta == 2 ? 1 : a.a_mode;
+  const int a_mode = kCta == 2 && !kWide ? 1 : a.a_mode;
   if (threadIdx.x == 0) {
     // full[s] arrivals: A stage done (gather4: one expect_tx per A warp; cp.async: one asynchronous
     // arrive per A thread), the B warp's expect_tx (leader), and in a pair the peer's relay (leader).
-    // kMc: every CTA's B warp registers the A and B bytes of its stage (A arrives partly from the
-    // twin CTA's multicast), plus the peer's relay in the leader.
-    const uint32_t a_arrivals = kMc ? 0u : a_mode == 0 ? kAWarps : 32 * kAWarps;
-    const uint32_t full_count =
-        kMc ? 1u + (rank == 0 ? 1u : 0u) : a_arrivals + (rank == 0 ? 1u + (kCta == 2 ? 1u : 0u) : 0u);
+    const uint32_t a_arrivals = a_mode == 0 ? kAWarps : 32 * kAWarps;
+    const uint32_t full_count = a_arrivals + (rank == 0 ? 1u + (kCta == 2 ? 1u : 0u) : 0u);
     for (int s = 0; s < kSt; ++s) {
       mbar_init(full_bar(s), full_count);
-      mbar_init(empty_bar(s), kMc ? 2 : 1);   // kMc: a slot is free once BOTH pairs consumed it
+      mbar_init(empty_bar(s), 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(tfull_bar(i), 1);
@@ -324,27 +322,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int rbeg = kSplit && t.kind == 1 ? (int)rank * n_alloc : t.rt * kPairRows + (int)rank * kBM;
       const int nvalid = min(n_alloc, t.rows - rbeg);   // may be <= 0 for the second CTA of a pair tile
       const int32_t* idx = a.token_idx + t.row0;
-      if constexpr (kMc) {
-        // Rows [64 pr, 64 pr + 64) of this CTA's 128: warp p gathers 16 rows (lanes 0-3, 4 rows each)
-        // and multicasts them to this CTA and its twin; rows past the task's end repeat its last
-        // valid token (never stored).
-        const uint16_t mask = (uint16_t)((1u << crank) | (1u << (crank ^ 2u)));
-        const int rr = 64 * (int)pr + 16 * p + 4 * (lane & 3);
-        const int r0 = __ldg(idx + rbeg + min(rr + 0, nvalid - 1));
-        const int r1 = __ldg(idx + rbeg + min(rr + 1, nvalid - 1));
-        const int r2 = __ldg(idx + rbeg + min(rr + 2, nvalid - 1));
-        const int r3 = __ldg(idx + rbeg + min(rr + 3, nvalid - 1));
-        for (int kb = 0; kb < a.num_kb; ++kb, ++g) {
-          const int s = g % kSt;
-          wait_timed<kProf>(empty_bar(s), ((g / kSt) & 1u) ^ 1u, c_wait);
-          if constexpr (kProf) {
-            if (p == 0 && lane == 0) s_ts[kSt + s] = clock64();
-          }
-          if (lane < 4)
-            tma_gather4_mc(&tmX, full_bar(s), sA + s * kABytes + rr * 128, kb * kBK, r0, r1, r2, r3, mask, pol_x);
-          __syncwarp();
-        }
-      } else if (a_mode == 0) {
+      if (a_mode == 0) {
         // Rows past the task's end repeat its last valid token (their results are never stored).
         const int rr = 32 * p + 4 * (lane & 7);
         const int r0 = __ldg(idx + rbeg + min(rr + 0, nvalid - 1));
@@ -422,9 +400,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       int h, task, l;
       map_tile(s_prefix, s_sigma, a.M_pad, v, h, task, l);
       const Tile t = load_tile<kSplit>(params, task, l);
-      const int bnp = kMc ? t.bn / 2 : t.bn;         // columns of the pair's MMA
-      const int bnc = bnp / kCta;                   // columns of the block staged by this CTA
-      const int n0 = t.ct * t.bn + (int)pr * bnp + (int)rank * bnc;
+      const int bnp = t.bn / kHalves;               // columns of one MMA block
+      const int bnc = bnp / kCta;                   // columns of an MMA block staged by this CTA
+      const int n0 = t.ct * t.bn + (int)rank * bnc; // block h starts at n0 + h * bnp
       const int nbox = (bnc + 63) >> 6;
       for (int kb = 0; kb < a.num_kb; ++kb, ++g) {
         const int s = g % kSt;
@@ -445,27 +423,25 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
         if (lane == 0) {
           const uint32_t dstB = sB + s * kBSt;
-          if constexpr (kMc) {
-            // Own full barrier: this stage's A bytes (own + twin's multicast) and this CTA's W share.
-            mbar_arrive_expect_tx(full_bar(s), kABytes + nbox * kBBoxBytes);
-            if (a.w4d) {
-              tma_load_4d(&tmW, full_bar(s), dstB, 0, kb * kBK, n0 >> 6, t.expert, pol_w);
-            } else {
-              for (int j = 0; j < nbox; ++j)
-                tma_load_3d(&tmW, full_bar(s), dstB + j * kBBoxBytes, n0 + j * 64, kb * kBK, t.expert, pol_w);
-            }
-          } else if constexpr (kCta == 2) {
+          if constexpr (kCta == 2) {
             const uint32_t fb = leader(full_bar(s));
 #ifdef MOE_EXPERIMENTS
-            if (rank == 0) mbar_arrive_expect_tx(full_bar(s), kCta * nbox * kBBoxBytes + ((a.experiment & 4) ? kCta * kABytes : 0));
+            if (rank == 0)
+              mbar_arrive_expect_tx(full_bar(s), kHalves * kCta * nbox * kBBoxBytes +
+                                                     ((a.experiment & 4) ? kCta * kABytes : 0));
 #else
-            if (rank == 0) mbar_arrive_expect_tx(full_bar(s), kCta * nbox * kBBoxBytes);
+            if (rank == 0) mbar_arrive_expect_tx(full_bar(s), kHalves * kCta * nbox * kBBoxBytes);
 #endif
-            if (a.w4d) {
-              tma_load_4d_pair(&tmW, fb, dstB, 0, kb * kBK, n0 >> 6, t.expert, pol_w);
-            } else {
-              for (int j = 0; j < nbox; ++j)
-                tma_load_3d_pair(&tmW, fb, dstB + j * kBBoxBytes, n0 + j * 64, kb * kBK, t.expert, pol_w);
+#pragma unroll
+            for (int hf = 0; hf < kHalves; ++hf) {
+              const uint32_t dst = dstB + hf * nbox * kBBoxBytes;
+              const int nh = n0 + hf * bnp;
+              if (a.w4d) {
+                tma_load_4d_pair(&tmW, fb, dst, 0, kb * kBK, nh >> 6, t.expert, pol_w);
+              } else {
+                for (int j = 0; j < nbox; ++j)
+                  tma_load_3d_pair(&tmW, fb, dst + j * kBBoxBytes, nh + j * 64, kb * kBK, t.expert, pol_w);
+              }
             }
           } else {
             mbar_arrive_expect_tx(full_bar(s), nbox * kBBoxBytes);
@@ -506,8 +482,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         // kind 1: D[cols, tokens] = A[W block as MN-major M-operand] * B[tail tokens (K-major)],
         //         M = the pair's 256 output columns, N = the tail height (swap-AB).
         const uint32_t idesc = swap ? idesc_bf16_f32(kPairRows, t.height, /*A MN-major*/ 1, /*B K-major*/ 0)
-                                    : idesc_bf16_f32(kPairRows, kMc ? t.bn / 2 : t.bn, /*A K-major*/ 0,
+                                    : idesc_bf16_f32(kPairRows, t.bn / kHalves, /*A K-major*/ 0,
                                                      /*B MN-major*/ 1);
+        // Double-buffered: wait for accumulator `acc`.  Wide: accumulator half 0 now, half 1 just
+        // before the first half-1 MMA (the epilogue drains the halves in order).
         wait_timed<kProf>(tempty_bar(acc), acc_phase ^ 1u, c_tmem);     // epilogue(s) drained this accumulator
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * kAccCols;
@@ -535,7 +513,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             // (SBO); K step of 16 rows = +2 KB.  The two kinds only swap the operand roles.
 #ifdef MOE_EXPERIMENTS
             if (a.experiment & 16) {   // B read as K-major (wrong Y): is the MN-major B operand slower?
-              const uint32_t idk = idesc_bf16_f32(kPairRows, kMc ? t.bn / 2 : t.bn, 0, 0);
+              const uint32_t idk = idesc_bf16_f32(kPairRows, t.bn / kHalves, 0, 0);
 #pragma unroll
               for (int kk = 0; kk < kBK / 16; ++kk) {
                 const uint64_t ad = smem_desc_sw128(a0 + kk * 32, 16, 1024);
@@ -545,7 +523,23 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             } else
 #endif
-            if (!kSplit || !swap) {
+            if constexpr (kWide) {
+              // Two N = 256 blocks per K block: W columns [0, 256) of the tile from the first half of
+              // the stage's B bytes into TMEM columns [0, 256), columns [256, 512) into [256, 512).
+#pragma unroll
+              for (int hf = 0; hf < 2; ++hf) {
+                if (hf == 1 && kb == 0) {
+                  wait_timed<kProf>(tempty_bar(1), acc_phase ^ 1u, c_tmem);
+                  tc_fence_after();
+                }
+#pragma unroll
+                for (int kk = 0; kk < kBK / 16; ++kk) {
+                  const uint64_t ad = smem_desc_sw128(a0 + kk * 32, 16, 1024);
+                  const uint64_t bd = smem_desc_sw128(b0 + hf * (kBSt / 2) + kk * 2048, kBBoxBytes, 1024);
+                  mma_bf16_pair(tmem_base + hf * kAccCols, ad, bd, idesc, (kb | kk) != 0);
+                }
+              }
+            } else if (!kSplit || !swap) {
 #pragma unroll
               for (int kk = 0; kk < kBK / 16; ++kk) {
                 const uint64_t ad = smem_desc_sw128(a0 + kk * 32, 16, 1024);
@@ -563,8 +557,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
             if constexpr (kProf) s_ts[2 * kSt + s] = clock64();
-            if constexpr (kMc) mma_commit_pair(empty_bar(s), 0xF);        // all four CTAs (A is shared)
-            else if constexpr (kCta == 2) mma_commit_pair(empty_bar(s), 0x3);  // frees the slot in both CTAs
+            if constexpr (kCta == 2) mma_commit_pair(empty_bar(s), 0x3);  // frees the slot in both CTAs
             else mma_commit(empty_bar(s));
           }
           __syncwarp();
@@ -573,11 +566,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         if constexpr (kProf) t_end = clock64();
         if (lane == 0) {
           if constexpr (kCta == 2)   // accumulator ready in both CTAs of this pair
-            mma_commit_pair(tfull_bar(acc), (uint16_t)(0x3u << (crank & 2u)));
+            mma_commit_pair(tfull_bar(acc), 0x3);
           else mma_commit(tfull_bar(acc));
         }
         __syncwarp();
-        if (++acc == 2) {
+        if constexpr (kWide) {
+          acc_phase ^= 1u;                        // one (two-half) accumulator per tile
+        } else if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1u;
         }
@@ -673,59 +668,67 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool valid = grow < t.rows;
       const int64_t yrow = a.y_row_map ? (int64_t)__ldg(a.y_row_map + t.row0 + min(grow, t.rows - 1))
                                        : (int64_t)t.row0 + grow;
-      const int bnp = kMc ? t.bn / 2 : t.bn;        // this pair's columns of the tile
-      const int n0 = t.ct * t.bn + (int)pr * bnp;
-      const int col_end = min(n0 + bnp, a.N);
-      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * kAccCols;
-      const int wrow0 = grow - lane;                          // first task row of this warp's quarter
-      if (!kSplit && a.tma_store && wrow0 + 32 <= t.rows) {
-        // All 32 rows belong to the task: convert to bf16 into a 64B-swizzled 32 x 32 staging buffer
-        // (conflict-free 16-byte st.shared) and let TMA write the block; two buffers alternate, so
-        // the conversion of chunk i+1 overlaps the store of chunk i.  Partial quarters (the task's
-        // last rows) take the masked register path below: a box must not touch the next task's rows.
-        const uint32_t xr = (uint32_t)((lane >> 1) & 3);
-        for (int c = 0; c < bnp && n0 + c < a.N; c += 32) {
-          uint32_t r[32];
-          tmem_ld32(taddr + c, r);
-          tmem_wait_ld();
-          const uint32_t buf = ebuf + (n_chunk & 1u) * 2048u;
-          if (lane == 0) bulk_wait_group_read<1>();         // the store issued two chunks ago has read buf
-          __syncwarp();
+      const int bnp = t.bn / kHalves;               // columns of one accumulator block
+      const int wrow0 = grow - lane;                // first task row of this warp's quarter
+      const bool tma_rows = !kSplit && a.tma_store && wrow0 + 32 <= t.rows;
+#pragma unroll 1
+      for (int hf = 0; hf < kHalves; ++hf) {
+        const int n0 = t.ct * t.bn + hf * bnp;
+        const int col_end = min(n0 + bnp, a.N);
+        const int slot = kWide ? hf : acc;          // TMEM block and its tmem-empty barrier
+        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + slot * kAccCols;
+        if (tma_rows) {
+          // All 32 rows belong to the task: convert to bf16 into a 64B-swizzled 32 x 32 staging
+          // buffer (conflict-free 16-byte st.shared) and let TMA write the block; two buffers
+          // alternate, so the conversion of chunk i+1 overlaps the store of chunk i.  Partial
+          // quarters (the task's last rows) take the masked register path below: a box must not
+          // touch the next task's rows.
+          const uint32_t xr = (uint32_t)((lane >> 1) & 3);
+          for (int c = 0; c < bnp && n0 + c < a.N; c += 32) {
+            uint32_t r[32];
+            tmem_ld32(taddr + c, r);
+            tmem_wait_ld();
+            const uint32_t buf = ebuf + (n_chunk & 1u) * 2048u;
+            if (lane == 0) bulk_wait_group_read<1>();       // the store issued two chunks ago has read buf
+            __syncwarp();
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
-            st_shared_v4(buf + lane * 64 + ((j ^ xr) << 4), pack_bf16(r[8 * j], r[8 * j + 1]),
-                         pack_bf16(r[8 * j + 2], r[8 * j + 3]), pack_bf16(r[8 * j + 4], r[8 * j + 5]),
-                         pack_bf16(r[8 * j + 6], r[8 * j + 7]));
-          fence_proxy_async_smem();
-          __syncwarp();
+            for (int j = 0; j < 4; ++j)
+              st_shared_v4(buf + lane * 64 + ((j ^ xr) << 4), pack_bf16(r[8 * j], r[8 * j + 1]),
+                           pack_bf16(r[8 * j + 2], r[8 * j + 3]), pack_bf16(r[8 * j + 4], r[8 * j + 5]),
+                           pack_bf16(r[8 * j + 6], r[8 * j + 7]));
+            fence_proxy_async_smem();
+            __syncwarp();
 #ifdef MOE_EXPERIMENTS
-          if (!(a.experiment & 8))
+            if (!(a.experiment & 8))
 #endif
-          if (lane == 0) {
-            tma_store_2d(&tmY, buf, n0 + c, t.row0 + wrow0);
-            bulk_commit_group();
+            if (lane == 0) {
+              tma_store_2d(&tmY, buf, n0 + c, t.row0 + wrow0);
+              bulk_commit_group();
+            }
+            ++n_chunk;
           }
-          ++n_chunk;
-        }
-      } else {
-        for (int c = 0; c < bnp; c += 32) {
-          uint32_t r[32];
-          tmem_ld32(taddr + c, r);
-          tmem_wait_ld();
+        } else {
+          for (int c = 0; c < bnp; c += 32) {
+            uint32_t r[32];
+            tmem_ld32(taddr + c, r);
+            tmem_wait_ld();
 #ifdef MOE_EXPERIMENTS
-          if (a.experiment & 8) continue;
+            if (a.experiment & 8) continue;
 #endif
-          if (valid) store_chunk(a, yrow, n0 + c, col_end, r);
+            if (valid) store_chunk(a, yrow, n0 + c, col_end, r);
+          }
         }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if constexpr (kCta == 2) mbar_arrive_cluster(leader(tempty_bar(acc)));
-        else mbar_arrive(tempty_bar(acc));
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (kCta == 2) mbar_arrive_cluster(leader(tempty_bar(slot)));
+          else mbar_arrive(tempty_bar(slot));
+        }
       }
       if constexpr (kProf) c_work += clock64() - w0;
-      if (++acc == 2) {
+      if constexpr (kWide) {
+        acc_phase ^= 1u;
+      } else if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1u;
       }
@@ -898,10 +901,10 @@ extern "C" moe_status moe_device_info(int32_t* sm_count, int32_t* cc_major, int3
 
 namespace {
 
-template <bool kProf, int kCta, bool kSplit, bool kMc = false>
+template <bool kProf, int kCta, bool kSplit, bool kWide = false>
 cudaError_t set_attr() {
-  return cudaFuncSetAttribute(moe_gemm_kernel<kProf, kCta, kSplit, kMc>,
-                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(Geo<kCta, kSplit>::kSmem + 8 * kMaxMPad));
+  return cudaFuncSetAttribute(moe_gemm_kernel<kProf, kCta, kSplit, kWide>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)(Geo<kCta, kSplit, kWide>::kSmem + 8 * kMaxMPad));
 }
 
 cudaError_t set_smem_attrs() {
@@ -961,9 +964,9 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
   moe_status st = make_x_map(&tmX, X, T, v.H, (experiment & 4) ? kBM : 1);
   if (st != MOE_OK) return st;
   const bool w4d = (v.N % 64) == 0;
-  const bool mc = v.bm == 256 && v.bn > 256;      // cluster tile: two CTA pairs, A multicast
-  const int cta = (v.bm / kBM) * (mc ? 2 : 1);    // CTAs per tile: each stages bn / cta W columns
-  st = make_w_map(&tmW, W, v.E, v.H, v.N, v.bn / cta, w4d);
+  const bool wide = v.bm == 256 && v.bn == 512;   // wide pair tile: two N = 256 MMA blocks
+  const int cta = v.bm / kBM;                      // CTAs per tile: each stages bn / cta W columns
+  st = make_w_map(&tmW, W, v.E, v.H, v.N, v.bn / cta / (wide ? 2 : 1), w4d);   // per MMA block
   if (st != MOE_OK) return st;
 
   // TMA-store epilogue: bf16 Y in CSR row order (the EP combine path scatters rows: register stores).
@@ -1015,17 +1018,17 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
   if (attr_err != cudaSuccess) MOE_FAIL(MOE_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(attr_err));
   if (v.bm == 256) {
     const bool split = (v.flags & MOE_SPLIT_TAIL) != 0;
-    const int ncl = mc ? 4 : 2;                    // CTAs per scheduling unit
-    const int units = v.total < 0 ? sm_count_cached() / ncl : std::min(v.total, sm_count_cached() / ncl);
-    const size_t smem = (split ? Geo<2, true>::kSmem : Geo<2, false>::kSmem) + 8 * (size_t)v.M_pad;
+    const int pairs = v.total < 0 ? sm_count_cached() / 2 : std::min(v.total, sm_count_cached() / 2);
+    const size_t smem = (split ? Geo<2, true>::kSmem : wide ? Geo<2, false, true>::kSmem : Geo<2, false>::kSmem) +
+                        8 * (size_t)v.M_pad;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(ncl * units);
+    cfg.gridDim = dim3(2 * pairs);
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = (cudaStream_t)stream;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = ncl;
+    attr[0].val.clusterDim.x = 2;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // PDL: overlap the prologue
@@ -1033,7 +1036,7 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
     cfg.attrs = attr;
     cfg.numAttrs = 2;
     cudaError_t le;
-    if (mc)
+    if (wide)
       le = prof ? cudaLaunchKernelEx(&cfg, moe_gemm_kernel<true, 2, false, true>, tmX, tmW, tmY, a)
                 : cudaLaunchKernelEx(&cfg, moe_gemm_kernel<false, 2, false, true>, tmX, tmW, tmY, a);
     else if (split)

@@ -76,6 +76,8 @@ moe_status moe_plan_build(const int32_t* counts, int32_t E, int64_t H, int64_t N
     MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_plan_build: H=%lld and N=%lld must be multiples of 8 (16-byte TMA strides)",
              (long long)H, (long long)N);
   if (H >= INT_MAX || N >= INT_MAX) MOE_FAIL(MOE_ERR_CAPACITY, "moe_plan_build: H or N >= 2^31");
+  const bool auto_bn = bn == 0;
+  if (auto_bn) bn = 256;
   if (bm == 0) {
     // Auto: executed rows under each tile height, CTA-pair tiles credited with
     // their measured ~1.10x per-row advantage (half the W traffic per SM, 6-stage ring).
@@ -87,9 +89,11 @@ moe_status moe_plan_build(const int32_t* counts, int32_t E, int64_t H, int64_t N
     }
     bm = bn == 512 || (r256 * 100 <= r128 * 110 && bn % 32 == 0) ? 256 : 128;
   }
+  // Auto width: CTA-pair tiles go wide (256 x 512) whenever N has 512 columns.
+  if (auto_bn && bm == 256 && N >= 512 && !(flags & MOE_SPLIT_TAIL)) bn = 512;
   if (bm != 128 && bm != 256)
     MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_plan_build: bm=%d unsupported (128: one CTA, 256: CTA pair, 0: auto)", bm);
-  // bm = 256, bn = 512: cluster tile (two CTA pairs sharing the tile's token rows by multicast).
+  // bm = 256, bn = 512: wide pair tile (two N = 256 MMA blocks sharing the staged token rows).
   const bool cluster_tile = bm == 256 && bn == 512;
   if (!cluster_tile && (bn < 16 || bn > 256 || bn % (bm == 256 ? 32 : 16)))
     MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_plan_build: bn=%d must be a multiple of %d in [16, 256] (or 512 with bm=256)",
@@ -271,6 +275,7 @@ moe_status moe_plan_create(const int32_t* counts, int32_t E, int64_t H, int64_t 
     return st;
   }
   bm = p->blob[7];                              // resolved tile height (bm = 0 means auto)
+  bn = p->blob[8];                              // resolved tile width (bn = 0 means auto)
   flags = (uint32_t)p->blob[10];                // auto may add MOE_SPLIT_TAIL
   p->stream = (cudaStream_t)stream;
   p->E = E;

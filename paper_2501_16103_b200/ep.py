@@ -110,7 +110,7 @@ def _excl(x):
 class ExpertParallelMoE:
     """One rank of an expert-parallel MoE expert GEMM."""
 
-    def __init__(self, E: int, W_local, comm, bm: int = 0, bn: int = 256, out_dtype=torch.bfloat16, kernels=None):
+    def __init__(self, E: int, W_local, comm, bm: int = 0, bn: int = 0, out_dtype=torch.bfloat16, kernels=None):
         self.comm = comm
         self.G = comm.size
         if E % self.G:

@@ -229,20 +229,36 @@ RAGGED_SPLIT = [                    # MOE_SPLIT_TAIL: 256-row pair body tiles + 
 ]
 
 
+RAGGED_WIDE = [                     # bm = 256, bn = 512: two N = 256 MMA blocks per tile
+    (300, 5, 2, 200, 136),          # N < 256: the second block lies wholly past N
+    (700, 3, 2, 256, 1024),         # several row tiles, exact N tiles
+    (64, 16, 4, 128, 1408),         # N = 2.75 x 512 (DeepSeek-V2-Lite width)
+    (1, 8, 2, 4096, 1024),          # decode: one token
+    (1500, 4, 1, 128, 200),         # 3-D W map (N % 64 != 0)
+    (2048, 4, 2, 64, 1536),         # 1024 rows/expert on average
+]
+
+
 @pytest.mark.parametrize("T,E,k,H,N,bn,bm,a_path,flags",
                          [c + (128, "0", 0) for c in RAGGED] + [c + (128, "1", 0) for c in RAGGED]
                          + [c + (256, "1", 0) for c in RAGGED_PAIR]
-                         + [c + (256, 256, "1", M.MOE_SPLIT_TAIL) for c in RAGGED_SPLIT])
-@pytest.mark.parametrize("mode", ["int", "normal"])
+                         + [c + (256, 256, "1", M.MOE_SPLIT_TAIL) for c in RAGGED_SPLIT]
+                         + [c + (512, 256, a, 0) for c in RAGGED_WIDE for a in ("0", "1")])
+@pytest.mark.parametrize("mode", ["int", "int_bf16", "normal"])
 def test_gemm_ragged(T, E, k, H, N, bn, bm, a_path, flags, mode, monkeypatch):
     monkeypatch.setenv("MOE_A_PATH", a_path)          # A staging path: gather4 (0) / cp.async (1)
-    ids, X, W, Xd, Wd = _inputs(T, E, k, H, N, T + E, mode)
-    Y, counts, row_off, tok, *_ = run_path(ids, Xd, Wd, E, bn=bn, bm=bm, flags=flags)
+    ids, X, W, Xd, Wd = _inputs(T, E, k, H, N, T + E, "int" if mode == "int_bf16" else mode)
+    # int_bf16: bf16 output (the TMA-store epilogue for full 32-row quarters): the exact integer
+    # accumulator rounded once to bf16, compared bit for bit with the fp64 reference so rounded.
+    out = torch.bfloat16 if mode == "int_bf16" else torch.float32
+    Y, counts, row_off, tok, *_ = run_path(ids, Xd, Wd, E, bn=bn, bm=bm, flags=flags, out_dtype=out)
     rc, rr, rt, rs = omoe.buckets(ids, E)
     ref = omoe.expert_gemm(X, W, rt, rr)
     Yh = Y.cpu().double().numpy()
     assert not np.isnan(Yh).any(), "some Y element was never written"
-    if mode == "int":
+    if mode == "int_bf16":
+        assert np.array_equal(Yh, torch.from_numpy(ref).to(torch.bfloat16).double().numpy())
+    elif mode == "int":
         assert np.array_equal(Yh, ref)
     else:
         tol_check(torch.from_numpy(Yh), ref, f"ragged {T},{E},{k},{H},{N},{bn}")
@@ -282,7 +298,9 @@ def _sample_rows(row_off, counts, rng, per_expert=6):
     return np.array(rows)
 
 
-@pytest.mark.parametrize("cfg,bn,bm,flags", [("mix", 256, 128, 0), ("mix", 256, 256, 0), ("mix", 256, 0, 0),
+@pytest.mark.parametrize("cfg,bn,bm,flags", [("mix", 256, 128, 0), ("mix", 256, 256, 0), ("mix", 0, 0, 0),
+                                             ("mix", 512, 256, 0), ("ds", 512, 256, 0), ("paper_balanced", 0, 0, 0),
+                                             ("dec16", 512, 256, 0), ("paper_worst", 512, 256, 0),
                                              ("mix", 256, 256, 2), ("ds", 128, 128, 0), ("ds", 256, 256, 0),
                                              ("ds", 256, 256, 2), ("dec16", 256, 128, 0), ("dec16", 256, 0, 0),
                                              ("dec16", 256, 256, 2), ("paper_worst", 256, 256, 0),
@@ -299,7 +317,8 @@ def test_gemm_full_size_sampled(cfg, bn, bm, flags):
     assert np.array_equal(tok.cpu().numpy(), rt)
     rng = np.random.default_rng(1)
     rows = _sample_rows(rr, rc, rng)
-    cols = np.unique(np.concatenate([rng.integers(0, c.N, 40), [0, c.N - 1, bn - 1, bn]]))
+    cols = np.unique(np.concatenate([rng.integers(0, c.N, 40), [0, c.N - 1, 255, 256, 511, 512]]))
+    cols = cols[cols < c.N]
     ref = omoe.expert_gemm_entries(lambda t: wl.x_rows(seed, c.T, c.H, [t])[0],
                                    lambda e, cs: wl.w_columns(seed, c.E, c.H, c.N, e, cs),
                                    rt, rr, rows, cols)
@@ -325,6 +344,7 @@ def _device_plan_blob(counts, N, bm, bn, pad, H=64, split=0, order="natural"):
 @pytest.mark.parametrize("pad", ["max", "repeat"])
 @pytest.mark.parametrize("bm,bn,split,order", [(128, 256, 0, "natural"), (256, 256, 0, "natural"), (128, 48, 0, "natural"),
                                                (256, 96, 0, "natural"), (256, 256, 1, "natural"),
+                                               (256, 512, 0, "natural"), (256, 512, 0, "half_interval"),
                                                (128, 256, 0, "alternating"), (256, 256, 0, "half_interval")])
 def test_plan_device_bit_exact(pad, bm, bn, split, order):
     rng = np.random.default_rng(bm + bn)
@@ -375,6 +395,22 @@ def test_gemm_device_planned(T, E, k, H, N, bn, bm):
     torch.cuda.synchronize()
     rc, rr, rt, rs = omoe.buckets(ids2, E)
     assert np.array_equal(Y2.cpu().double().numpy(), omoe.expert_gemm(X, W, rt, rr))
+
+
+@pytest.mark.parametrize("bm,bn", [(256, 512), (0, 0)])
+@pytest.mark.parametrize("T,E,k,H,N", [(300, 5, 2, 200, 136), (513, 7, 3, 256, 1024), (2048, 6, 2, 128, 1408)])
+def test_gemm_device_planned_wide(T, E, k, H, N, bm, bn):
+    """Device plan (M_pad = pad32(E), tile count read in-kernel) with wide tiles and bf16 output
+    (TMA-store epilogue over a 2^31-row Y map): exact integers rounded once to bf16."""
+    ids, X, W, Xd, Wd = _inputs(T, E, k, H, N, T + E + 2, "int")
+    topk = torch.from_numpy(ids).cuda()
+    Yout = torch.full((T * k, N), float("nan"), dtype=torch.bfloat16, device="cuda")
+    Y, counts, row_off, tok, slot, plan = M.moe_forward(topk, Xd, Wd, E, bm=bm, bn=bn, Y=Yout, device_plan=True)
+    torch.cuda.synchronize()
+    assert (plan.bm, plan.bn) == ((256, 512) if N >= 512 or bn == 512 else (256, 256))
+    rc, rr, rt, rs = omoe.buckets(ids, E)
+    ref = torch.from_numpy(omoe.expert_gemm(X, W, rt, rr)).to(torch.bfloat16).double().numpy()
+    assert np.array_equal(Y.cpu().double().numpy(), ref)
 
 
 @pytest.mark.parametrize("order", ["alternating", "half_interval"])

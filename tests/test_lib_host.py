@@ -135,6 +135,44 @@ def test_planner_auto_tile_choice():
     assert moe_lib.parse_plan_blob(moe_lib.moe_plan_build(counts, c.H, c.N, 0, 256))["bm"] == 256
 
 
+def test_planner_wide_tiles_match_oracle():
+    """bm = 256, bn = 512 (wide pair tiles): the same Alg. 1/4 mapping over 512-column tiles."""
+    rng = random.Random(15)
+    for _ in range(200):
+        E = rng.randint(1, 300)
+        counts = np.array([0 if rng.random() < 0.3 else rng.randint(1, 3000) for _ in range(E)])
+        _compare(counts, 8 * rng.randint(1, 3000), 256, 512, rng.choice(["max", "repeat"]),
+                 order=rng.choice(["natural", "alternating", "half_interval"]))
+    with pytest.raises(moe_lib.MoeError):
+        moe_lib.moe_plan_build([5, 5], 64, 1024, 128, 512)                 # wide tiles are pair tiles
+    with pytest.raises(moe_lib.MoeError):
+        moe_lib.moe_plan_build([5, 5], 64, 1024, 256, 384)
+    with pytest.raises(moe_lib.MoeError):
+        moe_lib.moe_plan_build([5, 5], 64, 1024, 256, 512, moe_lib.MOE_SPLIT_TAIL)   # split needs bn = 256
+
+
+def test_planner_auto_tile_width():
+    """bn = 0: 512 when bm resolves to 256, N >= 512 and no split tails; else 256 (header rule)."""
+    rng = random.Random(16)
+    for _ in range(200):
+        E = rng.randint(1, 64)
+        counts = [0 if rng.random() < 0.3 else rng.randint(1, 5000) for _ in range(E)]
+        N = 8 * rng.randint(1, 400)
+        bm = rng.choice([0, 128, 256])
+        split = rng.random() < 0.2 and bm == 256
+        blob = moe_lib.parse_plan_blob(moe_lib.moe_plan_build(counts, 64, N, bm, 0,
+                                                              moe_lib.MOE_SPLIT_TAIL if split else 0))
+        r128 = sum(-(-m // 128) * 128 for m in counts)
+        r256 = sum(-(-m // 256) * 256 for m in counts)
+        bm_exp = bm or (256 if r256 * 100 <= r128 * 110 else 128)
+        assert blob["bm"] == bm_exp
+        assert blob["bn"] == (512 if bm_exp == 256 and N >= 512 and not split else 256)
+    c = synth.CONFIGS["mix"]
+    counts = np.bincount(synth.route(c).ravel(), minlength=c.E)
+    b = moe_lib.parse_plan_blob(moe_lib.moe_plan_build(counts, c.H, c.N))
+    assert (b["bm"], b["bn"]) == (256, 512)
+
+
 def test_planner_decode_bijection_through_blob():
     """Decode every block of a library-built blob with the oracle's Alg. 2 and check the lattice."""
     counts = np.array([300, 0, 5, 129, 0, 1000, 1])
