@@ -54,7 +54,14 @@ constexpr int kBStageBytes = 4 * kBBoxBytes;    // up to BN = 256
 constexpr int kAWarps = 4;                      // A producers (token rows): warps 0-3
 constexpr int kBWarp = kAWarps;                 // B producer (W block, TMA): warp 4
 constexpr int kMmaWarp = kAWarps + 1;           // tcgen05 issuer: warp 5
-constexpr int kEpiWarps = 4;                    // epilogue: warps 6-9 (TMEM lane quarters 2,3,0,1)
+#ifndef MOE_EPI_WARPS
+#define MOE_EPI_WARPS 8
+#endif
+// Epilogue: warps 6.. ; warp w drains TMEM lane quarter w % 4 (the tcgen05.ld lane rule), and the
+// kEpiWarps / 4 warps of one quarter take alternate 32-column chunks.
+constexpr int kEpiWarps = MOE_EPI_WARPS;
+static_assert(kEpiWarps == 4 || kEpiWarps == 8, "one or two warps per TMEM lane quarter");
+constexpr int kEpiGroups = kEpiWarps / 4;
 constexpr int kThreads = 32 * (kAWarps + 2 + kEpiWarps);
 constexpr int kDefaultAMode = 1;                // A staging: cp.async (see the A-producer comment)
 constexpr uint32_t kTmemCols = 512;             // 2 accumulators x 256 fp32 columns
@@ -211,9 +218,9 @@ struct Geo {
   static constexpr int kStages = kWide ? 4 : kCta == 2 ? 6 : 4;   // a 7th pair stage measured no gain (NOTES)
   static_assert(8 * (2 * kStages + 4) + 4 <= kBarBytes, "barrier block overlaps TilePrefix");
   static constexpr int kBStage = (kWide ? 2 : 1) * kBStageBytes / kCta;   // bytes of W per CTA per stage
-  // 4 KB per epilogue warp: two 2 KB bf16 staging buffers for the TMA-store epilogue, or the
-  // transpose buffer of swap-AB tail tiles (MOE_SPLIT_TAIL).
-  static constexpr int kEpiStage = kEpiWarps * 32 * 32 * 4;
+  // 16 KB: a 2 KB bf16 staging buffer per epilogue warp for the TMA-store epilogue (two per warp
+  // with four warps), or 4 KB transpose buffers for four warps on swap-AB tail tiles (MOE_SPLIT_TAIL).
+  static constexpr int kEpiStage = 16384;
   static constexpr size_t kSmem = 1024 + (size_t)kStages * (kABytes + kBStage) + kEpiStage + kBarBytes;
 };
 
@@ -605,10 +612,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     // ===================== epilogue: TMEM -> registers -> Y =====================
     const int q = warp & 3;                                   // TMEM lane quarter of this warp
+    const int ew = warp - (kMmaWarp + 1);                     // epilogue warp index
+    const int cg = ew >> 2;                                   // column group: chunks c/32 = cg mod kEpiGroups
     int acc = 0;
     uint32_t acc_phase = 0;
     uint32_t n_chunk = 0;                                     // TMA-store chunks issued by this warp
-    const uint32_t ebuf = sEpi + (uint32_t)(warp - (kMmaWarp + 1)) * 4096u;
+    const uint32_t ebuf = sEpi + (uint32_t)ew * (16384u / kEpiWarps);
     long long c_wait = 0, c_work = 0;
     for (int v = pair_id; v < total; v += n_pairs) {
       int h, task, l;
@@ -617,6 +626,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       wait_timed<kProf>(tfull_bar(acc), acc_phase, c_wait);
       const long long w0 = kProf ? clock64() : 0;
       tc_fence_after();
+      if (kSplit && t.kind == 1 && cg > 0) {
+        // Swap-AB tail tiles are drained by the first four epilogue warps alone.
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(leader(tempty_bar(acc)));
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1u;
+        }
+        continue;
+      }
       if (kSplit && t.kind == 1) {
         // Swap-AB tail: TMEM lane = output column, TMEM column = tail token.
         const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * kAccCols;
@@ -684,12 +703,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           // quarters (the task's last rows) take the masked register path below: a box must not
           // touch the next task's rows.
           const uint32_t xr = (uint32_t)((lane >> 1) & 3);
-          for (int c = 0; c < bnp && n0 + c < a.N; c += 32) {
+          for (int c = 32 * cg; c < bnp && n0 + c < a.N; c += 32 * kEpiGroups) {
             uint32_t r[32];
             tmem_ld32(taddr + c, r);
             tmem_wait_ld();
-            const uint32_t buf = ebuf + (n_chunk & 1u) * 2048u;
-            if (lane == 0) bulk_wait_group_read<1>();       // the store issued two chunks ago has read buf
+            // Four warps: two buffers per warp, reused every other chunk; eight: one buffer.
+            const uint32_t buf = kEpiWarps == 4 ? ebuf + (n_chunk & 1u) * 2048u : ebuf;
+            if (lane == 0) {                                  // the store that last used buf has read it
+              if constexpr (kEpiWarps == 4) bulk_wait_group_read<1>();
+              else bulk_wait_group_read<0>();
+            }
             __syncwarp();
 #pragma unroll
             for (int j = 0; j < 4; ++j)
@@ -708,7 +731,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ++n_chunk;
           }
         } else {
-          for (int c = 0; c < bnp; c += 32) {
+          for (int c = 32 * cg; c < bnp; c += 32 * kEpiGroups) {
             uint32_t r[32];
             tmem_ld32(taddr + c, r);
             tmem_wait_ld();
