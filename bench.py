@@ -235,7 +235,8 @@ def run_ours(args, cfg):
                 plan.update(counts_h)
         else:                                      # P:142 option 2: plan generated on the device,
             if plan is None:                       # fused into the routing scan (moe_route_plan)
-                plan = M.Plan(None, cfg.H, cfg.N, args.bm, args.bn, E=cfg.E)
+                bm, bn = (args.bm, args.bn) if args.bm or args.bn else M.suggest_tile(cfg.T * cfg.k, cfg.E, cfg.H, cfg.N)
+                plan = M.Plan(None, cfg.H, cfg.N, bm, bn, E=cfg.E)
             counts, row_off, tok, slot, _ = M.moe_route(topk_d, cfg.E, with_slot=False, plan=plan)
         g0 = torch.cuda.Event(enable_timing=True)
         g0.record(stream)

@@ -145,6 +145,15 @@ def _stream(stream=None) -> int:
     return int(s.cuda_stream)
 
 
+def suggest_tile(rows: int, E: int, H: int, N: int) -> tuple[int, int]:
+    """Tile shape (bm, bn) the automatic rule picks for `rows` routed rows spread evenly over E
+    experts — for plans created before the counts exist (device-built plans): the
+    device planner keeps the shape chosen at creation."""
+    per = max(1, -(-int(rows) // max(1, int(E))))
+    b = parse_plan_blob(moe_plan_build(np.full(E, per, dtype=np.int32), H, N, 0, 0))
+    return b["bm"], b["bn"]
+
+
 class Plan:
     """Device-resident plan (moe_plan_create / moe_plan_update / moe_plan_destroy)."""
 
@@ -374,6 +383,8 @@ def moe_forward(topk_ids, X, W, E: int, bm: int = 0, bn: int = 0, out_dtype=None
     H, N = int(X.shape[1]), int(W.shape[2])
     if device_plan:
         if plan is None:
+            if bm == 0 and bn == 0:
+                bm, bn = suggest_tile(topk_ids.numel(), E, H, N)
             plan = Plan(None, H, N, bm, bn, stream=stream, E=E)
         counts, row_off, token_idx, slot, _ = moe_route(topk_ids, E, stream=stream, plan=plan)
         counts_out = counts
