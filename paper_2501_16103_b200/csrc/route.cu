@@ -4,8 +4,16 @@
 // The paper scatters tokens into per-expert buckets with atomics, which leaves the
 // order inside a bucket to the hardware.  This build produces the same buckets in a
 // canonical, deterministic order — ascending token id (reading R3) — so Y rows are
-// reproducible run to run.  Over 1024-token chunks (A and B fused into one single-block
-// kernel for small batches, T*k <= 16K: two launches):
+// reproducible run to run.
+//
+// Up to kOneBlockMaxEntries (T*k) routing entries: ONE single-block launch (route_one_block_kernel).
+// Warp w owns a contiguous range of the (token, slot) entries; per 32-entry round,
+// __match_any_sync groups the lanes routed to the same expert, so each group costs one
+// shared-memory add (no atomics contention however skewed the routing); pass 1 counts per
+// (warp, expert), one scan gives every (warp, expert) its first CSR row (and the plan, with
+// plan_body), pass 2 replays the rounds and writes each entry at base + its rank in the group.
+//
+// Larger batches, over 1024-token chunks (three launches):
 //   A (grid = chunks):            per-chunk expert histogram (shared-memory counters) and input
 //                                 validation;
 //   B (one block, thread = expert): counts[e], row_off = exclusive scan, per-(chunk, expert)
@@ -36,7 +44,8 @@ constexpr int kChunk = 1024;         // tokens per chunk (= threads of kernels A
 constexpr int kMaxE = 1024;
 constexpr int kScanSmem = 6144;      // ints of the chunk histogram staged in shared memory (static smem budget)
 static_assert(kChunk == moe::dplan::kPlanThreads, "route_count_scan_kernel: one thread per chunk token");
-constexpr int64_t kFusedMaxEntries = 16384;  // one block's shared-memory atomics stay cheap up to here
+constexpr int64_t kOneBlockMaxEntries = 65536;   // one block's two passes stay under ~10 us up to here
+constexpr int kOneBlockWarps = moe::dplan::kPlanThreads / 32;
 
 // 1: a valid slot; 0: a masked slot (negative id); -1: invalid (id >= E or a duplicate).
 __device__ __forceinline__ int classify(const int32_t* row, int j, int E) {
@@ -105,49 +114,71 @@ __global__ void __launch_bounds__(moe::dplan::kPlanThreads)
   if (blob) moe::dplan::plan_body(e < E ? tot : 0, E, H, N, bm, bn, flags, blob);
 }
 
-// Small problems (chunks x experts fit in shared memory): one block does the histograms, the
-// scan and the plan — route becomes two launches.
+// One block (kPlanThreads threads) for T*k <= kOneBlockMaxEntries; dynamic shared memory holds
+// the per-(warp, expert) counters: kOneBlockWarps * E ints.
 __global__ void __launch_bounds__(moe::dplan::kPlanThreads)
-    route_count_scan_kernel(const int32_t* __restrict__ topk, int T, int k, int n_chunks, int E,
-                            int32_t* __restrict__ chunk_off, int32_t* __restrict__ counts,
-                            int32_t* __restrict__ row_off, int32_t* __restrict__ status, int H, int N, int bm,
-                            int bn, uint32_t flags, int32_t* __restrict__ blob) {
+    route_one_block_kernel(const int32_t* __restrict__ topk, int T, int k, int E, int32_t* __restrict__ counts,
+                           int32_t* __restrict__ row_off, int32_t* __restrict__ token_idx,
+                           int32_t* __restrict__ slot, int32_t* __restrict__ status, int H, int N, int bm, int bn,
+                           uint32_t flags, int32_t* __restrict__ blob) {
+  extern __shared__ int s_we[];                      // [kOneBlockWarps][E]: counts, then running CSR rows
   __shared__ long long s_warp[32];
-  __shared__ int s_cc[kScanSmem];
-  const int cells = n_chunks * E;
-  for (int i = threadIdx.x; i < cells; i += blockDim.x) s_cc[i] = 0;
+  moe::ptx::pdl_launch_dependents();                 // the GEMM prologue may start; it waits for us
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < kOneBlockWarps * E; i += blockDim.x) s_we[i] = 0;
   __syncthreads();
+  const int n = T * k;
+  const int per = ((n + kOneBlockWarps - 1) / kOneBlockWarps + 31) & ~31;   // entries per warp (whole rounds)
+  const int i0 = warp * per, i1 = min(n, i0 + per);
+  int* my = s_we + warp * E;
+  // Expert of entry i, or -1 (masked slot) / -2 (invalid: id >= E or repeated in its token's row).
+  auto expert_of = [&](int i) -> int {
+    if (i >= i1) return -1;
+    const int t = i / k, j = i - t * k;
+    const int cl = classify(topk + (int64_t)t * k, j, E);
+    return cl == 1 ? __ldg(topk + i) : (cl == 0 ? -1 : -2);
+  };
   int bad = 0;
-  for (int c = 0; c < n_chunks; ++c) {               // thread = token of chunk c (kChunk == blockDim)
-    const int t = c * kChunk + threadIdx.x;
-    if (t < T) {
-      const int32_t* row = topk + (int64_t)t * k;
-      for (int j = 0; j < k; ++j) {
-        const int cl = classify(row, j, E);
-        if (cl == 1) atomicAdd(&s_cc[c * E + row[j]], 1);
-        bad |= cl < 0;
-      }
-    }
+  for (int b = i0; b < i1; b += 32) {                // pass 1: per-(warp, expert) counts
+    const int e = expert_of(b + lane);
+    bad |= e == -2;
+    const unsigned grp = __match_any_sync(0xffffffffu, e);
+    if (e >= 0 && lane == __ffs(grp) - 1) my[e] += __popc(grp);
+    __syncwarp();
   }
   const int any_bad = __syncthreads_or(bad);
   if (threadIdx.x == 0 && status) *status = any_bad ? 1 : 0;
-  const int e = threadIdx.x;
+  const int e = threadIdx.x;                         // thread = expert
   long long tot = 0;
   if (e < E)
-    for (int c = 0; c < n_chunks; ++c) tot += s_cc[c * E + e];
+    for (int w = 0; w < kOneBlockWarps; ++w) tot += s_we[w * E + e];
   long long all;
   const long long incl = moe::dplan::block_scan_incl(tot, s_warp, &all);
   if (e < E) {
-    long long run = incl - tot;
+    long long run = incl - tot;                      // row_off[e]
     counts[e] = (int32_t)tot;
     row_off[e] = (int32_t)run;
-    for (int c = 0; c < n_chunks; ++c) {
-      const long long n = s_cc[c * E + e];
-      chunk_off[c * E + e] = (int32_t)run;
-      run += n;
+    for (int w = 0; w < kOneBlockWarps; ++w) {       // warp w's entries for e start here
+      const int c = s_we[w * E + e];
+      s_we[w * E + e] = (int32_t)run;
+      run += c;
     }
   }
   if (e == 0) row_off[E] = (int32_t)all;
+  __syncthreads();
+  for (int b = i0; b < i1; b += 32) {                // pass 2: stable placement (entry order = token order)
+    const int i = b + lane;
+    const int x = expert_of(i);
+    const unsigned grp = __match_any_sync(0xffffffffu, x);
+    if (x >= 0) {
+      const int pos = my[x] + __popc(grp & ((1u << lane) - 1u));
+      token_idx[pos] = i / k;
+      if (slot) slot[pos] = i - (i / k) * k;
+    }
+    __syncwarp();
+    if (x >= 0 && lane == __ffs(grp) - 1) my[x] += __popc(grp);
+    __syncwarp();
+  }
   if (blob) moe::dplan::plan_body(e < E ? tot : 0, E, H, N, bm, bn, flags, blob);
 }
 
@@ -191,15 +222,25 @@ moe_status route_impl(const int32_t* topk, int64_t T, int32_t k, int32_t E, int3
     if (pE != E) MOE_FAIL(MOE_ERR_INVALID, "moe_route_plan: plan has E=%d, routing E=%d", pE, E);
   }
   cudaStream_t s = (cudaStream_t)stream;
+  int32_t* blob = plan ? moe::plan_blob_dev_mut(plan) : nullptr;
+  cudaError_t err = cudaSuccess;
+  if (T * k <= kOneBlockMaxEntries) {
+    const size_t smem = sizeof(int) * (size_t)kOneBlockWarps * E;
+    static cudaError_t attr = cudaFuncSetAttribute(route_one_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   (int)(sizeof(int) * kOneBlockWarps * kMaxE));
+    if (attr != cudaSuccess) MOE_FAIL(MOE_ERR_CUDA, "moe_route: cudaFuncSetAttribute: %s", cudaGetErrorString(attr));
+    route_one_block_kernel<<<1, moe::dplan::kPlanThreads, smem, s>>>(topk, (int)T, k, E, counts, row_off, token_idx,
+                                                                     slot, status, pH, pN, pbm, pbn, pflags, blob);
+    err = cudaGetLastError();
+    if (err != cudaSuccess) MOE_FAIL(MOE_ERR_CUDA, "moe_route launch: %s", cudaGetErrorString(err));
+    if (plan) moe::plan_set_device_mode(plan, true);
+    return MOE_OK;
+  }
   const int n_chunks = (int)std::max<int64_t>(1, (T + kChunk - 1) / kChunk);
   int32_t* chunk = nullptr;
-  cudaError_t err = cudaMallocAsync((void**)&chunk, sizeof(int32_t) * (size_t)n_chunks * E, s);
+  err = cudaMallocAsync((void**)&chunk, sizeof(int32_t) * (size_t)n_chunks * E, s);
   if (err != cudaSuccess) MOE_FAIL(MOE_ERR_CUDA, "moe_route scratch: %s", cudaGetErrorString(err));
-  int32_t* blob = plan ? moe::plan_blob_dev_mut(plan) : nullptr;
-  if ((int64_t)n_chunks * E <= kScanSmem && T * k <= kFusedMaxEntries) {
-    route_count_scan_kernel<<<1, moe::dplan::kPlanThreads, 0, s>>>(topk, (int)T, k, n_chunks, E, chunk, counts,
-                                                                   row_off, status, pH, pN, pbm, pbn, pflags, blob);
-  } else {
+  {
     if (status) cudaMemsetAsync(status, 0, sizeof(int32_t), s);
     route_hist_kernel<<<n_chunks, kChunk, 0, s>>>(topk, (int)T, k, E, chunk, status);
     route_scan_kernel<<<1, moe::dplan::kPlanThreads, 0, s>>>(chunk, n_chunks, E, counts, row_off, pH, pN, pbm, pbn,

@@ -407,7 +407,7 @@ def test_gemm_device_planned_wide(T, E, k, H, N, bm, bn):
     Yout = torch.full((T * k, N), float("nan"), dtype=torch.bfloat16, device="cuda")
     Y, counts, row_off, tok, slot, plan = M.moe_forward(topk, Xd, Wd, E, bm=bm, bn=bn, Y=Yout, device_plan=True)
     torch.cuda.synchronize()
-    assert (plan.bm, plan.bn) == ((256, 512) if N >= 512 or bn == 512 else (256, 256))
+    assert (plan.bm, plan.bn) == ((bm, bn) if bn else M.suggest_tile(T * k, E, H, N))
     rc, rr, rt, rs = omoe.buckets(ids, E)
     ref = torch.from_numpy(omoe.expert_gemm(X, W, rt, rr)).to(torch.bfloat16).double().numpy()
     assert np.array_equal(Y.cpu().double().numpy(), ref)
@@ -479,3 +479,41 @@ def test_route_many_chunks_and_masked_slots():
         got = tok[a:b].cpu().numpy().tolist()
         assert got == [t for t in range(T) if e in ids[t]]
     assert n == int((ids >= 0).sum())
+
+
+@pytest.mark.parametrize("T,k,E,skew", [(20000, 3, 1024, 0.0), (8192, 6, 64, 1.2), (40000, 2, 64, 1.2),
+                                        (32768, 2, 8, 0.0), (32769, 2, 8, 0.0), (3, 1, 1, 0.0)])
+def test_route_one_block_and_chunked_paths(T, k, E, skew):
+    """T*k <= 65536 takes the single-block route (match_any groups), larger batches the chunked
+    three-kernel route; both must give the oracle's buckets exactly, with masked slots and
+    invalid entries (out of range, repeated in a token's row) dropped and reported."""
+    rng = np.random.default_rng(T + E)
+    if skew > 0:
+        ids = synth.route_gumbel(T, T, E, k, s=skew)
+    else:
+        ids = np.stack([rng.permutation(E)[:k] for _ in range(T)]).astype(np.int32)
+    ids = ids.astype(np.int32)
+    mask = rng.random((T, k)) < 0.1
+    ids[mask] = -1                                           # masked slots: skipped silently
+    bad_t = rng.integers(0, T, size=3)
+    if k >= 2:
+        ids[bad_t, 1] = np.where(ids[bad_t, 0] >= 0, ids[bad_t, 0], E)   # repeat or out of range
+    counts, row_off, tok, slot, status = M.moe_route(torch.from_numpy(ids).cuda(), E)
+    # reference: drop masked, out-of-range and repeated entries; tokens ascending per expert
+    lists = [[] for _ in range(E)]
+    for t in range(T):
+        seen = set()
+        for j in range(k):
+            e = int(ids[t, j])
+            if e < 0 or e >= E or e in seen:
+                continue
+            seen.add(e)
+            lists[e].append((t, j))
+    assert counts.cpu().numpy().tolist() == [len(b) for b in lists]
+    rt = [t for b in lists for (t, _) in b]
+    rs = [j for b in lists for (_, j) in b]
+    n = len(rt)
+    assert tok.cpu().numpy()[:n].tolist() == rt
+    assert slot.cpu().numpy()[:n].tolist() == rs
+    assert row_off.cpu().numpy().tolist() == np.concatenate([[0], np.cumsum([len(b) for b in lists])]).tolist()
+    assert status.item() == (1 if k >= 2 else 0)
