@@ -483,10 +483,11 @@ def test_route_many_chunks_and_masked_slots():
 
 @pytest.mark.parametrize("T,k,E,skew", [(20000, 3, 1024, 0.0), (8192, 6, 64, 1.2), (40000, 2, 64, 1.2),
                                         (32768, 2, 8, 0.0), (32769, 2, 8, 0.0), (3, 1, 1, 0.0)])
-def test_route_one_block_and_chunked_paths(T, k, E, skew):
-    """T*k <= 65536 takes the single-block route (match_any groups), larger batches the chunked
-    three-kernel route; both must give the oracle's buckets exactly, with masked slots and
-    invalid entries (out of range, repeated in a token's row) dropped and reported."""
+def test_route_place_and_split_paths(T, k, E, skew):
+    """chunks x experts <= 16K: histogram + fused scan/placement kernels (match_any groups);
+    larger (20 chunks x 1024 experts): histogram + single-block scan + chunk x expert compaction.
+    Both must give the oracle's buckets exactly, with masked slots and invalid entries (out of
+    range, repeated in a token's row) dropped and reported."""
     rng = np.random.default_rng(T + E)
     if skew > 0:
         ids = synth.route_gumbel(T, T, E, k, s=skew)
