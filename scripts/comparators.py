@@ -51,7 +51,7 @@ def main():
         counts_h = counts.cpu().numpy()
         ro = row_off.cpu().numpy()
         tok_l = tok.long()
-        plan = M.Plan(counts_h, c.H, c.N, 0, 256)
+        plan = M.Plan(counts_h, c.H, c.N, 0, 0)
         Y = torch.empty((tok.numel(), c.N), dtype=torch.bfloat16, device="cuda")
         res = {"config": name, "flops": c.flops}
         res["ours_ms"] = timed(lambda: M.moe_gemm(plan, X, tok, W, Y=Y), flush)
