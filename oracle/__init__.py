@@ -19,8 +19,10 @@ Modules
              P:298-301), tile decode (task, tile) -> rows/cols, the unbatched
              per-expert GEMM in fp64, tile-cover
              bookkeeping and an expert-parallel simulator.
+``ffn``      the full MoE FFN layer around the expert GEMM:
+             SwiGLU expert FFN (R14) and the weighted combine.
 
 Parity-pin status of every function is listed in DESIGN.md §"Oracle pins";
 no function here is "parity unpinned".
 """
-from . import mapping, moe  # noqa: F401
+from . import ffn, mapping, moe  # noqa: F401
