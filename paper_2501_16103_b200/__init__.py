@@ -26,13 +26,14 @@ MOE_PLAN_MAGIC = 0x4D4F4531
 MOE_PLAN_HEADER = 16
 MOE_PLAN_TASK_WORDS = 8
 
-# Public symbols of include/moe_sm100.h and include/moe_sm100_debug.h.
+# Public symbols of include/moe_sm100.h, moe_sm100_ep.h, moe_sm100_ffn.h and moe_sm100_debug.h.
 EXPORTED = (
     "moe_plan_blob_words", "moe_plan_build", "moe_plan_create", "moe_plan_update", "moe_plan_query",
     "moe_plan_blob", "moe_plan_device_blob", "moe_plan_destroy", "moe_route", "moe_gemm",
     "moe_decode_debug", "moe_device_info", "moe_last_error", "moe_version", "moe_probe_gather4",
     "moe_gemm_profile", "moe_plan_device", "moe_plan_sync", "moe_gemm_rowmap",
     "moe_ep_dispatch_plan", "moe_gather_rows", "moe_ep_combine_map", "moe_ep_unpack", "moe_route_plan",
+    "moe_gemm_swiglu", "moe_combine",
 )
 
 
@@ -88,6 +89,9 @@ def lib() -> ctypes.CDLL:
                                                 vp, vp, vp, vp]),
         "moe_ep_unpack": (ctypes.c_int32, [vp, vp, ctypes.c_int64, vp, vp, vp, ctypes.c_int32, ctypes.c_int32,
                                            ctypes.c_int64, vp, vp]),
+        "moe_gemm_swiglu": (ctypes.c_int32, [vp, vp, ctypes.c_int64, vp, vp, vp, vp, ctypes.c_int32, vp]),
+        "moe_combine": (ctypes.c_int32, [vp, ctypes.c_int32, ctypes.c_int64, ctypes.c_int32, ctypes.c_int64, vp, vp,
+                                         vp, ctypes.c_int32, vp, vp, ctypes.c_int32, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -278,6 +282,78 @@ def moe_gemm(plan: Plan, X, token_idx, W, Y=None, out_dtype=None, stream=None, r
         _check(lib().moe_gemm_rowmap(plan.handle, X.data_ptr(), X.shape[0], token_idx.data_ptr(), W.data_ptr(),
                                      Y.data_ptr(), yd, row_map.data_ptr(), _stream(stream)))
     return Y
+
+
+def moe_gemm_swiglu(plan: Plan, X, token_idx, W_gate, W_up, Y=None, out_dtype=None, stream=None):
+    """Y[sum m_e, I] = silu(X[token_idx] @ W_gate[e]) * (X[token_idx] @ W_up[e]) in one launch
+    (plan: N = I, bm = bn = 256; include/moe_sm100_ffn.h)."""
+    import torch
+
+    out_dtype = out_dtype or torch.bfloat16
+    for t in (X, W_gate, W_up):
+        assert t.is_cuda and t.dtype == torch.bfloat16 and t.is_contiguous()
+    assert W_gate.shape == W_up.shape
+    assert token_idx.dtype == torch.int32 and token_idx.is_contiguous()
+    if Y is None:
+        Y = torch.empty((int(token_idx.numel()), plan.N), dtype=out_dtype, device=X.device)
+    yd = MOE_DTYPE_F32 if Y.dtype == torch.float32 else MOE_DTYPE_BF16
+    _check(lib().moe_gemm_swiglu(plan.handle, X.data_ptr(), X.shape[0], token_idx.data_ptr(), W_gate.data_ptr(),
+                                 W_up.data_ptr(), Y.data_ptr(), yd, _stream(stream)))
+    return Y
+
+
+def moe_combine(Y, token_idx, slot, row_off, topk_w, out=None, out_dtype=None, stream=None):
+    """out[t] = sum_j topk_w[t, j] * Y[row(t, j)], rows recovered from the route's CSR."""
+    import torch
+
+    T, k = int(topk_w.shape[0]), int(topk_w.shape[1])
+    N = int(Y.shape[1])
+    E = int(row_off.numel()) - 1
+    assert topk_w.dtype == torch.float32 and topk_w.is_contiguous() and Y.is_contiguous()
+    assert slot is not None and slot.dtype == torch.int32 and token_idx.dtype == torch.int32
+    if out is None:
+        out = torch.empty((T, N), dtype=out_dtype or torch.bfloat16, device=Y.device)
+    yd = MOE_DTYPE_F32 if Y.dtype == torch.float32 else MOE_DTYPE_BF16
+    od = MOE_DTYPE_F32 if out.dtype == torch.float32 else MOE_DTYPE_BF16
+    _check(lib().moe_combine(Y.data_ptr(), yd, T, k, N, token_idx.data_ptr(), slot.data_ptr(), row_off.data_ptr(), E,
+                             topk_w.data_ptr(), out.data_ptr(), od, _stream(stream)))
+    return out
+
+
+class MoeFFN:
+    """The full MoE FFN layer on one GPU (R14): route (+ device plan
+    for the gated GEMM) -> device plan for the down GEMM -> moe_gemm_swiglu -> moe_gemm (rows in
+    CSR order, no gather) -> moe_combine.  Every step runs in the library's kernels; nothing
+    synchronises with the host, so a step can be captured in one CUDA graph."""
+
+    def __init__(self, W_gate, W_up, W_down, stream=None):
+        import torch
+
+        self.E, self.H, self.I = (int(x) for x in W_gate.shape)
+        assert W_down.shape == (self.E, self.I, W_down.shape[2])
+        self.Ho = int(W_down.shape[2])
+        self.Wg, self.Wu, self.Wd = W_gate, W_up, W_down
+        self.plan_gu = Plan(None, self.H, self.I, 256, 256, stream=stream, E=self.E)
+        self.plan_dn = None
+        self._rows = None
+        self._torch = torch
+
+    def forward(self, X, topk_ids, topk_w, out=None, out_dtype=None, stream=None):
+        torch = self._torch
+        T, k = int(topk_ids.shape[0]), int(topk_ids.shape[1])
+        R = T * k
+        if self.plan_dn is None:
+            bm, bn = suggest_tile(R, self.E, self.I, self.Ho)
+            self.plan_dn = Plan(None, self.I, self.Ho, bm, bn, stream=stream, E=self.E)
+        if self._rows is None or self._rows.numel() < R:
+            self._rows = torch.arange(R, dtype=torch.int32, device=X.device)
+        counts, row_off, tok, slot, _ = moe_route(topk_ids, self.E, stream=stream, plan=self.plan_gu)
+        self.plan_dn.update_device(counts, stream=stream)
+        Hmid = moe_gemm_swiglu(self.plan_gu, X, tok, self.Wg, self.Wu, stream=stream)
+        Y = moe_gemm(self.plan_dn, Hmid, self._rows[:R], self.Wd, stream=stream)
+        out = moe_combine(Y, tok, slot, row_off, topk_w, out=out, out_dtype=out_dtype, stream=stream)
+        self.last = dict(counts=counts, row_off=row_off, token_idx=tok, slot=slot, h=Hmid, y=Y)
+        return out
 
 
 PROF_SLOTS = ("mma_wait_tmem", "mma_wait_full", "mma_total", "prod_wait_empty", "epi_wait_full", "epi_work",

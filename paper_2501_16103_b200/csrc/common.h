@@ -7,6 +7,7 @@
 
 #include "moe_sm100.h"
 #include "moe_sm100_ep.h"
+#include "moe_sm100_ffn.h"
 
 namespace moe {
 

@@ -232,12 +232,17 @@ struct Geo {
 // shared-memory fills, half the barrier round trips).  The accumulator is not double-buffered: the
 // MMA waits for the epilogue to drain half 0 before the next tile's first MMAs, half 1 before the
 // next tile's first half-1 MMAs.
-template <bool kProf, int kCta, bool kSplit, bool kWide = false>
+// kGated (with kWide; moe_gemm_swiglu): the two N = 256 blocks are the SAME
+// 256 columns of W_gate (tmW) and W_up (tmW2); the epilogue writes silu(gate) * up (R14),
+// so a tile covers bn = 256 output columns.
+template <bool kProf, int kCta, bool kSplit, bool kWide = false, bool kGated = false>
 __global__ void __launch_bounds__(kThreads, 1)
     moe_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
-                    const __grid_constant__ CUtensorMap tmY, const GemmArgs a) {
+                    const __grid_constant__ CUtensorMap tmW2, const __grid_constant__ CUtensorMap tmY,
+                    const GemmArgs a) {
   static_assert(!kSplit || kCta == 2, "swap-AB tail tiles need CTA pairs (M = 256)");
   static_assert(!kWide || (kCta == 2 && !kSplit), "wide tiles are CTA-pair tiles");
+  static_assert(!kGated || kWide, "gated tiles use the wide tile's two accumulator blocks");
   constexpr int kSt = Geo<kCta, kSplit, kWide>::kStages;
   constexpr int kBSt = Geo<kCta, kSplit, kWide>::kBStage;
   constexpr int kHalves = kWide ? 2 : 1;                   // N = 256 MMA blocks per tile
@@ -289,6 +294,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmX);
     prefetch_tmap(&tmW);
+    if (kGated) prefetch_tmap(&tmW2);
     if (a.tma_store) prefetch_tmap(&tmY);
   }
   if (warp == kMmaWarp) tmem_alloc<kTmemCols, kCta>(smem_u32(tmem_holder));
@@ -407,9 +413,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       int h, task, l;
       map_tile(s_prefix, s_sigma, a.M_pad, v, h, task, l);
       const Tile t = load_tile<kSplit>(params, task, l);
-      const int bnp = t.bn / kHalves;               // columns of one MMA block
+      const int bnp = kGated ? t.bn : t.bn / kHalves;   // columns of one MMA block
       const int bnc = bnp / kCta;                   // columns of an MMA block staged by this CTA
-      const int n0 = t.ct * t.bn + (int)rank * bnc; // block h starts at n0 + h * bnp
+      const int n0 = t.ct * t.bn + (int)rank * bnc; // block h starts at n0 + h * bnp (gated: W_up at n0)
       const int nbox = (bnc + 63) >> 6;
       for (int kb = 0; kb < a.num_kb; ++kb, ++g) {
         const int s = g % kSt;
@@ -442,12 +448,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int hf = 0; hf < kHalves; ++hf) {
               const uint32_t dst = dstB + hf * nbox * kBBoxBytes;
-              const int nh = n0 + hf * bnp;
+              const int nh = kGated ? n0 : n0 + hf * bnp;
+              const CUtensorMap* wm = kGated && hf == 1 ? &tmW2 : &tmW;
               if (a.w4d) {
-                tma_load_4d_pair(&tmW, fb, dst, 0, kb * kBK, nh >> 6, t.expert, pol_w);
+                tma_load_4d_pair(wm, fb, dst, 0, kb * kBK, nh >> 6, t.expert, pol_w);
               } else {
                 for (int j = 0; j < nbox; ++j)
-                  tma_load_3d_pair(&tmW, fb, dst + j * kBBoxBytes, nh + j * 64, kb * kBK, t.expert, pol_w);
+                  tma_load_3d_pair(wm, fb, dst + j * kBBoxBytes, nh + j * 64, kb * kBK, t.expert, pol_w);
               }
             }
           } else {
@@ -489,8 +496,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         // kind 1: D[cols, tokens] = A[W block as MN-major M-operand] * B[tail tokens (K-major)],
         //         M = the pair's 256 output columns, N = the tail height (swap-AB).
         const uint32_t idesc = swap ? idesc_bf16_f32(kPairRows, t.height, /*A MN-major*/ 1, /*B K-major*/ 0)
-                                    : idesc_bf16_f32(kPairRows, t.bn / kHalves, /*A K-major*/ 0,
-                                                     /*B MN-major*/ 1);
+                                    : idesc_bf16_f32(kPairRows, kGated ? t.bn : t.bn / kHalves,
+                                                     /*A K-major*/ 0, /*B MN-major*/ 1);
         // Double-buffered: wait for accumulator `acc`.  Wide: accumulator half 0 now, half 1 just
         // before the first half-1 MMA (the epilogue drains the halves in order).
         wait_timed<kProf>(tempty_bar(acc), acc_phase ^ 1u, c_tmem);     // epilogue(s) drained this accumulator
@@ -520,7 +527,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             // (SBO); K step of 16 rows = +2 KB.  The two kinds only swap the operand roles.
 #ifdef MOE_EXPERIMENTS
             if (a.experiment & 16) {   // B read as K-major (wrong Y): is the MN-major B operand slower?
-              const uint32_t idk = idesc_bf16_f32(kPairRows, t.bn / kHalves, 0, 0);
+              const uint32_t idk = idesc_bf16_f32(kPairRows, kGated ? t.bn : t.bn / kHalves, 0, 0);
 #pragma unroll
               for (int kk = 0; kk < kBK / 16; ++kk) {
                 const uint64_t ad = smem_desc_sw128(a0 + kk * 32, 16, 1024);
@@ -687,65 +694,84 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool valid = grow < t.rows;
       const int64_t yrow = a.y_row_map ? (int64_t)__ldg(a.y_row_map + t.row0 + min(grow, t.rows - 1))
                                        : (int64_t)t.row0 + grow;
-      const int bnp = t.bn / kHalves;               // columns of one accumulator block
       const int wrow0 = grow - lane;                // first task row of this warp's quarter
       const bool tma_rows = !kSplit && a.tma_store && wrow0 + 32 <= t.rows;
-#pragma unroll 1
-      for (int hf = 0; hf < kHalves; ++hf) {
-        const int n0 = t.ct * t.bn + hf * bnp;
-        const int col_end = min(n0 + bnp, a.N);
-        const int slot = kWide ? hf : acc;          // TMEM block and its tmem-empty barrier
-        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + slot * kAccCols;
+      const uint32_t xr = (uint32_t)((lane >> 1) & 3);
+      // Write 32 fp32 results of this lane's row at columns [col, col + 32).  Full 32-row quarters:
+      // bf16 into a 64B-swizzled 32 x 32 staging buffer (conflict-free 16-byte st.shared) and one TMA
+      // tile store (with four warps two buffers alternate, so converting chunk i+1 overlaps storing
+      // chunk i).  Quarters holding the task's last rows take masked register stores: a box must not
+      // touch the next task's rows.
+      auto put_chunk = [&](uint32_t (&r)[32], int col, int col_end) {
+#ifdef MOE_EXPERIMENTS
+        if (a.experiment & 8) return;
+#endif
         if (tma_rows) {
-          // All 32 rows belong to the task: convert to bf16 into a 64B-swizzled 32 x 32 staging
-          // buffer (conflict-free 16-byte st.shared) and let TMA write the block; two buffers
-          // alternate, so the conversion of chunk i+1 overlaps the store of chunk i.  Partial
-          // quarters (the task's last rows) take the masked register path below: a box must not
-          // touch the next task's rows.
-          const uint32_t xr = (uint32_t)((lane >> 1) & 3);
-          for (int c = 32 * cg; c < bnp && n0 + c < a.N; c += 32 * kEpiGroups) {
-            uint32_t r[32];
-            tmem_ld32(taddr + c, r);
-            tmem_wait_ld();
-            // Four warps: two buffers per warp, reused every other chunk; eight: one buffer.
-            const uint32_t buf = kEpiWarps == 4 ? ebuf + (n_chunk & 1u) * 2048u : ebuf;
-            if (lane == 0) {                                  // the store that last used buf has read it
-              if constexpr (kEpiWarps == 4) bulk_wait_group_read<1>();
-              else bulk_wait_group_read<0>();
-            }
-            __syncwarp();
+          const uint32_t buf = kEpiWarps == 4 ? ebuf + (n_chunk & 1u) * 2048u : ebuf;
+          if (lane == 0) {                                  // the store that last used buf has read it
+            if constexpr (kEpiWarps == 4) bulk_wait_group_read<1>();
+            else bulk_wait_group_read<0>();
+          }
+          __syncwarp();
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
-              st_shared_v4(buf + lane * 64 + ((j ^ xr) << 4), pack_bf16(r[8 * j], r[8 * j + 1]),
-                           pack_bf16(r[8 * j + 2], r[8 * j + 3]), pack_bf16(r[8 * j + 4], r[8 * j + 5]),
-                           pack_bf16(r[8 * j + 6], r[8 * j + 7]));
-            fence_proxy_async_smem();
-            __syncwarp();
-#ifdef MOE_EXPERIMENTS
-            if (!(a.experiment & 8))
-#endif
-            if (lane == 0) {
-              tma_store_2d(&tmY, buf, n0 + c, t.row0 + wrow0);
-              bulk_commit_group();
-            }
-            ++n_chunk;
+          for (int j = 0; j < 4; ++j)
+            st_shared_v4(buf + lane * 64 + ((j ^ xr) << 4), pack_bf16(r[8 * j], r[8 * j + 1]),
+                         pack_bf16(r[8 * j + 2], r[8 * j + 3]), pack_bf16(r[8 * j + 4], r[8 * j + 5]),
+                         pack_bf16(r[8 * j + 6], r[8 * j + 7]));
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmY, buf, col, t.row0 + wrow0);
+            bulk_commit_group();
           }
-        } else {
-          for (int c = 32 * cg; c < bnp; c += 32 * kEpiGroups) {
-            uint32_t r[32];
-            tmem_ld32(taddr + c, r);
-            tmem_wait_ld();
-#ifdef MOE_EXPERIMENTS
-            if (a.experiment & 8) continue;
-#endif
-            if (valid) store_chunk(a, yrow, n0 + c, col_end, r);
+          ++n_chunk;
+        } else if (valid) {
+          store_chunk(a, yrow, col, col_end, r);
+        }
+      };
+      if constexpr (kGated) {
+        // h = silu(gate) * up: gate in TMEM block 0, up in block 1, same 256 output columns.
+        const int n0 = t.ct * t.bn;
+        const int col_end = min(n0 + t.bn, a.N);
+        const uint32_t ta = tmem_base + ((uint32_t)(q * 32) << 16);
+        for (int c = 32 * cg; c < t.bn && n0 + c < a.N; c += 32 * kEpiGroups) {
+          uint32_t g[32], u[32];
+          tmem_ld32(ta + c, g);
+          tmem_ld32(ta + kAccCols + c, u);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const float gv = __uint_as_float(g[i]);
+            g[i] = __float_as_uint(gv / (1.0f + __expf(-gv)) * __uint_as_float(u[i]));
           }
+          put_chunk(g, n0 + c, col_end);
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
-          if constexpr (kCta == 2) mbar_arrive_cluster(leader(tempty_bar(slot)));
-          else mbar_arrive(tempty_bar(slot));
+          mbar_arrive_cluster(leader(tempty_bar(0)));
+          mbar_arrive_cluster(leader(tempty_bar(1)));
+        }
+      } else {
+        const int bnp = t.bn / kHalves;             // columns of one accumulator block
+#pragma unroll 1
+        for (int hf = 0; hf < kHalves; ++hf) {
+          const int n0 = t.ct * t.bn + hf * bnp;
+          const int col_end = min(n0 + bnp, a.N);
+          const int slot = kWide ? hf : acc;        // TMEM block and its tmem-empty barrier
+          const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + slot * kAccCols;
+          for (int c = 32 * cg; c < bnp && (!tma_rows || n0 + c < a.N); c += 32 * kEpiGroups) {
+            uint32_t r[32];
+            tmem_ld32(taddr + c, r);
+            tmem_wait_ld();
+            put_chunk(r, n0 + c, col_end);
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            if constexpr (kCta == 2) mbar_arrive_cluster(leader(tempty_bar(slot)));
+            else mbar_arrive(tempty_bar(slot));
+          }
         }
       }
       if constexpr (kProf) c_work += clock64() - w0;
@@ -924,9 +950,10 @@ extern "C" moe_status moe_device_info(int32_t* sm_count, int32_t* cc_major, int3
 
 namespace {
 
-template <bool kProf, int kCta, bool kSplit, bool kWide = false>
+template <bool kProf, int kCta, bool kSplit, bool kWide = false, bool kGated = false>
 cudaError_t set_attr() {
-  return cudaFuncSetAttribute(moe_gemm_kernel<kProf, kCta, kSplit, kWide>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  return cudaFuncSetAttribute(moe_gemm_kernel<kProf, kCta, kSplit, kWide, kGated>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)(Geo<kCta, kSplit, kWide>::kSmem + 8 * kMaxMPad));
 }
 
@@ -934,10 +961,11 @@ cudaError_t set_smem_attrs() {
   static std::once_flag once;
   static cudaError_t err = cudaSuccess;
   std::call_once(once, [] {
-    cudaError_t e[8] = {set_attr<false, 1, false>(),      set_attr<true, 1, false>(),
+    cudaError_t e[10] = {set_attr<false, 1, false>(),      set_attr<true, 1, false>(),
                         set_attr<false, 2, false>(),      set_attr<true, 2, false>(),
                         set_attr<false, 2, true>(),       set_attr<true, 2, true>(),
-                        set_attr<false, 2, false, true>(), set_attr<true, 2, false, true>()};
+                        set_attr<false, 2, false, true>(), set_attr<true, 2, false, true>(),
+                        set_attr<false, 2, false, true, true>(), set_attr<true, 2, false, true, true>()};
     for (cudaError_t x : e)
       if (x != cudaSuccess && err == cudaSuccess) err = x;
   });
@@ -946,7 +974,7 @@ cudaError_t set_smem_attrs() {
 
 static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, const int32_t* token_idx,
                               const void* W, void* Y, int32_t y_dtype, void* stream, long long* prof,
-                              const int32_t* y_row_map = nullptr) {
+                              const int32_t* y_row_map = nullptr, const void* W2 = nullptr) {
   moe::clear_error();
   if (!plan) MOE_FAIL(MOE_ERR_INVALID, "moe_gemm: null plan");
   moe::BlobView v;
@@ -987,10 +1015,19 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
   moe_status st = make_x_map(&tmX, X, T, v.H, (experiment & 4) ? kBM : 1);
   if (st != MOE_OK) return st;
   const bool w4d = (v.N % 64) == 0;
+  const bool gated = W2 != nullptr;                // moe_gemm_swiglu: W_gate / W_up blocks
+  if (gated && !(v.bm == 256 && v.bn == 256))
+    MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_gemm_swiglu: the plan must have bm = 256, bn = 256 (got %d x %d)", v.bm, v.bn);
+  if (gated && !aligned16(W2)) MOE_FAIL(MOE_ERR_INVALID, "moe_gemm_swiglu: W_up must be 16-byte aligned");
   const bool wide = v.bm == 256 && v.bn == 512;   // wide pair tile: two N = 256 MMA blocks
   const int cta = v.bm / kBM;                      // CTAs per tile: each stages bn / cta W columns
   st = make_w_map(&tmW, W, v.E, v.H, v.N, v.bn / cta / (wide ? 2 : 1), w4d);   // per MMA block
   if (st != MOE_OK) return st;
+  CUtensorMap tmW2 = tmW;
+  if (gated) {
+    st = make_w_map(&tmW2, W2, v.E, v.H, v.N, v.bn / cta, w4d);
+    if (st != MOE_OK) return st;
+  }
 
   // TMA-store epilogue: bf16 Y in CSR row order (the EP combine path scatters rows: register stores).
   CUtensorMap tmY;
@@ -1042,7 +1079,8 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
   if (v.bm == 256) {
     const bool split = (v.flags & MOE_SPLIT_TAIL) != 0;
     const int pairs = v.total < 0 ? sm_count_cached() / 2 : std::min(v.total, sm_count_cached() / 2);
-    const size_t smem = (split ? Geo<2, true>::kSmem : wide ? Geo<2, false, true>::kSmem : Geo<2, false>::kSmem) +
+    const size_t smem = (split ? Geo<2, true>::kSmem : wide || gated ? Geo<2, false, true>::kSmem
+                                                                 : Geo<2, false>::kSmem) +
                         8 * (size_t)v.M_pad;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * pairs);
@@ -1059,15 +1097,18 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
     cfg.attrs = attr;
     cfg.numAttrs = 2;
     cudaError_t le;
-    if (wide)
-      le = prof ? cudaLaunchKernelEx(&cfg, moe_gemm_kernel<true, 2, false, true>, tmX, tmW, tmY, a)
-                : cudaLaunchKernelEx(&cfg, moe_gemm_kernel<false, 2, false, true>, tmX, tmW, tmY, a);
+    if (gated)
+      le = prof ? cudaLaunchKernelEx(&cfg, moe_gemm_kernel<true, 2, false, true, true>, tmX, tmW, tmW2, tmY, a)
+                : cudaLaunchKernelEx(&cfg, moe_gemm_kernel<false, 2, false, true, true>, tmX, tmW, tmW2, tmY, a);
+    else if (wide)
+      le = prof ? cudaLaunchKernelEx(&cfg, moe_gemm_kernel<true, 2, false, true>, tmX, tmW, tmW2, tmY, a)
+                : cudaLaunchKernelEx(&cfg, moe_gemm_kernel<false, 2, false, true>, tmX, tmW, tmW2, tmY, a);
     else if (split)
-      le = prof ? cudaLaunchKernelEx(&cfg, moe_gemm_kernel<true, 2, true>, tmX, tmW, tmY, a)
-                : cudaLaunchKernelEx(&cfg, moe_gemm_kernel<false, 2, true>, tmX, tmW, tmY, a);
+      le = prof ? cudaLaunchKernelEx(&cfg, moe_gemm_kernel<true, 2, true>, tmX, tmW, tmW2, tmY, a)
+                : cudaLaunchKernelEx(&cfg, moe_gemm_kernel<false, 2, true>, tmX, tmW, tmW2, tmY, a);
     else
-      le = prof ? cudaLaunchKernelEx(&cfg, moe_gemm_kernel<true, 2, false>, tmX, tmW, tmY, a)
-                : cudaLaunchKernelEx(&cfg, moe_gemm_kernel<false, 2, false>, tmX, tmW, tmY, a);
+      le = prof ? cudaLaunchKernelEx(&cfg, moe_gemm_kernel<true, 2, false>, tmX, tmW, tmW2, tmY, a)
+                : cudaLaunchKernelEx(&cfg, moe_gemm_kernel<false, 2, false>, tmX, tmW, tmW2, tmY, a);
     if (le != cudaSuccess) MOE_FAIL(MOE_ERR_CUDA, "moe_gemm pair launch: %s", cudaGetErrorString(le));
   } else {
     const int grid = v.total < 0 ? sm_count_cached() : std::min(v.total, sm_count_cached());
@@ -1081,8 +1122,8 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t le = prof ? cudaLaunchKernelEx(&cfg, moe_gemm_kernel<true, 1, false>, tmX, tmW, tmY, a)
-                          : cudaLaunchKernelEx(&cfg, moe_gemm_kernel<false, 1, false>, tmX, tmW, tmY, a);
+    cudaError_t le = prof ? cudaLaunchKernelEx(&cfg, moe_gemm_kernel<true, 1, false>, tmX, tmW, tmW2, tmY, a)
+                          : cudaLaunchKernelEx(&cfg, moe_gemm_kernel<false, 1, false>, tmX, tmW, tmW2, tmY, a);
     if (le != cudaSuccess) MOE_FAIL(MOE_ERR_CUDA, "moe_gemm launch: %s", cudaGetErrorString(le));
   }
   cudaError_t e = cudaGetLastError();
@@ -1097,6 +1138,12 @@ extern "C" {
 moe_status moe_gemm(const moe_plan* plan, const void* X, int64_t T, const int32_t* token_idx, const void* W,
                     void* Y, int32_t y_dtype, void* stream) {
   return gemm_launch(plan, X, T, token_idx, W, Y, y_dtype, stream, nullptr);
+}
+
+moe_status moe_gemm_swiglu(const moe_plan* plan, const void* X, int64_t T, const int32_t* token_idx,
+                           const void* W_gate, const void* W_up, void* Y, int32_t y_dtype, void* stream) {
+  if (!W_up) MOE_FAIL(MOE_ERR_INVALID, "moe_gemm_swiglu: null W_up");
+  return gemm_launch(plan, X, T, token_idx, W_gate, Y, y_dtype, stream, nullptr, nullptr, W_up);
 }
 
 moe_status moe_gemm_rowmap(const moe_plan* plan, const void* X, int64_t T, const int32_t* token_idx,
