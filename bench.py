@@ -187,6 +187,110 @@ def run_reference(args, cfg):
     print(json.dumps(line), flush=True)
 
 
+def route_launches(T: int, E: int) -> int:
+    """Kernels one moe_route(_plan) call launches (route.cu): histogram + fused scan/compaction
+    while chunks x experts <= 16384, else histogram + scan + compaction."""
+    chunks = max(1, -(-T // 1024))
+    return 2 if chunks * E <= 16384 else 3
+
+
+def run_ffn(args, cfg):
+    """--ffn: the full MoE FFN layer on the config's shape, N = the FFN width I:
+    route + device plans -> moe_gemm_swiglu (gate/up, SwiGLU epilogue) -> moe_gemm (down, H_out = H)
+    -> moe_combine, one CUDA graph per step.  Useful flops = 6 * sum(m_e) * H * I."""
+    import torch
+
+    import paper_2501_16103_b200 as M
+
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    M.moe_device_info()
+    peaks, peak_src = load_peaks()
+    H, I, E = cfg.H, cfg.N, cfg.E
+    ids = synth.route(cfg, args.seed)
+    topk_d = torch.from_numpy(ids).to(dev)
+    rng = np.random.default_rng(args.seed)
+    w = rng.random((cfg.T, cfg.k)).astype(np.float32)
+    w /= w.sum(axis=1, keepdims=True)
+    w_d = torch.from_numpy(w).to(dev)
+    Xd = synth.make_x_torch(args.seed, cfg.T, H, device=dev)
+    Wg = synth.make_w_torch(args.seed, E, H, I, device=dev)
+    Wu = synth.make_w_torch(args.seed + 1, E, H, I, device=dev)
+    Wdn = synth.make_w_torch(args.seed + 2, E, I, H, device=dev)
+    layer = M.MoeFFN(Wg, Wu, Wdn)
+    out = torch.empty((cfg.T, H), dtype=torch.bfloat16, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    rows = int((ids >= 0).sum())
+    flops = 6.0 * rows * H * I
+    for _ in range(args.warmup):
+        layer.forward(Xd, topk_d, w_d, out=out)
+    torch.cuda.synchronize()
+    # per-stage times (eager, events on the launching stream)
+    stages = {"route_plans": [], "swiglu_gemm": [], "down_gemm": [], "combine": []}
+    for _ in range(max(3, min(args.steps, 10))):
+        flush.zero_()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+        ev[0].record(stream)
+        counts, row_off, tok, slot, _ = M.moe_route(topk_d, E, plan=layer.plan_gu)
+        layer.plan_dn.update_device(counts)
+        ev[1].record(stream)
+        h = M.moe_gemm_swiglu(layer.plan_gu, Xd, tok, Wg, Wu)
+        ev[2].record(stream)
+        y = M.moe_gemm(layer.plan_dn, h, layer._rows[: cfg.T * cfg.k], Wdn)
+        ev[3].record(stream)
+        M.moe_combine(y, tok, slot, row_off, w_d, out=out)
+        ev[4].record(stream)
+        ev[4].synchronize()
+        for i, k in enumerate(stages):
+            stages[k].append(ev[i].elapsed_time(ev[i + 1]))
+    st = {k: statistics.mean(v) for k, v in stages.items()}
+    graph = torch.cuda.CUDAGraph()
+    side = torch.cuda.Stream()
+    side.wait_stream(stream)
+    with torch.cuda.stream(side):
+        layer.forward(Xd, topk_d, w_d, out=out)
+    stream.wait_stream(side)
+    with torch.cuda.graph(graph):
+        layer.forward(Xd, topk_d, w_d, out=out)
+    for _ in range(3):
+        graph.replay()
+    torch.cuda.synchronize()
+    step_ms = []
+    with ClockSampler(0) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            graph.replay()
+            s1.record(stream)
+            s1.synchronize()
+            step_ms.append(s0.elapsed_time(s1))
+    ms = statistics.mean(step_ms)
+    peak = float(peaks["bf16_tflops"])
+    gu = 4.0 * rows * H * I / (st["swiglu_gemm"] * 1e-3) / 1e12
+    dn = 2.0 * rows * H * I / (st["down_gemm"] * 1e-3) / 1e12
+    comb_bytes = rows * H * 2 + cfg.T * H * 2 + cfg.T * cfg.k * 8
+    line = {
+        "metric": "MoE FFN layer TFLOP/s (SwiGLU gate/up + down + weighted combine)", "value": flops / (ms * 1e-3) / 1e12,
+        "unit": "TFLOP/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "cuda_graph": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic",
+        "config": {"workload": f"{cfg.name} FFN: E={E} top-{cfg.k} T={cfg.T} H={H} I={I} routing={cfg.routing} "
+                               f"seed={args.seed}", "tiles": f"gate/up {layer.plan_gu.bm}x{layer.plan_gu.bn} (x2 "
+                               f"accumulators), down {layer.plan_dn.bm}x{layer.plan_dn.bn}",
+                   "l2": "flushed before every timed step (256 MiB memset)"},
+        "stages_ms": st,
+        "kernels": {"swiglu_gemm_tflops": gu, "down_gemm_tflops": dn,
+                    "combine_gbs": comb_bytes / (st["combine"] * 1e-3) / 1e9},
+        "roofline": {"bound": "tensor", "achieved": gu, "peak": peak, "unit": "TFLOP/s", "frac": gu / peak,
+                     "traffic": None, "kernel": "moe_gemm_kernel (gated)", "peak_source": peak_src},
+        "gpu_launches": (route_launches(cfg.T, E) + 1 + 1 + 1 + 2) * args.steps,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
 def config_dict(cfg, args):
     return {"workload": f"{cfg.name}: E={cfg.E} top-{cfg.k} T={cfg.T} H={cfg.H} N={cfg.N} "
                         f"routing={cfg.routing} seed={args.seed}",
@@ -389,7 +493,7 @@ def run_ours(args, cfg):
                           "traffic_source": tsrc}),
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": 4 * args.steps,   # route hist / scan(+plan) / scatter, GEMM
+            "gpu_launches": (route_launches(cfg.T, cfg.E) + 1) * args.steps,   # route (+plan), GEMM
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -532,6 +636,7 @@ def main():
                     help="time eager launches instead of one CUDA graph per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
+    ap.add_argument("--ffn", action="store_true", help="time the full MoE FFN layer (gate/up SwiGLU + down + combine)")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")
@@ -539,6 +644,8 @@ def main():
     ws = dist_env()[0]
     if args.impl == "reference":
         run_reference(args, cfg)
+    elif args.ffn:
+        run_ffn(args, cfg)
     elif ws > 1 or args.ep:
         run_ep(args, cfg)
     else:

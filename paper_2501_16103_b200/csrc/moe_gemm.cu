@@ -166,6 +166,12 @@ __device__ __forceinline__ Tile load_tile(const int32_t* params, int task, int l
   return t;
 }
 
+__device__ __forceinline__ float tanh_approx(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(uint32_t lo, uint32_t hi) {
   __nv_bfloat162 b = __floats2bfloat162_rn(__uint_as_float(lo), __uint_as_float(hi));
   return *reinterpret_cast<uint32_t*>(&b);
@@ -232,9 +238,12 @@ struct Geo {
 // shared-memory fills, half the barrier round trips).  The accumulator is not double-buffered: the
 // MMA waits for the epilogue to drain half 0 before the next tile's first MMAs, half 1 before the
 // next tile's first half-1 MMAs.
-// kGated (with kWide; moe_gemm_swiglu): the two N = 256 blocks are the SAME
-// 256 columns of W_gate (tmW) and W_up (tmW2); the epilogue writes silu(gate) * up (R14),
-// so a tile covers bn = 256 output columns.
+// kGated (with kWide; moe_gemm_swiglu): a tile covers bn = 256 output columns
+// n0 + [0, 256).  MMA block b (N = 256) multiplies [W_gate cols n0 + 128b + [0,128) | W_up cols
+// n0 + 128b + [0,128)] — the pair leader stages the gate half, the peer the up half — so TMEM
+// block b holds gate in columns [0,128) and up in [128,256) of the same 128 outputs, and the
+// epilogue writes silu(gate) * up (R14) block by block, freeing each as the plain wide
+// tile does.
 template <bool kProf, int kCta, bool kSplit, bool kWide = false, bool kGated = false>
 __global__ void __launch_bounds__(kThreads, 1)
     moe_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
@@ -413,9 +422,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       int h, task, l;
       map_tile(s_prefix, s_sigma, a.M_pad, v, h, task, l);
       const Tile t = load_tile<kSplit>(params, task, l);
-      const int bnp = kGated ? t.bn : t.bn / kHalves;   // columns of one MMA block
-      const int bnc = bnp / kCta;                   // columns of an MMA block staged by this CTA
-      const int n0 = t.ct * t.bn + (int)rank * bnc; // block h starts at n0 + h * bnp (gated: W_up at n0)
+      const int bnp = t.bn / kHalves;               // columns of one MMA block (gated: 128 gate + 128 up)
+      const int bnc = kGated ? 128 : bnp / kCta;    // columns of an MMA block staged by this CTA
+      const int n0 = kGated ? t.ct * t.bn : t.ct * t.bn + (int)rank * bnc;   // block h at n0 + h * bnp
       const int nbox = (bnc + 63) >> 6;
       for (int kb = 0; kb < a.num_kb; ++kb, ++g) {
         const int s = g % kSt;
@@ -448,8 +457,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int hf = 0; hf < kHalves; ++hf) {
               const uint32_t dst = dstB + hf * nbox * kBBoxBytes;
-              const int nh = kGated ? n0 : n0 + hf * bnp;
-              const CUtensorMap* wm = kGated && hf == 1 ? &tmW2 : &tmW;
+              const int nh = n0 + hf * bnp;
+              const CUtensorMap* wm = kGated && rank == 1 ? &tmW2 : &tmW;   // gated: leader gate, peer up
               if (a.w4d) {
                 tma_load_4d_pair(wm, fb, dst, 0, kb * kBK, nh >> 6, t.expert, pol_w);
               } else {
@@ -496,7 +505,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // kind 1: D[cols, tokens] = A[W block as MN-major M-operand] * B[tail tokens (K-major)],
         //         M = the pair's 256 output columns, N = the tail height (swap-AB).
         const uint32_t idesc = swap ? idesc_bf16_f32(kPairRows, t.height, /*A MN-major*/ 1, /*B K-major*/ 0)
-                                    : idesc_bf16_f32(kPairRows, kGated ? t.bn : t.bn / kHalves,
+                                    : idesc_bf16_f32(kPairRows, kGated ? 256 : t.bn / kHalves,
                                                      /*A K-major*/ 0, /*B MN-major*/ 1);
         // Double-buffered: wait for accumulator `acc`.  Wide: accumulator half 0 now, half 1 just
         // before the first half-1 MMA (the epilogue drains the halves in order).
@@ -527,7 +536,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             // (SBO); K step of 16 rows = +2 KB.  The two kinds only swap the operand roles.
 #ifdef MOE_EXPERIMENTS
             if (a.experiment & 16) {   // B read as K-major (wrong Y): is the MN-major B operand slower?
-              const uint32_t idk = idesc_bf16_f32(kPairRows, kGated ? t.bn : t.bn / kHalves, 0, 0);
+              const uint32_t idk = idesc_bf16_f32(kPairRows, kGated ? 256 : t.bn / kHalves, 0, 0);
 #pragma unroll
               for (int kk = 0; kk < kBK / 16; ++kk) {
                 const uint64_t ad = smem_desc_sw128(a0 + kk * 32, 16, 1024);
@@ -730,27 +739,29 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       };
       if constexpr (kGated) {
-        // h = silu(gate) * up: gate in TMEM block 0, up in block 1, same 256 output columns.
-        const int n0 = t.ct * t.bn;
-        const int col_end = min(n0 + t.bn, a.N);
-        const uint32_t ta = tmem_base + ((uint32_t)(q * 32) << 16);
-        for (int c = 32 * cg; c < t.bn && n0 + c < a.N; c += 32 * kEpiGroups) {
-          uint32_t g[32], u[32];
-          tmem_ld32(ta + c, g);
-          tmem_ld32(ta + kAccCols + c, u);
-          tmem_wait_ld();
+        // Block b: gate in TMEM columns [0,128), up in [128,256) of outputs n0 + 128b + [0,128).
+#pragma unroll 1
+        for (int hf = 0; hf < 2; ++hf) {
+          const int n0 = t.ct * t.bn + hf * 128;
+          const int col_end = min(n0 + 128, a.N);
+          const uint32_t ta = tmem_base + ((uint32_t)(q * 32) << 16) + hf * kAccCols;
+          for (int c = 32 * cg; c < 128 && (!tma_rows || n0 + c < a.N); c += 32 * kEpiGroups) {
+            uint32_t g[32], u[32];
+            tmem_ld32(ta + c, g);
+            tmem_ld32(ta + 128 + c, u);
+            tmem_wait_ld();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const float gv = __uint_as_float(g[i]);
-            g[i] = __float_as_uint(gv / (1.0f + __expf(-gv)) * __uint_as_float(u[i]));
+            for (int i = 0; i < 32; ++i) {
+              // silu(g) = g * sigmoid(g) = 0.5 g (1 + tanh(g / 2)): one SFU op (tanh.approx, relative
+              // error ~2^-11, below the bf16 rounding of h that follows) and two FMAs.
+              const float hg = 0.5f * __uint_as_float(g[i]);
+              g[i] = __float_as_uint(fmaf(hg, tanh_approx(hg), hg) * __uint_as_float(u[i]));
+            }
+            put_chunk(g, n0 + c, col_end);
           }
-          put_chunk(g, n0 + c, col_end);
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          mbar_arrive_cluster(leader(tempty_bar(0)));
-          mbar_arrive_cluster(leader(tempty_bar(1)));
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(leader(tempty_bar(hf)));
         }
       } else {
         const int bnp = t.bn / kHalves;             // columns of one accumulator block
