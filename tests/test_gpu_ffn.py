@@ -112,3 +112,10 @@ def test_moe_ffn_layer_matches_oracle(T, E, k, H, I, Ho, masked):
                          torch.from_numpy(w).cuda(), out_dtype=torch.float32)
     torch.cuda.synchronize()
     tol_check(out2.cpu().double().numpy(), offn.moe_ffn(X, Wg, Wu, Wd, ids2, w), "ffn step 2")
+
+
+def test_graft_entry_smoke():
+    """The driver's round-end smoke() must pass on the GPU box."""
+    import __graft_entry__
+
+    __graft_entry__.smoke()
