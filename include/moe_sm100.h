@@ -59,11 +59,12 @@ typedef int32_t moe_status;
 /* Plan flags. */
 #define MOE_PAD_MAX     0u  /* pad TilePrefix with INT32_MAX ("the maximum possible value") */
 #define MOE_PAD_REPEAT  1u  /* pad TilePrefix by repeating its last element                */
-#define MOE_SPLIT_TAIL  2u  /* bm = bn = 256: an expert whose m is not a multiple of 256 is kind 1 —
-                               the LAST row tile of each column block (its m mod 256 tail rows) runs
-                               as a swap-AB pair tile (W block as the M = 256 operand, the tail's
-                               tokens as N = tail rounded up to 16).  Same tile partition; a second
-                               tiling strategy in the launch (Alg. 3 with K = 2).        */
+#define MOE_SPLIT_TAIL  2u  /* bm = 256, bn = 256 or 512: an expert whose m is not a multiple of 256
+                               is kind 1 — the LAST row tile of each column block (its m mod 256 tail
+                               rows) runs as a swap-AB pair tile (each 256-column W block as the
+                               M = 256 operand, the tail's tokens as N = tail rounded up to 16).
+                               Same tile partition; a second tiling strategy in the launch
+                               (Alg. 3 with K = 2).                                      */
 
 /* ---- the compressed mapping ("plan blob"), int32 words -------------------
  * Built on the host by moe_plan_build (no GPU needed) and copied once to the
@@ -107,7 +108,7 @@ int64_t moe_plan_blob_words(int32_t E);
  *                    bm = 0: automatic — 256 unless the pair tiles' extra padding rows exceed
  *                    their ~10% per-row speed advantage (sum of ceil(m_e/256)*256 > 1.10 *
  *                    sum of ceil(m_e/128)*128).  bn = 0: automatic — 512 when bm resolves to
- *                    256, N >= 512 and MOE_SPLIT_TAIL is off, else 256.  The blob records
+ *                    256 and N >= 512, else 256.  The blob records
  *                    the resolved bm and bn.
  *   flags            MOE_PAD_MAX | MOE_PAD_REPEAT, optionally | MOE_SPLIT_TAIL and one of
  *                    MOE_ORDER_ALTERNATING / MOE_ORDER_HALF_INTERVAL (sigma order, §4.2).

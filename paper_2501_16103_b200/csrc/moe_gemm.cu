@@ -250,7 +250,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const __grid_constant__ CUtensorMap tmW2, const __grid_constant__ CUtensorMap tmY,
                     const GemmArgs a) {
   static_assert(!kSplit || kCta == 2, "swap-AB tail tiles need CTA pairs (M = 256)");
-  static_assert(!kWide || (kCta == 2 && !kSplit), "wide tiles are CTA-pair tiles");
+  static_assert(!kWide || kCta == 2, "wide tiles are CTA-pair tiles");
+  static_assert(!(kSplit && kGated), "swap-AB tail tiles are not gated");
   static_assert(!kGated || kWide, "gated tiles use the wide tile's two accumulator blocks");
   constexpr int kSt = Geo<kCta, kSplit, kWide>::kStages;
   constexpr int kBSt = Geo<kCta, kSplit, kWide>::kBStage;
@@ -555,11 +556,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                   wait_timed<kProf>(tempty_bar(1), acc_phase ^ 1u, c_tmem);
                   tc_fence_after();
                 }
+                if (kSplit && swap) {
+                  // swap-AB tail (kSplit kind 1): the W block is the M = 256 operand, tokens the N one
 #pragma unroll
-                for (int kk = 0; kk < kBK / 16; ++kk) {
-                  const uint64_t ad = smem_desc_sw128(a0 + kk * 32, 16, 1024);
-                  const uint64_t bd = smem_desc_sw128(b0 + hf * (kBSt / 2) + kk * 2048, kBBoxBytes, 1024);
-                  mma_bf16_pair(tmem_base + hf * kAccCols, ad, bd, idesc, (kb | kk) != 0);
+                  for (int kk = 0; kk < kBK / 16; ++kk) {
+                    const uint64_t tok = smem_desc_sw128(a0 + kk * 32, 16, 1024);
+                    const uint64_t wb = smem_desc_sw128(b0 + hf * (kBSt / 2) + kk * 2048, kBBoxBytes, 1024);
+                    mma_bf16_pair(tmem_base + hf * kAccCols, wb, tok, idesc, (kb | kk) != 0);
+                  }
+                } else {
+#pragma unroll
+                  for (int kk = 0; kk < kBK / 16; ++kk) {
+                    const uint64_t tok = smem_desc_sw128(a0 + kk * 32, 16, 1024);
+                    const uint64_t wb = smem_desc_sw128(b0 + hf * (kBSt / 2) + kk * 2048, kBBoxBytes, 1024);
+                    mma_bf16_pair(tmem_base + hf * kAccCols, tok, wb, idesc, (kb | kk) != 0);
+                  }
                 }
               }
             } else if (!kSplit || !swap) {
@@ -642,24 +653,45 @@ __global__ void __launch_bounds__(kThreads, 1)
       wait_timed<kProf>(tfull_bar(acc), acc_phase, c_wait);
       const long long w0 = kProf ? clock64() : 0;
       tc_fence_after();
+      if (kSplit && t.kind == 1 && a.tma_store) {
+        // The swap-AB transposes reuse the TMA-store staging buffers: every epilogue warp's earlier
+        // stores must have read their staging buffer first.
+        if (lane == 0) bulk_wait_group_read<0>();
+        named_bar_sync(1, 32 * kEpiWarps);
+      }
       if (kSplit && t.kind == 1 && cg > 0) {
         // Swap-AB tail tiles are drained by the first four epilogue warps alone.
+        if (a.tma_store) named_bar_sync(1, 32 * kEpiWarps);   // transposes done: staging reusable
         __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(leader(tempty_bar(acc)));
-        if (++acc == 2) {
+        if (lane == 0) {
+          if constexpr (kWide) {
+            mbar_arrive_cluster(leader(tempty_bar(0)));
+            mbar_arrive_cluster(leader(tempty_bar(1)));
+          } else {
+            mbar_arrive_cluster(leader(tempty_bar(acc)));
+          }
+        }
+        if constexpr (kWide) {
+          acc_phase ^= 1u;
+        } else if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1u;
         }
         continue;
       }
       if (kSplit && t.kind == 1) {
-        // Swap-AB tail: TMEM lane = output column, TMEM column = tail token.
-        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * kAccCols;
+        // Swap-AB tail: TMEM lane = output column, TMEM column = tail token.  Wide tiles: TMEM block
+        // hf holds W columns t.ct * 512 + 256 hf + [0, 256) (128 per CTA).
         // Transpose each 32 (columns) x 32 (tokens) block through this warp's smem buffer, then
         // write token rows with 16-byte stores (a warp covers 32 columns of 4 (fp32) / 8 (bf16) rows).
         uint8_t* buf = smem + (sEpi - base) + (warp - (kMmaWarp + 1)) * (32 * 32 * 4);
         const int esz = a.y_f32 ? 4 : 2;
-        const int col0 = t.ct * t.bn + (int)rank * (t.bn / kCta) + q * 32;   // this warp's 32 columns
+#pragma unroll 1
+        for (int hf = 0; hf < kHalves; ++hf) {
+        const int slot = kWide ? hf : acc;
+        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + slot * kAccCols;
+        const int bnb = t.bn / kHalves;               // columns of one TMEM block
+        const int col0 = t.ct * t.bn + hf * bnb + (int)rank * (bnb / kCta) + q * 32;   // this warp's 32 columns
         for (int c = 0; c < t.height; c += 32) {
           uint32_t r[32];
           tmem_ld32(taddr + c, r);
@@ -689,11 +721,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
-          if constexpr (kCta == 2) mbar_arrive_cluster(leader(tempty_bar(acc)));
-          else mbar_arrive(tempty_bar(acc));
+          if constexpr (kCta == 2) mbar_arrive_cluster(leader(tempty_bar(slot)));
+          else mbar_arrive(tempty_bar(slot));
         }
+        }
+        if (a.tma_store) named_bar_sync(1, 32 * kEpiWarps);   // transposes done: staging reusable
         if constexpr (kProf) c_work += clock64() - w0;
-        if (++acc == 2) {
+        if constexpr (kWide) {
+          acc_phase ^= 1u;
+        } else if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1u;
         }
@@ -704,7 +740,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int64_t yrow = a.y_row_map ? (int64_t)__ldg(a.y_row_map + t.row0 + min(grow, t.rows - 1))
                                        : (int64_t)t.row0 + grow;
       const int wrow0 = grow - lane;                // first task row of this warp's quarter
-      const bool tma_rows = !kSplit && a.tma_store && wrow0 + 32 <= t.rows;
+      const bool tma_rows = a.tma_store && wrow0 + 32 <= t.rows;
       const uint32_t xr = (uint32_t)((lane >> 1) & 3);
       // Write 32 fp32 results of this lane's row at columns [col, col + 32).  Full 32-row quarters:
       // bf16 into a 64B-swizzled 32 x 32 staging buffer (conflict-free 16-byte st.shared) and one TMA
@@ -972,11 +1008,12 @@ cudaError_t set_smem_attrs() {
   static std::once_flag once;
   static cudaError_t err = cudaSuccess;
   std::call_once(once, [] {
-    cudaError_t e[10] = {set_attr<false, 1, false>(),      set_attr<true, 1, false>(),
+    cudaError_t e[12] = {set_attr<false, 1, false>(),      set_attr<true, 1, false>(),
                         set_attr<false, 2, false>(),      set_attr<true, 2, false>(),
                         set_attr<false, 2, true>(),       set_attr<true, 2, true>(),
                         set_attr<false, 2, false, true>(), set_attr<true, 2, false, true>(),
-                        set_attr<false, 2, false, true, true>(), set_attr<true, 2, false, true, true>()};
+                        set_attr<false, 2, false, true, true>(), set_attr<true, 2, false, true, true>(),
+                        set_attr<false, 2, true, true>(), set_attr<true, 2, true, true>()};
     for (cudaError_t x : e)
       if (x != cudaSuccess && err == cudaSuccess) err = x;
   });
@@ -1090,8 +1127,10 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
   if (v.bm == 256) {
     const bool split = (v.flags & MOE_SPLIT_TAIL) != 0;
     const int pairs = v.total < 0 ? sm_count_cached() / 2 : std::min(v.total, sm_count_cached() / 2);
-    const size_t smem = (split ? Geo<2, true>::kSmem : wide || gated ? Geo<2, false, true>::kSmem
-                                                                 : Geo<2, false>::kSmem) +
+    const size_t smem = (split && wide   ? Geo<2, true, true>::kSmem
+                         : split         ? Geo<2, true>::kSmem
+                         : wide || gated ? Geo<2, false, true>::kSmem
+                                         : Geo<2, false>::kSmem) +
                         8 * (size_t)v.M_pad;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * pairs);
@@ -1111,6 +1150,9 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
     if (gated)
       le = prof ? cudaLaunchKernelEx(&cfg, moe_gemm_kernel<true, 2, false, true, true>, tmX, tmW, tmW2, tmY, a)
                 : cudaLaunchKernelEx(&cfg, moe_gemm_kernel<false, 2, false, true, true>, tmX, tmW, tmW2, tmY, a);
+    else if (wide && split)
+      le = prof ? cudaLaunchKernelEx(&cfg, moe_gemm_kernel<true, 2, true, true>, tmX, tmW, tmW2, tmY, a)
+                : cudaLaunchKernelEx(&cfg, moe_gemm_kernel<false, 2, true, true>, tmX, tmW, tmW2, tmY, a);
     else if (wide)
       le = prof ? cudaLaunchKernelEx(&cfg, moe_gemm_kernel<true, 2, false, true>, tmX, tmW, tmW2, tmY, a)
                 : cudaLaunchKernelEx(&cfg, moe_gemm_kernel<false, 2, false, true>, tmX, tmW, tmW2, tmY, a);

@@ -90,7 +90,7 @@ moe_status moe_plan_build(const int32_t* counts, int32_t E, int64_t H, int64_t N
     bm = bn == 512 || (r256 * 100 <= r128 * 110 && bn % 32 == 0) ? 256 : 128;
   }
   // Auto width: CTA-pair tiles go wide (256 x 512) whenever N has 512 columns.
-  if (auto_bn && bm == 256 && N >= 512 && !(flags & MOE_SPLIT_TAIL)) bn = 512;
+  if (auto_bn && bm == 256 && N >= 512) bn = 512;
   if (bm != 128 && bm != 256)
     MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_plan_build: bm=%d unsupported (128: one CTA, 256: CTA pair, 0: auto)", bm);
   // bm = 256, bn = 512: wide pair tile (two N = 256 MMA blocks sharing the staged token rows).
@@ -103,8 +103,9 @@ moe_status moe_plan_build(const int32_t* counts, int32_t E, int64_t H, int64_t N
   if ((flags & MOE_ORDER_ALTERNATING) && (flags & MOE_ORDER_HALF_INTERVAL))
     MOE_FAIL(MOE_ERR_INVALID, "moe_plan_build: choose one expert ordering");
   const bool split = (flags & MOE_SPLIT_TAIL) != 0;
-  if (split && (bm != 256 || bn != 256))
-    MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_plan_build: MOE_SPLIT_TAIL needs bm = bn = 256 (swap-AB tail tiles, M = 256)");
+  if (split && (bm != 256 || (bn != 256 && bn != 512)))
+    MOE_FAIL(MOE_ERR_UNSUPPORTED,
+             "moe_plan_build: MOE_SPLIT_TAIL needs bm = 256 and bn = 256 or 512 (swap-AB tail tiles, M = 256)");
   // CSR row offsets: exclusive prefix of counts in expert-id order.
   std::vector<int64_t> row_off(E + 1, 0);
   for (int32_t e = 0; e < E; ++e) {

@@ -243,7 +243,8 @@ RAGGED_WIDE = [                     # bm = 256, bn = 512: two N = 256 MMA blocks
                          [c + (128, "0", 0) for c in RAGGED] + [c + (128, "1", 0) for c in RAGGED]
                          + [c + (256, "1", 0) for c in RAGGED_PAIR]
                          + [c + (256, 256, "1", M.MOE_SPLIT_TAIL) for c in RAGGED_SPLIT]
-                         + [c + (512, 256, a, 0) for c in RAGGED_WIDE for a in ("0", "1")])
+                         + [c + (512, 256, a, 0) for c in RAGGED_WIDE for a in ("0", "1")]
+                         + [c + (512, 256, "1", M.MOE_SPLIT_TAIL) for c in RAGGED_SPLIT])
 @pytest.mark.parametrize("mode", ["int", "int_bf16", "normal"])
 def test_gemm_ragged(T, E, k, H, N, bn, bm, a_path, flags, mode, monkeypatch):
     monkeypatch.setenv("MOE_A_PATH", a_path)          # A staging path: gather4 (0) / cp.async (1)
@@ -301,6 +302,7 @@ def _sample_rows(row_off, counts, rng, per_expert=6):
 @pytest.mark.parametrize("cfg,bn,bm,flags", [("mix", 256, 128, 0), ("mix", 256, 256, 0), ("mix", 0, 0, 0),
                                              ("mix", 512, 256, 0), ("ds", 512, 256, 0), ("paper_balanced", 0, 0, 0),
                                              ("dec16", 512, 256, 0), ("paper_worst", 512, 256, 0),
+                                             ("mix", 512, 256, 2), ("ds", 512, 256, 2), ("paper_worst", 512, 256, 2),
                                              ("mix", 256, 256, 2), ("ds", 128, 128, 0), ("ds", 256, 256, 0),
                                              ("ds", 256, 256, 2), ("dec16", 256, 128, 0), ("dec16", 256, 0, 0),
                                              ("dec16", 256, 256, 2), ("paper_worst", 256, 256, 0),
@@ -345,6 +347,7 @@ def _device_plan_blob(counts, N, bm, bn, pad, H=64, split=0, order="natural"):
 @pytest.mark.parametrize("bm,bn,split,order", [(128, 256, 0, "natural"), (256, 256, 0, "natural"), (128, 48, 0, "natural"),
                                                (256, 96, 0, "natural"), (256, 256, 1, "natural"),
                                                (256, 512, 0, "natural"), (256, 512, 0, "half_interval"),
+                                               (256, 512, 1, "natural"),
                                                (128, 256, 0, "alternating"), (256, 256, 0, "half_interval")])
 def test_plan_device_bit_exact(pad, bm, bn, split, order):
     rng = np.random.default_rng(bm + bn)

@@ -109,7 +109,8 @@ def test_planner_split_tail_matches_oracle():
     for _ in range(200):
         E = rng.randint(1, 200)
         counts = np.array([0 if rng.random() < 0.3 else rng.randint(1, 3000) for _ in range(E)])
-        _compare(counts, 8 * rng.randint(1, 3000), 256, 256, rng.choice(["max", "repeat"]), split=True)
+        _compare(counts, 8 * rng.randint(1, 3000), 256, rng.choice([256, 512]), rng.choice(["max", "repeat"]),
+                 split=True)
     with pytest.raises(moe_lib.MoeError):
         moe_lib.moe_plan_build([5, 5], 64, 512, 256, 128, moe_lib.MOE_SPLIT_TAIL)   # needs bn = 256
 
@@ -147,12 +148,10 @@ def test_planner_wide_tiles_match_oracle():
         moe_lib.moe_plan_build([5, 5], 64, 1024, 128, 512)                 # wide tiles are pair tiles
     with pytest.raises(moe_lib.MoeError):
         moe_lib.moe_plan_build([5, 5], 64, 1024, 256, 384)
-    with pytest.raises(moe_lib.MoeError):
-        moe_lib.moe_plan_build([5, 5], 64, 1024, 256, 512, moe_lib.MOE_SPLIT_TAIL)   # split needs bn = 256
 
 
 def test_planner_auto_tile_width():
-    """bn = 0: 512 when bm resolves to 256, N >= 512 and no split tails; else 256 (header rule)."""
+    """bn = 0: 512 when bm resolves to 256 and N >= 512; else 256 (header rule)."""
     rng = random.Random(16)
     for _ in range(200):
         E = rng.randint(1, 64)
@@ -166,7 +165,7 @@ def test_planner_auto_tile_width():
         r256 = sum(-(-m // 256) * 256 for m in counts)
         bm_exp = bm or (256 if r256 * 100 <= r128 * 110 else 128)
         assert blob["bm"] == bm_exp
-        assert blob["bn"] == (512 if bm_exp == 256 and N >= 512 and not split else 256)
+        assert blob["bn"] == (512 if bm_exp == 256 and N >= 512 else 256)
     c = synth.CONFIGS["mix"]
     counts = np.bincount(synth.route(c).ravel(), minlength=c.E)
     b = moe_lib.parse_plan_blob(moe_lib.moe_plan_build(counts, c.H, c.N))
