@@ -166,6 +166,15 @@ __device__ __forceinline__ Tile load_tile(const int32_t* params, int task, int l
   return t;
 }
 
+// Wide tiles: the columns MMA block hf of column tile ct actually computes — all bn/2 of them,
+// except in a column tile passing N, where they are trimmed to the block's columns below N
+// rounded up to 128 (each CTA's half then stays on the 64-column W chunk grid); 0 = no MMA.
+__device__ __forceinline__ int wide_block_cols(int bn, int ct, int N, int hf) {
+  const int bnp = bn / 2;
+  const int nvalid = min(bn, N - ct * bn) - hf * bnp;
+  return nvalid <= 0 ? 0 : min(bnp, (nvalid + 127) & ~127);
+}
+
 __device__ __forceinline__ float tanh_approx(float x) {
   float y;
   asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -448,23 +457,38 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t dstB = sB + s * kBSt;
           if constexpr (kCta == 2) {
             const uint32_t fb = leader(full_bar(s));
+            // Per block: this CTA's first column and boxes.  Wide kind-0 tiles passing N stage only
+            // the trimmed block (wide_block_cols); the 4-D box always moves nbox chunks.
+            int nh[kHalves], nbx[kHalves];
+            uint32_t bytes = 0;
+#pragma unroll
+            for (int hf = 0; hf < kHalves; ++hf) {
+              nh[hf] = n0 + hf * bnp;
+              nbx[hf] = nbox;
+              if constexpr (kWide && !kGated) {
+                if (!(kSplit && t.kind == 1)) {
+                  const int nc = wide_block_cols(t.bn, t.ct, a.N, hf);
+                  nh[hf] = t.ct * t.bn + hf * bnp + (int)rank * (nc / 2);
+                  nbx[hf] = nc == 0 ? 0 : a.w4d ? nbox : (nc / 2 + 63) >> 6;
+                }
+              }
+              bytes += kCta * nbx[hf] * kBBoxBytes;
+            }
 #ifdef MOE_EXPERIMENTS
-            if (rank == 0)
-              mbar_arrive_expect_tx(full_bar(s), kHalves * kCta * nbox * kBBoxBytes +
-                                                     ((a.experiment & 4) ? kCta * kABytes : 0));
+            if (rank == 0) mbar_arrive_expect_tx(full_bar(s), bytes + ((a.experiment & 4) ? kCta * kABytes : 0));
 #else
-            if (rank == 0) mbar_arrive_expect_tx(full_bar(s), kHalves * kCta * nbox * kBBoxBytes);
+            if (rank == 0) mbar_arrive_expect_tx(full_bar(s), bytes);
 #endif
 #pragma unroll
             for (int hf = 0; hf < kHalves; ++hf) {
+              if (nbx[hf] == 0) continue;
               const uint32_t dst = dstB + hf * nbox * kBBoxBytes;
-              const int nh = n0 + hf * bnp;
               const CUtensorMap* wm = kGated && rank == 1 ? &tmW2 : &tmW;   // gated: leader gate, peer up
               if (a.w4d) {
-                tma_load_4d_pair(wm, fb, dst, 0, kb * kBK, nh >> 6, t.expert, pol_w);
+                tma_load_4d_pair(wm, fb, dst, 0, kb * kBK, nh[hf] >> 6, t.expert, pol_w);
               } else {
-                for (int j = 0; j < nbox; ++j)
-                  tma_load_3d_pair(wm, fb, dst + j * kBBoxBytes, nh + j * 64, kb * kBK, t.expert, pol_w);
+                for (int j = 0; j < nbx[hf]; ++j)
+                  tma_load_3d_pair(wm, fb, dst + j * kBBoxBytes, nh[hf] + j * 64, kb * kBK, t.expert, pol_w);
               }
             }
           } else {
@@ -508,6 +532,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t idesc = swap ? idesc_bf16_f32(kPairRows, t.height, /*A MN-major*/ 1, /*B K-major*/ 0)
                                     : idesc_bf16_f32(kPairRows, kGated ? 256 : t.bn / kHalves,
                                                      /*A K-major*/ 0, /*B MN-major*/ 1);
+        // Wide tiles past N (the last column tile when N is not a multiple of bn): each block's MMA
+        // covers wide_block_cols columns (zero: the block is skipped), matching what the B warp staged.
+        uint32_t idesc_blk[2] = {idesc, idesc};
+        int ncol_blk[2] = {1, 1};
+        if constexpr (kWide && !kGated) {
+          if (!swap) {
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+              ncol_blk[hf] = wide_block_cols(t.bn, t.ct, a.N, hf);
+              if (ncol_blk[hf] > 0) idesc_blk[hf] = idesc_bf16_f32(kPairRows, ncol_blk[hf], 0, 1);
+            }
+          }
+        }
         // Double-buffered: wait for accumulator `acc`.  Wide: accumulator half 0 now, half 1 just
         // before the first half-1 MMA (the epilogue drains the halves in order).
         wait_timed<kProf>(tempty_bar(acc), acc_phase ^ 1u, c_tmem);     // epilogue(s) drained this accumulator
@@ -564,12 +601,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint64_t wb = smem_desc_sw128(b0 + hf * (kBSt / 2) + kk * 2048, kBBoxBytes, 1024);
                     mma_bf16_pair(tmem_base + hf * kAccCols, wb, tok, idesc, (kb | kk) != 0);
                   }
-                } else {
+                } else if (ncol_blk[hf] > 0) {
 #pragma unroll
                   for (int kk = 0; kk < kBK / 16; ++kk) {
                     const uint64_t tok = smem_desc_sw128(a0 + kk * 32, 16, 1024);
                     const uint64_t wb = smem_desc_sw128(b0 + hf * (kBSt / 2) + kk * 2048, kBBoxBytes, 1024);
-                    mma_bf16_pair(tmem_base + hf * kAccCols, tok, wb, idesc, (kb | kk) != 0);
+                    mma_bf16_pair(tmem_base + hf * kAccCols, tok, wb, idesc_blk[hf], (kb | kk) != 0);
                   }
                 }
               }
@@ -692,6 +729,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + slot * kAccCols;
         const int bnb = t.bn / kHalves;               // columns of one TMEM block
         const int col0 = t.ct * t.bn + hf * bnb + (int)rank * (bnb / kCta) + q * 32;   // this warp's 32 columns
+        // TMEM lanes past this CTA's bnb / 2 columns (a box rounds up to 64) belong to the peer / next block
+        const int col_lim = min(t.ct * t.bn + hf * bnb + ((int)rank + 1) * (bnb / kCta), a.N);
         for (int c = 0; c < t.height; c += 32) {
           uint32_t r[32];
           tmem_ld32(taddr + c, r);
@@ -710,7 +749,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int j = j0 + lane / vec_per_row, piece = lane % vec_per_row;
             const int tok = c + j;
             const int col = col0 + piece * (16 / esz);
-            if (tok < t.rows && col < a.N) {
+            if (tok < t.rows && col < col_lim) {
               const int64_t yr = a.y_row_map ? (int64_t)__ldg(a.y_row_map + t.row0 + tok) : (int64_t)t.row0 + tok;
               const uint4 val = *reinterpret_cast<const uint4*>(buf + j * 32 * esz + piece * 16);
               *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(a.Y) + (yr * a.N + col) * esz) = val;
@@ -751,7 +790,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifdef MOE_EXPERIMENTS
         if (a.experiment & 8) return;
 #endif
-        if (tma_rows) {
+        if (tma_rows && col + 32 <= col_end) {        // a box never crosses the block / N
           const uint32_t buf = kEpiWarps == 4 ? ebuf + (n_chunk & 1u) * 2048u : ebuf;
           if (lane == 0) {                                  // the store that last used buf has read it
             if constexpr (kEpiWarps == 4) bulk_wait_group_read<1>();
@@ -1062,14 +1101,16 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
 #endif
   moe_status st = make_x_map(&tmX, X, T, v.H, (experiment & 4) ? kBM : 1);
   if (st != MOE_OK) return st;
-  const bool w4d = (v.N % 64) == 0;
   const bool gated = W2 != nullptr;                // moe_gemm_swiglu: W_gate / W_up blocks
   if (gated && !(v.bm == 256 && v.bn == 256))
     MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_gemm_swiglu: the plan must have bm = 256, bn = 256 (got %d x %d)", v.bm, v.bn);
   if (gated && !aligned16(W2)) MOE_FAIL(MOE_ERR_INVALID, "moe_gemm_swiglu: W_up must be 16-byte aligned");
-  const bool wide = v.bm == 256 && v.bn == 512;   // wide pair tile: two N = 256 MMA blocks
+  const bool wide = v.bm == 256 && v.bn > 256;    // wide pair tile: two N = bn/2 MMA blocks
   const int cta = v.bm / kBM;                      // CTAs per tile: each stages bn / cta W columns
-  st = make_w_map(&tmW, W, v.E, v.H, v.N, v.bn / cta / (wide ? 2 : 1), w4d);   // per MMA block
+  const int bnc_blk = v.bn / cta / (wide ? 2 : 1); // W columns one CTA stages per MMA block
+  // 4-D W view (one TMA per block): needs every CTA's block start on a 64-column chunk.
+  const bool w4d = (v.N % 64) == 0 && bnc_blk % 64 == 0;
+  st = make_w_map(&tmW, W, v.E, v.H, v.N, bnc_blk, w4d);
   if (st != MOE_OK) return st;
   CUtensorMap tmW2 = tmW;
   if (gated) {

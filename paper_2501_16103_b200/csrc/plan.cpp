@@ -87,25 +87,28 @@ moe_status moe_plan_build(const int32_t* counts, int32_t E, int64_t H, int64_t N
       r128 += ceil_div(m, 128) * 128;
       r256 += ceil_div(m, 256) * 256;
     }
-    bm = bn == 512 || (r256 * 100 <= r128 * 110 && bn % 32 == 0) ? 256 : 128;
+    bm = bn > 256 || (r256 * 100 <= r128 * 110 && bn % 32 == 0) ? 256 : 128;
   }
   // Auto width: CTA-pair tiles go wide (256 x 512) whenever N has 512 columns.
+  // (A last column tile past N trims its MMAs to the valid columns; narrower wide tiles such as
+  // 3 x 480 for N = 1408 measured slower — their W boxes start off the 64-column chunk grid.)
   if (auto_bn && bm == 256 && N >= 512) bn = 512;
   if (bm != 128 && bm != 256)
     MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_plan_build: bm=%d unsupported (128: one CTA, 256: CTA pair, 0: auto)", bm);
-  // bm = 256, bn = 512: wide pair tile (two N = 256 MMA blocks sharing the staged token rows).
-  const bool cluster_tile = bm == 256 && bn == 512;
-  if (!cluster_tile && (bn < 16 || bn > 256 || bn % (bm == 256 ? 32 : 16)))
-    MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_plan_build: bn=%d must be a multiple of %d in [16, 256] (or 512 with bm=256)",
-             bn, bm == 256 ? 32 : 16);
+  // bm = 256, 256 < bn <= 512: wide pair tile (two N = bn/2 MMA blocks sharing the staged token rows).
+  const bool wide_tile = bm == 256 && bn > 256 && bn <= 512 && bn % 32 == 0;
+  if (!wide_tile && (bn < 16 || bn > 256 || bn % (bm == 256 ? 32 : 16)))
+    MOE_FAIL(MOE_ERR_UNSUPPORTED,
+             "moe_plan_build: bn=%d must be a multiple of %d in [16, 256] (or of 32 in (256, 512] with bm=256)", bn,
+             bm == 256 ? 32 : 16);
   if (flags & ~(MOE_PAD_REPEAT | MOE_SPLIT_TAIL | MOE_ORDER_ALTERNATING | MOE_ORDER_HALF_INTERVAL))
     MOE_FAIL(MOE_ERR_INVALID, "moe_plan_build: unknown flags 0x%x", flags);
   if ((flags & MOE_ORDER_ALTERNATING) && (flags & MOE_ORDER_HALF_INTERVAL))
     MOE_FAIL(MOE_ERR_INVALID, "moe_plan_build: choose one expert ordering");
   const bool split = (flags & MOE_SPLIT_TAIL) != 0;
-  if (split && (bm != 256 || (bn != 256 && bn != 512)))
+  if (split && (bm != 256 || bn < 256))
     MOE_FAIL(MOE_ERR_UNSUPPORTED,
-             "moe_plan_build: MOE_SPLIT_TAIL needs bm = 256 and bn = 256 or 512 (swap-AB tail tiles, M = 256)");
+             "moe_plan_build: MOE_SPLIT_TAIL needs bm = 256 and bn = 256 or a wide tile (swap-AB tail tiles, M = 256)");
   // CSR row offsets: exclusive prefix of counts in expert-id order.
   std::vector<int64_t> row_off(E + 1, 0);
   for (int32_t e = 0; e < E; ++e) {

@@ -142,12 +142,14 @@ def test_planner_wide_tiles_match_oracle():
     for _ in range(200):
         E = rng.randint(1, 300)
         counts = np.array([0 if rng.random() < 0.3 else rng.randint(1, 3000) for _ in range(E)])
-        _compare(counts, 8 * rng.randint(1, 3000), 256, 512, rng.choice(["max", "repeat"]),
+        _compare(counts, 8 * rng.randint(1, 3000), 256, rng.choice([288, 384, 480, 512]), rng.choice(["max", "repeat"]),
                  order=rng.choice(["natural", "alternating", "half_interval"]))
     with pytest.raises(moe_lib.MoeError):
         moe_lib.moe_plan_build([5, 5], 64, 1024, 128, 512)                 # wide tiles are pair tiles
     with pytest.raises(moe_lib.MoeError):
-        moe_lib.moe_plan_build([5, 5], 64, 1024, 256, 384)
+        moe_lib.moe_plan_build([5, 5], 64, 1024, 256, 400)                 # block width 200: not a multiple of 16
+    with pytest.raises(moe_lib.MoeError):
+        moe_lib.moe_plan_build([5, 5], 64, 1024, 256, 544)
 
 
 def test_planner_auto_tile_width():
