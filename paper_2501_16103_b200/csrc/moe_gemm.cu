@@ -545,102 +545,174 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
-        // Double-buffered: wait for accumulator `acc`.  Wide: accumulator half 0 now, half 1 just
-        // before the first half-1 MMA (the epilogue drains the halves in order).
-        wait_timed<kProf>(tempty_bar(acc), acc_phase ^ 1u, c_tmem);     // epilogue(s) drained this accumulator
-        tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * kAccCols;
-        for (int kb = 0; kb < a.num_kb; ++kb, ++g) {
-          const int s = g % kSt;
-          const uint32_t par = (g / kSt) & 1u;
-          if constexpr (kProf) {
-            if (kb == 0 && n_tiles > 1) c_gap += clock64() - t_end;   // decode + accumulator hand-off
-          }
-          wait_timed<kProf>(full_bar(s), par, c_full);                   // both CTAs' bytes landed
-          long long t_i = 0;
-          if constexpr (kProf) {
-            const long long now = clock64();
-            c_lb += now - s_ts[s];
-            c_la += now - s_ts[kSt + s];
-            ++c_ns;
-            t_i = now;
-          }
-          tc_fence_after();
-          if (lane == 0) {
-            const uint32_t a0 = sA + s * kABytes;
-            const uint32_t b0 = sB + s * kBSt;
-            // Token rows: K-major SW128, 8-row groups 1024 B apart; K step of 16 = +32 B in the row.
-            // W block: MN-major SW128; 64-wide chunks 8 KB apart (LBO), 8-row K groups 1 KB apart
-            // (SBO); K step of 16 rows = +2 KB.  The two kinds only swap the operand roles.
-#ifdef MOE_EXPERIMENTS
-            if (a.experiment & 16) {   // B read as K-major (wrong Y): is the MN-major B operand slower?
-              const uint32_t idk = idesc_bf16_f32(kPairRows, kGated ? 256 : t.bn / kHalves, 0, 0);
+        if constexpr (kWide) {
+          // Wide tiles (TMEM holds one accumulator: block 0 = columns [0,256), block 1 = [256,512)).
+          // Block-staggered order so the epilogue drains one block while the other is still
+          // accumulating:
+          //   prologue  block 0 over K blocks [0, D)      (needs only block 0 of the last tile drained)
+          //             block 1 over [0, D), freeing each stage
+          //   middle    both blocks per K block, freeing each stage
+          //   tail      block 0 over [tail0, n), commit "block 0 full"; block 1 over [tail0, n), freeing,
+          //             commit "block 1 full"
+          // D = min(stages, n); the tail holds at most the whole ring.
+          const int n = a.num_kb;
+          const int D = min(kSt, n);
+          const int tail0 = max(D, n - D);
+          const uint32_t g0 = g;
+          auto slot = [&](int kb) { return (int)((g0 + kb) % kSt); };
+          auto wait_kb = [&](int kb) {
+            if constexpr (kProf) {
+              if (kb == 0 && n_tiles > 1) c_gap += clock64() - t_end;
+            }
+            wait_timed<kProf>(full_bar(slot(kb)), ((g0 + kb) / kSt) & 1u, c_full);
+            if constexpr (kProf) {
+              const long long now = clock64();
+              c_lb += now - s_ts[slot(kb)];
+              c_la += now - s_ts[kSt + slot(kb)];
+              ++c_ns;
+            }
+            tc_fence_after();
+          };
+          auto issue = [&](int hf, int kb) {
+            if (lane == 0) {
+              const uint32_t a0 = sA + slot(kb) * kABytes;
+              const uint32_t b0 = sB + slot(kb) * kBSt + hf * (kBSt / 2);
+              const uint32_t d = tmem_base + hf * kAccCols;
+              if (kSplit && swap) {
+                // swap-AB tail (kSplit kind 1): the W block is the M = 256 operand, tokens the N one
 #pragma unroll
-              for (int kk = 0; kk < kBK / 16; ++kk) {
-                const uint64_t ad = smem_desc_sw128(a0 + kk * 32, 16, 1024);
-                const uint64_t bd = smem_desc_sw128(b0 + kk * 32, 16, 1024);
-                if constexpr (kCta == 2) mma_bf16_pair(d_tmem, ad, bd, idk, (kb | kk) != 0);
-                else mma_bf16(d_tmem, ad, bd, idk, (kb | kk) != 0);
-              }
-            } else
-#endif
-            if constexpr (kWide) {
-              // Two N = 256 blocks per K block: W columns [0, 256) of the tile from the first half of
-              // the stage's B bytes into TMEM columns [0, 256), columns [256, 512) into [256, 512).
+                for (int kk = 0; kk < kBK / 16; ++kk)
+                  mma_bf16_pair(d, smem_desc_sw128(b0 + kk * 2048, kBBoxBytes, 1024),
+                                smem_desc_sw128(a0 + kk * 32, 16, 1024), idesc, (kb | kk) != 0);
+              } else if (ncol_blk[hf] > 0) {
 #pragma unroll
-              for (int hf = 0; hf < 2; ++hf) {
-                if (hf == 1 && kb == 0) {
-                  wait_timed<kProf>(tempty_bar(1), acc_phase ^ 1u, c_tmem);
-                  tc_fence_after();
-                }
-                if (kSplit && swap) {
-                  // swap-AB tail (kSplit kind 1): the W block is the M = 256 operand, tokens the N one
-#pragma unroll
-                  for (int kk = 0; kk < kBK / 16; ++kk) {
-                    const uint64_t tok = smem_desc_sw128(a0 + kk * 32, 16, 1024);
-                    const uint64_t wb = smem_desc_sw128(b0 + hf * (kBSt / 2) + kk * 2048, kBBoxBytes, 1024);
-                    mma_bf16_pair(tmem_base + hf * kAccCols, wb, tok, idesc, (kb | kk) != 0);
-                  }
-                } else if (ncol_blk[hf] > 0) {
-#pragma unroll
-                  for (int kk = 0; kk < kBK / 16; ++kk) {
-                    const uint64_t tok = smem_desc_sw128(a0 + kk * 32, 16, 1024);
-                    const uint64_t wb = smem_desc_sw128(b0 + hf * (kBSt / 2) + kk * 2048, kBBoxBytes, 1024);
-                    mma_bf16_pair(tmem_base + hf * kAccCols, tok, wb, idesc_blk[hf], (kb | kk) != 0);
-                  }
-                }
-              }
-            } else if (!kSplit || !swap) {
-#pragma unroll
-              for (int kk = 0; kk < kBK / 16; ++kk) {
-                const uint64_t ad = smem_desc_sw128(a0 + kk * 32, 16, 1024);
-                const uint64_t bd = smem_desc_sw128(b0 + kk * 2048, kBBoxBytes, 1024);
-                if constexpr (kCta == 2) mma_bf16_pair(d_tmem, ad, bd, idesc, (kb | kk) != 0);
-                else mma_bf16(d_tmem, ad, bd, idesc, (kb | kk) != 0);
-              }
-            } else {
-#pragma unroll
-              for (int kk = 0; kk < kBK / 16; ++kk) {
-                const uint64_t ad = smem_desc_sw128(b0 + kk * 2048, kBBoxBytes, 1024);
-                const uint64_t bd = smem_desc_sw128(a0 + kk * 32, 16, 1024);
-                if constexpr (kCta == 2) mma_bf16_pair(d_tmem, ad, bd, idesc, (kb | kk) != 0);
-                else mma_bf16(d_tmem, ad, bd, idesc, (kb | kk) != 0);
+                for (int kk = 0; kk < kBK / 16; ++kk)
+                  mma_bf16_pair(d, smem_desc_sw128(a0 + kk * 32, 16, 1024),
+                                smem_desc_sw128(b0 + kk * 2048, kBBoxBytes, 1024), idesc_blk[hf], (kb | kk) != 0);
               }
             }
-            if constexpr (kProf) s_ts[2 * kSt + s] = clock64();
-            if constexpr (kCta == 2) mma_commit_pair(empty_bar(s), 0x3);  // frees the slot in both CTAs
-            else mma_commit(empty_bar(s));
+            __syncwarp();
+          };
+          auto release = [&](int kb) {
+            if constexpr (kProf) {
+              if (lane == 0) s_ts[2 * kSt + slot(kb)] = clock64();
+            }
+            if (lane == 0) mma_commit_pair(empty_bar(slot(kb)), 0x3);   // frees the slot in both CTAs
+            __syncwarp();
+          };
+          auto block_full = [&](int hf) {
+            if (lane == 0) mma_commit_pair(tfull_bar(hf), 0x3);          // block hf final in both CTAs
+            __syncwarp();
+          };
+          const long long t_i = kProf ? clock64() : 0;
+          wait_timed<kProf>(tempty_bar(0), acc_phase ^ 1u, c_tmem);    // block 0 of the last tile drained
+          tc_fence_after();
+          for (int kb = 0; kb < D; ++kb) {
+            wait_kb(kb);
+            issue(0, kb);
+          }
+          if (n == D) block_full(0);
+          wait_timed<kProf>(tempty_bar(1), acc_phase ^ 1u, c_tmem);
+          tc_fence_after();
+          for (int kb = 0; kb < D; ++kb) {
+            issue(1, kb);
+            release(kb);
+          }
+          if (n == D) block_full(1);
+          for (int kb = D; kb < tail0; ++kb) {
+            wait_kb(kb);
+            issue(0, kb);
+            issue(1, kb);
+            release(kb);
+          }
+          if (tail0 < n) {
+            for (int kb = tail0; kb < n; ++kb) {
+              wait_kb(kb);
+              issue(0, kb);
+            }
+            block_full(0);
+            for (int kb = tail0; kb < n; ++kb) {
+              issue(1, kb);
+              release(kb);
+            }
+            block_full(1);
+          }
+          g += n;
+          if constexpr (kProf) {
+            c_issue += clock64() - t_i;
+            t_end = clock64();
+          }
+        } else {
+          // Double-buffered: wait for accumulator `acc`.
+          wait_timed<kProf>(tempty_bar(acc), acc_phase ^ 1u, c_tmem);     // epilogue(s) drained this accumulator
+          tc_fence_after();
+          const uint32_t d_tmem = tmem_base + acc * kAccCols;
+          for (int kb = 0; kb < a.num_kb; ++kb, ++g) {
+            const int s = g % kSt;
+            const uint32_t par = (g / kSt) & 1u;
+            if constexpr (kProf) {
+              if (kb == 0 && n_tiles > 1) c_gap += clock64() - t_end;   // decode + accumulator hand-off
+            }
+            wait_timed<kProf>(full_bar(s), par, c_full);                   // both CTAs' bytes landed
+            long long t_i = 0;
+            if constexpr (kProf) {
+              const long long now = clock64();
+              c_lb += now - s_ts[s];
+              c_la += now - s_ts[kSt + s];
+              ++c_ns;
+              t_i = now;
+            }
+            tc_fence_after();
+            if (lane == 0) {
+              const uint32_t a0 = sA + s * kABytes;
+              const uint32_t b0 = sB + s * kBSt;
+              // Token rows: K-major SW128, 8-row groups 1024 B apart; K step of 16 = +32 B in the row.
+              // W block: MN-major SW128; 64-wide chunks 8 KB apart (LBO), 8-row K groups 1 KB apart
+              // (SBO); K step of 16 rows = +2 KB.  The two kinds only swap the operand roles.
+#ifdef MOE_EXPERIMENTS
+              if (a.experiment & 16) {   // B read as K-major (wrong Y): is the MN-major B operand slower?
+                const uint32_t idk = idesc_bf16_f32(kPairRows, kGated ? 256 : t.bn / kHalves, 0, 0);
+#pragma unroll
+                for (int kk = 0; kk < kBK / 16; ++kk) {
+                  const uint64_t ad = smem_desc_sw128(a0 + kk * 32, 16, 1024);
+                  const uint64_t bd = smem_desc_sw128(b0 + kk * 32, 16, 1024);
+                  if constexpr (kCta == 2) mma_bf16_pair(d_tmem, ad, bd, idk, (kb | kk) != 0);
+                  else mma_bf16(d_tmem, ad, bd, idk, (kb | kk) != 0);
+                }
+              } else
+#endif
+              if (!kSplit || !swap) {
+#pragma unroll
+                for (int kk = 0; kk < kBK / 16; ++kk) {
+                  const uint64_t ad = smem_desc_sw128(a0 + kk * 32, 16, 1024);
+                  const uint64_t bd = smem_desc_sw128(b0 + kk * 2048, kBBoxBytes, 1024);
+                  if constexpr (kCta == 2) mma_bf16_pair(d_tmem, ad, bd, idesc, (kb | kk) != 0);
+                  else mma_bf16(d_tmem, ad, bd, idesc, (kb | kk) != 0);
+                }
+              } else {
+#pragma unroll
+                for (int kk = 0; kk < kBK / 16; ++kk) {
+                  const uint64_t ad = smem_desc_sw128(b0 + kk * 2048, kBBoxBytes, 1024);
+                  const uint64_t bd = smem_desc_sw128(a0 + kk * 32, 16, 1024);
+                  if constexpr (kCta == 2) mma_bf16_pair(d_tmem, ad, bd, idesc, (kb | kk) != 0);
+                  else mma_bf16(d_tmem, ad, bd, idesc, (kb | kk) != 0);
+                }
+              }
+              if constexpr (kProf) s_ts[2 * kSt + s] = clock64();
+              if constexpr (kCta == 2) mma_commit_pair(empty_bar(s), 0x3);  // frees the slot in both CTAs
+              else mma_commit(empty_bar(s));
+            }
+            __syncwarp();
+            if constexpr (kProf) c_issue += clock64() - t_i;
+          }
+          if constexpr (kProf) t_end = clock64();
+          if (lane == 0) {
+            if constexpr (kCta == 2)   // accumulator ready in both CTAs of this pair
+              mma_commit_pair(tfull_bar(acc), 0x3);
+            else mma_commit(tfull_bar(acc));
           }
           __syncwarp();
-          if constexpr (kProf) c_issue += clock64() - t_i;
         }
-        if constexpr (kProf) t_end = clock64();
-        if (lane == 0) {
-          if constexpr (kCta == 2)   // accumulator ready in both CTAs of this pair
-            mma_commit_pair(tfull_bar(acc), 0x3);
-          else mma_commit(tfull_bar(acc));
-        }
-        __syncwarp();
         if constexpr (kWide) {
           acc_phase ^= 1u;                        // one (two-half) accumulator per tile
         } else if (++acc == 2) {
@@ -683,6 +755,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t n_chunk = 0;                                     // TMA-store chunks issued by this warp
     const uint32_t ebuf = sEpi + (uint32_t)ew * (16384u / kEpiWarps);
     long long c_wait = 0, c_work = 0;
+    // Wide tiles: "block 0 full" is awaited with the tile, "block 1 full" before draining block 1.
+    auto wait_block1 = [&](int hf) {
+      if (kWide && hf == 1) {
+        wait_timed<kProf>(tfull_bar(1), acc_phase, c_wait);
+        tc_fence_after();
+      }
+    };
     for (int v = pair_id; v < total; v += n_pairs) {
       int h, task, l;
       map_tile(s_prefix, s_sigma, a.M_pad, v, h, task, l);
@@ -725,6 +804,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int esz = a.y_f32 ? 4 : 2;
 #pragma unroll 1
         for (int hf = 0; hf < kHalves; ++hf) {
+        wait_block1(hf);
         const int slot = kWide ? hf : acc;
         const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + slot * kAccCols;
         const int bnb = t.bn / kHalves;               // columns of one TMEM block
@@ -817,6 +897,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // Block b: gate in TMEM columns [0,128), up in [128,256) of outputs n0 + 128b + [0,128).
 #pragma unroll 1
         for (int hf = 0; hf < 2; ++hf) {
+          wait_block1(hf);
           const int n0 = t.ct * t.bn + hf * 128;
           const int col_end = min(n0 + 128, a.N);
           const uint32_t ta = tmem_base + ((uint32_t)(q * 32) << 16) + hf * kAccCols;
@@ -842,6 +923,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int bnp = t.bn / kHalves;             // columns of one accumulator block
 #pragma unroll 1
         for (int hf = 0; hf < kHalves; ++hf) {
+          wait_block1(hf);
           const int n0 = t.ct * t.bn + hf * bnp;
           const int col_end = min(n0 + bnp, a.N);
           const int slot = kWide ? hf : acc;        // TMEM block and its tmem-empty barrier
