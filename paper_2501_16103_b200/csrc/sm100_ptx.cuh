@@ -157,17 +157,6 @@ __device__ __forceinline__ void tma_gather4(const void* tmap, uint32_t bar, uint
       "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "l"(policy)
       : "memory");
 }
-// gather4 multicast: the four rows land at the same offset in every CTA of ctaMask, each
-// destination's mbarrier (same offset) receiving the complete_tx.
-__device__ __forceinline__ void tma_gather4_mc(const void* tmap, uint32_t bar, uint32_t dst, int32_t c0, int32_t r0,
-                                               int32_t r1, int32_t r2, int32_t r3, uint16_t mask, uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes.multicast::cluster"
-      ".L2::cache_hint [%0], [%1, {%3, %4, %5, %6, %7}], [%2], %8, %9;" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "h"(mask),
-      "l"(policy)
-      : "memory");
-}
 __device__ __forceinline__ uint64_t policy_evict_last() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
