@@ -237,7 +237,7 @@ def run_ffn(args, cfg):
         ev[1].record(stream)
         h = M.moe_gemm_swiglu(layer.plan_gu, Xd, tok, Wg, Wu)
         ev[2].record(stream)
-        y = M.moe_gemm(layer.plan_dn, h, layer._rows[: cfg.T * cfg.k], Wdn)
+        y = M.moe_gemm(layer.plan_dn, h, None, Wdn)
         ev[3].record(stream)
         M.moe_combine(y, tok, slot, row_off, w_d, out=out)
         ev[4].record(stream)

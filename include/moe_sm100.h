@@ -201,12 +201,15 @@ moe_status moe_route_plan(const int32_t* topk_ids_dev, int64_t T, int32_t k, int
 
 /*
  * The hot path: Y[row0 + r, n] = sum_h X[token_idx[row0 + r], h] * W[e, h, n]
- * for every task of the plan, in ONE persistent kernel launch (sm_100a: TMA
- * gather4 of token rows, TMA tiles of W, tcgen05.mma with fp32 accumulation in
- * TMEM, warp-specialised pipeline).
+ * for every task of the plan, in ONE persistent kernel launch (sm_100a: token rows
+ * gathered by cp.async (or TMA gather4), TMA tiles of W, tcgen05.mma with fp32
+ * accumulation in TMEM, warp-specialised pipeline).
  *   X_dev         [T, H] bf16 row-major (token activations), 16-byte aligned.
  *   token_idx_dev [sum m_e] int32, the CSR of moe_route, consistent with the
- *                 plan's counts (not re-checked on device).
+ *                 plan's counts (not re-checked on device).  NULL: the rows of X are
+ *                 already in the plan's CSR order (X row i = CSR row i, T >= sum m_e;
+ *                 e.g. the intermediate activations of the FFN layer) and are staged
+ *                 with one 128-row tile TMA per stage instead of a gather.
  *   W_dev         [E, H, N] bf16 row-major (expert weights), 16-byte aligned.
  *   Y_dev         [sum m_e, N] of y_dtype (MOE_DTYPE_BF16: fp32 accumulate, RNE
  *                 to bf16; MOE_DTYPE_F32: the fp32 accumulator), 16-byte aligned.

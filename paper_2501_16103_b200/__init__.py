@@ -263,23 +263,26 @@ def moe_route(topk_ids, E: int, with_slot: bool = True, stream=None, plan: "Plan
 
 
 def moe_gemm(plan: Plan, X, token_idx, W, Y=None, out_dtype=None, stream=None, row_map=None):
-    """Y[sum m_e, N] = per-expert X[token_idx] @ W[e] in one launch (row_map: Y row of CSR row i)."""
+    """Y[sum m_e, N] = per-expert X[token_idx] @ W[e] in one launch (row_map: Y row of CSR row i).
+    token_idx None: X's rows are already in CSR order (X row i = CSR row i)."""
     import torch
 
     out_dtype = out_dtype or torch.bfloat16
     assert X.is_cuda and X.dtype == torch.bfloat16 and X.is_contiguous()
     assert W.is_cuda and W.dtype == torch.bfloat16 and W.is_contiguous()
-    assert token_idx.dtype == torch.int32 and token_idx.is_contiguous()
-    rows = int(token_idx.numel())
+    if token_idx is not None:
+        assert token_idx.dtype == torch.int32 and token_idx.is_contiguous()
+    rows = int(token_idx.numel()) if token_idx is not None else int(X.shape[0])
+    tp = token_idx.data_ptr() if token_idx is not None else None
     if Y is None:
         Y = torch.empty((rows, plan.N), dtype=out_dtype, device=X.device)
     yd = MOE_DTYPE_F32 if Y.dtype == torch.float32 else MOE_DTYPE_BF16
     if row_map is None:
-        _check(lib().moe_gemm(plan.handle, X.data_ptr(), X.shape[0], token_idx.data_ptr(), W.data_ptr(),
+        _check(lib().moe_gemm(plan.handle, X.data_ptr(), X.shape[0], tp, W.data_ptr(),
                               Y.data_ptr(), yd, _stream(stream)))
     else:
         assert row_map.dtype == torch.int32 and row_map.is_contiguous()
-        _check(lib().moe_gemm_rowmap(plan.handle, X.data_ptr(), X.shape[0], token_idx.data_ptr(), W.data_ptr(),
+        _check(lib().moe_gemm_rowmap(plan.handle, X.data_ptr(), X.shape[0], tp, W.data_ptr(),
                                      Y.data_ptr(), yd, row_map.data_ptr(), _stream(stream)))
     return Y
 
@@ -335,7 +338,6 @@ class MoeFFN:
         self.Wg, self.Wu, self.Wd = W_gate, W_up, W_down
         self.plan_gu = Plan(None, self.H, self.I, 256, 256, stream=stream, E=self.E)
         self.plan_dn = None
-        self._rows = None
         self._torch = torch
 
     def forward(self, X, topk_ids, topk_w, out=None, out_dtype=None, stream=None):
@@ -345,12 +347,10 @@ class MoeFFN:
         if self.plan_dn is None:
             bm, bn = suggest_tile(R, self.E, self.I, self.Ho)
             self.plan_dn = Plan(None, self.I, self.Ho, bm, bn, stream=stream, E=self.E)
-        if self._rows is None or self._rows.numel() < R:
-            self._rows = torch.arange(R, dtype=torch.int32, device=X.device)
         counts, row_off, tok, slot, _ = moe_route(topk_ids, self.E, stream=stream, plan=self.plan_gu)
         self.plan_dn.update_device(counts, stream=stream)
         Hmid = moe_gemm_swiglu(self.plan_gu, X, tok, self.Wg, self.Wu, stream=stream)
-        Y = moe_gemm(self.plan_dn, Hmid, self._rows[:R], self.Wd, stream=stream)
+        Y = moe_gemm(self.plan_dn, Hmid, None, self.Wd, stream=stream)     # rows already in CSR order
         out = moe_combine(Y, tok, slot, row_off, topk_w, out=out, out_dtype=out_dtype, stream=stream)
         self.last = dict(counts=counts, row_off=row_off, token_idx=tok, slot=slot, h=Hmid, y=Y)
         return out

@@ -83,7 +83,8 @@ struct GemmArgs {
   int32_t T;
   int32_t w4d;               // W map is 4-D {64, H, N/64, E}: one TMA per B stage
   long long* prof;           // kProf builds only: per-CTA cycle counters (moe_gemm_profile)
-  int32_t a_mode;            // A staging: 0 = TMA tile::gather4, 1 = cp.async (LSU path), see DESIGN.md
+  int32_t a_mode;            // A staging: 0 = TMA tile::gather4, 1 = cp.async (LSU path), 2 = contiguous
+                             // rows (token_idx NULL: X row = CSR row) by one tile TMA per stage; DESIGN.md
   int32_t H;
   const __nv_bfloat16* X;
   int32_t experiment;        // MOE_EXPERIMENTS builds only (timing studies, wrong Y), bit mask: 1 = no A reads,
@@ -294,14 +295,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int n_pairs = gridDim.x / kCta;
   auto leader = [&](uint32_t addr) { return kCta == 2 ? mapa_shared(addr, 0) : addr; };
 
-  const int a_mode = kCta == 2 && !kWide ? 1 : a.a_mode;
+  const int a_mode = a.a_mode == 2 ? 2 : kCta == 2 && !kWide ? 1 : a.a_mode;
   if (threadIdx.x == 0) {
     // full[s] arrivals: A stage done (gather4: one expect_tx per A warp; cp.async: one asynchronous
-    // arrive per A thread), the B warp's expect_tx (leader), and in a pair the peer's relay (leader).
-    const uint32_t a_arrivals = a_mode == 0 ? kAWarps : 32 * kAWarps;
-    const uint32_t full_count = a_arrivals + (rank == 0 ? 1u + (kCta == 2 ? 1u : 0u) : 0u);
+    // arrive per A thread; contiguous rows: the 1-CTA A thread's expect_tx, while in a pair the
+    // A tile TMAs of both CTAs complete on the leader's barrier under the B warp's expect_tx), the
+    // B warp's expect_tx (leader), and in a pair the peer's relay (leader; not in a_mode 2).
+    const uint32_t a_arrivals = a_mode == 2 ? (kCta == 1 ? 1u : 0u) : a_mode == 0 ? kAWarps : 32 * kAWarps;
+    const uint32_t relay = kCta == 2 && a_mode != 2 ? 1u : 0u;
+    const uint32_t full_count = a_arrivals + (rank == 0 ? 1u + relay : 0u);
     for (int s = 0; s < kSt; ++s) {
-      mbar_init(full_bar(s), full_count);
+      mbar_init(full_bar(s), full_count > 0 ? full_count : 1u);   // a pair peer's are unused in a_mode 2
       mbar_init(empty_bar(s), 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -354,7 +358,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int rbeg = kSplit && t.kind == 1 ? (int)rank * n_alloc : t.rt * kPairRows + (int)rank * kBM;
       const int nvalid = min(n_alloc, t.rows - rbeg);   // may be <= 0 for the second CTA of a pair tile
       const int32_t* idx = a.token_idx + t.row0;
-      if (a_mode == 0) {
+      if (a_mode == 2) {
+        // Contiguous rows (X row = CSR row): one 128-row tile TMA per stage, issued by one thread.
+        // Rows past the task's end are the next task's (never stored); past X they are zero-filled.
+        if (p == 0 && lane == 0) {
+          for (int kb = 0; kb < a.num_kb; ++kb, ++g) {
+            const int s = g % kSt;
+            wait_timed<kProf>(empty_bar(s), ((g / kSt) & 1u) ^ 1u, c_wait);
+            if constexpr (kCta == 2) {
+              tma_load_2d_pair(&tmX, leader(full_bar(s)), sA + s * kABytes, kb * kBK, t.row0 + rbeg, pol_x);
+            } else {
+              mbar_arrive_expect_tx(full_bar(s), kABytes);
+              tma_load_2d(&tmX, full_bar(s), sA + s * kABytes, kb * kBK, t.row0 + rbeg, pol_x);
+            }
+          }
+        }
+        __syncwarp();
+      } else if (a_mode == 0) {
         // Rows past the task's end repeat its last valid token (their results are never stored).
         const int rr = 32 * p + 4 * (lane & 7);
         const int r0 = __ldg(idx + rbeg + min(rr + 0, nvalid - 1));
@@ -474,6 +494,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
               bytes += kCta * nbx[hf] * kBBoxBytes;
             }
+            if (a_mode == 2) bytes += kCta * kABytes;   // both CTAs' contiguous-row A tiles
 #ifdef MOE_EXPERIMENTS
             if (rank == 0) mbar_arrive_expect_tx(full_bar(s), bytes + ((a.experiment & 4) ? kCta * kABytes : 0));
 #else
@@ -734,7 +755,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           o[kProfMmaTileGap] = c_gap;
         }
       }
-    } else if (lane == 0) {
+    } else if (lane == 0 && a_mode != 2) {
       // Pair peer: relay "my A stage landed" (local full barrier, fed by cp.async arrivals) to the
       // leader's full barrier, where the MMA issuer waits for both CTAs' bytes.
       uint32_t g = 0;
@@ -1166,7 +1187,7 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
     if (!moe::blob_view(blob, words, &v)) MOE_FAIL(MOE_ERR_INVALID, "moe_gemm: corrupt plan");
     if (v.total == 0) return MOE_OK_EMPTY;
   }
-  if (!X || !token_idx || !W || !Y) MOE_FAIL(MOE_ERR_INVALID, "moe_gemm: null tensor pointer");
+  if (!X || !W || !Y) MOE_FAIL(MOE_ERR_INVALID, "moe_gemm: null tensor pointer");
   if (!aligned16(X) || !aligned16(W) || !aligned16(Y))
     MOE_FAIL(MOE_ERR_INVALID, "moe_gemm: X, W and Y must be 16-byte aligned");
   if (T < 1 || T >= INT_MAX) MOE_FAIL(MOE_ERR_INVALID, "moe_gemm: T=%lld outside [1, 2^31)", (long long)T);
@@ -1181,7 +1202,8 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
     experiment = ex ? atoi(ex) : 0;
   }
 #endif
-  moe_status st = make_x_map(&tmX, X, T, v.H, (experiment & 4) ? kBM : 1);
+  // token_idx NULL: X rows are the plan's CSR rows (a_mode 2: 128-row tile boxes).
+  moe_status st = make_x_map(&tmX, X, T, v.H, (experiment & 4) || !token_idx ? kBM : 1);
   if (st != MOE_OK) return st;
   const bool gated = W2 != nullptr;                // moe_gemm_swiglu: W_gate / W_up blocks
   if (gated && !(v.bm == 256 && v.bn == 256))
@@ -1241,7 +1263,7 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
   a.experiment = experiment;
   {
     const char* am = getenv("MOE_A_PATH");       // timing studies: force the A staging path
-    a.a_mode = am ? atoi(am) : kDefaultAMode;
+    a.a_mode = !token_idx ? 2 : am && (atoi(am) == 0 || atoi(am) == 1) ? atoi(am) : kDefaultAMode;
   }
 
   if (v.bm == 256 && (v.bn / 2) % 16) MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_gemm: pair tiles need bn %% 32 == 0");

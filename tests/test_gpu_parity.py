@@ -528,3 +528,21 @@ def test_route_place_and_split_paths(T, k, E, skew):
     assert slot.cpu().numpy()[:n].tolist() == rs
     assert row_off.cpu().numpy().tolist() == np.concatenate([[0], np.cumsum([len(b) for b in lists])]).tolist()
     assert status.item() == (1 if k >= 2 else 0)
+
+
+@pytest.mark.parametrize("bm,bn,flags", [(128, 256, 0), (256, 256, 0), (256, 512, 0), (256, 512, M.MOE_SPLIT_TAIL),
+                                         (256, 256, M.MOE_SPLIT_TAIL)])
+@pytest.mark.parametrize("T,E,k,H,N", [(300, 5, 2, 200, 136), (700, 3, 2, 256, 1024), (1, 8, 2, 512, 640)])
+def test_gemm_contiguous_rows_token_idx_null(T, E, k, H, N, bm, bn, flags):
+    """token_idx NULL: X already in CSR row order (one tile TMA per stage) — the same Y, bit for
+    bit, as gathering the same rows through the token-index array; exact vs the oracle (integers)."""
+    ids, X, W, Xd, Wd = _inputs(T, E, k, H, N, T + N, "int")
+    counts, row_off, tok, _, _ = M.moe_route(torch.from_numpy(ids).cuda(), E)
+    plan = M.Plan(counts.cpu().numpy(), H, N, bm, bn, flags)
+    Xc = Xd.index_select(0, tok.long()).contiguous()            # rows in CSR order
+    Yc = M.moe_gemm(plan, Xc, None, Wd, out_dtype=torch.float32)
+    Yg = M.moe_gemm(plan, Xd, tok, Wd, out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    assert torch.equal(Yc, Yg)
+    rc, rr, rt, rs = omoe.buckets(ids, E)
+    assert np.array_equal(Yc.cpu().double().numpy(), omoe.expert_gemm(X, W, rt, rr))
