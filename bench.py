@@ -457,9 +457,58 @@ def run_ours(args, cfg):
         if args.host_plan:
             h2d += 4 * plan.blob().size            # plan blob upload
             d2h += 4 * cfg.E                       # counts read back for the host planner
-        e2e = {"value": flops / (statistics.mean(e_ms) * 1e-3) / 1e12, "unit": "TFLOP/s",
+        serial_ms = statistics.mean(e_ms)
+        # Pipelined serving loop through the same public API: step i's H2D, step i-1's compute and
+        # step i-2's D2H overlap on three streams (inputs and outputs double-buffered); the timed
+        # region covers every step's copies.  The PCIe read-back of Y bounds it.
+        pipe_ms = None
+        if not args.host_plan:
+            s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+            Xb = [torch.empty_like(Xd) for _ in range(2)]
+            tb = [torch.empty_like(topk_d) for _ in range(2)]
+            Yb = [torch.empty_like(Ybuf) for _ in range(2)]
+            Yh = [Y_h, torch.empty(Y0.shape, dtype=Y0.dtype).pin_memory()]
+            ev_in = [torch.cuda.Event() for _ in range(2)]
+            ev_comp = [torch.cuda.Event() for _ in range(2)]
+            ev_out = [torch.cuda.Event() for _ in range(2)]
+            n_pipe = max(4, min(args.steps, 12))
+
+            def run_pipe(n):
+                for i in range(n):
+                    b = i % 2
+                    with torch.cuda.stream(s_in):
+                        if i >= 2:
+                            s_in.wait_event(ev_comp[b])          # step i-2 has consumed Xb[b], tb[b]
+                        Xb[b].copy_(X_h, non_blocking=True)
+                        tb[b].copy_(ids_h, non_blocking=True)
+                        ev_in[b].record(s_in)
+                    stream.wait_event(ev_in[b])
+                    if i >= 2:
+                        stream.wait_event(ev_out[b])             # step i-2's D2H has read Yb[b]
+                    M.moe_forward(tb[b], Xb[b], Wd, cfg.E, bm=args.bm, bn=args.bn, out_dtype=out_dtype, plan=plan,
+                                  Y=Yb[b])
+                    ev_comp[b].record(stream)
+                    with torch.cuda.stream(s_out):
+                        s_out.wait_event(ev_comp[b])
+                        Yh[b].copy_(Yb[b], non_blocking=True)
+                        ev_out[b].record(s_out)
+                stream.wait_stream(s_in)
+                stream.wait_stream(s_out)
+
+            run_pipe(2)
+            torch.cuda.synchronize()
+            p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            p0.record(stream)
+            s_in.wait_stream(stream)
+            run_pipe(n_pipe)
+            p1.record(stream)
+            p1.synchronize()
+            pipe_ms = p0.elapsed_time(p1) / n_pipe
+        e_best = pipe_ms if pipe_ms is not None else serial_ms
+        e2e = {"value": flops / (e_best * 1e-3) / 1e12, "unit": "TFLOP/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "ms_per_step": statistics.mean(e_ms)}
+               "ms_per_step": e_best, "mode": "pipelined: H2D / compute / D2H on three streams, double-buffered"
+               if pipe_ms is not None else "serial", "serial_ms_per_step": serial_ms}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
