@@ -546,3 +546,13 @@ def test_gemm_contiguous_rows_token_idx_null(T, E, k, H, N, bm, bn, flags):
     assert torch.equal(Yc, Yg)
     rc, rr, rt, rs = omoe.buckets(ids, E)
     assert np.array_equal(Yc.cpu().double().numpy(), omoe.expert_gemm(X, W, rt, rr))
+
+
+@pytest.mark.parametrize("bm,bn", [(128, 256), (256, 512)])
+def test_gemm_1024_experts(bm, bn):
+    """M_pad = 1024 (32 warp-vote chunks per decode), most experts with 0-3 rows."""
+    T, E, k, H, N = 1024, 1024, 4, 128, 256
+    ids, X, W, Xd, Wd = _inputs(T, E, k, H, N, 1234, "int")
+    Y, counts, row_off, tok, *_ = run_path(ids, Xd, Wd, E, bn=bn, bm=bm)
+    rc, rr, rt, rs = omoe.buckets(ids, E)
+    assert np.array_equal(Y.cpu().double().numpy(), omoe.expert_gemm(X, W, rt, rr))
