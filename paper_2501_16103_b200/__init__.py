@@ -150,11 +150,14 @@ def _stream(stream=None) -> int:
 
 
 def suggest_tile(rows: int, E: int, H: int, N: int) -> tuple[int, int]:
-    """Tile shape (bm, bn) the automatic rule picks for `rows` routed rows spread evenly over E
-    experts — for plans created before the counts exist (device-built plans): the
-    device planner keeps the shape chosen at creation."""
-    per = max(1, -(-int(rows) // max(1, int(E))))
-    b = parse_plan_blob(moe_plan_build(np.full(E, per, dtype=np.int32), H, N, 0, 0))
+    """Tile shape (bm, bn) the automatic rule picks for `rows` routed rows spread evenly over
+    min(E, rows) experts — for plans created before the counts exist (device-built plans,
+    P:142): the device planner keeps the shape chosen at creation."""
+    active = max(1, min(int(E), int(rows)))
+    per = max(1, -(-int(rows) // active))
+    counts = np.zeros(E, dtype=np.int32)
+    counts[:active] = per
+    b = parse_plan_blob(moe_plan_build(counts, H, N, 0, 0))
     return b["bm"], b["bn"]
 
 
