@@ -231,7 +231,10 @@ __device__ __forceinline__ void wait_timed(uint32_t bar, uint32_t parity, long l
 // kWide) stages 128 rows + 256 W columns per CTA: 48 KB, four stages.
 template <int kCta, bool kSplit = false, bool kWide = false>
 struct Geo {
-  static constexpr int kStages = kWide ? 4 : kCta == 2 ? 6 : 4;   // a 7th pair stage measured no gain (NOTES)
+#ifndef MOE_WIDE_STAGES
+#define MOE_WIDE_STAGES 4
+#endif
+  static constexpr int kStages = kWide ? MOE_WIDE_STAGES : kCta == 2 ? 6 : 4;   // a 7th pair stage: no gain (NOTES)
   static_assert(8 * (2 * kStages + 4) + 4 <= kBarBytes, "barrier block overlaps TilePrefix");
   static constexpr int kBStage = (kWide ? 2 : 1) * kBStageBytes / kCta;   // bytes of W per CTA per stage
   // 16 KB: a 2 KB bf16 staging buffer per epilogue warp for the TMA-store epilogue (two per warp
