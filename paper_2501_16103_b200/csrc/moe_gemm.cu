@@ -6,18 +6,20 @@
 //     mapping over TilePrefix (Alg. 2 + chunk loop) and sigma (Alg. 4
 //     line 289) — "let all warps execute the algorithm";
 //   * warps 0-3 (A producers) stage, per 64-wide K block, the tile's 128 token
-//     rows straight from X through the token-index array (no gathered
-//     copy): either with TMA tile::gather4 or with cp.async on the LSU path (the
-//     default: gather4 is issue-rate bound at ~17-21 B/clk/SM, below the 32 B/clk
-//     a 128x256 tile consumes; DESIGN.md §A staging);
-//   * warp 4 (B producer) stages the expert's W block with one 4-D TMA tile load;
-//     both feed a 4-stage SW128 shared-memory ring guarded by mbarriers
-//     (P:352-353's two-stage prefetch, deepened);
-//   * warp 5 issues tcgen05.mma (M=128, N=BN, K=16, bf16 x bf16 -> fp32) into a
-//     double-buffered TMEM accumulator (P:351's WGMMA, Blackwell-native);
-//   * warps 6-9 drain TMEM with tcgen05.ld, convert and store Y rows, masked to
-//     the task's rows and to N, overlapping the next tile's main loop.
-// Static batching: CTA b processes v = b, b + grid, b + 2*grid, ... (no
+//     rows per CTA straight from X through the token-index array (no
+//     gathered copy): cp.async on the LSU path by default, TMA tile::gather4 as an
+//     option, one tile TMA when the rows are already in CSR order (token_idx NULL);
+//   * warp 4 (B producer) stages the expert's W block with 4-D TMA tile loads;
+//     both feed an SW128 shared-memory ring guarded by mbarriers (4-6 stages;
+//     P:352-353's two-stage prefetch, deepened);
+//   * warp 5 issues tcgen05.mma (bf16 x bf16 -> fp32 in TMEM): 128 x BN tiles on one
+//     CTA, 256 x BN on a CTA pair (cta_group::2), and the default 256 x 512 wide pair
+//     tile with two N = 256 accumulator blocks, block-staggered (P:351's WGMMA,
+//     Blackwell-native);
+//   * warps 6-13 drain TMEM with tcgen05.ld (two warps per lane quarter), convert and
+//     store Y through TMA tile stores (or masked register stores for a task's last
+//     rows), overlapping the next tile's main loop.
+// Static batching: CTA (pair) b processes v = b, b + grid, b + 2*grid, ... (no
 // dynamic scheduler, no atomics).  Within a task, tiles are ordered row-tile
 // fastest (R5), so CTAs of one wave share W column blocks in L2
 // (the paper's "tile swizzle").
