@@ -236,7 +236,10 @@ struct Geo {
 #ifndef MOE_WIDE_STAGES
 #define MOE_WIDE_STAGES 4
 #endif
-  static constexpr int kStages = kWide ? MOE_WIDE_STAGES : kCta == 2 ? 6 : 4;   // a 7th pair stage: no gain (NOTES)
+#ifndef MOE_CTA1_STAGES
+#define MOE_CTA1_STAGES 4
+#endif
+  static constexpr int kStages = kWide ? MOE_WIDE_STAGES : kCta == 2 ? 6 : MOE_CTA1_STAGES;   // 7th pair stage: no gain
   static_assert(8 * (2 * kStages + 4) + 4 <= kBarBytes, "barrier block overlaps TilePrefix");
   static constexpr int kBStage = (kWide ? 2 : 1) * kBStageBytes / kCta;   // bytes of W per CTA per stage
   // 16 KB: a 2 KB bf16 staging buffer per epilogue warp for the TMA-store epilogue (two per warp
