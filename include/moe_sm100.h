@@ -100,7 +100,9 @@ int64_t moe_plan_blob_words(int32_t E);
  * Build the compressed mapping on the host.
  *   counts_host [E]  tokens routed to each expert (m_e >= 0), host memory.
  *   H, N             GEMM K and expert output width; both must be multiples of 8.
- *   bm, bn           tile shape.  bm = 128: one CTA per tile (tcgen05 M=128, cta_group::1);
+ *   bm, bn           tile shape.  bm = 64 (bn = 256): decode tile — one CTA, swap-AB (the
+ *                    W block as two M = 128 operands, <= 64 tokens as N), opt-in;
+ *                    bm = 128: one CTA per tile (tcgen05 M=128, cta_group::1);
  *                    bm = 256: a CTA pair per tile (tcgen05 M=256, cta_group::2, each
  *                    CTA 128 rows and half of the W block).  16 <= bn <= 256, bn % 16 == 0
  *                    (bn % 32 == 0 when bm = 256), or bn = 512 with bm = 256: a wide pair

@@ -996,6 +996,211 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Decode-regime tiles (bm = 64: every expert has <= 64 rows; SURVEY §8's skinny batches).
+// The GEMM is HBM-bound on W, so the tile is swap-AB on one CTA: the W block (256 columns,
+// two M = 128 blocks, MN-major) is the MMA's M operand and the tile's <= 64 token rows its N
+// operand (N = rows rounded up to 16).  A stage is 32 KB of W + 8 KB of tokens, so five stages
+// keep 160 KB of W in flight per SM (the 128 x 256 tile: 4 x 32 KB behind 16 KB token stages).
+// TMEM lane = output column, TMEM column = token: the epilogue stores each token row's 32
+// columns per warp with one coalesced 64 / 128-byte store, no transpose.  DESIGN.md §6.4.
+// ---------------------------------------------------------------------------
+constexpr int kDecRows = 64;                       // tokens per tile (the plan's bm)
+constexpr int kDecCols = 256;                      // W columns per tile (the plan's bn)
+constexpr int kDecSt = 5;
+constexpr int kDecTokBytes = kDecRows * kBK * 2;   // 8 KB
+constexpr int kDecWBytes = kDecCols * kBK * 2;     // 32 KB
+constexpr int kDecAccCols = 128;                   // per accumulator: 2 blocks x 64 token columns
+constexpr size_t kDecSmem = 1024 + (size_t)kDecSt * (kDecTokBytes + kDecWBytes) + kBarBytes;
+static_assert(8 * (2 * kDecSt + 4) + 4 <= 256, "decode barrier block overlaps its timestamps");
+
+__global__ void __launch_bounds__(kThreads, 1)
+    moe_gemm_decode_kernel(const __grid_constant__ CUtensorMap tmW, const GemmArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  uint8_t* smem = smem_raw + (base - raw);
+  const uint32_t sTok = base;
+  const uint32_t sW = sTok + kDecSt * kDecTokBytes;
+  const uint32_t sBar = sW + kDecSt * kDecWBytes;
+  auto full_bar = [&](int s) { return sBar + 8u * s; };
+  auto empty_bar = [&](int s) { return sBar + 8u * (kDecSt + s); };
+  auto tfull_bar = [&](int i) { return sBar + 8u * (2 * kDecSt + i); };
+  auto tempty_bar = [&](int i) { return sBar + 8u * (2 * kDecSt + 2 + i); };
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + (sBar - base) + 8 * (2 * kDecSt + 4));
+  int32_t* s_prefix = reinterpret_cast<int32_t*>(smem + (sBar - base) + kBarBytes);
+  int32_t* s_sigma = s_prefix + a.M_pad;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int total = a.total;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kDecSt; ++s) {
+      mbar_init(full_bar(s), 32 * kAWarps + 1);    // token copies (one arrive per A thread) + W bytes
+      mbar_init(empty_bar(s), 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(tfull_bar(i), 1);
+      mbar_init(tempty_bar(i), kEpiWarps);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) prefetch_tmap(&tmW);
+  if (warp == kMmaWarp) tmem_alloc<256, 1>(smem_u32(tmem_holder));
+  pdl_wait();
+  for (int i = threadIdx.x; i < 2 * a.M_pad; i += blockDim.x) s_prefix[i] = a.plan[MOE_PLAN_HEADER + i];
+  if (total < 0) total = __ldg(a.plan + 2);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+  const int32_t* params = a.plan + a.off_params;
+
+  if (warp < kAWarps) {
+    // ===== token rows: 64 per tile, cp.async 16 B per thread, 8 threads per 128-byte row =====
+    const int ch = threadIdx.x & 7, rsub = threadIdx.x >> 3;    // rsub in [0, 16)
+    const uint32_t dst_off = rsub * 128 + ((ch ^ (rsub & 7)) << 4);
+    uint32_t g = 0;
+    for (int v = blockIdx.x; v < total; v += gridDim.x) {
+      int h, task, l;
+      map_tile(s_prefix, s_sigma, a.M_pad, v, h, task, l);
+      const Tile t = load_tile(params, task, l);
+      const int rbeg = t.rt * kDecRows;
+      const int nvalid = min(kDecRows, t.rows - rbeg);
+      const __nv_bfloat16* src[4];
+      uint32_t rowok = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int r = rsub + 16 * j;
+        const int tok = r < nvalid ? (a.token_idx ? __ldg(a.token_idx + t.row0 + rbeg + r) : t.row0 + rbeg + r) : 0;
+        src[j] = a.X + (int64_t)tok * a.H + ch * 8;
+        rowok |= (r < nvalid ? 1u : 0u) << j;
+      }
+      for (int kb = 0; kb < a.num_kb; ++kb, ++g) {
+        const int s = g % kDecSt;
+        mbar_wait(empty_bar(s), ((g / kDecSt) & 1u) ^ 1u);
+        const int kcol = kb * kBK;
+        const bool colok = kcol + ch * 8 < a.H;
+        const uint32_t dst = sTok + s * kDecTokBytes + dst_off;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const bool ok = colok && ((rowok >> j) & 1u);
+          cp_async_16(dst + j * 16 * 128, ok ? src[j] + kcol : a.X, ok ? 16u : 0u);
+        }
+        cp_async_mbar_arrive_noinc(full_bar(s));
+      }
+    }
+  } else if (warp == kBWarp) {
+    // ===== the W block: 256 columns x 64 K per stage, one 4-D TMA (or 4 3-D boxes) =====
+    const uint64_t pol_w = policy_evict_normal();
+    uint32_t g = 0;
+    for (int v = blockIdx.x; v < total; v += gridDim.x) {
+      int h, task, l;
+      map_tile(s_prefix, s_sigma, a.M_pad, v, h, task, l);
+      const Tile t = load_tile(params, task, l);
+      const int n0 = t.ct * kDecCols;
+      for (int kb = 0; kb < a.num_kb; ++kb, ++g) {
+        const int s = g % kDecSt;
+        mbar_wait(empty_bar(s), ((g / kDecSt) & 1u) ^ 1u);
+        if (lane == 0) {
+          const uint32_t dst = sW + s * kDecWBytes;
+          mbar_arrive_expect_tx(full_bar(s), kDecWBytes);
+          if (a.w4d) {
+            tma_load_4d(&tmW, full_bar(s), dst, 0, kb * kBK, n0 >> 6, t.expert, pol_w);
+          } else {
+            for (int j = 0; j < kDecCols / 64; ++j)
+              tma_load_3d(&tmW, full_bar(s), dst + j * kBBoxBytes, n0 + j * 64, kb * kBK, t.expert, pol_w);
+          }
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp == kMmaWarp) {
+    // ===== swap-AB MMAs: D[col, token] += W_block[k, col]^T tokens[token, k], two M = 128 blocks =====
+    uint32_t g = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int v = blockIdx.x; v < total; v += gridDim.x) {
+      int h, task, l;
+      map_tile(s_prefix, s_sigma, a.M_pad, v, h, task, l);
+      const Tile t = load_tile(params, task, l);
+      const int ntok = (min(kDecRows, t.rows - t.rt * kDecRows) + 15) & ~15;
+      const uint32_t idesc = idesc_bf16_f32(128, ntok, /*A MN-major*/ 1, /*B K-major*/ 0);
+      mbar_wait(tempty_bar(acc), acc_phase ^ 1u);
+      tc_fence_after();
+      for (int kb = 0; kb < a.num_kb; ++kb, ++g) {
+        const int s = g % kDecSt;
+        mbar_wait(full_bar(s), (g / kDecSt) & 1u);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t w0 = sW + s * kDecWBytes, t0 = sTok + s * kDecTokBytes;
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf)
+#pragma unroll
+            for (int kk = 0; kk < kBK / 16; ++kk)
+              mma_bf16(tmem_base + acc * kDecAccCols + hf * 64,
+                       smem_desc_sw128(w0 + hf * 2 * kBBoxBytes + kk * 2048, kBBoxBytes, 1024),
+                       smem_desc_sw128(t0 + kk * 32, 16, 1024), idesc, (kb | kk) != 0);
+          mma_commit(empty_bar(s));
+        }
+        __syncwarp();
+      }
+      if (lane == 0) mma_commit(tfull_bar(acc));
+      __syncwarp();
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1u;
+      }
+    }
+  } else {
+    // ===== epilogue: warp -> (block cg, TMEM lane quarter q): 32 output columns, every token =====
+    const int q = warp & 3;
+    const int cg = (warp - (kMmaWarp + 1)) >> 2;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int v = blockIdx.x; v < total; v += gridDim.x) {
+      int h, task, l;
+      map_tile(s_prefix, s_sigma, a.M_pad, v, h, task, l);
+      const Tile t = load_tile(params, task, l);
+      const int rbeg = t.rt * kDecRows;
+      const int nvalid = min(kDecRows, t.rows - rbeg);
+      const int col = t.ct * kDecCols + cg * 128 + q * 32 + lane;
+      mbar_wait(tfull_bar(acc), acc_phase);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * kDecAccCols + cg * 64;
+      for (int c = 0; c < nvalid; c += 32) {
+        uint32_t r[32];
+        tmem_ld32(taddr + c, r);
+        tmem_wait_ld();
+        if (col < a.N) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            if (c + j < nvalid) {
+              const int csr = t.row0 + rbeg + c + j;
+              const int64_t yr = a.y_row_map ? (int64_t)__ldg(a.y_row_map + csr) : (int64_t)csr;
+              if (a.y_f32)
+                reinterpret_cast<float*>(a.Y)[yr * a.N + col] = __uint_as_float(r[j]);
+              else
+                reinterpret_cast<__nv_bfloat16*>(a.Y)[yr * a.N + col] = __float2bfloat16_rn(__uint_as_float(r[j]));
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty_bar(acc));
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1u;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kMmaWarp) {
+    tc_fence_after();
+    tmem_dealloc<256, 1>(tmem_base);
+  }
+}
+
 // Decode every virtual tile with the same device function as the GEMM.
 __global__ void decode_debug_kernel(const int32_t* plan, int total, int M_pad, int off_params, int32_t* out) {
   extern __shared__ int32_t s_pre[];
@@ -1166,6 +1371,9 @@ cudaError_t set_smem_attrs() {
                         set_attr<false, 2, true, true>(), set_attr<true, 2, true, true>()};
     for (cudaError_t x : e)
       if (x != cudaSuccess && err == cudaSuccess) err = x;
+    const cudaError_t d = cudaFuncSetAttribute(moe_gemm_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)(kDecSmem + 8 * kMaxMPad));
+    if (d != cudaSuccess && err == cudaSuccess) err = d;
   });
   return err;
 }
@@ -1218,7 +1426,7 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
     MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_gemm_swiglu: the plan must have bm = 256, bn = 256 (got %d x %d)", v.bm, v.bn);
   if (gated && !aligned16(W2)) MOE_FAIL(MOE_ERR_INVALID, "moe_gemm_swiglu: W_up must be 16-byte aligned");
   const bool wide = v.bm == 256 && v.bn > 256;    // wide pair tile: two N = bn/2 MMA blocks
-  const int cta = v.bm / kBM;                      // CTAs per tile: each stages bn / cta W columns
+  const int cta = v.bm == 256 ? 2 : 1;             // CTAs per tile: each stages bn / cta W columns
   const int bnc_blk = v.bn / cta / (wide ? 2 : 1); // W columns one CTA stages per MMA block
   // 4-D W view (one TMA per block): needs every CTA's block start on a 64-column chunk.
   const bool w4d = (v.N % 64) == 0 && bnc_blk % 64 == 0;
@@ -1277,7 +1485,24 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
   if (v.bm == 256 && (v.bn / 2) % 16) MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_gemm: pair tiles need bn %% 32 == 0");
   cudaError_t attr_err = set_smem_attrs();
   if (attr_err != cudaSuccess) MOE_FAIL(MOE_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(attr_err));
-  if (v.bm == 256) {
+  if (v.bm == kDecRows) {
+    // Decode-regime tiles: swap-AB on one CTA (moe_gemm_decode_kernel).
+    if (gated || v.bn != kDecCols || (v.flags & MOE_SPLIT_TAIL))
+      MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_gemm: bm = 64 tiles need bn = 256, no split tails, not gated");
+    const int grid = v.total < 0 ? sm_count_cached() : std::min(v.total, sm_count_cached());
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = kDecSmem + 8 * (size_t)v.M_pad;
+    cfg.stream = (cudaStream_t)stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t le = cudaLaunchKernelEx(&cfg, moe_gemm_decode_kernel, tmW, a);
+    if (le != cudaSuccess) MOE_FAIL(MOE_ERR_CUDA, "moe_gemm decode launch: %s", cudaGetErrorString(le));
+  } else if (v.bm == 256) {
     const bool split = (v.flags & MOE_SPLIT_TAIL) != 0;
     const int pairs = v.total < 0 ? sm_count_cached() / 2 : std::min(v.total, sm_count_cached() / 2);
     const size_t smem = (split && wide   ? Geo<2, true, true>::kSmem

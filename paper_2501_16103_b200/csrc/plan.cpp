@@ -88,13 +88,17 @@ moe_status moe_plan_build(const int32_t* counts, int32_t E, int64_t H, int64_t N
       r256 += ceil_div(m, 256) * 256;
     }
     bm = bn > 256 || (r256 * 100 <= r128 * 110 && bn % 32 == 0) ? 256 : 128;
+    // (bm = 64, the decode swap-AB tile, is opt-in: measured no faster than 128 x 256; §6.4.)
   }
   // Auto width: CTA-pair tiles go wide (256 x 512) whenever N has 512 columns.
   // (A last column tile past N trims its MMAs to the valid columns; narrower wide tiles such as
   // 3 x 480 for N = 1408 measured slower — their W boxes start off the 64-column chunk grid.)
   if (auto_bn && bm == 256 && N >= 512) bn = 512;
-  if (bm != 128 && bm != 256)
-    MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_plan_build: bm=%d unsupported (128: one CTA, 256: CTA pair, 0: auto)", bm);
+  if (bm != 64 && bm != 128 && bm != 256)
+    MOE_FAIL(MOE_ERR_UNSUPPORTED,
+             "moe_plan_build: bm=%d unsupported (64: decode swap-AB tile, 128: one CTA, 256: CTA pair, 0: auto)", bm);
+  if (bm == 64 && (bn != 256 || (flags & MOE_SPLIT_TAIL)))
+    MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_plan_build: bm=64 (decode tiles) needs bn=256 and no MOE_SPLIT_TAIL");
   // bm = 256, 256 < bn <= 512: wide pair tile (two N = bn/2 MMA blocks sharing the staged token rows).
   const bool wide_tile = bm == 256 && bn > 256 && bn <= 512 && bn % 32 == 0;
   if (!wide_tile && (bn < 16 || bn > 256 || bn % (bm == 256 ? 32 : 16)))

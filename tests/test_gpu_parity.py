@@ -237,6 +237,12 @@ RAGGED_WIDE = [                     # bm = 256, bn = 512: two N = 256 MMA blocks
     (1500, 4, 1, 128, 200),         # 3-D W map (N % 64 != 0)
     (2048, 4, 2, 64, 1536),         # 1024 rows/expert on average
 ]
+RAGGED_DECODE = [                   # bm = 64 decode tiles (swap-AB, one CTA): any rows, 64 per tile
+    (1, 8, 2, 4096, 1024),          # one token
+    (40, 8, 2, 200, 136),           # K tail, N tail (3-D W map), ~10 rows per expert
+    (300, 5, 2, 256, 512),          # several 64-row tiles per expert
+    (64, 16, 4, 128, 1408),
+]
 RAGGED_WIDE_BN = [                  # wide tiles narrower than 512: blocks of bn/2 (not a multiple of 32 / 64)
     (300, 5, 2, 200, 1408, 480),    # DS width: 3 x 480, block 240 = 7.5 epilogue chunks
     (513, 7, 3, 256, 1000, 352),    # block 176: 2.75 W chunks per CTA half-block
@@ -250,7 +256,8 @@ RAGGED_WIDE_BN = [                  # wide tiles narrower than 512: blocks of bn
                          + [c + (256, 256, "1", M.MOE_SPLIT_TAIL) for c in RAGGED_SPLIT]
                          + [c + (512, 256, a, 0) for c in RAGGED_WIDE for a in ("0", "1")]
                          + [c + (512, 256, "1", M.MOE_SPLIT_TAIL) for c in RAGGED_SPLIT]
-                         + [c[:5] + (c[5], 256, "1", f) for c in RAGGED_WIDE_BN for f in (0, M.MOE_SPLIT_TAIL)])
+                         + [c[:5] + (c[5], 256, "1", f) for c in RAGGED_WIDE_BN for f in (0, M.MOE_SPLIT_TAIL)]
+                         + [c + (256, 64, "1", 0) for c in RAGGED_DECODE])
 @pytest.mark.parametrize("mode", ["int", "int_bf16", "normal"])
 def test_gemm_ragged(T, E, k, H, N, bn, bm, a_path, flags, mode, monkeypatch):
     monkeypatch.setenv("MOE_A_PATH", a_path)          # A staging path: gather4 (0) / cp.async (1)
@@ -310,6 +317,7 @@ def _sample_rows(row_off, counts, rng, per_expert=6):
                                              ("dec16", 512, 256, 0), ("paper_worst", 512, 256, 0),
                                              ("mix", 512, 256, 2), ("ds", 512, 256, 2), ("paper_worst", 512, 256, 2),
                                              ("ds", 0, 0, 0), ("ds", 480, 256, 2),
+                                             ("dec16", 256, 64, 0), ("dec256", 256, 64, 0), ("dec1", 256, 64, 0),
                                              ("mix", 256, 256, 2), ("ds", 128, 128, 0), ("ds", 256, 256, 0),
                                              ("ds", 256, 256, 2), ("dec16", 256, 128, 0), ("dec16", 256, 0, 0),
                                              ("dec16", 256, 256, 2), ("paper_worst", 256, 256, 0),

@@ -174,6 +174,21 @@ def test_planner_auto_tile_width():
     assert (b["bm"], b["bn"]) == (256, 512)
 
 
+def test_planner_decode_regime_tiles():
+    """bm = 64 (opt-in 64-token swap-AB decode tiles, bn 256): the mapping is Alg. 1/4 over those
+    tiles; bm = 0 never picks them."""
+    rng = random.Random(17)
+    for _ in range(100):
+        E = rng.randint(1, 64)
+        counts = [0 if rng.random() < 0.4 else rng.randint(1, 300) for _ in range(E)]
+        if not any(counts):
+            continue
+        _compare(np.array(counts), 8 * rng.randint(1, 2000), 64, 256, rng.choice(["max", "repeat"]))
+        assert moe_lib.parse_plan_blob(moe_lib.moe_plan_build(counts, 64, 14336))["bm"] != 64
+    with pytest.raises(moe_lib.MoeError):
+        moe_lib.moe_plan_build([3, 4], 64, 1024, 64, 256, moe_lib.MOE_SPLIT_TAIL)
+
+
 def test_planner_decode_bijection_through_blob():
     """Decode every block of a library-built blob with the oracle's Alg. 2 and check the lattice."""
     counts = np.array([300, 0, 5, 129, 0, 1000, 1])
@@ -195,7 +210,10 @@ def test_planner_errors():
         moe_lib.moe_plan_build([1, 2], 63, 128)
     assert e.value.status == -2
     with pytest.raises(moe_lib.MoeError) as e:
-        moe_lib.moe_plan_build([1, 2], 64, 128, bm=64)
+        moe_lib.moe_plan_build([1, 2], 64, 128, bm=32)
+    assert e.value.status == -2
+    with pytest.raises(moe_lib.MoeError) as e:                  # decode tiles are 64 x 256
+        moe_lib.moe_plan_build([1, 2], 64, 128, bm=64, bn=128)
     assert e.value.status == -2
     with pytest.raises(moe_lib.MoeError) as e:
         moe_lib.moe_plan_build([1, 2], 64, 128, bn=24)
