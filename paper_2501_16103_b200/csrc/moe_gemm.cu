@@ -178,6 +178,15 @@ __device__ __forceinline__ int wide_block_cols(int bn, int ct, int N, int hf) {
   return nvalid <= 0 ? 0 : min(bnp, (nvalid + 127) & ~127);
 }
 
+// Wide kind-0 tiles whose valid rows fit in 128 ("half" tiles: an expert's short last row tile)
+// run M = 128 pair MMAs — 64 rows per CTA, half the tensor time; the D layout then folds each
+// block's columns: [0, N/2) in TMEM lanes 0-63, [N/2, N) in lanes 64-127 (CUTLASS's UMMA_2SM
+// "2x2" data path for M = 128), each over TMEM columns [0, N/2).
+template <bool kWide, bool kGated>
+__device__ __forceinline__ bool half_tile(int rows, int rt, bool swap) {
+  return kWide && !kGated && !swap && rows - rt * 256 <= 128;
+}
+
 __device__ __forceinline__ float tanh_approx(float x) {
   float y;
   asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -362,8 +371,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const Tile t = load_tile<kSplit>(params, task, l);
       // kind 0: this CTA's 128 rows of the tile; kind 1 (swap-AB tail): this CTA's half of the
       // tail's `height` token rows, which the MMA reads as its N operand.
-      const int n_alloc = kSplit && t.kind == 1 ? t.height / kCta : kBM;
-      const int rbeg = kSplit && t.kind == 1 ? (int)rank * n_alloc : t.rt * kPairRows + (int)rank * kBM;
+      const bool hlf = half_tile<kWide, kGated>(t.rows, t.rt, kSplit && t.kind == 1);
+      const int n_alloc = kSplit && t.kind == 1 ? t.height / kCta : hlf ? kBM / 2 : kBM;
+      const int rbeg = kSplit && t.kind == 1 ? (int)rank * n_alloc : t.rt * kPairRows + (int)rank * n_alloc;
       const int nvalid = min(n_alloc, t.rows - rbeg);   // may be <= 0 for the second CTA of a pair tile
       const int32_t* idx = a.token_idx + t.row0;
       if (a_mode == 2) {
@@ -570,7 +580,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int hf = 0; hf < 2; ++hf) {
               ncol_blk[hf] = wide_block_cols(t.bn, t.ct, a.N, hf);
-              if (ncol_blk[hf] > 0) idesc_blk[hf] = idesc_bf16_f32(kPairRows, ncol_blk[hf], 0, 1);
+              const int m = half_tile<kWide, kGated>(t.rows, t.rt, false) ? kPairRows / 2 : kPairRows;
+              if (ncol_blk[hf] > 0) idesc_blk[hf] = idesc_bf16_f32(m, ncol_blk[hf], 0, 1);
             }
           }
         }
@@ -883,7 +894,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         continue;
       }
-      const int grow = t.rt * kPairRows + (int)rank * kBM + q * 32 + lane;   // row within the task
+      // Half tiles (M = 128 pair MMA): lane quarters 0/1 hold rows 0-31 / 32-63 of this CTA's 64
+      // for the block's first half of columns, quarters 2/3 the same rows for the second half.
+      const bool hlf = half_tile<kWide, kGated>(t.rows, t.rt, kSplit && t.kind == 1);
+      const int grow = hlf ? t.rt * kPairRows + (int)rank * (kBM / 2) + (q & 1) * 32 + lane
+                           : t.rt * kPairRows + (int)rank * kBM + q * 32 + lane;   // row within the task
       const bool valid = grow < t.rows;
       const int64_t yrow = a.y_row_map ? (int64_t)__ldg(a.y_row_map + t.row0 + min(grow, t.rows - 1))
                                        : (int64_t)t.row0 + grow;
@@ -953,11 +968,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
         for (int hf = 0; hf < kHalves; ++hf) {
           wait_block1(hf);
-          const int n0 = t.ct * t.bn + hf * bnp;
-          const int col_end = min(n0 + bnp, a.N);
+          // columns of this warp's lanes: the whole block, or (half tile) its first / second half
+          const int hw = hlf ? wide_block_cols(t.bn, t.ct, a.N, hf) / 2 : bnp;
+          const int n0 = t.ct * t.bn + hf * bnp + (hlf ? (q >> 1) * hw : 0);
+          const int col_end = min(n0 + hw, a.N);
           const int slot = kWide ? hf : acc;        // TMEM block and its tmem-empty barrier
           const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + slot * kAccCols;
-          for (int c = 32 * cg; c < bnp && (!tma_rows || n0 + c < a.N); c += 32 * kEpiGroups) {
+          for (int c = 32 * cg; c < hw && (!tma_rows || n0 + c < a.N); c += 32 * kEpiGroups) {
             uint32_t r[32];
             tmem_ld32(taddr + c, r);
             tmem_wait_ld();
