@@ -564,3 +564,43 @@ def test_gemm_1024_experts(bm, bn):
     Y, counts, row_off, tok, *_ = run_path(ids, Xd, Wd, E, bn=bn, bm=bm)
     rc, rr, rt, rs = omoe.buckets(ids, E)
     assert np.array_equal(Y.cpu().double().numpy(), omoe.expert_gemm(X, W, rt, rr))
+
+
+TILE_VARIANTS = [(128, 256, 0), (128, 112, 0), (256, 256, 0), (256, 256, M.MOE_SPLIT_TAIL), (256, 512, 0),
+                 (256, 512, M.MOE_SPLIT_TAIL), (256, 384, 0), (256, 480, M.MOE_SPLIT_TAIL), (64, 256, 0),
+                 (256, 512, M.MOE_ORDER_HALF_INTERVAL), (128, 256, M.MOE_PAD_REPEAT | M.MOE_ORDER_ALTERNATING)]
+
+
+@pytest.mark.parametrize("case", range(88))
+def test_gemm_fuzz_tile_variants(case):
+    """Random shapes (ragged K, N, rows; empty experts; a skewed or uniform routing) through a
+    random tile variant: exact integers, fp32 and bf16 (TMA-store) outputs, gathered or
+    CSR-ordered (token_idx NULL) rows — all bit-exact against the oracle."""
+    rng = np.random.default_rng(1000 + case)
+    E = int(rng.integers(1, 24))
+    k = int(rng.integers(1, min(E, 6) + 1))
+    T = int(rng.choice([1, 7, 64, 200, 513, 1500]))
+    H = int(8 * rng.integers(1, 80))
+    N = int(8 * rng.integers(1, 200))
+    bm, bn, flags = TILE_VARIANTS[case % len(TILE_VARIANTS)]
+    s = float(rng.choice([0.0, 1.2]))
+    n_empty = int(rng.integers(0, max(1, E - k)))
+    ids = synth.route_gumbel(case, T, E, k, s=s, n_empty=min(n_empty, E - k))
+    X = synth.make_x(case, T, H, "int")
+    W = synth.make_w(case, E, H, N, "int")
+    Xd = torch.from_numpy(X).to(torch.bfloat16).cuda()
+    Wd = torch.from_numpy(W).to(torch.bfloat16).cuda()
+    counts, row_off, tok, _, _ = M.moe_route(torch.from_numpy(ids).cuda(), E)
+    plan = M.Plan(counts.cpu().numpy(), H, N, bm, bn, flags)
+    rc, rr, rt, rs = omoe.buckets(ids, E)
+    ref = omoe.expert_gemm(X, W, rt, rr)
+    out = torch.float32 if case % 2 == 0 else torch.bfloat16
+    contiguous = case % 3 == 0
+    Xin = Xd.index_select(0, tok.long()).contiguous() if contiguous else Xd
+    Y = torch.full((tok.numel(), N), float("nan"), dtype=out, device="cuda")
+    if plan.total_tiles:
+        M.moe_gemm(plan, Xin, None if contiguous else tok, Wd, Y=Y)
+    torch.cuda.synchronize()
+    got = Y.cpu().double().numpy()
+    exp = ref if out == torch.float32 else torch.from_numpy(ref).to(torch.bfloat16).double().numpy()
+    assert np.array_equal(got, exp), f"case {case}: T={T} E={E} k={k} H={H} N={N} tile={bm}x{bn} flags={flags}"
