@@ -604,3 +604,27 @@ def test_gemm_fuzz_tile_variants(case):
     got = Y.cpu().double().numpy()
     exp = ref if out == torch.float32 else torch.from_numpy(ref).to(torch.bfloat16).double().numpy()
     assert np.array_equal(got, exp), f"case {case}: T={T} E={E} k={k} H={H} N={N} tile={bm}x{bn} flags={flags}"
+
+
+@pytest.mark.parametrize("case", range(24))
+def test_forward_device_plan_fuzz(case):
+    """moe_forward with the plan built on the device inside the routing kernels (M_pad = pad32(E),
+    tile count read in-kernel), random shapes and tile variants, two steps on one plan."""
+    rng = np.random.default_rng(5000 + case)
+    E = int(rng.integers(1, 40))
+    k = int(rng.integers(1, min(E, 4) + 1))
+    T = int(rng.choice([1, 33, 300, 1100]))
+    H = int(8 * rng.integers(1, 64))
+    N = int(8 * rng.integers(1, 160))
+    bm, bn, flags = TILE_VARIANTS[case % len(TILE_VARIANTS)]
+    X = synth.make_x(case, T, H, "int")
+    W = synth.make_w(case, E, H, N, "int")
+    Xd = torch.from_numpy(X).to(torch.bfloat16).cuda()
+    Wd = torch.from_numpy(W).to(torch.bfloat16).cuda()
+    plan = M.Plan(None, H, N, bm, bn, flags, E=E)
+    for step in range(2):
+        ids = synth.route_gumbel(case * 7 + step, T, E, k, s=1.2 if step else 0.0)
+        Y, *_ = M.moe_forward(torch.from_numpy(ids).cuda(), Xd, Wd, E, plan=plan, out_dtype=torch.float32)
+        torch.cuda.synchronize()
+        rc, rr, rt, rs = omoe.buckets(ids, E)
+        assert np.array_equal(Y.cpu().double().numpy(), omoe.expert_gemm(X, W, rt, rr)), f"case {case} step {step}"
