@@ -8,8 +8,8 @@ A step = one pass of the whole hot path over one batch of synthetic input
 sigma) + blob H2D -> moe_gemm (one tcgen05 launch over every expert tile).
 `value` = useful FLOPs (2 * sum m_e * H * N) / device step time, inputs resident
 in HBM; `e2e` = the same metric with X / top-k ids copied from pinned host memory
-and Y copied back inside the timed region.  L2 is flushed (256 MiB memset)
-before every timed step.  `--impl reference` times the fp64 CPU oracle on a
+and Y copied back inside the timed region.  L2 is flushed (256 MiB memset, then a
+256 MiB read so no dirty line is left to write back) before every timed step.  `--impl reference` times the fp64 CPU oracle on a
 bounded sample of the same workload (the tier's reference arm).
 
 Multi-GPU (torchrun, N > 1): see DESIGN.md §Multi-GPU; each rank runs the
@@ -187,6 +187,30 @@ def run_reference(args, cfg):
     print(json.dumps(line), flush=True)
 
 
+class L2Flush:
+    """Between timed steps: write a 256 MiB buffer (evicts everything), then read another 256 MiB
+    one, so L2 holds only clean lines of the flush buffer.  The timed kernel then misses in L2 for
+    all its inputs and does not pay the HBM write-back of the flush's own dirty lines (the state
+    ncu's --cache-control all gives a replayed kernel).  `write_only()` is the plain memset flush."""
+
+    def __init__(self, torch, dev):
+        self.w = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+        self.r = torch.ones(32 << 20, dtype=torch.int64, device=dev)
+
+    def write_only(self):
+        self.w.zero_()
+
+    def __call__(self):
+        self.w.zero_()
+        self.r.sum()
+
+
+def host_pad(torch, ms: float = 2.0):
+    """Queue a GPU sleep so the host enqueues the timed launches before the device reaches them:
+    events then bracket device time only, not the Python/ctypes launch latency of an eager call."""
+    torch.cuda._sleep(int(ms * 2.0e6))             # ~2e6 cycles per ms at the 1.9-2.0 GHz boost clock
+
+
 def route_launches(T: int, E: int) -> int:
     """Kernels one moe_route(_plan) call launches (route.cu): histogram + fused scan/compaction
     while chunks x experts <= 16384, else histogram + scan + compaction."""
@@ -219,7 +243,7 @@ def run_ffn(args, cfg):
     Wdn = synth.make_w_torch(args.seed + 2, E, I, H, device=dev)
     layer = M.MoeFFN(Wg, Wu, Wdn)
     out = torch.empty((cfg.T, H), dtype=torch.bfloat16, device=dev)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush = L2Flush(torch, dev)
     stream = torch.cuda.current_stream()
     rows = int((ids >= 0).sum())
     flops = 6.0 * rows * H * I
@@ -229,8 +253,9 @@ def run_ffn(args, cfg):
     # per-stage times (eager, events on the launching stream)
     stages = {"route_plans": [], "swiglu_gemm": [], "down_gemm": [], "combine": []}
     for _ in range(max(3, min(args.steps, 10))):
-        flush.zero_()
+        flush()
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+        host_pad(torch)
         ev[0].record(stream)
         counts, row_off, tok, slot, _ = M.moe_route(topk_d, E, plan=layer.plan_gu)
         layer.plan_dn.update_device(counts)
@@ -259,8 +284,9 @@ def run_ffn(args, cfg):
     step_ms = []
     with ClockSampler(0) as clk:
         for _ in range(args.steps):
-            flush.zero_()
+            flush()
             s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            host_pad(torch, 0.5)
             s0.record(stream)
             graph.replay()
             s1.record(stream)
@@ -279,7 +305,7 @@ def run_ffn(args, cfg):
         "config": {"workload": f"{cfg.name} FFN: E={E} top-{cfg.k} T={cfg.T} H={H} I={I} routing={cfg.routing} "
                                f"seed={args.seed}", "tiles": f"gate/up {layer.plan_gu.bm}x{layer.plan_gu.bn} (x2 "
                                f"accumulators), down {layer.plan_dn.bm}x{layer.plan_dn.bn}",
-                   "l2": "flushed before every timed step (256 MiB memset)"},
+                   "l2": "flushed before every timed step (256 MiB memset + 256 MiB read: clean L2)"},
         "stages_ms": st,
         "kernels": {"swiglu_gemm_tflops": gu, "down_gemm_tflops": dn,
                     "combine_gbs": comb_bytes / (st["combine"] * 1e-3) / 1e9},
@@ -296,7 +322,9 @@ def config_dict(cfg, args):
                         f"routing={cfg.routing} seed={args.seed}",
             "tile": f"{getattr(args, 'bm_resolved', args.bm) or 'auto'}x{getattr(args, 'bn_resolved', args.bn) or 'auto'}", "out_dtype": args.out_dtype,
             "planner": "host (counts D2H + moe_plan_update)" if args.host_plan else "device (moe_plan_device)", "global_batch": cfg.T,
-            "l2": "flushed before every timed step (256 MiB memset); W alone exceeds L2",
+            "l2": "flushed before every timed step (256 MiB memset + 256 MiB read: clean L2); W alone exceeds L2",
+            "timing": "CUDA events on the launching stream; a GPU sleep queued ahead of each timed step "
+                      "keeps host launch latency out of the device time (e2e includes it)",
             "parallelism": f"ep{args.gpus}" if args.gpus > 1 else "1 GPU"}
 
 
@@ -322,13 +350,13 @@ def run_ours(args, cfg):
     topk_d = torch.from_numpy(ids).to(dev)
     Xd = synth.make_x_torch(args.seed, cfg.T, cfg.H, device=dev)
     Wd = synth.make_w_torch(args.seed, cfg.E, cfg.H, cfg.N, device=dev)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush = L2Flush(torch, dev)
     flops = cfg.flops
     stream = torch.cuda.current_stream()
 
     plan = None
 
-    def step(Y=None):
+    def step(Y=None, pad_gemm=False):
         nonlocal plan
         if args.host_plan:                         # P:142 option 1: counts D2H, plan on the host
             counts, row_off, tok, slot, _ = M.moe_route(topk_d, cfg.E, with_slot=False)
@@ -342,6 +370,8 @@ def run_ours(args, cfg):
                 bm, bn = (args.bm, args.bn) if args.bm or args.bn else M.suggest_tile(cfg.T * cfg.k, cfg.E, cfg.H, cfg.N)
                 plan = M.Plan(None, cfg.H, cfg.N, bm, bn, E=cfg.E)
             counts, row_off, tok, slot, _ = M.moe_route(topk_d, cfg.E, with_slot=False, plan=plan)
+        if pad_gemm:                               # host-planned: the host synchronised above; let it
+            host_pad(torch, 0.2)                   # enqueue the GEMM before the device reaches g0
         g0 = torch.cuda.Event(enable_timing=True)
         g0.record(stream)
         Y = M.moe_gemm(plan, Xd, tok, Wd, Y=Y, out_dtype=out_dtype)
@@ -353,17 +383,31 @@ def run_ours(args, cfg):
         step(Ybuf)
     torch.cuda.synchronize()
 
-    # (1) eager steps: per-launch GEMM time on the launching stream (the roofline's kernel time)
+    # (1) eager steps: per-launch GEMM time on the launching stream (the roofline's kernel time).
+    # A GPU sleep ahead of each step lets the host enqueue it first, so the events see device time
+    # only (the host-planned mode still synchronises inside the step, before the GEMM launch).
     step_ms_eager, gemm_ms = [], []
     for _ in range(args.steps):
-        flush.zero_()
+        flush()
         s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        host_pad(torch)
         s0.record(stream)
-        _, g0 = step(Ybuf)
+        _, g0 = step(Ybuf, pad_gemm=args.host_plan)
         s1.record(stream)
         s1.synchronize()
         step_ms_eager.append(s0.elapsed_time(s1))
         gemm_ms.append(g0.elapsed_time(s1))
+    # the same launches after a write-only (memset) flush: the kernel also pays the HBM write-back of
+    # the flush's dirty lines (reported beside the clean-L2 time, not used for the roofline)
+    gemm_ms_dirty = []
+    for _ in range(min(args.steps, 10)):
+        flush.write_only()
+        s1 = torch.cuda.Event(enable_timing=True)
+        host_pad(torch)
+        _, g0 = step(Ybuf, pad_gemm=args.host_plan)
+        s1.record(stream)
+        s1.synchronize()
+        gemm_ms_dirty.append(g0.elapsed_time(s1))
     # (2) the step as one CUDA graph (route + device plan + GEMM, no host synchronisation inside)
     graph = None
     if args.graph and not args.host_plan:
@@ -385,8 +429,9 @@ def run_ours(args, cfg):
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
-            flush.zero_()
+            flush()
             s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            host_pad(torch, 0.5)
             s0.record(stream)
             if graph is not None:
                 graph.replay()
@@ -445,7 +490,7 @@ def run_ours(args, cfg):
         torch.cuda.synchronize()
         e_ms = []
         for _ in range(max(3, min(args.steps, 10))):
-            flush.zero_()
+            flush()
             s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s0.record(stream)
             e2e_step()
@@ -521,12 +566,13 @@ def run_ours(args, cfg):
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": statistics.mean(step_ms), "higher_is_better": True,
-            "ms_per_step_eager": statistics.mean(step_ms_eager),
+            "ms_per_step_eager": None if args.host_plan else statistics.mean(step_ms_eager),
             "cuda_graph": graph is not None,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": config_dict(cfg, args),
             "pct_of_peak": value / peak,
             "kernel": {"name": "moe_gemm_kernel", "ms_per_launch": gemm_avg, "tflops": achieved,
+                       "ms_per_launch_after_memset_flush": statistics.mean(gemm_ms_dirty),
                        "pct_of_measured_burst_peak": achieved / peak,
                        "pct_of_measured_sustained_peak": achieved / float(peaks["bf16_tflops_sustained"]),
                        "pct_of_datasheet_2250": achieved / 2250.0},
@@ -582,7 +628,7 @@ def run_ep(args, base):
                                      "normal", 6, dev).reshape(T_l, cfg.H)
     W_l = synth.make_w_torch(args.seed, cfg.E, cfg.H, cfg.N, device=dev, experts=range(rank * El, (rank + 1) * El))
     moe = ExpertParallelMoE(cfg.E, W_l, TorchComm(), bm=args.bm, bn=args.bn, out_dtype=out_dtype)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush = L2Flush(torch, dev)
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
         moe.forward(topk_l, X_l)
@@ -593,7 +639,7 @@ def run_ep(args, base):
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
-            flush.zero_()
+            flush()
             s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s0.record(stream)
             moe.forward(topk_l, X_l)
@@ -624,7 +670,7 @@ def run_ep(args, base):
         Xe, te = torch.empty_like(X_l), torch.empty_like(topk_l)
         e_ms = []
         for i in range(2 + max(3, min(args.steps, 10))):
-            flush.zero_()
+            flush()
             dist.barrier()
             s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s0.record(stream)
@@ -650,7 +696,7 @@ def run_ep(args, base):
                        "tile": f"{moe.kernels._plans[('ep', args.bm, args.bn)].bm}x{moe.kernels._plans[('ep', args.bm, args.bn)].bn}",
                        "out_dtype": args.out_dtype, "global_batch": cfg.T, "parallelism": f"ep{ws}",
                        "collectives": "NCCL all_to_all_single (torch.distributed): counts, dispatch rows, "
-                                      "combine rows", "l2": "flushed before every timed step"},
+                                      "combine rows", "l2": "flushed before every timed step (memset + read: clean L2)"},
             "pct_of_peak": value / (peak * ws),
             "per_rank": [{"ms_per_step": float(g[0]), "gemm_ms": float(g[1]), "gemm_tflops": float(g[2])}
                          for g in gathered],
