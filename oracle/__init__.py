@@ -21,8 +21,10 @@ Modules
              bookkeeping and an expert-parallel simulator.
 ``ffn``      the full MoE FFN layer around the expert GEMM:
              SwiGLU expert FFN (R14) and the weighted combine.
+``fp8``      the OCP E4M3 decode written out and the expert GEMM on decoded FP8
+             values with a per-expert scale (R15).
 
 Parity-pin status of every function is listed in DESIGN.md §"Oracle pins";
 no function here is "parity unpinned".
 """
-from . import ffn, mapping, moe  # noqa: F401
+from . import ffn, fp8, mapping, moe  # noqa: F401

@@ -26,14 +26,14 @@ MOE_PLAN_MAGIC = 0x4D4F4531
 MOE_PLAN_HEADER = 16
 MOE_PLAN_TASK_WORDS = 8
 
-# Public symbols of include/moe_sm100.h, moe_sm100_ep.h, moe_sm100_ffn.h and moe_sm100_debug.h.
+# Public symbols of include/moe_sm100.h, moe_sm100_ep.h, moe_sm100_ffn.h, moe_sm100_fp8.h and moe_sm100_debug.h.
 EXPORTED = (
     "moe_plan_blob_words", "moe_plan_build", "moe_plan_create", "moe_plan_update", "moe_plan_query",
     "moe_plan_blob", "moe_plan_device_blob", "moe_plan_destroy", "moe_route", "moe_gemm",
     "moe_decode_debug", "moe_device_info", "moe_last_error", "moe_version", "moe_probe_gather4",
     "moe_gemm_profile", "moe_plan_device", "moe_plan_sync", "moe_gemm_rowmap",
     "moe_ep_dispatch_plan", "moe_gather_rows", "moe_ep_combine_map", "moe_ep_unpack", "moe_route_plan",
-    "moe_gemm_swiglu", "moe_combine",
+    "moe_gemm_swiglu", "moe_combine", "moe_gemm_fp8",
 )
 
 
@@ -90,6 +90,7 @@ def lib() -> ctypes.CDLL:
         "moe_ep_unpack": (ctypes.c_int32, [vp, vp, ctypes.c_int64, vp, vp, vp, ctypes.c_int32, ctypes.c_int32,
                                            ctypes.c_int64, vp, vp]),
         "moe_gemm_swiglu": (ctypes.c_int32, [vp, vp, ctypes.c_int64, vp, vp, vp, vp, ctypes.c_int32, vp]),
+        "moe_gemm_fp8": (ctypes.c_int32, [vp, vp, ctypes.c_int64, vp, vp, vp, vp, ctypes.c_int32, vp]),
         "moe_combine": (ctypes.c_int32, [vp, ctypes.c_int32, ctypes.c_int64, ctypes.c_int32, ctypes.c_int64, vp, vp,
                                          vp, ctypes.c_int32, vp, vp, ctypes.c_int32, vp]),
     }
@@ -287,6 +288,30 @@ def moe_gemm(plan: Plan, X, token_idx, W, Y=None, out_dtype=None, stream=None, r
         assert row_map.dtype == torch.int32 and row_map.is_contiguous()
         _check(lib().moe_gemm_rowmap(plan.handle, X.data_ptr(), X.shape[0], tp, W.data_ptr(),
                                      Y.data_ptr(), yd, row_map.data_ptr(), _stream(stream)))
+    return Y
+
+
+def moe_gemm_fp8(plan: Plan, X, token_idx, W, scale=None, Y=None, out_dtype=None, stream=None):
+    """Y[sum m_e, N] = scale[e] * (X[token_idx] @ W[e]) on FP8 E4M3 X [T, H] and W [E, H, N]
+    (torch.float8_e4m3fn or uint8 codes), fp32 accumulate, one launch (include/moe_sm100_fp8.h).
+    scale: [E] fp32 device tensor or None; token_idx None: X's rows are already in CSR order."""
+    import torch
+
+    out_dtype = out_dtype or torch.bfloat16
+    f8 = (torch.float8_e4m3fn, torch.uint8)
+    assert X.is_cuda and X.dtype in f8 and X.is_contiguous()
+    assert W.is_cuda and W.dtype in f8 and W.is_contiguous()
+    if token_idx is not None:
+        assert token_idx.dtype == torch.int32 and token_idx.is_contiguous()
+    if scale is not None:
+        assert scale.is_cuda and scale.dtype == torch.float32 and scale.is_contiguous()
+    rows = int(token_idx.numel()) if token_idx is not None else int(X.shape[0])
+    if Y is None:
+        Y = torch.empty((rows, plan.N), dtype=out_dtype, device=X.device)
+    yd = MOE_DTYPE_F32 if Y.dtype == torch.float32 else MOE_DTYPE_BF16
+    _check(lib().moe_gemm_fp8(plan.handle, X.data_ptr(), X.shape[0],
+                              token_idx.data_ptr() if token_idx is not None else None, W.data_ptr(),
+                              scale.data_ptr() if scale is not None else None, Y.data_ptr(), yd, _stream(stream)))
     return Y
 
 

@@ -93,6 +93,7 @@ struct GemmArgs {
                              // 2 = no B loads, 4 = A as contiguous tile TMA (pairs), 8 = no Y stores
   const int32_t* y_row_map;  // nullable: Y row of CSR row i is y_row_map[i] (EP combine buffer)
   int32_t tma_store;         // bf16 Y in CSR row order: full 32-row quarters leave through TMA tile stores
+  const float* scale;        // FP8 path, nullable: Y rows of expert e are scaled by scale[e] (fp32, epilogue)
 };
 
 // Per-CTA counters written by the instrumented build (kProf = true).
@@ -172,10 +173,13 @@ __device__ __forceinline__ Tile load_tile(const int32_t* params, int task, int l
 // Wide tiles: the columns MMA block hf of column tile ct actually computes — all bn/2 of them,
 // except in a column tile passing N, where they are trimmed to the block's columns below N
 // rounded up to 128 (each CTA's half then stays on the 64-column W chunk grid); 0 = no MMA.
+// (FP8: W chunks are 128 columns, so blocks are trimmed to multiples of 256.)
+template <bool kFp8 = false>
 __device__ __forceinline__ int wide_block_cols(int bn, int ct, int N, int hf) {
+  constexpr int kGran = kFp8 ? 256 : 128;
   const int bnp = bn / 2;
   const int nvalid = min(bn, N - ct * bn) - hf * bnp;
-  return nvalid <= 0 ? 0 : min(bnp, (nvalid + 127) & ~127);
+  return nvalid <= 0 ? 0 : min(bnp, (nvalid + kGran - 1) & ~(kGran - 1));
 }
 
 // Wide kind-0 tiles whose valid rows fit in 128 ("half" tiles: an expert's short last row tile)
@@ -271,7 +275,9 @@ struct Geo {
 // block b holds gate in columns [0,128) and up in [128,256) of the same 128 outputs, and the
 // epilogue writes silu(gate) * up (R14) block by block, freeing each as the plain wide
 // tile does.
-template <bool kProf, int kCta, bool kSplit, bool kWide = false, bool kGated = false>
+// kFp8 (moe_gemm_fp8): X and W in FP8 E4M3, tcgen05.mma kind::f8f6f4, fp32 accumulate, optional
+// per-expert fp32 scale in the epilogue.  Stages keep their byte sizes: a K block is 128 FP8 values.
+template <bool kProf, int kCta, bool kSplit, bool kWide = false, bool kGated = false, bool kFp8 = false>
 __global__ void __launch_bounds__(kThreads, 1)
     moe_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
                     const __grid_constant__ CUtensorMap tmW2, const __grid_constant__ CUtensorMap tmY,
@@ -283,6 +289,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int kSt = Geo<kCta, kSplit, kWide>::kStages;
   constexpr int kBSt = Geo<kCta, kSplit, kWide>::kBStage;
   constexpr int kHalves = kWide ? 2 : 1;                   // N = 256 MMA blocks per tile
+  // Element type: a stage holds 128-byte K rows either way, so a K block is 64 bf16 or 128 FP8
+  // values; a W box is 64 (bf16) or 128 (FP8) columns x one K block (8 / 16 KB); one MMA consumes
+  // 32 bytes of K (K = 16 bf16 / 32 FP8), i.e. 16 / 32 rows of the MN-major W box (+2 / +4 KB).
+  constexpr int kKB = kFp8 ? 128 : kBK;
+  constexpr int kCS = kFp8 ? 7 : 6;                        // log2(W columns per box)
+  constexpr int kBox = kFp8 ? 128 * 128 : kBBoxBytes;
+  constexpr int kKStep = kFp8 ? 4096 : 2048;
+  static_assert(!kFp8 || (!kSplit && !kGated && !kProf), "FP8: plain and wide tiles");
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;            // SW128 atoms need 1024-byte alignment
@@ -384,10 +398,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int s = g % kSt;
             wait_timed<kProf>(empty_bar(s), ((g / kSt) & 1u) ^ 1u, c_wait);
             if constexpr (kCta == 2) {
-              tma_load_2d_pair(&tmX, leader(full_bar(s)), sA + s * kABytes, kb * kBK, t.row0 + rbeg, pol_x);
+              tma_load_2d_pair(&tmX, leader(full_bar(s)), sA + s * kABytes, kb * kKB, t.row0 + rbeg, pol_x);
             } else {
               mbar_arrive_expect_tx(full_bar(s), kABytes);
-              tma_load_2d(&tmX, full_bar(s), sA + s * kABytes, kb * kBK, t.row0 + rbeg, pol_x);
+              tma_load_2d(&tmX, full_bar(s), sA + s * kABytes, kb * kKB, t.row0 + rbeg, pol_x);
             }
           }
         }
@@ -404,16 +418,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           wait_timed<kProf>(empty_bar(s), ((g / kSt) & 1u) ^ 1u, c_wait);
           if (lane == 0) mbar_arrive_expect_tx(full_bar(s), kABytes / kAWarps);
           __syncwarp();
-          if (lane < 8) tma_gather4(&tmX, full_bar(s), sA + s * kABytes + rr * 128, kb * kBK, r0, r1, r2, r3, pol_x);
+          if (lane < 8) tma_gather4(&tmX, full_bar(s), sA + s * kABytes + rr * 128, kb * kKB, r0, r1, r2, r3, pol_x);
         }
       } else {
-        const __nv_bfloat16* src[8];
+        // Byte addressing: a row of X is H * (1 or 2) bytes; thread ch copies bytes [16 ch, 16 ch + 16)
+        // of the row's 128-byte K block.
+        const int64_t row_bytes = (int64_t)a.H * (kFp8 ? 1 : 2);
+        const uint8_t* src[8];
         uint32_t rowok = 0;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const int r = rsub + 16 * j;
           const int tok = r < nvalid ? __ldg(idx + rbeg + r) : 0;
-          src[j] = a.X + (int64_t)tok * a.H + ch * 8;
+          src[j] = reinterpret_cast<const uint8_t*>(a.X) + (int64_t)tok * row_bytes + ch * 16;
           rowok |= (r < nvalid ? 1u : 0u) << j;
         }
         for (int kb = 0; kb < a.num_kb; ++kb, ++g) {
@@ -439,8 +456,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             continue;
           }
 #endif
-          const int kcol = kb * kBK;
-          const bool colok = kcol + ch * 8 < a.H;
+          const int64_t kbyte = (int64_t)kb * 128;
+          const bool colok = kbyte + ch * 16 < row_bytes;
           const uint32_t dst = sA + s * kABytes + dst_off;
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
@@ -449,7 +466,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #else
             const bool ok = colok && ((rowok >> j) & 1u);
 #endif
-            cp_async_16(dst + j * 16 * 128, ok ? src[j] + kcol : a.X, ok ? 16u : 0u);
+            cp_async_16(dst + j * 16 * 128, ok ? (const void*)(src[j] + kbyte) : (const void*)a.X, ok ? 16u : 0u);
           }
           cp_async_mbar_arrive_noinc(full_bar(s));
         }
@@ -473,7 +490,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int bnp = t.bn / kHalves;               // columns of one MMA block (gated: 128 gate + 128 up)
       const int bnc = kGated ? 128 : bnp / kCta;    // columns of an MMA block staged by this CTA
       const int n0 = kGated ? t.ct * t.bn : t.ct * t.bn + (int)rank * bnc;   // block h at n0 + h * bnp
-      const int nbox = (bnc + 63) >> 6;
+      const int nbox = (bnc + (1 << kCS) - 1) >> kCS;
       for (int kb = 0; kb < a.num_kb; ++kb, ++g) {
         const int s = g % kSt;
         wait_timed<kProf>(empty_bar(s), ((g / kSt) & 1u) ^ 1u, c_wait);
@@ -505,12 +522,12 @@ __global__ void __launch_bounds__(kThreads, 1)
               nbx[hf] = nbox;
               if constexpr (kWide && !kGated) {
                 if (!(kSplit && t.kind == 1)) {
-                  const int nc = wide_block_cols(t.bn, t.ct, a.N, hf);
+                  const int nc = wide_block_cols<kFp8>(t.bn, t.ct, a.N, hf);
                   nh[hf] = t.ct * t.bn + hf * bnp + (int)rank * (nc / 2);
-                  nbx[hf] = nc == 0 ? 0 : a.w4d ? nbox : (nc / 2 + 63) >> 6;
+                  nbx[hf] = nc == 0 ? 0 : a.w4d ? nbox : (nc / 2 + (1 << kCS) - 1) >> kCS;
                 }
               }
-              bytes += kCta * nbx[hf] * kBBoxBytes;
+              bytes += kCta * nbx[hf] * kBox;
             }
             if (a_mode == 2) bytes += kCta * kABytes;   // both CTAs' contiguous-row A tiles
 #ifdef MOE_EXPERIMENTS
@@ -521,22 +538,22 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int hf = 0; hf < kHalves; ++hf) {
               if (nbx[hf] == 0) continue;
-              const uint32_t dst = dstB + hf * nbox * kBBoxBytes;
+              const uint32_t dst = dstB + hf * nbox * kBox;
               const CUtensorMap* wm = kGated && rank == 1 ? &tmW2 : &tmW;   // gated: leader gate, peer up
               if (a.w4d) {
-                tma_load_4d_pair(wm, fb, dst, 0, kb * kBK, nh[hf] >> 6, t.expert, pol_w);
+                tma_load_4d_pair(wm, fb, dst, 0, kb * kKB, nh[hf] >> kCS, t.expert, pol_w);
               } else {
                 for (int j = 0; j < nbx[hf]; ++j)
-                  tma_load_3d_pair(wm, fb, dst + j * kBBoxBytes, nh[hf] + j * 64, kb * kBK, t.expert, pol_w);
+                  tma_load_3d_pair(wm, fb, dst + j * kBox, nh[hf] + (j << kCS), kb * kKB, t.expert, pol_w);
               }
             }
           } else {
-            mbar_arrive_expect_tx(full_bar(s), nbox * kBBoxBytes);
+            mbar_arrive_expect_tx(full_bar(s), nbox * kBox);
             if (a.w4d) {
-              tma_load_4d(&tmW, full_bar(s), dstB, 0, kb * kBK, n0 >> 6, t.expert, pol_w);
+              tma_load_4d(&tmW, full_bar(s), dstB, 0, kb * kKB, n0 >> kCS, t.expert, pol_w);
             } else {
               for (int j = 0; j < nbox; ++j)
-                tma_load_3d(&tmW, full_bar(s), dstB + j * kBBoxBytes, n0 + j * 64, kb * kBK, t.expert, pol_w);
+                tma_load_3d(&tmW, full_bar(s), dstB + j * kBox, n0 + (j << kCS), kb * kKB, t.expert, pol_w);
             }
           }
         }
@@ -569,8 +586,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         // kind 1: D[cols, tokens] = A[W block as MN-major M-operand] * B[tail tokens (K-major)],
         //         M = the pair's 256 output columns, N = the tail height (swap-AB).
         const uint32_t idesc = swap ? idesc_bf16_f32(kPairRows, t.height, /*A MN-major*/ 1, /*B K-major*/ 0)
-                                    : idesc_bf16_f32(kPairRows, kGated ? 256 : t.bn / kHalves,
-                                                     /*A K-major*/ 0, /*B MN-major*/ 1);
+                                    : idesc_f32acc<kFp8>(kPairRows, kGated ? 256 : t.bn / kHalves,
+                                                         /*A K-major*/ 0, /*B MN-major*/ 1);
         // Wide tiles past N (the last column tile when N is not a multiple of bn): each block's MMA
         // covers wide_block_cols columns (zero: the block is skipped), matching what the B warp staged.
         uint32_t idesc_blk[2] = {idesc, idesc};
@@ -579,9 +596,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (!swap) {
 #pragma unroll
             for (int hf = 0; hf < 2; ++hf) {
-              ncol_blk[hf] = wide_block_cols(t.bn, t.ct, a.N, hf);
+              ncol_blk[hf] = wide_block_cols<kFp8>(t.bn, t.ct, a.N, hf);
               const int m = half_tile<kWide, kGated>(t.rows, t.rt, false) ? kPairRows / 2 : kPairRows;
-              if (ncol_blk[hf] > 0) idesc_blk[hf] = idesc_bf16_f32(m, ncol_blk[hf], 0, 1);
+              if (ncol_blk[hf] > 0) idesc_blk[hf] = idesc_f32acc<kFp8>(m, ncol_blk[hf], 0, 1);
             }
           }
         }
@@ -627,8 +644,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               } else if (ncol_blk[hf] > 0) {
 #pragma unroll
                 for (int kk = 0; kk < kBK / 16; ++kk)
-                  mma_bf16_pair(d, smem_desc_sw128(a0 + kk * 32, 16, 1024),
-                                smem_desc_sw128(b0 + kk * 2048, kBBoxBytes, 1024), idesc_blk[hf], (kb | kk) != 0);
+                  mma_issue<kFp8, 2>(d, smem_desc_sw128(a0 + kk * 32, 16, 1024),
+                                     smem_desc_sw128(b0 + kk * kKStep, kBox, 1024), idesc_blk[hf], (kb | kk) != 0);
               }
             }
             __syncwarp();
@@ -710,7 +727,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               // W block: MN-major SW128; 64-wide chunks 8 KB apart (LBO), 8-row K groups 1 KB apart
               // (SBO); K step of 16 rows = +2 KB.  The two kinds only swap the operand roles.
 #ifdef MOE_EXPERIMENTS
-              if (a.experiment & 16) {   // B read as K-major (wrong Y): is the MN-major B operand slower?
+              if (!kFp8 && (a.experiment & 16)) {   // B read as K-major (wrong Y): is the MN-major B operand slower?
                 const uint32_t idk = idesc_bf16_f32(kPairRows, kGated ? 256 : t.bn / kHalves, 0, 0);
 #pragma unroll
                 for (int kk = 0; kk < kBK / 16; ++kk) {
@@ -725,9 +742,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int kk = 0; kk < kBK / 16; ++kk) {
                   const uint64_t ad = smem_desc_sw128(a0 + kk * 32, 16, 1024);
-                  const uint64_t bd = smem_desc_sw128(b0 + kk * 2048, kBBoxBytes, 1024);
-                  if constexpr (kCta == 2) mma_bf16_pair(d_tmem, ad, bd, idesc, (kb | kk) != 0);
-                  else mma_bf16(d_tmem, ad, bd, idesc, (kb | kk) != 0);
+                  const uint64_t bd = smem_desc_sw128(b0 + kk * kKStep, kBox, 1024);
+                  mma_issue<kFp8, kCta>(d_tmem, ad, bd, idesc, (kb | kk) != 0);
                 }
               } else {
 #pragma unroll
@@ -969,7 +985,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int hf = 0; hf < kHalves; ++hf) {
           wait_block1(hf);
           // columns of this warp's lanes: the whole block, or (half tile) its first / second half
-          const int hw = hlf ? wide_block_cols(t.bn, t.ct, a.N, hf) / 2 : bnp;
+          const int hw = hlf ? wide_block_cols<kFp8>(t.bn, t.ct, a.N, hf) / 2 : bnp;
           const int n0 = t.ct * t.bn + hf * bnp + (hlf ? (q >> 1) * hw : 0);
           const int col_end = min(n0 + hw, a.N);
           const int slot = kWide ? hf : acc;        // TMEM block and its tmem-empty barrier
@@ -978,6 +994,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t r[32];
             tmem_ld32(taddr + c, r);
             tmem_wait_ld();
+            if constexpr (kFp8) {
+              if (a.scale) {
+                const float sc = __ldg(a.scale + t.expert);
+#pragma unroll
+                for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * sc);
+              }
+            }
             put_chunk(r, n0 + c, col_end);
           }
           tc_fence_before();
@@ -1281,14 +1304,15 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-moe_status make_x_map(CUtensorMap* m, const void* X, int64_t T, int64_t H, int box_rows = 1) {
+// fp8: X holds FP8 E4M3 bytes (a box is 128 values = 128 bytes, like 64 bf16).
+moe_status make_x_map(CUtensorMap* m, const void* X, int64_t T, int64_t H, int box_rows = 1, bool fp8 = false) {
   auto fn = encode_fn();
   if (!fn) MOE_FAIL(MOE_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
   const cuuint64_t dims[2] = {(cuuint64_t)H, (cuuint64_t)T};
-  const cuuint64_t strides[1] = {(cuuint64_t)H * 2};
-  const cuuint32_t box[2] = {(cuuint32_t)kBK, (cuuint32_t)box_rows};   // gather4: box_rows = 1
+  const cuuint64_t strides[1] = {(cuuint64_t)H * (fp8 ? 1 : 2)};
+  const cuuint32_t box[2] = {(cuuint32_t)(fp8 ? 128 : kBK), (cuuint32_t)box_rows};   // gather4: box_rows = 1
   const cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(X), dims, strides, box, estr,
+  CUresult r = fn(m, fp8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(X), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) MOE_FAIL(MOE_ERR_CUDA, "cuTensorMapEncodeTiled(X) failed: %d", (int)r);
@@ -1310,11 +1334,22 @@ moe_status make_y_map(CUtensorMap* m, void* Y, int64_t R, int64_t N) {
 }
 
 // bn_cta: W columns one CTA stages per K block (the 4-D box spans ceil(bn_cta / 64) chunks).
-moe_status make_w_map(CUtensorMap* m, const void* W, int64_t E, int64_t H, int64_t N, int bn_cta, bool w4d) {
+// fp8: W holds FP8 E4M3 bytes; chunks of 128 columns (128 bytes), K blocks of 128 rows (4-D only).
+moe_status make_w_map(CUtensorMap* m, const void* W, int64_t E, int64_t H, int64_t N, int bn_cta, bool w4d,
+                      bool fp8 = false) {
   auto fn = encode_fn();
   if (!fn) MOE_FAIL(MOE_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
   CUresult r;
-  if (w4d) {
+  if (fp8) {
+    if (!w4d) MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_gemm_fp8: needs N %% 128 == 0 and 128-column CTA blocks");
+    const cuuint64_t dims[4] = {128, (cuuint64_t)H, (cuuint64_t)(N / 128), (cuuint64_t)E};
+    const cuuint64_t strides[3] = {(cuuint64_t)N, 128, (cuuint64_t)H * N};
+    const cuuint32_t box[4] = {128, 128, (cuuint32_t)((bn_cta + 127) / 128), 1};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void*>(W), dims, strides, box, estr,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else if (w4d) {
     // W viewed as {64 (n within chunk), H, N/64 (chunk), E}: one box = the whole B stage,
     // laid out chunk-major, then k, then n — the MN-major SW128 canonical layout.
     const cuuint64_t dims[4] = {64, (cuuint64_t)H, (cuuint64_t)(N / 64), (cuuint64_t)E};
@@ -1369,9 +1404,9 @@ extern "C" moe_status moe_device_info(int32_t* sm_count, int32_t* cc_major, int3
 
 namespace {
 
-template <bool kProf, int kCta, bool kSplit, bool kWide = false, bool kGated = false>
+template <bool kProf, int kCta, bool kSplit, bool kWide = false, bool kGated = false, bool kFp8 = false>
 cudaError_t set_attr() {
-  return cudaFuncSetAttribute(moe_gemm_kernel<kProf, kCta, kSplit, kWide, kGated>,
+  return cudaFuncSetAttribute(moe_gemm_kernel<kProf, kCta, kSplit, kWide, kGated, kFp8>,
                               cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)(Geo<kCta, kSplit, kWide>::kSmem + 8 * kMaxMPad));
 }
@@ -1380,7 +1415,9 @@ cudaError_t set_smem_attrs() {
   static std::once_flag once;
   static cudaError_t err = cudaSuccess;
   std::call_once(once, [] {
-    cudaError_t e[12] = {set_attr<false, 1, false>(),      set_attr<true, 1, false>(),
+    cudaError_t e[15] = {set_attr<false, 1, false>(),      set_attr<true, 1, false>(),
+                        set_attr<false, 1, false, false, false, true>(), set_attr<false, 2, false, false, false, true>(),
+                        set_attr<false, 2, false, true, false, true>(),
                         set_attr<false, 2, false>(),      set_attr<true, 2, false>(),
                         set_attr<false, 2, true>(),       set_attr<true, 2, true>(),
                         set_attr<false, 2, false, true>(), set_attr<true, 2, false, true>(),
@@ -1397,7 +1434,8 @@ cudaError_t set_smem_attrs() {
 
 static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, const int32_t* token_idx,
                               const void* W, void* Y, int32_t y_dtype, void* stream, long long* prof,
-                              const int32_t* y_row_map = nullptr, const void* W2 = nullptr) {
+                              const int32_t* y_row_map = nullptr, const void* W2 = nullptr, bool fp8 = false,
+                              const float* scale = nullptr) {
   moe::clear_error();
   if (!plan) MOE_FAIL(MOE_ERR_INVALID, "moe_gemm: null plan");
   moe::BlobView v;
@@ -1436,7 +1474,18 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
   }
 #endif
   // token_idx NULL: X rows are the plan's CSR rows (a_mode 2: 128-row tile boxes).
-  moe_status st = make_x_map(&tmX, X, T, v.H, (experiment & 4) || !token_idx ? kBM : 1);
+  if (fp8) {
+    // FP8 E4M3 (moe_gemm_fp8): 1-CTA tiles (bn % 128 == 0) and CTA-pair / wide tiles whose CTA
+    // blocks are 128 columns (bn = 256 or 512); TMA strides need 16-byte rows.
+    if (prof || W2) MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_gemm_fp8: no profiling / gated variant");
+    if (v.bm == kDecRows || (v.flags & MOE_SPLIT_TAIL))
+      MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_gemm_fp8: bm = 64 decode tiles and MOE_SPLIT_TAIL plans are bf16-only");
+    const bool ok_tile = v.bm == 128 ? v.bn % 128 == 0 : (v.bn == 256 || v.bn == 512);
+    if (!ok_tile || v.N % 128 || v.H % 16)
+      MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_gemm_fp8: needs N %% 128 == 0, H %% 16 == 0 and a %d x %d tile of "
+               "128-column CTA blocks (1-CTA bn %% 128 == 0, pair bn = 256 or 512)", v.bm, v.bn);
+  }
+  moe_status st = make_x_map(&tmX, X, T, v.H, (experiment & 4) || !token_idx ? kBM : 1, fp8);
   if (st != MOE_OK) return st;
   const bool gated = W2 != nullptr;                // moe_gemm_swiglu: W_gate / W_up blocks
   if (gated && !(v.bm == 256 && v.bn == 256))
@@ -1446,8 +1495,8 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
   const int cta = v.bm == 256 ? 2 : 1;             // CTAs per tile: each stages bn / cta W columns
   const int bnc_blk = v.bn / cta / (wide ? 2 : 1); // W columns one CTA stages per MMA block
   // 4-D W view (one TMA per block): needs every CTA's block start on a 64-column chunk.
-  const bool w4d = (v.N % 64) == 0 && bnc_blk % 64 == 0;
-  st = make_w_map(&tmW, W, v.E, v.H, v.N, bnc_blk, w4d);
+  const bool w4d = fp8 ? (v.N % 128) == 0 && bnc_blk % 128 == 0 : (v.N % 64) == 0 && bnc_blk % 64 == 0;
+  st = make_w_map(&tmW, W, v.E, v.H, v.N, bnc_blk, w4d, fp8);
   if (st != MOE_OK) return st;
   CUtensorMap tmW2 = tmW;
   if (gated) {
@@ -1482,7 +1531,8 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
   a.Y = Y;
   a.y_f32 = y_dtype == MOE_DTYPE_F32;
   a.N = v.N;
-  a.num_kb = (int32_t)moe::ceil_div(v.H, kBK);
+  a.num_kb = (int32_t)moe::ceil_div(v.H, fp8 ? 128 : kBK);
+  a.scale = scale;
   a.total = v.total;
   a.M_pad = v.M_pad;
   a.off_params = (int32_t)v.off_params;
@@ -1497,6 +1547,7 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
   {
     const char* am = getenv("MOE_A_PATH");       // timing studies: force the A staging path
     a.a_mode = !token_idx ? 2 : am && (atoi(am) == 0 || atoi(am) == 1) ? atoi(am) : kDefaultAMode;
+    if (fp8 && a.a_mode == 0) a.a_mode = 1;      // FP8 rows are staged by cp.async (or tile TMA)
   }
 
   if (v.bm == 256 && (v.bn / 2) % 16) MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_gemm: pair tiles need bn %% 32 == 0");
@@ -1542,7 +1593,11 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
     cfg.attrs = attr;
     cfg.numAttrs = 2;
     cudaError_t le;
-    if (gated)
+    if (fp8 && wide)
+      le = cudaLaunchKernelEx(&cfg, moe_gemm_kernel<false, 2, false, true, false, true>, tmX, tmW, tmW2, tmY, a);
+    else if (fp8)
+      le = cudaLaunchKernelEx(&cfg, moe_gemm_kernel<false, 2, false, false, false, true>, tmX, tmW, tmW2, tmY, a);
+    else if (gated)
       le = prof ? cudaLaunchKernelEx(&cfg, moe_gemm_kernel<true, 2, false, true, true>, tmX, tmW, tmW2, tmY, a)
                 : cudaLaunchKernelEx(&cfg, moe_gemm_kernel<false, 2, false, true, true>, tmX, tmW, tmW2, tmY, a);
     else if (wide && split)
@@ -1570,8 +1625,10 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t le = prof ? cudaLaunchKernelEx(&cfg, moe_gemm_kernel<true, 1, false>, tmX, tmW, tmW2, tmY, a)
-                          : cudaLaunchKernelEx(&cfg, moe_gemm_kernel<false, 1, false>, tmX, tmW, tmW2, tmY, a);
+    cudaError_t le = fp8    ? cudaLaunchKernelEx(&cfg, moe_gemm_kernel<false, 1, false, false, false, true>, tmX, tmW,
+                                                 tmW2, tmY, a)
+                     : prof ? cudaLaunchKernelEx(&cfg, moe_gemm_kernel<true, 1, false>, tmX, tmW, tmW2, tmY, a)
+                            : cudaLaunchKernelEx(&cfg, moe_gemm_kernel<false, 1, false>, tmX, tmW, tmW2, tmY, a);
     if (le != cudaSuccess) MOE_FAIL(MOE_ERR_CUDA, "moe_gemm launch: %s", cudaGetErrorString(le));
   }
   cudaError_t e = cudaGetLastError();
@@ -1592,6 +1649,11 @@ moe_status moe_gemm_swiglu(const moe_plan* plan, const void* X, int64_t T, const
                            const void* W_gate, const void* W_up, void* Y, int32_t y_dtype, void* stream) {
   if (!W_up) MOE_FAIL(MOE_ERR_INVALID, "moe_gemm_swiglu: null W_up");
   return gemm_launch(plan, X, T, token_idx, W_gate, Y, y_dtype, stream, nullptr, nullptr, W_up);
+}
+
+moe_status moe_gemm_fp8(const moe_plan* plan, const void* X, int64_t T, const int32_t* token_idx, const void* W,
+                        const float* scale, void* Y, int32_t y_dtype, void* stream) {
+  return gemm_launch(plan, X, T, token_idx, W, Y, y_dtype, stream, nullptr, nullptr, nullptr, true, scale);
 }
 
 moe_status moe_gemm_rowmap(const moe_plan* plan, const void* X, int64_t T, const int32_t* token_idx,
