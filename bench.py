@@ -123,10 +123,13 @@ def load_traffic(workload: str):
 # ---------------------------------------------------------------------------
 # CPU oracle timing (cpu_baseline leg / reference arm)
 # ---------------------------------------------------------------------------
-def oracle_sample(cfg, seed: int, budget_s: float, cache: dict | None = None):
-    """Times oracle.moe.expert_gemm expert by expert on the workload until budget_s of
-    CPU work has been spent (input generation excluded).  Returns (flops, seconds, sample, cores)."""
+def oracle_sample(cfg, seed: int, budget_s: float, cache: dict | None = None, fp8: bool = False):
+    """Times oracle.moe.expert_gemm (fp8: oracle.fp8.expert_gemm_fp8 on E4M3 codes) expert by expert
+    on the workload until budget_s of CPU work has been spent (input generation excluded).
+    Returns (flops, seconds, sample, cores)."""
+    from oracle import fp8 as ofp8
     from oracle import moe as omoe
+    from synth import fp8 as sfp8
     try:
         from threadpoolctl import threadpool_info
         cores = sum(int(i.get("num_threads", 1)) for i in threadpool_info() if i.get("user_api") == "blas") or 1
@@ -135,26 +138,31 @@ def oracle_sample(cfg, seed: int, budget_s: float, cache: dict | None = None):
     cache = {} if cache is None else cache
     if "inputs" not in cache:
         ids = synth.route(cfg, seed)
-        cache["inputs"] = (omoe.buckets(ids, cfg.E), synth.make_x(seed, cfg.T, cfg.H))
+        cache["inputs"] = (omoe.buckets(ids, cfg.E),
+                           sfp8.make_x_fp8(seed, cfg.T, cfg.H) if fp8 else synth.make_x(seed, cfg.T, cfg.H))
     (counts, row_off, tok, _), X = cache["inputs"]
     flops, secs, done = 0, 0.0, []
     for e in range(cfg.E):
         if counts[e] == 0:
             continue
         if e not in cache:                                               # generation is not timed
-            cache[e] = synth.make_w(seed, cfg.E, cfg.H, cfg.N, experts=[e])   # [1, H, N]
+            cache[e] = (sfp8.w_fp8_columns(seed, cfg.E, cfg.H, cfg.N, e, np.arange(cfg.N))[None] if fp8
+                        else synth.make_w(seed, cfg.E, cfg.H, cfg.N, experts=[e]))   # [1, H, N]
         W = cache[e]
         a, b = int(row_off[e]), int(row_off[e + 1])
         sub_tok = tok[a:b]
         t0 = time.perf_counter()
-        omoe.expert_gemm(X, W, sub_tok, np.array([0, b - a]))
+        if fp8:
+            ofp8.expert_gemm_fp8(X, W, sub_tok, np.array([0, b - a]), [2.0 ** -synth.w_scale_exp(cfg.H)])
+        else:
+            omoe.expert_gemm(X, W, sub_tok, np.array([0, b - a]))
         secs += time.perf_counter() - t0
         flops += 2 * (b - a) * cfg.H * cfg.N
         done.append(e)
         if secs >= budget_s:
             break
     sample = (f"{cfg.name} seed {seed}: experts {done} ({int(sum(counts[e] for e in done))} of "
-              f"{int(counts.sum())} rows, full H x N), fp64 numpy/OpenBLAS")
+              f"{int(counts.sum())} rows, full H x N), fp64 numpy/OpenBLAS" + (" on decoded E4M3 codes" if fp8 else ""))
     return flops, secs, sample, cores
 
 
@@ -322,6 +330,7 @@ def config_dict(cfg, args):
                         f"routing={cfg.routing} seed={args.seed}",
             "tile": f"{getattr(args, 'bm_resolved', args.bm) or 'auto'}x{getattr(args, 'bn_resolved', args.bn) or 'auto'}", "out_dtype": args.out_dtype,
             "planner": "host (counts D2H + moe_plan_update)" if args.host_plan else "device (moe_plan_device)", "global_batch": cfg.T,
+            "operands": "FP8 E4M3 X and W, per-expert fp32 scale" if getattr(args, "dtype", "bf16") == "fp8" else "bf16",
             "l2": "flushed before every timed step (256 MiB memset + 256 MiB read: clean L2); W alone exceeds L2",
             "timing": "CUDA events on the launching stream; a GPU sleep queued ahead of each timed step "
                       "keeps host launch latency out of the device time (e2e includes it)",
@@ -348,8 +357,22 @@ def run_ours(args, cfg):
 
     ids = synth.route(cfg, args.seed)
     topk_d = torch.from_numpy(ids).to(dev)
-    Xd = synth.make_x_torch(args.seed, cfg.T, cfg.H, device=dev)
-    Wd = synth.make_w_torch(args.seed, cfg.E, cfg.H, cfg.N, device=dev)
+    fp8 = args.dtype == "fp8"
+    if fp8:                                        # FP8 E4M3 codes + per-expert scale (synth/fp8.py)
+        from synth import fp8 as sfp8
+        Xd = sfp8.make_x_fp8_torch(args.seed, cfg.T, cfg.H, device=dev)
+        Wd = sfp8.make_w_fp8_torch(args.seed, cfg.E, cfg.H, cfg.N, device=dev)
+        w_scale = torch.from_numpy(sfp8.w_scale(cfg.E, cfg.H)).to(dev)
+    else:
+        Xd = synth.make_x_torch(args.seed, cfg.T, cfg.H, device=dev)
+        Wd = synth.make_w_torch(args.seed, cfg.E, cfg.H, cfg.N, device=dev)
+        w_scale = None
+    esz = 1 if fp8 else 2
+
+    def gemm(plan, X, tok, W, Y=None):
+        if fp8:
+            return M.moe_gemm_fp8(plan, X, tok, W, w_scale, Y=Y, out_dtype=out_dtype)
+        return M.moe_gemm(plan, X, tok, W, Y=Y, out_dtype=out_dtype)
     flush = L2Flush(torch, dev)
     flops = cfg.flops
     stream = torch.cuda.current_stream()
@@ -374,7 +397,7 @@ def run_ours(args, cfg):
             host_pad(torch, 0.2)                   # enqueue the GEMM before the device reaches g0
         g0 = torch.cuda.Event(enable_timing=True)
         g0.record(stream)
-        Y = M.moe_gemm(plan, Xd, tok, Wd, Y=Y, out_dtype=out_dtype)
+        Y = gemm(plan, Xd, tok, Wd, Y=Y)
         return Y, g0
 
     Y0, _ = step()
@@ -419,7 +442,7 @@ def run_ours(args, cfg):
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
             _, _, tok_g, _, _ = M.moe_route(topk_d, cfg.E, with_slot=False, plan=plan)
-            M.moe_gemm(plan, Xd, tok_g, Wd, Y=Ybuf, out_dtype=out_dtype)
+            gemm(plan, Xd, tok_g, Wd, Y=Ybuf)
         for _ in range(3):
             graph.replay()
         torch.cuda.synchronize()
@@ -451,21 +474,23 @@ def run_ours(args, cfg):
     value = flops * ws * args.steps / (t_total * 1e-3) / 1e12
     gemm_avg = statistics.mean(gemm_ms)
     achieved = flops / (gemm_avg * 1e-3) / 1e12
-    peak = float(peaks["bf16_tflops"])
+    # FP8 contractions take the bf16 measured peak x the nominal FP8 / BF16 ratio (4.5 / 2.25 PF).
+    peak = float(peaks["bf16_tflops"]) * (2.0 if fp8 else 1.0)
     # Algorithmic HBM bytes of one moe_gemm launch: W of active experts, the token
     # rows routed anywhere, Y (out dtype) and the token-index array.
     counts_np = np.bincount(ids.ravel(), minlength=cfg.E)
     ybytes = 2 if out_dtype == torch.bfloat16 else 4
-    alg_bytes = (int((counts_np > 0).sum()) * cfg.H * cfg.N * 2 + len(np.unique(ids)) * cfg.H * 2
-                 + int(counts_np.sum()) * (cfg.N * ybytes + 4))
+    alg_bytes = (int((counts_np > 0).sum()) * cfg.H * cfg.N * esz + len(np.unique(ids)) * cfg.H * esz
+                 + int(counts_np.sum()) * (cfg.N * ybytes + 4) + (4 * cfg.E if fp8 else 0))
     hbm = float(peaks["hbm_gbs"])
     mem_bound = flops / alg_bytes < peak * 1e12 / (hbm * 1e9)
-    traffic, tsrc = load_traffic(cfg.name)
+    traffic, tsrc = load_traffic(("fp8_" if fp8 else "") + cfg.name)
 
     # ---- e2e through the public API with pinned host buffers
     e2e = None
     if not args.no_e2e:
-        X_h = synth.make_x_torch(args.seed, cfg.T, cfg.H).pin_memory()
+        X_h = (sfp8.make_x_fp8_torch(args.seed, cfg.T, cfg.H) if fp8
+               else synth.make_x_torch(args.seed, cfg.T, cfg.H)).pin_memory()
         ids_h = torch.from_numpy(ids).pin_memory()
         Y_h = torch.empty(Y0.shape, dtype=Y0.dtype).pin_memory()
         Xe = torch.empty_like(Xd)
@@ -481,7 +506,7 @@ def run_ours(args, cfg):
             Xe.copy_(X_h, non_blocking=True)
             te.copy_(ids_h, non_blocking=True)
             Y, counts, _, _, _, _ = M.moe_forward(te, Xe, Wd, cfg.E, bm=args.bm, bn=args.bn, out_dtype=out_dtype,
-                                                  plan=plan, device_plan=not args.host_plan, Y=Ybuf)
+                                                  plan=plan, device_plan=not args.host_plan, Y=Ybuf, scale=w_scale)
             Y_h.copy_(Y, non_blocking=True)
             return counts
 
@@ -531,7 +556,7 @@ def run_ours(args, cfg):
                     if i >= 2:
                         stream.wait_event(ev_out[b])             # step i-2's D2H has read Yb[b]
                     M.moe_forward(tb[b], Xb[b], Wd, cfg.E, bm=args.bm, bn=args.bn, out_dtype=out_dtype, plan=plan,
-                                  Y=Yb[b])
+                                  Y=Yb[b], scale=w_scale)
                     ev_comp[b].record(stream)
                     with torch.cuda.stream(s_out):
                         s_out.wait_event(ev_comp[b])
@@ -557,7 +582,7 @@ def run_ours(args, cfg):
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        f, s, sample, cores = oracle_sample(cfg, args.seed, args.cpu_budget)
+        f, s, sample, cores = oracle_sample(cfg, args.seed, args.cpu_budget, fp8=fp8)
         cpu = {"value": f / s / 1e12, "unit": "TFLOP/s", "cores": cores, "kind": "oracle", "sample": sample,
                "seconds": s}
 
@@ -568,14 +593,15 @@ def run_ours(args, cfg):
             "warmup": args.warmup, "ms_per_step": statistics.mean(step_ms), "higher_is_better": True,
             "ms_per_step_eager": None if args.host_plan else statistics.mean(step_ms_eager),
             "cuda_graph": graph is not None,
-            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "scaling": "weak", "vs_baseline": None, "dtype": "fp8_e4m3" if fp8 else "bf16", "data": "synthetic",
             "config": config_dict(cfg, args),
             "pct_of_peak": value / peak,
             "kernel": {"name": "moe_gemm_kernel", "ms_per_launch": gemm_avg, "tflops": achieved,
                        "ms_per_launch_after_memset_flush": statistics.mean(gemm_ms_dirty),
                        "pct_of_measured_burst_peak": achieved / peak,
-                       "pct_of_measured_sustained_peak": achieved / float(peaks["bf16_tflops_sustained"]),
-                       "pct_of_datasheet_2250": achieved / 2250.0},
+                       "pct_of_measured_sustained_peak": achieved / (float(peaks["bf16_tflops_sustained"])
+                                                                     * (2.0 if fp8 else 1.0)),
+                       "pct_of_datasheet_2250": achieved / (4500.0 if fp8 else 2250.0)},
             "roofline": ({"bound": "hbm", "achieved": alg_bytes / (gemm_avg * 1e-3) / 1e9, "peak": hbm,
                           "unit": "GB/s", "frac": alg_bytes / (gemm_avg * 1e-3) / 1e9 / hbm, "traffic": traffic,
                           "peak_source": f"{peak_src} hbm_gbs", "algorithmic_bytes_per_launch": alg_bytes,
@@ -583,7 +609,8 @@ def run_ours(args, cfg):
                          if mem_bound else
                          {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                           "frac": achieved / peak, "traffic": traffic,
-                          "peak_source": f"{peak_src} bf16_tflops (burst; kernel timed per launch)",
+                          "peak_source": f"{peak_src} bf16_tflops (burst; kernel timed per launch)"
+                                         + (" x 2 (nominal FP8 / BF16 dense ratio, 4.5 / 2.25 PF)" if fp8 else ""),
                           "algorithmic_flops_per_launch": flops, "algorithmic_bytes_per_launch": alg_bytes,
                           "traffic_source": tsrc}),
             "cpu_baseline": cpu,
@@ -724,6 +751,8 @@ def main():
     ap.add_argument("--bn", type=int, default=0)
     ap.add_argument("--bm", type=int, default=0, help="tile rows: 128 (1 CTA), 256 (CTA pair), 0 = planner's choice")
     ap.add_argument("--out-dtype", choices=["bf16", "f32"], default="bf16")
+    ap.add_argument("--dtype", choices=["bf16", "fp8"], default="bf16",
+                    help="operand type of X and W: bf16 (the paper's) or FP8 E4M3 with a per-expert scale")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--host-plan", action="store_true", help="plan on the host (counts D2H) instead of on the device")
     ap.add_argument("--ep", action="store_true", help="run the expert-parallel path even on one GPU")

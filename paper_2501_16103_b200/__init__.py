@@ -475,8 +475,11 @@ def moe_probe_gather4(X, rows, col0: int, stream=None):
 
 
 def moe_forward(topk_ids, X, W, E: int, bm: int = 0, bn: int = 0, out_dtype=None, plan: Plan | None = None,
-                stream=None, device_plan: bool = True, Y=None):
+                stream=None, device_plan: bool = True, Y=None, scale=None):
     """One MoE expert-GEMM step: route -> plan -> single-launch GEMM.
+
+    X / W in bf16 run moe_gemm; in FP8 E4M3 (torch.float8_e4m3fn or uint8 codes) moe_gemm_fp8 with
+    the optional per-expert fp32 `scale`.
 
     device_plan=True: the plan is built on the device from the route's counts (moe_plan_device),
     no host synchronisation; counts are returned as a device tensor.  device_plan=False: counts
@@ -499,5 +502,8 @@ def moe_forward(topk_ids, X, W, E: int, bm: int = 0, bn: int = 0, out_dtype=None
             plan = Plan(counts_out, H, N, bm, bn, stream=stream)
         else:
             plan.update(counts_out, stream=stream)
-    Y = moe_gemm(plan, X, token_idx, W, Y=Y, out_dtype=out_dtype or torch.bfloat16, stream=stream)
+    if X.dtype in (torch.float8_e4m3fn, torch.uint8):
+        Y = moe_gemm_fp8(plan, X, token_idx, W, scale, Y=Y, out_dtype=out_dtype or torch.bfloat16, stream=stream)
+    else:
+        Y = moe_gemm(plan, X, token_idx, W, Y=Y, out_dtype=out_dtype or torch.bfloat16, stream=stream)
     return Y, counts_out, row_off, token_idx, slot, plan
