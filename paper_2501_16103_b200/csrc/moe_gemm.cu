@@ -62,7 +62,14 @@ constexpr int kMmaWarp = kAWarps + 1;           // tcgen05 issuer: warp 5
 // Epilogue: warps 6.. ; warp w drains TMEM lane quarter w % 4 (the tcgen05.ld lane rule), and the
 // kEpiWarps / 4 warps of one quarter take alternate 32-column chunks.
 constexpr int kEpiWarps = MOE_EPI_WARPS;
-static_assert(kEpiWarps == 4 || kEpiWarps == 8, "one or two warps per TMEM lane quarter");
+static_assert(kEpiWarps == 4 || kEpiWarps == 8 || kEpiWarps == 16, "1, 2 or 4 warps per TMEM lane quarter");
+// TMA-store staging per epilogue warp: two 2 KB buffers (converting chunk i+1 overlaps the store
+// of chunk i) with four warps or MOE_EPI_DBUF, else one.
+#ifndef MOE_EPI_DBUF
+#define MOE_EPI_DBUF 0
+#endif
+constexpr bool kEpiDbuf = kEpiWarps == 4 || MOE_EPI_DBUF;
+constexpr uint32_t kEpiBufBytes = kEpiDbuf ? 4096u : 2048u;
 constexpr int kEpiGroups = kEpiWarps / 4;
 constexpr int kThreads = 32 * (kAWarps + 2 + kEpiWarps);
 constexpr int kDefaultAMode = 1;                // A staging: cp.async (see the A-producer comment)
@@ -257,7 +264,7 @@ struct Geo {
   static constexpr int kBStage = (kWide ? 2 : 1) * kBStageBytes / kCta;   // bytes of W per CTA per stage
   // 16 KB: a 2 KB bf16 staging buffer per epilogue warp for the TMA-store epilogue (two per warp
   // with four warps), or 4 KB transpose buffers for four warps on swap-AB tail tiles (MOE_SPLIT_TAIL).
-  static constexpr int kEpiStage = 16384;
+  static constexpr int kEpiStage = 16384 > kEpiWarps * kEpiBufBytes ? 16384 : kEpiWarps * kEpiBufBytes;
   static constexpr size_t kSmem = 1024 + (size_t)kStages * (kABytes + kBStage) + kEpiStage + kBarBytes;
 };
 
@@ -809,7 +816,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     uint32_t n_chunk = 0;                                     // TMA-store chunks issued by this warp
-    const uint32_t ebuf = sEpi + (uint32_t)ew * (16384u / kEpiWarps);
+    const uint32_t ebuf = sEpi + (uint32_t)ew * kEpiBufBytes;
     long long c_wait = 0, c_work = 0;
     // Wide tiles: "block 0 full" is awaited with the tile, "block 1 full" before draining block 1.
     auto wait_block1 = [&](int hf) {
@@ -931,9 +938,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (a.experiment & 8) return;
 #endif
         if (tma_rows && col + 32 <= col_end) {        // a box never crosses the block / N
-          const uint32_t buf = kEpiWarps == 4 ? ebuf + (n_chunk & 1u) * 2048u : ebuf;
+          const uint32_t buf = kEpiDbuf ? ebuf + (n_chunk & 1u) * 2048u : ebuf;
           if (lane == 0) {                                  // the store that last used buf has read it
-            if constexpr (kEpiWarps == 4) bulk_wait_group_read<1>();
+            if constexpr (kEpiDbuf) bulk_wait_group_read<1>();
             else bulk_wait_group_read<0>();
           }
           __syncwarp();
@@ -1404,11 +1411,13 @@ extern "C" moe_status moe_device_info(int32_t* sm_count, int32_t* cc_major, int3
 
 namespace {
 
+constexpr size_t kMaxSmem = 232448;              // 227 KB of opt-in dynamic shared memory per CTA (sm_100)
+
 template <bool kProf, int kCta, bool kSplit, bool kWide = false, bool kGated = false, bool kFp8 = false>
 cudaError_t set_attr() {
+  const size_t want = Geo<kCta, kSplit, kWide>::kSmem + 8 * kMaxMPad;
   return cudaFuncSetAttribute(moe_gemm_kernel<kProf, kCta, kSplit, kWide, kGated, kFp8>,
-                              cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)(Geo<kCta, kSplit, kWide>::kSmem + 8 * kMaxMPad));
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(want < kMaxSmem ? want : kMaxSmem));
 }
 
 cudaError_t set_smem_attrs() {
@@ -1578,6 +1587,7 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
                          : wide || gated ? Geo<2, false, true>::kSmem
                                          : Geo<2, false>::kSmem) +
                         8 * (size_t)v.M_pad;
+    if (smem > kMaxSmem) MOE_FAIL(MOE_ERR_CAPACITY, "moe_gemm: %d tasks need %zu B of shared memory", v.M_pad, smem);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * pairs);
     cfg.blockDim = dim3(kThreads);
@@ -1619,6 +1629,8 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = Geo<1>::kSmem + 8 * (size_t)v.M_pad;
+    if (cfg.dynamicSmemBytes > kMaxSmem)
+      MOE_FAIL(MOE_ERR_CAPACITY, "moe_gemm: %d tasks need %zu B of shared memory", v.M_pad, cfg.dynamicSmemBytes);
     cfg.stream = (cudaStream_t)stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
