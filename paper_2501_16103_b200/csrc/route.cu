@@ -17,7 +17,9 @@
 //                       (0, 0) writes counts / row_off and, with a plan, runs the device planner
 //                       body (P:142 / P:144).
 // When chunks x experts exceeds kPlaceMaxCells, the scan runs once in a single-block kernel
-// between A and the compaction (three launches).
+// between A and the compaction (three launches).  Small batches (T <= 1024 tokens, E <= 16,
+// k <= 8: the decode regime) take one single-block kernel instead (route_small_kernel: thread =
+// token, experts in turn, ballot / popcount ranks; no scratch allocation).
 // Negative ids are masked slots (expert parallelism: slots owned by another rank) and are
 // skipped silently.  Invalid entries (id >= E, or an id repeated later in the same token's
 // list) are dropped consistently by A and C and reported in *status.
@@ -53,6 +55,90 @@ __device__ __forceinline__ int classify(const int32_t* row, int j, int E) {
   for (int i = 0; i < j; ++i)
     if (row[i] == x) return -1;
   return 1;
+}
+
+// Small batches: one block, thread = token.  Validation as route_hist_kernel; then for expert
+// e = 0, 1, ... the tokens routed to e are ranked in token order by a ballot / popcount per warp
+// and a prefix over the warps, so token_idx is the same stable CSR as the multi-kernel path.
+constexpr int kSmallMaxE = 16;
+__global__ void __launch_bounds__(kChunk)
+    route_small_kernel(const int32_t* __restrict__ topk, int T, int k, int E, int32_t* __restrict__ counts,
+                       int32_t* __restrict__ row_off, int32_t* __restrict__ token_idx, int32_t* __restrict__ slot,
+                       int32_t* __restrict__ status, int H, int N, int bm, int bn, uint32_t flags,
+                       int32_t* __restrict__ blob) {
+  moe::ptx::pdl_launch_dependents();                 // the GEMM prologue may start; it waits for us
+  __shared__ int s_wc[kChunk / 32][kSmallMaxE];
+  __shared__ int s_cnt[kSmallMaxE], s_base[kSmallMaxE];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int32_t* row = topk + (int64_t)t * k;
+  int r[kRegK], v[kRegK];
+  int bad = 0;
+#pragma unroll
+  for (int j = 0; j < kRegK; ++j) r[j] = t < T && j < k ? __ldg(row + j) : -1;
+#pragma unroll
+  for (int j = 0; j < kRegK; ++j) {
+    int x = j < k ? r[j] : -1;
+    if (x >= E) {
+      bad = 1;
+      x = -1;
+    }
+#pragma unroll
+    for (int i = 0; i < j; ++i)
+      if (x >= 0 && r[i] == x) {
+        bad = 1;
+        x = -1;
+      }
+    v[j] = x;
+  }
+  // Per warp and expert: how many of the warp's tokens are routed there (one ballot per expert),
+  // then one barrier; warp 0 turns the [warps x experts] counts into expert bases.
+  const int n_warps = (T + 31) / 32;                 // warps holding tokens (T <= 1024)
+  unsigned mk[kRegK];                                // slot j: this warp's ballot for expert v[j]
+#pragma unroll
+  for (int j = 0; j < kRegK; ++j) mk[j] = 0;
+  if (warp < n_warps) {
+    for (int e = 0; e < E; ++e) {
+      bool hit = false;
+#pragma unroll
+      for (int j = 0; j < kRegK; ++j) hit |= v[j] == e;
+      const unsigned m = __ballot_sync(0xffffffffu, hit);
+      if (lane == 0) s_wc[warp][e] = __popc(m);
+#pragma unroll
+      for (int j = 0; j < kRegK; ++j)
+        if (v[j] == e) mk[j] = m;
+    }
+  }
+  __syncthreads();
+  if (warp == 0) {
+    int tot = 0;                                     // lane e: tokens of expert e
+    if (lane < E)
+      for (int w = 0; w < n_warps; ++w) tot += s_wc[w][lane];
+    int incl = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane < E) {
+      s_cnt[lane] = tot;
+      s_base[lane] = incl - tot;
+      counts[lane] = tot;
+      row_off[lane] = incl - tot;
+    }
+    if (lane == E - 1) row_off[E] = incl;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kRegK; ++j) {                  // one write per (token, expert) hit
+    if (v[j] < 0) continue;
+    int pos = s_base[v[j]] + __popc(mk[j] & ((1u << lane) - 1u));
+    for (int w = 0; w < warp; ++w) pos += s_wc[w][v[j]];
+    token_idx[pos] = t;
+    if (slot) slot[pos] = j;
+  }
+  bad = __syncthreads_or(bad);
+  if (t == 0 && status) *status = bad ? 1 : 0;
+  if (blob) moe::dplan::plan_body(t < E ? s_cnt[t] : 0, E, H, N, bm, bn, flags, blob);
 }
 
 __global__ void __launch_bounds__(kChunk) route_hist_kernel(const int32_t* __restrict__ topk, int T, int k, int E,
@@ -250,6 +336,16 @@ moe_status route_impl(const int32_t* topk, int64_t T, int32_t k, int32_t E, int3
   }
   cudaStream_t s = (cudaStream_t)stream;
   int32_t* blob = plan ? moe::plan_blob_dev_mut(plan) : nullptr;
+  const char* small_env = getenv("MOE_ROUTE_SMALL");   // MOE_ROUTE_SMALL=0: always the multi-kernel path
+  const bool small_ok = !(small_env && atoi(small_env) == 0);
+  if (small_ok && T <= kChunk && E <= kSmallMaxE && k <= kRegK) {
+    route_small_kernel<<<1, kChunk, 0, s>>>(topk, (int)T, k, E, counts, row_off, token_idx, slot, status, pH, pN,
+                                            pbm, pbn, pflags, blob);
+    cudaError_t e1 = cudaGetLastError();
+    if (e1 != cudaSuccess) MOE_FAIL(MOE_ERR_CUDA, "moe_route launch: %s", cudaGetErrorString(e1));
+    if (plan) moe::plan_set_device_mode(plan, true);
+    return MOE_OK;
+  }
   const int n_chunks = (int)std::max<int64_t>(1, (T + kChunk - 1) / kChunk);
   int32_t* scratch = nullptr;                        // chunk histograms [n_chunks][E], flags [n_chunks]
   cudaError_t err = cudaMallocAsync((void**)&scratch, sizeof(int32_t) * (size_t)n_chunks * (E + 1), s);

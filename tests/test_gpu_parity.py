@@ -140,7 +140,7 @@ def test_decode_large_total():
 
 
 # ---------------------------------------------------------------------------- route (bit-exact)
-@pytest.mark.parametrize("cfg", ["tiny", "mix", "ds", "paper_worst", "dec1", "ep"])
+@pytest.mark.parametrize("cfg", ["tiny", "mix", "ds", "paper_worst", "dec1", "dec16", "dec256", "ep"])
 def test_route_bit_exact(cfg):
     c = synth.CONFIGS[cfg]
     ids = synth.route(c, 0)
@@ -462,7 +462,7 @@ def test_gemm_device_planned_all_empty():
     assert (Y == 7.0).all()
 
 
-@pytest.mark.parametrize("cfg", ["tiny", "mix", "ds", "paper_worst", "dec1", "ep"])
+@pytest.mark.parametrize("cfg", ["tiny", "mix", "ds", "paper_worst", "dec1", "dec16", "dec256", "ep"])
 def test_route_plan_fused_matches_separate(cfg):
     """moe_route_plan = moe_route + moe_plan_device, bit for bit (and both = the oracle)."""
     c = synth.CONFIGS[cfg]
@@ -499,13 +499,18 @@ def test_route_many_chunks_and_masked_slots():
     assert n == int((ids >= 0).sum())
 
 
-@pytest.mark.parametrize("T,k,E,skew", [(20000, 3, 1024, 0.0), (8192, 6, 64, 1.2), (40000, 2, 64, 1.2),
-                                        (32768, 2, 8, 0.0), (32769, 2, 8, 0.0), (3, 1, 1, 0.0)])
-def test_route_place_and_split_paths(T, k, E, skew):
+@pytest.mark.parametrize("T,k,E,skew,small", [(20000, 3, 1024, 0.0, "1"), (8192, 6, 64, 1.2, "1"),
+                                              (40000, 2, 64, 1.2, "1"), (32768, 2, 8, 0.0, "1"),
+                                              (32769, 2, 8, 0.0, "1"), (3, 1, 1, 0.0, "1"), (3, 1, 1, 0.0, "0"),
+                                              (1024, 2, 8, 0.0, "1"), (1024, 2, 8, 0.0, "0"), (1000, 8, 16, 1.2, "1"),
+                                              (1, 2, 8, 0.0, "1"), (77, 3, 5, 0.0, "1"), (1025, 2, 8, 0.0, "1")])
+def test_route_place_and_split_paths(T, k, E, skew, small, monkeypatch):
     """chunks x experts <= 16K: histogram + fused scan/placement kernels (match_any groups);
-    larger (20 chunks x 1024 experts): histogram + single-block scan + chunk x expert compaction.
-    Both must give the oracle's buckets exactly, with masked slots and invalid entries (out of
-    range, repeated in a token's row) dropped and reported."""
+    larger (20 chunks x 1024 experts): histogram + single-block scan + chunk x expert compaction;
+    T <= 1024, E <= 16, k <= 8: the single-block small-batch kernel (MOE_ROUTE_SMALL=0 forces the
+    multi-kernel path).  All must give the oracle's buckets exactly, with masked slots and invalid
+    entries (out of range, repeated in a token's row) dropped and reported."""
+    monkeypatch.setenv("MOE_ROUTE_SMALL", small)
     rng = np.random.default_rng(T + E)
     if skew > 0:
         ids = synth.route_gumbel(T, T, E, k, s=skew)
