@@ -35,6 +35,7 @@ import synth  # noqa: E402
 
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 METRIC = "MoE GEMM TFLOPS and % of B200 BF16 tensor peak at 1/2/4/8 GPUs"
+ORDER_FLAGS = {"natural": 0, "alternating": 4, "half_interval": 8}   # MOE_ORDER_* (include/moe_sm100.h)
 
 
 def load_peaks():
@@ -331,6 +332,7 @@ def config_dict(cfg, args):
             "tile": f"{getattr(args, 'bm_resolved', args.bm) or 'auto'}x{getattr(args, 'bn_resolved', args.bn) or 'auto'}", "out_dtype": args.out_dtype,
             "planner": "host (counts D2H + moe_plan_update)" if args.host_plan else "device (moe_plan_device)", "global_batch": cfg.T,
             "operands": "FP8 E4M3 X and W, per-expert fp32 scale" if getattr(args, "dtype", "bf16") == "fp8" else "bf16",
+            "task_order": getattr(args, "order", "natural"),
             "l2": "flushed before every timed step (256 MiB memset + 256 MiB read: clean L2); W alone exceeds L2",
             "timing": "CUDA events on the launching stream; a GPU sleep queued ahead of each timed step "
                       "keeps host launch latency out of the device time (e2e includes it)",
@@ -385,13 +387,13 @@ def run_ours(args, cfg):
             counts, row_off, tok, slot, _ = M.moe_route(topk_d, cfg.E, with_slot=False)
             counts_h = counts.cpu().numpy()
             if plan is None:
-                plan = M.Plan(counts_h, cfg.H, cfg.N, args.bm, args.bn)
+                plan = M.Plan(counts_h, cfg.H, cfg.N, args.bm, args.bn, ORDER_FLAGS[args.order])
             else:
                 plan.update(counts_h)
         else:                                      # P:142 option 2: plan generated on the device,
             if plan is None:                       # fused into the routing scan (moe_route_plan)
                 bm, bn = (args.bm, args.bn) if args.bm or args.bn else M.suggest_tile(cfg.T * cfg.k, cfg.E, cfg.H, cfg.N)
-                plan = M.Plan(None, cfg.H, cfg.N, bm, bn, E=cfg.E)
+                plan = M.Plan(None, cfg.H, cfg.N, bm, bn, ORDER_FLAGS[args.order], E=cfg.E)
             counts, row_off, tok, slot, _ = M.moe_route(topk_d, cfg.E, with_slot=False, plan=plan)
         if pad_gemm:                               # host-planned: the host synchronised above; let it
             host_pad(torch, 0.2)                   # enqueue the GEMM before the device reaches g0
@@ -751,6 +753,8 @@ def main():
     ap.add_argument("--bn", type=int, default=0)
     ap.add_argument("--bm", type=int, default=0, help="tile rows: 128 (1 CTA), 256 (CTA pair), 0 = planner's choice")
     ap.add_argument("--out-dtype", choices=["bf16", "f32"], default="bf16")
+    ap.add_argument("--order", choices=list(ORDER_FLAGS), default="natural",
+                    help="sigma order of the plan's tasks (P:317-322 expert ordering; DESIGN.md R7)")
     ap.add_argument("--dtype", choices=["bf16", "fp8"], default="bf16",
                     help="operand type of X and W: bf16 (the paper's) or FP8 E4M3 with a per-expert scale")
     ap.add_argument("--no-e2e", action="store_true")
