@@ -149,3 +149,49 @@ def test_fp8_full_size_sampled(cfg, bm, bn):
     got = Y[torch.from_numpy(rows).cuda()][:, torch.from_numpy(cols).cuda()].cpu()
     tol_check(got, ref, cfg)
     assert not torch.isnan(Y.float()).any().item()
+
+
+FP8_TILES = [(128, 128, 0), (128, 256, 0), (128, 128, 1), (256, 256, 0), (256, 512, 0),
+             (256, 512, 8), (128, 256, 1 | 4)]          # 8 = MOE_ORDER_HALF_INTERVAL, 1 | 4 = PAD_REPEAT | ALTERNATING
+
+
+@pytest.mark.parametrize("case", range(42))
+def test_fp8_fuzz_tile_variants(case):
+    """Random shapes (ragged K in 16-byte steps, N in 128-column steps, rows; empty experts; skewed or
+    uniform routing), random FP8 tile variant, host- or device-built plan, gathered or CSR-ordered
+    rows, fp32 / bf16 output, random power-of-two scales: bit-exact against the oracle."""
+    rng = np.random.default_rng(7000 + case)
+    E = int(rng.integers(1, 24))
+    k = int(rng.integers(1, min(E, 6) + 1))
+    T = int(rng.choice([1, 7, 64, 200, 513, 1500]))
+    H = int(16 * rng.integers(1, 60))
+    N = int(128 * rng.integers(1, 14))
+    bm, bn, flags = FP8_TILES[case % len(FP8_TILES)]
+    s = float(rng.choice([0.0, 1.2]))
+    n_empty = int(rng.integers(0, max(1, E - k)))
+    ids = synth.route_gumbel(case, T, E, k, s=s, n_empty=min(n_empty, E - k))
+    Xc, Wc = sfp8.make_x_fp8(case, T, H, "int"), sfp8.make_w_fp8(case, E, H, N, "int")
+    scale = (2.0 ** rng.integers(-3, 4, size=E)).astype(np.float32)
+    topk = torch.from_numpy(ids).cuda()
+    Xd, Wd = torch.from_numpy(Xc).cuda(), torch.from_numpy(Wc).cuda()
+    device_plan = case % 4 == 1
+    if device_plan:
+        plan = M.Plan(None, H, N, bm, bn, flags, E=E)
+        counts, row_off, tok, _, _ = M.moe_route(topk, E, plan=plan)
+        launch = True
+    else:
+        counts, row_off, tok, _, _ = M.moe_route(topk, E)
+        plan = M.Plan(counts.cpu().numpy(), H, N, bm, bn, flags)
+        launch = plan.total_tiles > 0
+    rc, rr, rt, rs = omoe.buckets(ids, E)
+    ref = ofp8.expert_gemm_fp8(Xc, Wc, rt, rr, scale)
+    out = torch.float32 if case % 2 == 0 else torch.bfloat16
+    contiguous = case % 3 == 0
+    Xin = Xd.index_select(0, tok.long()).contiguous() if contiguous else Xd
+    Y = torch.full((tok.numel(), N), float("nan"), dtype=out, device="cuda")
+    if launch:
+        M.moe_gemm_fp8(plan, Xin, None if contiguous else tok, Wd, torch.from_numpy(scale).cuda(), Y=Y)
+    torch.cuda.synchronize()
+    got = Y.cpu().double().numpy()
+    exp = ref if out == torch.float32 else torch.from_numpy(ref).to(torch.bfloat16).double().numpy()
+    assert np.array_equal(got, exp), f"case {case}: T={T} E={E} k={k} H={H} N={N} tile={bm}x{bn} flags={flags}"
