@@ -220,9 +220,12 @@ def host_pad(torch, ms: float = 2.0):
     torch.cuda._sleep(int(ms * 2.0e6))             # ~2e6 cycles per ms at the 1.9-2.0 GHz boost clock
 
 
-def route_launches(T: int, E: int) -> int:
-    """Kernels one moe_route(_plan) call launches (route.cu): histogram + fused scan/compaction
-    while chunks x experts <= 16384, else histogram + scan + compaction."""
+def route_launches(T: int, E: int, k: int = 2) -> int:
+    """Kernels one moe_route(_plan) call launches (route.cu): the single-block small-batch kernel
+    when T <= 1024, E <= 16, k <= 8; else histogram + fused scan/compaction while chunks x experts
+    <= 16384, else histogram + scan + compaction."""
+    if T <= 1024 and E <= 16 and k <= 8 and os.environ.get("MOE_ROUTE_SMALL", "1") != "0":
+        return 1
     chunks = max(1, -(-T // 1024))
     return 2 if chunks * E <= 16384 else 3
 
@@ -320,7 +323,7 @@ def run_ffn(args, cfg):
                     "combine_gbs": comb_bytes / (st["combine"] * 1e-3) / 1e9},
         "roofline": {"bound": "tensor", "achieved": gu, "peak": peak, "unit": "TFLOP/s", "frac": gu / peak,
                      "traffic": None, "kernel": "moe_gemm_kernel (gated)", "peak_source": peak_src},
-        "gpu_launches": (route_launches(cfg.T, E) + 1 + 1 + 1 + 2) * args.steps,
+        "gpu_launches": (route_launches(cfg.T, E, cfg.k) + 1 + 1 + 1 + 2) * args.steps,
         "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)
@@ -617,7 +620,7 @@ def run_ours(args, cfg):
                           "traffic_source": tsrc}),
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": (route_launches(cfg.T, cfg.E) + 1) * args.steps,   # route (+plan), GEMM
+            "gpu_launches": (route_launches(cfg.T, cfg.E, cfg.k) + 1) * args.steps,   # route (+plan), GEMM
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
