@@ -656,10 +656,18 @@ def run_ep(args, base):
     ids = synth.route(cfg, args.seed)               # the global batch (identical on every rank)
     T_l, El = T_total // ws, cfg.E // ws
     topk_l = torch.from_numpy(np.ascontiguousarray(ids[rank * T_l:(rank + 1) * T_l])).to(dev)
-    X_l = synth.counter_values_torch(args.seed, synth.workloads.STREAM_X, rank * T_l * cfg.H, T_l * cfg.H,
-                                     "normal", 6, dev).reshape(T_l, cfg.H)
-    W_l = synth.make_w_torch(args.seed, cfg.E, cfg.H, cfg.N, device=dev, experts=range(rank * El, (rank + 1) * El))
-    moe = ExpertParallelMoE(cfg.E, W_l, TorchComm(), bm=args.bm, bn=args.bn, out_dtype=out_dtype)
+    fp8 = args.dtype == "fp8"
+    if fp8:                                          # FP8 E4M3 rows and weights (synth/fp8.py, R15)
+        from synth import fp8 as sfp8
+        X_l = sfp8.make_x_fp8_torch(args.seed, T_l, cfg.H, device=dev, row0=rank * T_l)
+        W_l = sfp8.make_w_fp8_torch(args.seed, cfg.E, cfg.H, cfg.N, device=dev, experts=range(rank * El, (rank + 1) * El))
+        w_scale = torch.from_numpy(sfp8.w_scale(El, cfg.H)).to(dev)
+    else:
+        X_l = synth.counter_values_torch(args.seed, synth.workloads.STREAM_X, rank * T_l * cfg.H, T_l * cfg.H,
+                                         "normal", 6, dev).reshape(T_l, cfg.H)
+        W_l = synth.make_w_torch(args.seed, cfg.E, cfg.H, cfg.N, device=dev, experts=range(rank * El, (rank + 1) * El))
+        w_scale = None
+    moe = ExpertParallelMoE(cfg.E, W_l, TorchComm(), bm=args.bm, bn=args.bn, out_dtype=out_dtype, w_scale=w_scale)
     flush = L2Flush(torch, dev)
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
@@ -688,7 +696,7 @@ def run_ep(args, base):
     gemm_avg = statistics.mean(gemm_ms)
     flops_l = 2 * local_rows[-1] * cfg.H * cfg.N
     achieved = flops_l / (gemm_avg * 1e-3) / 1e12
-    peak = float(peaks["bf16_tflops"])
+    peak = float(peaks["bf16_tflops"]) * (2.0 if fp8 else 1.0)
     per_rank = torch.tensor([statistics.mean(step_ms), gemm_avg, achieved], device=dev)
     gathered = [torch.zeros_like(per_rank) for _ in range(ws)]
     dist.all_gather(gathered, per_rank)
@@ -716,13 +724,14 @@ def run_ep(args, base):
         te_max = torch.tensor([sum(e_ms)], device=dev)
         dist.all_reduce(te_max, op=dist.ReduceOp.MAX)
         e2e = {"value": cfg.flops * len(e_ms) / (float(te_max.item()) * 1e-3) / 1e12, "unit": "TFLOP/s",
-               "h2d_bytes_per_step": int(X_h.numel() * 2 + ids_h.numel() * 4) * ws,
+               "h2d_bytes_per_step": int(X_h.numel() * X_h.element_size() + ids_h.numel() * 4) * ws,
                "d2h_bytes_per_step": int(out_h.numel() * out_h.element_size()) * ws}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": float(t.item()) / args.steps, "higher_is_better": True,
-            "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "fp8_e4m3" if fp8 else "bf16",
+            "data": "synthetic",
             "config": {"workload": f"{cfg.name}: E={cfg.E} top-{cfg.k} T={cfg.T} ({T_l}/rank) H={cfg.H} N={cfg.N} "
                                    f"routing={cfg.routing} seed={args.seed}",
                        "tile": f"{moe.kernels._plans[('ep', args.bm, args.bn)].bm}x{moe.kernels._plans[('ep', args.bm, args.bn)].bn}",
@@ -734,11 +743,13 @@ def run_ep(args, base):
                          for g in gathered],
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": None,
-                         "peak_source": f"{peak_src} bf16_tflops (rank 0's GEMM launch)",
+                         "peak_source": f"{peak_src} bf16_tflops (rank 0's GEMM launch)"
+                                        + (" x 2 (nominal FP8 / BF16 dense ratio)" if fp8 else ""),
                          "algorithmic_flops_per_launch": flops_l},
             "cpu_baseline": None,
             "e2e": e2e,
-            "gpu_launches": 9 * args.steps,   # dispatch 2, gather 1, route 2, plan 1, combine map 1, GEMM 1, unpack 1
+            # dispatch 2, gather 1, route (1-3, on the received rows), plan 1, combine map 1, GEMM 1, unpack 1
+            "gpu_launches": (7 + route_launches(sum(moe.last["recv_rows"]), El, cfg.k)) * args.steps,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

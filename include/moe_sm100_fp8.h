@@ -39,6 +39,16 @@ extern "C" {
 moe_status moe_gemm_fp8(const moe_plan* plan, const void* X, int64_t T, const int32_t* token_idx, const void* W,
                         const float* scale, void* Y, int32_t y_dtype, void* stream);
 
+/*
+ * As moe_gemm_fp8, but CSR row i of the plan is stored at Y row y_row_map[i] (device int32
+ * [sum m_e], a permutation into Y's rows) — the expert-parallel combine send buffer
+ * (include/moe_sm100_ep.h, moe_ep_combine_map), as moe_gemm_rowmap does for bf16.
+ * Errors as moe_gemm_fp8, plus MOE_ERR_INVALID for a null y_row_map.
+ */
+moe_status moe_gemm_fp8_rowmap(const moe_plan* plan, const void* X, int64_t T, const int32_t* token_idx,
+                               const void* W, const float* scale, void* Y, int32_t y_dtype, const int32_t* y_row_map,
+                               void* stream);
+
 #ifdef __cplusplus
 }
 #endif

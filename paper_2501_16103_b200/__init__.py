@@ -33,7 +33,7 @@ EXPORTED = (
     "moe_decode_debug", "moe_device_info", "moe_last_error", "moe_version", "moe_probe_gather4",
     "moe_gemm_profile", "moe_plan_device", "moe_plan_sync", "moe_gemm_rowmap",
     "moe_ep_dispatch_plan", "moe_gather_rows", "moe_ep_combine_map", "moe_ep_unpack", "moe_route_plan",
-    "moe_gemm_swiglu", "moe_combine", "moe_gemm_fp8",
+    "moe_gemm_swiglu", "moe_combine", "moe_gemm_fp8", "moe_gemm_fp8_rowmap",
 )
 
 
@@ -91,6 +91,7 @@ def lib() -> ctypes.CDLL:
                                            ctypes.c_int64, vp, vp]),
         "moe_gemm_swiglu": (ctypes.c_int32, [vp, vp, ctypes.c_int64, vp, vp, vp, vp, ctypes.c_int32, vp]),
         "moe_gemm_fp8": (ctypes.c_int32, [vp, vp, ctypes.c_int64, vp, vp, vp, vp, ctypes.c_int32, vp]),
+        "moe_gemm_fp8_rowmap": (ctypes.c_int32, [vp, vp, ctypes.c_int64, vp, vp, vp, vp, ctypes.c_int32, vp, vp]),
         "moe_combine": (ctypes.c_int32, [vp, ctypes.c_int32, ctypes.c_int64, ctypes.c_int32, ctypes.c_int64, vp, vp,
                                          vp, ctypes.c_int32, vp, vp, ctypes.c_int32, vp]),
     }
@@ -291,10 +292,11 @@ def moe_gemm(plan: Plan, X, token_idx, W, Y=None, out_dtype=None, stream=None, r
     return Y
 
 
-def moe_gemm_fp8(plan: Plan, X, token_idx, W, scale=None, Y=None, out_dtype=None, stream=None):
+def moe_gemm_fp8(plan: Plan, X, token_idx, W, scale=None, Y=None, out_dtype=None, stream=None, row_map=None):
     """Y[sum m_e, N] = scale[e] * (X[token_idx] @ W[e]) on FP8 E4M3 X [T, H] and W [E, H, N]
     (torch.float8_e4m3fn or uint8 codes), fp32 accumulate, one launch (include/moe_sm100_fp8.h).
-    scale: [E] fp32 device tensor or None; token_idx None: X's rows are already in CSR order."""
+    scale: [E] fp32 device tensor or None; token_idx None: X's rows are already in CSR order;
+    row_map: Y row of CSR row i (moe_gemm_fp8_rowmap)."""
     import torch
 
     out_dtype = out_dtype or torch.bfloat16
@@ -309,9 +311,15 @@ def moe_gemm_fp8(plan: Plan, X, token_idx, W, scale=None, Y=None, out_dtype=None
     if Y is None:
         Y = torch.empty((rows, plan.N), dtype=out_dtype, device=X.device)
     yd = MOE_DTYPE_F32 if Y.dtype == torch.float32 else MOE_DTYPE_BF16
-    _check(lib().moe_gemm_fp8(plan.handle, X.data_ptr(), X.shape[0],
-                              token_idx.data_ptr() if token_idx is not None else None, W.data_ptr(),
-                              scale.data_ptr() if scale is not None else None, Y.data_ptr(), yd, _stream(stream)))
+    tp = token_idx.data_ptr() if token_idx is not None else None
+    sp = scale.data_ptr() if scale is not None else None
+    if row_map is None:
+        _check(lib().moe_gemm_fp8(plan.handle, X.data_ptr(), X.shape[0], tp, W.data_ptr(), sp, Y.data_ptr(), yd,
+                                  _stream(stream)))
+    else:
+        assert row_map.dtype == torch.int32 and row_map.is_contiguous()
+        _check(lib().moe_gemm_fp8_rowmap(plan.handle, X.data_ptr(), X.shape[0], tp, W.data_ptr(), sp, Y.data_ptr(),
+                                         yd, row_map.data_ptr(), _stream(stream)))
     return Y
 
 

@@ -1668,6 +1668,13 @@ moe_status moe_gemm_fp8(const moe_plan* plan, const void* X, int64_t T, const in
   return gemm_launch(plan, X, T, token_idx, W, Y, y_dtype, stream, nullptr, nullptr, nullptr, true, scale);
 }
 
+moe_status moe_gemm_fp8_rowmap(const moe_plan* plan, const void* X, int64_t T, const int32_t* token_idx,
+                               const void* W, const float* scale, void* Y, int32_t y_dtype, const int32_t* y_row_map,
+                               void* stream) {
+  if (!y_row_map) MOE_FAIL(MOE_ERR_INVALID, "moe_gemm_fp8_rowmap: null y_row_map");
+  return gemm_launch(plan, X, T, token_idx, W, Y, y_dtype, stream, nullptr, y_row_map, nullptr, true, scale);
+}
+
 moe_status moe_gemm_rowmap(const moe_plan* plan, const void* X, int64_t T, const int32_t* token_idx,
                            const void* W, void* Y, int32_t y_dtype, const int32_t* y_row_map, void* stream) {
   if (!y_row_map) MOE_FAIL(MOE_ERR_INVALID, "moe_gemm_rowmap: null y_row_map");

@@ -34,8 +34,8 @@ class CudaKernels:
 
     def __init__(self):
         from . import (Plan, moe_ep_combine_map, moe_ep_dispatch_plan, moe_ep_unpack, moe_gather_rows, moe_gemm,
-                       moe_route)
-        self._Plan, self._gemm, self._route = Plan, moe_gemm, moe_route
+                       moe_gemm_fp8, moe_route)
+        self._Plan, self._gemm, self._gemm_fp8, self._route = Plan, moe_gemm, moe_gemm_fp8, moe_route
         self.dispatch_plan = moe_ep_dispatch_plan
         self.gather_rows = moe_gather_rows
         self.combine_map = moe_ep_combine_map
@@ -46,14 +46,17 @@ class CudaKernels:
         counts, row_off, tok, slot, _ = self._route(ids, E)
         return counts, tok, slot
 
-    def gemm(self, key, counts, Xr, tok, W, Y, row_map, bm, bn):
+    def gemm(self, key, counts, Xr, tok, W, Y, row_map, bm, bn, scale=None):
         plan = self._plans.get(key)
         if plan is None:
             plan = self._Plan(None, W.shape[1], W.shape[2], bm, bn, E=W.shape[0])
             self._plans[key] = plan
         plan.update_device(counts)
         if tok.numel():
-            self._gemm(plan, Xr, tok, W, Y=Y, row_map=row_map)
+            if W.dtype in (torch.uint8, torch.float8_e4m3fn):     # FP8 E4M3 (include/moe_sm100_fp8.h)
+                self._gemm_fp8(plan, Xr, tok, W, scale, Y=Y, row_map=row_map)
+            else:
+                self._gemm(plan, Xr, tok, W, Y=Y, row_map=row_map)
         return Y
 
 
@@ -110,7 +113,10 @@ def _excl(x):
 class ExpertParallelMoE:
     """One rank of an expert-parallel MoE expert GEMM."""
 
-    def __init__(self, E: int, W_local, comm, bm: int = 0, bn: int = 0, out_dtype=torch.bfloat16, kernels=None):
+    def __init__(self, E: int, W_local, comm, bm: int = 0, bn: int = 0, out_dtype=torch.bfloat16, kernels=None,
+                 w_scale=None):
+        """W_local [E/G, H, N]: bf16, or FP8 E4M3 codes (uint8 / float8_e4m3fn) with the optional
+        per-local-expert fp32 w_scale [E/G]; X rows then travel as FP8 (half the dispatch bytes)."""
         self.comm = comm
         self.G = comm.size
         if E % self.G:
@@ -119,6 +125,7 @@ class ExpertParallelMoE:
         if W_local.shape[0] != self.El:
             raise ValueError("W_local must hold E / G experts")
         self.W = W_local
+        self.w_scale = w_scale
         self.bm, self.bn, self.out_dtype = bm, bn, out_dtype
         self.kernels = kernels if kernels is not None else CudaKernels()
         self.last = {}
@@ -126,7 +133,8 @@ class ExpertParallelMoE:
         self.gemm_events = None
 
     def forward(self, topk_local, X_local):
-        """topk_local [T_l, k] int32 global expert ids, X_local [T_l, H] bf16 -> out [T_l * k, N]."""
+        """topk_local [T_l, k] int32 global expert ids, X_local [T_l, H] bf16 (FP8 codes with FP8
+        weights) -> out [T_l * k, N]."""
         K, G, comm = self.kernels, self.G, self.comm
         dev = X_local.device
         T_l, k = topk_local.shape
@@ -154,7 +162,7 @@ class ExpertParallelMoE:
         if self.time_gemm:
             ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
             ev[0].record()
-        K.gemm(("ep", self.bm, self.bn), counts_l, Xr, tok_l, self.W, Ysend, row_map, self.bm, self.bn)
+        K.gemm(("ep", self.bm, self.bn), counts_l, Xr, tok_l, self.W, Ysend, row_map, self.bm, self.bn, self.w_scale)
         if self.time_gemm:
             ev[1].record()
             self.gemm_events = ev

@@ -106,16 +106,20 @@ def _codes_torch(seed, stream, start, count, mode, device):
     return encode_torch(c.to(torch.int32), SHIFT[mode])
 
 
-def make_x_fp8_torch(seed: int, T: int, H: int, mode: str = "normal", device="cpu"):
-    return _codes_torch(seed, STREAM_X, 0, T * H, mode, device).reshape(T, H)
+def make_x_fp8_torch(seed: int, T: int, H: int, mode: str = "normal", device="cpu", row0: int = 0):
+    """Rows [row0, row0 + T) of X (one expert-parallel rank's tokens when row0 > 0)."""
+    return _codes_torch(seed, STREAM_X, row0 * H, T * H, mode, device).reshape(T, H)
 
 
-def make_w_fp8_torch(seed: int, E: int, H: int, N: int, mode: str = "normal", device="cpu", chunk=1 << 26):
+def make_w_fp8_torch(seed: int, E: int, H: int, N: int, mode: str = "normal", device="cpu", chunk=1 << 26,
+                     experts: range | None = None):
+    """W [E, H, N] codes, or the contiguous expert range `experts` of it (one EP rank's share)."""
     import torch
 
-    total = E * H * N
+    ex = range(E) if experts is None else experts
+    start, total = ex.start * H * N, len(ex) * H * N
     out = torch.empty(total, dtype=torch.uint8, device=device)
     for s in range(0, total, chunk):
         n = min(chunk, total - s)
-        out[s:s + n] = _codes_torch(seed, STREAM_W, s, n, mode, device)
-    return out.reshape(E, H, N)
+        out[s:s + n] = _codes_torch(seed, STREAM_W, start + s, n, mode, device)
+    return out.reshape(len(ex), H, N)

@@ -52,12 +52,15 @@ class CpuKernels:
             ret_meta[pos] = (r - int(recv_off[s])) * k + int(slot[i])
         return row_map, ret_meta
 
-    def gemm(self, key, counts, Xr, tok, W, Y, row_map, bm, bn):
+    def gemm(self, key, counts, Xr, tok, W, Y, row_map, bm, bn, scale=None):
+        fp8 = W.dtype == torch.uint8                      # E4M3 codes (include/moe_sm100_fp8.h)
+        dec = (lambda a: a.view(torch.float8_e4m3fn).double()) if fp8 else (lambda a: a.double())
         row0 = 0
         for e in range(W.shape[0]):
             m = int(counts[e])
+            s = float(scale[e]) if scale is not None else 1.0
             for i in range(row0, row0 + m):
-                Y[int(row_map[i])] = (Xr[int(tok[i])].double() @ W[e].double()).to(Y.dtype)
+                Y[int(row_map[i])] = (s * (dec(Xr[int(tok[i])]) @ dec(W[e]))).to(Y.dtype)
             row0 += m
         return Y
 

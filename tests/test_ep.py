@@ -68,8 +68,24 @@ def test_ep_exchange_gloo_world2():
     assert last[0]["ret_rows"] == [last[g]["back_rows"][0] for g in range(2)]
 
 
-def _run_virtual(G, kernels_fn, device, out_dtype, E=8, k=2, T_l=12, H=16, N=24, seed=0):
-    ids, X, W, ref = _problem(G, E, k, T_l, H, N, seed)
+def _problem_fp8(G, E=8, k=2, T_l=12, H=16, N=24, seed=0):
+    """FP8 E4M3 integer codes (synth/fp8.py), per-expert power-of-two scales; reference = the P:90
+    per-(token, slot) definition on the decoded values (oracle/fp8.py), times the expert's scale."""
+    from oracle import fp8 as ofp8
+    from synth import fp8 as sfp8
+    T = G * T_l
+    ids = synth.route_gumbel(seed, T, E, k)
+    X, W = sfp8.make_x_fp8(seed, T, H, "int"), sfp8.make_w_fp8(seed, E, H, N, "int")
+    scale = (2.0 ** (np.arange(E) % 4 - 1)).astype(np.float32)
+    ref = omoe.per_slot_outputs(ids, ofp8.e4m3_decode(X), ofp8.e4m3_decode(W)) * scale[ids.reshape(-1)][:, None]
+    return ids, X, W, ref, scale
+
+
+def _run_virtual(G, kernels_fn, device, out_dtype, E=8, k=2, T_l=12, H=16, N=24, seed=0, fp8=False):
+    if fp8:
+        ids, X, W, ref, scale = _problem_fp8(G, E, k, T_l, H, N, seed)
+    else:
+        ids, X, W, ref = _problem(G, E, k, T_l, H, N, seed)
     El = E // G
     comm = ThreadComm(G)
     outs, errs = [None] * G, []
@@ -79,11 +95,15 @@ def _run_virtual(G, kernels_fn, device, out_dtype, E=8, k=2, T_l=12, H=16, N=24,
             comm.bind(r)
             Wl = torch.from_numpy(W[r * El:(r + 1) * El])
             Xl = torch.from_numpy(X[r * T_l:(r + 1) * T_l])
-            if device == "cuda":
+            sl = None
+            if fp8:                                            # uint8 E4M3 codes travel as they are
+                sl = torch.from_numpy(scale[r * El:(r + 1) * El]).to(device)
+                Wl, Xl = Wl.to(device), Xl.to(device)
+            elif device == "cuda":
                 Wl, Xl = Wl.to(torch.bfloat16).cuda(), Xl.to(torch.bfloat16).cuda()
             else:
                 Wl, Xl = Wl.float(), Xl.float()
-            moe = ExpertParallelMoE(E, Wl, comm, out_dtype=out_dtype, kernels=kernels_fn())
+            moe = ExpertParallelMoE(E, Wl, comm, out_dtype=out_dtype, kernels=kernels_fn(), w_scale=sl)
             outs[r] = moe.forward(torch.from_numpy(ids[r * T_l:(r + 1) * T_l]).to(device), Xl).cpu()
         except Exception as e:  # pragma: no cover
             errs.append(repr(e))
@@ -102,6 +122,22 @@ def _run_virtual(G, kernels_fn, device, out_dtype, E=8, k=2, T_l=12, H=16, N=24,
 @pytest.mark.parametrize("G", [1, 2, 4])
 def test_ep_exchange_virtual_ranks_cpu(G):
     got, ref = _run_virtual(G, _cpu_kernels, "cpu", torch.float32)
+    assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("G", [1, 2, 4])
+def test_ep_exchange_virtual_ranks_cpu_fp8(G):
+    """FP8 weights and token rows (E4M3 codes, per-expert scales) through the same exchange."""
+    got, ref = _run_virtual(G, _cpu_kernels, "cpu", torch.float32, fp8=True)
+    assert np.array_equal(got, ref)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("G", [1, 2, 4, 8])
+def test_ep_cuda_kernels_virtual_ranks_fp8(G):
+    """moe_gemm_fp8_rowmap in the expert-parallel path: FP8 rows dispatched, results combined."""
+    from paper_2501_16103_b200.ep import CudaKernels
+    got, ref = _run_virtual(G, CudaKernels, "cuda", torch.float32, E=8, k=2, T_l=40, H=64, N=256, fp8=True)
     assert np.array_equal(got, ref)
 
 
