@@ -48,6 +48,12 @@ moe_status moe_probe_gather4(const void* X_dev, int64_t T, int64_t H, const int3
 moe_status moe_gemm_profile(const moe_plan* plan, const void* X_dev, int64_t T, const int32_t* token_idx_dev,
                             const void* W_dev, void* Y_dev, int32_t y_dtype, long long* prof_dev, void* stream);
 
+/* The same counters for moe_gemm_fp8 (include/moe_sm100_fp8.h) on wide pair tiles (bm 256, bn 512);
+ * other tiles: MOE_ERR_UNSUPPORTED.  Y identical to moe_gemm_fp8. */
+moe_status moe_gemm_fp8_profile(const moe_plan* plan, const void* X_dev, int64_t T, const int32_t* token_idx_dev,
+                                const void* W_dev, const float* scale_dev, void* Y_dev, int32_t y_dtype,
+                                long long* prof_dev, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

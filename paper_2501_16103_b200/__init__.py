@@ -33,7 +33,7 @@ EXPORTED = (
     "moe_decode_debug", "moe_device_info", "moe_last_error", "moe_version", "moe_probe_gather4",
     "moe_gemm_profile", "moe_plan_device", "moe_plan_sync", "moe_gemm_rowmap",
     "moe_ep_dispatch_plan", "moe_gather_rows", "moe_ep_combine_map", "moe_ep_unpack", "moe_route_plan",
-    "moe_gemm_swiglu", "moe_combine", "moe_gemm_fp8", "moe_gemm_fp8_rowmap",
+    "moe_gemm_swiglu", "moe_combine", "moe_gemm_fp8", "moe_gemm_fp8_rowmap", "moe_gemm_fp8_profile",
 )
 
 
@@ -92,6 +92,7 @@ def lib() -> ctypes.CDLL:
         "moe_gemm_swiglu": (ctypes.c_int32, [vp, vp, ctypes.c_int64, vp, vp, vp, vp, ctypes.c_int32, vp]),
         "moe_gemm_fp8": (ctypes.c_int32, [vp, vp, ctypes.c_int64, vp, vp, vp, vp, ctypes.c_int32, vp]),
         "moe_gemm_fp8_rowmap": (ctypes.c_int32, [vp, vp, ctypes.c_int64, vp, vp, vp, vp, ctypes.c_int32, vp, vp]),
+        "moe_gemm_fp8_profile": (ctypes.c_int32, [vp, vp, ctypes.c_int64, vp, vp, vp, vp, ctypes.c_int32, vp, vp]),
         "moe_combine": (ctypes.c_int32, [vp, ctypes.c_int32, ctypes.c_int64, ctypes.c_int32, ctypes.c_int64, vp, vp,
                                          vp, ctypes.c_int32, vp, vp, ctypes.c_int32, vp]),
     }
@@ -397,8 +398,9 @@ PROF_SLOTS = ("mma_wait_tmem", "mma_wait_full", "mma_total", "prod_wait_empty", 
               "release", "stages")
 
 
-def moe_gemm_profile(plan: Plan, X, token_idx, W, Y, stream=None):
-    """Instrumented moe_gemm: returns Y and per-CTA cycle counters [grid, 8] (see moe_sm100_debug.h)."""
+def moe_gemm_profile(plan: Plan, X, token_idx, W, Y, stream=None, scale=None):
+    """Instrumented moe_gemm (FP8 X / W: moe_gemm_fp8_profile): returns Y and per-CTA cycle counters
+    [grid, 16] (see moe_sm100_debug.h)."""
     import torch
 
     n_sm = moe_device_info()[0]
@@ -406,8 +408,13 @@ def moe_gemm_profile(plan: Plan, X, token_idx, W, Y, stream=None):
     grid = min(total, n_sm) if plan.bm == 128 else 2 * min(total, n_sm // 2)
     prof = torch.zeros((max(grid, 1), len(PROF_SLOTS)), dtype=torch.int64, device=X.device)
     yd = MOE_DTYPE_F32 if Y.dtype == torch.float32 else MOE_DTYPE_BF16
-    _check(lib().moe_gemm_profile(plan.handle, X.data_ptr(), X.shape[0], token_idx.data_ptr(), W.data_ptr(),
-                                  Y.data_ptr(), yd, prof.data_ptr(), _stream(stream)))
+    if X.dtype in (torch.uint8, torch.float8_e4m3fn):
+        _check(lib().moe_gemm_fp8_profile(plan.handle, X.data_ptr(), X.shape[0], token_idx.data_ptr(), W.data_ptr(),
+                                          scale.data_ptr() if scale is not None else None, Y.data_ptr(), yd,
+                                          prof.data_ptr(), _stream(stream)))
+    else:
+        _check(lib().moe_gemm_profile(plan.handle, X.data_ptr(), X.shape[0], token_idx.data_ptr(), W.data_ptr(),
+                                      Y.data_ptr(), yd, prof.data_ptr(), _stream(stream)))
     return Y, prof[:grid]
 
 

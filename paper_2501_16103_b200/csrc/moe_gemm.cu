@@ -303,7 +303,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int kCS = kFp8 ? 7 : 6;                        // log2(W columns per box)
   constexpr int kBox = kFp8 ? 128 * 128 : kBBoxBytes;
   constexpr int kKStep = kFp8 ? 4096 : 2048;
-  static_assert(!kFp8 || (!kSplit && !kGated && !kProf), "FP8: plain and wide tiles");
+  static_assert(!kFp8 || (!kSplit && !kGated), "FP8: plain and wide tiles");
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;            // SW128 atoms need 1024-byte alignment
@@ -1424,9 +1424,9 @@ cudaError_t set_smem_attrs() {
   static std::once_flag once;
   static cudaError_t err = cudaSuccess;
   std::call_once(once, [] {
-    cudaError_t e[15] = {set_attr<false, 1, false>(),      set_attr<true, 1, false>(),
+    cudaError_t e[16] = {set_attr<false, 1, false>(),      set_attr<true, 1, false>(),
                         set_attr<false, 1, false, false, false, true>(), set_attr<false, 2, false, false, false, true>(),
-                        set_attr<false, 2, false, true, false, true>(),
+                        set_attr<false, 2, false, true, false, true>(), set_attr<true, 2, false, true, false, true>(),
                         set_attr<false, 2, false>(),      set_attr<true, 2, false>(),
                         set_attr<false, 2, true>(),       set_attr<true, 2, true>(),
                         set_attr<false, 2, false, true>(), set_attr<true, 2, false, true>(),
@@ -1486,7 +1486,9 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
   if (fp8) {
     // FP8 E4M3 (moe_gemm_fp8): 1-CTA tiles (bn % 128 == 0) and CTA-pair / wide tiles whose CTA
     // blocks are 128 columns (bn = 256 or 512); TMA strides need 16-byte rows.
-    if (prof || W2) MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_gemm_fp8: no profiling / gated variant");
+    if (W2) MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_gemm_fp8: no gated variant");
+    if (prof && !(v.bm == 256 && v.bn > 256))
+      MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_gemm_fp8_profile: instrumented for wide pair tiles only");
     if (v.bm == kDecRows || (v.flags & MOE_SPLIT_TAIL))
       MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_gemm_fp8: bm = 64 decode tiles and MOE_SPLIT_TAIL plans are bf16-only");
     const bool ok_tile = v.bm == 128 ? v.bn % 128 == 0 : (v.bn == 256 || v.bn == 512);
@@ -1604,7 +1606,8 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
     cfg.numAttrs = 2;
     cudaError_t le;
     if (fp8 && wide)
-      le = cudaLaunchKernelEx(&cfg, moe_gemm_kernel<false, 2, false, true, false, true>, tmX, tmW, tmW2, tmY, a);
+      le = prof ? cudaLaunchKernelEx(&cfg, moe_gemm_kernel<true, 2, false, true, false, true>, tmX, tmW, tmW2, tmY, a)
+                : cudaLaunchKernelEx(&cfg, moe_gemm_kernel<false, 2, false, true, false, true>, tmX, tmW, tmW2, tmY, a);
     else if (fp8)
       le = cudaLaunchKernelEx(&cfg, moe_gemm_kernel<false, 2, false, false, false, true>, tmX, tmW, tmW2, tmY, a);
     else if (gated)
@@ -1685,6 +1688,13 @@ moe_status moe_gemm_profile(const moe_plan* plan, const void* X, int64_t T, cons
                             const void* W, void* Y, int32_t y_dtype, long long* prof_dev, void* stream) {
   if (!prof_dev) MOE_FAIL(MOE_ERR_INVALID, "moe_gemm_profile: null prof_dev");
   return gemm_launch(plan, X, T, token_idx, W, Y, y_dtype, stream, prof_dev);
+}
+
+moe_status moe_gemm_fp8_profile(const moe_plan* plan, const void* X, int64_t T, const int32_t* token_idx,
+                                const void* W, const float* scale, void* Y, int32_t y_dtype, long long* prof_dev,
+                                void* stream) {
+  if (!prof_dev) MOE_FAIL(MOE_ERR_INVALID, "moe_gemm_fp8_profile: null prof_dev");
+  return gemm_launch(plan, X, T, token_idx, W, Y, y_dtype, stream, prof_dev, nullptr, nullptr, true, scale);
 }
 
 moe_status moe_decode_debug(const moe_plan* plan, int32_t* out, void* stream) {

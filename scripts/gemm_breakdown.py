@@ -22,19 +22,27 @@ def main():
     bn = int(sys.argv[2]) if len(sys.argv) > 2 else 256
     bm = int(sys.argv[3]) if len(sys.argv) > 3 else 128
     flags = int(sys.argv[4]) if len(sys.argv) > 4 else 0
+    fp8 = os.environ.get("FP8", "0") == "1"          # FP8 E4M3 operands (moe_gemm_fp8)
     c = synth.CONFIGS[name]
     ids = torch.from_numpy(synth.route(c, 0)).cuda()
-    X = synth.make_x_torch(0, c.T, c.H, device="cuda")
-    W = synth.make_w_torch(0, c.E, c.H, c.N, device="cuda")
+    if fp8:
+        from synth import fp8 as sfp8
+        X = sfp8.make_x_fp8_torch(0, c.T, c.H, device="cuda")
+        W = sfp8.make_w_fp8_torch(0, c.E, c.H, c.N, device="cuda")
+        gemm = M.moe_gemm_fp8
+    else:
+        X = synth.make_x_torch(0, c.T, c.H, device="cuda")
+        W = synth.make_w_torch(0, c.E, c.H, c.N, device="cuda")
+        gemm = M.moe_gemm
     counts, row_off, tok, _, _ = M.moe_route(ids, c.E)
     plan = M.Plan(counts.cpu().numpy(), c.H, c.N, bm, bn, flags)
     Y = torch.empty((tok.numel(), c.N), dtype=torch.bfloat16, device="cuda")
     for _ in range(3):
-        M.moe_gemm(plan, X, tok, W, Y=Y)
+        gemm(plan, X, tok, W, Y=Y)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     ev[0].record()
     for _ in range(10):
-        M.moe_gemm(plan, X, tok, W, Y=Y)
+        gemm(plan, X, tok, W, Y=Y)
     ev[1].record()
     torch.cuda.synchronize()
     t_plain = ev[0].elapsed_time(ev[1]) / 10
@@ -57,7 +65,7 @@ def main():
         th = threading.Thread(target=sample)
         th.start()
         for _ in range(n_launch):
-            M.moe_gemm(plan, X, tok, W, Y=Y)
+            gemm(plan, X, tok, W, Y=Y)
         torch.cuda.synchronize()
         th.join()
         sm_mhz = sorted(samples)[len(samples) // 2] if samples else None
@@ -74,7 +82,7 @@ def main():
     p = pall[0::2] if bm == 256 else pall           # MMA counters live in the pair leaders
     tot = p[:, 2]
     out = {
-        "config": name, "bn": bn, "bm": bm, "flags": flags, "tiles": plan.total_tiles, "ms_plain": t_plain, "ms_instrumented": t_prof,
+        "config": name, "fp8": fp8, "bn": bn, "bm": bm, "flags": flags, "tiles": plan.total_tiles, "ms_plain": t_plain, "ms_instrumented": t_prof,
         "tflops_plain": c.flops / t_plain / 1e9, "sm_mhz_plain": sm_mhz,
         "tensor_frac_at_clock": (c.flops / t_plain / 1e9) / (148 * 8192 * sm_mhz * 1e-6) if sm_mhz else None,
         "identical_Y": bool(torch.equal(Y, Y2)),
