@@ -667,11 +667,20 @@ def run_ep(args, base):
                                          "normal", 6, dev).reshape(T_l, cfg.H)
         W_l = synth.make_w_torch(args.seed, cfg.E, cfg.H, cfg.N, device=dev, experts=range(rank * El, (rank + 1) * El))
         w_scale = None
+    native = None
+    if not args.ep_python:                           # the library's moe_ep_* step (NCCL from C++)
+        uid = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(M.moe_ep_unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, 0)
+        native = M.NativeExpertParallel(bytes(uid.cpu().numpy().tobytes()), rank, ws, cfg.E, W_l, w_scale=w_scale,
+                                        bm=args.bm, bn=args.bn)
     moe = ExpertParallelMoE(cfg.E, W_l, TorchComm(), bm=args.bm, bn=args.bn, out_dtype=out_dtype, w_scale=w_scale)
     flush = L2Flush(torch, dev)
     stream = torch.cuda.current_stream()
+    fwd = (lambda t, x: native.forward(t, x, out_dtype=out_dtype)) if native is not None else moe.forward
     for _ in range(args.warmup):
-        moe.forward(topk_l, X_l)
+        fwd(topk_l, X_l)
     torch.cuda.synchronize()
     moe.time_gemm = True
     step_ms, gemm_ms, local_rows = [], [], []
@@ -682,12 +691,16 @@ def run_ep(args, base):
             flush()
             s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s0.record(stream)
-            moe.forward(topk_l, X_l)
+            fwd(topk_l, X_l)
             s1.record(stream)
             s1.synchronize()
             step_ms.append(s0.elapsed_time(s1))
-            gemm_ms.append(moe.gemm_events[0].elapsed_time(moe.gemm_events[1]))
-            local_rows.append(moe.last["local_rows"])
+            if native is None:
+                gemm_ms.append(moe.gemm_events[0].elapsed_time(moe.gemm_events[1]))
+                local_rows.append(moe.last["local_rows"])
+            else:                                    # events the library records around its GEMM launch
+                gemm_ms.append(native.last_gemm_ms())
+                local_rows.append(native.last_rows()["local_rows"])
     torch.cuda.synchronize()
     dist.barrier()
     t = torch.tensor([sum(step_ms)], device=dev)
@@ -705,7 +718,7 @@ def run_ep(args, base):
     if not args.no_e2e:
         X_h = X_l.cpu().pin_memory()
         ids_h = topk_l.cpu().pin_memory()
-        out0 = moe.forward(topk_l, X_l)
+        out0 = fwd(topk_l, X_l)
         out_h = torch.empty(out0.shape, dtype=out0.dtype).pin_memory()
         Xe, te = torch.empty_like(X_l), torch.empty_like(topk_l)
         e_ms = []
@@ -716,7 +729,7 @@ def run_ep(args, base):
             s0.record(stream)
             Xe.copy_(X_h, non_blocking=True)
             te.copy_(ids_h, non_blocking=True)
-            out_h.copy_(moe.forward(te, Xe), non_blocking=True)
+            out_h.copy_(fwd(te, Xe), non_blocking=True)
             s1.record(stream)
             s1.synchronize()
             if i >= 2:
@@ -726,6 +739,8 @@ def run_ep(args, base):
         e2e = {"value": cfg.flops * len(e_ms) / (float(te_max.item()) * 1e-3) / 1e12, "unit": "TFLOP/s",
                "h2d_bytes_per_step": int(X_h.numel() * X_h.element_size() + ids_h.numel() * 4) * ws,
                "d2h_bytes_per_step": int(out_h.numel() * out_h.element_size()) * ws}
+    probe = M.Plan(None, cfg.H, cfg.N, args.bm, args.bn, E=El)     # the local GEMM's resolved tile shape
+    tile_ep = f"{probe.bm}x{probe.bn}"
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": ws, "steps": args.steps,
@@ -734,22 +749,26 @@ def run_ep(args, base):
             "data": "synthetic",
             "config": {"workload": f"{cfg.name}: E={cfg.E} top-{cfg.k} T={cfg.T} ({T_l}/rank) H={cfg.H} N={cfg.N} "
                                    f"routing={cfg.routing} seed={args.seed}",
-                       "tile": f"{moe.kernels._plans[('ep', args.bm, args.bn)].bm}x{moe.kernels._plans[('ep', args.bm, args.bn)].bn}",
+                       "tile": tile_ep,
                        "out_dtype": args.out_dtype, "global_batch": cfg.T, "parallelism": f"ep{ws}",
-                       "collectives": "NCCL all_to_all_single (torch.distributed): counts, dispatch rows, "
-                                      "combine rows", "l2": "flushed before every timed step (memset + read: clean L2)"},
+                       "collectives": ("NCCL grouped send/recv from the library (moe_ep_forward): counts, "
+                                       "dispatch rows, combine rows") if native is not None else
+                                      ("NCCL all_to_all_single (torch.distributed): counts, dispatch rows, "
+                                       "combine rows"), "l2": "flushed before every timed step (memset + read: clean L2)"},
             "pct_of_peak": value / (peak * ws),
             "per_rank": [{"ms_per_step": float(g[0]), "gemm_ms": float(g[1]), "gemm_tflops": float(g[2])}
                          for g in gathered],
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": None,
-                         "peak_source": f"{peak_src} bf16_tflops (rank 0's GEMM launch)"
+                         "peak_source": f"{peak_src} bf16_tflops (rank 0's GEMM launch"
+                                        + ("; moe_ep_forward's events around its GEMM launch)" if native else ")")
                                         + (" x 2 (nominal FP8 / BF16 dense ratio)" if fp8 else ""),
                          "algorithmic_flops_per_launch": flops_l},
             "cpu_baseline": None,
             "e2e": e2e,
             # dispatch 2, gather 1, route (1-3, on the received rows), plan 1, combine map 1, GEMM 1, unpack 1
-            "gpu_launches": (7 + route_launches(sum(moe.last["recv_rows"]), El, cfg.k)) * args.steps,
+            "gpu_launches": (7 + route_launches(native.last_rows()["received"] if native is not None
+                                                else sum(moe.last["recv_rows"]), El, cfg.k)) * args.steps,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -767,6 +786,9 @@ def main():
     ap.add_argument("--bn", type=int, default=0)
     ap.add_argument("--bm", type=int, default=0, help="tile rows: 128 (1 CTA), 256 (CTA pair), 0 = planner's choice")
     ap.add_argument("--out-dtype", choices=["bf16", "f32"], default="bf16")
+    ap.add_argument("--ep-python", action="store_true",
+                    help="expert parallelism orchestrated in Python over torch.distributed all_to_all_single "
+                         "(default: the library's moe_ep_forward, NCCL called from C++)")
     ap.add_argument("--order", choices=list(ORDER_FLAGS), default="natural",
                     help="sigma order of the plan's tasks (P:317-322 expert ordering; DESIGN.md R7)")
     ap.add_argument("--dtype", choices=["bf16", "fp8"], default="bf16",
@@ -788,7 +810,7 @@ def main():
         run_reference(args, cfg)
     elif args.ffn:
         run_ffn(args, cfg)
-    elif ws > 1 or args.ep:
+    elif ws > 1 or args.ep or args.ep_python:
         run_ep(args, cfg)
     else:
         run_ours(args, cfg)

@@ -62,6 +62,53 @@ moe_status moe_ep_unpack(const void* rows_dev, const int32_t* ret_meta_dev, int6
                          const int32_t* send_off_dev, const int32_t* send_tok_dev, int32_t G, int32_t k,
                          int64_t row_bytes, void* out_dev, void* stream);
 
+/* ------------------------------------------------------------------------------------------
+ * The whole expert-parallel step in the library (SURVEY §8(b) moe_ep_*): NCCL is called from
+ * C++ (libnccl.so.2 resolved at run time with dlopen — the one the process already loaded, e.g.
+ * PyTorch's; no link-time dependency); the host only bootstraps the 128-byte unique id.
+ * Per step, on `stream`: moe_ep_dispatch_plan -> grouped ncclSend/ncclRecv of the 2-int counts
+ * -> ONE stream synchronisation (the split sizes, as the all-to-all-v needs them on the host) ->
+ * moe_gather_rows + grouped send/recv of rows and local-id metadata -> moe_route + moe_plan_device
+ * on the received rows -> moe_ep_combine_map -> moe_gemm_rowmap / moe_gemm_fp8_rowmap into the
+ * combine send buffer -> grouped send/recv of result rows + metadata -> moe_ep_unpack.
+ * Scratch is stream-ordered (cudaMallocAsync / cudaFreeAsync); the handle owns the NCCL
+ * communicator, a device plan for the local experts and pinned host staging.
+ * ------------------------------------------------------------------------------------------ */
+#define MOE_DTYPE_E4M3 2          /* x_dtype of moe_ep_forward: FP8 E4M3 rows and weights */
+
+typedef struct moe_ep moe_ep;     /* opaque, library-owned */
+
+/* Writes a fresh NCCL unique id (128 bytes) to id_out (host); rank 0 calls it, the caller
+ * broadcasts it.  MOE_ERR_NCCL when libnccl.so.2 cannot be loaded or fails. */
+moe_status moe_ep_unique_id(void* id_out);
+
+/* Collective over `world` ranks (blocking until all joined): communicator for this rank.
+ * E % world == 0 experts; rank g owns experts [g E/world, (g+1) E/world).  bm / bn: the local
+ * GEMM's tile shape (0: the planner's choice).  The calling thread's current CUDA device is used. */
+moe_status moe_ep_create(const void* unique_id, int32_t rank, int32_t world, int32_t E, int32_t bm, int32_t bn,
+                         moe_ep** out);
+
+/*
+ * One step.  topk_dev [T, k] int32 global expert ids of this rank's T tokens (negative = masked);
+ * X_dev [T, H] (x_dtype MOE_DTYPE_BF16 or MOE_DTYPE_E4M3); W_dev [E/world, H, N] of the same
+ * type (this rank's experts); w_scale_dev [E/world] fp32 (E4M3 only, nullable);
+ * out_dev [T k, N] of out_dtype (MOE_DTYPE_BF16 / MOE_DTYPE_F32): out[t k + j] = the product of
+ * token t with expert topk[t, j] (rows of masked slots are not written).
+ * Returns MOE_OK, MOE_ERR_INVALID, MOE_ERR_UNSUPPORTED (as the GEMMs), MOE_ERR_CUDA, MOE_ERR_NCCL.
+ */
+moe_status moe_ep_forward(moe_ep* ep, const int32_t* topk_dev, int64_t T, int32_t k, const void* X_dev, int64_t H,
+                          int32_t x_dtype, const void* W_dev, int64_t N, const float* w_scale_dev, void* out_dev,
+                          int32_t out_dtype, void* stream);
+
+/* Row counts of the last step: sent (dispatch), received (dispatch), local expert rows (GEMM). */
+moe_status moe_ep_last_rows(const moe_ep* ep, int64_t* sent, int64_t* received, int64_t* local_rows);
+
+/* Device time of the last step's GEMM launch (CUDA events recorded around it on the step's
+ * stream; waits for the second one).  MOE_OK_EMPTY (0 ms) when the rank had no local rows. */
+moe_status moe_ep_last_gemm_ms(const moe_ep* ep, float* ms);
+
+void moe_ep_destroy(moe_ep* ep);
+
 #ifdef __cplusplus
 }
 #endif

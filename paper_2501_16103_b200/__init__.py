@@ -19,7 +19,7 @@ LIB_PATH = os.environ.get("MOE_LIB") or os.path.join(HERE, "libmoe_sm100.so")
 
 MOE_OK, MOE_OK_EMPTY = 0, 1
 MOE_ERR = {-1: "INVALID", -2: "UNSUPPORTED", -3: "CAPACITY", -4: "CUDA", -5: "NCCL"}
-MOE_DTYPE_BF16, MOE_DTYPE_F32 = 0, 1
+MOE_DTYPE_BF16, MOE_DTYPE_F32, MOE_DTYPE_E4M3 = 0, 1, 2
 MOE_PAD_MAX, MOE_PAD_REPEAT, MOE_SPLIT_TAIL = 0, 1, 2
 MOE_ORDER_ALTERNATING, MOE_ORDER_HALF_INTERVAL = 4, 8
 MOE_PLAN_MAGIC = 0x4D4F4531
@@ -34,6 +34,8 @@ EXPORTED = (
     "moe_gemm_profile", "moe_plan_device", "moe_plan_sync", "moe_gemm_rowmap",
     "moe_ep_dispatch_plan", "moe_gather_rows", "moe_ep_combine_map", "moe_ep_unpack", "moe_route_plan",
     "moe_gemm_swiglu", "moe_combine", "moe_gemm_fp8", "moe_gemm_fp8_rowmap", "moe_gemm_fp8_profile",
+    "moe_ep_unique_id", "moe_ep_create", "moe_ep_forward", "moe_ep_last_rows", "moe_ep_last_gemm_ms",
+    "moe_ep_destroy",
 )
 
 
@@ -93,6 +95,14 @@ def lib() -> ctypes.CDLL:
         "moe_gemm_fp8": (ctypes.c_int32, [vp, vp, ctypes.c_int64, vp, vp, vp, vp, ctypes.c_int32, vp]),
         "moe_gemm_fp8_rowmap": (ctypes.c_int32, [vp, vp, ctypes.c_int64, vp, vp, vp, vp, ctypes.c_int32, vp, vp]),
         "moe_gemm_fp8_profile": (ctypes.c_int32, [vp, vp, ctypes.c_int64, vp, vp, vp, vp, ctypes.c_int32, vp, vp]),
+        "moe_ep_unique_id": (ctypes.c_int32, [vp]),
+        "moe_ep_create": (ctypes.c_int32, [vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                           ctypes.c_int32, ctypes.POINTER(vp)]),
+        "moe_ep_forward": (ctypes.c_int32, [vp, vp, ctypes.c_int64, ctypes.c_int32, vp, ctypes.c_int64,
+                                            ctypes.c_int32, vp, ctypes.c_int64, vp, vp, ctypes.c_int32, vp]),
+        "moe_ep_last_rows": (ctypes.c_int32, [vp, c_i64p, c_i64p, c_i64p]),
+        "moe_ep_last_gemm_ms": (ctypes.c_int32, [vp, ctypes.POINTER(ctypes.c_float)]),
+        "moe_ep_destroy": (None, [vp]),
         "moe_combine": (ctypes.c_int32, [vp, ctypes.c_int32, ctypes.c_int64, ctypes.c_int32, ctypes.c_int64, vp, vp,
                                          vp, ctypes.c_int32, vp, vp, ctypes.c_int32, vp]),
     }
@@ -522,3 +532,61 @@ def moe_forward(topk_ids, X, W, E: int, bm: int = 0, bn: int = 0, out_dtype=None
     else:
         Y = moe_gemm(plan, X, token_idx, W, Y=Y, out_dtype=out_dtype or torch.bfloat16, stream=stream)
     return Y, counts_out, row_off, token_idx, slot, plan
+
+
+# ---------------------------------------------------------------------------
+# the expert-parallel step in the library (include/moe_sm100_ep.h, moe_ep_*: NCCL from C++)
+# ---------------------------------------------------------------------------
+def moe_ep_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().moe_ep_unique_id(buf))
+    return buf.raw
+
+
+class NativeExpertParallel:
+    """One rank of the library's expert-parallel step (moe_ep_create / moe_ep_forward).
+    unique_id: 128 bytes from moe_ep_unique_id() on rank 0, shared by the caller."""
+
+    def __init__(self, unique_id: bytes, rank: int, world: int, E: int, W_local, w_scale=None, bm: int = 0,
+                 bn: int = 0):
+        import torch
+
+        assert len(unique_id) == 128
+        self.W, self.w_scale, self.E, self.world = W_local, w_scale, E, world
+        self.fp8 = W_local.dtype in (torch.uint8, torch.float8_e4m3fn)
+        self._h = ctypes.c_void_p()
+        _check(lib().moe_ep_create(ctypes.create_string_buffer(unique_id, 128), rank, world, E, bm, bn,
+                                   ctypes.byref(self._h)))
+
+    def forward(self, topk_local, X_local, out=None, out_dtype=None, stream=None):
+        import torch
+
+        out_dtype = out_dtype or torch.bfloat16
+        T, k = topk_local.shape
+        N = self.W.shape[2]
+        assert X_local.is_contiguous() and topk_local.dtype == torch.int32 and topk_local.is_contiguous()
+        if out is None:
+            out = torch.empty((T * k, N), dtype=out_dtype, device=X_local.device)
+        _check(lib().moe_ep_forward(self._h, topk_local.data_ptr(), T, k, X_local.data_ptr(), X_local.shape[1],
+                                    MOE_DTYPE_E4M3 if self.fp8 else MOE_DTYPE_BF16, self.W.data_ptr(), N,
+                                    self.w_scale.data_ptr() if self.w_scale is not None else None, out.data_ptr(),
+                                    MOE_DTYPE_F32 if out.dtype == torch.float32 else MOE_DTYPE_BF16,
+                                    _stream(stream)))
+        return out
+
+    def last_gemm_ms(self) -> float:
+        """Device time of the last step's GEMM launch (0 when this rank had no local rows)."""
+        ms = ctypes.c_float()
+        _check(lib().moe_ep_last_gemm_ms(self._h, ctypes.byref(ms)))
+        return float(ms.value)
+
+    def last_rows(self):
+        a, b, c = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        _check(lib().moe_ep_last_rows(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
+        return {"sent": a.value, "received": b.value, "local_rows": c.value}
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and _lib is not None:
+            _lib.moe_ep_destroy(h)
+            self._h = None

@@ -20,7 +20,7 @@ NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_SOURCES = ["moe_gemm.cu", "route.cu", "plan_device.cu", "ep.cu", "ffn.cu"]
-CPP_SOURCES = ["plan.cpp"]
+CPP_SOURCES = ["plan.cpp", "ep_nccl.cpp"]
 HEADERS = ["common.h", "sm100_ptx.cuh", "plan_body.cuh"]
 
 

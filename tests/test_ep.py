@@ -175,3 +175,27 @@ def test_ep_nccl_world1():
         assert np.array_equal(out.cpu().double().numpy(), ref)
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("fp8", [False, True])
+@pytest.mark.parametrize("bm,bn", [(0, 0), (128, 256)])
+def test_ep_native_nccl_world1(fp8, bm, bn):
+    """The library's own expert-parallel step (moe_ep_create / moe_ep_forward: NCCL called from C++,
+    a one-rank communicator on one GPU) against the P:90 definition, and equal to the Python path."""
+    import paper_2501_16103_b200 as M
+    E, k, T, H, N = 8, 2, 300, 64, 256
+    if fp8:
+        ids, X, W, ref, scale = _problem_fp8(1, E, k, T, H, N, seed=4)
+        Xd, Wd, sc = torch.from_numpy(X).cuda(), torch.from_numpy(W).cuda(), torch.from_numpy(scale).cuda()
+    else:
+        ids, X, W, ref = _problem(1, E, k, T, H, N, seed=4)
+        Xd, Wd, sc = torch.from_numpy(X).to(torch.bfloat16).cuda(), torch.from_numpy(W).to(torch.bfloat16).cuda(), None
+    ep = M.NativeExpertParallel(M.moe_ep_unique_id(), 0, 1, E, Wd, w_scale=sc, bm=bm, bn=bn)
+    topk = torch.from_numpy(ids).cuda()
+    for _ in range(2):                                   # the plan and the communicator are reused
+        out = ep.forward(topk, Xd, out_dtype=torch.float32)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().double().numpy(), ref)
+    assert ep.last_rows() == {"sent": T, "received": T, "local_rows": T * k}
+    assert ep.last_gemm_ms() > 0
