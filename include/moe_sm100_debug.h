@@ -54,6 +54,14 @@ moe_status moe_gemm_fp8_profile(const moe_plan* plan, const void* X_dev, int64_t
                                 const void* W_dev, const float* scale_dev, void* Y_dev, int32_t y_dtype,
                                 long long* prof_dev, void* stream);
 
+/* Test transport for the library's expert-parallel step (include/moe_sm100_ep.h): `world`
+ * handles (eps_out[world]) of one process and device that exchange rows with device copies
+ * instead of NCCL, so the multi-rank orchestration of moe_ep_forward runs on one GPU.  Rank r's
+ * moe_ep_forward must be called from its own host thread with its own stream, all ranks
+ * concurrently (each exchange is a rendezvous of all `world` threads).  moe_ep_destroy each. */
+typedef struct moe_ep moe_ep;
+moe_status moe_ep_create_loopback(int32_t world, int32_t E, int32_t bm, int32_t bn, moe_ep** eps_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -35,7 +35,7 @@ EXPORTED = (
     "moe_ep_dispatch_plan", "moe_gather_rows", "moe_ep_combine_map", "moe_ep_unpack", "moe_route_plan",
     "moe_gemm_swiglu", "moe_combine", "moe_gemm_fp8", "moe_gemm_fp8_rowmap", "moe_gemm_fp8_profile",
     "moe_ep_unique_id", "moe_ep_create", "moe_ep_forward", "moe_ep_last_rows", "moe_ep_last_gemm_ms",
-    "moe_ep_destroy",
+    "moe_ep_destroy", "moe_ep_create_loopback",
 )
 
 
@@ -102,6 +102,8 @@ def lib() -> ctypes.CDLL:
                                             ctypes.c_int32, vp, ctypes.c_int64, vp, vp, ctypes.c_int32, vp]),
         "moe_ep_last_rows": (ctypes.c_int32, [vp, c_i64p, c_i64p, c_i64p]),
         "moe_ep_last_gemm_ms": (ctypes.c_int32, [vp, ctypes.POINTER(ctypes.c_float)]),
+        "moe_ep_create_loopback": (ctypes.c_int32, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                                    ctypes.POINTER(vp)]),
         "moe_ep_destroy": (None, [vp]),
         "moe_combine": (ctypes.c_int32, [vp, ctypes.c_int32, ctypes.c_int64, ctypes.c_int32, ctypes.c_int64, vp, vp,
                                          vp, ctypes.c_int32, vp, vp, ctypes.c_int32, vp]),
@@ -548,15 +550,27 @@ class NativeExpertParallel:
     unique_id: 128 bytes from moe_ep_unique_id() on rank 0, shared by the caller."""
 
     def __init__(self, unique_id: bytes, rank: int, world: int, E: int, W_local, w_scale=None, bm: int = 0,
-                 bn: int = 0):
+                 bn: int = 0, handle=None):
         import torch
 
-        assert len(unique_id) == 128
         self.W, self.w_scale, self.E, self.world = W_local, w_scale, E, world
         self.fp8 = W_local.dtype in (torch.uint8, torch.float8_e4m3fn)
+        if handle is not None:                     # from loopback_group (test transport)
+            self._h = handle
+            return
+        assert len(unique_id) == 128
         self._h = ctypes.c_void_p()
         _check(lib().moe_ep_create(ctypes.create_string_buffer(unique_id, 128), rank, world, E, bm, bn,
                                    ctypes.byref(self._h)))
+
+    @staticmethod
+    def loopback_group(world: int, E: int, W_locals, w_scales=None, bm: int = 0, bn: int = 0):
+        """`world` virtual ranks on one device exchanging by device copies (moe_ep_create_loopback,
+        include/moe_sm100_debug.h); call each rank's forward from its own thread and stream."""
+        hs = (ctypes.c_void_p * world)()
+        _check(lib().moe_ep_create_loopback(world, E, bm, bn, hs))
+        return [NativeExpertParallel(b"", r, world, E, W_locals[r], None if w_scales is None else w_scales[r],
+                                     handle=ctypes.c_void_p(hs[r])) for r in range(world)]
 
     def forward(self, topk_local, X_local, out=None, out_dtype=None, stream=None):
         import torch

@@ -10,12 +10,15 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <condition_variable>
 #include <cstring>
 #include <mutex>
+#include <memory>
 #include <type_traits>
 #include <vector>
 
 #include "common.h"
+#include "moe_sm100_debug.h"
 #include "moe_sm100_fp8.h"
 
 namespace {
@@ -87,10 +90,68 @@ struct Scratch {
   }
 };
 
+// Test transport (moe_ep_create_loopback): G virtual ranks of one process on one device, each
+// driven by its own host thread and stream; an exchange publishes the source buffer and its
+// per-peer row counts, every rank copies its segments from the peers' buffers (after their
+// "ready" events), and no rank reuses its source before every peer's copies are done.
+struct Loopback {
+  int G = 1;
+  std::mutex m;
+  std::condition_variable cv;
+  int arrived = 0;
+  int64_t gen = 0;
+  std::vector<const void*> src;
+  std::vector<std::vector<int64_t>> send;
+  std::vector<cudaEvent_t> ready, done;
+  ~Loopback() {
+    for (cudaEvent_t e : ready)
+      if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : done)
+      if (e) cudaEventDestroy(e);
+  }
+  void barrier() {
+    std::unique_lock<std::mutex> lk(m);
+    const int64_t g = gen;
+    if (++arrived == G) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != g; });
+    }
+  }
+};
+
 // All-to-all-v of rows: peer p gets rows [send_off[p], send_off[p] + send[p]) of `src`, this rank
 // receives recv[p] rows from p at recv_off[p] of `dst` (row_bytes each).
+moe_status exchange_loopback(Loopback* lb, int rank, const void* src, const std::vector<int64_t>& send, void* dst,
+                             const std::vector<int64_t>& recv, int64_t row_bytes, cudaStream_t s) {
+  lb->src[rank] = src;
+  lb->send[rank] = send;
+  CUDA_TRY(cudaEventRecord(lb->ready[rank], s));
+  lb->barrier();
+  int64_t ro = 0;
+  for (int p = 0; p < lb->G; ++p) {
+    if (recv[p]) {
+      int64_t off = 0;                                 // peer p's rows for ranks before me
+      for (int q = 0; q < rank; ++q) off += lb->send[p][q];
+      if (lb->send[p][rank] != recv[p]) MOE_FAIL(MOE_ERR_NCCL, "loopback: size mismatch");
+      CUDA_TRY(cudaStreamWaitEvent(s, lb->ready[p], 0));
+      CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(dst) + ro * row_bytes,
+                               static_cast<const char*>(lb->src[p]) + off * row_bytes, (size_t)(recv[p] * row_bytes),
+                               cudaMemcpyDeviceToDevice, s));
+    }
+    ro += recv[p];
+  }
+  CUDA_TRY(cudaEventRecord(lb->done[rank], s));
+  lb->barrier();
+  for (int p = 0; p < lb->G; ++p) CUDA_TRY(cudaStreamWaitEvent(s, lb->done[p], 0));
+  return MOE_OK;
+}
+
 moe_status exchange(const void* src, const std::vector<int64_t>& send, void* dst, const std::vector<int64_t>& recv,
-                    int64_t row_bytes, ncclComm_t comm, cudaStream_t s) {
+                    int64_t row_bytes, ncclComm_t comm, cudaStream_t s, Loopback* lb = nullptr, int rank = 0) {
+  if (lb) return exchange_loopback(lb, rank, src, send, dst, recv, row_bytes, s);
   const NcclApi& n = nccl();
   NCCL_TRY(n.GroupStart());
   int64_t so = 0, ro = 0;
@@ -119,6 +180,7 @@ struct moe_ep {
   int64_t sent = 0, received = 0, local_rows = 0;
   cudaEvent_t gemm_ev[2] = {nullptr, nullptr};   // around the last step's GEMM launch
   bool gemm_timed = false;
+  std::shared_ptr<Loopback> lb;                   // test transport instead of NCCL (moe_ep_create_loopback)
 };
 
 extern "C" {
@@ -206,7 +268,7 @@ moe_status moe_ep_forward(moe_ep* ep, const int32_t* topk, int64_t T, int32_t k,
   // 2. counts all-to-all (2 ints per peer), one host read of the split sizes
   {
     std::vector<int64_t> two(G, 1);
-    MOE_TRY(exchange(counts2, two, recv2, two, 8, ep->comm, s));
+    MOE_TRY(exchange(counts2, two, recv2, two, 8, ep->comm, s, ep->lb.get(), ep->rank));
   }
   int32_t* h = ep->host;
   CUDA_TRY(cudaMemcpyAsync(h, counts2, sizeof(int32_t) * 2 * G, cudaMemcpyDeviceToHost, s));
@@ -230,8 +292,8 @@ moe_status moe_ep_forward(moe_ep* ep, const int32_t* topk, int64_t T, int32_t k,
   int32_t* Mr = sc.get<int32_t>((size_t)(R * k), &err);
   MOE_TRY(chk());
   if (S) MOE_TRY(moe_gather_rows(X, send_tok, S, x_row, Xs, s));
-  MOE_TRY(exchange(Xs, send_rows, Xr, recv_rows, x_row, ep->comm, s));
-  MOE_TRY(exchange(send_meta, send_rows, Mr, recv_rows, 4 * (int64_t)k, ep->comm, s));
+  MOE_TRY(exchange(Xs, send_rows, Xr, recv_rows, x_row, ep->comm, s, ep->lb.get(), ep->rank));
+  MOE_TRY(exchange(send_meta, send_rows, Mr, recv_rows, 4 * (int64_t)k, ep->comm, s, ep->lb.get(), ep->rank));
   // 4. local experts: buckets over the received rows (masked slots skipped), device plan
   int32_t* counts_l = sc.get<int32_t>(El, &err);
   int32_t* row_off_l = sc.get<int32_t>(El + 1, &err);
@@ -276,12 +338,42 @@ moe_status moe_ep_forward(moe_ep* ep, const int32_t* topk, int64_t T, int32_t k,
   char* Yb = sc.get<char>((size_t)(B * y_row), &err);
   int32_t* Mb = sc.get<int32_t>((size_t)B, &err);
   MOE_TRY(chk());
-  MOE_TRY(exchange(Ysend, ret_rows, Yb, back_rows, y_row, ep->comm, s));
-  MOE_TRY(exchange(ret_meta, ret_rows, Mb, back_rows, 4, ep->comm, s));
+  MOE_TRY(exchange(Ysend, ret_rows, Yb, back_rows, y_row, ep->comm, s, ep->lb.get(), ep->rank));
+  MOE_TRY(exchange(ret_meta, ret_rows, Mb, back_rows, 4, ep->comm, s, ep->lb.get(), ep->rank));
   if (B) MOE_TRY(moe_ep_unpack(Yb, Mb, B, offs + 2 * (G + 1), send_off, send_tok, G, k, y_row, out, s));
   ep->sent = S;
   ep->received = R;
   ep->local_rows = Rr;
+  return MOE_OK;
+}
+
+moe_status moe_ep_create_loopback(int32_t world, int32_t E, int32_t bm, int32_t bn, moe_ep** eps_out) {
+  moe::clear_error();
+  if (!eps_out || world < 1 || E < 1 || E % world) MOE_FAIL(MOE_ERR_INVALID, "moe_ep_create_loopback: bad arguments");
+  auto lb = std::make_shared<Loopback>();
+  lb->G = world;
+  lb->src.assign(world, nullptr);
+  lb->send.assign(world, {});
+  lb->ready.assign(world, nullptr);
+  lb->done.assign(world, nullptr);
+  for (int r = 0; r < world; ++r) {
+    if (cudaEventCreateWithFlags(&lb->ready[r], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&lb->done[r], cudaEventDisableTiming) != cudaSuccess)
+      MOE_FAIL(MOE_ERR_CUDA, "moe_ep_create_loopback: events");
+  }
+  for (int r = 0; r < world; ++r) {
+    moe_ep* ep = new moe_ep;
+    ep->rank = r;
+    ep->world = world;
+    ep->E = E;
+    ep->bm = bm;
+    ep->bn = bn;
+    ep->lb = lb;
+    if (cudaMallocHost((void**)&ep->host, sizeof(int32_t) * (4 * world + 3 * (world + 1))) != cudaSuccess ||
+        cudaEventCreate(&ep->gemm_ev[0]) != cudaSuccess || cudaEventCreate(&ep->gemm_ev[1]) != cudaSuccess)
+      MOE_FAIL(MOE_ERR_CUDA, "moe_ep_create_loopback: staging");
+    eps_out[r] = ep;
+  }
   return MOE_OK;
 }
 

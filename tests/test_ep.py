@@ -199,3 +199,52 @@ def test_ep_native_nccl_world1(fp8, bm, bn):
         assert np.array_equal(out.cpu().double().numpy(), ref)
     assert ep.last_rows() == {"sent": T, "received": T, "local_rows": T * k}
     assert ep.last_gemm_ms() > 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("G,fp8", [(2, False), (4, False), (8, False), (4, True), (8, True)])
+def test_ep_native_loopback_multirank(G, fp8):
+    """The library's multi-rank orchestration (moe_ep_forward) with G virtual ranks on one GPU: the
+    test transport moves rows by device copies where NCCL would send them (moe_ep_create_loopback);
+    one host thread and stream per rank; bit-exact vs the P:90 per-(token, slot) definition."""
+    import paper_2501_16103_b200 as M
+    E, k, T_l, H, N = 8, 2, 40, 64, 256
+    if fp8:
+        ids, X, W, ref, scale = _problem_fp8(G, E, k, T_l, H, N, seed=G)
+    else:
+        ids, X, W, ref = _problem(G, E, k, T_l, H, N, seed=G)
+        scale = None
+    El = E // G
+    Ws, scs, Xs, tks = [], [], [], []
+    for r in range(G):
+        w = torch.from_numpy(W[r * El:(r + 1) * El])
+        x = torch.from_numpy(X[r * T_l:(r + 1) * T_l])
+        Ws.append(w.cuda() if fp8 else w.to(torch.bfloat16).cuda())
+        Xs.append(x.cuda() if fp8 else x.to(torch.bfloat16).cuda())
+        scs.append(torch.from_numpy(scale[r * El:(r + 1) * El]).cuda() if fp8 else None)
+        tks.append(torch.from_numpy(np.ascontiguousarray(ids[r * T_l:(r + 1) * T_l])).cuda())
+    torch.cuda.synchronize()
+    eps = M.NativeExpertParallel.loopback_group(G, E, Ws, scs if fp8 else None)
+    outs, errs = [None] * G, []
+
+    def body(r):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for _ in range(2):
+                    outs[r] = eps[r].forward(tks[r], Xs[r], out_dtype=torch.float32)
+            s.synchronize()
+        except Exception as e:  # pragma: no cover
+            errs.append(repr(e))
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(G)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=120)
+    assert not errs, errs
+    got = torch.cat([o.cpu() for o in outs]).double().numpy()
+    assert np.array_equal(got, ref)
+    rows = [ep.last_rows() for ep in eps]
+    assert sum(r["sent"] for r in rows) == sum(r["received"] for r in rows)
+    assert sum(r["local_rows"] for r in rows) == G * T_l * k
