@@ -12,3 +12,7 @@ python scripts/paper_table1.py --out gpurun_out/${TAG}_paper_table1.json > gpuru
 python scripts/comparators.py > gpurun_out/${TAG}_comparators.jsonl 2>&1
 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_${TAG}_reference.json 2>&1
 echo refresh done
+python bench.py --ep --steps 10 --warmup 3 > gpurun_out/bench_${TAG}_ep_native_mix.json 2>&1
+python bench.py --ep --dtype fp8 --steps 10 --warmup 3 > gpurun_out/bench_${TAG}_ep_native_mix_fp8.json 2>&1
+python bench.py --ep --config ep --steps 5 --warmup 3 --no-e2e > gpurun_out/bench_${TAG}_ep_native_8x22b.json 2>&1
+echo refresh ep done
