@@ -58,9 +58,11 @@ moe_status moe_gemm_fp8_profile(const moe_plan* plan, const void* X_dev, int64_t
  * handles (eps_out[world]) of one process and device that exchange rows with device copies
  * instead of NCCL, so the multi-rank orchestration of moe_ep_forward runs on one GPU.  Rank r's
  * moe_ep_forward must be called from its own host thread with its own stream, all ranks
- * concurrently (each exchange is a rendezvous of all `world` threads).  moe_ep_destroy each. */
+ * concurrently (each exchange is a rendezvous of all `world` threads).  fused != 0: the GEMM
+ * epilogue stores result rows straight into the owners' receive buffers (the peer-memory combine)
+ * instead of a send buffer + exchange.  moe_ep_destroy each. */
 typedef struct moe_ep moe_ep;
-moe_status moe_ep_create_loopback(int32_t world, int32_t E, int32_t bm, int32_t bn, moe_ep** eps_out);
+moe_status moe_ep_create_loopback(int32_t world, int32_t E, int32_t bm, int32_t bn, int32_t fused, moe_ep** eps_out);
 
 #ifdef __cplusplus
 }

@@ -54,6 +54,32 @@ moe_status moe_ep_combine_map(const int32_t* token_idx_dev, const int32_t* slot_
                               int32_t* cursor_dev, int32_t* row_map_dev, int32_t* ret_meta_dev, void* stream);
 
 /*
+ * Fused combine (the GEMM epilogue writes each result row straight into the token owner's receive
+ * buffer, over NVLink peer memory between GPUs).  For the n CSR rows (token_idx_dev / slot_dev as
+ * moe_ep_combine_map, recv_off_dev [G+1]): with source s = the segment of row r, and pos = a slot
+ * among s's rows (any order) plus peer_off_dev[s], row_ptr_dev[i] = peer_rows_dev[s] + pos * row_bytes
+ * and ((int32_t*)peer_meta_dev[s])[pos] = (r - recv_off[s]) * k + j.  peer_rows_dev / peer_meta_dev:
+ * [G] device arrays of the owners' row / tag buffer addresses; peer_off_dev [G] int32: where this
+ * rank's segment starts in owner s's buffers.
+ * cursor_dev: [G] int32 scratch.  Pass row_ptr_dev to moe_gemm_rowptr.
+ */
+moe_status moe_ep_combine_ptr(const int32_t* token_idx_dev, const int32_t* slot_dev, int64_t n,
+                              const int32_t* recv_off_dev, int32_t G, int32_t k, int32_t* cursor_dev,
+                              const unsigned long long* peer_rows_dev, const unsigned long long* peer_meta_dev,
+                              const int32_t* peer_off_dev, int64_t row_bytes, unsigned long long* row_ptr_dev,
+                              void* stream);
+
+/*
+ * The expert GEMM (moe_gemm / moe_gemm_fp8 by x_dtype: MOE_DTYPE_BF16 or MOE_DTYPE_E4M3 (2), with
+ * the optional per-expert scale for E4M3) storing CSR row i at the device address y_row_ptr_dev[i]
+ * (N values of y_dtype, 16-byte aligned; any memory the GPU can write, e.g. a peer's buffer).
+ * Plain, pair and wide tiles; MOE_ERR_UNSUPPORTED for bm = 64 and MOE_SPLIT_TAIL plans.
+ */
+moe_status moe_gemm_rowptr(const moe_plan* plan, const void* X_dev, int64_t T, const int32_t* token_idx_dev,
+                           const void* W_dev, int32_t x_dtype, const float* scale_dev,
+                           const unsigned long long* y_row_ptr_dev, int32_t y_dtype, void* stream);
+
+/*
  * Source side.  rows_dev: n returned result rows (segment per destination given by
  * ret_off_dev [G+1]) with their ret_meta_dev; send_off_dev / send_tok_dev from
  * moe_ep_dispatch_plan.  out_dev[t * k + j, :] = the returned row of (token t, slot j).

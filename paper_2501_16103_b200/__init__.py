@@ -35,7 +35,7 @@ EXPORTED = (
     "moe_ep_dispatch_plan", "moe_gather_rows", "moe_ep_combine_map", "moe_ep_unpack", "moe_route_plan",
     "moe_gemm_swiglu", "moe_combine", "moe_gemm_fp8", "moe_gemm_fp8_rowmap", "moe_gemm_fp8_profile",
     "moe_ep_unique_id", "moe_ep_create", "moe_ep_forward", "moe_ep_last_rows", "moe_ep_last_gemm_ms",
-    "moe_ep_destroy", "moe_ep_create_loopback",
+    "moe_ep_destroy", "moe_ep_create_loopback", "moe_ep_combine_ptr", "moe_gemm_rowptr",
 )
 
 
@@ -103,7 +103,11 @@ def lib() -> ctypes.CDLL:
         "moe_ep_last_rows": (ctypes.c_int32, [vp, c_i64p, c_i64p, c_i64p]),
         "moe_ep_last_gemm_ms": (ctypes.c_int32, [vp, ctypes.POINTER(ctypes.c_float)]),
         "moe_ep_create_loopback": (ctypes.c_int32, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
-                                                    ctypes.POINTER(vp)]),
+                                                    ctypes.c_int32, ctypes.POINTER(vp)]),
+        "moe_ep_combine_ptr": (ctypes.c_int32, [vp, vp, ctypes.c_int64, vp, ctypes.c_int32, ctypes.c_int32, vp, vp, vp,
+                                                vp, ctypes.c_int64, vp, vp]),
+        "moe_gemm_rowptr": (ctypes.c_int32, [vp, vp, ctypes.c_int64, vp, vp, ctypes.c_int32, vp, vp, ctypes.c_int32,
+                                             vp]),
         "moe_ep_destroy": (None, [vp]),
         "moe_combine": (ctypes.c_int32, [vp, ctypes.c_int32, ctypes.c_int64, ctypes.c_int32, ctypes.c_int64, vp, vp,
                                          vp, ctypes.c_int32, vp, vp, ctypes.c_int32, vp]),
@@ -564,11 +568,12 @@ class NativeExpertParallel:
                                    ctypes.byref(self._h)))
 
     @staticmethod
-    def loopback_group(world: int, E: int, W_locals, w_scales=None, bm: int = 0, bn: int = 0):
+    def loopback_group(world: int, E: int, W_locals, w_scales=None, bm: int = 0, bn: int = 0, fused: bool = False):
         """`world` virtual ranks on one device exchanging by device copies (moe_ep_create_loopback,
-        include/moe_sm100_debug.h); call each rank's forward from its own thread and stream."""
+        include/moe_sm100_debug.h); fused: the GEMM epilogue writes into the owners' buffers.
+        Call each rank's forward from its own thread and stream."""
         hs = (ctypes.c_void_p * world)()
-        _check(lib().moe_ep_create_loopback(world, E, bm, bn, hs))
+        _check(lib().moe_ep_create_loopback(world, E, bm, bn, 1 if fused else 0, hs))
         return [NativeExpertParallel(b"", r, world, E, W_locals[r], None if w_scales is None else w_scales[r],
                                      handle=ctypes.c_void_p(hs[r])) for r in range(world)]
 

@@ -137,6 +137,23 @@ __global__ void ep_combine_map_kernel(const int32_t* __restrict__ token_idx, con
 
 // Source side: returned row i (from destination d = segment of i in ret_off) goes to
 // out[t * k + j] with t = send_tok[send_off[d] + meta / k], j = meta % k.  One warp per row.
+// Fused combine (moe_ep_combine_ptr): the row's destination is a row of the token owner's receive
+// buffer (peer memory), so the GEMM epilogue stores it there directly.
+__global__ void ep_combine_ptr_kernel(const int32_t* __restrict__ token_idx, const int32_t* __restrict__ slot,
+                                      int n, const int32_t* __restrict__ recv_off, int G, int k,
+                                      int32_t* __restrict__ cursor, const unsigned long long* __restrict__ peer_rows,
+                                      const unsigned long long* __restrict__ peer_meta,
+                                      const int32_t* __restrict__ peer_off, long long row_bytes,
+                                      unsigned long long* __restrict__ row_ptr) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int r = token_idx[i];
+    const int s = segment_of(recv_off, G, r);
+    const int pos = peer_off[s] + atomicAdd(cursor + s, 1);
+    row_ptr[i] = peer_rows[s] + (unsigned long long)pos * row_bytes;
+    reinterpret_cast<int32_t*>(peer_meta[s])[pos] = (r - recv_off[s]) * k + slot[i];
+  }
+}
+
 __global__ void ep_unpack_kernel(const uint4* __restrict__ rows, const int32_t* __restrict__ ret_meta, int n,
                                  const int32_t* __restrict__ ret_off, const int32_t* __restrict__ send_off,
                                  const int32_t* __restrict__ send_tok, int G, int k, int row_vec,
@@ -208,6 +225,26 @@ moe_status moe_ep_combine_map(const int32_t* token_idx, const int32_t* slot, int
                                                ret_meta);
   e = cudaGetLastError();
   if (e != cudaSuccess) MOE_FAIL(MOE_ERR_CUDA, "moe_ep_combine_map launch: %s", cudaGetErrorString(e));
+  return MOE_OK;
+}
+
+moe_status moe_ep_combine_ptr(const int32_t* token_idx, const int32_t* slot, int64_t n, const int32_t* recv_off,
+                              int32_t G, int32_t k, int32_t* cursor, const unsigned long long* peer_rows,
+                              const unsigned long long* peer_meta, const int32_t* peer_off, int64_t row_bytes,
+                              unsigned long long* row_ptr, void* stream) {
+  moe::clear_error();
+  if (n == 0) return MOE_OK;
+  if (!token_idx || !slot || !recv_off || !cursor || !peer_rows || !peer_meta || !peer_off || !row_ptr || G < 1 || k < 1 ||
+      n < 0 || n >= INT_MAX || row_bytes <= 0 || row_bytes % 16)
+    MOE_FAIL(MOE_ERR_INVALID, "moe_ep_combine_ptr: bad argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(cursor, 0, sizeof(int32_t) * G, s);
+  if (e != cudaSuccess) MOE_FAIL(MOE_ERR_CUDA, "moe_ep_combine_ptr memset: %s", cudaGetErrorString(e));
+  const int blocks = (int)std::min<int64_t>((n + 255) / 256, 4 * 148);
+  ep_combine_ptr_kernel<<<blocks, 256, 0, s>>>(token_idx, slot, (int)n, recv_off, G, k, cursor, peer_rows, peer_meta,
+                                               peer_off, row_bytes, row_ptr);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) MOE_FAIL(MOE_ERR_CUDA, "moe_ep_combine_ptr launch: %s", cudaGetErrorString(e));
   return MOE_OK;
 }
 

@@ -11,6 +11,8 @@
 #include <nccl.h>
 
 #include <condition_variable>
+#include <cstdlib>
+#include <algorithm>
 #include <cstring>
 #include <mutex>
 #include <memory>
@@ -103,6 +105,7 @@ struct Loopback {
   std::vector<const void*> src;
   std::vector<std::vector<int64_t>> send;
   std::vector<cudaEvent_t> ready, done;
+  std::vector<void*> rows_base, meta_base;       // fused combine: every rank's receive buffers
   ~Loopback() {
     for (cudaEvent_t e : ready)
       if (e) cudaEventDestroy(e);
@@ -149,6 +152,16 @@ moe_status exchange_loopback(Loopback* lb, int rank, const void* src, const std:
   return MOE_OK;
 }
 
+// Every rank's stream waits for every rank's work enqueued so far (fused combine: the peers'
+// GEMMs have written this rank's receive buffer).
+moe_status sync_loopback(Loopback* lb, int rank, cudaStream_t s) {
+  CUDA_TRY(cudaEventRecord(lb->done[rank], s));
+  lb->barrier();
+  for (int p = 0; p < lb->G; ++p) CUDA_TRY(cudaStreamWaitEvent(s, lb->done[p], 0));
+  lb->barrier();                                   // done[] may be re-recorded only after everyone waited
+  return MOE_OK;
+}
+
 moe_status exchange(const void* src, const std::vector<int64_t>& send, void* dst, const std::vector<int64_t>& recv,
                     int64_t row_bytes, ncclComm_t comm, cudaStream_t s, Loopback* lb = nullptr, int rank = 0) {
   if (lb) return exchange_loopback(lb, rank, src, send, dst, recv, row_bytes, s);
@@ -171,6 +184,10 @@ moe_status exchange(const void* src, const std::vector<int64_t>& send, void* dst
 
 }  // namespace
 
+// Pinned host staging per rank: counts [G][2], recv [G][2], recv / ret / back offsets 3 (G+1),
+// back prefix [G] (int32), then peer row / tag buffer addresses [2][G] (uint64, 8-byte aligned).
+inline size_t host_staging_bytes(int G) { return (size_t)4 * (4 * G + 3 * (G + 1) + G + 2) + (size_t)16 * G; }
+
 struct moe_ep {
   ncclComm_t comm = nullptr;
   int32_t rank = 0, world = 1, E = 0, bm = 0, bn = 0;
@@ -181,6 +198,12 @@ struct moe_ep {
   cudaEvent_t gemm_ev[2] = {nullptr, nullptr};   // around the last step's GEMM launch
   bool gemm_timed = false;
   std::shared_ptr<Loopback> lb;                   // test transport instead of NCCL (moe_ep_create_loopback)
+  // Fused combine: the GEMM epilogue stores result rows into the owners' receive buffers (this
+  // rank's own with one rank; the peers' with the loopback transport).  Persistent, grow-only.
+  bool fused = false;
+  char* rows_buf = nullptr;
+  int32_t* meta_buf = nullptr;
+  int64_t cap_bytes = 0, cap_rows = 0;
 };
 
 extern "C" {
@@ -208,6 +231,12 @@ moe_status moe_ep_create(const void* unique_id, int32_t rank, int32_t world, int
   ep->E = E;
   ep->bm = bm;
   ep->bn = bn;
+  {
+    // With one rank the combine never leaves the device: fuse it into the GEMM epilogue.  Between
+    // GPUs the same path needs the peers' buffers mapped (CUDA IPC), not built yet: NCCL exchange.
+    const char* f = getenv("MOE_EP_FUSED");
+    ep->fused = world == 1 && !(f && atoi(f) == 0);
+  }
   ncclUniqueId id;
   std::memcpy(&id, unique_id, sizeof(id));
   ncclResult_t r = nccl().CommInitRank(&ep->comm, world, id, rank);
@@ -225,7 +254,7 @@ moe_status moe_ep_create(const void* unique_id, int32_t rank, int32_t world, int
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
     }
   }
-  if (cudaMallocHost((void**)&ep->host, sizeof(int32_t) * (4 * world + 3 * (world + 1))) != cudaSuccess ||
+  if (cudaMallocHost((void**)&ep->host, host_staging_bytes(world)) != cudaSuccess ||
       cudaEventCreate(&ep->gemm_ev[0]) != cudaSuccess || cudaEventCreate(&ep->gemm_ev[1]) != cudaSuccess) {
     nccl().CommDestroy(ep->comm);
     delete ep;
@@ -318,6 +347,60 @@ moe_status moe_ep_forward(moe_ep* ep, const int32_t* topk, int64_t T, int32_t k,
   }
   int32_t* offs = sc.get<int32_t>(3 * (G + 1), &err);
   int32_t* cursor = sc.get<int32_t>(G, &err);
+  if (ep->fused) {
+    // 5'. fused combine: each result row goes straight into its owner's receive buffer.
+    if (!ep->rows_buf || B * y_row > ep->cap_bytes || B > ep->cap_rows) {   // grow-only (stream idle here)
+      if (ep->rows_buf) cudaFree(ep->rows_buf);
+      if (ep->meta_buf) cudaFree(ep->meta_buf);
+      ep->rows_buf = nullptr;
+      ep->meta_buf = nullptr;
+      ep->cap_bytes = std::max<int64_t>({B * y_row, 2 * ep->cap_bytes, 16});
+      ep->cap_rows = std::max<int64_t>({B, 2 * ep->cap_rows, 4});
+      CUDA_TRY(cudaMalloc((void**)&ep->rows_buf, (size_t)ep->cap_bytes));
+      CUDA_TRY(cudaMalloc((void**)&ep->meta_buf, sizeof(int32_t) * (size_t)ep->cap_rows));
+    }
+    Loopback* lb = ep->lb.get();
+    if (lb) {                                        // published before the offsets exchange (a rendezvous)
+      lb->rows_base[ep->rank] = ep->rows_buf;
+      lb->meta_base[ep->rank] = ep->meta_buf;
+    }
+    // where this rank's rows start in each owner's buffer: owner s's prefix over its sources
+    int32_t* pre_h = off_h + 3 * (G + 1);
+    for (int p = 0; p < G; ++p) pre_h[p] = off_h[2 * (G + 1) + p];
+    int32_t* pre_d = sc.get<int32_t>(G, &err);
+    int32_t* at_d = sc.get<int32_t>(G, &err);
+    unsigned long long* peer_d = sc.get<unsigned long long>(2 * (size_t)G, &err);
+    unsigned long long* row_ptr = sc.get<unsigned long long>((size_t)Rr, &err);
+    MOE_TRY(chk());
+    CUDA_TRY(cudaMemcpyAsync(offs, off_h, sizeof(int32_t) * 3 * (G + 1), cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(pre_d, pre_h, sizeof(int32_t) * G, cudaMemcpyHostToDevice, s));
+    {
+      std::vector<int64_t> one(G, 1);
+      MOE_TRY(exchange(pre_d, one, at_d, one, 4, ep->comm, s, lb, ep->rank));
+    }
+    unsigned long long* peer_h = reinterpret_cast<unsigned long long*>(
+        (reinterpret_cast<uintptr_t>(pre_h + G) + 7) & ~uintptr_t(7));
+    for (int p = 0; p < G; ++p) {
+      peer_h[p] = (unsigned long long)(lb ? lb->rows_base[p] : (void*)ep->rows_buf);
+      peer_h[G + p] = (unsigned long long)(lb ? lb->meta_base[p] : (void*)ep->meta_buf);
+    }
+    CUDA_TRY(cudaMemcpyAsync(peer_d, peer_h, sizeof(unsigned long long) * 2 * G, cudaMemcpyHostToDevice, s));
+    if (Rr) {
+      MOE_TRY(moe_ep_combine_ptr(tok_l, slot_l, Rr, offs, G, k, cursor, peer_d, peer_d + G, at_d, y_row, row_ptr, s));
+      // 6'. the single-launch expert GEMM; its epilogue stores every row at its owner
+      CUDA_TRY(cudaEventRecord(ep->gemm_ev[0], s));
+      MOE_TRY(moe_gemm_rowptr(ep->plan, Xr, R, tok_l, W, x_dtype, w_scale, row_ptr, out_dtype, s));
+      CUDA_TRY(cudaEventRecord(ep->gemm_ev[1], s));
+    }
+    ep->gemm_timed = Rr > 0;
+    if (lb) MOE_TRY(sync_loopback(lb, ep->rank, s));   // the peers' GEMMs have written this rank's rows
+    if (B) MOE_TRY(moe_ep_unpack(ep->rows_buf, ep->meta_buf, B, offs + 2 * (G + 1), send_off, send_tok, G, k, y_row,
+                                 out, s));
+    ep->sent = S;
+    ep->received = R;
+    ep->local_rows = Rr;
+    return MOE_OK;
+  }
   int32_t* row_map = sc.get<int32_t>((size_t)Rr, &err);
   int32_t* ret_meta = sc.get<int32_t>((size_t)Rr, &err);
   char* Ysend = sc.get<char>((size_t)(Rr * y_row), &err);
@@ -347,7 +430,7 @@ moe_status moe_ep_forward(moe_ep* ep, const int32_t* topk, int64_t T, int32_t k,
   return MOE_OK;
 }
 
-moe_status moe_ep_create_loopback(int32_t world, int32_t E, int32_t bm, int32_t bn, moe_ep** eps_out) {
+moe_status moe_ep_create_loopback(int32_t world, int32_t E, int32_t bm, int32_t bn, int32_t fused, moe_ep** eps_out) {
   moe::clear_error();
   if (!eps_out || world < 1 || E < 1 || E % world) MOE_FAIL(MOE_ERR_INVALID, "moe_ep_create_loopback: bad arguments");
   auto lb = std::make_shared<Loopback>();
@@ -356,6 +439,8 @@ moe_status moe_ep_create_loopback(int32_t world, int32_t E, int32_t bm, int32_t 
   lb->send.assign(world, {});
   lb->ready.assign(world, nullptr);
   lb->done.assign(world, nullptr);
+  lb->rows_base.assign(world, nullptr);
+  lb->meta_base.assign(world, nullptr);
   for (int r = 0; r < world; ++r) {
     if (cudaEventCreateWithFlags(&lb->ready[r], cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&lb->done[r], cudaEventDisableTiming) != cudaSuccess)
@@ -369,7 +454,8 @@ moe_status moe_ep_create_loopback(int32_t world, int32_t E, int32_t bm, int32_t 
     ep->bm = bm;
     ep->bn = bn;
     ep->lb = lb;
-    if (cudaMallocHost((void**)&ep->host, sizeof(int32_t) * (4 * world + 3 * (world + 1))) != cudaSuccess ||
+    ep->fused = fused != 0;
+    if (cudaMallocHost((void**)&ep->host, host_staging_bytes(world)) != cudaSuccess ||
         cudaEventCreate(&ep->gemm_ev[0]) != cudaSuccess || cudaEventCreate(&ep->gemm_ev[1]) != cudaSuccess)
       MOE_FAIL(MOE_ERR_CUDA, "moe_ep_create_loopback: staging");
     eps_out[r] = ep;
@@ -400,6 +486,8 @@ void moe_ep_destroy(moe_ep* ep) {
   if (!ep) return;
   for (cudaEvent_t e : ep->gemm_ev)
     if (e) cudaEventDestroy(e);
+  if (ep->rows_buf) cudaFree(ep->rows_buf);
+  if (ep->meta_buf) cudaFree(ep->meta_buf);
   if (ep->plan) moe_plan_destroy(ep->plan);
   if (ep->comm) nccl().CommDestroy(ep->comm);
   if (ep->host) cudaFreeHost(ep->host);

@@ -101,6 +101,8 @@ struct GemmArgs {
   const int32_t* y_row_map;  // nullable: Y row of CSR row i is y_row_map[i] (EP combine buffer)
   int32_t tma_store;         // bf16 Y in CSR row order: full 32-row quarters leave through TMA tile stores
   const float* scale;        // FP8 path, nullable: Y rows of expert e are scaled by scale[e] (fp32, epilogue)
+  const unsigned long long* y_row_ptr;   // nullable: CSR row i is stored at address y_row_ptr[i] (any device
+                                         // memory the SM can write: the EP combine buffers of peer ranks)
 };
 
 // Per-CTA counters written by the instrumented build (kProf = true).
@@ -211,10 +213,10 @@ __device__ __forceinline__ uint32_t pack_bf16(uint32_t lo, uint32_t hi) {
 
 // Store 32 consecutive fp32 accumulator columns [col0, col0+32) of one Y row,
 // masked to col < col_end (col_end is a multiple of 8).
-__device__ __forceinline__ void store_chunk(const GemmArgs& a, int64_t yrow, int col0, int col_end,
+__device__ __forceinline__ void store_chunk(const GemmArgs& a, uint8_t* yrow_ptr, int col0, int col_end,
                                             const uint32_t (&v)[32]) {
   if (a.y_f32) {
-    float* y = reinterpret_cast<float*>(a.Y) + yrow * a.N;
+    float* y = reinterpret_cast<float*>(yrow_ptr);
 #pragma unroll
     for (int g = 0; g < 8; ++g) {
       const int c = col0 + 4 * g;
@@ -224,7 +226,7 @@ __device__ __forceinline__ void store_chunk(const GemmArgs& a, int64_t yrow, int
       }
     }
   } else {
-    __nv_bfloat16* y = reinterpret_cast<__nv_bfloat16*>(a.Y) + yrow * a.N;
+    __nv_bfloat16* y = reinterpret_cast<__nv_bfloat16*>(yrow_ptr);
 #pragma unroll
     for (int g = 0; g < 4; ++g) {
       const int c = col0 + 8 * g;
@@ -925,6 +927,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool valid = grow < t.rows;
       const int64_t yrow = a.y_row_map ? (int64_t)__ldg(a.y_row_map + t.row0 + min(grow, t.rows - 1))
                                        : (int64_t)t.row0 + grow;
+      uint8_t* const yrow_ptr =
+          a.y_row_ptr ? reinterpret_cast<uint8_t*>(__ldg(a.y_row_ptr + t.row0 + min(grow, t.rows - 1)))
+                      : reinterpret_cast<uint8_t*>(a.Y) + yrow * a.N * (a.y_f32 ? 4 : 2);
       const int wrow0 = grow - lane;                // first task row of this warp's quarter
       const bool tma_rows = a.tma_store && wrow0 + 32 <= t.rows;
       const uint32_t xr = (uint32_t)((lane >> 1) & 3);
@@ -957,7 +962,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           ++n_chunk;
         } else if (valid) {
-          store_chunk(a, yrow, col, col_end, r);
+          store_chunk(a, yrow_ptr, col, col_end, r);
         }
       };
       if constexpr (kGated) {
@@ -1444,7 +1449,7 @@ cudaError_t set_smem_attrs() {
 static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, const int32_t* token_idx,
                               const void* W, void* Y, int32_t y_dtype, void* stream, long long* prof,
                               const int32_t* y_row_map = nullptr, const void* W2 = nullptr, bool fp8 = false,
-                              const float* scale = nullptr) {
+                              const float* scale = nullptr, const unsigned long long* y_row_ptr = nullptr) {
   moe::clear_error();
   if (!plan) MOE_FAIL(MOE_ERR_INVALID, "moe_gemm: null plan");
   moe::BlobView v;
@@ -1518,7 +1523,9 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
   // TMA-store epilogue: bf16 Y in CSR row order (the EP combine path scatters rows: register stores).
   CUtensorMap tmY;
   std::memset(&tmY, 0, sizeof(tmY));
-  bool tma_store = y_dtype == MOE_DTYPE_BF16 && !y_row_map;
+  bool tma_store = y_dtype == MOE_DTYPE_BF16 && !y_row_map && !y_row_ptr;
+  if (y_row_ptr && (v.bm == kDecRows || (v.flags & MOE_SPLIT_TAIL) || W2))
+    MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_gemm_rowptr: plain / pair / wide tiles only (no bm = 64, split tails, gating)");
   {
     const char* ep = getenv("MOE_EPI_TMA");        // timing studies: 0 = register stores only
     if (ep && atoi(ep) == 0) tma_store = false;
@@ -1550,6 +1557,7 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
   a.w4d = w4d ? 1 : 0;
   a.prof = prof;
   a.y_row_map = y_row_map;
+  a.y_row_ptr = y_row_ptr;
   a.tma_store = tma_store ? 1 : 0;
   a.T = (int32_t)T;
   a.H = v.H;
@@ -1676,6 +1684,16 @@ moe_status moe_gemm_fp8_rowmap(const moe_plan* plan, const void* X, int64_t T, c
                                void* stream) {
   if (!y_row_map) MOE_FAIL(MOE_ERR_INVALID, "moe_gemm_fp8_rowmap: null y_row_map");
   return gemm_launch(plan, X, T, token_idx, W, Y, y_dtype, stream, nullptr, y_row_map, nullptr, true, scale);
+}
+
+moe_status moe_gemm_rowptr(const moe_plan* plan, const void* X, int64_t T, const int32_t* token_idx, const void* W,
+                           int32_t x_dtype, const float* scale, const unsigned long long* y_row_ptr, int32_t y_dtype,
+                           void* stream) {
+  if (!y_row_ptr) MOE_FAIL(MOE_ERR_INVALID, "moe_gemm_rowptr: null y_row_ptr");
+  if (x_dtype != MOE_DTYPE_BF16 && x_dtype != MOE_DTYPE_E4M3) MOE_FAIL(MOE_ERR_INVALID, "moe_gemm_rowptr: x_dtype");
+  // Y is unused (every row has its own address); a non-null placeholder passes the argument checks.
+  return gemm_launch(plan, X, T, token_idx, W, const_cast<unsigned long long*>(y_row_ptr), y_dtype, stream, nullptr,
+                     nullptr, nullptr, x_dtype == MOE_DTYPE_E4M3, scale, y_row_ptr);
 }
 
 moe_status moe_gemm_rowmap(const moe_plan* plan, const void* X, int64_t T, const int32_t* token_idx,

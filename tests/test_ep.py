@@ -178,11 +178,14 @@ def test_ep_nccl_world1():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("fused", ["1", "0"])
 @pytest.mark.parametrize("fp8", [False, True])
 @pytest.mark.parametrize("bm,bn", [(0, 0), (128, 256)])
-def test_ep_native_nccl_world1(fp8, bm, bn):
+def test_ep_native_nccl_world1(fp8, bm, bn, fused, monkeypatch):
+    monkeypatch.setenv("MOE_EP_FUSED", fused)
     """The library's own expert-parallel step (moe_ep_create / moe_ep_forward: NCCL called from C++,
-    a one-rank communicator on one GPU) against the P:90 definition, and equal to the Python path."""
+    a one-rank communicator on one GPU; the combine fused into the GEMM epilogue, and with
+    MOE_EP_FUSED=0 the send buffer + exchange) against the P:90 definition."""
     import paper_2501_16103_b200 as M
     E, k, T, H, N = 8, 2, 300, 64, 256
     if fp8:
@@ -202,8 +205,9 @@ def test_ep_native_nccl_world1(fp8, bm, bn):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("fused", [False, True])
 @pytest.mark.parametrize("G,fp8", [(2, False), (4, False), (8, False), (4, True), (8, True)])
-def test_ep_native_loopback_multirank(G, fp8):
+def test_ep_native_loopback_multirank(G, fp8, fused):
     """The library's multi-rank orchestration (moe_ep_forward) with G virtual ranks on one GPU: the
     test transport moves rows by device copies where NCCL would send them (moe_ep_create_loopback);
     one host thread and stream per rank; bit-exact vs the P:90 per-(token, slot) definition."""
@@ -224,7 +228,7 @@ def test_ep_native_loopback_multirank(G, fp8):
         scs.append(torch.from_numpy(scale[r * El:(r + 1) * El]).cuda() if fp8 else None)
         tks.append(torch.from_numpy(np.ascontiguousarray(ids[r * T_l:(r + 1) * T_l])).cuda())
     torch.cuda.synchronize()
-    eps = M.NativeExpertParallel.loopback_group(G, E, Ws, scs if fp8 else None)
+    eps = M.NativeExpertParallel.loopback_group(G, E, Ws, scs if fp8 else None, fused=fused)
     outs, errs = [None] * G, []
 
     def body(r):
