@@ -2,18 +2,21 @@
 """Benchmark of the statically batched MoE expert GEMM (arXiv 2501.16103) on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config mix]
+                    [--dtype bf16|fp8] [--ffn] [--ep] [--host-plan] [--order natural|...]
 
-A step = one pass of the whole hot path over one batch of synthetic input
-(SURVEY §8(a)): moe_route (device buckets) -> counts D2H -> host plan (Alg. 1 +
-sigma) + blob H2D -> moe_gemm (one tcgen05 launch over every expert tile).
-`value` = useful FLOPs (2 * sum m_e * H * N) / device step time, inputs resident
-in HBM; `e2e` = the same metric with X / top-k ids copied from pinned host memory
-and Y copied back inside the timed region.  L2 is flushed (256 MiB memset, then a
-256 MiB read so no dirty line is left to write back) before every timed step.  `--impl reference` times the fp64 CPU oracle on a
-bounded sample of the same workload (the tier's reference arm).
+A step = one pass of the whole hot path over one batch of synthetic input:
+moe_route_plan (device buckets + the device-built compressed mapping, Alg. 1 + sigma) ->
+moe_gemm (one tcgen05 launch over every expert tile), replayed as one CUDA graph; --host-plan
+plans on the host instead (counts D2H, blob H2D).  `value` = useful FLOPs (2 * sum m_e * H * N)
+/ device step time, inputs resident in HBM; `e2e` = the same metric through the public API with
+X / top-k ids copied from pinned host memory and Y copied back inside the timed region.  L2 is
+flushed (256 MiB memset, then a 256 MiB read so no dirty line is left to write back) before
+every timed step.  `--impl reference` times the fp64 CPU oracle on a bounded sample of the same
+workload (the tier's reference arm).
 
-Multi-GPU (torchrun, N > 1): see DESIGN.md §Multi-GPU; each rank runs the
-expert-parallel shard of the `ep` workload.
+Multi-GPU (torchrun, N > 1) or --ep: the expert-parallel step in the library (moe_ep_forward,
+NCCL from C++; --ep-python: the torch.distributed orchestration) — weak scaling on the Mix shape,
+strong scaling on the 8x22B `ep` shape.
 """
 from __future__ import annotations
 
