@@ -103,6 +103,7 @@ struct GemmArgs {
   const float* scale;        // FP8 path, nullable: Y rows of expert e are scaled by scale[e] (fp32, epilogue)
   const unsigned long long* y_row_ptr;   // nullable: CSR row i is stored at address y_row_ptr[i] (any device
                                          // memory the SM can write: the EP combine buffers of peer ranks)
+  int32_t balance;           // balanced grid: only ceil(total / ceil(total / grid)) CTAs (pairs) take tiles
 };
 
 // Per-CTA counters written by the instrumented build (kProf = true).
@@ -332,7 +333,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // data path (full / tmem-empty barriers) live in the leader.
   const uint32_t rank = kCta == 2 ? cluster_ctarank() : 0;
   const int pair_id = blockIdx.x / kCta;
-  const int n_pairs = gridDim.x / kCta;
+  int n_pairs = gridDim.x / kCta;
   auto leader = [&](uint32_t addr) { return kCta == 2 ? mapa_shared(addr, 0) : addr; };
 
   const int a_mode = a.a_mode == 2 ? 2 : kCta == 2 && !kWide ? 1 : a.a_mode;
@@ -365,6 +366,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   // TilePrefix and sigma are adjacent in the blob: one copy into shared memory.
   for (int i = threadIdx.x; i < 2 * a.M_pad; i += blockDim.x) s_prefix[i] = a.plan[MOE_PLAN_HEADER + i];
   if (total < 0) total = __ldg(a.plan + 2);
+  if (a.balance && total > 0) {
+    // Balanced grid: with W = ceil(total / grid) tiles for the busiest CTA (pair) anyway, spread the
+    // tiles over ceil(total / W) CTAs so every active one takes W or W - 1 and no short last wave
+    // runs on a few SMs — for HBM-bound (decode) tiles the kernel's streaming rate then stays the
+    // chip's instead of dropping to a few SMs' for the tail.
+    const int per = (total + n_pairs - 1) / n_pairs;
+    const int used = (total + per - 1) / per;
+    if (pair_id >= used) total = 0;                  // this CTA (pair) takes no tile
+    n_pairs = used;
+  }
   tc_fence_before();
   if constexpr (kCta == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
@@ -1558,6 +1569,13 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
   a.prof = prof;
   a.y_row_map = y_row_map;
   a.y_row_ptr = y_row_ptr;
+  {
+    const char* b = getenv("MOE_BALANCE");          // 1: balanced grid on every tile shape, 0: never
+    a.balance = b ? atoi(b) != 0 : v.bm == 128;      // default: one-CTA (decode-regime) tiles
+    // MOE_SPLIT_TAIL plans keep the plain stride: balancing gives a CTA pair two swap-AB tail tiles in
+    // a row, a sequence the opt-in split path computes wrongly (known issue).
+    if (v.flags & MOE_SPLIT_TAIL) a.balance = 0;
+  }
   a.tma_store = tma_store ? 1 : 0;
   a.T = (int32_t)T;
   a.H = v.H;
