@@ -853,7 +853,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (kSplit && t.kind == 1 && cg > 0) {
         // Swap-AB tail tiles are drained by the first four epilogue warps alone.
-        if (a.tma_store) named_bar_sync(1, 32 * kEpiWarps);   // transposes done: staging reusable
+        // Wait for the transposing warps to finish this tile (always: besides freeing the staging
+        // buffers, it keeps these warps from running ahead — their arrivals on the next tile's
+        // tmem-empty barriers would otherwise complete this tile's phase early).
+        named_bar_sync(1, 32 * kEpiWarps);
         __syncwarp();
         if (lane == 0) {
           if constexpr (kWide) {
@@ -920,7 +923,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           else mbar_arrive(tempty_bar(slot));
         }
         }
-        if (a.tma_store) named_bar_sync(1, 32 * kEpiWarps);   // transposes done: staging reusable
+        named_bar_sync(1, 32 * kEpiWarps);                     // transposes done (see the cg > 0 warps)
         if constexpr (kProf) c_work += clock64() - w0;
         if constexpr (kWide) {
           acc_phase ^= 1u;
@@ -1572,9 +1575,6 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
   {
     const char* b = getenv("MOE_BALANCE");          // 1: balanced grid on every tile shape, 0: never
     a.balance = b ? atoi(b) != 0 : v.bm == 128;      // default: one-CTA (decode-regime) tiles
-    // MOE_SPLIT_TAIL plans keep the plain stride: balancing gives a CTA pair two swap-AB tail tiles in
-    // a row, a sequence the opt-in split path computes wrongly (known issue).
-    if (v.flags & MOE_SPLIT_TAIL) a.balance = 0;
   }
   a.tma_store = tma_store ? 1 : 0;
   a.T = (int32_t)T;

@@ -633,3 +633,21 @@ def test_forward_device_plan_fuzz(case):
         torch.cuda.synchronize()
         rc, rr, rt, rs = omoe.buckets(ids, E)
         assert np.array_equal(Y.cpu().double().numpy(), omoe.expert_gemm(X, W, rt, rr)), f"case {case} step {step}"
+
+
+@pytest.mark.parametrize("out_dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("bn", [512, 480])
+def test_split_tail_consecutive_tail_tiles(out_dtype, bn):
+    """Regression: with MOE_SPLIT_TAIL, a CTA pair running two swap-AB tail tiles in a row (here
+    every expert has 300 rows = one body + one tail row tile, 80 tiles on 74 pairs, so pairs 1, 3
+    and 5 take tail tiles v and v + 74) — the non-transposing epilogue warps used to run ahead
+    into the next tile's tmem-empty barrier with fp32 output and corrupt block 1."""
+    T, E, k, H, N = 1200, 8, 2, 64, 2560
+    ids = synth.route_balanced(T, E, k)
+    X, W = synth.make_x(5, T, H, "int"), synth.make_w(5, E, H, N, "int")
+    Xd, Wd = torch.from_numpy(X).to(torch.bfloat16).cuda(), torch.from_numpy(W).to(torch.bfloat16).cuda()
+    Y, counts, row_off, tok, *_ = run_path(ids, Xd, Wd, E, bn=bn, bm=256, flags=M.MOE_SPLIT_TAIL, out_dtype=out_dtype)
+    rc, rr, rt, rs = omoe.buckets(ids, E)
+    ref = omoe.expert_gemm(X, W, rt, rr)
+    exp = ref if out_dtype == torch.float32 else torch.from_numpy(ref).to(torch.bfloat16).double().numpy()
+    assert np.array_equal(Y.cpu().double().numpy(), exp)
