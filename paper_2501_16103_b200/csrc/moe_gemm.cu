@@ -682,6 +682,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
           };
           const long long t_i = kProf ? clock64() : 0;
+#ifdef MOE_EXPERIMENTS
+          if (!(a.experiment & 64))                                      // 64: never wait (timing only)
+#endif
           wait_timed<kProf>(tempty_bar(0), acc_phase ^ 1u, c_tmem);    // block 0 of the last tile drained
           tc_fence_after();
           for (int kb = 0; kb < D; ++kb) {
@@ -689,6 +692,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             issue(0, kb);
           }
           if (n == D) block_full(0);
+#ifdef MOE_EXPERIMENTS
+          if (!(a.experiment & 64))
+#endif
           wait_timed<kProf>(tempty_bar(1), acc_phase ^ 1u, c_tmem);
           tc_fence_after();
           for (int kb = 0; kb < D; ++kb) {
