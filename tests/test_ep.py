@@ -252,3 +252,52 @@ def test_ep_native_loopback_multirank(G, fp8, fused):
     rows = [ep.last_rows() for ep in eps]
     assert sum(r["sent"] for r in rows) == sum(r["received"] for r in rows)
     assert sum(r["local_rows"] for r in rows) == G * T_l * k
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("fused", [False, True])
+def test_ep_native_loopback_masked_slots(fused):
+    """Masked slots (negative ids) and skewed routing with empty experts through the library's
+    multi-rank step (G = 4 virtual ranks): valid slots equal the P:90 definition, masked slots are
+    not written (NaN sentinel kept)."""
+    import paper_2501_16103_b200 as M
+    G, E, k, T_l, H, N = 4, 16, 4, 64, 64, 256
+    T = G * T_l
+    rng = np.random.default_rng(11)
+    ids = synth.route_gumbel(11, T, E, k, s=1.2, n_empty=3)
+    mask = rng.random((T, k)) < 0.15
+    ids = np.where(mask, -1, ids).astype(np.int32)
+    X, W = synth.make_x(11, T, H, "int"), synth.make_w(11, E, H, N, "int")
+    El = E // G
+    Ws = [torch.from_numpy(W[r * El:(r + 1) * El]).to(torch.bfloat16).cuda() for r in range(G)]
+    Xs = [torch.from_numpy(X[r * T_l:(r + 1) * T_l]).to(torch.bfloat16).cuda() for r in range(G)]
+    tks = [torch.from_numpy(np.ascontiguousarray(ids[r * T_l:(r + 1) * T_l])).cuda() for r in range(G)]
+    outs = [torch.full((T_l * k, N), float("nan"), dtype=torch.float32, device="cuda") for _ in range(G)]
+    torch.cuda.synchronize()
+    eps = M.NativeExpertParallel.loopback_group(G, E, Ws, fused=fused)
+    errs = []
+
+    def body(r):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                eps[r].forward(tks[r], Xs[r], out=outs[r])
+            s.synchronize()
+        except Exception as e:  # pragma: no cover
+            errs.append(repr(e))
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(G)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=120)
+    assert not errs, errs
+    got = torch.cat([o.cpu() for o in outs]).double().numpy()
+    valid = (ids >= 0).reshape(-1)
+    ref = np.zeros((T * k, N))
+    for t in range(T):
+        for j in range(k):
+            if ids[t, j] >= 0:
+                ref[t * k + j] = X[t] @ W[ids[t, j]]
+    assert np.array_equal(got[valid], ref[valid])
+    assert np.isnan(got[~valid]).all()
