@@ -89,3 +89,13 @@ def test_expert_gemm_fp8_rank_one_closed_form():
     Y = ofp8.expert_gemm_fp8(X, W, tok, row_off, np.array([1.0, 0.125], dtype=np.float32))
     assert np.all(Y[:T] == H * 3.0) and np.all(Y[T:] == 0.125 * H * 3.0)
     assert np.array_equal(ofp8.expert_gemm_fp8_entries(X[:2], W[1][:, :3], 0.125), np.full((2, 3), 0.125 * H * 3.0))
+
+
+def test_rank_slices_match_full_generation():
+    """Expert-parallel ranks generate their own token rows / expert range of the same codes."""
+    torch = pytest.importorskip("torch")
+    X = sfp8.make_x_fp8(2, 12, 32)
+    assert np.array_equal(sfp8.make_x_fp8_torch(2, 4, 32, row0=8).numpy(), X[8:12])
+    W = sfp8.make_w_fp8(2, 4, 16, 24)
+    assert np.array_equal(sfp8.make_w_fp8_torch(2, 4, 16, 24, experts=range(2, 4), chunk=100).numpy(), W[2:4])
+    assert np.array_equal(sfp8.w_scale(3, 4096), np.full(3, 2.0 ** -6, dtype=np.float32))
