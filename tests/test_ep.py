@@ -301,3 +301,46 @@ def test_ep_native_loopback_masked_slots(fused):
                 ref[t * k + j] = X[t] @ W[ids[t, j]]
     assert np.array_equal(got[valid], ref[valid])
     assert np.isnan(got[~valid]).all()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("fp8", [False, True])
+def test_ep_native_full_size_sampled(fp8):
+    """bench.py --ep's launch configuration: the Mixtral shape (T 4096, E 8, top-2, H 4096,
+    N 14336) through the library's EP step (one NCCL rank, combine fused into the GEMM); sampled
+    (token, slot) rows and columns against the fp64 oracle within the north-star tolerance."""
+    import paper_2501_16103_b200 as M
+    from oracle import fp8 as ofp8
+    from synth import fp8 as sfp8
+    from synth import workloads as wl
+    c = synth.CONFIGS["mix"]
+    ids = synth.route(c, 0)
+    if fp8:
+        Xd = sfp8.make_x_fp8_torch(0, c.T, c.H, device="cuda")
+        Wd = sfp8.make_w_fp8_torch(0, c.E, c.H, c.N, device="cuda")
+        scale = sfp8.w_scale(c.E, c.H)
+        sc = torch.from_numpy(scale).cuda()
+    else:
+        Xd = synth.make_x_torch(0, c.T, c.H, device="cuda")
+        Wd = synth.make_w_torch(0, c.E, c.H, c.N, device="cuda")
+        sc = None
+    ep = M.NativeExpertParallel(M.moe_ep_unique_id(), 0, 1, c.E, Wd, w_scale=sc)
+    out = ep.forward(torch.from_numpy(ids).cuda(), Xd, out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(3)
+    toks = np.unique(np.concatenate([[0, c.T - 1], rng.integers(0, c.T, 10)]))
+    cols = np.unique(np.concatenate([[0, c.N - 1, 255, 256], rng.integers(0, c.N, 20)]))
+    got = out[torch.from_numpy(np.repeat(toks * c.k, c.k) + np.tile(np.arange(c.k), len(toks))).cuda()]
+    got = got[:, torch.from_numpy(cols).cuda()].cpu().double().numpy()
+    ref = np.zeros_like(got)
+    for i, t in enumerate(toks):
+        for j in range(c.k):
+            e = int(ids[t, j])
+            if fp8:
+                ref[i * c.k + j] = ofp8.expert_gemm_fp8_entries(sfp8.x_fp8_rows(0, c.T, c.H, [t]),
+                                                                sfp8.w_fp8_columns(0, c.E, c.H, c.N, e, cols), scale[e])[0]
+            else:
+                ref[i * c.k + j] = wl.x_rows(0, c.T, c.H, [t])[0] @ wl.w_columns(0, c.E, c.H, c.N, e, cols)
+    d = np.abs(got - ref)
+    assert (d <= 1e-2 * (np.abs(ref) + 1)).all(), d.max()
+    assert np.linalg.norm(got - ref) <= 2e-3 * np.linalg.norm(ref)
