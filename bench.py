@@ -595,6 +595,14 @@ def run_ours(args, cfg):
                "seconds": s}
 
     args.bm_resolved, args.bn_resolved = plan.bm, plan.bn
+    # Host planner time (Alg. 1 + sigma + task table for this step's counts; SURVEY §8(d) reports it
+    # apart from the kernel), median of 50 calls of moe_plan_build.
+    hp = []
+    for _ in range(50):
+        t0 = time.perf_counter()
+        M.moe_plan_build(counts_np.astype(np.int32), cfg.H, cfg.N, plan.bm, plan.bn)
+        hp.append((time.perf_counter() - t0) * 1e6)
+    host_plan_us = statistics.median(hp)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": ws, "steps": args.steps,
@@ -604,7 +612,10 @@ def run_ours(args, cfg):
             "scaling": "weak", "vs_baseline": None, "dtype": "fp8_e4m3" if fp8 else "bf16", "data": "synthetic",
             "config": config_dict(cfg, args),
             "pct_of_peak": value / peak,
+            "step_ms_median": statistics.median(step_ms), "step_ms_min": min(step_ms),
+            "host_plan_us": host_plan_us,
             "kernel": {"name": "moe_gemm_kernel", "ms_per_launch": gemm_avg, "tflops": achieved,
+                       "ms_per_launch_median": statistics.median(gemm_ms), "ms_per_launch_min": min(gemm_ms),
                        "ms_per_launch_after_memset_flush": statistics.mean(gemm_ms_dirty),
                        "pct_of_measured_burst_peak": achieved / peak,
                        "pct_of_measured_sustained_peak": achieved / (float(peaks["bf16_tflops_sustained"])
@@ -743,6 +754,16 @@ def run_ep(args, base):
                "h2d_bytes_per_step": int(X_h.numel() * X_h.element_size() + ids_h.numel() * 4) * ws,
                "d2h_bytes_per_step": int(out_h.numel() * out_h.element_size()) * ws}
     probe = M.Plan(None, cfg.H, cfg.N, args.bm, args.bn, E=El)     # the local GEMM's resolved tile shape
+    # rank 0's exchange traffic per step (rows out / in for dispatch and return, incl. its own share)
+    if native is not None:
+        lr = native.last_rows()
+        x_b = cfg.H * (1 if fp8 else 2)
+        y_b = cfg.N * (2 if out_dtype == torch.bfloat16 else 4)
+        exch_bytes = {"dispatch_rows_sent": lr["sent"], "dispatch_rows_received": lr["received"],
+                      "dispatch_bytes": (lr["sent"] + lr["received"]) * x_b,
+                      "combine_rows": lr["local_rows"], "combine_bytes": lr["local_rows"] * y_b}
+    else:
+        exch_bytes = None
     tile_ep = f"{probe.bm}x{probe.bn}"
     if rank == 0:
         line = {
@@ -759,6 +780,7 @@ def run_ep(args, base):
                                       ("NCCL all_to_all_single (torch.distributed): counts, dispatch rows, "
                                        "combine rows"), "l2": "flushed before every timed step (memset + read: clean L2)"},
             "pct_of_peak": value / (peak * ws),
+            "exchange_bytes_per_step_rank0": exch_bytes,
             "per_rank": [{"ms_per_step": float(g[0]), "gemm_ms": float(g[1]), "gemm_tflops": float(g[2])}
                          for g in gathered],
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
