@@ -857,14 +857,63 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) bulk_wait_group_read<0>();
         named_bar_sync(1, 32 * kEpiWarps);
       }
-      if (kSplit && t.kind == 1 && cg > 0) {
-        // Swap-AB tail tiles are drained by the first four epilogue warps alone.
-        // Wait for the transposing warps to finish this tile (always: besides freeing the staging
-        // buffers, it keeps these warps from running ahead — their arrivals on the next tile's
-        // tmem-empty barriers would otherwise complete this tile's phase early).
+      if (kSplit && t.kind == 1) {
+        // Swap-AB tail: drained by the first four epilogue warps (cg == 0) alone; TMEM lane = output
+        // column, TMEM column = tail token.  Wide tiles: TMEM block hf holds W columns t.ct * 512 +
+        // 256 hf + [0, 256) (128 per CTA).  Each 32 (columns) x 32 (tokens) block is transposed
+        // through the warp's smem buffer, then token rows leave as 16-byte stores (a warp covers 32
+        // columns of 4 (fp32) / 8 (bf16) rows).
+        if (cg == 0) {
+          uint8_t* buf = smem + (sEpi - base) + (warp - (kMmaWarp + 1)) * (32 * 32 * 4);
+          const int esz = a.y_f32 ? 4 : 2;
+#pragma unroll 1
+          for (int hf = 0; hf < kHalves; ++hf) {
+          wait_block1(hf);
+          const int slot = kWide ? hf : acc;
+          const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + slot * kAccCols;
+          const int bnb = t.bn / kHalves;               // columns of one TMEM block
+          const int col0 = t.ct * t.bn + hf * bnb + (int)rank * (bnb / kCta) + q * 32;   // this warp's 32 columns
+          // TMEM lanes past this CTA's bnb / 2 columns (a box rounds up to 64) belong to the peer / next block
+          const int col_lim = min(t.ct * t.bn + hf * bnb + ((int)rank + 1) * (bnb / kCta), a.N);
+          for (int c = 0; c < t.height; c += 32) {
+            uint32_t r[32];
+            tmem_ld32(taddr + c, r);
+            tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {              // token c+j, column lane -> buf[j][lane]
+              if (a.y_f32)
+                reinterpret_cast<uint32_t*>(buf)[j * 32 + lane] = r[j];
+              else
+                reinterpret_cast<__nv_bfloat16*>(buf)[j * 32 + lane] = __float2bfloat16_rn(__uint_as_float(r[j]));
+            }
+            __syncwarp();
+            const int vec_per_row = 32 * esz / 16;      // 16-byte pieces per 32-column row segment
+            const int rows_per_pass = 32 / vec_per_row;
+            for (int j0 = 0; j0 < 32; j0 += rows_per_pass) {
+              const int j = j0 + lane / vec_per_row, piece = lane % vec_per_row;
+              const int tok = c + j;
+              const int col = col0 + piece * (16 / esz);
+              if (tok < t.rows && col < col_lim) {
+                const int64_t yr = a.y_row_map ? (int64_t)__ldg(a.y_row_map + t.row0 + tok) : (int64_t)t.row0 + tok;
+                const uint4 val = *reinterpret_cast<const uint4*>(buf + j * 32 * esz + piece * 16);
+                *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(a.Y) + (yr * a.N + col) * esz) = val;
+              }
+            }
+            __syncwarp();
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            if constexpr (kCta == 2) mbar_arrive_cluster(leader(tempty_bar(slot)));
+            else mbar_arrive(tempty_bar(slot));
+          }
+          }
+        }
+        // Every epilogue warp meets here (one barrier site): the staging buffers are free again, and
+        // the other warps cannot run ahead — their arrivals on the next tile's tmem-empty barriers
+        // would otherwise complete this tile's phase early.
         named_bar_sync(1, 32 * kEpiWarps);
-        __syncwarp();
-        if (lane == 0) {
+        if (cg > 0 && lane == 0) {
           if constexpr (kWide) {
             mbar_arrive_cluster(leader(tempty_bar(0)));
             mbar_arrive_cluster(leader(tempty_bar(1)));
@@ -872,64 +921,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_arrive_cluster(leader(tempty_bar(acc)));
           }
         }
-        if constexpr (kWide) {
-          acc_phase ^= 1u;
-        } else if (++acc == 2) {
-          acc = 0;
-          acc_phase ^= 1u;
-        }
-        continue;
-      }
-      if (kSplit && t.kind == 1) {
-        // Swap-AB tail: TMEM lane = output column, TMEM column = tail token.  Wide tiles: TMEM block
-        // hf holds W columns t.ct * 512 + 256 hf + [0, 256) (128 per CTA).
-        // Transpose each 32 (columns) x 32 (tokens) block through this warp's smem buffer, then
-        // write token rows with 16-byte stores (a warp covers 32 columns of 4 (fp32) / 8 (bf16) rows).
-        uint8_t* buf = smem + (sEpi - base) + (warp - (kMmaWarp + 1)) * (32 * 32 * 4);
-        const int esz = a.y_f32 ? 4 : 2;
-#pragma unroll 1
-        for (int hf = 0; hf < kHalves; ++hf) {
-        wait_block1(hf);
-        const int slot = kWide ? hf : acc;
-        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + slot * kAccCols;
-        const int bnb = t.bn / kHalves;               // columns of one TMEM block
-        const int col0 = t.ct * t.bn + hf * bnb + (int)rank * (bnb / kCta) + q * 32;   // this warp's 32 columns
-        // TMEM lanes past this CTA's bnb / 2 columns (a box rounds up to 64) belong to the peer / next block
-        const int col_lim = min(t.ct * t.bn + hf * bnb + ((int)rank + 1) * (bnb / kCta), a.N);
-        for (int c = 0; c < t.height; c += 32) {
-          uint32_t r[32];
-          tmem_ld32(taddr + c, r);
-          tmem_wait_ld();
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {              // token c+j, column lane -> buf[j][lane]
-            if (a.y_f32)
-              reinterpret_cast<uint32_t*>(buf)[j * 32 + lane] = r[j];
-            else
-              reinterpret_cast<__nv_bfloat16*>(buf)[j * 32 + lane] = __float2bfloat16_rn(__uint_as_float(r[j]));
-          }
-          __syncwarp();
-          const int vec_per_row = 32 * esz / 16;      // 16-byte pieces per 32-column row segment
-          const int rows_per_pass = 32 / vec_per_row;
-          for (int j0 = 0; j0 < 32; j0 += rows_per_pass) {
-            const int j = j0 + lane / vec_per_row, piece = lane % vec_per_row;
-            const int tok = c + j;
-            const int col = col0 + piece * (16 / esz);
-            if (tok < t.rows && col < col_lim) {
-              const int64_t yr = a.y_row_map ? (int64_t)__ldg(a.y_row_map + t.row0 + tok) : (int64_t)t.row0 + tok;
-              const uint4 val = *reinterpret_cast<const uint4*>(buf + j * 32 * esz + piece * 16);
-              *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(a.Y) + (yr * a.N + col) * esz) = val;
-            }
-          }
-          __syncwarp();
-        }
-        tc_fence_before();
         __syncwarp();
-        if (lane == 0) {
-          if constexpr (kCta == 2) mbar_arrive_cluster(leader(tempty_bar(slot)));
-          else mbar_arrive(tempty_bar(slot));
-        }
-        }
-        named_bar_sync(1, 32 * kEpiWarps);                     // transposes done (see the cg > 0 warps)
         if constexpr (kProf) c_work += clock64() - w0;
         if constexpr (kWide) {
           acc_phase ^= 1u;

@@ -204,7 +204,9 @@ __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
 // Named barrier over `count` threads (a multiple of 32) of the CTA; id 0 is __syncthreads.
+// bar.sync is warp-aligned: the warp is reconverged first (callers may arrive from lane-divergent code).
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t count) {
+  __syncwarp();
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 // Make this thread's generic-proxy shared-memory writes visible to the async proxy (tcgen05 / TMA).

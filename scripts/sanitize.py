@@ -54,7 +54,38 @@ def main():
     w = torch.rand((T, k), device="cuda")
     layer.forward(Xd, topk, w)
     torch.cuda.synchronize()
-    print(f"sanitize workload ok: {n} GEMM variants + CSR rows + both route paths + FFN layer")
+    # decode tiles with the balanced grid (more tiles than SMs), and the library's EP step over the
+    # loopback transport (2 virtual ranks, one thread each), combine fused into the epilogue
+    Td, Hd, Nd = 16, 256, 14336
+    idd = synth.route_gumbel(2, Td, 8, 2)
+    Xq, Wq = synth.make_x(2, Td, Hd, "int"), synth.make_w(2, 8, Hd, Nd, "int")
+    Yd, *_ = M.moe_forward(torch.from_numpy(idd).cuda(), torch.from_numpy(Xq).to(torch.bfloat16).cuda(),
+                           torch.from_numpy(Wq).to(torch.bfloat16).cuda(), 8, bm=128, bn=256, out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    c3, r3, t3, s3 = omoe.buckets(idd, 8)
+    assert np.array_equal(Yd.cpu().double().numpy(), omoe.expert_gemm(Xq, Wq, t3, r3))
+    import threading
+    G, Tl = 2, 64
+    ide = synth.route_gumbel(3, G * Tl, 8, 2)
+    Xe, We = synth.make_x(3, G * Tl, 64, "int"), synth.make_w(3, 8, 64, 256, "int")
+    eps = M.NativeExpertParallel.loopback_group(
+        G, 8, [torch.from_numpy(We[4 * r:4 * r + 4]).to(torch.bfloat16).cuda() for r in range(G)], fused=True)
+    outs = [None] * G
+
+    def body(r):
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            outs[r] = eps[r].forward(torch.from_numpy(np.ascontiguousarray(ide[r * Tl:(r + 1) * Tl])).cuda(),
+                                     torch.from_numpy(Xe[r * Tl:(r + 1) * Tl]).to(torch.bfloat16).cuda(),
+                                     out_dtype=torch.float32)
+        s.synchronize()
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(G)]
+    [t.start() for t in th]
+    [t.join() for t in th]
+    assert np.array_equal(torch.cat([o.cpu() for o in outs]).double().numpy(), omoe.per_slot_outputs(ide, Xe, We))
+    print(f"sanitize workload ok: {n} GEMM variants + CSR rows + both route paths + FFN layer + balanced decode "
+          f"grid + EP step (loopback, fused combine)")
 
 
 if __name__ == "__main__":
