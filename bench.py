@@ -227,7 +227,7 @@ def route_launches(T: int, E: int, k: int = 2) -> int:
     """Kernels one moe_route(_plan) call launches (route.cu): the single-block small-batch kernel
     when T <= 1024, E <= 16, k <= 8; else histogram + fused scan/compaction while chunks x experts
     <= 16384, else histogram + scan + compaction."""
-    if T <= 1024 and E <= 16 and k <= 8 and os.environ.get("MOE_ROUTE_SMALL", "1") != "0":
+    if T <= 1024 and E <= 16 and k <= 8:
         return 1
     chunks = max(1, -(-T // 1024))
     return 2 if chunks * E <= 16384 else 3
@@ -488,7 +488,8 @@ def run_ours(args, cfg):
     # rows routed anywhere, Y (out dtype) and the token-index array.
     counts_np = np.bincount(ids.ravel(), minlength=cfg.E)
     ybytes = 2 if out_dtype == torch.bfloat16 else 4
-    alg_bytes = (int((counts_np > 0).sum()) * cfg.H * cfg.N * esz + len(np.unique(ids)) * cfg.H * esz
+    n_tokens = int((ids >= 0).any(axis=1).sum())   # distinct tokens routed anywhere: each X row is read once
+    alg_bytes = (int((counts_np > 0).sum()) * cfg.H * cfg.N * esz + n_tokens * cfg.H * esz
                  + int(counts_np.sum()) * (cfg.N * ybytes + 4) + (4 * cfg.E if fp8 else 0))
     hbm = float(peaks["hbm_gbs"])
     mem_bound = flops / alg_bytes < peak * 1e12 / (hbm * 1e9)

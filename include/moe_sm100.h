@@ -52,6 +52,16 @@ typedef int32_t moe_status;
 #define MOE_ORDER_HALF_INTERVAL  8u  /* same sort; the i-th busiest task takes the i-th slot of the
                                         bit-reversal (van der Corput) sequence over the slots        */
 
+/* Launch options carried by the plan (moe_gemm reads them from the plan it is given; they never
+ * change Y).  Defaults are the measured-fastest choices; these exist for
+ * same-box A/B timing and for tests that pin the alternative paths.                                 */
+#define MOE_GRID_BALANCED  16u  /* persistent grid over ceil(tiles / ceil(tiles / CTAs)) CTAs (pairs), each
+                                   W or W-1 tiles (default for one-CTA tiles only)                    */
+#define MOE_GRID_STATIC    32u  /* plain static stride over all CTAs (pairs), never balanced           */
+#define MOE_A_GATHER4      64u  /* stage token rows with TMA tile::gather4 (one-CTA tiles) instead of
+                                   cp.async                                                           */
+#define MOE_EPI_REGISTER  128u  /* bf16 Y through masked register stores only (no TMA tile stores)    */
+
 /* Output element types of moe_gemm. */
 #define MOE_DTYPE_BF16 0
 #define MOE_DTYPE_F32  1
@@ -157,6 +167,22 @@ moe_status moe_plan_update(moe_plan* plan, const int32_t* counts_host, void* str
  */
 moe_status moe_plan_device(moe_plan* plan, const int32_t* counts_dev, void* stream);
 
+/*
+ * The tile shape (bm, bn) moe_plan_build's automatic rule (bm = bn = 0) picks for `rows` routed rows
+ * spread evenly over min(E, rows) experts: the expectation for a plan created before its counts exist.
+ * Pure host code.
+ */
+moe_status moe_plan_suggest_tile(int64_t rows, int32_t E, int64_t H, int64_t N, int32_t* bm, int32_t* bn);
+
+/*
+ * moe_plan_create(NULL counts, ...) for a device-planned step whose batch has about expected_rows routed
+ * rows (T * k): with bm = bn = 0 the tile shape is moe_plan_suggest_tile(expected_rows, ...), so a
+ * C-ABI caller gets the shape the automatic rule would choose for its batch (e.g. one-CTA tiles for a
+ * decode step) instead of the count-free default.  Other arguments as moe_plan_create.
+ */
+moe_status moe_plan_create_expected(int64_t expected_rows, int32_t E, int64_t H, int64_t N, int32_t bm, int32_t bn,
+                                    uint32_t flags, void* stream, moe_plan** out);
+
 /* Copy a device-planned blob back to the host (synchronises `stream`; NULL = plan's stream). */
 moe_status moe_plan_sync(moe_plan* plan, void* stream);
 
@@ -200,6 +226,20 @@ moe_status moe_route(const int32_t* topk_ids_dev, int64_t T, int32_t k, int32_t 
 moe_status moe_route_plan(const int32_t* topk_ids_dev, int64_t T, int32_t k, int32_t E,
                           int32_t* counts_dev, int32_t* row_off_dev, int32_t* token_idx_dev,
                           int32_t* slot_dev, int32_t* status_dev, moe_plan* plan, void* stream);
+
+/*
+ * moe_route / moe_route_plan with explicit kernel-path options (same results on every path; for
+ * same-box timing and for tests that pin each path):
+ *   MOE_ROUTE_NO_SMALL       never the single-block small-batch kernel (T <= 1024, E <= 16, k <= 8)
+ *   MOE_ROUTE_THREE_KERNELS  histogram + scan block + compaction instead of the fused two-kernel form
+ * plan: NULL (moe_route) or a plan to fill on the device (moe_route_plan).
+ */
+#define MOE_ROUTE_NO_SMALL       1u
+#define MOE_ROUTE_THREE_KERNELS  2u
+moe_status moe_route_ex(const int32_t* topk_ids_dev, int64_t T, int32_t k, int32_t E,
+                        int32_t* counts_dev, int32_t* row_off_dev, int32_t* token_idx_dev,
+                        int32_t* slot_dev, int32_t* status_dev, moe_plan* plan, uint32_t route_flags,
+                        void* stream);
 
 /*
  * The hot path: Y[row0 + r, n] = sum_h X[token_idx[row0 + r], h] * W[e, h, n]

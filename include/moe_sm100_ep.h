@@ -108,11 +108,16 @@ typedef struct moe_ep moe_ep;     /* opaque, library-owned */
  * broadcasts it.  MOE_ERR_NCCL when libnccl.so.2 cannot be loaded or fails. */
 moe_status moe_ep_unique_id(void* id_out);
 
+/* moe_ep_create flags. */
+#define MOE_EP_UNFUSED 1u   /* one rank: return result rows through the send buffer + exchange instead
+                               of storing them from the GEMM epilogue into the receive buffer (A/B) */
+
 /* Collective over `world` ranks (blocking until all joined): communicator for this rank.
  * E % world == 0 experts; rank g owns experts [g E/world, (g+1) E/world).  bm / bn: the local
- * GEMM's tile shape (0: the planner's choice).  The calling thread's current CUDA device is used. */
+ * GEMM's tile shape (0: the planner's choice).  flags: MOE_EP_* above.  The calling thread's
+ * current CUDA device is used.  Step scratch comes from a memory pool owned by the handle. */
 moe_status moe_ep_create(const void* unique_id, int32_t rank, int32_t world, int32_t E, int32_t bm, int32_t bn,
-                         moe_ep** out);
+                         uint32_t flags, moe_ep** out);
 
 /*
  * One step.  topk_dev [T, k] int32 global expert ids of this rank's T tokens (negative = masked);

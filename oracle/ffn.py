@@ -81,3 +81,29 @@ def swiglu_rows(X, W_gate, W_up, token_idx, row_off, h_bf16: bool = True):
 def sigmoid_scalar(z: float) -> float:
     """Reference scalar for pins: 1 / (1 + e^-z)."""
     return 1.0 / (1.0 + math.exp(-z))
+
+
+def moe_ffn_entries(x_row, w_gate_e, w_up_e, w_down_cols, topk_ids, topk_w, tokens, cols, h_bf16: bool = True):
+    """Sampled entries of moe_ffn: out[i, c] = sum_j topk_w[t_i, j] * expert_ffn(X[t_i], e(t_i, j))[cols[c]]
+    (R14), the same definition with inputs fetched on demand so a full-size layer can be checked
+    without materialising every weight on the host: x_row(t) -> [H], w_gate_e(e) / w_up_e(e) -> [H, I],
+    w_down_cols(e, cols) -> [I, len(cols)].  Experts are visited one at a time (one expert's
+    weights in memory)."""
+    topk_ids = np.asarray(topk_ids)
+    tokens = [int(t) for t in tokens]
+    out = np.zeros((len(tokens), len(cols)))
+    xs = {t: np.asarray(x_row(t), dtype=np.float64)[None, :] for t in set(tokens)}
+    experts = sorted({int(topk_ids[t, j]) for t in tokens for j in range(topk_ids.shape[1]) if topk_ids[t, j] >= 0})
+    for e in experts:
+        g_w, u_w = np.asarray(w_gate_e(e), dtype=np.float64), np.asarray(w_up_e(e), dtype=np.float64)
+        d_w = np.asarray(w_down_cols(e, cols), dtype=np.float64)
+        for i, t in enumerate(tokens):
+            for j in range(topk_ids.shape[1]):
+                if int(topk_ids[t, j]) != e:
+                    continue
+                h = silu(xs[t] @ g_w) * (xs[t] @ u_w)
+                if h_bf16:
+                    h = round_bf16(h)
+                out[i] += float(topk_w[t, j]) * (h @ d_w)[0]
+        del g_w, u_w, d_w
+    return out

@@ -20,8 +20,11 @@ LIB_PATH = os.environ.get("MOE_LIB") or os.path.join(HERE, "libmoe_sm100.so")
 MOE_OK, MOE_OK_EMPTY = 0, 1
 MOE_ERR = {-1: "INVALID", -2: "UNSUPPORTED", -3: "CAPACITY", -4: "CUDA", -5: "NCCL"}
 MOE_DTYPE_BF16, MOE_DTYPE_F32, MOE_DTYPE_E4M3 = 0, 1, 2
+MOE_EP_UNFUSED = 1
 MOE_PAD_MAX, MOE_PAD_REPEAT, MOE_SPLIT_TAIL = 0, 1, 2
 MOE_ORDER_ALTERNATING, MOE_ORDER_HALF_INTERVAL = 4, 8
+MOE_GRID_BALANCED, MOE_GRID_STATIC, MOE_A_GATHER4, MOE_EPI_REGISTER = 16, 32, 64, 128
+MOE_ROUTE_NO_SMALL, MOE_ROUTE_THREE_KERNELS = 1, 2
 MOE_PLAN_MAGIC = 0x4D4F4531
 MOE_PLAN_HEADER = 16
 MOE_PLAN_TASK_WORDS = 8
@@ -36,6 +39,7 @@ EXPORTED = (
     "moe_gemm_swiglu", "moe_combine", "moe_gemm_fp8", "moe_gemm_fp8_rowmap", "moe_gemm_fp8_profile",
     "moe_ep_unique_id", "moe_ep_create", "moe_ep_forward", "moe_ep_last_rows", "moe_ep_last_gemm_ms",
     "moe_ep_destroy", "moe_ep_create_loopback", "moe_ep_combine_ptr", "moe_gemm_rowptr",
+    "moe_route_ex", "moe_plan_suggest_tile", "moe_plan_create_expected",
 )
 
 
@@ -74,6 +78,13 @@ def lib() -> ctypes.CDLL:
         "moe_route": (ctypes.c_int32, [vp, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, vp, vp, vp, vp, vp, vp]),
         "moe_route_plan": (ctypes.c_int32, [vp, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, vp, vp, vp, vp, vp,
                                             vp, vp]),
+        "moe_route_ex": (ctypes.c_int32, [vp, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, vp, vp, vp, vp, vp,
+                                          vp, ctypes.c_uint32, vp]),
+        "moe_plan_suggest_tile": (ctypes.c_int32, [ctypes.c_int64, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64,
+                                                   c_i32p, c_i32p]),
+        "moe_plan_create_expected": (ctypes.c_int32, [ctypes.c_int64, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64,
+                                                      ctypes.c_int32, ctypes.c_int32, ctypes.c_uint32, vp,
+                                                      ctypes.POINTER(vp)]),
         "moe_gemm": (ctypes.c_int32, [vp, vp, ctypes.c_int64, vp, vp, vp, ctypes.c_int32, vp]),
         "moe_decode_debug": (ctypes.c_int32, [vp, vp, vp]),
         "moe_device_info": (ctypes.c_int32, [c_i32p, c_i32p, c_i32p]),
@@ -97,7 +108,7 @@ def lib() -> ctypes.CDLL:
         "moe_gemm_fp8_profile": (ctypes.c_int32, [vp, vp, ctypes.c_int64, vp, vp, vp, vp, ctypes.c_int32, vp, vp]),
         "moe_ep_unique_id": (ctypes.c_int32, [vp]),
         "moe_ep_create": (ctypes.c_int32, [vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
-                                           ctypes.c_int32, ctypes.POINTER(vp)]),
+                                           ctypes.c_int32, ctypes.c_uint32, ctypes.POINTER(vp)]),
         "moe_ep_forward": (ctypes.c_int32, [vp, vp, ctypes.c_int64, ctypes.c_int32, vp, ctypes.c_int64,
                                             ctypes.c_int32, vp, ctypes.c_int64, vp, vp, ctypes.c_int32, vp]),
         "moe_ep_last_rows": (ctypes.c_int32, [vp, c_i64p, c_i64p, c_i64p]),
@@ -169,15 +180,11 @@ def _stream(stream=None) -> int:
 
 
 def suggest_tile(rows: int, E: int, H: int, N: int) -> tuple[int, int]:
-    """Tile shape (bm, bn) the automatic rule picks for `rows` routed rows spread evenly over
-    min(E, rows) experts — for plans created before the counts exist (device-built plans,
-    P:142): the device planner keeps the shape chosen at creation."""
-    active = max(1, min(int(E), int(rows)))
-    per = max(1, -(-int(rows) // active))
-    counts = np.zeros(E, dtype=np.int32)
-    counts[:active] = per
-    b = parse_plan_blob(moe_plan_build(counts, H, N, 0, 0))
-    return b["bm"], b["bn"]
+    """Tile shape (bm, bn) the library's automatic rule picks for `rows` routed rows spread evenly over
+    min(E, rows) experts (moe_plan_suggest_tile) — for plans created before the counts exist."""
+    bm, bn = ctypes.c_int32(), ctypes.c_int32()
+    _check(lib().moe_plan_suggest_tile(int(rows), int(E), int(H), int(N), ctypes.byref(bm), ctypes.byref(bn)))
+    return bm.value, bn.value
 
 
 class Plan:
@@ -259,7 +266,8 @@ def moe_device_info() -> tuple[int, int, int]:
     return n.value, ma.value, mi.value
 
 
-def moe_route(topk_ids, E: int, with_slot: bool = True, stream=None, plan: "Plan | None" = None):
+def moe_route(topk_ids, E: int, with_slot: bool = True, stream=None, plan: "Plan | None" = None,
+              route_flags: int = 0):
     """topk_ids: int32 CUDA tensor [T, k] -> (counts[E], row_off[E+1], token_idx[T*k], slot, status).
 
     With masked (negative) or invalid ids only the first sum(counts) = row_off[E] entries of
@@ -276,10 +284,13 @@ def moe_route(topk_ids, E: int, with_slot: bool = True, stream=None, plan: "Plan
     status = torch.zeros(1, dtype=torch.int32, device=dev)
     args = (topk_ids.data_ptr(), T, k, E, counts.data_ptr(), row_off.data_ptr(), token_idx.data_ptr(),
             slot.data_ptr() if slot is not None else None, status.data_ptr())
-    if plan is None:
+    if route_flags:                              # explicit kernel path (moe_route_ex)
+        _check(lib().moe_route_ex(*args, plan.handle if plan is not None else None, route_flags, _stream(stream)))
+    elif plan is None:
         _check(lib().moe_route(*args, _stream(stream)))
     else:                                        # fused with the device planner (moe_route_plan)
         _check(lib().moe_route_plan(*args, plan.handle, _stream(stream)))
+    if plan is not None:
         plan.device_resident = True
     return counts, row_off, token_idx[: T * k], (slot[: T * k] if slot is not None else None), status
 
@@ -554,18 +565,24 @@ class NativeExpertParallel:
     unique_id: 128 bytes from moe_ep_unique_id() on rank 0, shared by the caller."""
 
     def __init__(self, unique_id: bytes, rank: int, world: int, E: int, W_local, w_scale=None, bm: int = 0,
-                 bn: int = 0, handle=None):
+                 bn: int = 0, handle=None, fused: bool = True):
         import torch
 
         self.W, self.w_scale, self.E, self.world = W_local, w_scale, E, world
         self.fp8 = W_local.dtype in (torch.uint8, torch.float8_e4m3fn)
+        assert W_local.is_cuda and W_local.is_contiguous() and W_local.dim() == 3
+        assert W_local.shape[0] == E // world, "W_local must hold this rank's E / world experts"
+        assert self.fp8 or W_local.dtype == torch.bfloat16
+        if w_scale is not None:
+            assert self.fp8 and w_scale.dtype == torch.float32 and w_scale.is_contiguous()
+            assert w_scale.numel() == W_local.shape[0]
         if handle is not None:                     # from loopback_group (test transport)
             self._h = handle
             return
         assert len(unique_id) == 128
         self._h = ctypes.c_void_p()
         _check(lib().moe_ep_create(ctypes.create_string_buffer(unique_id, 128), rank, world, E, bm, bn,
-                                   ctypes.byref(self._h)))
+                                   0 if fused else MOE_EP_UNFUSED, ctypes.byref(self._h)))
 
     @staticmethod
     def loopback_group(world: int, E: int, W_locals, w_scales=None, bm: int = 0, bn: int = 0, fused: bool = False):
@@ -584,8 +601,13 @@ class NativeExpertParallel:
         T, k = topk_local.shape
         N = self.W.shape[2]
         assert X_local.is_contiguous() and topk_local.dtype == torch.int32 and topk_local.is_contiguous()
+        assert X_local.dim() == 2 and X_local.shape[0] == T and X_local.shape[1] == self.W.shape[1], \
+            "X_local must be [T, H] with the experts' H"
+        x_fp8 = X_local.dtype in (torch.uint8, torch.float8_e4m3fn)
+        assert x_fp8 == self.fp8 and (x_fp8 or X_local.dtype == torch.bfloat16), "X and W must both be bf16 or E4M3"
         if out is None:
             out = torch.empty((T * k, N), dtype=out_dtype, device=X_local.device)
+        assert out.is_contiguous() and tuple(out.shape) == (T * k, N) and out.dtype in (torch.bfloat16, torch.float32)
         _check(lib().moe_ep_forward(self._h, topk_local.data_ptr(), T, k, X_local.data_ptr(), X_local.shape[1],
                                     MOE_DTYPE_E4M3 if self.fp8 else MOE_DTYPE_BF16, self.W.data_ptr(), N,
                                     self.w_scale.data_ptr() if self.w_scale is not None else None, out.data_ptr(),

@@ -21,6 +21,16 @@ constexpr int kThreads = 1024;
 
 __device__ __forceinline__ bool owns(int e, int d, int El) { return e >= 0 && e / El == d; }
 
+// Slot j of a token's top-k row counts only at the first occurrence of its expert id: a repeated
+// id is an invalid input that moe_route drops (R10), so dispatch must neither count nor
+// forward it (the receiving rank's route would drop it and the return-row totals would disagree).
+__device__ __forceinline__ bool first_slot(const int32_t* __restrict__ row, int j) {
+  const int e = row[j];
+  for (int i = 0; i < j; ++i)
+    if (row[i] == e) return false;
+  return true;
+}
+
 // Block d: rows to send to d (tokens with >= 1 slot owned by d) and result rows d returns
 // (slots owned by d).
 __global__ void __launch_bounds__(kThreads)
@@ -29,7 +39,8 @@ __global__ void __launch_bounds__(kThreads)
   int rows = 0, slots = 0;
   for (int t = threadIdx.x; t < T; t += blockDim.x) {
     int n = 0;
-    for (int j = 0; j < k; ++j) n += owns(topk[(int64_t)t * k + j], d, El);
+    const int32_t* row = topk + (int64_t)t * k;
+    for (int j = 0; j < k; ++j) n += owns(row[j], d, El) && first_slot(row, j);
     rows += n > 0;
     slots += n;
   }
@@ -91,9 +102,10 @@ __global__ void __launch_bounds__(kThreads)
     if (hit) {
       const int pos = base + woff + __popc(m & lt);
       send_tok[pos] = t;
+      const int32_t* row = topk + (int64_t)t * k;
       for (int j = 0; j < k; ++j) {
-        const int e = topk[(int64_t)t * k + j];
-        send_meta[(int64_t)pos * k + j] = owns(e, d, El) ? e - d * El : -1;
+        const int e = row[j];
+        send_meta[(int64_t)pos * k + j] = owns(e, d, El) && first_slot(row, j) ? e - d * El : -1;
       }
     }
     base += tot;

@@ -75,22 +75,39 @@ const NcclApi& nccl() {
     if (s_ < 0) return s_;                \
   } while (0)
 
-// Stream-ordered scratch, released on the same stream when the step returns.
+// Stream-ordered scratch from the handle's private memory pool, released on the same stream when
+// the step returns (the pool keeps the blocks: no trip to the OS at the step's synchronisation).
 struct Scratch {
   cudaStream_t s;
+  cudaMemPool_t pool;
   std::vector<void*> bufs;
-  explicit Scratch(cudaStream_t st) : s(st) {}
+  Scratch(cudaStream_t st, cudaMemPool_t p) : s(st), pool(p) {}
   ~Scratch() {
     for (void* p : bufs) cudaFreeAsync(p, s);
   }
   template <class T>
   T* get(size_t n, cudaError_t* err) {
     void* p = nullptr;
-    *err = cudaMallocAsync(&p, n ? n * sizeof(T) : 16, s);
+    *err = cudaMallocFromPoolAsync(&p, n ? n * sizeof(T) : 16, pool, s);
     if (*err == cudaSuccess) bufs.push_back(p);
     return static_cast<T*>(p);
   }
 };
+
+// A device memory pool private to one moe_ep handle, never trimmed (release threshold = max).
+cudaError_t make_pool(cudaMemPool_t* pool) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  cudaMemPoolProps props = {};
+  props.allocType = cudaMemAllocationTypePinned;
+  props.location.type = cudaMemLocationTypeDevice;
+  props.location.id = dev;
+  e = cudaMemPoolCreate(pool, &props);
+  if (e != cudaSuccess) return e;
+  uint64_t keep = UINT64_MAX;
+  return cudaMemPoolSetAttribute(*pool, cudaMemPoolAttrReleaseThreshold, &keep);
+}
 
 // Test transport (moe_ep_create_loopback): G virtual ranks of one process on one device, each
 // driven by its own host thread and stream; an exchange publishes the source buffer and its
@@ -201,6 +218,7 @@ struct moe_ep {
   // Fused combine: the GEMM epilogue stores result rows into the owners' receive buffers (this
   // rank's own with one rank; the peers' with the loopback transport).  Persistent, grow-only.
   bool fused = false;
+  cudaMemPool_t pool = nullptr;                   // step scratch (private to this handle)
   char* rows_buf = nullptr;
   int32_t* meta_buf = nullptr;
   int64_t cap_bytes = 0, cap_rows = 0;
@@ -219,11 +237,12 @@ moe_status moe_ep_unique_id(void* id_out) {
 }
 
 moe_status moe_ep_create(const void* unique_id, int32_t rank, int32_t world, int32_t E, int32_t bm, int32_t bn,
-                         moe_ep** out) {
+                         uint32_t flags, moe_ep** out) {
   moe::clear_error();
   if (!unique_id || !out) MOE_FAIL(MOE_ERR_INVALID, "moe_ep_create: null argument");
   if (world < 1 || rank < 0 || rank >= world || E < 1 || E % world)
     MOE_FAIL(MOE_ERR_INVALID, "moe_ep_create: rank %d, world %d, E %d (E %% world must be 0)", rank, world, E);
+  if (flags & ~MOE_EP_UNFUSED) MOE_FAIL(MOE_ERR_INVALID, "moe_ep_create: unknown flags 0x%x", flags);
   if (!nccl().ok) MOE_FAIL(MOE_ERR_NCCL, "moe_ep_create: libnccl.so.2 not loadable");
   moe_ep* ep = new moe_ep;
   ep->rank = rank;
@@ -231,12 +250,10 @@ moe_status moe_ep_create(const void* unique_id, int32_t rank, int32_t world, int
   ep->E = E;
   ep->bm = bm;
   ep->bn = bn;
-  {
-    // With one rank the combine never leaves the device: fuse it into the GEMM epilogue.  Between
-    // GPUs the same path needs the peers' buffers mapped (CUDA IPC), not built yet: NCCL exchange.
-    const char* f = getenv("MOE_EP_FUSED");
-    ep->fused = world == 1 && !(f && atoi(f) == 0);
-  }
+  // With one rank the combine never leaves the device: fuse it into the GEMM epilogue (moe_gemm_rowptr,
+  // which has no bm = 64 decode-tile form: those tiles keep the send buffer + exchange).  Between
+  // GPUs the same path needs the peers' buffers mapped (CUDA IPC), not built yet: NCCL exchange.
+  ep->fused = world == 1 && !(flags & MOE_EP_UNFUSED) && bm != 64;
   ncclUniqueId id;
   std::memcpy(&id, unique_id, sizeof(id));
   ncclResult_t r = nccl().CommInitRank(&ep->comm, world, id, rank);
@@ -244,21 +261,12 @@ moe_status moe_ep_create(const void* unique_id, int32_t rank, int32_t world, int
     delete ep;
     MOE_FAIL(MOE_ERR_NCCL, "ncclCommInitRank: %s", nccl().GetErrorString(r));
   }
-  {
-    // Step scratch comes from the device's default memory pool (cudaMallocAsync): keep freed
-    // blocks in the pool across the step's synchronisation instead of returning them to the OS.
-    int dev = 0;
-    cudaMemPool_t pool;
-    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t keep = UINT64_MAX;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-    }
-  }
-  if (cudaMallocHost((void**)&ep->host, host_staging_bytes(world)) != cudaSuccess ||
+  if (make_pool(&ep->pool) != cudaSuccess || cudaMallocHost((void**)&ep->host, host_staging_bytes(world)) != cudaSuccess ||
       cudaEventCreate(&ep->gemm_ev[0]) != cudaSuccess || cudaEventCreate(&ep->gemm_ev[1]) != cudaSuccess) {
     nccl().CommDestroy(ep->comm);
+    if (ep->pool) cudaMemPoolDestroy(ep->pool);
     delete ep;
-    MOE_FAIL(MOE_ERR_CUDA, "moe_ep_create: pinned staging");
+    MOE_FAIL(MOE_ERR_CUDA, "moe_ep_create: memory pool / pinned staging");
   }
   *out = ep;
   return MOE_OK;
@@ -279,7 +287,7 @@ moe_status moe_ep_forward(moe_ep* ep, const int32_t* topk, int64_t T, int32_t k,
   const int64_t y_row = N * (out_dtype == MOE_DTYPE_F32 ? 4 : 2);
   if (x_row % 16 || y_row % 16) MOE_FAIL(MOE_ERR_INVALID, "moe_ep_forward: rows must be multiples of 16 bytes");
   cudaStream_t s = (cudaStream_t)stream;
-  Scratch sc(s);
+  Scratch sc(s, ep->pool);
   cudaError_t err = cudaSuccess;
   auto chk = [&]() -> moe_status {
     if (err != cudaSuccess) MOE_FAIL(MOE_ERR_CUDA, "moe_ep_forward scratch: %s", cudaGetErrorString(err));
@@ -454,8 +462,8 @@ moe_status moe_ep_create_loopback(int32_t world, int32_t E, int32_t bm, int32_t 
     ep->bm = bm;
     ep->bn = bn;
     ep->lb = lb;
-    ep->fused = fused != 0;
-    if (cudaMallocHost((void**)&ep->host, host_staging_bytes(world)) != cudaSuccess ||
+    ep->fused = fused != 0 && bm != 64;
+    if (make_pool(&ep->pool) != cudaSuccess || cudaMallocHost((void**)&ep->host, host_staging_bytes(world)) != cudaSuccess ||
         cudaEventCreate(&ep->gemm_ev[0]) != cudaSuccess || cudaEventCreate(&ep->gemm_ev[1]) != cudaSuccess)
       MOE_FAIL(MOE_ERR_CUDA, "moe_ep_create_loopback: staging");
     eps_out[r] = ep;
@@ -491,6 +499,10 @@ void moe_ep_destroy(moe_ep* ep) {
   if (ep->plan) moe_plan_destroy(ep->plan);
   if (ep->comm) nccl().CommDestroy(ep->comm);
   if (ep->host) cudaFreeHost(ep->host);
+  if (ep->pool) {
+    cudaDeviceSynchronize();                       // frees enqueued on the step streams have run
+    cudaMemPoolDestroy(ep->pool);
+  }
   delete ep;
 }
 

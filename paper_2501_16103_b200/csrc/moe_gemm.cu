@@ -1396,15 +1396,21 @@ moe_status make_w_map(CUtensorMap* m, const void* W, int64_t E, int64_t H, int64
   return MOE_OK;
 }
 
+constexpr int kMaxDevices = 64;
+
+int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev < 0 || dev >= kMaxDevices ? 0 : dev;
+}
+
+// SM count of the current device (cached per device: a process may drive several GPUs).
 int sm_count_cached() {
-  static int n = 0;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-  });
-  return n;
+  static int n[kMaxDevices] = {};
+  static std::once_flag once[kMaxDevices];
+  const int dev = current_device();
+  std::call_once(once[dev], [dev] { cudaDeviceGetAttribute(&n[dev], cudaDevAttrMultiProcessorCount, dev); });
+  return n[dev];
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
@@ -1437,10 +1443,13 @@ cudaError_t set_attr() {
                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(want < kMaxSmem ? want : kMaxSmem));
 }
 
+// Function attributes are per device: set once for each device the process launches on.
 cudaError_t set_smem_attrs() {
-  static std::once_flag once;
-  static cudaError_t err = cudaSuccess;
-  std::call_once(once, [] {
+  static std::once_flag once[kMaxDevices];
+  static cudaError_t errs[kMaxDevices] = {};
+  const int dev = current_device();
+  cudaError_t& err = errs[dev];
+  std::call_once(once[dev], [&err] {
     cudaError_t e[16] = {set_attr<false, 1, false>(),      set_attr<true, 1, false>(),
                         set_attr<false, 1, false, false, false, true>(), set_attr<false, 2, false, false, false, true>(),
                         set_attr<false, 2, false, true, false, true>(), set_attr<true, 2, false, true, false, true>(),
@@ -1538,10 +1547,7 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
   bool tma_store = y_dtype == MOE_DTYPE_BF16 && !y_row_map && !y_row_ptr;
   if (y_row_ptr && (v.bm == kDecRows || (v.flags & MOE_SPLIT_TAIL) || W2))
     MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_gemm_rowptr: plain / pair / wide tiles only (no bm = 64, split tails, gating)");
-  {
-    const char* ep = getenv("MOE_EPI_TMA");        // timing studies: 0 = register stores only
-    if (ep && atoi(ep) == 0) tma_store = false;
-  }
+  if (v.flags & MOE_EPI_REGISTER) tma_store = false;   // plan option: register stores only
   if (tma_store) {
     // Rows of Y: the plan's total (host plan); a device plan's count is on the device, so the
     // map spans 2^31-1 rows — every box the kernel stores lies inside one task's rows.
@@ -1570,20 +1576,16 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
   a.prof = prof;
   a.y_row_map = y_row_map;
   a.y_row_ptr = y_row_ptr;
-  {
-    const char* b = getenv("MOE_BALANCE");          // 1: balanced grid on every tile shape, 0: never
-    a.balance = b ? atoi(b) != 0 : v.bm == 128;      // default: one-CTA (decode-regime) tiles
-  }
+  // Balanced grid: default for one-CTA (decode-regime) tiles; plan options force it on / off.
+  a.balance = (v.flags & MOE_GRID_BALANCED) ? 1 : (v.flags & MOE_GRID_STATIC) ? 0 : v.bm == 128;
   a.tma_store = tma_store ? 1 : 0;
   a.T = (int32_t)T;
   a.H = v.H;
   a.X = reinterpret_cast<const __nv_bfloat16*>(X);
   a.experiment = experiment;
-  {
-    const char* am = getenv("MOE_A_PATH");       // timing studies: force the A staging path
-    a.a_mode = !token_idx ? 2 : am && (atoi(am) == 0 || atoi(am) == 1) ? atoi(am) : kDefaultAMode;
-    if (fp8 && a.a_mode == 0) a.a_mode = 1;      // FP8 rows are staged by cp.async (or tile TMA)
-  }
+  // A staging: contiguous rows by tile TMA (token_idx NULL), TMA gather4 (plan option), else cp.async.
+  a.a_mode = !token_idx ? 2 : (v.flags & MOE_A_GATHER4) ? 0 : kDefaultAMode;
+  if (fp8 && a.a_mode == 0) a.a_mode = 1;        // FP8 rows are staged by cp.async (or tile TMA)
 
   if (v.bm == 256 && (v.bn / 2) % 16) MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_gemm: pair tiles need bn %% 32 == 0");
   cudaError_t attr_err = set_smem_attrs();

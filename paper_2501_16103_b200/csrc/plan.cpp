@@ -105,8 +105,11 @@ moe_status moe_plan_build(const int32_t* counts, int32_t E, int64_t H, int64_t N
     MOE_FAIL(MOE_ERR_UNSUPPORTED,
              "moe_plan_build: bn=%d must be a multiple of %d in [16, 256] (or of 32 in (256, 512] with bm=256)", bn,
              bm == 256 ? 32 : 16);
-  if (flags & ~(MOE_PAD_REPEAT | MOE_SPLIT_TAIL | MOE_ORDER_ALTERNATING | MOE_ORDER_HALF_INTERVAL))
+  if (flags & ~(MOE_PAD_REPEAT | MOE_SPLIT_TAIL | MOE_ORDER_ALTERNATING | MOE_ORDER_HALF_INTERVAL | MOE_GRID_BALANCED |
+                MOE_GRID_STATIC | MOE_A_GATHER4 | MOE_EPI_REGISTER))
     MOE_FAIL(MOE_ERR_INVALID, "moe_plan_build: unknown flags 0x%x", flags);
+  if ((flags & MOE_GRID_BALANCED) && (flags & MOE_GRID_STATIC))
+    MOE_FAIL(MOE_ERR_INVALID, "moe_plan_build: MOE_GRID_BALANCED and MOE_GRID_STATIC are exclusive");
   if ((flags & MOE_ORDER_ALTERNATING) && (flags & MOE_ORDER_HALF_INTERVAL))
     MOE_FAIL(MOE_ERR_INVALID, "moe_plan_build: choose one expert ordering");
   const bool split = (flags & MOE_SPLIT_TAIL) != 0;
@@ -306,6 +309,36 @@ moe_status moe_plan_create(const int32_t* counts, int32_t E, int64_t H, int64_t 
   }
   *out = p;
   return st;
+}
+
+moe_status moe_plan_suggest_tile(int64_t rows, int32_t E, int64_t H, int64_t N, int32_t* bm, int32_t* bn) {
+  moe::clear_error();
+  if (!bm || !bn) MOE_FAIL(MOE_ERR_INVALID, "moe_plan_suggest_tile: null output");
+  if (rows < 0 || E < 1) MOE_FAIL(MOE_ERR_INVALID, "moe_plan_suggest_tile: rows=%lld E=%d", (long long)rows, E);
+  // The automatic rule of moe_plan_build applied to `rows` routed rows spread evenly over
+  // min(E, rows) experts (the expectation for plans built before the counts exist).
+  const int64_t active = std::max<int64_t>(1, std::min<int64_t>(E, rows));
+  const int64_t per = std::max<int64_t>(1, ceil_div(rows, active));
+  if (per >= INT_MAX) MOE_FAIL(MOE_ERR_CAPACITY, "moe_plan_suggest_tile: rows per expert >= 2^31");
+  std::vector<int32_t> counts(E, 0);
+  for (int64_t e = 0; e < active; ++e) counts[e] = (int32_t)per;
+  std::vector<int32_t> blob(moe_plan_blob_words(E));
+  int64_t len = 0;
+  moe_status st = moe_plan_build(counts.data(), E, H, N, 0, 0, 0, blob.data(), (int64_t)blob.size(), &len);
+  if (st < 0) return st;
+  *bm = blob[7];
+  *bn = blob[8];
+  return MOE_OK;
+}
+
+moe_status moe_plan_create_expected(int64_t expected_rows, int32_t E, int64_t H, int64_t N, int32_t bm, int32_t bn,
+                                    uint32_t flags, void* stream, moe_plan** out) {
+  moe::clear_error();
+  if (bm == 0 && bn == 0) {
+    moe_status st = moe_plan_suggest_tile(expected_rows, E, H, N, &bm, &bn);
+    if (st < 0) return st;
+  }
+  return moe_plan_create(nullptr, E, H, N, bm, bn, flags, stream, out);
 }
 
 moe_status moe_plan_update(moe_plan* p, const int32_t* counts, void* stream) {

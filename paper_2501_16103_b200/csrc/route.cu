@@ -322,7 +322,8 @@ __global__ void __launch_bounds__(kChunk) route_scatter_kernel(const int32_t* __
 }
 
 moe_status route_impl(const int32_t* topk, int64_t T, int32_t k, int32_t E, int32_t* counts, int32_t* row_off,
-                      int32_t* token_idx, int32_t* slot, int32_t* status, moe_plan* plan, void* stream) {
+                      int32_t* token_idx, int32_t* slot, int32_t* status, moe_plan* plan, uint32_t route_flags,
+                      void* stream) {
   moe::clear_error();
   if (T < 0 || k < 1 || k > 32 || E < 1 || E > kMaxE)
     MOE_FAIL(MOE_ERR_INVALID, "moe_route: T=%lld k=%d E=%d outside T>=0, 1<=k<=32, 1<=E<=1024", (long long)T, k, E);
@@ -336,8 +337,9 @@ moe_status route_impl(const int32_t* topk, int64_t T, int32_t k, int32_t E, int3
   }
   cudaStream_t s = (cudaStream_t)stream;
   int32_t* blob = plan ? moe::plan_blob_dev_mut(plan) : nullptr;
-  const char* small_env = getenv("MOE_ROUTE_SMALL");   // MOE_ROUTE_SMALL=0: always the multi-kernel path
-  const bool small_ok = !(small_env && atoi(small_env) == 0);
+  if (route_flags & ~(MOE_ROUTE_NO_SMALL | MOE_ROUTE_THREE_KERNELS))
+    MOE_FAIL(MOE_ERR_INVALID, "moe_route_ex: unknown flags 0x%x", route_flags);
+  const bool small_ok = !(route_flags & MOE_ROUTE_NO_SMALL);
   if (small_ok && T <= kChunk && E <= kSmallMaxE && k <= kRegK) {
     route_small_kernel<<<1, kChunk, 0, s>>>(topk, (int)T, k, E, counts, row_off, token_idx, slot, status, pH, pN,
                                             pbm, pbn, pflags, blob);
@@ -353,10 +355,7 @@ moe_status route_impl(const int32_t* topk, int64_t T, int32_t k, int32_t E, int3
   int32_t* chunk = scratch;
   int32_t* chunk_bad = scratch + (size_t)n_chunks * E;
   route_hist_kernel<<<n_chunks, kChunk, 0, s>>>(topk, (int)T, k, E, chunk, chunk_bad);
-  static const bool force_split = [] {               // timing studies: MOE_ROUTE_SPLIT=1
-    const char* v = getenv("MOE_ROUTE_SPLIT");
-    return v && atoi(v) != 0;
-  }();
+  const bool force_split = (route_flags & MOE_ROUTE_THREE_KERNELS) != 0;
   if ((int64_t)n_chunks * E <= kPlaceMaxCells && T > 0 && !force_split) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(n_chunks, E);
@@ -389,12 +388,18 @@ moe_status route_impl(const int32_t* topk, int64_t T, int32_t k, int32_t E, int3
 extern "C" moe_status moe_route(const int32_t* topk, int64_t T, int32_t k, int32_t E, int32_t* counts,
                                 int32_t* row_off, int32_t* token_idx, int32_t* slot, int32_t* status,
                                 void* stream) {
-  return route_impl(topk, T, k, E, counts, row_off, token_idx, slot, status, nullptr, stream);
+  return route_impl(topk, T, k, E, counts, row_off, token_idx, slot, status, nullptr, 0, stream);
 }
 
 extern "C" moe_status moe_route_plan(const int32_t* topk, int64_t T, int32_t k, int32_t E, int32_t* counts,
                                      int32_t* row_off, int32_t* token_idx, int32_t* slot, int32_t* status,
                                      moe_plan* plan, void* stream) {
   if (!plan) MOE_FAIL(MOE_ERR_INVALID, "moe_route_plan: null plan");
-  return route_impl(topk, T, k, E, counts, row_off, token_idx, slot, status, plan, stream);
+  return route_impl(topk, T, k, E, counts, row_off, token_idx, slot, status, plan, 0, stream);
+}
+
+extern "C" moe_status moe_route_ex(const int32_t* topk, int64_t T, int32_t k, int32_t E, int32_t* counts,
+                                   int32_t* row_off, int32_t* token_idx, int32_t* slot, int32_t* status,
+                                   moe_plan* plan, uint32_t route_flags, void* stream) {
+  return route_impl(topk, T, k, E, counts, row_off, token_idx, slot, status, plan, route_flags, stream);
 }

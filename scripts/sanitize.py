@@ -37,10 +37,8 @@ def main():
     Yc = M.moe_gemm(plan, Xd.index_select(0, tok.long()).contiguous(), None, Wd, out_dtype=torch.float32)
     torch.cuda.synchronize()
     assert np.array_equal(Yc.cpu().double().numpy(), ref)
-    os.environ["MOE_ROUTE_SMALL"] = "0"
-    c2, r2, t2, s2, _ = M.moe_route(topk, E)
+    c2, r2, t2, s2, _ = M.moe_route(topk, E, route_flags=M.MOE_ROUTE_NO_SMALL)
     assert torch.equal(t2, tok)
-    os.environ.pop("MOE_ROUTE_SMALL")
     X8, W8 = sfp8.make_x_fp8(1, T, H, "int"), sfp8.make_w_fp8(1, E, H, N, "int")
     ref8 = ofp8.expert_gemm_fp8(X8, W8, rt, rr)
     for bm, bn in ((128, 256), (256, 512)):

@@ -1,0 +1,87 @@
+"""Same-box timing of moe_gemm launch variants (tile shape, plan flags, sigma order) on named configs.
+
+    python scripts/tile_probe.py --cases paper_worst:256:512:0:natural,paper_worst:256:512:2:half_interval
+        [--reps 20] [--out gpurun_out/probe.jsonl]
+
+A case is cfg:bm:bn:flags:order; flags is the integer moe_plan flag word (2 = MOE_SPLIT_TAIL, ...).
+Kernel time = CUDA events around one moe_gemm launch after a clean-L2 flush (bench.py's method),
+median over reps.  Prints one JSON line per case with TFLOP/s and the fraction of the measured peak.
+"""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2501_16103_b200 as M  # noqa: E402
+import synth  # noqa: E402
+
+ORDER = {"natural": 0, "alternating": M.MOE_ORDER_ALTERNATING, "half_interval": M.MOE_ORDER_HALF_INTERVAL}
+
+
+class CleanFlush:
+    def __init__(self):
+        self.w = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+        self.r = torch.ones(32 << 20, dtype=torch.int64, device="cuda")
+
+    def __call__(self):
+        self.w.zero_()
+        self.r.sum()
+
+
+def time_gemm(plan, X, tok, W, Y, flush, reps):
+    for _ in range(3):
+        M.moe_gemm(plan, X, tok, W, Y=Y)
+    ms = []
+    for _ in range(reps):
+        flush()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda._sleep(4_000_000)
+        a.record()
+        M.moe_gemm(plan, X, tok, W, Y=Y)
+        b.record()
+        b.synchronize()
+        ms.append(a.elapsed_time(b))
+    return float(np.median(ms)), float(np.min(ms))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--cases", required=True)
+    ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--out", default=None)
+    args = ap.parse_args()
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    peak = float(json.load(open(p))["bf16_tflops"]) if os.path.exists(p) else 1590.0
+    flush = CleanFlush()
+    cache = {}
+    out = open(args.out, "a") if args.out else None
+    for case in args.cases.split(","):
+        cfg, bm, bn, flags, order = case.split(":")
+        c = synth.CONFIGS[cfg]
+        if cfg not in cache:
+            cache.clear()
+            ids = torch.from_numpy(synth.route(c)).cuda()
+            counts, row_off, tok, _, _ = M.moe_route(ids, c.E)
+            X = synth.make_x_torch(0, c.T, c.H, device="cuda")
+            W = synth.make_w_torch(0, c.E, c.H, c.N, device="cuda")
+            Y = torch.empty((tok.numel(), c.N), dtype=torch.bfloat16, device="cuda")
+            cache[cfg] = (counts.cpu().numpy(), tok, X, W, Y)
+        counts_h, tok, X, W, Y = cache[cfg]
+        plan = M.Plan(counts_h, c.H, c.N, int(bm), int(bn), int(flags) | ORDER[order])
+        ms, mn = time_gemm(plan, X, tok, W, Y, flush, args.reps)
+        tf = c.flops / (ms * 1e-3) / 1e12
+        line = {"case": case, "tile": f"{plan.bm}x{plan.bn}", "tiles": plan.total_tiles, "ms": ms, "ms_min": mn,
+                "tflops": tf, "frac": tf / peak}
+        print(json.dumps(line), flush=True)
+        if out:
+            out.write(json.dumps(line) + "\n")
+
+
+if __name__ == "__main__":
+    main()

@@ -8,6 +8,9 @@ the torch twin (device side) produce identical BYTES and no floating-point round
 "normal" uses shift 6 (|value| <= 3.75, std ~1.1) for X and W alike; the W ~ N(0,1)/sqrt(H)
 magnitude of the bf16 recipe is carried by the per-expert fp32 scale 2**-w_scale_exp(H)
 (``w_scale``), the way FP8 weights are stored with a per-tensor scale.  "int" uses shift 0.
+"full": the code is the low byte of h itself — every finite E4M3 value, subnormals and
++-448 included, exponents spread over the whole format (the two NaN codes 0x7F / 0xFF map to
++-448, 0x7E / 0xFE); products and sums then need fp32 rounding (``w_scale``: 2**-(w_scale_exp(H)+8)).
 """
 from __future__ import annotations
 
@@ -15,7 +18,7 @@ import numpy as np
 
 from .workloads import STREAM_W, STREAM_X, _M32, _fmix32_np, _key, w_scale_exp
 
-SHIFT = {"normal": 6, "int": 0}
+SHIFT = {"normal": 6, "int": 0, "full": 0}
 
 
 def _c_np(seed: int, stream: int, idx: np.ndarray, mode: str) -> np.ndarray:
@@ -58,6 +61,11 @@ def encode_torch(c, shift: int):
 
 
 def _codes_np(seed, stream, idx, mode):
+    if mode == "full":
+        h = _fmix32_np((np.asarray(idx, dtype=np.int64).astype(np.uint64)
+                        ^ np.uint64(_key(seed, stream))).astype(np.uint32))
+        b = (h & np.uint32(255)).astype(np.uint8)
+        return np.where((b & np.uint8(127)) == 127, b ^ np.uint8(1), b).astype(np.uint8)
     return encode_np(_c_np(seed, stream, idx, mode), SHIFT[mode])
 
 
@@ -84,6 +92,8 @@ def w_fp8_columns(seed: int, E: int, H: int, N: int, e: int, cols, mode: str = "
 
 def w_scale(E: int, H: int, mode: str = "normal") -> np.ndarray:
     """Per-expert fp32 scale paired with make_w_fp8: 2**-w_scale_exp(H) ("normal"), 1 ("int")."""
+    if mode == "full":
+        return np.full(E, 2.0 ** -(w_scale_exp(H) + 8), dtype=np.float32)
     return np.full(E, 2.0 ** -w_scale_exp(H) if mode == "normal" else 1.0, dtype=np.float32)
 
 
@@ -101,6 +111,9 @@ def _codes_torch(seed, stream, start, count, mode, device):
         c = (h % 9) - 4
     elif mode == "normal":
         c = (h & 127) + ((h >> 8) & 127) + ((h >> 16) & 127) + ((h >> 24) & 127) - 254
+    elif mode == "full":
+        b = h & 255
+        return torch.where((b & 127) == 127, b ^ 1, b).to(torch.uint8)
     else:
         raise ValueError(mode)
     return encode_torch(c.to(torch.int32), SHIFT[mode])

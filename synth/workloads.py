@@ -25,6 +25,11 @@ Recipes (stated again in DESIGN.md §"Input recipe"):
   - "normal" mode: X = c * 2**-6 (std ~1.15); W = c * 2**-(6 + w_scale_exp(H))
     with ``w_scale_exp(H) = floor(log2(H)/2 + 1/2)`` (W ~ N(0,1)/sqrt(H)).
   - "int" mode: values (h mod 9) - 4 in {-4..4} (exact in bf16).
+  - "generic" mode: a full bf16 bit pattern built with integer operations — sign = bit 31
+    of h, a random 7-bit mantissa (bits 0-6), exponent offset ((h >> 8) & 15) - 8 (16 octaves) —
+    value = (-1)^s (1 + m/128) 2^(e_off + 2 - shift).  Unlike "normal", its products carry 16
+    significant bits over ~30 octaves, so fp32 accumulation must round (the regime the north
+    star's tolerance is for; tests/test_synth.py proves it with exact int64 sums).
 """
 from __future__ import annotations
 
@@ -189,7 +194,21 @@ def counter_values(seed: int, stream: int, index: np.ndarray, mode: str, shift: 
         c = ((h & np.uint32(127)) + ((h >> np.uint32(8)) & np.uint32(127))
              + ((h >> np.uint32(16)) & np.uint32(127)) + ((h >> np.uint32(24)) & np.uint32(127)))
         return (c.astype(np.float64) - 254.0) * 2.0 ** (-shift)
+    if mode == "generic":
+        bits = generic_bits_np(h, shift)
+        return ((bits.astype(np.uint32) << np.uint32(16)).view(np.float32)).astype(np.float64)
     raise ValueError(mode)
+
+
+def generic_bits_np(h: np.ndarray, shift: int) -> np.ndarray:
+    """bf16 bit patterns of "generic" mode (uint16): sign | biased exponent | 7-bit mantissa."""
+    h = np.asarray(h, dtype=np.uint32)
+    sign = (h >> np.uint32(31)) & np.uint32(1)
+    mant = h & np.uint32(127)
+    bexp = ((h >> np.uint32(8)) & np.uint32(15)).astype(np.int64) - 8 + 2 - shift + 127
+    if bexp.size and (bexp.min() < 1 or bexp.max() > 254):
+        raise ValueError("generic exponent outside the bf16 normal range")
+    return ((sign << np.uint32(15)) | (bexp.astype(np.uint32) << np.uint32(7)) | mant).astype(np.uint16)
 
 
 def _shift_x() -> int:
@@ -256,6 +275,11 @@ def counter_values_torch(seed: int, stream: int, start: int, count: int, mode: s
     if mode == "normal":
         c = (h & 127) + ((h >> 8) & 127) + ((h >> 16) & 127) + ((h >> 24) & 127)
         return ((c - 254).to(torch.float32) * (2.0 ** (-shift))).to(dtype)
+    if mode == "generic":                          # same integer recipe as generic_bits_np
+        bexp = ((h >> 8) & 15) - 8 + 2 - shift + 127
+        bits = (((h >> 31) & 1) << 15) | (bexp << 7) | (h & 127)
+        bits = torch.where(bits >= 32768, bits - 65536, bits).to(torch.int16)
+        return bits.view(torch.bfloat16).to(dtype)
     raise ValueError(mode)
 
 

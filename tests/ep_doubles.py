@@ -11,8 +11,12 @@ class CpuKernels:
         El = E // G
         counts2 = torch.zeros((G, 2), dtype=torch.int32)
         toks, metas, off = [], [], [0]
+        # a repeated id in a token's row counts once, at its first slot (as the CUDA kernels do)
+        first = torch.ones_like(topk, dtype=torch.bool)
+        for j in range(1, k):
+            first[:, j] = ~(topk[:, :j] == topk[:, j:j + 1]).any(1)
         for d in range(G):
-            own = (topk >= 0) & (topk // El == d)
+            own = (topk >= 0) & (topk // El == d) & first
             rows = torch.nonzero(own.any(1)).flatten()
             counts2[d, 0] = rows.numel()
             counts2[d, 1] = int(own.sum())

@@ -181,11 +181,10 @@ def test_ep_nccl_world1():
 @pytest.mark.parametrize("fused", ["1", "0"])
 @pytest.mark.parametrize("fp8", [False, True])
 @pytest.mark.parametrize("bm,bn", [(0, 0), (128, 256)])
-def test_ep_native_nccl_world1(fp8, bm, bn, fused, monkeypatch):
-    monkeypatch.setenv("MOE_EP_FUSED", fused)
+def test_ep_native_nccl_world1(fp8, bm, bn, fused):
     """The library's own expert-parallel step (moe_ep_create / moe_ep_forward: NCCL called from C++,
     a one-rank communicator on one GPU; the combine fused into the GEMM epilogue, and with
-    MOE_EP_FUSED=0 the send buffer + exchange) against the P:90 definition."""
+    MOE_EP_UNFUSED the send buffer + exchange) against the P:90 definition."""
     import paper_2501_16103_b200 as M
     E, k, T, H, N = 8, 2, 300, 64, 256
     if fp8:
@@ -194,7 +193,7 @@ def test_ep_native_nccl_world1(fp8, bm, bn, fused, monkeypatch):
     else:
         ids, X, W, ref = _problem(1, E, k, T, H, N, seed=4)
         Xd, Wd, sc = torch.from_numpy(X).to(torch.bfloat16).cuda(), torch.from_numpy(W).to(torch.bfloat16).cuda(), None
-    ep = M.NativeExpertParallel(M.moe_ep_unique_id(), 0, 1, E, Wd, w_scale=sc, bm=bm, bn=bn)
+    ep = M.NativeExpertParallel(M.moe_ep_unique_id(), 0, 1, E, Wd, w_scale=sc, bm=bm, bn=bn, fused=fused == "1")
     topk = torch.from_numpy(ids).cuda()
     for _ in range(2):                                   # the plan and the communicator are reused
         out = ep.forward(topk, Xd, out_dtype=torch.float32)
@@ -255,11 +254,14 @@ def test_ep_native_loopback_multirank(G, fp8, fused):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("repeat", [False, True])
 @pytest.mark.parametrize("fused", [False, True])
-def test_ep_native_loopback_masked_slots(fused):
+def test_ep_native_loopback_masked_slots(fused, repeat):
     """Masked slots (negative ids) and skewed routing with empty experts through the library's
     multi-rank step (G = 4 virtual ranks): valid slots equal the P:90 definition, masked slots are
-    not written (NaN sentinel kept)."""
+    not written (NaN sentinel kept).  repeat: some tokens list an expert twice (an invalid input,
+    DESIGN.md R10) — only the first slot of that expert is computed, the repeat stays unwritten and
+    nothing else is disturbed (repeated ids used to overrun the return metadata)."""
     import paper_2501_16103_b200 as M
     G, E, k, T_l, H, N = 4, 16, 4, 64, 64, 256
     T = G * T_l
@@ -267,6 +269,10 @@ def test_ep_native_loopback_masked_slots(fused):
     ids = synth.route_gumbel(11, T, E, k, s=1.2, n_empty=3)
     mask = rng.random((T, k)) < 0.15
     ids = np.where(mask, -1, ids).astype(np.int32)
+    if repeat:
+        rep = np.nonzero(rng.random(T) < 0.2)[0]
+        ids[rep, 2] = ids[rep, 0]
+        ids[rep[::2], 3] = ids[rep[::2], 1]
     X, W = synth.make_x(11, T, H, "int"), synth.make_w(11, E, H, N, "int")
     El = E // G
     Ws = [torch.from_numpy(W[r * El:(r + 1) * El]).to(torch.bfloat16).cuda() for r in range(G)]
@@ -293,7 +299,8 @@ def test_ep_native_loopback_masked_slots(fused):
         t.join(timeout=120)
     assert not errs, errs
     got = torch.cat([o.cpu() for o in outs]).double().numpy()
-    valid = (ids >= 0).reshape(-1)
+    first = np.array([[ids[t, j] not in ids[t, :j] for j in range(k)] for t in range(T)])
+    valid = ((ids >= 0) & first).reshape(-1)
     ref = np.zeros((T * k, N))
     for t in range(T):
         for j in range(k):
@@ -301,6 +308,8 @@ def test_ep_native_loopback_masked_slots(fused):
                 ref[t * k + j] = X[t] @ W[ids[t, j]]
     assert np.array_equal(got[valid], ref[valid])
     assert np.isnan(got[~valid]).all()
+    rows = [ep.last_rows() for ep in eps]
+    assert sum(r["local_rows"] for r in rows) == int(valid.sum())
 
 
 @pytest.mark.gpu

@@ -259,8 +259,9 @@ RAGGED_WIDE_BN = [                  # wide tiles narrower than 512: blocks of bn
                          + [c[:5] + (c[5], 256, "1", f) for c in RAGGED_WIDE_BN for f in (0, M.MOE_SPLIT_TAIL)]
                          + [c + (256, 64, "1", 0) for c in RAGGED_DECODE])
 @pytest.mark.parametrize("mode", ["int", "int_bf16", "normal"])
-def test_gemm_ragged(T, E, k, H, N, bn, bm, a_path, flags, mode, monkeypatch):
-    monkeypatch.setenv("MOE_A_PATH", a_path)          # A staging path: gather4 (0) / cp.async (1)
+def test_gemm_ragged(T, E, k, H, N, bn, bm, a_path, flags, mode):
+    if a_path == "0":                                  # A staging path: gather4 (plan option) / cp.async
+        flags |= M.MOE_A_GATHER4
     ids, X, W, Xd, Wd = _inputs(T, E, k, H, N, T + E, "int" if mode == "int_bf16" else mode)
     # int_bf16: bf16 output (the TMA-store epilogue for full 32-row quarters): the exact integer
     # accumulator rounded once to bf16, compared bit for bit with the fp64 reference so rounded.
@@ -504,13 +505,12 @@ def test_route_many_chunks_and_masked_slots():
                                               (32769, 2, 8, 0.0, "1"), (3, 1, 1, 0.0, "1"), (3, 1, 1, 0.0, "0"),
                                               (1024, 2, 8, 0.0, "1"), (1024, 2, 8, 0.0, "0"), (1000, 8, 16, 1.2, "1"),
                                               (1, 2, 8, 0.0, "1"), (77, 3, 5, 0.0, "1"), (1025, 2, 8, 0.0, "1")])
-def test_route_place_and_split_paths(T, k, E, skew, small, monkeypatch):
+def test_route_place_and_split_paths(T, k, E, skew, small):
     """chunks x experts <= 16K: histogram + fused scan/placement kernels (match_any groups);
     larger (20 chunks x 1024 experts): histogram + single-block scan + chunk x expert compaction;
-    T <= 1024, E <= 16, k <= 8: the single-block small-batch kernel (MOE_ROUTE_SMALL=0 forces the
+    T <= 1024, E <= 16, k <= 8: the single-block small-batch kernel (MOE_ROUTE_NO_SMALL forces the
     multi-kernel path).  All must give the oracle's buckets exactly, with masked slots and invalid
     entries (out of range, repeated in a token's row) dropped and reported."""
-    monkeypatch.setenv("MOE_ROUTE_SMALL", small)
     rng = np.random.default_rng(T + E)
     if skew > 0:
         ids = synth.route_gumbel(T, T, E, k, s=skew)
@@ -522,7 +522,8 @@ def test_route_place_and_split_paths(T, k, E, skew, small, monkeypatch):
     bad_t = rng.integers(0, T, size=3)
     if k >= 2:
         ids[bad_t, 1] = np.where(ids[bad_t, 0] >= 0, ids[bad_t, 0], E)   # repeat or out of range
-    counts, row_off, tok, slot, status = M.moe_route(torch.from_numpy(ids).cuda(), E)
+    counts, row_off, tok, slot, status = M.moe_route(torch.from_numpy(ids).cuda(), E,
+                                                     route_flags=0 if small == "1" else M.MOE_ROUTE_NO_SMALL)
     # reference: drop masked, out-of-range and repeated entries; tokens ascending per expert
     lists = [[] for _ in range(E)]
     for t in range(T):

@@ -239,3 +239,30 @@ def test_planner_errors():
     st = L.moe_plan_build(c.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), 3, 64, 128, 128, 256, 0,
                           blob.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), blob.size, ctypes.byref(n))
     assert st == moe_lib.MOE_OK_EMPTY
+
+
+def test_suggest_tile_in_library():
+    """moe_plan_suggest_tile (C ABI): the automatic rule applied to an even spread of the expected rows —
+    pair tiles (256 x 512) for Mix / DS-sized batches, one-CTA 128 x 256 for decode batches."""
+    assert moe_lib.suggest_tile(4096 * 2, 8, 4096, 14336) == (256, 512)
+    assert moe_lib.suggest_tile(8192 * 6, 64, 2048, 1408) == (256, 512)
+    assert moe_lib.suggest_tile(2, 8, 4096, 14336) == (128, 256)
+    assert moe_lib.suggest_tile(32, 8, 4096, 14336) == (128, 256)
+    # the same as building the even-spread plan by hand
+    counts = np.zeros(8, dtype=np.int32)
+    counts[:8] = 100
+    b = moe_lib.parse_plan_blob(moe_lib.moe_plan_build(counts, 4096, 14336, 0, 0))
+    assert moe_lib.suggest_tile(800, 8, 4096, 14336) == (b["bm"], b["bn"])
+    bm, bn = ctypes.c_int32(), ctypes.c_int32()
+    assert moe_lib.lib().moe_plan_suggest_tile(-1, 8, 64, 64, ctypes.byref(bm), ctypes.byref(bn)) == -1
+
+
+def test_plan_launch_option_flags():
+    """Launch options live in the plan (no environment switches): accepted, recorded in the blob,
+    mutually exclusive grid options rejected."""
+    counts = [5, 0, 300]
+    for f in (moe_lib.MOE_GRID_BALANCED, moe_lib.MOE_GRID_STATIC, moe_lib.MOE_A_GATHER4, moe_lib.MOE_EPI_REGISTER):
+        p = moe_lib.parse_plan_blob(moe_lib.moe_plan_build(counts, 64, 256, 128, 128, f))
+        assert p["flags"] == f
+    with pytest.raises(moe_lib.MoeError):
+        moe_lib.moe_plan_build(counts, 64, 256, 128, 128, moe_lib.MOE_GRID_BALANCED | moe_lib.MOE_GRID_STATIC)

@@ -107,3 +107,19 @@ def test_swiglu_rows_layout_matches_layer():
         for r in range(row_off[e], row_off[e + 1]):
             out[tok[r]] += w[tok[r], slot[r]] * (h[r] @ Wd[e])
     assert np.allclose(out, ffn.moe_ffn(X, Wg, Wu, Wd, ids, w), rtol=1e-12, atol=1e-12)
+
+
+def test_moe_ffn_entries_equals_layer():
+    """The on-demand sampled form equals the whole-layer definition on the sampled entries."""
+    rng = np.random.default_rng(3)
+    T, E, k, H, I, Ho = 9, 4, 2, 6, 10, 5
+    X = rng.standard_normal((T, H))
+    Wg, Wu, Wd = rng.standard_normal((E, H, I)), rng.standard_normal((E, H, I)), rng.standard_normal((E, I, Ho))
+    ids = np.array([rng.permutation(E)[:k] for _ in range(T)])
+    ids[2, 1] = -1
+    w = rng.random((T, k))
+    full = ffn.moe_ffn(X, Wg, Wu, Wd, ids, w)
+    toks, cols = [0, 2, 7, 8], [4, 1]
+    got = ffn.moe_ffn_entries(lambda t: X[t], lambda e: Wg[e], lambda e: Wu[e], lambda e, cs: Wd[e][:, cs],
+                              ids, w, toks, cols)
+    assert np.allclose(got, full[np.ix_(toks, cols)], rtol=1e-13, atol=1e-13)
