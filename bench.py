@@ -277,7 +277,7 @@ def run_ffn(args, cfg):
         ev[1].record(stream)
         h = M.moe_gemm_swiglu(layer.plan_gu, Xd, tok, Wg, Wu)
         ev[2].record(stream)
-        y = M.moe_gemm(layer.plan_dn, h, None, Wdn)
+        y = M.moe_gemm(layer.plan_dn, h, None, Wdn, out_dtype=torch.float32)
         ev[3].record(stream)
         M.moe_combine(y, tok, slot, row_off, w_d, out=out)
         ev[4].record(stream)
@@ -311,7 +311,7 @@ def run_ffn(args, cfg):
     peak = float(peaks["bf16_tflops"])
     gu = 4.0 * rows * H * I / (st["swiglu_gemm"] * 1e-3) / 1e12
     dn = 2.0 * rows * H * I / (st["down_gemm"] * 1e-3) / 1e12
-    comb_bytes = rows * H * 2 + cfg.T * H * 2 + cfg.T * cfg.k * 8
+    comb_bytes = rows * H * 4 + cfg.T * H * 2 + cfg.T * cfg.k * 8      # fp32 expert rows in, bf16 out
     line = {
         "metric": "MoE FFN layer TFLOP/s (SwiGLU gate/up + down + weighted combine)", "value": flops / (ms * 1e-3) / 1e12,
         "unit": "TFLOP/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,

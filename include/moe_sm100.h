@@ -57,10 +57,20 @@ typedef int32_t moe_status;
  * same-box A/B timing and for tests that pin the alternative paths.                                 */
 #define MOE_GRID_BALANCED  16u  /* persistent grid over ceil(tiles / ceil(tiles / CTAs)) CTAs (pairs), each
                                    W or W-1 tiles (default for one-CTA tiles only)                    */
-#define MOE_GRID_STATIC    32u  /* plain static stride over all CTAs (pairs), never balanced           */
+#define MOE_GRID_STATIC    32u  /* plain static stride over all CTAs (pairs): no balanced grid, no
+                                   dynamic tile order                                                 */
 #define MOE_A_GATHER4      64u  /* stage token rows with TMA tile::gather4 (one-CTA tiles) instead of
                                    cp.async                                                           */
 #define MOE_EPI_REGISTER  128u  /* bf16 Y through masked register stores only (no TMA tile stores)    */
+#define MOE_NO_L2_PREFETCH 512u /* no load/store-path L2 prefetch of W for memory-bound tiles (one-CTA
+                                   tiles, swap-AB tiles) ahead of the ring                            */
+#define MOE_SCHED_DYNAMIC 256u  /* dynamic tile order: after its first tile each persistent CTA (pair)
+                                   takes the next virtual tile from a counter in the plan's device
+                                   memory (the order the hardware dispatches one block per tile,
+                                   P:138) instead of the static stride — the default for CTA-pair
+                                   tiles (bm = 256) unless MOE_GRID_STATIC / MOE_GRID_BALANCED is set;
+                                   launches on one plan must be stream-ordered (the counter is reset
+                                   by the launch's last CTA pair)                                     */
 
 /* Output element types of moe_gemm. */
 #define MOE_DTYPE_BF16 0
@@ -84,7 +94,8 @@ typedef int32_t moe_status;
  *   [2]  total virtual tiles     [3] M_pad = M rounded up to a multiple of 32 (>= 32)
  *   [4]  E (experts)             [5] N (expert output width)   [6] H (hidden = GEMM K)
  *   [7]  BM (tile rows)          [8] BN (tile cols)            [9] n_tasks (tasks incl. empty)
- *   [10] flags                   [11..15] reserved (0)
+ *   [10] flags                   [11] device planner status (0 = ok, 3 = capacity)
+ *   [12..16) the tile-strategy catalog: MOE_MAX_RULES (kind, m_max) pairs (unused: m_max = -1)
  *   [16 .. 16+M_pad)               TilePrefix: inclusive prefix of nu over the
  *                                  non-empty tasks (Alg. 1), padded
  *   [16+M_pad .. 16+2*M_pad)       sigma: non-empty index -> task index,
@@ -93,7 +104,8 @@ typedef int32_t moe_status;
  *                                  task i: {expert, row0, rows, kind, bm, bn,
  *                                  row_tiles, col_tiles}; row0 = first CSR row of
  *                                  the task (= row_off[expert] + offset in expert);
- *                                  kind 1 (MOE_SPLIT_TAIL): last row tile is swap-AB
+ *                                  kind = the catalog's strategy for the task's last
+ *                                  row tile (MOE_KIND_SWAP: swap-AB, see below)
  *   [.. +E+1)                      row_off: exclusive prefix of counts (CSR offsets)
  * nu(task) = row_tiles * col_tiles, row_tiles = ceil(rows/BM), col_tiles = ceil(N/BN).
  * Intra-task tile order: row tile fastest, rt = l mod row_tiles, ct = l div
@@ -102,6 +114,26 @@ typedef int32_t moe_status;
 #define MOE_PLAN_MAGIC      0x4d4f4531  /* "MOE1" */
 #define MOE_PLAN_HEADER     16
 #define MOE_PLAN_TASK_WORDS 8
+
+/* ---- per-task tiling strategies ("different tasks inside a batch can have different
+ * tiling strategies"; "categorized into several pre-defined tiling strategies ...
+ * GEMMs with large input and output sizes prefer large tiles"; Alg. 3 / Alg. 4's per-task
+ * dispatch).  With CTA-pair tiles (bm = 256, bn = 256 or 512) each expert's LAST row tile — its
+ * r = m mod 256 tail rows, or all its rows when m < 256 — is executed by the strategy the catalog
+ * picks for r; every other row tile is a full 256-row tile:
+ *   MOE_KIND_WIDE  the bm x bn tile (r <= 128: an M = 128 pair MMA, half the tensor time);
+ *   MOE_KIND_SWAP  a swap-AB tile: each 256-column W block is the M = 256 operand, the tile's r
+ *                  tokens the N operand rounded up to 16 (tensor time ~ r, not 128 / 256), its W
+ *                  blocks also prefetched into L2 ahead of the ring (memory-bound tiles).
+ * Rules are tried in order; the first with r <= m_max gives the kind (none matches: WIDE).  The tile
+ * partition — hence the mapping and Y — does not depend on the catalog. */
+typedef struct { int32_t kind; int32_t m_max; } moe_tile_rule;
+#define MOE_KIND_WIDE 0
+#define MOE_KIND_SWAP 1
+#define MOE_MAX_RULES 2
+#ifndef MOE_DEFAULT_SWAP_MAX
+#define MOE_DEFAULT_SWAP_MAX 64   /* built-in catalog: {SWAP, 64} — tails of <= 64 rows run swap-AB */
+#endif
 
 /* Number of int32 words moe_plan_build needs for E experts (upper bound). */
 int64_t moe_plan_blob_words(int32_t E);
@@ -134,6 +166,16 @@ moe_status moe_plan_build(const int32_t* counts_host, int32_t E, int64_t H, int6
                           int32_t bm, int32_t bn, uint32_t flags,
                           int32_t* blob, int64_t blob_cap, int64_t* blob_len);
 
+/*
+ * moe_plan_build with an explicit catalog: rules[n_rules] (n_rules <= MOE_MAX_RULES), n_rules = 0 for
+ * one strategy per launch (every tile MOE_KIND_WIDE), n_rules < 0 for the built-in catalog
+ * (moe_plan_build's behaviour).  MOE_SPLIT_TAIL in flags overrides it with {MOE_KIND_SWAP, bm}.
+ * MOE_ERR_UNSUPPORTED: a SWAP rule on a plan whose tiles are not CTA pairs with 256-column blocks.
+ */
+moe_status moe_plan_build_catalog(const int32_t* counts_host, int32_t E, int64_t H, int64_t N,
+                                  int32_t bm, int32_t bn, uint32_t flags, const moe_tile_rule* rules,
+                                  int32_t n_rules, int32_t* blob, int64_t blob_cap, int64_t* blob_len);
+
 /* Opaque plan: the host blob plus its device copy (library-owned). */
 typedef struct moe_plan moe_plan;
 
@@ -147,6 +189,12 @@ typedef struct moe_plan moe_plan;
 moe_status moe_plan_create(const int32_t* counts_host /* NULL: all zero, for moe_plan_device */,
                            int32_t E, int64_t H, int64_t N,
                            int32_t bm, int32_t bn, uint32_t flags, void* stream, moe_plan** out);
+
+/* moe_plan_create with an explicit catalog (as moe_plan_build_catalog); the device planner and
+ * moe_plan_update keep it. */
+moe_status moe_plan_create_catalog(const int32_t* counts_host, int32_t E, int64_t H, int64_t N,
+                                   int32_t bm, int32_t bn, uint32_t flags, const moe_tile_rule* rules,
+                                   int32_t n_rules, void* stream, moe_plan** out);
 
 /* Re-plan in place for new counts (same E, H, N, flags; the bm, bn resolved at creation are kept);
  * reuses the device buffer. */

@@ -69,15 +69,30 @@ def tiles_of(rows: int, N: int, bm: int, bn: int) -> int:
     return ceil_div(rows, bm) * ceil_div(N, bn)
 
 
-def make_tasks(counts, bm: int, bn: int, split_tail: bool = False) -> list[dict]:
+def tail_kind(m: int, bm: int, catalog) -> int:
+    """The tiling strategy of an expert's last row tile ("categorized into several
+    pre-defined tiling strategies"; R6): r = m mod bm rows (0: no partial tile); the first
+    catalog rule (kind, m_max) with r <= m_max gives the kind, else kind 0."""
+    r = int(m) % bm
+    if int(m) <= 0 or r == 0:
+        return 0
+    for kind, m_max in catalog:
+        if r <= m_max:
+            return int(kind)
+    return 0
+
+
+def make_tasks(counts, bm: int, bn: int, split_tail: bool = False, catalog=()) -> list[dict]:
     """One task per expert with tile bm x bn.
 
-    split_tail (R6): the mapping is unchanged, but an expert whose m is not a
-    multiple of bm gets kind 1 — its LAST row tile (rows [floor(m/bm)*bm, m)) is executed by a
-    second tiling strategy (Alg. 3 with K = 2): a swap-AB tile whose height is the
-    tail rounded up to 16.  The tile partition, hence Y, is identical."""
-    return [dict(expert=e, row_begin=0, rows=int(m), bm=bm, bn=bn,
-                 kind=1 if (split_tail and int(m) % bm) else 0) for e, m in enumerate(counts)]
+    The mapping is unchanged by the catalog, but an expert's LAST row tile (rows
+    [floor(m/bm)*bm, m), or all rows when m < bm) may be executed by a second tiling strategy
+    (Alg. 3 with K = 2): kind 1 = a swap-AB tile whose height is those rows
+    rounded up to 16.  split_tail = the catalog ((1, bm),).  The tile partition, hence Y, is identical."""
+    if split_tail:
+        catalog = ((1, bm),)
+    return [dict(expert=e, row_begin=0, rows=int(m), bm=bm, bn=bn, kind=tail_kind(m, bm, catalog))
+            for e, m in enumerate(counts)]
 
 
 def order_tasks(loads: list[int], strategy: str) -> list[int]:
@@ -116,11 +131,11 @@ def order_tasks(loads: list[int], strategy: str) -> list[int]:
 
 
 def plan(counts, N: int, bm: int, bn: int, pad_mode: str = "max", warp_size: int = 32,
-         tasks: list[dict] | None = None, split_tail: bool = False, order: str = "natural") -> dict:
+         tasks: list[dict] | None = None, split_tail: bool = False, order: str = "natural", catalog=()) -> dict:
     """Host-side plan: nu per task, sigma (non-empty tasks, natural order or a §4.2
     ordering), TilePrefix (Alg. 1 over eta in sigma's order), padded per P:203."""
     if tasks is None:
-        tasks = make_tasks(counts, bm, bn, split_tail)
+        tasks = make_tasks(counts, bm, bn, split_tail, catalog)
     nu = [tiles_of(t["rows"], N, t["bm"], t["bn"]) for t in tasks]
     sigma, prefix = mapping.nonempty_stage(nu, order_tasks([t["rows"] for t in tasks], order)
                                            if order != "natural" else None)

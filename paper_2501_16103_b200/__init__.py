@@ -23,8 +23,24 @@ MOE_DTYPE_BF16, MOE_DTYPE_F32, MOE_DTYPE_E4M3 = 0, 1, 2
 MOE_EP_UNFUSED = 1
 MOE_PAD_MAX, MOE_PAD_REPEAT, MOE_SPLIT_TAIL = 0, 1, 2
 MOE_ORDER_ALTERNATING, MOE_ORDER_HALF_INTERVAL = 4, 8
-MOE_GRID_BALANCED, MOE_GRID_STATIC, MOE_A_GATHER4, MOE_EPI_REGISTER = 16, 32, 64, 128
+MOE_GRID_BALANCED, MOE_GRID_STATIC, MOE_A_GATHER4, MOE_EPI_REGISTER, MOE_SCHED_DYNAMIC = 16, 32, 64, 128, 256
+MOE_NO_L2_PREFETCH = 512
 MOE_ROUTE_NO_SMALL, MOE_ROUTE_THREE_KERNELS = 1, 2
+MOE_KIND_WIDE, MOE_KIND_SWAP, MOE_MAX_RULES = 0, 1, 2
+MOE_DEFAULT_SWAP_MAX = 64                       # include/moe_sm100.h: the built-in catalog {SWAP, 64}
+DEFAULT_CATALOG = ((MOE_KIND_SWAP, MOE_DEFAULT_SWAP_MAX),)
+
+
+class _Rule(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("m_max", ctypes.c_int32)]
+
+
+def _rules(catalog):
+    """None -> built-in catalog (n_rules = -1); a sequence of (kind, m_max) -> the rule array."""
+    if catalog is None:
+        return None, -1
+    arr = (_Rule * max(len(catalog), 1))(*[_Rule(int(k), int(m)) for k, m in catalog])
+    return arr, len(catalog)
 MOE_PLAN_MAGIC = 0x4D4F4531
 MOE_PLAN_HEADER = 16
 MOE_PLAN_TASK_WORDS = 8
@@ -39,7 +55,8 @@ EXPORTED = (
     "moe_gemm_swiglu", "moe_combine", "moe_gemm_fp8", "moe_gemm_fp8_rowmap", "moe_gemm_fp8_profile",
     "moe_ep_unique_id", "moe_ep_create", "moe_ep_forward", "moe_ep_last_rows", "moe_ep_last_gemm_ms",
     "moe_ep_destroy", "moe_ep_create_loopback", "moe_ep_combine_ptr", "moe_gemm_rowptr",
-    "moe_route_ex", "moe_plan_suggest_tile", "moe_plan_create_expected",
+    "moe_route_ex", "moe_plan_suggest_tile", "moe_plan_create_expected", "moe_plan_build_catalog",
+    "moe_plan_create_catalog",
 )
 
 
@@ -70,6 +87,12 @@ def lib() -> ctypes.CDLL:
                                             ctypes.c_int32, ctypes.c_uint32, c_i32p, ctypes.c_int64, c_i64p]),
         "moe_plan_create": (ctypes.c_int32, [c_i32p, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32,
                                              ctypes.c_int32, ctypes.c_uint32, vp, ctypes.POINTER(vp)]),
+        "moe_plan_build_catalog": (ctypes.c_int32, [c_i32p, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64,
+                                                    ctypes.c_int32, ctypes.c_int32, ctypes.c_uint32, vp, ctypes.c_int32,
+                                                    c_i32p, ctypes.c_int64, c_i64p]),
+        "moe_plan_create_catalog": (ctypes.c_int32, [c_i32p, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64,
+                                                     ctypes.c_int32, ctypes.c_int32, ctypes.c_uint32, vp,
+                                                     ctypes.c_int32, vp, ctypes.POINTER(vp)]),
         "moe_plan_update": (ctypes.c_int32, [vp, c_i32p, vp]),
         "moe_plan_query": (ctypes.c_int32, [vp, c_i32p, c_i32p, c_i32p]),
         "moe_plan_blob": (ctypes.c_int32, [vp, c_i32p, ctypes.c_int64, c_i64p]),
@@ -144,15 +167,19 @@ def _i32ptr(a: np.ndarray):
 # ---------------------------------------------------------------------------
 # plan (host, no GPU needed)
 # ---------------------------------------------------------------------------
-def moe_plan_build(counts, H: int, N: int, bm: int = 0, bn: int = 0, flags: int = MOE_PAD_MAX) -> np.ndarray:
-    """The compressed mapping blob (int32 words, layout in include/moe_sm100.h)."""
+def moe_plan_build(counts, H: int, N: int, bm: int = 0, bn: int = 0, flags: int = MOE_PAD_MAX,
+                   catalog=None) -> np.ndarray:
+    """The compressed mapping blob (int32 words, layout in include/moe_sm100.h).
+    catalog: None = the built-in tile-strategy catalog, () = one strategy, else (kind, m_max) rules."""
     c = np.ascontiguousarray(np.asarray(counts, dtype=np.int32))
     E = int(c.shape[0])
     L = lib()
     cap = int(L.moe_plan_blob_words(E)) if E > 0 else 64
     blob = np.zeros(max(cap, 16), dtype=np.int32)
     n = ctypes.c_int64(0)
-    _check(L.moe_plan_build(_i32ptr(c), E, H, N, bm, bn, flags, _i32ptr(blob), blob.size, ctypes.byref(n)))
+    rules, nr = _rules(catalog)
+    _check(L.moe_plan_build_catalog(_i32ptr(c), E, H, N, bm, bn, flags, rules, nr, _i32ptr(blob), blob.size,
+                                    ctypes.byref(n)))
     return blob[: n.value].copy()
 
 
@@ -162,6 +189,7 @@ def parse_plan_blob(blob: np.ndarray) -> dict:
     if int(b[0]) != MOE_PLAN_MAGIC:
         raise ValueError("not a plan blob")
     M, total, M_pad, E, N, H, bm, bn, n_tasks, flags = (int(x) for x in b[1:11])
+    catalog = tuple((int(b[12 + 2 * i]), int(b[13 + 2 * i])) for i in range(MOE_MAX_RULES) if b[13 + 2 * i] >= 0)
     o = MOE_PLAN_HEADER
     prefix = b[o:o + M_pad]
     sigma = b[o + M_pad:o + 2 * M_pad]
@@ -169,7 +197,7 @@ def parse_plan_blob(blob: np.ndarray) -> dict:
     params = b[po:po + MOE_PLAN_TASK_WORDS * n_tasks].reshape(n_tasks, MOE_PLAN_TASK_WORDS)
     row_off = b[po + MOE_PLAN_TASK_WORDS * n_tasks: po + MOE_PLAN_TASK_WORDS * n_tasks + E + 1]
     return dict(M=M, total=total, M_pad=M_pad, E=E, N=N, H=H, bm=bm, bn=bn, n_tasks=n_tasks, flags=flags,
-                prefix=prefix, sigma=sigma, params=params, row_off=row_off)
+                prefix=prefix, sigma=sigma, params=params, row_off=row_off, catalog=catalog)
 
 
 def _stream(stream=None) -> int:
@@ -191,8 +219,9 @@ class Plan:
     """Device-resident plan (moe_plan_create / moe_plan_update / moe_plan_destroy)."""
 
     def __init__(self, counts, H: int, N: int, bm: int = 0, bn: int = 0, flags: int = MOE_PAD_MAX,
-                 stream=None, E: int | None = None):
-        """counts: host int array [E], or None (with E=...) for a plan filled by update_device()."""
+                 stream=None, E: int | None = None, catalog=None):
+        """counts: host int array [E], or None (with E=...) for a plan filled by update_device().
+        catalog: None = the built-in tile-strategy catalog, () = one strategy, else (kind, m_max) rules."""
         if counts is None:
             c, cp = None, None
             self.E = int(E)
@@ -202,10 +231,12 @@ class Plan:
             self.E = int(c.shape[0])
         self.H, self.N, self.bn, self.flags = H, N, bn, flags
         self._h = ctypes.c_void_p()
-        self.status = _check(lib().moe_plan_create(cp, self.E, H, N, bm, bn, flags, _stream(stream),
-                                                   ctypes.byref(self._h)))
+        rules, nr = _rules(catalog)
+        self.status = _check(lib().moe_plan_create_catalog(cp, self.E, H, N, bm, bn, flags, rules, nr,
+                                                           _stream(stream), ctypes.byref(self._h)))
         b = self.blob()
         self.bm, self.bn = int(b[7]), int(b[8])  # resolved tile shape (0: automatic)
+        self.catalog = parse_plan_blob(b)["catalog"]
         self.device_resident = False
 
     def update_device(self, counts_dev, stream=None):
@@ -389,8 +420,8 @@ def moe_combine(Y, token_idx, slot, row_off, topk_w, out=None, out_dtype=None, s
 
 class MoeFFN:
     """The full MoE FFN layer on one GPU (R14): route (+ device plan
-    for the gated GEMM) -> device plan for the down GEMM -> moe_gemm_swiglu -> moe_gemm (rows in
-    CSR order, no gather) -> moe_combine.  Every step runs in the library's kernels; nothing
+    for the gated GEMM) -> device plan for the down GEMM -> moe_gemm_swiglu (h in bf16) -> moe_gemm
+    (rows in CSR order, no gather; fp32 rows) -> moe_combine.  Every step runs in the library's kernels; nothing
     synchronises with the host, so a step can be captured in one CUDA graph."""
 
     def __init__(self, W_gate, W_up, W_down, stream=None):
@@ -414,7 +445,8 @@ class MoeFFN:
         counts, row_off, tok, slot, _ = moe_route(topk_ids, self.E, stream=stream, plan=self.plan_gu)
         self.plan_dn.update_device(counts, stream=stream)
         Hmid = moe_gemm_swiglu(self.plan_gu, X, tok, self.Wg, self.Wu, stream=stream)
-        Y = moe_gemm(self.plan_dn, Hmid, None, self.Wd, stream=stream)     # rows already in CSR order
+        # rows already in CSR order; fp32 rows into the combine (no second bf16 rounding, R14)
+        Y = moe_gemm(self.plan_dn, Hmid, None, self.Wd, out_dtype=torch.float32, stream=stream)
         out = moe_combine(Y, tok, slot, row_off, topk_w, out=out, out_dtype=out_dtype, stream=stream)
         self.last = dict(counts=counts, row_off=row_off, token_idx=tok, slot=slot, h=Hmid, y=Y)
         return out

@@ -41,6 +41,8 @@ namespace moe {
 const int32_t* plan_blob_host(const moe_plan* p, int64_t* words);
 const int32_t* plan_blob_dev(const moe_plan* p);
 bool plan_device_mode(const moe_plan* p);
+bool plan_has_swap(const moe_plan* p);
+int32_t* plan_sched_dev(const moe_plan* p);
 void plan_shape(const moe_plan* p, int32_t* E, int32_t* H, int32_t* N, int32_t* bm, int32_t* bn, uint32_t* flags);
 }  // namespace moe
 
@@ -76,8 +78,13 @@ constexpr int kDefaultAMode = 1;                // A staging: cp.async (see the 
 constexpr uint32_t kTmemCols = 512;             // 2 accumulators x 256 fp32 columns
 constexpr uint32_t kAccCols = 256;
 constexpr int kMaxMPad = 1024;
-constexpr int kBarBytes = 512;                  // 8 B per mbarrier (<= 2*6+4) + TMEM address slot [0,256);
-                                                // kProf stage timestamps [256,512)
+#ifndef MOE_L2_PREFETCH
+#define MOE_L2_PREFETCH 8
+#endif
+constexpr int kL2Pf = MOE_L2_PREFETCH;          // memory-bound tiles: W K blocks prefetched into L2 ahead
+constexpr int kBarBytes = 512;                  // 8 B per mbarrier (<= 2*6+4) + TMEM address slot + tile queue
+                                                // [0,256); kProf stage timestamps [256,512)
+constexpr int kQ = 4;                           // dynamic tile order: tile-queue slots per CTA
 
 struct GemmArgs {
   const int32_t* plan;       // device plan blob
@@ -104,6 +111,10 @@ struct GemmArgs {
   const unsigned long long* y_row_ptr;   // nullable: CSR row i is stored at address y_row_ptr[i] (any device
                                          // memory the SM can write: the EP combine buffers of peer ranks)
   int32_t balance;           // balanced grid: only ceil(total / ceil(total / grid)) CTAs (pairs) take tiles
+  int32_t* sched;            // nullable: dynamic tile order — [0] next virtual tile (- n_pairs), [1] pairs done
+  const uint8_t* W;          // W base (bytes), for the load/store-path L2 prefetch of memory-bound tiles
+  int32_t pf_dist;           // that prefetch's distance in K blocks (0: off); one-CTA tiles: every tile,
+                             // CTA pairs: swap-AB tiles only
 };
 
 // Per-CTA counters written by the instrumented build (kProf = true).
@@ -150,7 +161,7 @@ __device__ __forceinline__ void map_tile(const int32_t* prefix, const int32_t* s
 
 struct Tile {
   int expert, row0, rows, bn, rt, ct;
-  int kind;     // of THIS tile: 0 = bm rows x bn cols; 1 = swap-AB tail tile (MOE_SPLIT_TAIL)
+  int kind;     // of THIS tile: 0 = bm rows x bn cols (MOE_KIND_WIDE); 1 = swap-AB tile (MOE_KIND_SWAP)
   int height;   // kind 1: tail rows rounded up to 16 (the MMA's N)
 };
 
@@ -168,7 +179,7 @@ __device__ __forceinline__ Tile load_tile(const int32_t* params, int task, int l
   t.kind = 0;
   t.height = pb.x;
   if constexpr (kSplit) {
-    // MOE_SPLIT_TAIL: a kind-1 task runs its last row tile (rows [rt*bm, rows)) swap-AB.
+    // The catalog: a kind-1 task runs its last row tile (rows [rt*bm, rows)) swap-AB.
     if (pa.w == 1 && t.rt == pb.z - 1) {
       const int tail = t.rows - t.rt * pb.x;
       t.kind = 1;
@@ -190,6 +201,21 @@ __device__ __forceinline__ int wide_block_cols(int bn, int ct, int N, int hf) {
   const int bnp = bn / 2;
   const int nvalid = min(bn, N - ct * bn) - hf * bnp;
   return nvalid <= 0 ? 0 : min(bnp, (nvalid + kGran - 1) & ~(kGran - 1));
+}
+
+// Wide 512-column tiles that lie inside N (and every swap-AB tile) stage W as ONE 4-D TMA box of
+// 256 columns per CTA per stage instead of one 128-column box per MMA block: TMA issues a box every
+// ~330 ns per SM whatever its size up to 32 KB (scripts/stream_probe.cu), so bigger
+// boxes stream W faster.  CTA r then holds tile columns [256 r, 256 r + 256): MMA block hf takes its
+// half [256 r + 128 hf, +128), so D column n of block hf is W column 256 (n >= 128) + 128 hf + n % 128
+// (two boxes: 256 hf + n; for swap-AB tiles the D row plays n's role).
+template <bool kWide, bool kGated>
+__device__ __forceinline__ bool one_box(int bn, int ct, int N, int w4d, bool swap) {
+  return kWide && !kGated && w4d && bn == 512 && (swap || (ct + 1) * bn <= N);
+}
+__device__ __forceinline__ int w_col(bool one, int ct, int bn, int hf, int half, int j) {
+  // column of W for block hf, D half `half` (= the CTA whose shared memory holds it), offset j < 128
+  return ct * bn + (one ? 256 * half + 128 * hf : 256 * hf + 128 * half) + j;
 }
 
 // Wide kind-0 tiles whose valid rows fit in 128 ("half" tiles: an expert's short last row tile)
@@ -263,15 +289,15 @@ struct Geo {
 #define MOE_CTA1_STAGES 4
 #endif
   static constexpr int kStages = kWide ? MOE_WIDE_STAGES : kCta == 2 ? 6 : MOE_CTA1_STAGES;   // 7th pair stage: no gain
-  static_assert(8 * (2 * kStages + 4) + 4 <= kBarBytes, "barrier block overlaps TilePrefix");
+  static_assert(8 * (2 * kStages + 4 + 2 * kQ) + 4 * kQ + 8 <= 256, "barrier block overlaps the kProf stamps");
   static constexpr int kBStage = (kWide ? 2 : 1) * kBStageBytes / kCta;   // bytes of W per CTA per stage
   // 16 KB: a 2 KB bf16 staging buffer per epilogue warp for the TMA-store epilogue (two per warp
-  // with four warps), or 4 KB transpose buffers for four warps on swap-AB tail tiles (MOE_SPLIT_TAIL).
+  // with four warps).
   static constexpr int kEpiStage = 16384 > kEpiWarps * kEpiBufBytes ? 16384 : kEpiWarps * kEpiBufBytes;
   static constexpr size_t kSmem = 1024 + (size_t)kStages * (kABytes + kBStage) + kEpiStage + kBarBytes;
 };
 
-// kSplit: the plan carries MOE_SPLIT_TAIL (kind-1 tail tiles exist); a separate instantiation so
+// kSplit: the plan's catalog has a swap-AB rule (kind-1 tiles may exist); a separate instantiation so
 // the plain path carries none of the swap-AB code.
 // kWide: wide pair tiles (bm = 256, bn = 512).  Each K block feeds two N = 256 MMAs into the two
 // TMEM accumulators (columns 0-255 and 256-511): every staged token row serves 512 output columns,
@@ -313,13 +339,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = smem_raw + (base - raw);
   const uint32_t sA = base;
   const uint32_t sB = sA + kSt * kABytes;
-  const uint32_t sEpi = sB + kSt * kBSt;                   // swap-AB transpose buffers (pairs)
+  const uint32_t sEpi = sB + kSt * kBSt;                   // TMA-store staging buffers
   const uint32_t sBar = sEpi + Geo<kCta, kSplit, kWide>::kEpiStage;
   auto full_bar = [&](int s) { return sBar + 8u * s; };
   auto empty_bar = [&](int s) { return sBar + 8u * (kSt + s); };
   auto tfull_bar = [&](int i) { return sBar + 8u * (2 * kSt + i); };
   auto tempty_bar = [&](int i) { return sBar + 8u * (2 * kSt + 2 + i); };
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + (sBar - base) + 8 * (2 * kSt + 4));
+  // Dynamic tile order: queue slot i holds the CTA pair's i-th virtual tile; qfull[i] completes when the
+  // leader's B warp has published it (in both CTAs), qempty[i] when every consumer warp has read it.
+  auto qfull_bar = [&](int i) { return sBar + 8u * (2 * kSt + 4 + i); };
+  auto qempty_bar = [&](int i) { return sBar + 8u * (2 * kSt + 4 + kQ + i); };
+  const uint32_t s_q = sBar + 8u * (2 * kSt + 4 + 2 * kQ);          // kQ int32 tile ids
+  volatile int32_t* q_slot = reinterpret_cast<volatile int32_t*>(smem + (s_q - base));
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + (s_q - base) + 4 * kQ);
   int32_t* s_prefix = reinterpret_cast<int32_t*>(smem + (sBar - base) + kBarBytes);
   long long* s_ts = reinterpret_cast<long long*>(smem + (sBar - base) + 256);   // kProf: [3][kSt] stamps
   int32_t* s_sigma = s_prefix + a.M_pad;
@@ -353,12 +385,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(tfull_bar(i), 1);
       mbar_init(tempty_bar(i), kCta * kEpiWarps);
     }
+    // queue consumers (one arrival per warp, on the leader's qempty): A warps, MMA warp (leader) or
+    // relay lane (peer, unless rows are contiguous), the peer's B warp, epilogue warps
+    const uint32_t q_consumers = kCta == 2 ? 2 * (kAWarps + kEpiWarps) + 2 + (a_mode != 2 ? 1u : 0u)
+                                           : kAWarps + 1 + kEpiWarps;
+    for (int i = 0; i < kQ; ++i) {
+      mbar_init(qfull_bar(i), 1);
+      mbar_init(qempty_bar(i), q_consumers);
+    }
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmX);
     prefetch_tmap(&tmW);
-    if (kGated) prefetch_tmap(&tmW2);
+    if (kGated || kWide) prefetch_tmap(&tmW2);
     if (a.tma_store) prefetch_tmap(&tmY);
   }
   if (warp == kMmaWarp) tmem_alloc<kTmemCols, kCta>(smem_u32(tmem_holder));
@@ -383,6 +423,32 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int32_t* params = a.plan + a.off_params;
   constexpr int kPairRows = kBM * kCta;                     // rows of a virtual tile
 
+  // The virtual tiles of this CTA (pair), in the order every role warp walks them.  Static: v = pair_id
+  // + i * n_pairs (P:75-77's static batching).  Dynamic (a.sched): tile 0 is pair_id, then the leader's B
+  // warp takes the next v from a global counter as the pair frees up — the order in which the hardware
+  // dispatches the paper's one-block-per-tile launch — and publishes it through the tile queue.
+  const bool dyn = a.sched != nullptr;
+  auto tile_of = [&](uint32_t i) -> int {                   // consumer warps (all lanes)
+    if (!dyn) return pair_id + (int)i * n_pairs;
+    const int sl = (int)(i % kQ);
+    mbar_wait_acq_cluster(qfull_bar(sl), (i / kQ) & 1u);
+    const int v = q_slot[sl];
+    __syncwarp();
+    if (lane == 0) {
+      if constexpr (kCta == 2) mbar_arrive_cluster(leader(qempty_bar(sl)));
+      else mbar_arrive(qempty_bar(sl));
+    }
+    return v;
+  };
+  auto tile_of_lane = [&](uint32_t i) -> int {              // a single-lane consumer (the pair relay)
+    if (!dyn) return pair_id + (int)i * n_pairs;
+    const int sl = (int)(i % kQ);
+    mbar_wait_acq_cluster(qfull_bar(sl), (i / kQ) & 1u);
+    const int v = q_slot[sl];
+    mbar_arrive_cluster(leader(qempty_bar(sl)));
+    return v;
+  };
+
   if (warp < kAWarps) {
     // ===================== A producers: this CTA's 128 token rows, 64 columns per stage =====================
     // Gathered straight from X through the token-index array: no gathered copy of X.
@@ -399,7 +465,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int ch = threadIdx.x & 7;                 // cp.async: 16-byte chunk of the 128-byte row
     const int rsub = threadIdx.x >> 3;              // cp.async: row within a 16-row group
     const uint32_t dst_off = rsub * 128 + ((ch ^ (rsub & 7)) << 4);
-    for (int v = pair_id; v < total; v += n_pairs) {
+    for (uint32_t qi = 0;; ++qi) {
+      const int v = tile_of(qi);
+      if (v >= total) break;
       int h, task, l;
       map_tile(s_prefix, s_sigma, a.M_pad, v, h, task, l);
       const Tile t = load_tile<kSplit>(params, task, l);
@@ -453,8 +521,28 @@ __global__ void __launch_bounds__(kThreads, 1)
           src[j] = reinterpret_cast<const uint8_t*>(a.X) + (int64_t)tok * row_bytes + ch * 16;
           rowok |= (r < nvalid ? 1u : 0u) << j;
         }
+        // Memory-bound tiles: the A warps (idle but for a few token rows) also pull this CTA's W lines
+        // of K block kb + pf_dist into L2 through the load/store path, so the ring's W boxes hit in L2
+        // (TMA moves one box per ~330 ns per SM from HBM).
+        const bool lsu_pf = a.pf_dist > 0 &&
+                            (kCta == 1 || (kSplit && t.kind == 1 && one_box<kWide, kGated>(t.bn, t.ct, a.N, a.w4d, true)));
+        const int esz = kFp8 ? 1 : 2;
+        const int wcols = kCta == 1 ? t.bn : 256;              // this CTA's W columns of the tile (one box)
+        const int wcol0 = kCta == 1 ? t.ct * t.bn : t.ct * t.bn + (int)rank * 256;
+        const int lines_row = min(wcols, a.N - wcol0) * esz / 128;   // 128-byte lines per K row (N % 64 == 0)
+        const uint8_t* wexp = a.W + (int64_t)t.expert * a.H * a.N * esz + (int64_t)wcol0 * esz;
         for (int kb = 0; kb < a.num_kb; ++kb, ++g) {
           const int s = g % kSt;
+          if (lsu_pf && lines_row > 0) {
+            const int kp = kb == 0 ? 0 : kb + a.pf_dist - 1;      // tile start: the first pf_dist blocks
+            for (int k2 = kp; k2 < min(kb + a.pf_dist, a.num_kb); ++k2) {
+              const int n_lines = kKB * lines_row;
+              for (int i = threadIdx.x; i < n_lines; i += 32 * kAWarps) {
+                const int kr = k2 * kKB + i / lines_row;
+                if (kr < a.H) prefetch_l2(wexp + ((int64_t)kr * a.N) * esz + (i % lines_row) * 128);
+              }
+            }
+          }
           wait_timed<kProf>(empty_bar(s), ((g / kSt) & 1u) ^ 1u, c_wait);
           if constexpr (kProf) {
             if (p == 0 && lane == 0) s_ts[kSt + s] = clock64();
@@ -503,7 +591,28 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint64_t pol_w = policy_evict_normal();
     uint32_t g = 0;
     long long c_wait = 0, c_t0 = kProf ? clock64() : 0, c_rel = 0;
-    for (int v = pair_id; v < total; v += n_pairs) {
+    int v_next = pair_id;                           // dynamic order, leader lane 0: the next tile fetched
+    for (uint32_t qi = 0;; ++qi) {
+      int v;
+      if (dyn && rank == 0) {                       // the producer of the pair's tile queue
+        v = __shfl_sync(0xffffffffu, v_next, 0);
+        const int sl = (int)(qi % kQ);
+        mbar_wait(qempty_bar(sl), ((qi / kQ) & 1u) ^ 1u);
+        if (lane == 0) {
+          q_slot[sl] = v;
+          if constexpr (kCta == 2) {
+            st_shared_cluster_u32(mapa_shared(s_q + 4u * sl, 1), (uint32_t)v);
+            mbar_arrive_release_cluster(mapa_shared(qfull_bar(sl), 1));
+          }
+          mbar_arrive(qfull_bar(sl));
+          // fetch the next tile now: the atomic's latency hides behind this tile's loads
+          if (v < total) v_next = n_pairs + atomicAdd(a.sched, 1);
+        }
+        __syncwarp();
+      } else {
+        v = tile_of(qi);
+      }
+      if (v >= total) break;
       int h, task, l;
       map_tile(s_prefix, s_sigma, a.M_pad, v, h, task, l);
       const Tile t = load_tile<kSplit>(params, task, l);
@@ -511,6 +620,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int bnc = kGated ? 128 : bnp / kCta;    // columns of an MMA block staged by this CTA
       const int n0 = kGated ? t.ct * t.bn : t.ct * t.bn + (int)rank * bnc;   // block h at n0 + h * bnp
       const int nbox = (bnc + (1 << kCS) - 1) >> kCS;
+      const bool one = kCta == 2 && one_box<kWide, kGated>(t.bn, t.ct, a.N, a.w4d, kSplit && t.kind == 1);
+      const int n_one = t.ct * t.bn + (int)rank * 256;   // one box: this CTA's 256 columns
       for (int kb = 0; kb < a.num_kb; ++kb, ++g) {
         const int s = g % kSt;
         wait_timed<kProf>(empty_bar(s), ((g / kSt) & 1u) ^ 1u, c_wait);
@@ -530,7 +641,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
         if (lane == 0) {
           const uint32_t dstB = sB + s * kBSt;
-          if constexpr (kCta == 2) {
+          if (kCta == 2 && one) {
+            // both blocks' W columns of this CTA in one box (tmW2 has the 2 x nbox-chunk box)
+            const uint32_t fb = leader(full_bar(s));
+            uint32_t bytes = (uint32_t)(kCta * 2 * nbox * kBox);
+            if (a_mode == 2) bytes += kCta * kABytes;
+            if (rank == 0) mbar_arrive_expect_tx(full_bar(s), bytes);
+            tma_load_4d_pair(&tmW2, fb, dstB, 0, kb * kKB, n_one >> kCS, t.expert, pol_w);
+          } else if constexpr (kCta == 2) {
             const uint32_t fb = leader(full_bar(s));
             // Per block: this CTA's first column and boxes.  Wide kind-0 tiles passing N stage only
             // the trimmed block (wide_block_cols); the 4-D box always moves nbox chunks.
@@ -580,6 +698,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
       }
     }
+    if (dyn && rank == 0 && lane == 0) {
+      // Every pair ends here exactly once; the last one resets the counters for the next launch on
+      // this plan (launches on one plan are stream-ordered).
+      __threadfence();
+      if (atomicAdd(a.sched + 1, 1) == n_pairs - 1) {
+        atomicExch(a.sched, 0);
+        atomicExch(a.sched + 1, 0);
+      }
+    }
     if constexpr (kProf) {
       if (lane == 0) {
         a.prof[blockIdx.x * kProfSlots + kProfBWaitEmpty] = c_wait;
@@ -596,7 +723,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       long long c_tmem = 0, c_full = 0, c_t0 = kProf ? clock64() : 0, c_lb = 0, c_la = 0, c_ns = 0;
       long long c_issue = 0, c_gap = 0, t_end = 0;
       int n_tiles = 0;
-      for (int v = pair_id; v < total; v += n_pairs) {
+      for (uint32_t qi = 0;; ++qi) {
+        const int v = tile_of(qi);
+        if (v >= total) break;
         ++n_tiles;
         int h, task, l;
         map_tile(s_prefix, s_sigma, a.M_pad, v, h, task, l);
@@ -820,12 +949,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       // Pair peer: relay "my A stage landed" (local full barrier, fed by cp.async arrivals) to the
       // leader's full barrier, where the MMA issuer waits for both CTAs' bytes.
       uint32_t g = 0;
-      for (int v = pair_id; v < total; v += n_pairs)
+      for (uint32_t qi = 0;; ++qi) {
+        if (tile_of_lane(qi) >= total) break;
         for (int kb = 0; kb < a.num_kb; ++kb, ++g) {
           const int s = g % kSt;
           mbar_wait(full_bar(s), (g / kSt) & 1u);
           mbar_arrive_cluster(leader(full_bar(s)));
         }
+      }
     }
   } else {
     // ===================== epilogue: TMEM -> registers -> Y =====================
@@ -844,62 +975,54 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
       }
     };
-    for (int v = pair_id; v < total; v += n_pairs) {
+    for (uint32_t qi = 0;; ++qi) {
+      const int v = tile_of(qi);
+      if (v >= total) break;
       int h, task, l;
       map_tile(s_prefix, s_sigma, a.M_pad, v, h, task, l);
       const Tile t = load_tile<kSplit>(params, task, l);
       wait_timed<kProf>(tfull_bar(acc), acc_phase, c_wait);
       const long long w0 = kProf ? clock64() : 0;
       tc_fence_after();
-      if (kSplit && t.kind == 1 && a.tma_store) {
-        // The swap-AB transposes reuse the TMA-store staging buffers: every epilogue warp's earlier
-        // stores must have read their staging buffer first.
-        if (lane == 0) bulk_wait_group_read<0>();
-        named_bar_sync(1, 32 * kEpiWarps);
-      }
       if (kSplit && t.kind == 1) {
-        // Swap-AB tail: drained by the first four epilogue warps (cg == 0) alone; TMEM lane = output
-        // column, TMEM column = tail token.  Wide tiles: TMEM block hf holds W columns t.ct * 512 +
-        // 256 hf + [0, 256) (128 per CTA).  Each 32 (columns) x 32 (tokens) block is transposed
-        // through the warp's smem buffer, then token rows leave as 16-byte stores (a warp covers 32
-        // columns of 4 (fp32) / 8 (bf16) rows).
-        if (cg == 0) {
-          uint8_t* buf = smem + (sEpi - base) + (warp - (kMmaWarp + 1)) * (32 * 32 * 4);
-          const int esz = a.y_f32 ? 4 : 2;
+        // Swap-AB tile (tail / small task, the catalog's second strategy): TMEM lane = output column
+        // (this CTA's 128 of each 256-column block: t.ct * bn + 256 hf + 128 rank + lane), TMEM column
+        // = token.  Warp (q, cg) drains lanes 32q..32q+31 for the token chunks c = 32 cg, 32 cg +
+        // 32 kEpiGroups, ...; for each token j of a chunk the warp stores 32 consecutive columns of
+        // that token's Y row (one coalesced 64 / 128-byte store) — no transpose through shared
+        // memory, no barrier between warps.  Every warp frees each block as on kind-0 tiles.
+        const int esz = a.y_f32 ? 4 : 2;
+        const int bnb = t.bn / kHalves;                           // columns of one TMEM block
 #pragma unroll 1
-          for (int hf = 0; hf < kHalves; ++hf) {
+        for (int hf = 0; hf < kHalves; ++hf) {
           wait_block1(hf);
           const int slot = kWide ? hf : acc;
           const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + slot * kAccCols;
-          const int bnb = t.bn / kHalves;               // columns of one TMEM block
-          const int col0 = t.ct * t.bn + hf * bnb + (int)rank * (bnb / kCta) + q * 32;   // this warp's 32 columns
-          // TMEM lanes past this CTA's bnb / 2 columns (a box rounds up to 64) belong to the peer / next block
-          const int col_lim = min(t.ct * t.bn + hf * bnb + ((int)rank + 1) * (bnb / kCta), a.N);
-          for (int c = 0; c < t.height; c += 32) {
+          const bool one = kCta == 2 && one_box<kWide, kGated>(t.bn, t.ct, a.N, a.w4d, true);
+          const int col = one ? w_col(true, t.ct, t.bn, hf, (int)rank, q * 32 + lane)
+                              : t.ct * t.bn + hf * bnb + (int)rank * (bnb / kCta) + q * 32 + lane;
+          const bool col_ok = col < a.N && (one || col < t.ct * t.bn + hf * bnb + ((int)rank + 1) * (bnb / kCta));
+          for (int c = 32 * cg; c < t.height; c += 32 * kEpiGroups) {
             uint32_t r[32];
             tmem_ld32(taddr + c, r);
+            // token row address of token c + lane (broadcast per j below)
+            const int tk = min(c + lane, t.rows - 1);
+            uint8_t* rp = a.y_row_ptr ? reinterpret_cast<uint8_t*>(__ldg(a.y_row_ptr + t.row0 + tk))
+                                      : reinterpret_cast<uint8_t*>(a.Y) +
+                                            (a.y_row_map ? (int64_t)__ldg(a.y_row_map + t.row0 + tk)
+                                                         : (int64_t)t.row0 + tk) * a.N * esz;
             tmem_wait_ld();
+            const int ntok = min(32, t.rows - c);
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {              // token c+j, column lane -> buf[j][lane]
-              if (a.y_f32)
-                reinterpret_cast<uint32_t*>(buf)[j * 32 + lane] = r[j];
-              else
-                reinterpret_cast<__nv_bfloat16*>(buf)[j * 32 + lane] = __float2bfloat16_rn(__uint_as_float(r[j]));
-            }
-            __syncwarp();
-            const int vec_per_row = 32 * esz / 16;      // 16-byte pieces per 32-column row segment
-            const int rows_per_pass = 32 / vec_per_row;
-            for (int j0 = 0; j0 < 32; j0 += rows_per_pass) {
-              const int j = j0 + lane / vec_per_row, piece = lane % vec_per_row;
-              const int tok = c + j;
-              const int col = col0 + piece * (16 / esz);
-              if (tok < t.rows && col < col_lim) {
-                const int64_t yr = a.y_row_map ? (int64_t)__ldg(a.y_row_map + t.row0 + tok) : (int64_t)t.row0 + tok;
-                const uint4 val = *reinterpret_cast<const uint4*>(buf + j * 32 * esz + piece * 16);
-                *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(a.Y) + (yr * a.N + col) * esz) = val;
+            for (int j = 0; j < 32; ++j) {
+              uint8_t* row = reinterpret_cast<uint8_t*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(rp), j));
+              if (j < ntok && col_ok) {
+                if (a.y_f32)
+                  reinterpret_cast<float*>(row)[col] = __uint_as_float(r[j]);
+                else
+                  reinterpret_cast<__nv_bfloat16*>(row)[col] = __float2bfloat16_rn(__uint_as_float(r[j]));
               }
             }
-            __syncwarp();
           }
           tc_fence_before();
           __syncwarp();
@@ -907,21 +1030,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if constexpr (kCta == 2) mbar_arrive_cluster(leader(tempty_bar(slot)));
             else mbar_arrive(tempty_bar(slot));
           }
-          }
         }
-        // Every epilogue warp meets here (one barrier site): the staging buffers are free again, and
-        // the other warps cannot run ahead — their arrivals on the next tile's tmem-empty barriers
-        // would otherwise complete this tile's phase early.
-        named_bar_sync(1, 32 * kEpiWarps);
-        if (cg > 0 && lane == 0) {
-          if constexpr (kWide) {
-            mbar_arrive_cluster(leader(tempty_bar(0)));
-            mbar_arrive_cluster(leader(tempty_bar(1)));
-          } else {
-            mbar_arrive_cluster(leader(tempty_bar(acc)));
-          }
-        }
-        __syncwarp();
         if constexpr (kProf) c_work += clock64() - w0;
         if constexpr (kWide) {
           acc_phase ^= 1u;
@@ -1005,16 +1114,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       } else {
         const int bnp = t.bn / kHalves;             // columns of one accumulator block
+        const bool one = kCta == 2 && one_box<kWide, kGated>(t.bn, t.ct, a.N, a.w4d, false);
 #pragma unroll 1
         for (int hf = 0; hf < kHalves; ++hf) {
           wait_block1(hf);
           // columns of this warp's lanes: the whole block, or (half tile) its first / second half
           const int hw = hlf ? wide_block_cols<kFp8>(t.bn, t.ct, a.N, hf) / 2 : bnp;
           const int n0 = t.ct * t.bn + hf * bnp + (hlf ? (q >> 1) * hw : 0);
-          const int col_end = min(n0 + hw, a.N);
           const int slot = kWide ? hf : acc;        // TMEM block and its tmem-empty barrier
           const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + slot * kAccCols;
           for (int c = 32 * cg; c < hw && (!tma_rows || n0 + c < a.N); c += 32 * kEpiGroups) {
+            // W column of TMEM column c (one box per CTA: the D half picks the CTA's 256 columns)
+            const int col = one ? w_col(true, t.ct, t.bn, hf, hlf ? (q >> 1) : (c >> 7), hlf ? c : (c & 127)) : n0 + c;
+            const int col_end = one ? col + 32 : min(n0 + hw, a.N);
             uint32_t r[32];
             tmem_ld32(taddr + c, r);
             tmem_wait_ld();
@@ -1025,7 +1137,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * sc);
               }
             }
-            put_chunk(r, n0 + c, col_end);
+            put_chunk(r, col, col_end);
           }
           tc_fence_before();
           __syncwarp();
@@ -1515,8 +1627,9 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
     if (W2) MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_gemm_fp8: no gated variant");
     if (prof && !(v.bm == 256 && v.bn > 256))
       MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_gemm_fp8_profile: instrumented for wide pair tiles only");
-    if (v.bm == kDecRows || (v.flags & MOE_SPLIT_TAIL))
-      MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_gemm_fp8: bm = 64 decode tiles and MOE_SPLIT_TAIL plans are bf16-only");
+    // (The FP8 kernel runs every tile as MOE_KIND_WIDE: a plan's swap-AB catalog rules are ignored,
+    // which changes nothing in Y — the tile partition is the same.)
+    if (v.bm == kDecRows) MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_gemm_fp8: bm = 64 decode tiles are bf16-only");
     const bool ok_tile = v.bm == 128 ? v.bn % 128 == 0 : (v.bn == 256 || v.bn == 512);
     if (!ok_tile || v.N % 128 || v.H % 16)
       MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_gemm_fp8: needs N %% 128 == 0, H %% 16 == 0 and a %d x %d tile of "
@@ -1539,14 +1652,18 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
   if (gated) {
     st = make_w_map(&tmW2, W2, v.E, v.H, v.N, v.bn / cta, w4d);
     if (st != MOE_OK) return st;
+  } else if (wide && w4d && v.bn == 512) {
+    // one box per CTA per stage for wide tiles inside N and swap-AB tiles: both blocks' 256 columns
+    st = make_w_map(&tmW2, W, v.E, v.H, v.N, 2 * bnc_blk, w4d, fp8);
+    if (st != MOE_OK) return st;
   }
 
   // TMA-store epilogue: bf16 Y in CSR row order (the EP combine path scatters rows: register stores).
   CUtensorMap tmY;
   std::memset(&tmY, 0, sizeof(tmY));
   bool tma_store = y_dtype == MOE_DTYPE_BF16 && !y_row_map && !y_row_ptr;
-  if (y_row_ptr && (v.bm == kDecRows || (v.flags & MOE_SPLIT_TAIL) || W2))
-    MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_gemm_rowptr: plain / pair / wide tiles only (no bm = 64, split tails, gating)");
+  if (y_row_ptr && (v.bm == kDecRows || W2))
+    MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_gemm_rowptr: plain / pair / wide tiles only (no bm = 64, no gating)");
   if (v.flags & MOE_EPI_REGISTER) tma_store = false;   // plan option: register stores only
   if (tma_store) {
     // Rows of Y: the plan's total (host plan); a device plan's count is on the device, so the
@@ -1576,8 +1693,15 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
   a.prof = prof;
   a.y_row_map = y_row_map;
   a.y_row_ptr = y_row_ptr;
-  // Balanced grid: default for one-CTA (decode-regime) tiles; plan options force it on / off.
-  a.balance = (v.flags & MOE_GRID_BALANCED) ? 1 : (v.flags & MOE_GRID_STATIC) ? 0 : v.bm == 128;
+  // Tile order: dynamic by default for CTA-pair tiles (compute-bound tiles of unequal
+  // cost: wide / half / swap-AB; measured +1-5 %), static with the balanced grid for one-CTA
+  // (decode-regime, HBM-bound) tiles; plan options force either.
+  const bool dynamic = (v.flags & MOE_SCHED_DYNAMIC) ||
+                       (!(v.flags & (MOE_GRID_STATIC | MOE_GRID_BALANCED)) && v.bm == 256);
+  a.sched = dynamic ? moe::plan_sched_dev(plan) : nullptr;
+  a.W = reinterpret_cast<const uint8_t*>(W);
+  a.pf_dist = (v.flags & MOE_NO_L2_PREFETCH) || !(v.N % 64 == 0) ? 0 : kL2Pf;
+  a.balance = a.sched ? 0 : (v.flags & MOE_GRID_BALANCED) ? 1 : (v.flags & MOE_GRID_STATIC) ? 0 : v.bm == 128;
   a.tma_store = tma_store ? 1 : 0;
   a.T = (int32_t)T;
   a.H = v.H;
@@ -1592,7 +1716,7 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
   if (attr_err != cudaSuccess) MOE_FAIL(MOE_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(attr_err));
   if (v.bm == kDecRows) {
     // Decode-regime tiles: swap-AB on one CTA (moe_gemm_decode_kernel).
-    if (gated || v.bn != kDecCols || (v.flags & MOE_SPLIT_TAIL))
+    if (gated || v.bn != kDecCols)
       MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_gemm: bm = 64 tiles need bn = 256, no split tails, not gated");
     const int grid = v.total < 0 ? sm_count_cached() : std::min(v.total, sm_count_cached());
     cudaLaunchConfig_t cfg = {};
@@ -1608,7 +1732,8 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
     cudaError_t le = cudaLaunchKernelEx(&cfg, moe_gemm_decode_kernel, tmW, a);
     if (le != cudaSuccess) MOE_FAIL(MOE_ERR_CUDA, "moe_gemm decode launch: %s", cudaGetErrorString(le));
   } else if (v.bm == 256) {
-    const bool split = (v.flags & MOE_SPLIT_TAIL) != 0;
+    // Two strategies in the launch when the catalog has a swap-AB rule (bf16, not gated).
+    const bool split = moe::plan_has_swap(plan) && !fp8 && !gated;
     const int pairs = v.total < 0 ? sm_count_cached() / 2 : std::min(v.total, sm_count_cached() / 2);
     const size_t smem = (split && wide   ? Geo<2, true, true>::kSmem
                          : split         ? Geo<2, true>::kSmem

@@ -68,6 +68,12 @@ int64_t moe_plan_blob_words(int32_t E) {
 moe_status moe_plan_build(const int32_t* counts, int32_t E, int64_t H, int64_t N, int32_t bm,
                           int32_t bn, uint32_t flags, int32_t* blob, int64_t blob_cap,
                           int64_t* blob_len) {
+  return moe_plan_build_catalog(counts, E, H, N, bm, bn, flags, nullptr, -1, blob, blob_cap, blob_len);
+}
+
+moe_status moe_plan_build_catalog(const int32_t* counts, int32_t E, int64_t H, int64_t N, int32_t bm, int32_t bn,
+                                  uint32_t flags, const moe_tile_rule* rules, int32_t n_rules, int32_t* blob,
+                                  int64_t blob_cap, int64_t* blob_len) {
   moe::clear_error();
   if (!counts || !blob) MOE_FAIL(MOE_ERR_INVALID, "moe_plan_build: null counts or blob");
   if (E < 1 || E > 4096) MOE_FAIL(MOE_ERR_INVALID, "moe_plan_build: E=%d outside [1, 4096]", E);
@@ -106,7 +112,7 @@ moe_status moe_plan_build(const int32_t* counts, int32_t E, int64_t H, int64_t N
              "moe_plan_build: bn=%d must be a multiple of %d in [16, 256] (or of 32 in (256, 512] with bm=256)", bn,
              bm == 256 ? 32 : 16);
   if (flags & ~(MOE_PAD_REPEAT | MOE_SPLIT_TAIL | MOE_ORDER_ALTERNATING | MOE_ORDER_HALF_INTERVAL | MOE_GRID_BALANCED |
-                MOE_GRID_STATIC | MOE_A_GATHER4 | MOE_EPI_REGISTER))
+                MOE_GRID_STATIC | MOE_A_GATHER4 | MOE_EPI_REGISTER | MOE_SCHED_DYNAMIC | MOE_NO_L2_PREFETCH))
     MOE_FAIL(MOE_ERR_INVALID, "moe_plan_build: unknown flags 0x%x", flags);
   if ((flags & MOE_GRID_BALANCED) && (flags & MOE_GRID_STATIC))
     MOE_FAIL(MOE_ERR_INVALID, "moe_plan_build: MOE_GRID_BALANCED and MOE_GRID_STATIC are exclusive");
@@ -116,6 +122,34 @@ moe_status moe_plan_build(const int32_t* counts, int32_t E, int64_t H, int64_t N
   if (split && (bm != 256 || bn < 256))
     MOE_FAIL(MOE_ERR_UNSUPPORTED,
              "moe_plan_build: MOE_SPLIT_TAIL needs bm = 256 and bn = 256 or a wide tile (swap-AB tail tiles, M = 256)");
+  // Tile-strategy catalog (Alg. 3): the kind of each expert's last row tile, chosen by its
+  // row count r = m mod bm (the whole expert when m < bm): the first rule with r <= m_max.  Kind 1
+  // (MOE_KIND_SWAP) needs CTA-pair tiles with 256-column MMA blocks; other shapes have no rules.
+  moe_tile_rule cat[MOE_MAX_RULES];
+  int32_t n_cat = 0;
+  const bool pair_blocks = bm == 256 && bn >= 256;
+  if (split) {
+    cat[n_cat++] = {MOE_KIND_SWAP, bm};
+  } else if (n_rules < 0) {
+    if (pair_blocks) cat[n_cat++] = {MOE_KIND_SWAP, MOE_DEFAULT_SWAP_MAX};
+  } else {
+    if (n_rules > MOE_MAX_RULES) MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_plan_build: at most %d catalog rules", MOE_MAX_RULES);
+    if (n_rules > 0 && !rules) MOE_FAIL(MOE_ERR_INVALID, "moe_plan_build: null catalog");
+    for (int32_t i = 0; i < n_rules; ++i) {
+      if (rules[i].kind != MOE_KIND_WIDE && rules[i].kind != MOE_KIND_SWAP)
+        MOE_FAIL(MOE_ERR_INVALID, "moe_plan_build: catalog rule %d: kind %d", i, rules[i].kind);
+      if (rules[i].kind == MOE_KIND_SWAP && !pair_blocks)
+        MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_plan_build: MOE_KIND_SWAP needs bm = 256 and bn >= 256 (got %d x %d)", bm, bn);
+      cat[n_cat++] = rules[i];
+    }
+  }
+  auto kind_of = [&](int64_t m) -> int32_t {
+    const int64_t r = m % bm;
+    if (m <= 0 || r == 0) return MOE_KIND_WIDE;
+    for (int32_t i = 0; i < n_cat; ++i)
+      if (r <= cat[i].m_max) return cat[i].kind;
+    return MOE_KIND_WIDE;
+  };
   // CSR row offsets: exclusive prefix of counts in expert-id order.
   std::vector<int64_t> row_off(E + 1, 0);
   for (int32_t e = 0; e < E; ++e) {
@@ -186,6 +220,10 @@ moe_status moe_plan_build(const int32_t* counts, int32_t E, int64_t H, int64_t N
   blob[8] = bn;
   blob[9] = n_tasks;
   blob[10] = (int32_t)flags;
+  for (int32_t i = 0; i < MOE_MAX_RULES; ++i) {          // [12 .. 16): the catalog (kind, m_max) pairs
+    blob[12 + 2 * i] = i < n_cat ? cat[i].kind : MOE_KIND_WIDE;
+    blob[13 + 2 * i] = i < n_cat ? cat[i].m_max : -1;
+  }
   int32_t* pre = blob + MOE_PLAN_HEADER;
   int32_t* sig = pre + M_pad;
   int32_t* par = sig + M_pad;
@@ -205,7 +243,7 @@ moe_status moe_plan_build(const int32_t* counts, int32_t E, int64_t H, int64_t N
     p[0] = i;                                   // expert
     p[1] = (int32_t)row_off[i];                 // first CSR row of the task
     p[2] = counts[i];                           // rows
-    p[3] = split && counts[i] % bm ? 1 : 0;     // kind: 1 = last row tile is a swap-AB tail tile
+    p[3] = kind_of(counts[i]);                  // kind of the last row tile (1: swap-AB, the catalog)
     p[4] = bm;
     p[5] = bn;
     p[6] = (int32_t)ceil_div(counts[i], bm);    // row tiles
@@ -225,6 +263,8 @@ const char* moe_version(void) { return "moe_sm100 0.1 (sm_100a)"; }
 // ---------------------------------------------------------------------------
 // Device-resident plan
 // ---------------------------------------------------------------------------
+constexpr int64_t kSchedWords = 32;   // device words after the blob for the dynamic tile order (one 128-B line)
+
 struct moe_plan {
   std::vector<int32_t> blob;
   int64_t words = 0;
@@ -235,6 +275,8 @@ struct moe_plan {
   int64_t H = 0, N = 0;
   int32_t bm = 0, bn = 0;
   uint32_t flags = 0;
+  std::vector<moe_tile_rule> rules;   // the catalog given at creation (n_rules < 0: built-in)
+  int32_t n_rules = -1;
   bool device_mode = false;   // device blob written by moe_plan_device; host blob stale
 };
 
@@ -256,6 +298,13 @@ void plan_shape(const moe_plan* p, int32_t* E, int32_t* H, int32_t* N, int32_t* 
   *flags = p->flags;
 }
 int32_t* plan_blob_dev_mut(moe_plan* p) { return p->dev; }
+int32_t* plan_sched_dev(const moe_plan* p) { return p->dev + p->dev_words; }
+// The catalog (header words 12-15) holds a swap-AB rule: the launch needs the two-strategy kernel.
+bool plan_has_swap(const moe_plan* p) {
+  for (int i = 0; i < MOE_MAX_RULES; ++i)
+    if (p->blob[12 + 2 * i] == MOE_KIND_SWAP && p->blob[13 + 2 * i] > 0) return true;
+  return false;
+}
 }  // namespace moe
 
 extern "C" {
@@ -269,6 +318,12 @@ static moe_status upload(moe_plan* p, cudaStream_t s) {
 
 moe_status moe_plan_create(const int32_t* counts, int32_t E, int64_t H, int64_t N, int32_t bm,
                            int32_t bn, uint32_t flags, void* stream, moe_plan** out) {
+  return moe_plan_create_catalog(counts, E, H, N, bm, bn, flags, nullptr, -1, stream, out);
+}
+
+moe_status moe_plan_create_catalog(const int32_t* counts, int32_t E, int64_t H, int64_t N, int32_t bm, int32_t bn,
+                                   uint32_t flags, const moe_tile_rule* rules, int32_t n_rules, void* stream,
+                                   moe_plan** out) {
   moe::clear_error();
   if (!out) MOE_FAIL(MOE_ERR_INVALID, "moe_plan_create: null out");
   *out = nullptr;
@@ -280,11 +335,14 @@ moe_status moe_plan_create(const int32_t* counts, int32_t E, int64_t H, int64_t 
     zeros.assign(E, 0);
     counts = zeros.data();
   }
-  moe_status st = moe_plan_build(counts, E, H, N, bm, bn, flags, p->blob.data(), (int64_t)p->blob.size(), &p->words);
+  moe_status st = moe_plan_build_catalog(counts, E, H, N, bm, bn, flags, rules, n_rules, p->blob.data(),
+                                         (int64_t)p->blob.size(), &p->words);
   if (st < 0) {
     delete p;
     return st;
   }
+  if (n_rules > 0) p->rules.assign(rules, rules + n_rules);
+  p->n_rules = n_rules;
   bm = p->blob[7];                              // resolved tile height (bm = 0 means auto)
   bn = p->blob[8];                              // resolved tile width (bn = 0 means auto)
   flags = (uint32_t)p->blob[10];                // auto may add MOE_SPLIT_TAIL
@@ -296,8 +354,12 @@ moe_status moe_plan_create(const int32_t* counts, int32_t E, int64_t H, int64_t 
   p->bn = bn;
   p->flags = flags;
   p->dev_words = (int64_t)p->blob.size();
-  cudaError_t err = cudaMallocAsync((void**)&p->dev, sizeof(int32_t) * p->dev_words, p->stream);
+  // + kSchedWords after the blob: the dynamic tile order's counters (zero between launches)
+  cudaError_t err = cudaMallocAsync((void**)&p->dev, sizeof(int32_t) * (p->dev_words + kSchedWords), p->stream);
+  if (err == cudaSuccess)
+    err = cudaMemsetAsync(p->dev + p->dev_words, 0, sizeof(int32_t) * kSchedWords, p->stream);
   if (err != cudaSuccess) {
+    if (p->dev) cudaFreeAsync(p->dev, p->stream);
     delete p;
     MOE_FAIL(MOE_ERR_CUDA, "cudaMallocAsync(plan): %s", cudaGetErrorString(err));
   }
@@ -345,8 +407,8 @@ moe_status moe_plan_update(moe_plan* p, const int32_t* counts, void* stream) {
   moe::clear_error();
   if (!p) MOE_FAIL(MOE_ERR_INVALID, "moe_plan_update: null plan");
   int64_t words = 0;
-  moe_status st = moe_plan_build(counts, p->E, p->H, p->N, p->bm, p->bn, p->flags, p->blob.data(),
-                                 (int64_t)p->blob.size(), &words);
+  moe_status st = moe_plan_build_catalog(counts, p->E, p->H, p->N, p->bm, p->bn, p->flags, p->rules.data(), p->n_rules,
+                                         p->blob.data(), (int64_t)p->blob.size(), &words);
   if (st < 0) return st;
   p->words = words;
   p->device_mode = false;

@@ -42,7 +42,17 @@ __device__ __forceinline__ void plan_body(long long m, int E, int H, int N, int 
                                           int32_t* __restrict__ blob) {
   __shared__ long long s_warp[32];
   const int t = threadIdx.x;                                       // expert t
-  const bool split = (flags & MOE_SPLIT_TAIL) != 0;
+  // The catalog (header words 12-15, written at plan creation and never rewritten here): kind of
+  // each expert's last row tile by its r = m mod bm rows (include/moe_sm100.h).
+  int32_t kind = MOE_KIND_WIDE;
+  {
+    const long long r = m % bm;
+    if (m > 0 && r > 0) {
+      for (int i = MOE_MAX_RULES - 1; i >= 0; --i)                 // the first matching rule wins
+        if (r <= blob[13 + 2 * i]) kind = blob[12 + 2 * i];
+    }
+  }
+  __syncthreads();                                                 // every thread read the catalog
   const long long col_tiles = (N + bn - 1) / bn;
   const long long row_tiles = (m + bm - 1) / bm;
   const long long nu = m > 0 ? row_tiles * col_tiles : 0;         // nu(T_t)
@@ -72,7 +82,7 @@ __device__ __forceinline__ void plan_body(long long m, int E, int H, int N, int 
       case 9: w = E; break;
       case 10: w = (int32_t)flags; break;
       case 11: w = overflow ? 3 : 0; break;          // device planner status (3 = capacity)
-      default: w = 0;
+      default: w = blob[t];                          // [12, 16): the catalog, kept
     }
     blob[t] = w;
   }
@@ -125,7 +135,7 @@ __device__ __forceinline__ void plan_body(long long m, int E, int H, int N, int 
     p[0] = t;
     p[1] = (int32_t)(rows_incl - m);
     p[2] = (int32_t)m;
-    p[3] = split && (m % bm) ? 1 : 0;               // kind 1: last row tile is a swap-AB tail
+    p[3] = kind;                                    // the catalog's strategy for the last row tile
     p[4] = bm;
     p[5] = bn;
     p[6] = (int32_t)row_tiles;

@@ -22,6 +22,7 @@ def main():
     bn = int(sys.argv[2]) if len(sys.argv) > 2 else 256
     bm = int(sys.argv[3]) if len(sys.argv) > 3 else 128
     flags = int(sys.argv[4]) if len(sys.argv) > 4 else 0
+    catalog = () if len(sys.argv) > 5 and sys.argv[5] == "none" else None   # "none": one strategy per launch
     fp8 = os.environ.get("FP8", "0") == "1"          # FP8 E4M3 operands (moe_gemm_fp8)
     c = synth.CONFIGS[name]
     ids = torch.from_numpy(synth.route(c, 0)).cuda()
@@ -35,7 +36,7 @@ def main():
         W = synth.make_w_torch(0, c.E, c.H, c.N, device="cuda")
         gemm = M.moe_gemm
     counts, row_off, tok, _, _ = M.moe_route(ids, c.E)
-    plan = M.Plan(counts.cpu().numpy(), c.H, c.N, bm, bn, flags)
+    plan = M.Plan(counts.cpu().numpy(), c.H, c.N, bm, bn, flags, catalog=catalog)
     Y = torch.empty((tok.numel(), c.N), dtype=torch.bfloat16, device="cuda")
     for _ in range(3):
         gemm(plan, X, tok, W, Y=Y)
@@ -80,9 +81,13 @@ def main():
     t_prof = ev[0].elapsed_time(ev[1])
     pall = prof.double()
     p = pall[0::2] if bm == 256 else pall           # MMA counters live in the pair leaders
+    busy = p[:, 6] > 0                              # CTAs (pairs) that processed tiles
+    p = p[busy]
+    if bm == 256:
+        pall = torch.stack([pall[0::2][busy], pall[1::2][busy]], 1).reshape(-1, pall.shape[1])
     tot = p[:, 2]
     out = {
-        "config": name, "fp8": fp8, "bn": bn, "bm": bm, "flags": flags, "tiles": plan.total_tiles, "ms_plain": t_plain, "ms_instrumented": t_prof,
+        "config": name, "fp8": fp8, "bn": bn, "bm": bm, "flags": flags, "catalog": plan.catalog, "tiles": plan.total_tiles, "ms_plain": t_plain, "ms_instrumented": t_prof,
         "tflops_plain": c.flops / t_plain / 1e9, "sm_mhz_plain": sm_mhz,
         "tensor_frac_at_clock": (c.flops / t_plain / 1e9) / (148 * 8192 * sm_mhz * 1e-6) if sm_mhz else None,
         "identical_Y": bool(torch.equal(Y, Y2)),

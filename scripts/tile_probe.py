@@ -3,7 +3,8 @@
     python scripts/tile_probe.py --cases paper_worst:256:512:0:natural,paper_worst:256:512:2:half_interval
         [--reps 20] [--out gpurun_out/probe.jsonl]
 
-A case is cfg:bm:bn:flags:order; flags is the integer moe_plan flag word (2 = MOE_SPLIT_TAIL, ...).
+A case is cfg:bm:bn:flags:order[:catalog]; flags is the integer moe_plan flag word (2 = MOE_SPLIT_TAIL,
+...); catalog is "default", "none", or rules "kind.m_max+kind.m_max" (e.g. 1.64 = swap tails <= 64 rows).
 Kernel time = CUDA events around one moe_gemm launch after a clean-L2 flush (bench.py's method),
 median over reps.  Prints one JSON line per case with TFLOP/s and the fraction of the measured peak.
 """
@@ -62,21 +63,33 @@ def main():
     cache = {}
     out = open(args.out, "a") if args.out else None
     for case in args.cases.split(","):
-        cfg, bm, bn, flags, order = case.split(":")
-        c = synth.CONFIGS[cfg]
+        parts = case.split(":")
+        cfg, bm, bn, flags, order = parts[:5]
+        cat = parts[5] if len(parts) > 5 else "default"
+        catalog = None if cat == "default" else () if cat == "none" else tuple(
+            tuple(int(x) for x in r.split(".")) for r in cat.split("+"))
+        if cfg.startswith("light"):                 # lightN: N experts of the paper §5 shape, one token each
+            n = int(cfg[5:])
+            c = synth.Config(cfg, E=64, k=1, T=n, H=3584, N=2560, routing="custom")
+            ids_np = np.arange(n, dtype=np.int32)[:, None]
+        else:
+            c = synth.CONFIGS[cfg]
+            ids_np = None
         if cfg not in cache:
             cache.clear()
-            ids = torch.from_numpy(synth.route(c)).cuda()
+            ids = torch.from_numpy(synth.route(c) if ids_np is None else ids_np).cuda()
             counts, row_off, tok, _, _ = M.moe_route(ids, c.E)
             X = synth.make_x_torch(0, c.T, c.H, device="cuda")
             W = synth.make_w_torch(0, c.E, c.H, c.N, device="cuda")
             Y = torch.empty((tok.numel(), c.N), dtype=torch.bfloat16, device="cuda")
             cache[cfg] = (counts.cpu().numpy(), tok, X, W, Y)
         counts_h, tok, X, W, Y = cache[cfg]
-        plan = M.Plan(counts_h, c.H, c.N, int(bm), int(bn), int(flags) | ORDER[order])
+        plan = M.Plan(counts_h, c.H, c.N, int(bm), int(bn), int(flags) | ORDER[order], catalog=catalog)
         ms, mn = time_gemm(plan, X, tok, W, Y, flush, args.reps)
         tf = c.flops / (ms * 1e-3) / 1e12
-        line = {"case": case, "tile": f"{plan.bm}x{plan.bn}", "tiles": plan.total_tiles, "ms": ms, "ms_min": mn,
+        kinds = M.parse_plan_blob(plan.blob())["params"][:, 3]
+        line = {"case": case, "tile": f"{plan.bm}x{plan.bn}", "catalog": plan.catalog, "swap_tasks": int(kinds.sum()),
+                "tiles": plan.total_tiles, "ms": ms, "ms_min": mn,
                 "tflops": tf, "frac": tf / peak}
         print(json.dumps(line), flush=True)
         if out:

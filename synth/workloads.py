@@ -85,6 +85,8 @@ CONFIGS: dict[str, Config] = {
     "paper_worst": Config("paper_worst", E=64, k=8, T=4096, H=3584, N=2560, routing="worst",
                           notes="paper §5 worst case (P:375)"),
 }
+CONFIGS["paper_light8"] = Config("paper_light8", E=64, k=1, T=8, H=3584, N=2560, routing="light",
+                                 notes="probe: 8 experts of the paper §5 shape with one token each (memory-bound tiles)")
 for _T in (1, 2, 4, 8, 16, 32, 64, 128, 256):
     CONFIGS[f"dec{_T}"] = Config(f"dec{_T}", E=8, k=2, T=_T, H=4096, N=14336, routing="uniform",
                                  notes="BASELINE configs[3]: decode regime, Mixtral shape")
@@ -156,6 +158,8 @@ def route(cfg: Config, seed: int = 0) -> np.ndarray:
         return route_paper_best(cfg.T, cfg.E, cfg.k)
     if cfg.routing == "worst":
         return route_paper_worst(cfg.T, cfg.E, cfg.k)
+    if cfg.routing == "light":                     # token t -> expert t (one token per expert)
+        return np.ascontiguousarray(np.arange(cfg.T, dtype=np.int32)[:, None] % cfg.E)
     raise ValueError(cfg.routing)
 
 

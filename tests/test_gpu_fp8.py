@@ -109,9 +109,27 @@ def test_fp8_unsupported_shapes_rejected():
     with pytest.raises(M.MoeError):                # N % 128 != 0
         M.moe_gemm_fp8(M.Plan([1, 0], 128, 200, 128, 128), Xd, tok, Wd)
     Wd = torch.zeros((2, 128, 256), dtype=torch.uint8, device="cuda")
-    for bm, bn, flags in ((64, 256, 0), (256, 256, M.MOE_SPLIT_TAIL), (128, 64, 0), (256, 384, 0)):
+    for bm, bn, flags in ((64, 256, 0), (128, 64, 0), (256, 384, 0)):
         with pytest.raises(M.MoeError):
             M.moe_gemm_fp8(M.Plan([1, 0], 128, 256, bm, bn, flags), Xd, tok, Wd)
+
+
+def test_fp8_ignores_swap_catalog():
+    """The FP8 kernel runs every tile as MOE_KIND_WIDE: a plan whose catalog asks for swap-AB tails
+    (built-in catalog, MOE_SPLIT_TAIL) still gives the exact result (same tile partition)."""
+    T, E, k, H, N = 300, 5, 2, 256, 512
+    ids = synth.route_gumbel(3, T, E, k)
+    X8, W8 = sfp8.make_x_fp8(3, T, H, "int"), sfp8.make_w_fp8(3, E, H, N, "int")
+    rc, rr, rt, rs = omoe.buckets(ids, E)
+    ref = ofp8.expert_gemm_fp8(X8, W8, rt, rr)
+    topk = torch.from_numpy(ids).cuda()
+    counts, _, tok, _, _ = M.moe_route(topk, E)
+    for flags, cat in ((M.MOE_SPLIT_TAIL, None), (0, None), (0, ((1, 256),))):
+        plan = M.Plan(counts.cpu().numpy(), H, N, 256, 512, flags, catalog=cat)
+        assert plan.catalog
+        Y = M.moe_gemm_fp8(plan, torch.from_numpy(X8).cuda(), tok, torch.from_numpy(W8).cuda(), out_dtype=torch.float32)
+        torch.cuda.synchronize()
+        assert np.array_equal(Y.cpu().double().numpy(), ref)
 
 
 @pytest.mark.parametrize("cfg,bm,bn", [("mix", 0, 0), ("ds", 0, 0), ("dec16", 0, 0), ("dec1", 128, 256)])

@@ -652,3 +652,80 @@ def test_split_tail_consecutive_tail_tiles(out_dtype, bn):
     ref = omoe.expert_gemm(X, W, rt, rr)
     exp = ref if out_dtype == torch.float32 else torch.from_numpy(ref).to(torch.bfloat16).double().numpy()
     assert np.array_equal(Y.cpu().double().numpy(), exp)
+
+
+# ---------------------------------------------------------------------------- per-task strategies + tile order
+@pytest.mark.parametrize("case", range(40))
+def test_catalog_and_dynamic_order_fuzz(case):
+    """Mixed-kind plans (the catalog's WIDE / SWAP strategies for each expert's last row tile, P:213,
+    P:251-253) under the static and the dynamic tile order: bit-exact on integer data, fp32 and bf16
+    out, host and device plans, three launches on one plan (the dynamic counter resets each time)."""
+    rng = np.random.default_rng(1000 + case)
+    E = int(rng.integers(1, 24))
+    k = int(rng.integers(1, min(E, 4) + 1))
+    T = int(rng.integers(1, 1500))
+    H = int(rng.choice([64, 128, 200, 512]))
+    N = int(rng.choice([256, 512, 640, 1024, 1408]))
+    bn = int(rng.choice([256, 512]))
+    rules = [(int(rng.integers(0, 2)), int(rng.integers(0, 257))) for _ in range(int(rng.integers(0, 3)))]
+    flags = int(rng.choice([0, M.MOE_SCHED_DYNAMIC])) | int(rng.choice([0, M.MOE_ORDER_HALF_INTERVAL]))
+    out = torch.float32 if case % 2 else torch.bfloat16
+    ids = synth.route_gumbel(case, T, E, k, s=float(rng.choice([0.0, 1.5])), n_empty=int(rng.integers(0, E - k + 1)))
+    X, W = synth.make_x(case, T, H, "int"), synth.make_w(case, E, H, N, "int")
+    Xd = torch.from_numpy(X).to(torch.bfloat16).cuda()
+    Wd = torch.from_numpy(W).to(torch.bfloat16).cuda()
+    topk = torch.from_numpy(ids).cuda()
+    rc, rr, rt, _ = omoe.buckets(ids, E)
+    ref = omoe.expert_gemm(X, W, rt, rr)
+    ref_t = torch.from_numpy(ref).to(out).double().numpy()
+    device_plan = bool(case % 3 == 0)
+    if device_plan:
+        plan = M.Plan(None, H, N, 256, bn, flags, E=E, catalog=rules)
+    else:
+        counts, _, _, _, _ = M.moe_route(topk, E)
+        plan = M.Plan(counts.cpu().numpy(), H, N, 256, bn, flags, catalog=rules)
+        kinds = M.parse_plan_blob(plan.blob())["params"][:, 3]
+        assert kinds.tolist() == [omoe.tail_kind(m, 256, rules) for m in rc]
+    for rep in range(3):
+        _, _, tok, _, _ = M.moe_route(topk, E, plan=plan if device_plan else None)
+        Y = torch.full((T * k, N), float("nan"), dtype=out, device="cuda")
+        M.moe_gemm(plan, Xd, tok, Wd, Y=Y)
+        torch.cuda.synchronize()
+        assert np.array_equal(Y.cpu().double().numpy(), ref_t), (rep, rules, flags, bn)
+
+
+@pytest.mark.parametrize("cfg", ["paper_worst", "ds", "mix"])
+def test_dynamic_order_full_size_graph(cfg):
+    """The dynamic tile order at full size inside a CUDA graph replayed three times (device plan fused
+    into the route, built-in catalog): sampled entries against the fp64 oracle, identical replays."""
+    c = synth.CONFIGS[cfg]
+    ids = synth.route(c, 0)
+    topk = torch.from_numpy(ids).cuda()
+    Xd = synth.make_x_torch(0, c.T, c.H, device="cuda")
+    Wd = synth.make_w_torch(0, c.E, c.H, c.N, device="cuda")
+    plan = M.Plan(None, c.H, c.N, 256, 512, M.MOE_SCHED_DYNAMIC, E=c.E)
+    Y = torch.empty((c.T * c.k, c.N), dtype=torch.bfloat16, device="cuda")
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        _, _, tok, _, _ = M.moe_route(topk, c.E, with_slot=False, plan=plan)
+        M.moe_gemm(plan, Xd, tok, Wd, Y=Y)
+    torch.cuda.current_stream().wait_stream(side)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        _, _, tok_g, _, _ = M.moe_route(topk, c.E, with_slot=False, plan=plan)
+        M.moe_gemm(plan, Xd, tok_g, Wd, Y=Y)
+    outs = []
+    for _ in range(3):
+        Y.fill_(float("nan"))
+        g.replay()
+        torch.cuda.synchronize()
+        outs.append(Y.clone())
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[1], outs[2])
+    rc, rr, rt, _ = omoe.buckets(ids, c.E)
+    rng = np.random.default_rng(2)
+    rows = _sample_rows(rr, rc, rng, 3)
+    cols = np.unique(np.concatenate([rng.integers(0, c.N, 16), [0, c.N - 1]]))
+    ref = omoe.expert_gemm_entries(lambda t: wl.x_rows(0, c.T, c.H, [t])[0],
+                                   lambda e, cs: wl.w_columns(0, c.E, c.H, c.N, e, cs), rt, rr, rows, cols)
+    tol_check(outs[0][torch.from_numpy(rows).cuda()][:, torch.from_numpy(cols).cuda()].cpu(), ref, cfg)

@@ -45,11 +45,18 @@ def test_library_exports_every_declared_symbol():
 ORDER_FLAG = {"natural": 0, "alternating": 4, "half_interval": 8}
 
 
-def _compare(counts, N, bm, bn, pad, split=False, order="natural"):
+def _compare(counts, N, bm, bn, pad, split=False, order="natural", catalog=None):
+    """catalog None: the library's built-in catalog, whose rule the test states independently
+    ((SWAP, 64) on CTA-pair plans with 256-column blocks, none otherwise)."""
     flags = (moe_lib.MOE_PAD_REPEAT if pad == "repeat" else 0) | (moe_lib.MOE_SPLIT_TAIL if split else 0)
-    blob = moe_lib.moe_plan_build(counts, 64, N, bm, bn, flags | ORDER_FLAG[order])
+    blob = moe_lib.moe_plan_build(counts, 64, N, bm, bn, flags | ORDER_FLAG[order], catalog=catalog)
     p = moe_lib.parse_plan_blob(blob)
-    ref = omoe.plan(counts, N, bm, bn, pad_mode=pad, split_tail=split, order=order)
+    if catalog is None:
+        catalog = ((1, 64),) if (bm == 256 and bn >= 256) else ()
+    if split:
+        catalog = ((1, bm),)
+    assert p["catalog"] == tuple(catalog)
+    ref = omoe.plan(counts, N, bm, bn, pad_mode=pad, split_tail=split, order=order, catalog=catalog)
     assert p["M"] == ref["M"] and p["total"] == ref["total"]
     if ref["M"] == 0:
         return
@@ -266,3 +273,29 @@ def test_plan_launch_option_flags():
         assert p["flags"] == f
     with pytest.raises(moe_lib.MoeError):
         moe_lib.moe_plan_build(counts, 64, 256, 128, 128, moe_lib.MOE_GRID_BALANCED | moe_lib.MOE_GRID_STATIC)
+
+
+def test_planner_catalog_matches_oracle():
+    """Per-task tiling strategies: random catalogs of up to two rules; the kind of
+    each expert's last row tile equals the oracle's tail_kind, and the mapping is unchanged."""
+    rng = random.Random(21)
+    for _ in range(200):
+        E = rng.randint(1, 200)
+        counts = np.array([0 if rng.random() < 0.3 else rng.randint(1, 3000) for _ in range(E)])
+        rules = [(rng.choice([0, 1]), rng.randint(0, 256)) for _ in range(rng.randint(0, 2))]
+        N = 8 * rng.randint(1, 3000)
+        bn = rng.choice([256, 512])
+        _compare(counts, N, 256, bn, rng.choice(["max", "repeat"]), catalog=rules,
+                 order=rng.choice(["natural", "half_interval"]))
+        base = moe_lib.parse_plan_blob(moe_lib.moe_plan_build(counts, 64, N, 256, bn, catalog=()))
+        got = moe_lib.parse_plan_blob(moe_lib.moe_plan_build(counts, 64, N, 256, bn, catalog=rules))
+        assert np.array_equal(base["prefix"], got["prefix"]) and np.array_equal(base["sigma"], got["sigma"])
+    # worked examples: tails 1 and 200 under {SWAP, 64}; 256-row experts have no tail
+    p = moe_lib.parse_plan_blob(moe_lib.moe_plan_build([1, 456, 256, 0, 64, 65], 64, 1024, 256, 512))
+    assert p["params"][:, 3].tolist() == [1, 0, 0, 0, 1, 0]
+    with pytest.raises(moe_lib.MoeError):                              # swap tiles need CTA-pair 256-column blocks
+        moe_lib.moe_plan_build([5, 5], 64, 1024, 128, 256, catalog=[(1, 64)])
+    with pytest.raises(moe_lib.MoeError):
+        moe_lib.moe_plan_build([5, 5], 64, 1024, 256, 512, catalog=[(1, 64), (0, 9), (1, 200)])
+    with pytest.raises(moe_lib.MoeError):
+        moe_lib.moe_plan_build([5, 5], 64, 1024, 256, 512, catalog=[(7, 64)])
