@@ -170,6 +170,17 @@ def oracle_sample(cfg, seed: int, budget_s: float, cache: dict | None = None, fp
     return flops, secs, sample, cores
 
 
+def ref_config(cfg, args, ws: int) -> dict:
+    """The reference arm reports the `config` our arm prints for the same command (the tile label is the
+    planner's host rule, moe_plan_suggest_tile; nothing of our engine runs in this arm)."""
+    if ws > 1 or args.ep:
+        return ep_config(cfg, ws, args)
+    import paper_2501_16103_b200 as M
+    if not (args.bm or args.bn):
+        args.bm_resolved, args.bn_resolved = M.suggest_tile(cfg.T * cfg.k, cfg.E, cfg.H, cfg.N)
+    return config_dict(cfg, args)
+
+
 def run_reference(args, cfg):
     ws, rank, _ = dist_env()
     if rank != 0:
@@ -192,7 +203,7 @@ def run_reference(args, cfg):
         "impl": "reference", "metric": METRIC, "value": v, "unit": "TFLOP/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(statistics.mean(ms)),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": config_dict(cfg, args),
+        "data": "synthetic", "config": ref_config(cfg, args, ws),
         "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": info[1], "kind": "oracle", "sample": info[0]},
         "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -330,6 +341,31 @@ def run_ffn(args, cfg):
         "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)
+
+
+def ep_workload(base, ws: int):
+    """The expert-parallel workload at ws ranks: strong scaling on the 8x22B `ep` shape (total T fixed),
+    weak scaling otherwise (T per rank fixed).  Returns (config, strong, T per rank, experts per rank)."""
+    strong = base.name == "ep"
+    T_total = base.T if strong else base.T * ws
+    if base.E % ws or T_total % ws:
+        raise SystemExit(f"E={base.E} and T={T_total} must be divisible by {ws} ranks")
+    cfg = synth.Config(f"{base.name}-ep{ws}", E=base.E, k=base.k, T=T_total, H=base.H, N=base.N,
+                       routing=base.routing, zipf_s=base.zipf_s, n_empty=base.n_empty)
+    return cfg, strong, T_total // ws, base.E // ws
+
+
+def ep_config(base, ws: int, args) -> dict:
+    """`config` of an N > 1 line (both arms print the same one)."""
+    import paper_2501_16103_b200 as M
+    cfg, _, T_l, El = ep_workload(base, ws)
+    bm, bn = (args.bm, args.bn) if args.bm or args.bn else M.suggest_tile(T_l * cfg.k, El, cfg.H, cfg.N)
+    return {"workload": f"{cfg.name}: E={cfg.E} top-{cfg.k} T={cfg.T} ({T_l}/rank) H={cfg.H} N={cfg.N} "
+                        f"routing={cfg.routing} seed={args.seed}",
+            "tile": f"{bm}x{bn}", "out_dtype": args.out_dtype,
+            "operands": "FP8 E4M3 X and W, per-expert fp32 scale" if getattr(args, "dtype", "bf16") == "fp8" else "bf16",
+            "global_batch": cfg.T, "parallelism": f"ep{ws}",
+            "l2": "flushed before every timed step (memset + read: clean L2)"}
 
 
 def config_dict(cfg, args):
@@ -656,20 +692,25 @@ def run_ep(args, base):
     for k_, v_ in (("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", "29531"), ("RANK", "0"), ("WORLD_SIZE", "1")):
         os.environ.setdefault(k_, v_)                 # `--ep` on one GPU without torchrun
     ws, rank, local = dist_env()
+    # More ranks than GPUs (a functional run of the multi-rank path on a smaller box): ranks share
+    # devices, the process group is gloo (NCCL refuses two ranks on one GPU), the peer transport maps
+    # regions with CUDA IPC on the same device.  The line says so; it is not a scaling number.
+    n_dev = torch.cuda.device_count()
+    shared = n_dev < ws
+    local = local % n_dev
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
+    if shared:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=dev)
+    cdev = torch.device("cpu") if shared else dev    # where the bench's own small collectives run
     M.moe_device_info()
     peaks, peak_src = load_peaks()
     out_dtype = torch.bfloat16 if args.out_dtype == "bf16" else torch.float32
-    strong = base.name == "ep"                      # BASELINE configs[4]: total T fixed across N
-    T_total = base.T if strong else base.T * ws     # otherwise weak scaling: T per GPU fixed
-    if base.E % ws or T_total % ws:
-        raise SystemExit(f"E={base.E} and T={T_total} must be divisible by {ws} ranks")
-    cfg = synth.Config(f"{base.name}-ep{ws}", E=base.E, k=base.k, T=T_total, H=base.H, N=base.N,
-                       routing=base.routing, zipf_s=base.zipf_s, n_empty=base.n_empty)
+    cfg, strong, T_l, El = ep_workload(base, ws)
+    T_total = cfg.T
     ids = synth.route(cfg, args.seed)               # the global batch (identical on every rank)
-    T_l, El = T_total // ws, cfg.E // ws
     topk_l = torch.from_numpy(np.ascontiguousarray(ids[rank * T_l:(rank + 1) * T_l])).to(dev)
     fp8 = args.dtype == "fp8"
     if fp8:                                          # FP8 E4M3 rows and weights (synth/fp8.py, R15)
@@ -683,7 +724,18 @@ def run_ep(args, base):
         W_l = synth.make_w_torch(args.seed, cfg.E, cfg.H, cfg.N, device=dev, experts=range(rank * El, (rank + 1) * El))
         w_scale = None
     native = None
-    if not args.ep_python:                           # the library's moe_ep_* step (NCCL from C++)
+    peer = not args.ep_python and args.ep_transport == "peer"
+    out_view = None
+    if peer:                                         # the library's moe_ep_* step over symmetric peer memory
+        def allgather(blob):
+            got = [None] * ws
+            dist.all_gather_object(got, blob)
+            return got
+        y_bytes = cfg.N * (2 if out_dtype == torch.bfloat16 else 4)
+        native = M.PeerExpertParallel(rank, ws, cfg.E, W_l, max_tokens=T_l, k=cfg.k, allgather=allgather,
+                                      w_scale=w_scale, bm=args.bm, bn=args.bn, max_out_bytes=y_bytes)
+        out_view = native.output(T_l, cfg.N, out_dtype)          # zero copy: the rows stay in the output buffer
+    elif not args.ep_python:                         # the library's moe_ep_* step (NCCL from C++)
         uid = torch.zeros(128, dtype=torch.uint8, device=dev)
         if rank == 0:
             uid.copy_(torch.frombuffer(bytearray(M.moe_ep_unique_id()), dtype=torch.uint8))
@@ -693,7 +745,12 @@ def run_ep(args, base):
     moe = ExpertParallelMoE(cfg.E, W_l, TorchComm(), bm=args.bm, bn=args.bn, out_dtype=out_dtype, w_scale=w_scale)
     flush = L2Flush(torch, dev)
     stream = torch.cuda.current_stream()
-    fwd = (lambda t, x: native.forward(t, x, out_dtype=out_dtype)) if native is not None else moe.forward
+    if peer:
+        fwd = lambda t, x: native.forward(t, x, out=out_view)            # noqa: E731
+    elif native is not None:
+        fwd = lambda t, x: native.forward(t, x, out_dtype=out_dtype)     # noqa: E731
+    else:
+        fwd = moe.forward
     for _ in range(args.warmup):
         fwd(topk_l, X_l)
     torch.cuda.synchronize()
@@ -718,14 +775,14 @@ def run_ep(args, base):
                 local_rows.append(native.last_rows()["local_rows"])
     torch.cuda.synchronize()
     dist.barrier()
-    t = torch.tensor([sum(step_ms)], device=dev)
+    t = torch.tensor([sum(step_ms)], device=cdev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     value = cfg.flops * args.steps / (float(t.item()) * 1e-3) / 1e12
     gemm_avg = statistics.mean(gemm_ms)
     flops_l = 2 * local_rows[-1] * cfg.H * cfg.N
     achieved = flops_l / (gemm_avg * 1e-3) / 1e12
     peak = float(peaks["bf16_tflops"]) * (2.0 if fp8 else 1.0)
-    per_rank = torch.tensor([statistics.mean(step_ms), gemm_avg, achieved], device=dev)
+    per_rank = torch.tensor([statistics.mean(step_ms), gemm_avg, achieved], device=cdev)
     gathered = [torch.zeros_like(per_rank) for _ in range(ws)]
     dist.all_gather(gathered, per_rank)
     # e2e: the rank's X / top-k ids from pinned host memory, result rows back to the host
@@ -749,12 +806,11 @@ def run_ep(args, base):
             s1.synchronize()
             if i >= 2:
                 e_ms.append(s0.elapsed_time(s1))
-        te_max = torch.tensor([sum(e_ms)], device=dev)
+        te_max = torch.tensor([sum(e_ms)], device=cdev)
         dist.all_reduce(te_max, op=dist.ReduceOp.MAX)
         e2e = {"value": cfg.flops * len(e_ms) / (float(te_max.item()) * 1e-3) / 1e12, "unit": "TFLOP/s",
                "h2d_bytes_per_step": int(X_h.numel() * X_h.element_size() + ids_h.numel() * 4) * ws,
                "d2h_bytes_per_step": int(out_h.numel() * out_h.element_size()) * ws}
-    probe = M.Plan(None, cfg.H, cfg.N, args.bm, args.bn, E=El)     # the local GEMM's resolved tile shape
     # rank 0's exchange traffic per step (rows out / in for dispatch and return, incl. its own share)
     if native is not None:
         lr = native.last_rows()
@@ -765,21 +821,22 @@ def run_ep(args, base):
                       "combine_rows": lr["local_rows"], "combine_bytes": lr["local_rows"] * y_b}
     else:
         exch_bytes = None
-    tile_ep = f"{probe.bm}x{probe.bn}"
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": float(t.item()) / args.steps, "higher_is_better": True,
             "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "fp8_e4m3" if fp8 else "bf16",
             "data": "synthetic",
-            "config": {"workload": f"{cfg.name}: E={cfg.E} top-{cfg.k} T={cfg.T} ({T_l}/rank) H={cfg.H} N={cfg.N} "
-                                   f"routing={cfg.routing} seed={args.seed}",
-                       "tile": tile_ep,
-                       "out_dtype": args.out_dtype, "global_batch": cfg.T, "parallelism": f"ep{ws}",
-                       "collectives": ("NCCL grouped send/recv from the library (moe_ep_forward): counts, "
+            "config": {**ep_config(base, ws, args),
+                       **({"oversubscribed": f"{ws} ranks on {n_dev} GPU(s): functional run, not a scaling number"}
+                          if shared else {}),
+                       "collectives": ("none: symmetric peer memory (CUDA IPC) — dispatch rows stored into the "
+                                       "owners' receive buffers, the GEMM epilogue storing result rows into the "
+                                       "token owners' outputs, device-side epoch flags (moe_ep_peer_*)") if peer else
+                                      ("NCCL grouped send/recv from the library (moe_ep_forward): counts, "
                                        "dispatch rows, combine rows") if native is not None else
                                       ("NCCL all_to_all_single (torch.distributed): counts, dispatch rows, "
-                                       "combine rows"), "l2": "flushed before every timed step (memset + read: clean L2)"},
+                                       "combine rows")},
             "pct_of_peak": value / (peak * ws),
             "exchange_bytes_per_step_rank0": exch_bytes,
             "per_rank": [{"ms_per_step": float(g[0]), "gemm_ms": float(g[1]), "gemm_tflops": float(g[2])}
@@ -792,9 +849,12 @@ def run_ep(args, base):
                          "algorithmic_flops_per_launch": flops_l},
             "cpu_baseline": None,
             "e2e": e2e,
-            # dispatch 2, gather 1, route (1-3, on the received rows), plan 1, combine map 1, GEMM 1, unpack 1
-            "gpu_launches": (7 + route_launches(native.last_rows()["received"] if native is not None
-                                                else sum(moe.last["recv_rows"]), El, cfg.k)) * args.steps,
+            # NCCL / torch paths: dispatch plan 2, gather 1, route (1-3, on the received rows), plan 1, combine
+            # map 1, GEMM 1, unpack 1.  Peer path: dispatch plan 2, dispatch 1, signal + wait 2, route (on the
+            # G * T_l receive rows), id reset 1, row pointers 1, GEMM 1, signal + wait 2.
+            "gpu_launches": ((10 + route_launches(ws * T_l, El, cfg.k)) if peer else
+                             (7 + route_launches(native.last_rows()["received"] if native is not None
+                                                 else sum(moe.last["recv_rows"]), El, cfg.k))) * args.steps,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -815,6 +875,8 @@ def main():
     ap.add_argument("--ep-python", action="store_true",
                     help="expert parallelism orchestrated in Python over torch.distributed all_to_all_single "
                          "(default: the library's moe_ep_forward, NCCL called from C++)")
+    ap.add_argument("--ep-transport", choices=["peer", "nccl"], default="peer",
+                    help="the library's EP step: symmetric peer memory over CUDA IPC (default) or NCCL send/recv")
     ap.add_argument("--order", choices=list(ORDER_FLAGS), default="natural",
                     help="sigma order of the plan's tasks (P:317-322 expert ordering; DESIGN.md R7)")
     ap.add_argument("--dtype", choices=["bf16", "fp8"], default="bf16",
@@ -831,7 +893,19 @@ def main():
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")
     cfg = synth.CONFIGS[args.config]
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        # `--gpus N` without torchrun: re-launch as N ranks (one process per GPU) and return their exit code
+        import socket
+        import subprocess
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        raise SystemExit(subprocess.call(cmd))
     ws = dist_env()[0]
+    if ws != args.gpus and args.impl == "ours":
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={ws}: launch with --nproc-per-node {args.gpus}")
     if args.impl == "reference":
         run_reference(args, cfg)
     elif args.ffn:

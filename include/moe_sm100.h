@@ -62,8 +62,8 @@ typedef int32_t moe_status;
 #define MOE_A_GATHER4      64u  /* stage token rows with TMA tile::gather4 (one-CTA tiles) instead of
                                    cp.async                                                           */
 #define MOE_EPI_REGISTER  128u  /* bf16 Y through masked register stores only (no TMA tile stores)    */
-#define MOE_NO_L2_PREFETCH 512u /* no load/store-path L2 prefetch of W for memory-bound tiles (one-CTA
-                                   tiles, swap-AB tiles) ahead of the ring                            */
+#define MOE_L2_PREFETCH   512u  /* load/store-path L2 prefetch of W for memory-bound tiles (one-CTA tiles,
+                                   swap-AB tiles) ahead of the ring — opt-in: measured slower */
 #define MOE_SCHED_DYNAMIC 256u  /* dynamic tile order: after its first tile each persistent CTA (pair)
                                    takes the next virtual tile from a counter in the plan's device
                                    memory (the order the hardware dispatches one block per tile,

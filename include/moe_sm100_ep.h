@@ -138,7 +138,55 @@ moe_status moe_ep_last_rows(const moe_ep* ep, int64_t* sent, int64_t* received, 
  * stream; waits for the second one).  MOE_OK_EMPTY (0 ms) when the rank had no local rows. */
 moe_status moe_ep_last_gemm_ms(const moe_ep* ep, float* ms);
 
+/* Releases the handle (either transport).  Peer handles: every rank must have finished its last step
+ * (synchronise, then a barrier of the caller's) before any rank destroys, since peers store into
+ * this rank's region. */
 void moe_ep_destroy(moe_ep* ep);
+
+/* ------------------------------------------------------------------------------------------
+ * The same step over symmetric peer memory (no collective library, no host synchronisation).
+ * Each rank allocates one device region: receive buffers for max_tokens rows from every rank
+ * (fixed segment per source), its output rows in (token, slot) order, epoch flags.  The region is
+ * exported as a CUDA IPC handle inside a MOE_EP_PEER_BLOB_BYTES blob; the caller all-gathers the
+ * blobs (plumbing, e.g. torch.distributed) and every rank maps every peer's region once
+ * (moe_ep_peer_connect; ranks of one process on one device use the pointers directly).  A step on
+ * `stream` (moe_ep_forward on a peer handle):
+ *   moe_ep_dispatch_plan -> each token row stored once into each owning rank's receive buffer
+ *   (NVLink peer stores between GPUs) -> release/acquire epoch flags at system scope -> moe_route_plan
+ *   over the received ids -> the single-launch GEMM whose epilogue stores every result row straight
+ *   into its token owner's output (moe_gemm_rowptr: the combine overlaps the GEMM tile by tile) ->
+ *   epoch flags -> a copy of the computed rows into out_dev (skipped when out_dev is the handle's own
+ *   output, moe_ep_peer_output: zero copy; its rows stay valid until the next step).
+ * Every call is stream-ordered and host-synchronisation-free (CUDA-graph capturable).  All ranks run
+ * the same number of steps with the same k, H, N, dtypes; T <= max_tokens per rank and step.
+ * A rank whose peer never signals does not hang: its waits give up after the timeout (default 60 s,
+ * moe_ep_peer_set_timeout) and moe_ep_peer_status reports 2.  P:94-98 (EP background), DESIGN.md §9.
+ * ------------------------------------------------------------------------------------------ */
+#define MOE_EP_PEER_BLOB_BYTES 256
+
+/* Collective-free local part of the setup.  E % world == 0 (world <= 64); bm / bn: the local GEMM's
+ * tile shape (0: the planner's choice for max_tokens * k expected rows); max_x_row_bytes /
+ * max_y_row_bytes: capacities of a token row (H * 2 bf16, H E4M3) and a result row (N * 2 bf16,
+ * N * 4 fp32), multiples of 16.  Writes this rank's blob (MOE_EP_PEER_BLOB_BYTES, host) to blob_out.
+ * The region (world * max_tokens * (max_x_row_bytes + 4 k + 4) + max_tokens * k * max_y_row_bytes bytes)
+ * is initialised before the call returns.  The calling thread's current device is used. */
+moe_status moe_ep_peer_create(int32_t rank, int32_t world, int32_t E, int32_t bm, int32_t bn, int64_t max_tokens,
+                              int32_t k, int64_t max_x_row_bytes, int64_t max_y_row_bytes, moe_ep** out,
+                              void* blob_out);
+
+/* blobs: world * MOE_EP_PEER_BLOB_BYTES bytes (host), rank order (the all-gather of every rank's blob).
+ * Maps the peers' regions (cudaIpcOpenMemHandle, peer access enabled lazily).  MOE_ERR_INVALID when a
+ * blob does not belong to this group. */
+moe_status moe_ep_peer_connect(moe_ep* ep, const void* blobs);
+
+/* The handle's output rows (device; row t * k + j of the step's result row bytes) and their capacity. */
+moe_status moe_ep_peer_output(const moe_ep* ep, void** out_dev, int64_t* bytes);
+
+/* Timeout of the device-side waits, in ns (default 60 s). */
+moe_status moe_ep_peer_set_timeout(moe_ep* ep, int64_t timeout_ns);
+
+/* Synchronises the last step's stream; *status = 0, or 2 if a wait timed out (results invalid). */
+moe_status moe_ep_peer_status(moe_ep* ep, int32_t* status);
 
 #ifdef __cplusplus
 }

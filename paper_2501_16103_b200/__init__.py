@@ -24,7 +24,7 @@ MOE_EP_UNFUSED = 1
 MOE_PAD_MAX, MOE_PAD_REPEAT, MOE_SPLIT_TAIL = 0, 1, 2
 MOE_ORDER_ALTERNATING, MOE_ORDER_HALF_INTERVAL = 4, 8
 MOE_GRID_BALANCED, MOE_GRID_STATIC, MOE_A_GATHER4, MOE_EPI_REGISTER, MOE_SCHED_DYNAMIC = 16, 32, 64, 128, 256
-MOE_NO_L2_PREFETCH = 512
+MOE_L2_PREFETCH = 512
 MOE_ROUTE_NO_SMALL, MOE_ROUTE_THREE_KERNELS = 1, 2
 MOE_KIND_WIDE, MOE_KIND_SWAP, MOE_MAX_RULES = 0, 1, 2
 MOE_DEFAULT_SWAP_MAX = 64                       # include/moe_sm100.h: the built-in catalog {SWAP, 64}
@@ -56,7 +56,8 @@ EXPORTED = (
     "moe_ep_unique_id", "moe_ep_create", "moe_ep_forward", "moe_ep_last_rows", "moe_ep_last_gemm_ms",
     "moe_ep_destroy", "moe_ep_create_loopback", "moe_ep_combine_ptr", "moe_gemm_rowptr",
     "moe_route_ex", "moe_plan_suggest_tile", "moe_plan_create_expected", "moe_plan_build_catalog",
-    "moe_plan_create_catalog",
+    "moe_plan_create_catalog", "moe_ep_peer_create", "moe_ep_peer_connect", "moe_ep_peer_output",
+    "moe_ep_peer_set_timeout", "moe_ep_peer_status",
 )
 
 
@@ -143,6 +144,13 @@ def lib() -> ctypes.CDLL:
         "moe_gemm_rowptr": (ctypes.c_int32, [vp, vp, ctypes.c_int64, vp, vp, ctypes.c_int32, vp, vp, ctypes.c_int32,
                                              vp]),
         "moe_ep_destroy": (None, [vp]),
+        "moe_ep_peer_create": (ctypes.c_int32, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                                ctypes.c_int32, ctypes.c_int64, ctypes.c_int32, ctypes.c_int64,
+                                                ctypes.c_int64, ctypes.POINTER(vp), vp]),
+        "moe_ep_peer_connect": (ctypes.c_int32, [vp, vp]),
+        "moe_ep_peer_output": (ctypes.c_int32, [vp, ctypes.POINTER(vp), c_i64p]),
+        "moe_ep_peer_set_timeout": (ctypes.c_int32, [vp, ctypes.c_int64]),
+        "moe_ep_peer_status": (ctypes.c_int32, [vp, c_i32p]),
         "moe_combine": (ctypes.c_int32, [vp, ctypes.c_int32, ctypes.c_int64, ctypes.c_int32, ctypes.c_int64, vp, vp,
                                          vp, ctypes.c_int32, vp, vp, ctypes.c_int32, vp]),
     }
@@ -663,3 +671,88 @@ class NativeExpertParallel:
         if h and _lib is not None:
             _lib.moe_ep_destroy(h)
             self._h = None
+
+
+MOE_EP_PEER_BLOB_BYTES = 256
+
+
+class PeerExpertParallel(NativeExpertParallel):
+    """One rank of the library's expert-parallel step over symmetric peer memory (moe_ep_peer_create /
+    moe_ep_peer_connect / moe_ep_forward; include/moe_sm100_ep.h): dispatch rows are stored straight into
+    the owners' receive buffers and the GEMM epilogue stores result rows straight into the token owners'
+    outputs (CUDA IPC mappings; NVLink stores between GPUs), ordered by device-side epoch flags.
+    allgather(blob: bytes) -> list[bytes] in rank order is the caller's plumbing (e.g. torch.distributed
+    all_gather_object); construct with connect=False and call connect(blobs) to drive several handles of
+    one process (virtual ranks, see `group`)."""
+
+    def __init__(self, rank: int, world: int, E: int, W_local, max_tokens: int, k: int, allgather=None,
+                 w_scale=None, bm: int = 0, bn: int = 0, max_out_bytes: int | None = None, connect: bool = True):
+        import torch
+
+        super().__init__(b"", rank, world, E, W_local, w_scale=w_scale, handle=ctypes.c_void_p(0))
+        H, N = W_local.shape[1], W_local.shape[2]
+        x_row = H * (1 if self.fp8 else 2)
+        y_row = max_out_bytes if max_out_bytes is not None else N * 4
+        self.max_tokens, self.k = max_tokens, k
+        self._h = ctypes.c_void_p()
+        blob = ctypes.create_string_buffer(MOE_EP_PEER_BLOB_BYTES)
+        _check(lib().moe_ep_peer_create(rank, world, E, bm, bn, max_tokens, k, x_row, y_row, ctypes.byref(self._h),
+                                        blob))
+        self.blob = blob.raw
+        self._torch = torch
+        if connect:
+            assert allgather is not None, "allgather(blob) -> [blob of rank 0, ..., rank world-1] is needed"
+            self.connect(allgather(self.blob))
+
+    def connect(self, blobs):
+        assert len(blobs) == self.world and all(len(b) == MOE_EP_PEER_BLOB_BYTES for b in blobs)
+        _check(lib().moe_ep_peer_connect(self._h, ctypes.create_string_buffer(b"".join(blobs), len(blobs) *
+                                                                                MOE_EP_PEER_BLOB_BYTES)))
+
+    @staticmethod
+    def group(world: int, E: int, W_locals, max_tokens: int, k: int, w_scales=None, bm: int = 0, bn: int = 0,
+              max_out_bytes: int | None = None):
+        """`world` virtual ranks of this process on the current device (one host thread can drive them
+        all: a step never blocks the host)."""
+        eps = [PeerExpertParallel(r, world, E, W_locals[r], max_tokens, k, w_scale=None if w_scales is None
+                                  else w_scales[r], bm=bm, bn=bn, max_out_bytes=max_out_bytes, connect=False)
+               for r in range(world)]
+        blobs = [e.blob for e in eps]
+        for e in eps:
+            e.connect(blobs)
+        return eps
+
+    def output(self, T: int, N: int, dtype=None):
+        """The handle's own output rows as a [T * k, N] tensor view (zero copy: pass it as `out`)."""
+        torch = self._torch
+        dtype = dtype or torch.bfloat16
+        ptr, nbytes = ctypes.c_void_p(), ctypes.c_int64()
+        _check(lib().moe_ep_peer_output(self._h, ctypes.byref(ptr), ctypes.byref(nbytes)))
+        esz = torch.empty((), dtype=dtype).element_size()
+        assert T * self.k * N * esz <= nbytes.value
+        return _device_view(ptr.value, (T * self.k, N), dtype, torch.cuda.current_device())
+
+    def set_timeout(self, seconds: float):
+        _check(lib().moe_ep_peer_set_timeout(self._h, int(seconds * 1e9)))
+
+    def status(self) -> int:
+        """0, or 2 if a device-side wait of the last step timed out (synchronises)."""
+        st = ctypes.c_int32()
+        _check(lib().moe_ep_peer_status(self._h, ctypes.byref(st)))
+        return int(st.value)
+
+
+def _device_view(ptr: int, shape, dtype, device: int):
+    """A torch tensor over library-owned device memory (no copy; the library keeps ownership)."""
+    import torch
+
+    class _Cai:
+        pass
+
+    typestr = {torch.bfloat16: "<i2", torch.float32: "<f4"}[dtype]
+    c = _Cai()
+    c.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (ptr, False), "version": 3,
+                                  "strides": None}
+    t = torch.as_tensor(c, device=torch.device("cuda", device))
+    return t.view(dtype) if dtype == torch.bfloat16 else t
+

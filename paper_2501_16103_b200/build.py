@@ -20,8 +20,8 @@ NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_SOURCES = ["moe_gemm.cu", "route.cu", "plan_device.cu", "ep.cu", "ffn.cu"]
-CPP_SOURCES = ["plan.cpp", "ep_nccl.cpp"]
-HEADERS = ["common.h", "sm100_ptx.cuh", "plan_body.cuh"]
+CPP_SOURCES = ["plan.cpp", "ep_nccl.cpp", "ep_peer.cpp"]
+HEADERS = ["common.h", "sm100_ptx.cuh", "plan_body.cuh", "ep_internal.h"]
 
 
 def _newer(target: str, deps: list[str]) -> bool:

@@ -14,6 +14,7 @@
 #include <climits>
 
 #include "common.h"
+#include "ep_internal.h"
 
 namespace {
 
@@ -181,12 +182,175 @@ __global__ void ep_unpack_kernel(const uint4* __restrict__ rows, const int32_t* 
   }
 }
 
+
+// ---------------------------------------------------------------------------------------------
+// Peer-memory transport (ep_peer.cpp): every rank's symmetric buffers are mapped in
+// every process (CUDA IPC), so dispatch rows are stored straight into the owners' receive buffers
+// (NVLink peer stores between GPUs), the GEMM epilogue stores result rows straight into the token
+// owners' output buffers, and ranks order those stores with epoch flags (release / acquire at
+// system scope) instead of host synchronisation.
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Send row i (destination d = segment of i in send_off) -> row rank * T_max + (i - send_off[d]) of d's
+// receive buffers: the token row (one warp, 16-byte vectors, four loads in flight per lane), its k
+// destination-local ids and its source-local token index.  Block 0 also stores the row count per
+// destination into the destination's count word for this source.
+__global__ void __launch_bounds__(256)
+    ep_peer_dispatch_kernel(const uint4* __restrict__ X, int row_vec, const int32_t* __restrict__ send_off,
+                            const int32_t* __restrict__ send_tok, const int32_t* __restrict__ send_meta, int G, int k,
+                            int rank, long long T_max, const moe::PeerPtrs* __restrict__ peers) {
+  if (blockIdx.x == 0)
+    for (int d = threadIdx.x; d < G; d += blockDim.x)
+      reinterpret_cast<int32_t*>(peers[d].flags)[moe::kCountWord + rank] = send_off[d + 1] - send_off[d];
+  const int S = send_off[G];
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < S; i += warps) {
+    const int d = segment_of(send_off, G, i);
+    const long long row = rank * T_max + (i - send_off[d]);
+    const moe::PeerPtrs p = peers[d];
+    const int t = send_tok[i];
+    const uint4* src = X + (long long)t * row_vec;
+    uint4* dst = reinterpret_cast<uint4*>(p.x) + row * row_vec;
+    int c = lane;
+    for (; c + 96 < row_vec; c += 128) {
+      const uint4 v0 = src[c], v1 = src[c + 32], v2 = src[c + 64], v3 = src[c + 96];
+      dst[c] = v0;
+      dst[c + 32] = v1;
+      dst[c + 64] = v2;
+      dst[c + 96] = v3;
+    }
+    for (; c < row_vec; c += 32) dst[c] = src[c];
+    if (lane < k) reinterpret_cast<int32_t*>(p.meta)[row * k + lane] = send_meta[(long long)i * k + lane];
+    if (lane == 0) reinterpret_cast<int32_t*>(p.tok)[row] = t;
+  }
+}
+
+// Epoch signal to every rank d: flags_d[word0 + rank] = epoch (bump: this step's new epoch).  The
+// stores of the kernels before it on the stream happen-before this kernel; the system-scope fence
+// and release make them visible to d before d observes the flag.
+__global__ void ep_peer_signal_kernel(const moe::PeerPtrs* __restrict__ peers, int G, int rank, int word0,
+                                      uint32_t* epoch, int bump) {
+  __shared__ uint32_t e;
+  if (threadIdx.x == 0) {
+    uint32_t v = *epoch;
+    if (bump) *epoch = ++v;
+    e = v;
+  }
+  __syncthreads();
+  __threadfence_system();
+  for (int d = threadIdx.x; d < G; d += blockDim.x)
+    st_release_sys(reinterpret_cast<uint32_t*>(peers[d].flags) + word0 + rank, e);
+}
+
+// Wait until every source s has signalled this step's epoch on flags[word0 + s] (acquire, system
+// scope; wrap-safe comparison).  A peer that never signals cannot hang the stream: after timeout_ns
+// the wait gives up and sets *status = 2 (moe_ep_peer_status reports it).
+__global__ void ep_peer_wait_kernel(const uint32_t* flags, int G, int word0, const uint32_t* epoch, int32_t* status,
+                                    long long timeout_ns) {
+  const uint32_t e = *epoch;
+  for (int s = threadIdx.x; s < G; s += blockDim.x) {
+    const unsigned long long t0 = globaltimer_ns();
+    while ((int32_t)(ld_acquire_sys(flags + word0 + s) - e) < 0) {
+      if ((long long)(globaltimer_ns() - t0) > timeout_ns) {
+        atomicExch(status, 2);
+        break;
+      }
+      __nanosleep(256);
+    }
+  }
+}
+
+// Local CSR row i (received row r = tok_l[i], slot j = slot_l[i]) -> the address of row
+// (t * k + j) in source s's output buffer, s = r / T_max, t = the source's token index of r.
+__global__ void ep_peer_combine_ptr_kernel(const int32_t* __restrict__ row_off_l, int El,
+                                           const int32_t* __restrict__ tok_l, const int32_t* __restrict__ slot_l,
+                                           const int32_t* __restrict__ recv_tok, long long T_max, int k,
+                                           const moe::PeerPtrs* __restrict__ peers, long long y_row, long long n_cap,
+                                           unsigned long long* __restrict__ row_ptr) {
+  const long long n = min((long long)row_off_l[El], n_cap);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int r = tok_l[i];
+    const int s = (int)(r / T_max);
+    const long long t = recv_tok[r];
+    row_ptr[i] = peers[s].out + (unsigned long long)((t * k + slot_l[i]) * y_row);
+  }
+}
+
+// out[t k + j] = src[t k + j] for every slot the step computed (valid id, first occurrence in the row):
+// the rows of masked slots are left as the caller had them (moe_ep_forward's contract).
+__global__ void ep_peer_copy_out_kernel(const uint4* __restrict__ src, const int32_t* __restrict__ topk, int n, int k,
+                                        int row_vec, uint4* __restrict__ out) {
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += warps) {
+    const int32_t* row = topk + (long long)(i / k) * k;
+    const int j = i % k;
+    if (row[j] < 0 || !first_slot(row, j)) continue;
+    const uint4* s = src + (long long)i * row_vec;
+    uint4* o = out + (long long)i * row_vec;
+    for (int c = threadIdx.x & 31; c < row_vec; c += 32) o[c] = s[c];
+  }
+}
+
 int grid_for(int64_t warps_needed) {
   const int64_t b = (warps_needed + 7) / 8;
   return (int)(b < 1 ? 1 : (b > 4 * 148 ? 4 * 148 : b));
 }
 
 }  // namespace
+
+namespace moe {
+
+cudaError_t ep_peer_dispatch(const void* X, int64_t x_row, const int32_t* send_off, const int32_t* send_tok,
+                             const int32_t* send_meta, int G, int k, int rank, int64_t T_max, const PeerPtrs* peers,
+                             cudaStream_t s) {
+  ep_peer_dispatch_kernel<<<2 * 148, 256, 0, s>>>((const uint4*)X, (int)(x_row / 16), send_off, send_tok, send_meta,
+                                                   G, k, rank, T_max, peers);
+  return cudaGetLastError();
+}
+
+cudaError_t ep_peer_signal(const PeerPtrs* peers, int G, int rank, int word0, uint32_t* epoch, bool bump,
+                           cudaStream_t s) {
+  ep_peer_signal_kernel<<<1, 64, 0, s>>>(peers, G, rank, word0, epoch, bump ? 1 : 0);
+  return cudaGetLastError();
+}
+
+cudaError_t ep_peer_wait(const uint32_t* flags, int G, int word0, const uint32_t* epoch, int32_t* status,
+                         long long timeout_ns, cudaStream_t s) {
+  ep_peer_wait_kernel<<<1, 64, 0, s>>>(flags, G, word0, epoch, status, timeout_ns);
+  return cudaGetLastError();
+}
+
+cudaError_t ep_peer_combine_ptr(const int32_t* row_off_l, int El, const int32_t* tok_l, const int32_t* slot_l,
+                                const int32_t* recv_tok, int64_t T_max, int k, const PeerPtrs* peers, int64_t y_row,
+                                int64_t n_cap, unsigned long long* row_ptr, cudaStream_t s) {
+  ep_peer_combine_ptr_kernel<<<2 * 148, 256, 0, s>>>(row_off_l, El, tok_l, slot_l, recv_tok, T_max, k, peers, y_row,
+                                                      n_cap, row_ptr);
+  return cudaGetLastError();
+}
+
+cudaError_t ep_peer_copy_out(const void* src, const int32_t* topk, int64_t T, int k, int64_t y_row, void* out,
+                             cudaStream_t s) {
+  if (T * k == 0) return cudaSuccess;
+  ep_peer_copy_out_kernel<<<grid_for(T * k), 256, 0, s>>>((const uint4*)src, topk, (int)(T * k), k, (int)(y_row / 16),
+                                                          (uint4*)out);
+  return cudaGetLastError();
+}
+
+}  // namespace moe
 
 extern "C" {
 

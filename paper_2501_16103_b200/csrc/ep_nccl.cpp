@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "common.h"
+#include "ep_internal.h"
 #include "moe_sm100_debug.h"
 #include "moe_sm100_fp8.h"
 
@@ -109,6 +110,9 @@ cudaError_t make_pool(cudaMemPool_t* pool) {
   return cudaMemPoolSetAttribute(*pool, cudaMemPoolAttrReleaseThreshold, &keep);
 }
 
+}  // namespace
+
+namespace moe {
 // Test transport (moe_ep_create_loopback): G virtual ranks of one process on one device, each
 // driven by its own host thread and stream; an exchange publishes the source buffer and its
 // per-peer row counts, every rank copies its segments from the peers' buffers (after their
@@ -141,6 +145,10 @@ struct Loopback {
     }
   }
 };
+}  // namespace moe
+
+namespace {
+using moe::Loopback;
 
 // All-to-all-v of rows: peer p gets rows [send_off[p], send_off[p] + send[p]) of `src`, this rank
 // receives recv[p] rows from p at recv_off[p] of `dst` (row_bytes each).
@@ -180,7 +188,8 @@ moe_status sync_loopback(Loopback* lb, int rank, cudaStream_t s) {
 }
 
 moe_status exchange(const void* src, const std::vector<int64_t>& send, void* dst, const std::vector<int64_t>& recv,
-                    int64_t row_bytes, ncclComm_t comm, cudaStream_t s, Loopback* lb = nullptr, int rank = 0) {
+                    int64_t row_bytes, void* comm_, cudaStream_t s, Loopback* lb = nullptr, int rank = 0) {
+  ncclComm_t comm = static_cast<ncclComm_t>(comm_);
   if (lb) return exchange_loopback(lb, rank, src, send, dst, recv, row_bytes, s);
   const NcclApi& n = nccl();
   NCCL_TRY(n.GroupStart());
@@ -205,24 +214,6 @@ moe_status exchange(const void* src, const std::vector<int64_t>& send, void* dst
 // back prefix [G] (int32), then peer row / tag buffer addresses [2][G] (uint64, 8-byte aligned).
 inline size_t host_staging_bytes(int G) { return (size_t)4 * (4 * G + 3 * (G + 1) + G + 2) + (size_t)16 * G; }
 
-struct moe_ep {
-  ncclComm_t comm = nullptr;
-  int32_t rank = 0, world = 1, E = 0, bm = 0, bn = 0;
-  moe_plan* plan = nullptr;            // local experts, device-planned each step
-  int64_t plan_H = -1, plan_N = -1;
-  int32_t* host = nullptr;             // pinned: counts [G][2] + recv [G][2] + offsets 3 (G+1)
-  int64_t sent = 0, received = 0, local_rows = 0;
-  cudaEvent_t gemm_ev[2] = {nullptr, nullptr};   // around the last step's GEMM launch
-  bool gemm_timed = false;
-  std::shared_ptr<Loopback> lb;                   // test transport instead of NCCL (moe_ep_create_loopback)
-  // Fused combine: the GEMM epilogue stores result rows into the owners' receive buffers (this
-  // rank's own with one rank; the peers' with the loopback transport).  Persistent, grow-only.
-  bool fused = false;
-  cudaMemPool_t pool = nullptr;                   // step scratch (private to this handle)
-  char* rows_buf = nullptr;
-  int32_t* meta_buf = nullptr;
-  int64_t cap_bytes = 0, cap_rows = 0;
-};
 
 extern "C" {
 
@@ -256,14 +247,16 @@ moe_status moe_ep_create(const void* unique_id, int32_t rank, int32_t world, int
   ep->fused = world == 1 && !(flags & MOE_EP_UNFUSED) && bm != 64;
   ncclUniqueId id;
   std::memcpy(&id, unique_id, sizeof(id));
-  ncclResult_t r = nccl().CommInitRank(&ep->comm, world, id, rank);
+  ncclComm_t comm = nullptr;
+  ncclResult_t r = nccl().CommInitRank(&comm, world, id, rank);
+  ep->comm = comm;
   if (r != ncclSuccess) {
     delete ep;
     MOE_FAIL(MOE_ERR_NCCL, "ncclCommInitRank: %s", nccl().GetErrorString(r));
   }
   if (make_pool(&ep->pool) != cudaSuccess || cudaMallocHost((void**)&ep->host, host_staging_bytes(world)) != cudaSuccess ||
       cudaEventCreate(&ep->gemm_ev[0]) != cudaSuccess || cudaEventCreate(&ep->gemm_ev[1]) != cudaSuccess) {
-    nccl().CommDestroy(ep->comm);
+    nccl().CommDestroy(static_cast<ncclComm_t>(ep->comm));
     if (ep->pool) cudaMemPoolDestroy(ep->pool);
     delete ep;
     MOE_FAIL(MOE_ERR_CUDA, "moe_ep_create: memory pool / pinned staging");
@@ -282,6 +275,8 @@ moe_status moe_ep_forward(moe_ep* ep, const int32_t* topk, int64_t T, int32_t k,
   if (out_dtype != MOE_DTYPE_BF16 && out_dtype != MOE_DTYPE_F32)
     MOE_FAIL(MOE_ERR_INVALID, "moe_ep_forward: out_dtype %d", out_dtype);
   if (T < 0 || k < 1 || k > 32 || H < 1 || N < 1) MOE_FAIL(MOE_ERR_INVALID, "moe_ep_forward: T, k, H or N out of range");
+  if (ep->peer) return moe::ep_peer_forward(ep, topk, T, k, X, H, x_dtype, W, N, w_scale, out, out_dtype,
+                                            (cudaStream_t)stream);
   const int G = ep->world, El = ep->E / G;
   const int64_t x_row = H * (x_dtype == MOE_DTYPE_E4M3 ? 1 : 2);
   const int64_t y_row = N * (out_dtype == MOE_DTYPE_F32 ? 4 : 2);
@@ -474,6 +469,7 @@ moe_status moe_ep_create_loopback(int32_t world, int32_t E, int32_t bm, int32_t 
 moe_status moe_ep_last_rows(const moe_ep* ep, int64_t* sent, int64_t* received, int64_t* local_rows) {
   moe::clear_error();
   if (!ep) MOE_FAIL(MOE_ERR_INVALID, "moe_ep_last_rows: null handle");
+  if (ep->peer) return moe::ep_peer_last_rows(ep, sent, received, local_rows);
   if (sent) *sent = ep->sent;
   if (received) *received = ep->received;
   if (local_rows) *local_rows = ep->local_rows;
@@ -492,12 +488,13 @@ moe_status moe_ep_last_gemm_ms(const moe_ep* ep, float* ms) {
 
 void moe_ep_destroy(moe_ep* ep) {
   if (!ep) return;
+  if (ep->peer) moe::ep_peer_release(ep);
   for (cudaEvent_t e : ep->gemm_ev)
     if (e) cudaEventDestroy(e);
   if (ep->rows_buf) cudaFree(ep->rows_buf);
   if (ep->meta_buf) cudaFree(ep->meta_buf);
   if (ep->plan) moe_plan_destroy(ep->plan);
-  if (ep->comm) nccl().CommDestroy(ep->comm);
+  if (ep->comm) nccl().CommDestroy(static_cast<ncclComm_t>(ep->comm));
   if (ep->host) cudaFreeHost(ep->host);
   if (ep->pool) {
     cudaDeviceSynchronize();                       // frees enqueued on the step streams have run

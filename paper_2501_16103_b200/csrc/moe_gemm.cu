@@ -1700,7 +1700,7 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
                        (!(v.flags & (MOE_GRID_STATIC | MOE_GRID_BALANCED)) && v.bm == 256);
   a.sched = dynamic ? moe::plan_sched_dev(plan) : nullptr;
   a.W = reinterpret_cast<const uint8_t*>(W);
-  a.pf_dist = (v.flags & MOE_NO_L2_PREFETCH) || !(v.N % 64 == 0) ? 0 : kL2Pf;
+  a.pf_dist = (v.flags & MOE_L2_PREFETCH) && v.N % 64 == 0 ? kL2Pf : 0;
   a.balance = a.sched ? 0 : (v.flags & MOE_GRID_BALANCED) ? 1 : (v.flags & MOE_GRID_STATIC) ? 0 : v.bm == 128;
   a.tma_store = tma_store ? 1 : 0;
   a.T = (int32_t)T;
