@@ -38,7 +38,7 @@ import synth  # noqa: E402
 
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 METRIC = "MoE GEMM TFLOPS and % of B200 BF16 tensor peak at 1/2/4/8 GPUs"
-ORDER_FLAGS = {"natural": 0, "alternating": 4, "half_interval": 8}   # MOE_ORDER_* (include/moe_sm100.h)
+ORDER_FLAGS = {"natural": 0, "alternating": 4, "half_interval": 8, "light_last": 4096}   # MOE_ORDER_* (include/moe_sm100.h)
 
 
 def load_peaks():

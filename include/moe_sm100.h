@@ -51,6 +51,12 @@ typedef int32_t moe_status;
                                         the busiest half with the rest: b1, s1, b2, s2, ...          */
 #define MOE_ORDER_HALF_INTERVAL  8u  /* same sort; the i-th busiest task takes the i-th slot of the
                                         bit-reversal (van der Corput) sequence over the slots        */
+#define MOE_ORDER_LIGHT_LAST  4096u  /* tasks of > MOE_LIGHT_ROWS rows first, then the light ones (each group
+                                        in expert order); with the dynamic tile order (CTA-pair tiles)
+                                        the kernel then interleaves the light tiles among the others in
+                                        proportion, so memory-bound tiles overlap compute-bound ones
+                                        instead of streaming W all at once           */
+#define MOE_LIGHT_ROWS 64
 
 /* Launch options carried by the plan (moe_gemm reads them from the plan it is given; they never
  * change Y).  Defaults are the measured-fastest choices; these exist for
@@ -71,6 +77,10 @@ typedef int32_t moe_status;
                                    tiles (bm = 256) unless MOE_GRID_STATIC / MOE_GRID_BALANCED is set;
                                    launches on one plan must be stream-ordered (the counter is reset
                                    by the launch's last CTA pair)                                     */
+
+#define MOE_NO_STREAM_K  1024u /* one-CTA tiles: never split a tile's K blocks across CTAs (stream-K, used by
+                                   default when every task has <= 32 rows and whole tiles would leave SMs
+                                   idle: the decode regime)                            */
 
 /* Output element types of moe_gemm. */
 #define MOE_DTYPE_BF16 0

@@ -95,6 +95,9 @@ def make_tasks(counts, bm: int, bn: int, split_tail: bool = False, catalog=()) -
             for e, m in enumerate(counts)]
 
 
+LIGHT_ROWS = 64   # a task of at most this many rows streams its W block (memory-bound)
+
+
 def order_tasks(loads: list[int], strategy: str) -> list[int]:
     """§4.2 expert ordering over the NON-EMPTY tasks, as SPEC formalises it
     (S:341-346): sort by load descending, ties by lower id; 'alternating' interleaves the
@@ -103,6 +106,11 @@ def order_tasks(loads: list[int], strategy: str) -> list[int]:
     ids = [j for j in range(len(loads)) if loads[j] > 0]
     if strategy == "natural":
         return ids
+    if strategy == "light_last":
+        # DESIGN.md R7 / §6.7: the memory-bound ("light", <= LIGHT_ROWS rows) tasks after every other
+        # non-empty task, each group in natural order, so a scheduler can interleave the two groups'
+        # tiles in proportion (P:317-320's aim: a wave mixes busy and non-busy experts).
+        return [j for j in ids if loads[j] > LIGHT_ROWS] + [j for j in ids if loads[j] <= LIGHT_ROWS]
     desc = sorted(ids, key=lambda j: (-loads[j], j))
     n = len(desc)
     if strategy == "alternating":

@@ -22,9 +22,11 @@ MOE_ERR = {-1: "INVALID", -2: "UNSUPPORTED", -3: "CAPACITY", -4: "CUDA", -5: "NC
 MOE_DTYPE_BF16, MOE_DTYPE_F32, MOE_DTYPE_E4M3 = 0, 1, 2
 MOE_EP_UNFUSED = 1
 MOE_PAD_MAX, MOE_PAD_REPEAT, MOE_SPLIT_TAIL = 0, 1, 2
-MOE_ORDER_ALTERNATING, MOE_ORDER_HALF_INTERVAL = 4, 8
+MOE_ORDER_ALTERNATING, MOE_ORDER_HALF_INTERVAL, MOE_ORDER_LIGHT_LAST = 4, 8, 4096
+MOE_LIGHT_ROWS = 64
 MOE_GRID_BALANCED, MOE_GRID_STATIC, MOE_A_GATHER4, MOE_EPI_REGISTER, MOE_SCHED_DYNAMIC = 16, 32, 64, 128, 256
 MOE_L2_PREFETCH = 512
+MOE_NO_STREAM_K = 1024
 MOE_ROUTE_NO_SMALL, MOE_ROUTE_THREE_KERNELS = 1, 2
 MOE_KIND_WIDE, MOE_KIND_SWAP, MOE_MAX_RULES = 0, 1, 2
 MOE_DEFAULT_SWAP_MAX = 64                       # include/moe_sm100.h: the built-in catalog {SWAP, 64}

@@ -43,6 +43,7 @@ const int32_t* plan_blob_dev(const moe_plan* p);
 bool plan_device_mode(const moe_plan* p);
 bool plan_has_swap(const moe_plan* p);
 int32_t* plan_sched_dev(const moe_plan* p);
+float* plan_sk_ws(const moe_plan* p, int32_t** cnt, int32_t* ctas);
 void plan_shape(const moe_plan* p, int32_t* E, int32_t* H, int32_t* N, int32_t* bm, int32_t* bn, uint32_t* flags);
 }  // namespace moe
 
@@ -115,6 +116,10 @@ struct GemmArgs {
   const uint8_t* W;          // W base (bytes), for the load/store-path L2 prefetch of memory-bound tiles
   int32_t pf_dist;           // that prefetch's distance in K blocks (0: off); one-CTA tiles: every tile,
                              // CTA pairs: swap-AB tiles only
+  float* sk_ws;              // nullable: stream-K partial accumulators (one-CTA tiles)
+  int32_t* sk_cnt;           //           and per-tile arrival counters (zero between launches)
+  int32_t light_merge;       // MOE_ORDER_LIGHT_LAST plan under the dynamic tile order: interleave the light
+                             // (memory-bound) tail of the virtual tiles among the others in proportion
 };
 
 // Per-CTA counters written by the instrumented build (kProf = true).
@@ -157,6 +162,15 @@ __device__ __forceinline__ void map_tile(const int32_t* prefix, const int32_t* s
   h = hh;
   l = v - base;                                            // l <- B - k
   task = sigma[hh];                                        // h~ <- sigma(h)
+}
+
+// Stream-K (one-CTA memory-bound tiles): the K blocks of all tiles in virtual-tile order
+// form one sequence of KT = total * num_kb blocks; CTA c of G owns [sk_bound(c), sk_bound(c + 1)), i.e.
+// every CTA streams the same number of W blocks whatever the tile count.  A tile split between CTAs is
+// summed by the last of them to finish, in K order (deterministic).
+__device__ __forceinline__ long long sk_bound(long long c, long long KT, int G) { return c * KT / G; }
+__device__ __forceinline__ int sk_cta_of(long long p, long long KT, int G) {   // the CTA owning K block p
+  return (int)(((p + 1) * G + KT - 1) / KT - 1);
 }
 
 struct Tile {
@@ -406,7 +420,31 @@ __global__ void __launch_bounds__(kThreads, 1)
   // TilePrefix and sigma are adjacent in the blob: one copy into shared memory.
   for (int i = threadIdx.x; i < 2 * a.M_pad; i += blockDim.x) s_prefix[i] = a.plan[MOE_PLAN_HEADER + i];
   if (total < 0) total = __ldg(a.plan + 2);
-  if (a.balance && total > 0) {
+  // Stream-K for one-CTA tiles when whole tiles would leave SMs idle (the balanced grid uses fewer CTAs
+  // than launched) and every task is short enough for the partial-accumulator slots (decode batches).
+  bool sk = false;
+  long long sk_kt = 0;
+  if constexpr (kCta == 1 && !kWide && !kSplit && !kGated) {
+    __shared__ int s_sk_rows;
+    if (a.sk_ws != nullptr && total > 0 && total <= moe::kSKMaxTiles) {
+      const int grid = (int)gridDim.x;
+      const int per = (total + grid - 1) / grid, used = (total + per - 1) / per;
+      const long long kt = (long long)total * a.num_kb;
+      if (used < grid && kt >= grid) {
+        if (threadIdx.x == 0) s_sk_rows = 0;
+        __syncthreads();
+        const int n_tasks = __ldg(a.plan + 9);
+        int mx = 0;
+        for (int i = threadIdx.x; i < n_tasks; i += blockDim.x)
+          mx = max(mx, __ldg(a.plan + a.off_params + i * MOE_PLAN_TASK_WORDS + 2));
+        atomicMax(&s_sk_rows, mx);
+        __syncthreads();
+        sk = s_sk_rows <= moe::kSKRows;
+        sk_kt = kt;
+      }
+    }
+  }
+  if (!sk && a.balance && total > 0) {
     // Balanced grid: with W = ceil(total / grid) tiles for the busiest CTA (pair) anyway, spread the
     // tiles over ceil(total / W) CTAs so every active one takes W or W - 1 and no short last wave
     // runs on a few SMs — for HBM-bound (decode) tiles the kernel's streaming rate then stays the
@@ -448,6 +486,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_arrive_cluster(leader(qempty_bar(sl)));
     return v;
   };
+  // The i-th unit of work of this CTA (pair): a virtual tile v and its K blocks [k0, k1) — the whole tile,
+  // or under stream-K the tile's part inside this CTA's share of the K-block sequence.  Every role warp
+  // walks the same units (its own cursor).
+  const long long sk_beg = sk ? sk_bound(blockIdx.x, sk_kt, gridDim.x) : 0;
+  const long long sk_end = sk ? sk_bound(blockIdx.x + 1, sk_kt, gridDim.x) : 0;
+  long long sk_pos = sk_beg;
+  auto next_unit = [&](uint32_t i, int& v, int& k0, int& k1) -> bool {
+    if (sk) {
+      if (sk_pos >= sk_end) return false;
+      v = (int)(sk_pos / a.num_kb);
+      k0 = (int)(sk_pos - (long long)v * a.num_kb);
+      k1 = (int)min((long long)a.num_kb, k0 + (sk_end - sk_pos));
+      sk_pos += k1 - k0;
+      return true;
+    }
+    v = tile_of(i);
+    k0 = 0;
+    k1 = a.num_kb;
+    return v < total;
+  };
 
   if (warp < kAWarps) {
     // ===================== A producers: this CTA's 128 token rows, 64 columns per stage =====================
@@ -466,8 +524,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int rsub = threadIdx.x >> 3;              // cp.async: row within a 16-row group
     const uint32_t dst_off = rsub * 128 + ((ch ^ (rsub & 7)) << 4);
     for (uint32_t qi = 0;; ++qi) {
-      const int v = tile_of(qi);
-      if (v >= total) break;
+      int v, k0, k1;
+      if (!next_unit(qi, v, k0, k1)) break;
       int h, task, l;
       map_tile(s_prefix, s_sigma, a.M_pad, v, h, task, l);
       const Tile t = load_tile<kSplit>(params, task, l);
@@ -482,7 +540,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // Contiguous rows (X row = CSR row): one 128-row tile TMA per stage, issued by one thread.
         // Rows past the task's end are the next task's (never stored); past X they are zero-filled.
         if (p == 0 && lane == 0) {
-          for (int kb = 0; kb < a.num_kb; ++kb, ++g) {
+          for (int kb = k0; kb < k1; ++kb, ++g) {
             const int s = g % kSt;
             wait_timed<kProf>(empty_bar(s), ((g / kSt) & 1u) ^ 1u, c_wait);
             if constexpr (kCta == 2) {
@@ -501,7 +559,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int r1 = __ldg(idx + rbeg + min(rr + 1, nvalid - 1));
         const int r2 = __ldg(idx + rbeg + min(rr + 2, nvalid - 1));
         const int r3 = __ldg(idx + rbeg + min(rr + 3, nvalid - 1));
-        for (int kb = 0; kb < a.num_kb; ++kb, ++g) {
+        for (int kb = k0; kb < k1; ++kb, ++g) {
           const int s = g % kSt;
           wait_timed<kProf>(empty_bar(s), ((g / kSt) & 1u) ^ 1u, c_wait);
           if (lane == 0) mbar_arrive_expect_tx(full_bar(s), kABytes / kAWarps);
@@ -531,11 +589,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int wcol0 = kCta == 1 ? t.ct * t.bn : t.ct * t.bn + (int)rank * 256;
         const int lines_row = min(wcols, a.N - wcol0) * esz / 128;   // 128-byte lines per K row (N % 64 == 0)
         const uint8_t* wexp = a.W + (int64_t)t.expert * a.H * a.N * esz + (int64_t)wcol0 * esz;
-        for (int kb = 0; kb < a.num_kb; ++kb, ++g) {
+        for (int kb = k0; kb < k1; ++kb, ++g) {
           const int s = g % kSt;
           if (lsu_pf && lines_row > 0) {
-            const int kp = kb == 0 ? 0 : kb + a.pf_dist - 1;      // tile start: the first pf_dist blocks
-            for (int k2 = kp; k2 < min(kb + a.pf_dist, a.num_kb); ++k2) {
+            const int kp = kb == k0 ? kb : kb + a.pf_dist - 1;    // unit start: the first pf_dist blocks
+            for (int k2 = kp; k2 < min(kb + a.pf_dist, k1); ++k2) {
               const int n_lines = kKB * lines_row;
               for (int i = threadIdx.x; i < n_lines; i += 32 * kAWarps) {
                 const int kr = k2 * kKB + i / lines_row;
@@ -591,11 +649,29 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint64_t pol_w = policy_evict_normal();
     uint32_t g = 0;
     long long c_wait = 0, c_t0 = kProf ? clock64() : 0, c_rel = 0;
-    int v_next = pair_id;                           // dynamic order, leader lane 0: the next tile fetched
+    int v_next = pair_id;                           // dynamic order, leader lane 0: the next position fetched
+    // MOE_ORDER_LIGHT_LAST: virtual tiles [0, C) are heavy tasks', [C, total) light tasks'.
+    // Fetch position i takes the Bresenham merge of the two runs: light iff floor((i+1) L / total) >
+    // floor(i L / total), L = total - C, so every window of consecutive fetches holds both kinds in
+    // proportion while each run keeps its own order (row tiles of a column block stay together).
+    int light0 = total;
+    if (dyn && rank == 0 && a.light_merge) {
+      const int M = __ldg(a.plan + 1);
+      int h = 0;
+      while (h < M && __ldg(params + s_sigma[h] * MOE_PLAN_TASK_WORDS + 2) > MOE_LIGHT_ROWS) ++h;
+      light0 = h == 0 ? 0 : s_prefix[h - 1];
+    }
+    auto merged = [&](int i) -> int {
+      if (i >= total || light0 >= total) return i;
+      const long long L = total - light0;
+      const int before = (int)((long long)i * L / total), upto = (int)((long long)(i + 1) * L / total);
+      return upto > before ? light0 + before : i - before;
+    };
     for (uint32_t qi = 0;; ++qi) {
-      int v;
+      int v, k0 = 0, k1 = a.num_kb;
       if (dyn && rank == 0) {                       // the producer of the pair's tile queue
-        v = __shfl_sync(0xffffffffu, v_next, 0);
+        const int pos = __shfl_sync(0xffffffffu, v_next, 0);
+        v = merged(pos);
         const int sl = (int)(qi % kQ);
         mbar_wait(qempty_bar(sl), ((qi / kQ) & 1u) ^ 1u);
         if (lane == 0) {
@@ -605,12 +681,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_arrive_release_cluster(mapa_shared(qfull_bar(sl), 1));
           }
           mbar_arrive(qfull_bar(sl));
-          // fetch the next tile now: the atomic's latency hides behind this tile's loads
-          if (v < total) v_next = n_pairs + atomicAdd(a.sched, 1);
+          // fetch the next position now: the atomic's latency hides behind this tile's loads
+          if (pos < total) v_next = n_pairs + atomicAdd(a.sched, 1);
         }
         __syncwarp();
-      } else {
-        v = tile_of(qi);
+      } else if (!next_unit(qi, v, k0, k1)) {
+        break;
       }
       if (v >= total) break;
       int h, task, l;
@@ -622,7 +698,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int nbox = (bnc + (1 << kCS) - 1) >> kCS;
       const bool one = kCta == 2 && one_box<kWide, kGated>(t.bn, t.ct, a.N, a.w4d, kSplit && t.kind == 1);
       const int n_one = t.ct * t.bn + (int)rank * 256;   // one box: this CTA's 256 columns
-      for (int kb = 0; kb < a.num_kb; ++kb, ++g) {
+      for (int kb = k0; kb < k1; ++kb, ++g) {
         const int s = g % kSt;
         wait_timed<kProf>(empty_bar(s), ((g / kSt) & 1u) ^ 1u, c_wait);
         if constexpr (kProf) {
@@ -724,8 +800,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       long long c_issue = 0, c_gap = 0, t_end = 0;
       int n_tiles = 0;
       for (uint32_t qi = 0;; ++qi) {
-        const int v = tile_of(qi);
-        if (v >= total) break;
+        int v, k0, k1;
+        if (!next_unit(qi, v, k0, k1)) break;
         ++n_tiles;
         int h, task, l;
         map_tile(s_prefix, s_sigma, a.M_pad, v, h, task, l);
@@ -859,11 +935,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           wait_timed<kProf>(tempty_bar(acc), acc_phase ^ 1u, c_tmem);     // epilogue(s) drained this accumulator
           tc_fence_after();
           const uint32_t d_tmem = tmem_base + acc * kAccCols;
-          for (int kb = 0; kb < a.num_kb; ++kb, ++g) {
+          for (int kb = k0; kb < k1; ++kb, ++g) {
             const int s = g % kSt;
             const uint32_t par = (g / kSt) & 1u;
             if constexpr (kProf) {
-              if (kb == 0 && n_tiles > 1) c_gap += clock64() - t_end;   // decode + accumulator hand-off
+              if (kb == k0 && n_tiles > 1) c_gap += clock64() - t_end;  // decode + accumulator hand-off
             }
             wait_timed<kProf>(full_bar(s), par, c_full);                   // both CTAs' bytes landed
             long long t_i = 0;
@@ -898,15 +974,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int kk = 0; kk < kBK / 16; ++kk) {
                   const uint64_t ad = smem_desc_sw128(a0 + kk * 32, 16, 1024);
                   const uint64_t bd = smem_desc_sw128(b0 + kk * kKStep, kBox, 1024);
-                  mma_issue<kFp8, kCta>(d_tmem, ad, bd, idesc, (kb | kk) != 0);
+                  mma_issue<kFp8, kCta>(d_tmem, ad, bd, idesc, kb != k0 || kk != 0);
                 }
               } else {
 #pragma unroll
                 for (int kk = 0; kk < kBK / 16; ++kk) {
                   const uint64_t ad = smem_desc_sw128(b0 + kk * 2048, kBBoxBytes, 1024);
                   const uint64_t bd = smem_desc_sw128(a0 + kk * 32, 16, 1024);
-                  if constexpr (kCta == 2) mma_bf16_pair(d_tmem, ad, bd, idesc, (kb | kk) != 0);
-                  else mma_bf16(d_tmem, ad, bd, idesc, (kb | kk) != 0);
+                  if constexpr (kCta == 2) mma_bf16_pair(d_tmem, ad, bd, idesc, kb != k0 || kk != 0);
+                  else mma_bf16(d_tmem, ad, bd, idesc, kb != k0 || kk != 0);
                 }
               }
               if constexpr (kProf) s_ts[2 * kSt + s] = clock64();
@@ -976,8 +1052,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     };
     for (uint32_t qi = 0;; ++qi) {
-      const int v = tile_of(qi);
-      if (v >= total) break;
+      int v, k0, k1;
+      const long long unit_beg = sk_pos;            // stream-K: where this unit starts in the K sequence
+      if (!next_unit(qi, v, k0, k1)) break;
       int h, task, l;
       map_tile(s_prefix, s_sigma, a.M_pad, v, h, task, l);
       const Tile t = load_tile<kSplit>(params, task, l);
@@ -1086,6 +1163,78 @@ __global__ void __launch_bounds__(kThreads, 1)
           store_chunk(a, yrow_ptr, col, col_end, r);
         }
       };
+      if (sk && !(k0 == 0 && k1 == a.num_kb)) {
+        // Stream-K part of a split tile (rows <= kSKRows: lane quarter 0 holds them).  1. the partial
+        // accumulator goes to this CTA's slot (0: the unit starts the CTA's share, 1: it ends it) and
+        // TMEM is freed; 2. the epilogue warps meet, one thread counts this CTA's arrival at the tile;
+        // 3. the last CTA to arrive sums every part in K order (CTA order) and stores Y.
+        const int slot = acc;
+        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + slot * kAccCols;
+        const int wslot = 2 * (int)blockIdx.x + (unit_beg == sk_beg ? 0 : 1);
+        const int n0 = t.ct * t.bn;
+        const int col_end = min(n0 + t.bn, a.N);
+        if (q == 0) {
+          float* wrow = a.sk_ws + ((size_t)wslot * moe::kSKRows + lane) * moe::kSKCols;
+          for (int c = 32 * cg; c < t.bn; c += 32 * kEpiGroups) {
+            uint32_t r[32];
+            tmem_ld32(taddr + c, r);
+            tmem_wait_ld();
+            if (valid) {
+#pragma unroll
+              for (int i = 0; i < 8; ++i)
+                *reinterpret_cast<uint4*>(wrow + c + 4 * i) = make_uint4(r[4 * i], r[4 * i + 1], r[4 * i + 2], r[4 * i + 3]);
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty_bar(slot));
+        __threadfence();
+        __shared__ int s_sk_last;
+        named_bar_sync(1, 32 * kEpiWarps);
+        const long long p0 = (long long)v * a.num_kb;
+        const int c_first = sk_cta_of(p0, sk_kt, gridDim.x);
+        const int c_last = sk_cta_of(p0 + a.num_kb - 1, sk_kt, gridDim.x);
+        if (ew == 0 && lane == 0) s_sk_last = atomicAdd(a.sk_cnt + v, 1) == c_last - c_first;
+        named_bar_sync(1, 32 * kEpiWarps);
+        if (s_sk_last) {
+          __threadfence();
+          if (q == 0 && valid) {
+            for (int c = 32 * cg; c < t.bn; c += 32 * kEpiGroups) {
+              uint32_t r[32];                         // the fp32 sum, as store_chunk takes it
+#pragma unroll
+              for (int i = 0; i < 32; ++i) r[i] = 0u;
+              for (int cc = c_first; cc <= c_last; ++cc) {
+                const int ws2 = 2 * cc + (sk_bound(cc, sk_kt, gridDim.x) >= p0 ? 0 : 1);
+                const float4* src =
+                    reinterpret_cast<const float4*>(a.sk_ws + ((size_t)ws2 * moe::kSKRows + lane) * moe::kSKCols + c);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                  const float4 f = __ldcg(src + i);
+                  r[4 * i] = __float_as_uint(__uint_as_float(r[4 * i]) + f.x);
+                  r[4 * i + 1] = __float_as_uint(__uint_as_float(r[4 * i + 1]) + f.y);
+                  r[4 * i + 2] = __float_as_uint(__uint_as_float(r[4 * i + 2]) + f.z);
+                  r[4 * i + 3] = __float_as_uint(__uint_as_float(r[4 * i + 3]) + f.w);
+                }
+              }
+              if constexpr (kFp8) {
+                if (a.scale) {
+                  const float sc = __ldg(a.scale + t.expert);
+#pragma unroll
+                  for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * sc);
+                }
+              }
+              store_chunk(a, yrow_ptr, n0 + c, col_end, r);
+            }
+          }
+          if (ew == 0 && lane == 0) a.sk_cnt[v] = 0;   // for the next launch on this plan
+        }
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1u;
+        }
+        continue;
+      }
       if constexpr (kGated) {
         // Block b: gate in TMEM columns [0,128), up in [128,256) of outputs n0 + 128b + [0,128).
 #pragma unroll 1
@@ -1699,9 +1848,19 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
   const bool dynamic = (v.flags & MOE_SCHED_DYNAMIC) ||
                        (!(v.flags & (MOE_GRID_STATIC | MOE_GRID_BALANCED)) && v.bm == 256);
   a.sched = dynamic ? moe::plan_sched_dev(plan) : nullptr;
+  a.light_merge = dynamic && (v.flags & MOE_ORDER_LIGHT_LAST) ? 1 : 0;
   a.W = reinterpret_cast<const uint8_t*>(W);
   a.pf_dist = (v.flags & MOE_L2_PREFETCH) && v.N % 64 == 0 ? kL2Pf : 0;
   a.balance = a.sched ? 0 : (v.flags & MOE_GRID_BALANCED) ? 1 : (v.flags & MOE_GRID_STATIC) ? 0 : v.bm == 128;
+  // Stream-K (one-CTA tiles; the kernel decides per launch from the tile count and task heights): needs
+  // the plan's workspace, static tile order and one CTA per SM.
+  a.sk_ws = nullptr;
+  a.sk_cnt = nullptr;
+  int sk_ctas = 0;
+  if (v.bm == 128 && !a.sched && !(v.flags & (MOE_NO_STREAM_K | MOE_GRID_STATIC)) && !prof) {
+    a.sk_ws = moe::plan_sk_ws(plan, &a.sk_cnt, &sk_ctas);
+    if (sk_ctas != sm_count_cached()) a.sk_ws = nullptr;   // workspace sized for another device
+  }
   a.tma_store = tma_store ? 1 : 0;
   a.T = (int32_t)T;
   a.H = v.H;
@@ -1778,7 +1937,8 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
                 : cudaLaunchKernelEx(&cfg, moe_gemm_kernel<false, 2, false>, tmX, tmW, tmW2, tmY, a);
     if (le != cudaSuccess) MOE_FAIL(MOE_ERR_CUDA, "moe_gemm pair launch: %s", cudaGetErrorString(le));
   } else {
-    const int grid = v.total < 0 ? sm_count_cached() : std::min(v.total, sm_count_cached());
+    // one CTA per SM when the kernel may choose stream-K (it spreads the K blocks over every CTA)
+    const int grid = v.total < 0 || a.sk_ws ? sm_count_cached() : std::min(v.total, sm_count_cached());
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kThreads);

@@ -111,12 +111,12 @@ moe_status moe_plan_build_catalog(const int32_t* counts, int32_t E, int64_t H, i
     MOE_FAIL(MOE_ERR_UNSUPPORTED,
              "moe_plan_build: bn=%d must be a multiple of %d in [16, 256] (or of 32 in (256, 512] with bm=256)", bn,
              bm == 256 ? 32 : 16);
-  if (flags & ~(MOE_PAD_REPEAT | MOE_SPLIT_TAIL | MOE_ORDER_ALTERNATING | MOE_ORDER_HALF_INTERVAL | MOE_GRID_BALANCED |
-                MOE_GRID_STATIC | MOE_A_GATHER4 | MOE_EPI_REGISTER | MOE_SCHED_DYNAMIC | MOE_L2_PREFETCH))
+  if (flags & ~(MOE_PAD_REPEAT | MOE_SPLIT_TAIL | MOE_ORDER_ALTERNATING | MOE_ORDER_HALF_INTERVAL | MOE_ORDER_LIGHT_LAST | MOE_GRID_BALANCED |
+                MOE_GRID_STATIC | MOE_A_GATHER4 | MOE_EPI_REGISTER | MOE_SCHED_DYNAMIC | MOE_L2_PREFETCH | MOE_NO_STREAM_K))
     MOE_FAIL(MOE_ERR_INVALID, "moe_plan_build: unknown flags 0x%x", flags);
   if ((flags & MOE_GRID_BALANCED) && (flags & MOE_GRID_STATIC))
     MOE_FAIL(MOE_ERR_INVALID, "moe_plan_build: MOE_GRID_BALANCED and MOE_GRID_STATIC are exclusive");
-  if ((flags & MOE_ORDER_ALTERNATING) && (flags & MOE_ORDER_HALF_INTERVAL))
+  if (__builtin_popcount(flags & (MOE_ORDER_ALTERNATING | MOE_ORDER_HALF_INTERVAL | MOE_ORDER_LIGHT_LAST)) > 1)
     MOE_FAIL(MOE_ERR_INVALID, "moe_plan_build: choose one expert ordering");
   const bool split = (flags & MOE_SPLIT_TAIL) != 0;
   if (split && (bm != 256 || bn < 256))
@@ -170,7 +170,10 @@ moe_status moe_plan_build_catalog(const int32_t* counts, int32_t E, int64_t H, i
   std::vector<int32_t> sigma;
   for (int32_t i = 0; i < n_tasks; ++i)
     if (nu[i] > 0) sigma.push_back(i);
-  if (flags & (MOE_ORDER_ALTERNATING | MOE_ORDER_HALF_INTERVAL)) {
+  if (flags & MOE_ORDER_LIGHT_LAST) {
+    // heavy tasks, then the light (memory-bound) ones, each group in expert order
+    std::stable_partition(sigma.begin(), sigma.end(), [&](int32_t i) { return counts[i] > MOE_LIGHT_ROWS; });
+  } else if (flags & (MOE_ORDER_ALTERNATING | MOE_ORDER_HALF_INTERVAL)) {
     // §4.2 expert ordering: busy (compute-bound) and non-busy (memory-bound)
     // experts interleaved so a wave of CTAs mixes both.  sigma stays an injection.
     std::vector<int32_t> desc = sigma;
@@ -278,6 +281,9 @@ struct moe_plan {
   std::vector<moe_tile_rule> rules;   // the catalog given at creation (n_rules < 0: built-in)
   int32_t n_rules = -1;
   bool device_mode = false;   // device blob written by moe_plan_device; host blob stale
+  float* sk_ws = nullptr;     // one-CTA plans: stream-K partial accumulators [2 * sk_ctas][kSKRows][kSKCols]
+  int32_t* sk_cnt = nullptr;  //                 per-tile arrival counters [kSKMaxTiles] (zero between launches)
+  int32_t sk_ctas = 0;
 };
 
 namespace moe {
@@ -299,6 +305,11 @@ void plan_shape(const moe_plan* p, int32_t* E, int32_t* H, int32_t* N, int32_t* 
 }
 int32_t* plan_blob_dev_mut(moe_plan* p) { return p->dev; }
 int32_t* plan_sched_dev(const moe_plan* p) { return p->dev + p->dev_words; }
+float* plan_sk_ws(const moe_plan* p, int32_t** cnt, int32_t* ctas) {
+  *cnt = p->sk_cnt;
+  *ctas = p->sk_ctas;
+  return p->sk_ws;
+}
 // The catalog (header words 12-15) holds a swap-AB rule: the launch needs the two-strategy kernel.
 bool plan_has_swap(const moe_plan* p) {
   for (int i = 0; i < MOE_MAX_RULES; ++i)
@@ -363,8 +374,31 @@ moe_status moe_plan_create_catalog(const int32_t* counts, int32_t E, int64_t H, 
     delete p;
     MOE_FAIL(MOE_ERR_CUDA, "cudaMallocAsync(plan): %s", cudaGetErrorString(err));
   }
+  if (bm == 128 && !(flags & MOE_NO_STREAM_K)) {
+    // stream-K workspace of one-CTA plans: 2 partial slots per SM, counters zeroed
+    int dev = 0, sms = 0;
+    err = cudaGetDevice(&dev);
+    if (err == cudaSuccess) err = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (err == cudaSuccess) {
+      p->sk_ctas = sms;
+      const size_t ws = sizeof(float) * 2 * (size_t)sms * moe::kSKRows * moe::kSKCols;
+      err = cudaMallocAsync((void**)&p->sk_ws, ws + sizeof(int32_t) * moe::kSKMaxTiles, p->stream);
+    }
+    if (err == cudaSuccess) {
+      p->sk_cnt = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(p->sk_ws) +
+                                             sizeof(float) * 2 * (size_t)p->sk_ctas * moe::kSKRows * moe::kSKCols);
+      err = cudaMemsetAsync(p->sk_cnt, 0, sizeof(int32_t) * moe::kSKMaxTiles, p->stream);
+    }
+    if (err != cudaSuccess) {
+      if (p->sk_ws) cudaFreeAsync(p->sk_ws, p->stream);
+      cudaFreeAsync(p->dev, p->stream);
+      delete p;
+      MOE_FAIL(MOE_ERR_CUDA, "plan stream-K workspace: %s", cudaGetErrorString(err));
+    }
+  }
   moe_status up = upload(p, p->stream);
   if (up != MOE_OK) {
+    if (p->sk_ws) cudaFreeAsync(p->sk_ws, p->stream);
     cudaFreeAsync(p->dev, p->stream);
     delete p;
     return up;
@@ -458,6 +492,7 @@ const int32_t* moe_plan_device_blob(const moe_plan* p) { return p ? p->dev : nul
 
 void moe_plan_destroy(moe_plan* p) {
   if (!p) return;
+  if (p->sk_ws) cudaFreeAsync(p->sk_ws, p->stream);
   if (p->dev) cudaFreeAsync(p->dev, p->stream);
   delete p;
 }

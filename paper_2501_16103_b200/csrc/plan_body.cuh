@@ -60,6 +60,10 @@ __device__ __forceinline__ void plan_body(long long m, int E, int H, int N, int 
   const long long rows_incl = block_scan_incl(m, s_warp, &rows_total);
   block_scan_incl(nu, s_warp, &tiles_total);                       // total tiles
   const long long ne_incl = block_scan_incl(nu > 0 ? 1 : 0, s_warp, &ne_total);
+  // MOE_ORDER_LIGHT_LAST: heavy non-empty tasks first, then the light ones (both in expert order)
+  const bool heavy = nu > 0 && m > MOE_LIGHT_ROWS;
+  long long heavy_total;
+  const long long heavy_incl = block_scan_incl(heavy ? 1 : 0, s_warp, &heavy_total);
   const int M = (int)ne_total;                                      // |eta|
   const int M_pad = E <= 32 ? 32 : (E + 31) / 32 * 32;
   const bool overflow = rows_total >= INT_MAX || tiles_total >= INT_MAX;
@@ -95,7 +99,11 @@ __device__ __forceinline__ void plan_body(long long m, int E, int H, int N, int 
   __syncthreads();
   if (t < E && nu > 0) {
     int slot = (int)(ne_incl - 1);
-    if (flags & (MOE_ORDER_ALTERNATING | MOE_ORDER_HALF_INTERVAL)) {
+    if (flags & MOE_ORDER_LIGHT_LAST) {
+      // light task: after every heavy one, at its rank among the light ones (ne_incl - heavy_incl of them
+      // up to and including t)
+      slot = heavy ? (int)(heavy_incl - 1) : (int)(heavy_total + (ne_incl - heavy_incl) - 1);
+    } else if (flags & (MOE_ORDER_ALTERNATING | MOE_ORDER_HALF_INTERVAL)) {
       int r = 0;                                     // rank in descending load order
       for (int j = 0; j < E; ++j) {
         const int mj = s_m[j];

@@ -22,7 +22,8 @@ import torch  # noqa: E402
 import paper_2501_16103_b200 as M  # noqa: E402
 import synth  # noqa: E402
 
-ORDER = {"natural": 0, "alternating": M.MOE_ORDER_ALTERNATING, "half_interval": M.MOE_ORDER_HALF_INTERVAL}
+ORDER = {"natural": 0, "alternating": M.MOE_ORDER_ALTERNATING, "half_interval": M.MOE_ORDER_HALF_INTERVAL,
+         "light_last": M.MOE_ORDER_LIGHT_LAST}
 
 
 class CleanFlush:

@@ -347,7 +347,8 @@ def test_gemm_full_size_sampled(cfg, bn, bm, flags):
 
 
 # ---------------------------------------------------------------------------- device-side planner
-ORDER_FLAG = {"natural": 0, "alternating": M.MOE_ORDER_ALTERNATING, "half_interval": M.MOE_ORDER_HALF_INTERVAL}
+ORDER_FLAG = {"natural": 0, "alternating": M.MOE_ORDER_ALTERNATING, "half_interval": M.MOE_ORDER_HALF_INTERVAL,
+              "light_last": M.MOE_ORDER_LIGHT_LAST}
 
 
 def _device_plan_blob(counts, N, bm, bn, pad, H=64, split=0, order="natural"):
@@ -364,7 +365,8 @@ def _device_plan_blob(counts, N, bm, bn, pad, H=64, split=0, order="natural"):
                                                (256, 96, 0, "natural"), (256, 256, 1, "natural"),
                                                (256, 512, 0, "natural"), (256, 512, 0, "half_interval"),
                                                (256, 512, 1, "natural"),
-                                               (128, 256, 0, "alternating"), (256, 256, 0, "half_interval")])
+                                               (128, 256, 0, "alternating"), (256, 256, 0, "half_interval"),
+                                               (256, 512, 0, "light_last"), (128, 256, 0, "light_last")])
 def test_plan_device_bit_exact(pad, bm, bn, split, order):
     rng = np.random.default_rng(bm + bn)
     cases = [np.array([11, 0, 11, 10]), np.zeros(5, dtype=np.int64), np.array([1]), np.array([256, 512, 5, 0, 300]),
@@ -432,7 +434,7 @@ def test_gemm_device_planned_wide(T, E, k, H, N, bm, bn):
     assert np.array_equal(Y.cpu().double().numpy(), ref)
 
 
-@pytest.mark.parametrize("order", ["alternating", "half_interval"])
+@pytest.mark.parametrize("order", ["alternating", "half_interval", "light_last"])
 def test_gemm_ordering_invariance(order):
     """Y is bit-identical under every §4.2 ordering (paper worst case, integer data)."""
     c = synth.CONFIGS["paper_worst"]

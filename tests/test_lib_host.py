@@ -42,7 +42,7 @@ def test_library_exports_every_declared_symbol():
     assert b"sm_100a" in L.moe_version()
 
 
-ORDER_FLAG = {"natural": 0, "alternating": 4, "half_interval": 8}
+ORDER_FLAG = {"natural": 0, "alternating": 4, "half_interval": 8, "light_last": 4096}
 
 
 def _compare(counts, N, bm, bn, pad, split=False, order="natural", catalog=None):
@@ -102,13 +102,15 @@ def test_planner_expert_ordering_matches_oracle():
         E = rng.randint(1, 300)
         counts = np.array([0 if rng.random() < 0.3 else rng.randint(1, 3000) for _ in range(E)])
         counts[rng.randrange(E)] = counts[rng.randrange(E)]          # ties
-        _compare(counts, 8 * rng.randint(1, 800), 128, 256, "max", order=rng.choice(["alternating", "half_interval"]))
+        _compare(counts, 8 * rng.randint(1, 800), 128, 256, "max",
+                 order=rng.choice(["alternating", "half_interval", "light_last"]))
     c = synth.CONFIGS["paper_worst"]
     counts = np.bincount(synth.route(c).ravel(), minlength=c.E)
-    for order in ("alternating", "half_interval"):
+    for order in ("alternating", "half_interval", "light_last"):
         _compare(counts, c.N, 256, 256, "max", order=order)
-    with pytest.raises(moe_lib.MoeError):
-        moe_lib.moe_plan_build([1, 2], 64, 128, 128, 128, 4 | 8)
+    for bad in (4 | 8, 4 | 4096, 8 | 4096):
+        with pytest.raises(moe_lib.MoeError):
+            moe_lib.moe_plan_build([1, 2], 64, 128, 128, 128, bad)
 
 
 def test_planner_split_tail_matches_oracle():

@@ -132,16 +132,23 @@ def test_expert_ordering_spec_examples():
     rng = random.Random(8)
     for _ in range(100):
         loads = [0 if rng.random() < 0.3 else rng.randint(1, 50) for _ in range(rng.randint(1, 70))]
-        for st in ("natural", "alternating", "half_interval"):
+        for st in ("natural", "alternating", "half_interval", "light_last"):
             o = moe.order_tasks(loads, st)
             assert sorted(o) == [j for j in range(len(loads)) if loads[j] > 0]     # a permutation of eta
+
+
+def test_light_last_order_by_hand():
+    """light_last: tasks of > 64 rows in expert order, then the light ones in expert order (R7)."""
+    assert moe.order_tasks([65, 64, 0, 1, 300, 2, 65], "light_last") == [0, 4, 6, 1, 3, 5]
+    assert moe.order_tasks([1, 2, 3], "light_last") == [0, 1, 2]                    # all light: natural
+    assert moe.order_tasks([100, 200], "light_last") == [0, 1]                      # none light: natural
 
 
 def test_ordering_keeps_the_tile_partition():
     """ordering changes only the tile order, never the partition (hence never Y)."""
     counts = [4096] * 7 + [4096 - 56] + [1] * 56
     row_off = np.concatenate([[0], np.cumsum(counts)])
-    for st in ("alternating", "half_interval"):
+    for st in ("alternating", "half_interval", "light_last"):
         p = moe.plan(counts, 2560, 128, 256, order=st)
         assert sorted(p["sigma"]) == list(range(64))
         cover = np.zeros((sum(counts), 2560), dtype=np.int8)
