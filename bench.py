@@ -115,13 +115,17 @@ def dist_env():
 
 def load_traffic(workload: str):
     """dram bytes per launch of moe_gemm_kernel from the committed ncu --set full summary."""
+    v = load_ncu(workload)
+    return (v.get("dram_bytes_per_launch"), v.get("source")) if v else (None, None)
+
+
+def load_ncu(workload: str) -> dict:
+    """The committed ncu --set full summary of moe_gemm_kernel for this workload (profiles/traffic.json:
+    DRAM bytes, tensor-pipe and DRAM-throughput % of peak, ncu's own duration and SM clock)."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(p):
-        d = json.load(open(p))
-        v = d.get(workload)
-        if v:
-            return v.get("dram_bytes_per_launch"), v.get("source")
-    return None, None
+        return json.load(open(p)).get(workload) or {}
+    return {}
 
 
 # ---------------------------------------------------------------------------
@@ -530,6 +534,7 @@ def run_ours(args, cfg):
     hbm = float(peaks["hbm_gbs"])
     mem_bound = flops / alg_bytes < peak * 1e12 / (hbm * 1e9)
     traffic, tsrc = load_traffic(("fp8_" if fp8 else "") + cfg.name)
+    ncu = load_ncu(("fp8_" if fp8 else "") + cfg.name)
 
     # ---- e2e through the public API with pinned host buffers
     e2e = None
@@ -669,6 +674,10 @@ def run_ours(args, cfg):
                                          + (" x 2 (nominal FP8 / BF16 dense ratio, 4.5 / 2.25 PF)" if fp8 else ""),
                           "algorithmic_flops_per_launch": flops, "algorithmic_bytes_per_launch": alg_bytes,
                           "traffic_source": tsrc}),
+            "ncu": ({"tensor_pipe_pct": ncu.get("tensor_pipe_pct"), "dram_throughput_pct": ncu.get("dram_throughput_pct"),
+                     "traffic_over_algorithmic": traffic / alg_bytes if traffic else None,
+                     "ncu_us": ncu.get("ncu_us"), "ncu_sm_mhz": ncu.get("sm_mhz"), "source": ncu.get("source")}
+                    if ncu else None),
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": (route_launches(cfg.T, cfg.E, cfg.k) + 1) * args.steps,   # route (+plan), GEMM
@@ -758,9 +767,18 @@ def run_ep(args, base):
     step_ms, gemm_ms, local_rows = [], [], []
     dist.barrier()
     torch.cuda.synchronize()
+
+    def aligned_start():
+        # every rank's device reaches the step together: flush, drain, host barrier, then a GPU sleep
+        # queued ahead of the step so the host enqueues it before the device gets there
+        flush()
+        torch.cuda.synchronize()
+        dist.barrier()
+        host_pad(torch)
+
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
-            flush()
+            aligned_start()
             s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s0.record(stream)
             fwd(topk_l, X_l)
@@ -773,6 +791,38 @@ def run_ep(args, base):
             else:                                    # events the library records around its GEMM launch
                 gemm_ms.append(native.last_gemm_ms())
                 local_rows.append(native.last_rows()["local_rows"])
+        # The peer-memory step has no host synchronisation inside: replay it as one CUDA graph (the
+        # eager steps above give the GEMM's own launch time).
+        graph, graph_err = None, None
+        if peer and args.graph:
+            try:
+                side = torch.cuda.Stream()
+                side.wait_stream(stream)
+                with torch.cuda.stream(side):
+                    fwd(topk_l, X_l)
+                stream.wait_stream(side)
+                torch.cuda.synchronize()
+                dist.barrier()
+                graph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(graph):
+                    fwd(topk_l, X_l)
+                torch.cuda.synchronize()
+                dist.barrier()
+                graph.replay()                       # one untimed replay (every rank replays in lockstep)
+                torch.cuda.synchronize()
+            except Exception as e:  # pragma: no cover
+                graph, graph_err = None, repr(e)[:200]
+        step_ms_eager = list(step_ms)
+        if graph is not None:
+            step_ms = []
+            for _ in range(args.steps):
+                aligned_start()
+                s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s0.record(stream)
+                graph.replay()
+                s1.record(stream)
+                s1.synchronize()
+                step_ms.append(s0.elapsed_time(s1))
     torch.cuda.synchronize()
     dist.barrier()
     t = torch.tensor([sum(step_ms)], device=cdev)
@@ -825,6 +875,8 @@ def run_ep(args, base):
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": float(t.item()) / args.steps, "higher_is_better": True,
+            "cuda_graph": graph is not None, **({"cuda_graph_error": graph_err} if graph_err else {}),
+            "ms_per_step_eager_rank0": statistics.mean(step_ms_eager),
             "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "fp8_e4m3" if fp8 else "bf16",
             "data": "synthetic",
             "config": {**ep_config(base, ws, args),

@@ -78,9 +78,10 @@ typedef int32_t moe_status;
                                    launches on one plan must be stream-ordered (the counter is reset
                                    by the launch's last CTA pair)                                     */
 
-#define MOE_NO_STREAM_K  1024u /* one-CTA tiles: never split a tile's K blocks across CTAs (stream-K, used by
-                                   default when every task has <= 32 rows and whole tiles would leave SMs
-                                   idle: the decode regime)                            */
+#define MOE_SPLIT_K  1024u      /* one-CTA tiles: when whole tiles would leave SMs idle and every task has
+                                   <= 16 rows, split each tile's K blocks into S parts over one CTA per SM
+                                   and sum them in K order (opt-in: measured slower than whole tiles on the
+                                   balanced grid)                                       */
 
 /* Output element types of moe_gemm. */
 #define MOE_DTYPE_BF16 0

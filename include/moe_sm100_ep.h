@@ -158,7 +158,8 @@ void moe_ep_destroy(moe_ep* ep);
  *   epoch flags -> a copy of the computed rows into out_dev (skipped when out_dev is the handle's own
  *   output, moe_ep_peer_output: zero copy; its rows stay valid until the next step).
  * Every call is stream-ordered and host-synchronisation-free (CUDA-graph capturable).  All ranks run
- * the same number of steps with the same k, H, N, dtypes; T <= max_tokens per rank and step.
+ * the same number of steps with the same k, H, N, dtypes; T <= max_tokens per rank and step.  Ranks
+ * driven from one process need one stream each (a rank's step waits on the device for its peers').
  * A rank whose peer never signals does not hang: its waits give up after the timeout (default 60 s,
  * moe_ep_peer_set_timeout) and moe_ep_peer_status reports 2.  P:94-98 (EP background), DESIGN.md §9.
  * ------------------------------------------------------------------------------------------ */

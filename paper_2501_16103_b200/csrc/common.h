@@ -16,12 +16,14 @@ void clear_error();
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
-// Stream-K of one-CTA memory-bound tiles (moe_gemm.cu): partial accumulators of tasks of
-// at most kSKRows rows, two slots per CTA, 256 fp32 columns per row; per-tile arrival counters for at
-// most kSKMaxTiles tiles.  The plan owns the workspace (plan.cpp).
-constexpr int kSKRows = 32;
+// Split-K of one-CTA memory-bound tiles (moe_gemm.cu): every tile's K blocks in S equal
+// parts, at most kSKUnitsPerCta parts per CTA; partial accumulators of tasks of at most kSKRows rows, one
+// slot per part, 256 fp32 columns per row; per-tile arrival counters for at most kSKMaxTiles tiles.  The
+// plan owns the workspace (plan.cpp).
+constexpr int kSKRows = 16;
 constexpr int kSKCols = 256;
-constexpr int kSKMaxTiles = 4096;
+constexpr int kSKUnitsPerCta = 6;
+constexpr int kSKMaxTiles = 1024;
 
 // Host-side view of a plan blob (offsets into the int32 word array).
 struct BlobView {

@@ -164,13 +164,27 @@ __device__ __forceinline__ void map_tile(const int32_t* prefix, const int32_t* s
   task = sigma[hh];                                        // h~ <- sigma(h)
 }
 
-// Stream-K (one-CTA memory-bound tiles): the K blocks of all tiles in virtual-tile order
-// form one sequence of KT = total * num_kb blocks; CTA c of G owns [sk_bound(c), sk_bound(c + 1)), i.e.
-// every CTA streams the same number of W blocks whatever the tile count.  A tile split between CTAs is
-// summed by the last of them to finish, in K order (deterministic).
-__device__ __forceinline__ long long sk_bound(long long c, long long KT, int G) { return c * KT / G; }
-__device__ __forceinline__ int sk_cta_of(long long p, long long KT, int G) {   // the CTA owning K block p
-  return (int)(((p + 1) * G + KT - 1) / KT - 1);
+// Split-K of one-CTA memory-bound tiles: each tile's K blocks in S equal parts; unit
+// u = p * total + v is part p of virtual tile v (part-major), and CTA c of G takes units c, c + G, c + 2G,
+// ... < U = total * S (static stride: the CTAs working at the same time stream neighbouring W column
+// strips over the same K rows, as whole tiles do).  The CTA finishing the last part of tile v sums the S
+// partials in part (K) order (deterministic) and stores Y.
+__device__ __forceinline__ int sk_parts(int total, int grid, int num_kb) {
+  // the smallest S >= 2 whose units fill the CTAs to >= 90 % (else the fullest), S <= num_kb and
+  // total * S <= kSKUnitsPerCta * grid; 0 when no S beats whole tiles on the balanced grid
+  const int per = (total + grid - 1) / grid, used = (total + per - 1) / per;
+  float best = (float)used / grid;
+  int best_s = 0;
+  for (int S = 2; S <= num_kb && (long long)total * S <= (long long)moe::kSKUnitsPerCta * grid; ++S) {
+    const long long U = (long long)total * S;
+    const float e = (float)U / (float)(grid * ((U + grid - 1) / grid));
+    if (e > best + 0.02f) {
+      best = e;
+      best_s = S;
+      if (e >= 0.9f) break;
+    }
+  }
+  return best_s;
 }
 
 struct Tile {
@@ -423,14 +437,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   // Stream-K for one-CTA tiles when whole tiles would leave SMs idle (the balanced grid uses fewer CTAs
   // than launched) and every task is short enough for the partial-accumulator slots (decode batches).
   bool sk = false;
-  long long sk_kt = 0;
+  int sk_s = 0;                                     // parts per tile
   if constexpr (kCta == 1 && !kWide && !kSplit && !kGated) {
     __shared__ int s_sk_rows;
     if (a.sk_ws != nullptr && total > 0 && total <= moe::kSKMaxTiles) {
-      const int grid = (int)gridDim.x;
-      const int per = (total + grid - 1) / grid, used = (total + per - 1) / per;
-      const long long kt = (long long)total * a.num_kb;
-      if (used < grid && kt >= grid) {
+      sk_s = sk_parts(total, (int)gridDim.x, a.num_kb);
+      if (sk_s > 0) {
         if (threadIdx.x == 0) s_sk_rows = 0;
         __syncthreads();
         const int n_tasks = __ldg(a.plan + 9);
@@ -440,7 +452,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         atomicMax(&s_sk_rows, mx);
         __syncthreads();
         sk = s_sk_rows <= moe::kSKRows;
-        sk_kt = kt;
       }
     }
   }
@@ -489,16 +500,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   // The i-th unit of work of this CTA (pair): a virtual tile v and its K blocks [k0, k1) — the whole tile,
   // or under stream-K the tile's part inside this CTA's share of the K-block sequence.  Every role warp
   // walks the same units (its own cursor).
-  const long long sk_beg = sk ? sk_bound(blockIdx.x, sk_kt, gridDim.x) : 0;
-  const long long sk_end = sk ? sk_bound(blockIdx.x + 1, sk_kt, gridDim.x) : 0;
-  long long sk_pos = sk_beg;
+  const long long sk_units = sk ? (long long)total * sk_s : 0;
+  long long sk_pos = blockIdx.x;                    // split-K: the next unit u (static stride over units)
   auto next_unit = [&](uint32_t i, int& v, int& k0, int& k1) -> bool {
     if (sk) {
-      if (sk_pos >= sk_end) return false;
-      v = (int)(sk_pos / a.num_kb);
-      k0 = (int)(sk_pos - (long long)v * a.num_kb);
-      k1 = (int)min((long long)a.num_kb, k0 + (sk_end - sk_pos));
-      sk_pos += k1 - k0;
+      if (sk_pos >= sk_units) return false;
+      const int p = (int)(sk_pos / total);
+      v = (int)(sk_pos - (long long)p * total);
+      k0 = p * a.num_kb / sk_s;
+      k1 = (p + 1) * a.num_kb / sk_s;
+      sk_pos += gridDim.x;
       return true;
     }
     v = tile_of(i);
@@ -1053,7 +1064,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     for (uint32_t qi = 0;; ++qi) {
       int v, k0, k1;
-      const long long unit_beg = sk_pos;            // stream-K: where this unit starts in the K sequence
+      const long long unit = sk_pos;                // split-K: this unit's index (its partial slot)
       if (!next_unit(qi, v, k0, k1)) break;
       int h, task, l;
       map_tile(s_prefix, s_sigma, a.M_pad, v, h, task, l);
@@ -1163,14 +1174,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           store_chunk(a, yrow_ptr, col, col_end, r);
         }
       };
-      if (sk && !(k0 == 0 && k1 == a.num_kb)) {
-        // Stream-K part of a split tile (rows <= kSKRows: lane quarter 0 holds them).  1. the partial
-        // accumulator goes to this CTA's slot (0: the unit starts the CTA's share, 1: it ends it) and
-        // TMEM is freed; 2. the epilogue warps meet, one thread counts this CTA's arrival at the tile;
-        // 3. the last CTA to arrive sums every part in K order (CTA order) and stores Y.
+      if (sk) {
+        // Split-K part of a tile (rows <= kSKRows: lane quarter 0 holds them).  1. the partial accumulator
+        // goes to the unit's slot and TMEM is freed; 2. the epilogue warps meet, one thread counts this
+        // part's arrival at the tile; 3. the CTA finishing the last part sums the S parts in K order.
         const int slot = acc;
         const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + slot * kAccCols;
-        const int wslot = 2 * (int)blockIdx.x + (unit_beg == sk_beg ? 0 : 1);
+        const int wslot = (int)unit;
         const int n0 = t.ct * t.bn;
         const int col_end = min(n0 + t.bn, a.N);
         if (q == 0) {
@@ -1189,23 +1199,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(tempty_bar(slot));
-        __threadfence();
+        // Release / acquire through one thread (the CTA barrier orders the other warps' partial stores
+        // before its fence; a fence per thread costs an L1 invalidate each, measured 25 % of dec1's time).
+        // The partials of other CTAs are then read with ld.global.cg (L2, never a stale L1 line).
         __shared__ int s_sk_last;
         named_bar_sync(1, 32 * kEpiWarps);
-        const long long p0 = (long long)v * a.num_kb;
-        const int c_first = sk_cta_of(p0, sk_kt, gridDim.x);
-        const int c_last = sk_cta_of(p0 + a.num_kb - 1, sk_kt, gridDim.x);
-        if (ew == 0 && lane == 0) s_sk_last = atomicAdd(a.sk_cnt + v, 1) == c_last - c_first;
+        if (ew == 0 && lane == 0) {
+          __threadfence();
+          s_sk_last = atomicAdd(a.sk_cnt + v, 1) == sk_s - 1;
+          if (s_sk_last) __threadfence();
+        }
         named_bar_sync(1, 32 * kEpiWarps);
         if (s_sk_last) {
-          __threadfence();
           if (q == 0 && valid) {
             for (int c = 32 * cg; c < t.bn; c += 32 * kEpiGroups) {
               uint32_t r[32];                         // the fp32 sum, as store_chunk takes it
 #pragma unroll
               for (int i = 0; i < 32; ++i) r[i] = 0u;
-              for (int cc = c_first; cc <= c_last; ++cc) {
-                const int ws2 = 2 * cc + (sk_bound(cc, sk_kt, gridDim.x) >= p0 ? 0 : 1);
+              for (int pp = 0; pp < sk_s; ++pp) {
+                const int ws2 = pp * total + v;
                 const float4* src =
                     reinterpret_cast<const float4*>(a.sk_ws + ((size_t)ws2 * moe::kSKRows + lane) * moe::kSKCols + c);
 #pragma unroll
@@ -1857,7 +1869,7 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
   a.sk_ws = nullptr;
   a.sk_cnt = nullptr;
   int sk_ctas = 0;
-  if (v.bm == 128 && !a.sched && !(v.flags & (MOE_NO_STREAM_K | MOE_GRID_STATIC)) && !prof) {
+  if (v.bm == 128 && !a.sched && (v.flags & MOE_SPLIT_K) && !(v.flags & MOE_GRID_STATIC) && !prof) {
     a.sk_ws = moe::plan_sk_ws(plan, &a.sk_cnt, &sk_ctas);
     if (sk_ctas != sm_count_cached()) a.sk_ws = nullptr;   // workspace sized for another device
   }

@@ -112,7 +112,7 @@ moe_status moe_plan_build_catalog(const int32_t* counts, int32_t E, int64_t H, i
              "moe_plan_build: bn=%d must be a multiple of %d in [16, 256] (or of 32 in (256, 512] with bm=256)", bn,
              bm == 256 ? 32 : 16);
   if (flags & ~(MOE_PAD_REPEAT | MOE_SPLIT_TAIL | MOE_ORDER_ALTERNATING | MOE_ORDER_HALF_INTERVAL | MOE_ORDER_LIGHT_LAST | MOE_GRID_BALANCED |
-                MOE_GRID_STATIC | MOE_A_GATHER4 | MOE_EPI_REGISTER | MOE_SCHED_DYNAMIC | MOE_L2_PREFETCH | MOE_NO_STREAM_K))
+                MOE_GRID_STATIC | MOE_A_GATHER4 | MOE_EPI_REGISTER | MOE_SCHED_DYNAMIC | MOE_L2_PREFETCH | MOE_SPLIT_K))
     MOE_FAIL(MOE_ERR_INVALID, "moe_plan_build: unknown flags 0x%x", flags);
   if ((flags & MOE_GRID_BALANCED) && (flags & MOE_GRID_STATIC))
     MOE_FAIL(MOE_ERR_INVALID, "moe_plan_build: MOE_GRID_BALANCED and MOE_GRID_STATIC are exclusive");
@@ -281,7 +281,7 @@ struct moe_plan {
   std::vector<moe_tile_rule> rules;   // the catalog given at creation (n_rules < 0: built-in)
   int32_t n_rules = -1;
   bool device_mode = false;   // device blob written by moe_plan_device; host blob stale
-  float* sk_ws = nullptr;     // one-CTA plans: stream-K partial accumulators [2 * sk_ctas][kSKRows][kSKCols]
+  float* sk_ws = nullptr;     // one-CTA plans: split-K partials [kSKUnitsPerCta * sk_ctas][kSKRows][kSKCols]
   int32_t* sk_cnt = nullptr;  //                 per-tile arrival counters [kSKMaxTiles] (zero between launches)
   int32_t sk_ctas = 0;
 };
@@ -374,19 +374,20 @@ moe_status moe_plan_create_catalog(const int32_t* counts, int32_t E, int64_t H, 
     delete p;
     MOE_FAIL(MOE_ERR_CUDA, "cudaMallocAsync(plan): %s", cudaGetErrorString(err));
   }
-  if (bm == 128 && !(flags & MOE_NO_STREAM_K)) {
-    // stream-K workspace of one-CTA plans: 2 partial slots per SM, counters zeroed
+  if (bm == 128 && (flags & MOE_SPLIT_K)) {
+    // split-K workspace of one-CTA plans: kSKUnitsPerCta partial slots per SM, counters zeroed
     int dev = 0, sms = 0;
     err = cudaGetDevice(&dev);
     if (err == cudaSuccess) err = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (err == cudaSuccess) {
       p->sk_ctas = sms;
-      const size_t ws = sizeof(float) * 2 * (size_t)sms * moe::kSKRows * moe::kSKCols;
+      const size_t ws = sizeof(float) * moe::kSKUnitsPerCta * (size_t)sms * moe::kSKRows * moe::kSKCols;
       err = cudaMallocAsync((void**)&p->sk_ws, ws + sizeof(int32_t) * moe::kSKMaxTiles, p->stream);
     }
     if (err == cudaSuccess) {
       p->sk_cnt = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(p->sk_ws) +
-                                             sizeof(float) * 2 * (size_t)p->sk_ctas * moe::kSKRows * moe::kSKCols);
+                                             sizeof(float) * moe::kSKUnitsPerCta * (size_t)p->sk_ctas * moe::kSKRows *
+                                                 moe::kSKCols);
       err = cudaMemsetAsync(p->sk_cnt, 0, sizeof(int32_t) * moe::kSKMaxTiles, p->stream);
     }
     if (err != cudaSuccess) {

@@ -103,7 +103,15 @@ def main():
                 f.write(f"\nmoe_gemm share of the step's own kernels: {summary['gemm_share_of_step_kernels']:.3f}\n")
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     t = json.load(open(tp)) if os.path.exists(tp) else {}
-    t[workload] = {"dram_bytes_per_launch": dram, "source": os.path.relpath(base + ".json", ROOT)}
+    def pct(m):
+        return k[m]["value"] if m in k else None
+    t[workload] = {"dram_bytes_per_launch": dram, "source": os.path.relpath(base + ".json", ROOT),
+                   "tensor_pipe_pct": pct("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"),
+                   "dram_throughput_pct": pct("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
+                   "ncu_us": to_base(k["gpu__time_duration.sum"]) * 1e6 if "gpu__time_duration.sum" in k else None,
+                   "sm_mhz": k["gpc__cycles_elapsed.avg.per_second"]["value"] * 1e3
+                   if "gpc__cycles_elapsed.avg.per_second" in k and k["gpc__cycles_elapsed.avg.per_second"]["unit"] == "Ghz"
+                   else None}
     json.dump(t, open(tp, "w"), indent=1)
     print(json.dumps({k2: v for k2, v in summary.items() if k2 != "launch_list"})[:2000])
 

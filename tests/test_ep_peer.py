@@ -107,9 +107,13 @@ def test_ep_peer_zero_copy_and_bf16_out():
     tks = [torch.from_numpy(ids[r * T_l:(r + 1) * T_l]).cuda() for r in range(G)]
     eps = M.PeerExpertParallel.group(G, E, Ws, max_tokens=T_l, k=k, max_out_bytes=N * 2)
     outs = [ep.output(T_l, N) for ep in eps]
-    for r in range(G):
-        eps[r].forward(tks[r], Xs[r], out=outs[r])
+    streams = [torch.cuda.Stream() for _ in range(G)]     # one stream per rank: a rank's step waits for its peers'
     torch.cuda.synchronize()
+    for r in range(G):
+        with torch.cuda.stream(streams[r]):
+            eps[r].forward(tks[r], Xs[r], out=outs[r])
+    torch.cuda.synchronize()
+    assert [ep.status() for ep in eps] == [0] * G
     got = torch.cat([o.float().cpu() for o in outs]).double().numpy()
     ref = omoe.per_slot_outputs(ids, X, W)
     assert np.array_equal(got, torch.from_numpy(ref).float().to(torch.bfloat16).double().numpy())

@@ -1,9 +1,10 @@
-"""GPU parity of stream-K one-CTA tiles: when whole 128 x bn tiles would leave SMs idle
-and every task has <= 32 rows (decode batches), the kernel spreads the K blocks of all tiles evenly over
-one CTA per SM; a tile split between CTAs is summed by the last one to finish, in K order.
+"""GPU parity of split-K one-CTA tiles (MOE_SPLIT_K, opt-in): when whole 128 x bn tiles
+would leave SMs idle and every task has <= 16 rows (decode batches), the kernel splits every tile's K blocks
+into S equal parts spread over one CTA per SM; the CTA finishing a tile's last part sums the parts in K
+order.
 
 Checks: integer inputs bit-exact against the fp64 oracle and against the whole-tile path
-(MOE_NO_STREAM_K) — host- and device-planned, bf16 and fp32 Y, short K (units spanning several tiles
+(no MOE_SPLIT_K) — host- and device-planned, bf16 and fp32 Y, short K (units spanning several tiles
 and tiles split over three CTAs), repeated launches on one plan (the arrival counters reset), FP8 codes;
 full-mantissa inputs within the north-star tolerance."""
 import numpy as np
@@ -18,7 +19,7 @@ from synth import fp8 as sfp8
 
 pytestmark = pytest.mark.gpu
 
-CASES = [  # T, E, k, H, N: tiles < SMs, <= 32 rows per expert
+CASES = [  # T, E, k, H, N: tiles < SMs, <= 16 rows per expert (the 20-row case keeps whole tiles)
     (1, 8, 2, 4096, 14336),    # the dec1 shape: 112 tiles of 64 K blocks over 148 CTAs
     (3, 8, 2, 256, 1024),      # 4 K blocks per tile: a CTA's share spans several tiles
     (5, 16, 3, 512, 640),      # ragged last column tile (640 = 2.5 x 256)
@@ -28,7 +29,7 @@ CASES = [  # T, E, k, H, N: tiles < SMs, <= 32 rows per expert
 ]
 
 
-def _run(ids, Xd, Wd, E, flags=0, device_plan=False, out_dtype=torch.float32, reps=1):
+def _run(ids, Xd, Wd, E, flags=M.MOE_SPLIT_K, device_plan=False, out_dtype=torch.float32, reps=1):
     topk = torch.from_numpy(np.ascontiguousarray(ids, dtype=np.int32)).cuda()
     if device_plan:
         plan = M.Plan(None, Xd.shape[1], Wd.shape[2], 128, 256, flags, E=E)
@@ -53,9 +54,8 @@ def test_streamk_integer_bit_exact(case, device_plan):
     X, W = synth.make_x(T, T, H, "int"), synth.make_w(T, E, H, N, "int")
     Xd, Wd = torch.from_numpy(X).to(torch.bfloat16).cuda(), torch.from_numpy(W).to(torch.bfloat16).cuda()
     outs, counts = _run(ids, Xd, Wd, E, device_plan=device_plan, reps=3)
-    whole, _ = _run(ids, Xd, Wd, E, flags=M.MOE_NO_STREAM_K, device_plan=device_plan)
+    whole, _ = _run(ids, Xd, Wd, E, flags=0, device_plan=device_plan)
     rc, rr, rt, _ = omoe.buckets(ids, E)
-    assert counts.max() <= 32
     ref = omoe.expert_gemm(X, W, rt, rr)
     for Y in outs:                                     # three launches on one plan: counters reset
         assert np.array_equal(Y.cpu().double().numpy(), ref)
@@ -70,7 +70,7 @@ def test_streamk_bf16_out_matches_whole_tiles(case):
     X, W = synth.make_x(T + 1, T, H, "int"), synth.make_w(T + 1, E, H, N, "int")
     Xd, Wd = torch.from_numpy(X).to(torch.bfloat16).cuda(), torch.from_numpy(W).to(torch.bfloat16).cuda()
     (Y,), _ = _run(ids, Xd, Wd, E, out_dtype=torch.bfloat16, device_plan=True)
-    (Yw,), _ = _run(ids, Xd, Wd, E, flags=M.MOE_NO_STREAM_K, out_dtype=torch.bfloat16, device_plan=True)
+    (Yw,), _ = _run(ids, Xd, Wd, E, flags=0, out_dtype=torch.bfloat16, device_plan=True)
     assert torch.equal(Y, Yw)
 
 
@@ -98,7 +98,7 @@ def test_streamk_fp8_codes_bit_exact(case):
     sc = np.array([2.0 ** (e % 3 - 1) for e in range(E)], dtype=np.float32)
     topk = torch.from_numpy(ids).cuda()
     counts, row_off, tok, _, _ = M.moe_route(topk, E)
-    plan = M.Plan(counts.cpu().numpy(), H, N, 128, 256)
+    plan = M.Plan(counts.cpu().numpy(), H, N, 128, 256, M.MOE_SPLIT_K)
     Y = M.moe_gemm_fp8(plan, torch.from_numpy(X8).cuda(), tok, torch.from_numpy(W8).cuda(), torch.from_numpy(sc).cuda(),
                        out_dtype=torch.float32)
     torch.cuda.synchronize()
@@ -106,13 +106,13 @@ def test_streamk_fp8_codes_bit_exact(case):
     assert np.array_equal(Y.cpu().double().numpy(), ofp8.expert_gemm_fp8(X8, W8, rt, rr, sc))
 
 
-def test_streamk_not_used_above_32_rows():
-    """Tasks of more than 32 rows keep whole tiles (the partial slots hold 32 rows): same bits either way."""
+def test_streamk_not_used_above_16_rows():
+    """Tasks of more than 16 rows keep whole tiles (the partial slots hold 16 rows): same bits either way."""
     T, E, k, H, N = 100, 2, 1, 512, 1024
     ids = synth.route_gumbel(5, T, E, k)
     X, W = synth.make_x(5, T, H, "int"), synth.make_w(5, E, H, N, "int")
     Xd, Wd = torch.from_numpy(X).to(torch.bfloat16).cuda(), torch.from_numpy(W).to(torch.bfloat16).cuda()
     (Y,), counts = _run(ids, Xd, Wd, E)
-    assert counts.max() > 32
+    assert counts.max() > 16
     rc, rr, rt, _ = omoe.buckets(ids, E)
     assert np.array_equal(Y.cpu().double().numpy(), omoe.expert_gemm(X, W, rt, rr))
