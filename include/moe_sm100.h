@@ -141,10 +141,19 @@ typedef int32_t moe_status;
 typedef struct { int32_t kind; int32_t m_max; } moe_tile_rule;
 #define MOE_KIND_WIDE 0
 #define MOE_KIND_SWAP 1
+#define MOE_KIND_GEMV 2           /* a whole task of m <= m_max <= MOE_GEMV_MAX_ROWS rows (a single partial row
+                                     tile) computed as a GEMV on the CUDA cores by the epilogue warps between
+                                     their accumulator drains (wide pair tiles only): the task has no tiles
+                                     (nu = 0, outside TilePrefix and sigma), its W streams while the tensor
+                                     cores work on the other tasks                       */
+#define MOE_GEMV_MAX_ROWS 4
 #define MOE_MAX_RULES 2
 #ifndef MOE_DEFAULT_SWAP_MAX
 #define MOE_DEFAULT_SWAP_MAX 64   /* built-in catalog: {SWAP, 64} — tails of <= 64 rows run swap-AB */
 #endif
+
+/* A plan has work to launch when it has tiles (header word 2 > 0) or GEMV tasks; moe_gemm returns
+ * MOE_OK_EMPTY only when it has neither. */
 
 /* Number of int32 words moe_plan_build needs for E experts (upper bound). */
 int64_t moe_plan_blob_words(int32_t E);

@@ -69,14 +69,20 @@ def tiles_of(rows: int, N: int, bm: int, bn: int) -> int:
     return ceil_div(rows, bm) * ceil_div(N, bn)
 
 
+KIND_GEMV = 2   # a whole task of <= m_max rows computed as a CUDA-core GEMV, outside the tile space
+
+
 def tail_kind(m: int, bm: int, catalog) -> int:
     """The tiling strategy of an expert's last row tile ("categorized into several
     pre-defined tiling strategies"; R6): r = m mod bm rows (0: no partial tile); the first
-    catalog rule (kind, m_max) with r <= m_max gives the kind, else kind 0."""
+    catalog rule (kind, m_max) with r <= m_max gives the kind, else kind 0.  A GEMV rule (kind 2) applies
+    only to a task that is a single partial row tile (m < bm): the whole task is then that strategy."""
     r = int(m) % bm
     if int(m) <= 0 or r == 0:
         return 0
     for kind, m_max in catalog:
+        if int(kind) == KIND_GEMV and int(m) >= bm:
+            continue
         if r <= m_max:
             return int(kind)
     return 0
@@ -144,11 +150,14 @@ def plan(counts, N: int, bm: int, bn: int, pad_mode: str = "max", warp_size: int
     ordering), TilePrefix (Alg. 1 over eta in sigma's order), padded per P:203."""
     if tasks is None:
         tasks = make_tasks(counts, bm, bn, split_tail, catalog)
-    nu = [tiles_of(t["rows"], N, t["bm"], t["bn"]) for t in tasks]
-    sigma, prefix = mapping.nonempty_stage(nu, order_tasks([t["rows"] for t in tasks], order)
-                                           if order != "natural" else None)
+    # Alg. 3's per-task strategies: a GEMV task has no tiles (nu = 0, so the non-empty stage leaves it out
+    # of sigma / TilePrefix); its rows are computed by the GEMV strategy (DESIGN.md R6, §6.8).
+    nu = [0 if t.get("kind", 0) == KIND_GEMV else tiles_of(t["rows"], N, t["bm"], t["bn"]) for t in tasks]
+    loads = [t["rows"] if nu[i] > 0 else 0 for i, t in enumerate(tasks)]     # the tasks with tiles (eta)
+    sigma, prefix = mapping.nonempty_stage(nu, order_tasks(loads, order) if order != "natural" else None)
     padded = mapping.pad_tile_prefix(prefix, warp_size, pad_mode) if prefix else []
-    return dict(tasks=tasks, nu=nu, sigma=sigma, prefix=prefix, padded=padded,
+    gemv = [i for i, t in enumerate(tasks) if t.get("kind", 0) == KIND_GEMV and t["rows"] > 0]
+    return dict(tasks=tasks, nu=nu, sigma=sigma, prefix=prefix, padded=padded, gemv=gemv,
                 M=len(sigma), total=mapping.total_tiles(prefix), N=N, warp_size=warp_size)
 
 

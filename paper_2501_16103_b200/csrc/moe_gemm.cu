@@ -26,6 +26,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <climits>
@@ -120,6 +121,8 @@ struct GemmArgs {
   int32_t* sk_cnt;           //           and per-tile arrival counters (zero between launches)
   int32_t light_merge;       // MOE_ORDER_LIGHT_LAST plan under the dynamic tile order: interleave the light
                              // (memory-bound) tail of the virtual tiles among the others in proportion
+  int32_t* gemv_q;           // nullable: the plan may hold MOE_KIND_GEMV tasks (wide pair kernels): [0] next
+                             // GEMV unit, [1] epilogue warps done (both zero between launches)
 };
 
 // Per-CTA counters written by the instrumented build (kProf = true).
@@ -304,6 +307,59 @@ __device__ __forceinline__ void wait_timed(uint32_t bar, uint32_t parity, long l
     mbar_wait(bar, parity);
   }
 }
+
+// ---------------------------------------------------------------------------
+// MOE_KIND_GEMV tasks: Alg. 3's per-task strategy for tasks of <= MOE_GEMV_MAX_ROWS
+// rows.  They have no tiles; the epilogue warps of every CTA take GEMV units from a global queue and
+// work on them whenever they would otherwise wait for an accumulator, so the tasks' W streams while the
+// tensor cores compute the other tasks' tiles.  A unit = one task x 128 output columns x all of K, owned
+// by one warp: lanes 0-15 take K rows k..k+7, lanes 16-31 rows k+8..k+15 of each 16-row round, lane l
+// columns 8 (l mod 16) + [0, 8); fp32 accumulation in registers, the two half-warps summed at the end.
+// W rows are prefetched into L2 kGemvPf rounds ahead (no registers held for bytes in flight).
+// ---------------------------------------------------------------------------
+constexpr int kGemvCols = 128;
+constexpr int kGemvPf = 6;
+
+template <bool kFp8>
+struct GemvUnit {
+  int task = -1, rows = 0, row0 = 0, expert = 0, col0 = 0, kpos = 0;
+  float acc[MOE_GEMV_MAX_ROWS][8];
+
+  // 8 values (bf16: a uint4; E4M3: a uint2) -> fp32
+  __device__ __forceinline__ static void widen(const uint4& q, float (&f)[8]) {
+    if constexpr (kFp8) {
+      const uint32_t w[2] = {q.x, q.y};
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          uint32_t h2;
+          const uint16_t pair = (uint16_t)(w[i] >> (16 * j));
+          asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h2) : "h"(pair));
+          const __half2 hh = *reinterpret_cast<const __half2*>(&h2);
+          const float2 ff = __half22float2(hh);
+          f[4 * i + 2 * j] = ff.x;
+          f[4 * i + 2 * j + 1] = ff.y;
+        }
+      }
+    } else {
+      const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        f[2 * i] = __uint_as_float(w[i] << 16);
+        f[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+      }
+    }
+  }
+  __device__ __forceinline__ static uint4 load8(const uint8_t* p) {
+    if constexpr (kFp8) {
+      const uint2 v = __ldcs(reinterpret_cast<const uint2*>(p));
+      return make_uint4(v.x, v.y, 0u, 0u);
+    } else {
+      return __ldcs(reinterpret_cast<const uint4*>(p));
+    }
+  }
+};
 
 // Pipeline geometry per CTA-group size: a CTA pair (cta_group::2) splits the B block across the
 // two CTAs, so a stage is 32 KB instead of 48 KB and six stages fit.  A wide pair tile (256 x 512,
@@ -1055,10 +1111,149 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t n_chunk = 0;                                     // TMA-store chunks issued by this warp
     const uint32_t ebuf = sEpi + (uint32_t)ew * kEpiBufBytes;
     long long c_wait = 0, c_work = 0;
+    // ---- MOE_KIND_GEMV side work (wide kernels) ----
+    GemvUnit<kFp8> gu;
+    int g_units = -1;                               // -1: not counted yet; 0: none / queue exhausted
+    const int nb_cols = (a.N + kGemvCols - 1) / kGemvCols;
+    const int n_tasks_all = __ldg(a.plan + 9);
+    auto is_gemv = [&](int tk) {
+      return tk < n_tasks_all && __ldg(params + tk * MOE_PLAN_TASK_WORDS + 3) == MOE_KIND_GEMV &&
+             __ldg(params + tk * MOE_PLAN_TASK_WORDS + 2) > 0;
+    };
+    auto count_gemv = [&]() {
+      int n = 0;
+      for (int b = 0; b < n_tasks_all; b += 32) n += __popc(__ballot_sync(0xffffffffu, is_gemv(b + lane)));
+      return n;
+    };
+    auto find_gemv = [&](int j) -> int {           // the j-th GEMV task in task order
+      for (int b = 0; b < n_tasks_all; b += 32) {
+        const unsigned m = __ballot_sync(0xffffffffu, is_gemv(b + lane));
+        const int c = __popc(m);
+        if (j < c) return b + __fns(m, 0, j + 1);
+        j -= c;
+      }
+      return -1;
+    };
+    const size_t esz_in = kFp8 ? 1 : 2;
+    auto gemv_round = [&]() -> bool {               // one 16-row round of this warp's unit; false: no work left
+      if constexpr (!kWide || kGated) {
+        return false;
+      } else {
+        if (a.gemv_q == nullptr || g_units == 0) return false;
+        if (gu.task < 0) {
+          if (g_units < 0) g_units = count_gemv() * nb_cols;
+          int u = 0;
+          if (lane == 0) u = g_units > 0 ? atomicAdd(a.gemv_q, 1) : 0;
+          u = __shfl_sync(0xffffffffu, u, 0);
+          if (u >= g_units) {
+            if (lane == 0 && atomicAdd(a.gemv_q + 1, 1) == (int)(gridDim.x * kEpiWarps) - 1) {
+              a.gemv_q[0] = 0;                      // every epilogue warp is done: reset for the next launch
+              a.gemv_q[1] = 0;
+            }
+            g_units = 0;
+            return false;
+          }
+          const int j = u / nb_cols;
+          gu.task = find_gemv(j);
+          gu.expert = __ldg(params + gu.task * MOE_PLAN_TASK_WORDS + 0);
+          gu.row0 = __ldg(params + gu.task * MOE_PLAN_TASK_WORDS + 1);
+          gu.rows = __ldg(params + gu.task * MOE_PLAN_TASK_WORDS + 2);
+          gu.col0 = (u - j * nb_cols) * kGemvCols + (lane & 15) * 8;
+          gu.kpos = 0;
+#pragma unroll
+          for (int t = 0; t < MOE_GEMV_MAX_ROWS; ++t)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) gu.acc[t][i] = 0.f;
+        }
+        const int kr = gu.kpos + 8 * (lane >> 4);
+        const bool colok = gu.col0 < a.N;
+        const uint8_t* wbase = a.W + ((size_t)gu.expert * a.H) * a.N * esz_in + (size_t)gu.col0 * esz_in;
+        // L2 prefetch of the rows kGemvPf rounds ahead (one 128-byte line per lane pair ... per row)
+        {
+          const int kp = kr + 16 * kGemvPf;
+          if (colok && kp < a.H && (lane & 7) == 0)
+            for (int i = 0; i < 8; ++i) prefetch_l2(wbase + (size_t)(kp + i) * a.N * esz_in);
+        }
+        if (colok && kr < a.H) {
+          uint4 wv[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) wv[i] = GemvUnit<kFp8>::load8(wbase + (size_t)(kr + i) * a.N * esz_in);
+          const int64_t xrow = (int64_t)a.H * esz_in;
+#pragma unroll
+          for (int t = 0; t < MOE_GEMV_MAX_ROWS; ++t) {
+            if (t < gu.rows) {
+              const int tok = a.token_idx ? __ldg(a.token_idx + gu.row0 + t) : gu.row0 + t;
+              const uint8_t* xp = reinterpret_cast<const uint8_t*>(a.X) + tok * xrow + (int64_t)kr * esz_in;
+              uint4 xq;
+              if constexpr (kFp8) {
+                const uint2 v2 = __ldg(reinterpret_cast<const uint2*>(xp));
+                xq = make_uint4(v2.x, v2.y, 0u, 0u);
+              } else {
+                xq = __ldg(reinterpret_cast<const uint4*>(xp));
+              }
+              float xf[8];
+              GemvUnit<kFp8>::widen(xq, xf);
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                float wf[8];
+                GemvUnit<kFp8>::widen(wv[i], wf);
+#pragma unroll
+                for (int c = 0; c < 8; ++c) gu.acc[t][c] = fmaf(xf[i], wf[c], gu.acc[t][c]);
+              }
+            }
+          }
+        }
+        gu.kpos += 16;
+        if (gu.kpos >= a.H) {                       // unit done: sum the two half-warps, store the rows
+          float sc = 1.f;
+          if constexpr (kFp8) sc = a.scale ? __ldg(a.scale + gu.expert) : 1.f;
+#pragma unroll
+          for (int t = 0; t < MOE_GEMV_MAX_ROWS; ++t) {
+            uint32_t r[32];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              const float v2 = gu.acc[t][c] + __shfl_xor_sync(0xffffffffu, gu.acc[t][c], 16);
+              r[c] = __float_as_uint(kFp8 ? v2 * sc : v2);
+            }
+            if (t < gu.rows && lane < 16 && colok) {
+              const int grow = gu.row0 + t;
+              uint8_t* yp = a.y_row_ptr ? reinterpret_cast<uint8_t*>(__ldg(a.y_row_ptr + grow))
+                                        : reinterpret_cast<uint8_t*>(a.Y) +
+                                              (a.y_row_map ? (int64_t)__ldg(a.y_row_map + grow) : (int64_t)grow) *
+                                                  a.N * (a.y_f32 ? 4 : 2);
+              if (a.y_f32) {
+                float* y = reinterpret_cast<float*>(yp) + gu.col0;
+                *reinterpret_cast<uint4*>(y) = make_uint4(r[0], r[1], r[2], r[3]);
+                *reinterpret_cast<uint4*>(y + 4) = make_uint4(r[4], r[5], r[6], r[7]);
+              } else {
+                *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(yp) + gu.col0) =
+                    make_uint4(pack_bf16(r[0], r[1]), pack_bf16(r[2], r[3]), pack_bf16(r[4], r[5]),
+                               pack_bf16(r[6], r[7]));
+              }
+            }
+          }
+          gu.task = -1;
+        }
+        return true;
+      }
+    };
+    // Wait for an accumulator phase; with GEMV work queued, work on it while the phase is pending.
+    auto wait_acc = [&](uint32_t bar, uint32_t phase) {
+      if (a.gemv_q != nullptr && g_units != 0) {
+        while (!mbar_test_wait(bar, phase)) {
+          if (!gemv_round()) {
+            wait_timed<kProf>(bar, phase, c_wait);
+            return;
+          }
+        }
+        return;
+      }
+      wait_timed<kProf>(bar, phase, c_wait);
+    };
     // Wide tiles: "block 0 full" is awaited with the tile, "block 1 full" before draining block 1.
     auto wait_block1 = [&](int hf) {
       if (kWide && hf == 1) {
-        wait_timed<kProf>(tfull_bar(1), acc_phase, c_wait);
+        wait_acc(tfull_bar(1), acc_phase);
         tc_fence_after();
       }
     };
@@ -1069,7 +1264,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int h, task, l;
       map_tile(s_prefix, s_sigma, a.M_pad, v, h, task, l);
       const Tile t = load_tile<kSplit>(params, task, l);
-      wait_timed<kProf>(tfull_bar(acc), acc_phase, c_wait);
+      wait_acc(tfull_bar(acc), acc_phase);
       const long long w0 = kProf ? clock64() : 0;
       tc_fence_after();
       if (kSplit && t.kind == 1) {
@@ -1316,6 +1511,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         acc_phase ^= 1u;
       }
     }
+    while (gemv_round()) {
+    }                                                         // the GEMV units left after the last tile
     if (lane == 0) bulk_wait_group<0>();                      // TMA stores complete before exit
     if constexpr (kProf) {
       if (q == 0 && lane == 0) {
@@ -1760,11 +1957,23 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
     v.off_prefix = MOE_PLAN_HEADER;
     v.off_sigma = v.off_prefix + v.M_pad;
     v.off_params = v.off_sigma + v.M_pad;
-  } else {
+  }
+  // MOE_KIND_GEMV tasks (no tiles; computed by the epilogue warps of wide kernels): a host
+  // plan lists them in its task parameters, a device-planned one may have them when its catalog has the rule.
+  bool has_gemv = false;
+  {
     int64_t words = 0;
     const int32_t* blob = moe::plan_blob_host(plan, &words);
-    if (!moe::blob_view(blob, words, &v)) MOE_FAIL(MOE_ERR_INVALID, "moe_gemm: corrupt plan");
-    if (v.total == 0) return MOE_OK_EMPTY;
+    if (dev_planned) {
+      for (int i = 0; i < MOE_MAX_RULES; ++i) has_gemv |= blob[12 + 2 * i] == MOE_KIND_GEMV && blob[13 + 2 * i] > 0;
+    } else {
+      if (!moe::blob_view(blob, words, &v)) MOE_FAIL(MOE_ERR_INVALID, "moe_gemm: corrupt plan");
+      for (int i = 0; i < v.n_tasks; ++i) {
+        const int32_t* p = blob + v.off_params + (int64_t)MOE_PLAN_TASK_WORDS * i;
+        has_gemv |= p[3] == MOE_KIND_GEMV && p[2] > 0;
+      }
+      if (v.total == 0 && !has_gemv) return MOE_OK_EMPTY;
+    }
   }
   if (!X || !W || !Y) MOE_FAIL(MOE_ERR_INVALID, "moe_gemm: null tensor pointer");
   if (!aligned16(X) || !aligned16(W) || !aligned16(Y))
@@ -1861,6 +2070,9 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
                        (!(v.flags & (MOE_GRID_STATIC | MOE_GRID_BALANCED)) && v.bm == 256);
   a.sched = dynamic ? moe::plan_sched_dev(plan) : nullptr;
   a.light_merge = dynamic && (v.flags & MOE_ORDER_LIGHT_LAST) ? 1 : 0;
+  a.gemv_q = has_gemv ? moe::plan_sched_dev(plan) + 2 : nullptr;
+  if (has_gemv && !(wide && !gated))
+    MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_gemm: MOE_KIND_GEMV tasks need a wide pair tile plan (bm 256, bn > 256)");
   a.W = reinterpret_cast<const uint8_t*>(W);
   a.pf_dist = (v.flags & MOE_L2_PREFETCH) && v.N % 64 == 0 ? kL2Pf : 0;
   a.balance = a.sched ? 0 : (v.flags & MOE_GRID_BALANCED) ? 1 : (v.flags & MOE_GRID_STATIC) ? 0 : v.bm == 128;
@@ -1905,7 +2117,8 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
   } else if (v.bm == 256) {
     // Two strategies in the launch when the catalog has a swap-AB rule (bf16, not gated).
     const bool split = moe::plan_has_swap(plan) && !fp8 && !gated;
-    const int pairs = v.total < 0 ? sm_count_cached() / 2 : std::min(v.total, sm_count_cached() / 2);
+    // (GEMV tasks: every CTA's epilogue warps take GEMV units, so all SMs launch)
+    const int pairs = v.total < 0 || has_gemv ? sm_count_cached() / 2 : std::min(v.total, sm_count_cached() / 2);
     const size_t smem = (split && wide   ? Geo<2, true, true>::kSmem
                          : split         ? Geo<2, true>::kSmem
                          : wide || gated ? Geo<2, false, true>::kSmem

@@ -136,18 +136,23 @@ moe_status moe_plan_build_catalog(const int32_t* counts, int32_t E, int64_t H, i
     if (n_rules > MOE_MAX_RULES) MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_plan_build: at most %d catalog rules", MOE_MAX_RULES);
     if (n_rules > 0 && !rules) MOE_FAIL(MOE_ERR_INVALID, "moe_plan_build: null catalog");
     for (int32_t i = 0; i < n_rules; ++i) {
-      if (rules[i].kind != MOE_KIND_WIDE && rules[i].kind != MOE_KIND_SWAP)
+      if (rules[i].kind != MOE_KIND_WIDE && rules[i].kind != MOE_KIND_SWAP && rules[i].kind != MOE_KIND_GEMV)
         MOE_FAIL(MOE_ERR_INVALID, "moe_plan_build: catalog rule %d: kind %d", i, rules[i].kind);
       if (rules[i].kind == MOE_KIND_SWAP && !pair_blocks)
         MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_plan_build: MOE_KIND_SWAP needs bm = 256 and bn >= 256 (got %d x %d)", bm, bn);
+      if (rules[i].kind == MOE_KIND_GEMV && (!(bm == 256 && bn > 256) || rules[i].m_max > MOE_GEMV_MAX_ROWS))
+        MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_plan_build: MOE_KIND_GEMV needs wide pair tiles (bm = 256, bn > 256) and "
+                 "m_max <= %d (got %d x %d, m_max %d)", MOE_GEMV_MAX_ROWS, bm, bn, rules[i].m_max);
       cat[n_cat++] = rules[i];
     }
   }
   auto kind_of = [&](int64_t m) -> int32_t {
     const int64_t r = m % bm;
     if (m <= 0 || r == 0) return MOE_KIND_WIDE;
-    for (int32_t i = 0; i < n_cat; ++i)
+    for (int32_t i = 0; i < n_cat; ++i) {
+      if (cat[i].kind == MOE_KIND_GEMV && m >= bm) continue;   // GEMV: whole single-row-tile tasks only
       if (r <= cat[i].m_max) return cat[i].kind;
+    }
     return MOE_KIND_WIDE;
   };
   // CSR row offsets: exclusive prefix of counts in expert-id order.
@@ -164,7 +169,12 @@ moe_status moe_plan_build_catalog(const int32_t* counts, int32_t E, int64_t H, i
   const int32_t n_tasks = E;
   const int64_t col_tiles = ceil_div(N, bn);
   std::vector<int64_t> nu(n_tasks);
-  for (int32_t i = 0; i < n_tasks; ++i) nu[i] = counts[i] == 0 ? 0 : ceil_div(counts[i], bm) * col_tiles;
+  int32_t n_gemv = 0;                            // GEMV tasks have no tiles (Alg. 3's other strategy, §6.8)
+  for (int32_t i = 0; i < n_tasks; ++i) {
+    const bool gemv = counts[i] > 0 && kind_of(counts[i]) == MOE_KIND_GEMV;
+    n_gemv += gemv;
+    nu[i] = counts[i] == 0 || gemv ? 0 : ceil_div(counts[i], bm) * col_tiles;
+  }
 
   // Non-empty stage: sigma in natural order, then Alg. 1 over eta.
   std::vector<int32_t> sigma;
@@ -254,7 +264,7 @@ moe_status moe_plan_build_catalog(const int32_t* counts, int32_t E, int64_t H, i
   }
   for (int32_t e = 0; e <= E; ++e) roff[e] = (int32_t)row_off[e];
   if (blob_len) *blob_len = words;
-  return M == 0 ? MOE_OK_EMPTY : MOE_OK;
+  return M == 0 && n_gemv == 0 ? MOE_OK_EMPTY : MOE_OK;
 }
 
 const char* moe_last_error(void) { return moe::g_last_error.c_str(); }

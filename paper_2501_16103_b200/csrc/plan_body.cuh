@@ -48,14 +48,16 @@ __device__ __forceinline__ void plan_body(long long m, int E, int H, int N, int 
   {
     const long long r = m % bm;
     if (m > 0 && r > 0) {
-      for (int i = MOE_MAX_RULES - 1; i >= 0; --i)                 // the first matching rule wins
+      for (int i = MOE_MAX_RULES - 1; i >= 0; --i) {               // the first matching rule wins
+        if (blob[12 + 2 * i] == MOE_KIND_GEMV && m >= bm) continue;  // GEMV: whole single-tile tasks only
         if (r <= blob[13 + 2 * i]) kind = blob[12 + 2 * i];
+      }
     }
   }
   __syncthreads();                                                 // every thread read the catalog
   const long long col_tiles = (N + bn - 1) / bn;
   const long long row_tiles = (m + bm - 1) / bm;
-  const long long nu = m > 0 ? row_tiles * col_tiles : 0;         // nu(T_t)
+  const long long nu = m > 0 && kind != MOE_KIND_GEMV ? row_tiles * col_tiles : 0;   // nu(T_t); GEMV: no tiles
   long long rows_total, tiles_total, ne_total;
   const long long rows_incl = block_scan_incl(m, s_warp, &rows_total);
   block_scan_incl(nu, s_warp, &tiles_total);                       // total tiles

@@ -68,7 +68,7 @@ def _compare(counts, N, bm, bn, pad, split=False, order="natural", catalog=None)
         q = p["params"][i]
         assert q[0] == t["expert"] and q[1] == row_off[t["expert"]] + t["row_begin"] and q[2] == t["rows"]
         assert q[3] == t["kind"] and q[4] == t["bm"] and q[5] == t["bn"]
-        assert q[6] * q[7] == ref["nu"][i]
+        assert (0 if t["kind"] == 2 else q[6] * q[7]) == ref["nu"][i]
         assert q[6] == -(-t["rows"] // bm)
 
 
@@ -284,14 +284,19 @@ def test_planner_catalog_matches_oracle():
     for _ in range(200):
         E = rng.randint(1, 200)
         counts = np.array([0 if rng.random() < 0.3 else rng.randint(1, 3000) for _ in range(E)])
-        rules = [(rng.choice([0, 1]), rng.randint(0, 256)) for _ in range(rng.randint(0, 2))]
-        N = 8 * rng.randint(1, 3000)
         bn = rng.choice([256, 512])
+        kinds = [0, 1, 2] if bn == 512 else [0, 1]
+        rules = [(k_, rng.randint(0, 4) if k_ == 2 else rng.randint(0, 256))
+                 for k_ in (rng.choice(kinds) for _ in range(rng.randint(0, 2)))]
+        if rng.random() < 0.3:
+            counts = np.where(counts > 0, counts % 7, 0)                   # many 1-6 row experts
+        N = 8 * rng.randint(1, 3000)
         _compare(counts, N, 256, bn, rng.choice(["max", "repeat"]), catalog=rules,
-                 order=rng.choice(["natural", "half_interval"]))
-        base = moe_lib.parse_plan_blob(moe_lib.moe_plan_build(counts, 64, N, 256, bn, catalog=()))
-        got = moe_lib.parse_plan_blob(moe_lib.moe_plan_build(counts, 64, N, 256, bn, catalog=rules))
-        assert np.array_equal(base["prefix"], got["prefix"]) and np.array_equal(base["sigma"], got["sigma"])
+                 order=rng.choice(["natural", "half_interval", "light_last"]))
+        if all(k_ != 2 for k_, _ in rules):                                # swap / wide: mapping unchanged
+            base = moe_lib.parse_plan_blob(moe_lib.moe_plan_build(counts, 64, N, 256, bn, catalog=()))
+            got = moe_lib.parse_plan_blob(moe_lib.moe_plan_build(counts, 64, N, 256, bn, catalog=rules))
+            assert np.array_equal(base["prefix"], got["prefix"]) and np.array_equal(base["sigma"], got["sigma"])
     # worked examples: tails 1 and 200 under {SWAP, 64}; 256-row experts have no tail
     p = moe_lib.parse_plan_blob(moe_lib.moe_plan_build([1, 456, 256, 0, 64, 65], 64, 1024, 256, 512))
     assert p["params"][:, 3].tolist() == [1, 0, 0, 0, 1, 0]
@@ -301,3 +306,19 @@ def test_planner_catalog_matches_oracle():
         moe_lib.moe_plan_build([5, 5], 64, 1024, 256, 512, catalog=[(1, 64), (0, 9), (1, 200)])
     with pytest.raises(moe_lib.MoeError):
         moe_lib.moe_plan_build([5, 5], 64, 1024, 256, 512, catalog=[(7, 64)])
+
+
+def test_planner_gemv_strategy_by_hand():
+    """MOE_KIND_GEMV (Alg. 3's per-task strategy for <= 4-row tasks): whole tasks of
+    m <= m_max < 256 rows get kind 2 and no tiles — they leave TilePrefix and sigma; a 257-row expert's
+    1-row tail stays a tile (GEMV covers whole tasks only); wide pair tiles only, m_max <= 4."""
+    counts = [1, 456, 4, 0, 5, 257, 3]
+    p = moe_lib.parse_plan_blob(moe_lib.moe_plan_build(counts, 64, 1024, 256, 512, catalog=[(2, 4), (1, 64)]))
+    assert p["params"][:, 3].tolist() == [2, 0, 2, 0, 1, 1, 2]
+    assert p["M"] == 3 and p["sigma"][:3].tolist() == [1, 4, 5]           # experts 1, 4, 5 have tiles
+    assert p["total"] == (2 + 1 + 2) * 2                                   # row tiles x 2 column tiles
+    q = moe_lib.parse_plan_blob(moe_lib.moe_plan_build([2, 0, 1], 64, 1024, 256, 512, catalog=[(2, 4)]))
+    assert q["M"] == 0 and q["total"] == 0                                 # only GEMV tasks: still work (MOE_OK)
+    for bad in ([(2, 5)], [(2, 4)]):
+        with pytest.raises(moe_lib.MoeError):
+            moe_lib.moe_plan_build([1, 1], 64, 1024, 256, 256 if bad == [(2, 4)] else 512, catalog=bad)

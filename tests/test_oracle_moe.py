@@ -137,6 +137,15 @@ def test_expert_ordering_spec_examples():
             assert sorted(o) == [j for j in range(len(loads)) if loads[j] > 0]     # a permutation of eta
 
 
+def test_gemv_kind_by_hand():
+    """kind 2 (GEMV): whole tasks of m <= m_max < bm only; they have no tiles (nu = 0, not in sigma)."""
+    cat = ((2, 4), (1, 64))
+    assert [moe.tail_kind(m, 256, cat) for m in (0, 1, 4, 5, 64, 65, 257, 260, 320)] == [0, 2, 2, 1, 1, 0, 1, 1, 1]
+    p = moe.plan([1, 456, 4, 0, 5, 257, 3], 1024, 256, 512, catalog=cat)
+    assert p["nu"] == [0, 4, 0, 0, 2, 4, 0] and p["sigma"] == [1, 4, 5] and p["gemv"] == [0, 2, 6]
+    assert p["total"] == 10
+
+
 def test_light_last_order_by_hand():
     """light_last: tasks of > 64 rows in expert order, then the light ones in expert order (R7)."""
     assert moe.order_tasks([65, 64, 0, 1, 300, 2, 65], "light_last") == [0, 4, 6, 1, 3, 5]
