@@ -147,10 +147,15 @@ typedef struct { int32_t kind; int32_t m_max; } moe_tile_rule;
                                      (nu = 0, outside TilePrefix and sigma), its W streams while the tensor
                                      cores work on the other tasks                       */
 #define MOE_GEMV_MAX_ROWS 4
+#define MOE_GEMV_MIN_TILES 128    /* GEMV rules apply only when the plan's other tasks have >= this many tiles
+                                     (their tensor work must cover the GEMV streams); otherwise those tasks
+                                     fall through to the catalog's next rule                              */
 #define MOE_MAX_RULES 2
-#ifndef MOE_DEFAULT_SWAP_MAX
-#define MOE_DEFAULT_SWAP_MAX 64   /* built-in catalog: {SWAP, 64} — tails of <= 64 rows run swap-AB */
+#ifndef MOE_DEFAULT_GEMV_MAX
+#define MOE_DEFAULT_GEMV_MAX 4    /* built-in catalog of wide pair plans (bm 256, bn > 256): {GEMV, 4};
+                                     other shapes: no rules (SWAP is opt-in: measured no faster, §7.5)    */
 #endif
+#define MOE_DEFAULT_SWAP_MAX 64   /* the swap-AB rule tests and A/B runs use: {SWAP, 64}                   */
 
 /* A plan has work to launch when it has tiles (header word 2 > 0) or GEMV tasks; moe_gemm returns
  * MOE_OK_EMPTY only when it has neither. */

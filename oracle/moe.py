@@ -70,6 +70,7 @@ def tiles_of(rows: int, N: int, bm: int, bn: int) -> int:
 
 
 KIND_GEMV = 2   # a whole task of <= m_max rows computed as a CUDA-core GEMV, outside the tile space
+GEMV_MIN_TILES = 128
 
 
 def tail_kind(m: int, bm: int, catalog) -> int:
@@ -150,6 +151,11 @@ def plan(counts, N: int, bm: int, bn: int, pad_mode: str = "max", warp_size: int
     ordering), TilePrefix (Alg. 1 over eta in sigma's order), padded per P:203."""
     if tasks is None:
         tasks = make_tasks(counts, bm, bn, split_tail, catalog)
+        # GEMV rules apply only when the other tasks have >= GEMV_MIN_TILES tiles (their tensor work must
+        # cover the GEMV streams, DESIGN.md §6.8); otherwise those tasks take the next rule.
+        other = sum(tiles_of(t["rows"], N, t["bm"], t["bn"]) for t in tasks if t["kind"] != KIND_GEMV)
+        if any(t["kind"] == KIND_GEMV for t in tasks) and other < GEMV_MIN_TILES:
+            tasks = make_tasks(counts, bm, bn, split_tail, [r for r in catalog if int(r[0]) != KIND_GEMV])
     # Alg. 3's per-task strategies: a GEMV task has no tiles (nu = 0, so the non-empty stage leaves it out
     # of sigma / TilePrefix); its rows are computed by the GEMV strategy (DESIGN.md R6, §6.8).
     nu = [0 if t.get("kind", 0) == KIND_GEMV else tiles_of(t["rows"], N, t["bm"], t["bn"]) for t in tasks]

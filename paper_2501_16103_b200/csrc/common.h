@@ -1,5 +1,6 @@
 // Internal helpers shared by the library's translation units (not part of the ABI).
 #pragma once
+#include <cuda_runtime.h>
 #include <cstdarg>
 #include <cstdint>
 #include <cstdio>
@@ -34,6 +35,14 @@ struct BlobView {
 bool blob_view(const int32_t* blob, int64_t len, BlobView* v);
 
 struct moe_plan_impl;
+
+// Load every kernel of a translation unit on the current device now (CUDA lazy loading would otherwise
+// load a kernel at its first launch, which can wait for work already queued on the device — a deadlock
+// when that work waits, on the device, for a peer this thread has not enqueued yet; ep_peer.cpp).
+cudaError_t preload_gemm_kernels();
+cudaError_t preload_route_kernels();
+cudaError_t preload_ep_kernels();
+cudaError_t preload_plan_kernel();
 
 }  // namespace moe
 

@@ -441,3 +441,17 @@ moe_status moe_ep_unpack(const void* rows, const int32_t* ret_meta, int64_t n, c
 }
 
 }  // extern "C"
+
+cudaError_t moe::preload_ep_kernels() {
+  cudaFuncAttributes fa;
+  const void* ks[] = {(const void*)ep_count_kernel, (const void*)ep_scatter_kernel, (const void*)gather_rows_kernel,
+                      (const void*)ep_combine_map_kernel, (const void*)ep_combine_ptr_kernel, (const void*)ep_unpack_kernel,
+                      (const void*)ep_peer_dispatch_kernel, (const void*)ep_peer_signal_kernel,
+                      (const void*)ep_peer_wait_kernel, (const void*)ep_peer_combine_ptr_kernel,
+                      (const void*)ep_peer_copy_out_kernel};
+  for (const void* k : ks) {
+    const cudaError_t e = cudaFuncGetAttributes(&fa, k);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}

@@ -93,12 +93,8 @@ moe_status ep_peer_forward(moe_ep* ep, const int32_t* topk, int64_t T, int32_t k
     moe_status s_ = (expr); \
     if (s_ < 0) return s_;  \
   } while (0)
-  // 1. dispatch: per-destination deduplicated rows, stored into the owners' receive buffers
-  PEER_TRY(moe_ep_dispatch_plan(topk, T, k, ep->E, G, P.counts2, P.send_off, P.send_tok, P.send_meta, s));
-  PEER_CUDA(ep_peer_dispatch(X, x_row, P.send_off, P.send_tok, P.send_meta, G, k, ep->rank, P.T_max, P.peers_dev, s));
-  PEER_CUDA(ep_peer_signal(P.peers_dev, G, ep->rank, kDispatchWord, P.epoch_dev, true, s));
-  PEER_CUDA(ep_peer_wait(flags_mine, G, kDispatchWord, P.epoch_dev, P.status_dev, P.timeout_ns, s));
-  // 2. local experts: buckets over the received ids (empty rows are -1), device plan
+  // 0. host-side setup first (a plan for new H / N: host work and a small copy), before anything of this
+  //    step that waits on the device for the peers is enqueued
   if (!ep->plan || ep->plan_H != H || ep->plan_N != N) {
     if (ep->plan) moe_plan_destroy(ep->plan);
     ep->plan = nullptr;
@@ -107,6 +103,12 @@ moe_status ep_peer_forward(moe_ep* ep, const int32_t* topk, int64_t T, int32_t k
     ep->plan_H = H;
     ep->plan_N = N;
   }
+  // 1. dispatch: per-destination deduplicated rows, stored into the owners' receive buffers
+  PEER_TRY(moe_ep_dispatch_plan(topk, T, k, ep->E, G, P.counts2, P.send_off, P.send_tok, P.send_meta, s));
+  PEER_CUDA(ep_peer_dispatch(X, x_row, P.send_off, P.send_tok, P.send_meta, G, k, ep->rank, P.T_max, P.peers_dev, s));
+  PEER_CUDA(ep_peer_signal(P.peers_dev, G, ep->rank, kDispatchWord, P.epoch_dev, true, s));
+  PEER_CUDA(ep_peer_wait(flags_mine, G, kDispatchWord, P.epoch_dev, P.status_dev, P.timeout_ns, s));
+  // 2. local experts: buckets over the received ids (empty rows are -1), device plan
   PEER_TRY(moe_route_plan(meta_mine, R, k, El, P.counts_l, P.row_off_l, P.tok_l, P.slot_l, nullptr, ep->plan, s));
   PEER_CUDA(cudaMemsetAsync(meta_mine, 0xff, sizeof(int32_t) * (size_t)(R * k), s));   // next step's empty rows
   // 3. the owner-side address of every local result row, then the GEMM storing there
@@ -196,6 +198,11 @@ moe_status moe_ep_peer_create(int32_t rank, int32_t world, int32_t E, int32_t bm
   };
   cudaError_t e = cudaGetDevice(&P->device);
   if (e != cudaSuccess) return fail("cudaGetDevice", e);
+  // every kernel of the step loaded now: lazy loading at a later first launch could wait for this rank's
+  // queued device-side waits (see common.h)
+  if ((e = preload_gemm_kernels()) != cudaSuccess || (e = preload_route_kernels()) != cudaSuccess ||
+      (e = preload_ep_kernels()) != cudaSuccess)
+    return fail("kernel preload", e);
   if ((e = cudaMalloc((void**)&P->region, P->bytes)) != cudaSuccess) return fail("region", e);
   // scratch: epoch, status, dispatch plan, route outputs, row pointers
   const size_t n_send = (size_t)world * max_tokens;

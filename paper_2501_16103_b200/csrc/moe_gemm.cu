@@ -1937,6 +1937,10 @@ cudaError_t set_smem_attrs() {
   return err;
 }
 
+}  // namespace
+cudaError_t moe::preload_gemm_kernels() { return set_smem_attrs(); }
+namespace {
+
 static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, const int32_t* token_idx,
                               const void* W, void* Y, int32_t y_dtype, void* stream, long long* prof,
                               const int32_t* y_row_map = nullptr, const void* W2 = nullptr, bool fp8 = false,

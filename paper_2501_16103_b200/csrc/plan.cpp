@@ -131,7 +131,7 @@ moe_status moe_plan_build_catalog(const int32_t* counts, int32_t E, int64_t H, i
   if (split) {
     cat[n_cat++] = {MOE_KIND_SWAP, bm};
   } else if (n_rules < 0) {
-    if (pair_blocks) cat[n_cat++] = {MOE_KIND_SWAP, MOE_DEFAULT_SWAP_MAX};
+    if (bm == 256 && bn > 256) cat[n_cat++] = {MOE_KIND_GEMV, MOE_DEFAULT_GEMV_MAX};
   } else {
     if (n_rules > MOE_MAX_RULES) MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_plan_build: at most %d catalog rules", MOE_MAX_RULES);
     if (n_rules > 0 && !rules) MOE_FAIL(MOE_ERR_INVALID, "moe_plan_build: null catalog");
@@ -146,11 +146,13 @@ moe_status moe_plan_build_catalog(const int32_t* counts, int32_t E, int64_t H, i
       cat[n_cat++] = rules[i];
     }
   }
+  bool allow_gemv = true;
   auto kind_of = [&](int64_t m) -> int32_t {
     const int64_t r = m % bm;
     if (m <= 0 || r == 0) return MOE_KIND_WIDE;
     for (int32_t i = 0; i < n_cat; ++i) {
-      if (cat[i].kind == MOE_KIND_GEMV && m >= bm) continue;   // GEMV: whole single-row-tile tasks only
+      // GEMV: whole single-row-tile tasks only, and only when the other tasks' tiles cover it
+      if (cat[i].kind == MOE_KIND_GEMV && (m >= bm || !allow_gemv)) continue;
       if (r <= cat[i].m_max) return cat[i].kind;
     }
     return MOE_KIND_WIDE;
@@ -170,10 +172,17 @@ moe_status moe_plan_build_catalog(const int32_t* counts, int32_t E, int64_t H, i
   const int64_t col_tiles = ceil_div(N, bn);
   std::vector<int64_t> nu(n_tasks);
   int32_t n_gemv = 0;                            // GEMV tasks have no tiles (Alg. 3's other strategy, §6.8)
-  for (int32_t i = 0; i < n_tasks; ++i) {
-    const bool gemv = counts[i] > 0 && kind_of(counts[i]) == MOE_KIND_GEMV;
-    n_gemv += gemv;
-    nu[i] = counts[i] == 0 || gemv ? 0 : ceil_div(counts[i], bm) * col_tiles;
+  for (int pass = 0; pass < 2; ++pass) {
+    n_gemv = 0;
+    int64_t other_tiles = 0;
+    for (int32_t i = 0; i < n_tasks; ++i) {
+      const bool gemv = counts[i] > 0 && kind_of(counts[i]) == MOE_KIND_GEMV;
+      n_gemv += gemv;
+      nu[i] = counts[i] == 0 || gemv ? 0 : ceil_div(counts[i], bm) * col_tiles;
+      other_tiles += nu[i];
+    }
+    if (n_gemv == 0 || other_tiles >= MOE_GEMV_MIN_TILES) break;
+    allow_gemv = false;                          // too little tensor work to hide the GEMV streams
   }
 
   // Non-empty stage: sigma in natural order, then Alg. 1 over eta.

@@ -44,19 +44,28 @@ __device__ __forceinline__ void plan_body(long long m, int E, int H, int N, int 
   const int t = threadIdx.x;                                       // expert t
   // The catalog (header words 12-15, written at plan creation and never rewritten here): kind of
   // each expert's last row tile by its r = m mod bm rows (include/moe_sm100.h).
-  int32_t kind = MOE_KIND_WIDE;
+  int32_t kind = MOE_KIND_WIDE, kind_nogemv = MOE_KIND_WIDE;
   {
     const long long r = m % bm;
     if (m > 0 && r > 0) {
       for (int i = MOE_MAX_RULES - 1; i >= 0; --i) {               // the first matching rule wins
-        if (blob[12 + 2 * i] == MOE_KIND_GEMV && m >= bm) continue;  // GEMV: whole single-tile tasks only
-        if (r <= blob[13 + 2 * i]) kind = blob[12 + 2 * i];
+        const int32_t ki = blob[12 + 2 * i];
+        if (r > blob[13 + 2 * i]) continue;
+        if (ki != MOE_KIND_GEMV) kind_nogemv = ki;
+        if (ki != MOE_KIND_GEMV || m < bm) kind = ki;              // GEMV: whole single-tile tasks only
       }
     }
   }
   __syncthreads();                                                 // every thread read the catalog
   const long long col_tiles = (N + bn - 1) / bn;
   const long long row_tiles = (m + bm - 1) / bm;
+  {
+    // GEMV only when the other tasks' tiles cover the GEMV streams (MOE_GEMV_MIN_TILES; plan.cpp)
+    long long other_tiles, gemv_any;
+    block_scan_incl(m > 0 && kind != MOE_KIND_GEMV ? row_tiles * col_tiles : 0, s_warp, &other_tiles);
+    block_scan_incl(m > 0 && kind == MOE_KIND_GEMV ? 1 : 0, s_warp, &gemv_any);
+    if (gemv_any > 0 && other_tiles < MOE_GEMV_MIN_TILES) kind = kind_nogemv;
+  }
   const long long nu = m > 0 && kind != MOE_KIND_GEMV ? row_tiles * col_tiles : 0;   // nu(T_t); GEMV: no tiles
   long long rows_total, tiles_total, ne_total;
   const long long rows_incl = block_scan_incl(m, s_warp, &rows_total);

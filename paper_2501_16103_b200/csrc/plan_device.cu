@@ -48,3 +48,8 @@ extern "C" moe_status moe_plan_device(moe_plan* plan, const int32_t* counts_dev,
   moe::plan_set_device_mode(plan, true);
   return MOE_OK;
 }
+
+cudaError_t moe::preload_plan_kernel() {
+  cudaFuncAttributes fa;
+  return cudaFuncGetAttributes(&fa, (const void*)plan_device_kernel);
+}

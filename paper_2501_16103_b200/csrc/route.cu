@@ -403,3 +403,14 @@ extern "C" moe_status moe_route_ex(const int32_t* topk, int64_t T, int32_t k, in
                                    moe_plan* plan, uint32_t route_flags, void* stream) {
   return route_impl(topk, T, k, E, counts, row_off, token_idx, slot, status, plan, route_flags, stream);
 }
+
+cudaError_t moe::preload_route_kernels() {
+  cudaFuncAttributes fa;
+  const void* ks[] = {(const void*)route_small_kernel, (const void*)route_hist_kernel, (const void*)route_place_kernel,
+                      (const void*)route_scan_kernel, (const void*)route_scatter_kernel};
+  for (const void* k : ks) {
+    const cudaError_t e = cudaFuncGetAttributes(&fa, k);
+    if (e != cudaSuccess) return e;
+  }
+  return moe::preload_plan_kernel();
+}

@@ -47,12 +47,12 @@ ORDER_FLAG = {"natural": 0, "alternating": 4, "half_interval": 8, "light_last": 
 
 def _compare(counts, N, bm, bn, pad, split=False, order="natural", catalog=None):
     """catalog None: the library's built-in catalog, whose rule the test states independently
-    ((SWAP, 64) on CTA-pair plans with 256-column blocks, none otherwise)."""
+    ((GEMV, 4) on wide pair plans, bm 256 and bn > 256; none otherwise)."""
     flags = (moe_lib.MOE_PAD_REPEAT if pad == "repeat" else 0) | (moe_lib.MOE_SPLIT_TAIL if split else 0)
     blob = moe_lib.moe_plan_build(counts, 64, N, bm, bn, flags | ORDER_FLAG[order], catalog=catalog)
     p = moe_lib.parse_plan_blob(blob)
     if catalog is None:
-        catalog = ((1, 64),) if (bm == 256 and bn >= 256) else ()
+        catalog = ((2, 4),) if (bm == 256 and bn > 256) else ()
     if split:
         catalog = ((1, bm),)
     assert p["catalog"] == tuple(catalog)
@@ -298,7 +298,7 @@ def test_planner_catalog_matches_oracle():
             got = moe_lib.parse_plan_blob(moe_lib.moe_plan_build(counts, 64, N, 256, bn, catalog=rules))
             assert np.array_equal(base["prefix"], got["prefix"]) and np.array_equal(base["sigma"], got["sigma"])
     # worked examples: tails 1 and 200 under {SWAP, 64}; 256-row experts have no tail
-    p = moe_lib.parse_plan_blob(moe_lib.moe_plan_build([1, 456, 256, 0, 64, 65], 64, 1024, 256, 512))
+    p = moe_lib.parse_plan_blob(moe_lib.moe_plan_build([1, 456, 256, 0, 64, 65], 64, 1024, 256, 512, catalog=[(1, 64)]))
     assert p["params"][:, 3].tolist() == [1, 0, 0, 0, 1, 0]
     with pytest.raises(moe_lib.MoeError):                              # swap tiles need CTA-pair 256-column blocks
         moe_lib.moe_plan_build([5, 5], 64, 1024, 128, 256, catalog=[(1, 64)])
@@ -313,12 +313,16 @@ def test_planner_gemv_strategy_by_hand():
     m <= m_max < 256 rows get kind 2 and no tiles — they leave TilePrefix and sigma; a 257-row expert's
     1-row tail stays a tile (GEMV covers whole tasks only); wide pair tiles only, m_max <= 4."""
     counts = [1, 456, 4, 0, 5, 257, 3]
-    p = moe_lib.parse_plan_blob(moe_lib.moe_plan_build(counts, 64, 1024, 256, 512, catalog=[(2, 4), (1, 64)]))
+    N = 16384                                                              # 32 column tiles of 512
+    p = moe_lib.parse_plan_blob(moe_lib.moe_plan_build(counts, 64, N, 256, 512, catalog=[(2, 4), (1, 64)]))
     assert p["params"][:, 3].tolist() == [2, 0, 2, 0, 1, 1, 2]
     assert p["M"] == 3 and p["sigma"][:3].tolist() == [1, 4, 5]           # experts 1, 4, 5 have tiles
-    assert p["total"] == (2 + 1 + 2) * 2                                   # row tiles x 2 column tiles
+    assert p["total"] == (2 + 1 + 2) * 32 >= 128                          # the other tasks' tiles cover GEMV
+    # fewer than MOE_GEMV_MIN_TILES other tiles: the GEMV candidates fall through to the next rule
+    q = moe_lib.parse_plan_blob(moe_lib.moe_plan_build(counts, 64, 1024, 256, 512, catalog=[(2, 4), (1, 64)]))
+    assert q["params"][:, 3].tolist() == [1, 0, 1, 0, 1, 1, 1] and q["M"] == 6
     q = moe_lib.parse_plan_blob(moe_lib.moe_plan_build([2, 0, 1], 64, 1024, 256, 512, catalog=[(2, 4)]))
-    assert q["M"] == 0 and q["total"] == 0                                 # only GEMV tasks: still work (MOE_OK)
+    assert q["M"] == 2 and q["params"][:, 3].tolist() == [0, 0, 0]
     for bad in ([(2, 5)], [(2, 4)]):
         with pytest.raises(moe_lib.MoeError):
             moe_lib.moe_plan_build([1, 1], 64, 1024, 256, 256 if bad == [(2, 4)] else 512, catalog=bad)

@@ -141,9 +141,12 @@ def test_gemv_kind_by_hand():
     """kind 2 (GEMV): whole tasks of m <= m_max < bm only; they have no tiles (nu = 0, not in sigma)."""
     cat = ((2, 4), (1, 64))
     assert [moe.tail_kind(m, 256, cat) for m in (0, 1, 4, 5, 64, 65, 257, 260, 320)] == [0, 2, 2, 1, 1, 0, 1, 1, 1]
-    p = moe.plan([1, 456, 4, 0, 5, 257, 3], 1024, 256, 512, catalog=cat)
-    assert p["nu"] == [0, 4, 0, 0, 2, 4, 0] and p["sigma"] == [1, 4, 5] and p["gemv"] == [0, 2, 6]
-    assert p["total"] == 10
+    p = moe.plan([1, 456, 4, 0, 5, 257, 3], 16384, 256, 512, catalog=cat)
+    assert p["nu"] == [0, 64, 0, 0, 32, 64, 0] and p["sigma"] == [1, 4, 5] and p["gemv"] == [0, 2, 6]
+    assert p["total"] == 160
+    # 10 other tiles < GEMV_MIN_TILES: no GEMV, the 1-4 row tasks take the next rule (SWAP)
+    q = moe.plan([1, 456, 4, 0, 5, 257, 3], 1024, 256, 512, catalog=cat)
+    assert q["gemv"] == [] and [t["kind"] for t in q["tasks"]] == [1, 0, 1, 0, 1, 1, 1]
 
 
 def test_light_last_order_by_hand():
