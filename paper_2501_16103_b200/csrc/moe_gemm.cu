@@ -318,7 +318,10 @@ __device__ __forceinline__ void wait_timed(uint32_t bar, uint32_t parity, long l
 // W rows are prefetched into L2 kGemvPf rounds ahead (no registers held for bytes in flight).
 // ---------------------------------------------------------------------------
 constexpr int kGemvCols = 128;
-constexpr int kGemvPf = 6;
+#ifndef MOE_GEMV_PF
+#define MOE_GEMV_PF 6
+#endif
+constexpr int kGemvPf = MOE_GEMV_PF;   // rounds of W rows prefetched into L2 ahead (0: none)
 
 template <bool kFp8>
 struct GemvUnit {
@@ -1169,7 +1172,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool colok = gu.col0 < a.N;
         const uint8_t* wbase = a.W + ((size_t)gu.expert * a.H) * a.N * esz_in + (size_t)gu.col0 * esz_in;
         // L2 prefetch of the rows kGemvPf rounds ahead (one 128-byte line per lane pair ... per row)
-        {
+        if (kGemvPf > 0) {
           const int kp = kr + 16 * kGemvPf;
           if (colok && kp < a.H && (lane & 7) == 0)
             for (int i = 0; i < 8; ++i) prefetch_l2(wbase + (size_t)(kp + i) * a.N * esz_in);

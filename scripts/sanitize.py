@@ -1,7 +1,8 @@
 #!/usr/bin/env python
 """Small invocations of every kernel family for compute-sanitizer (memcheck / racecheck / synccheck):
 route (small + multi-kernel), device plan, bf16 GEMM (1-CTA, pair, wide, split tail, decode tile,
-CSR rows), FP8 GEMM (1-CTA, wide), the FFN layer's gated GEMM + combine, checked against the oracle."""
+CSR rows), FP8 GEMM (1-CTA, wide), the FFN layer's gated GEMM + combine, GEMV tasks, split-K decode tiles,
+the light-last merge, the loopback and peer-memory EP steps, checked against the oracle."""
 import os
 import sys
 
@@ -82,8 +83,42 @@ def main():
     [t.start() for t in th]
     [t.join() for t in th]
     assert np.array_equal(torch.cat([o.cpu() for o in outs]).double().numpy(), omoe.per_slot_outputs(ide, Xe, We))
+    # round 2: GEMV tasks in a wide plan (>= 128 other tiles), split-K one-CTA tiles, light-last order
+    # with the dynamic merge, the peer-memory EP step (2 virtual ranks, one thread)
+    Tg, Eg, Hg, Ng = 300, 12, 128, 16384
+    idg = np.zeros((Tg, 2), dtype=np.int32)
+    for i, e in enumerate(range(2, Eg)):
+        idg[i] = [e, 0]
+    for t in range(Eg - 2, Tg):
+        idg[t] = [0, 1] if t % 2 else [1, 0]
+    Xg, Wg2 = synth.make_x(6, Tg, Hg, "int"), synth.make_w(6, Eg, Hg, Ng, "int")
+    cg, rg, tg_, _ = omoe.buckets(idg, Eg)
+    for fl in (0, M.MOE_ORDER_LIGHT_LAST):
+        Yg, *_ = M.moe_forward(torch.from_numpy(idg).cuda(), torch.from_numpy(Xg).to(torch.bfloat16).cuda(),
+                               torch.from_numpy(Wg2).to(torch.bfloat16).cuda(), Eg,
+                               plan=M.Plan(None, Hg, Ng, 256, 512, fl, E=Eg), out_dtype=torch.float32)
+        torch.cuda.synchronize()
+        assert np.array_equal(Yg.cpu().double().numpy(), omoe.expert_gemm(Xg, Wg2, tg_, rg)), fl
+    Ys, *_ = M.moe_forward(torch.from_numpy(idd).cuda(), torch.from_numpy(Xq).to(torch.bfloat16).cuda(),
+                           torch.from_numpy(Wq).to(torch.bfloat16).cuda(), 8,
+                           plan=M.Plan(None, Hd, Nd, 128, 256, M.MOE_SPLIT_K, E=8), out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    assert np.array_equal(Ys.cpu().double().numpy(), omoe.expert_gemm(Xq, Wq, t3, r3))
+    peers = M.PeerExpertParallel.group(G, 8, [torch.from_numpy(We[4 * r:4 * r + 4]).to(torch.bfloat16).cuda()
+                                              for r in range(G)], max_tokens=Tl, k=2)
+    pouts = [torch.empty((Tl * 2, 256), device="cuda") for _ in range(G)]
+    pst = [torch.cuda.Stream() for _ in range(G)]
+    torch.cuda.synchronize()
+    for r in range(G):
+        with torch.cuda.stream(pst[r]):
+            peers[r].forward(torch.from_numpy(np.ascontiguousarray(ide[r * Tl:(r + 1) * Tl])).cuda(),
+                             torch.from_numpy(Xe[r * Tl:(r + 1) * Tl]).to(torch.bfloat16).cuda(), out=pouts[r])
+    torch.cuda.synchronize()
+    assert [p_.status() for p_ in peers] == [0] * G
+    assert np.array_equal(torch.cat([o.cpu() for o in pouts]).double().numpy(), omoe.per_slot_outputs(ide, Xe, We))
     print(f"sanitize workload ok: {n} GEMM variants + CSR rows + both route paths + FFN layer + balanced decode "
-          f"grid + EP step (loopback, fused combine)")
+          f"grid + EP step (loopback, fused combine) + GEMV tasks (natural, light-last) + split-K decode tiles + "
+          f"peer-memory EP step")
 
 
 if __name__ == "__main__":
