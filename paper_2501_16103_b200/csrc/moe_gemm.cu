@@ -315,13 +315,14 @@ __device__ __forceinline__ void wait_timed(uint32_t bar, uint32_t parity, long l
 // tensor cores compute the other tasks' tiles.  A unit = one task x 128 output columns x all of K, owned
 // by one warp: lanes 0-15 take K rows k..k+7, lanes 16-31 rows k+8..k+15 of each 16-row round, lane l
 // columns 8 (l mod 16) + [0, 8); fp32 accumulation in registers, the two half-warps summed at the end.
-// W rows are prefetched into L2 kGemvPf rounds ahead (no registers held for bytes in flight).
+// A round loads 16 W rows per batch (4 KB per warp in flight) and accumulates them; an L2 prefetch of rows
+// further ahead measured slower (paper worst 0.811 / 0.724 of peak at 6 / 16 rounds ahead vs 0.830 without).
 // ---------------------------------------------------------------------------
 constexpr int kGemvCols = 128;
-#ifndef MOE_GEMV_PF
-#define MOE_GEMV_PF 6
+#ifndef MOE_GEMV_BATCH
+#define MOE_GEMV_BATCH 1
 #endif
-constexpr int kGemvPf = MOE_GEMV_PF;   // rounds of W rows prefetched into L2 ahead (0: none)
+constexpr int kGemvBatch = MOE_GEMV_BATCH;   // 16-row batches per round
 
 template <bool kFp8>
 struct GemvUnit {
@@ -1168,45 +1169,43 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int i = 0; i < 8; ++i) gu.acc[t][i] = 0.f;
         }
-        const int kr = gu.kpos + 8 * (lane >> 4);
         const bool colok = gu.col0 < a.N;
         const uint8_t* wbase = a.W + ((size_t)gu.expert * a.H) * a.N * esz_in + (size_t)gu.col0 * esz_in;
-        // L2 prefetch of the rows kGemvPf rounds ahead (one 128-byte line per lane pair ... per row)
-        if (kGemvPf > 0) {
-          const int kp = kr + 16 * kGemvPf;
-          if (colok && kp < a.H && (lane & 7) == 0)
-            for (int i = 0; i < 8; ++i) prefetch_l2(wbase + (size_t)(kp + i) * a.N * esz_in);
-        }
-        if (colok && kr < a.H) {
-          uint4 wv[8];
+        // a round = kGemvBatch batches of 16 K rows: batch b, half-warp h takes rows kpos + 16 b + 8 h + [0, 8)
+        const int64_t xrow = (int64_t)a.H * esz_in;
 #pragma unroll
-          for (int i = 0; i < 8; ++i) wv[i] = GemvUnit<kFp8>::load8(wbase + (size_t)(kr + i) * a.N * esz_in);
-          const int64_t xrow = (int64_t)a.H * esz_in;
+        for (int b = 0; b < kGemvBatch; ++b) {
+          const int kr = gu.kpos + 16 * b + 8 * (lane >> 4);
+          if (colok && kr < a.H) {
+            uint4 wv[8];
 #pragma unroll
-          for (int t = 0; t < MOE_GEMV_MAX_ROWS; ++t) {
-            if (t < gu.rows) {
-              const int tok = a.token_idx ? __ldg(a.token_idx + gu.row0 + t) : gu.row0 + t;
-              const uint8_t* xp = reinterpret_cast<const uint8_t*>(a.X) + tok * xrow + (int64_t)kr * esz_in;
-              uint4 xq;
-              if constexpr (kFp8) {
-                const uint2 v2 = __ldg(reinterpret_cast<const uint2*>(xp));
-                xq = make_uint4(v2.x, v2.y, 0u, 0u);
-              } else {
-                xq = __ldg(reinterpret_cast<const uint4*>(xp));
-              }
-              float xf[8];
-              GemvUnit<kFp8>::widen(xq, xf);
+            for (int i = 0; i < 8; ++i) wv[i] = GemvUnit<kFp8>::load8(wbase + (size_t)(kr + i) * a.N * esz_in);
 #pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                float wf[8];
-                GemvUnit<kFp8>::widen(wv[i], wf);
+            for (int t = 0; t < MOE_GEMV_MAX_ROWS; ++t) {
+              if (t < gu.rows) {
+                const int tok = a.token_idx ? __ldg(a.token_idx + gu.row0 + t) : gu.row0 + t;
+                const uint8_t* xp = reinterpret_cast<const uint8_t*>(a.X) + tok * xrow + (int64_t)kr * esz_in;
+                uint4 xq;
+                if constexpr (kFp8) {
+                  const uint2 v2 = __ldg(reinterpret_cast<const uint2*>(xp));
+                  xq = make_uint4(v2.x, v2.y, 0u, 0u);
+                } else {
+                  xq = __ldg(reinterpret_cast<const uint4*>(xp));
+                }
+                float xf[8];
+                GemvUnit<kFp8>::widen(xq, xf);
 #pragma unroll
-                for (int c = 0; c < 8; ++c) gu.acc[t][c] = fmaf(xf[i], wf[c], gu.acc[t][c]);
+                for (int i = 0; i < 8; ++i) {
+                  float wf[8];
+                  GemvUnit<kFp8>::widen(wv[i], wf);
+#pragma unroll
+                  for (int c = 0; c < 8; ++c) gu.acc[t][c] = fmaf(xf[i], wf[c], gu.acc[t][c]);
+                }
               }
             }
           }
         }
-        gu.kpos += 16;
+        gu.kpos += 16 * kGemvBatch;
         if (gu.kpos >= a.H) {                       // unit done: sum the two half-warps, store the rows
           float sc = 1.f;
           if constexpr (kFp8) sc = a.scale ? __ldg(a.scale + gu.expert) : 1.f;

@@ -49,3 +49,43 @@ def test_oracle_sample_fp8_bounded():
     import synth
     f, s, sample, cores = bench.oracle_sample(synth.CONFIGS["tiny"], 0, 0.01, fp8=True)
     assert f > 0 and s > 0 and "E4M3" in sample and cores >= 1
+
+
+def test_gpus_flag_self_launches_one_rank_per_gpu(monkeypatch):
+    """`bench.py --gpus N` without torchrun re-launches itself as N ranks (torch.distributed.run, one
+    process per GPU, rendezvous on 127.0.0.1) and returns their exit code (--gpus was a label)."""
+    import bench
+    calls = []
+    monkeypatch.delenv("WORLD_SIZE", raising=False)
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4", "--steps", "2", "--warmup", "3"])
+    monkeypatch.setattr("subprocess.call", lambda cmd: calls.append(cmd) or 0)
+    with pytest.raises(SystemExit) as ex:
+        bench.main()
+    assert ex.value.code == 0 and len(calls) == 1
+    cmd = calls[0]
+    assert cmd[1:3] == ["-m", "torch.distributed.run"] and "--nproc-per-node=4" in cmd and "--nnodes=1" in cmd
+    assert cmd[cmd.index("--master-addr") + 1] == "127.0.0.1"
+    assert cmd[-6:] == ["--gpus", "4", "--steps", "2", "--warmup", "3"] and cmd[-7].endswith("bench.py")
+
+
+def test_gpus_flag_must_match_world_size(monkeypatch):
+    import bench
+    monkeypatch.setenv("WORLD_SIZE", "2")
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4"])
+    with pytest.raises(SystemExit) as ex:
+        bench.main()
+    assert "WORLD_SIZE=2" in str(ex.value.code)
+
+
+def test_ep_config_same_for_both_arms():
+    """At N > 1 the reference arm prints the config our arm prints (the driver compares them)."""
+    import argparse
+
+    import bench
+    import synth
+    args = argparse.Namespace(bm=0, bn=0, out_dtype="bf16", seed=0, dtype="bf16", ep=False, gpus=8)
+    c = bench.ref_config(synth.CONFIGS["mix"], args, 8)
+    assert c == bench.ep_config(synth.CONFIGS["mix"], 8, args)
+    assert c["workload"].startswith("mix-ep8: E=8 top-2 T=32768 (4096/rank)") and c["parallelism"] == "ep8"
+    s = bench.ep_config(synth.CONFIGS["ep"], 8, args)
+    assert "T=32768 (4096/rank)" in s["workload"]                        # 8x22B: strong scaling, total T fixed
