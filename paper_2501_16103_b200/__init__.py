@@ -277,12 +277,6 @@ class Plan:
     def total_tiles(self) -> int:
         return self.query()[1]
 
-    @property
-    def has_work(self) -> bool:
-        """Tiles or GEMV tasks (a GEMV launch has no tiles, §6.9): moe_gemm launches iff this is true."""
-        p = parse_plan_blob(self.blob())
-        return p["total"] > 0 or bool(((p["params"][:, 3] == MOE_KIND_GEMV) & (p["params"][:, 2] > 0)).any())
-
     def blob(self) -> np.ndarray:
         n = ctypes.c_int64()
         _check(lib().moe_plan_blob(self._h, None, 0, ctypes.byref(n)))

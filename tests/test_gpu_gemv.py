@@ -77,15 +77,14 @@ def test_gemv_integer_bit_exact(shape, device_plan):
 
 
 def test_gemv_below_min_tiles_falls_through():
-    """1-4 row experts next to one 9-row expert: not a GEMV launch (one task has > 4 rows) and far fewer
-    than MOE_GEMV_MIN_TILES other tiles to hide GEMV streams under, so the GEMV rule does not apply and
-    every task runs as tiles; exact either way."""
-    T, E, k, H, N = 28, 16, 1, 256, 768
-    ids = np.concatenate([np.arange(20) % E, np.zeros(8, dtype=np.int64)]).astype(np.int32)[:, None]
+    """Every expert has 1-4 rows: no tiles would cover the GEMV streams (< MOE_GEMV_MIN_TILES), so the
+    GEMV rule does not apply and the tasks run as tiles; exact either way."""
+    T, E, k, H, N = 20, 16, 1, 256, 768
+    ids = (np.arange(T, dtype=np.int32) % E)[:, None]
     X, W = synth.make_x(3, T, H, "int"), synth.make_w(3, E, H, N, "int")
     Xd, Wd = torch.from_numpy(X).to(torch.bfloat16).cuda(), torch.from_numpy(W).to(torch.bfloat16).cuda()
     (Y,), plan, counts = _run(ids, Xd, Wd, E, False)
-    assert counts.max() > 4 and plan.total_tiles == (counts > 0).sum() * 2
+    assert plan.total_tiles > 0 and counts.max() <= 4
     rc, rr, rt, _ = omoe.buckets(ids, E)
     assert np.array_equal(Y.cpu().double().numpy(), omoe.expert_gemm(X, W, rt, rr))
 

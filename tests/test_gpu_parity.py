@@ -608,7 +608,7 @@ def test_gemm_fuzz_tile_variants(case):
     contiguous = case % 3 == 0
     Xin = Xd.index_select(0, tok.long()).contiguous() if contiguous else Xd
     Y = torch.full((tok.numel(), N), float("nan"), dtype=out, device="cuda")
-    if plan.has_work:
+    if plan.total_tiles:
         M.moe_gemm(plan, Xin, None if contiguous else tok, Wd, Y=Y)
     torch.cuda.synchronize()
     got = Y.cpu().double().numpy()
