@@ -78,9 +78,6 @@ typedef int32_t moe_status;
                                    launches on one plan must be stream-ordered (the counter is reset
                                    by the launch's last CTA pair)                                     */
 
-#define MOE_NO_GEMV_LAUNCH 8192u /* keep tiles when every task has <= MOE_GEMV_MAX_ROWS rows (by default such a
-                                   plan is a GEMV launch: every task MOE_KIND_GEMV, no tiles, all SMs stream
-                                   W with 16-byte loads — a decode step)              */
 #define MOE_SPLIT_K  1024u      /* one-CTA tiles: when whole tiles would leave SMs idle and every task has
                                    <= 16 rows, split each tile's K blocks into S parts over one CTA per SM
                                    and sum them in K order (opt-in: measured slower than whole tiles on the

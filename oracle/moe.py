@@ -71,7 +71,6 @@ def tiles_of(rows: int, N: int, bm: int, bn: int) -> int:
 
 KIND_GEMV = 2   # a whole task of <= m_max rows computed as a CUDA-core GEMV, outside the tile space
 GEMV_MIN_TILES = 128
-GEMV_MAX_ROWS = 4
 
 
 def tail_kind(m: int, bm: int, catalog) -> int:
@@ -147,8 +146,7 @@ def order_tasks(loads: list[int], strategy: str) -> list[int]:
 
 
 def plan(counts, N: int, bm: int, bn: int, pad_mode: str = "max", warp_size: int = 32,
-         tasks: list[dict] | None = None, split_tail: bool = False, order: str = "natural", catalog=(),
-         gemv_launch: bool = True) -> dict:
+         tasks: list[dict] | None = None, split_tail: bool = False, order: str = "natural", catalog=()) -> dict:
     """Host-side plan: nu per task, sigma (non-empty tasks, natural order or a §4.2
     ordering), TilePrefix (Alg. 1 over eta in sigma's order), padded per P:203."""
     if tasks is None:
@@ -158,11 +156,6 @@ def plan(counts, N: int, bm: int, bn: int, pad_mode: str = "max", warp_size: int
         other = sum(tiles_of(t["rows"], N, t["bm"], t["bn"]) for t in tasks if t["kind"] != KIND_GEMV)
         if any(t["kind"] == KIND_GEMV for t in tasks) and other < GEMV_MIN_TILES:
             tasks = make_tasks(counts, bm, bn, split_tail, [r for r in catalog if int(r[0]) != KIND_GEMV])
-        # a GEMV launch: every non-empty task has <= GEMV_MAX_ROWS rows -> all GEMV
-        ne = [t for t in tasks if t["rows"] > 0]
-        if gemv_launch and bm != 64 and ne and all(t["rows"] <= GEMV_MAX_ROWS for t in ne):
-            for t in ne:
-                t["kind"] = KIND_GEMV
     # Alg. 3's per-task strategies: a GEMV task has no tiles (nu = 0, so the non-empty stage leaves it out
     # of sigma / TilePrefix); its rows are computed by the GEMV strategy (R6, §6.8).
     nu = [0 if t.get("kind", 0) == KIND_GEMV else tiles_of(t["rows"], N, t["bm"], t["bn"]) for t in tasks]

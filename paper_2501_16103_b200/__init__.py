@@ -27,7 +27,6 @@ MOE_LIGHT_ROWS = 64
 MOE_GRID_BALANCED, MOE_GRID_STATIC, MOE_A_GATHER4, MOE_EPI_REGISTER, MOE_SCHED_DYNAMIC = 16, 32, 64, 128, 256
 MOE_L2_PREFETCH = 512
 MOE_SPLIT_K = 1024
-MOE_NO_GEMV_LAUNCH = 8192
 MOE_ROUTE_NO_SMALL, MOE_ROUTE_THREE_KERNELS = 1, 2
 MOE_KIND_WIDE, MOE_KIND_SWAP, MOE_MAX_RULES = 0, 1, 2
 MOE_DEFAULT_SWAP_MAX = 64                       # include/moe_sm100.h: the swap-AB rule of tests and A/B runs
@@ -443,8 +442,7 @@ class MoeFFN:
         assert W_down.shape == (self.E, self.I, W_down.shape[2])
         self.Ho = int(W_down.shape[2])
         self.Wg, self.Wu, self.Wd = W_gate, W_up, W_down
-        # the gated GEMM has no GEMV path: its plan keeps tiles for decode-sized batches
-        self.plan_gu = Plan(None, self.H, self.I, 256, 256, MOE_NO_GEMV_LAUNCH, stream=stream, E=self.E)
+        self.plan_gu = Plan(None, self.H, self.I, 256, 256, stream=stream, E=self.E)
         self.plan_dn = None
         self._torch = torch
 

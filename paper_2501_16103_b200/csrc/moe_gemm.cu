@@ -365,149 +365,6 @@ struct GemvUnit {
   }
 };
 
-// ---------------------------------------------------------------------------
-// A GEMV launch: every task has <= MOE_GEMV_MAX_ROWS rows (a decode step), so the plan
-// has no tiles and every CTA of the launch streams W with 16-byte loads (the path that reaches ~6.2 TB/s
-// over the chip; §6.5).  Units = (GEMV task, 8 output columns) in task order, CTA c of G takes units
-// [c U / G, (c + 1) U / G), at most 32 at a time; thread t works on unit t mod n over the K rows
-// k = s, s + S, ... (s = t / n, S = threads / n), 8 rows in flight, fp32 sums for up to 4 tokens; the S
-// partial sums of a unit are added in slice order through shared memory (deterministic) and stored.
-// ---------------------------------------------------------------------------
-template <bool kFp8>
-__device__ __forceinline__ void gemv_launch_body(const GemmArgs& a, const int32_t* params, uint8_t* smem) {
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int n_tasks = __ldg(a.plan + 9);
-  int32_t* s_list = reinterpret_cast<int32_t*>(smem);                 // [n_tasks] GEMV task ids
-  int32_t* s_cnt = s_list + n_tasks;                                   // [nt + 1] per-thread counts / offsets
-  float* s_red = reinterpret_cast<float*>(s_cnt + nt + 2);             // [S][n][8 * MOE_GEMV_MAX_ROWS]
-  // 1. the GEMV tasks in task order (block compaction)
-  const int per = (n_tasks + nt - 1) / nt;
-  auto is_gemv = [&](int i) {
-    return __ldg(params + i * MOE_PLAN_TASK_WORDS + 3) == MOE_KIND_GEMV && __ldg(params + i * MOE_PLAN_TASK_WORDS + 2) > 0;
-  };
-  int c = 0;
-  for (int i = tid * per; i < min(n_tasks, (tid + 1) * per); ++i) c += is_gemv(i);
-  s_cnt[tid] = c;
-  __syncthreads();
-  if (tid == 0) {
-    int acc = 0;
-    for (int i = 0; i < nt; ++i) {
-      const int x = s_cnt[i];
-      s_cnt[i] = acc;
-      acc += x;
-    }
-    s_cnt[nt] = acc;
-  }
-  __syncthreads();
-  {
-    int pos = s_cnt[tid];
-    for (int i = tid * per; i < min(n_tasks, (tid + 1) * per); ++i)
-      if (is_gemv(i)) s_list[pos++] = i;
-  }
-  const int n_gemv = s_cnt[nt];
-  __syncthreads();
-  const int esz = kFp8 ? 1 : 2;
-  const int ng = (a.N + 7) / 8;                                        // 8-column groups per task
-  const long long U = (long long)n_gemv * ng;
-  const long long u0 = (long long)blockIdx.x * U / gridDim.x, u1 = ((long long)blockIdx.x + 1) * U / gridDim.x;
-  const int64_t xrow = (int64_t)a.H * esz;
-  for (long long base = u0; base < u1; base += 32) {
-    const int n = (int)min(32LL, u1 - base);
-    const int S = nt / n;
-    const int g = tid % n, sl = tid / n;
-    float acc[MOE_GEMV_MAX_ROWS][8];
-#pragma unroll
-    for (int t = 0; t < MOE_GEMV_MAX_ROWS; ++t)
-#pragma unroll
-      for (int i = 0; i < 8; ++i) acc[t][i] = 0.f;
-    const long long u = base + g;
-    const int j = (int)(u / ng), col0 = (int)(u - (long long)j * ng) * 8;
-    const int task = s_list[j];
-    const int expert = __ldg(params + task * MOE_PLAN_TASK_WORDS + 0);
-    const int row0 = __ldg(params + task * MOE_PLAN_TASK_WORDS + 1);
-    const int rows = __ldg(params + task * MOE_PLAN_TASK_WORDS + 2);
-    int tok[MOE_GEMV_MAX_ROWS];
-#pragma unroll
-    for (int t = 0; t < MOE_GEMV_MAX_ROWS; ++t)
-      tok[t] = t < rows ? (a.token_idx ? __ldg(a.token_idx + row0 + t) : row0 + t) : 0;
-    if (sl < S) {
-      const uint8_t* wbase = a.W + (size_t)expert * a.H * a.N * esz + (size_t)col0 * esz;
-      for (int k0 = sl; k0 < a.H; k0 += 8 * S) {
-        uint4 wv[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int k = k0 + i * S;
-          wv[i] = k < a.H ? GemvUnit<kFp8>::load8(wbase + (size_t)k * a.N * esz) : make_uint4(0u, 0u, 0u, 0u);
-        }
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int k = k0 + i * S;
-          if (k >= a.H) break;
-          float wf[8];
-          GemvUnit<kFp8>::widen(wv[i], wf);
-#pragma unroll
-          for (int t = 0; t < MOE_GEMV_MAX_ROWS; ++t) {
-            if (t < rows) {
-              const uint8_t* xp = reinterpret_cast<const uint8_t*>(a.X) + tok[t] * xrow + (int64_t)k * esz;
-              float xv;
-              if constexpr (kFp8) {
-                uint32_t h2;
-                const uint16_t pair = (uint16_t)__ldg(xp);
-                asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h2) : "h"(pair));
-                xv = __half2float(__ushort_as_half((unsigned short)(h2 & 0xffffu)));
-              } else {
-                xv = __uint_as_float((uint32_t)__ldg(reinterpret_cast<const unsigned short*>(xp)) << 16);
-              }
-#pragma unroll
-              for (int cc = 0; cc < 8; ++cc) acc[t][cc] = fmaf(xv, wf[cc], acc[t][cc]);
-            }
-          }
-        }
-      }
-#pragma unroll
-      for (int t = 0; t < MOE_GEMV_MAX_ROWS; ++t)
-#pragma unroll
-        for (int cc = 0; cc < 8; ++cc) s_red[((size_t)sl * n + g) * (8 * MOE_GEMV_MAX_ROWS) + t * 8 + cc] = acc[t][cc];
-    }
-    __syncthreads();
-    // 2. thread (g, t): the S partials of unit g, token t, summed in slice order, stored
-    if (tid < n * MOE_GEMV_MAX_ROWS) {
-      const int g2 = tid / MOE_GEMV_MAX_ROWS, t = tid % MOE_GEMV_MAX_ROWS;
-      const long long u2 = base + g2;
-      const int j2 = (int)(u2 / ng), c0 = (int)(u2 - (long long)j2 * ng) * 8;
-      const int task2 = s_list[j2];
-      const int rows2 = __ldg(params + task2 * MOE_PLAN_TASK_WORDS + 2);
-      if (t < rows2 && c0 < a.N) {
-        float sum[8];
-#pragma unroll
-        for (int cc = 0; cc < 8; ++cc) sum[cc] = 0.f;
-        for (int s2 = 0; s2 < S; ++s2)
-#pragma unroll
-          for (int cc = 0; cc < 8; ++cc) sum[cc] += s_red[((size_t)s2 * n + g2) * (8 * MOE_GEMV_MAX_ROWS) + t * 8 + cc];
-        float sc = 1.f;
-        if constexpr (kFp8) sc = a.scale ? __ldg(a.scale + __ldg(params + task2 * MOE_PLAN_TASK_WORDS + 0)) : 1.f;
-        const int grow = __ldg(params + task2 * MOE_PLAN_TASK_WORDS + 1) + t;
-        uint8_t* yp = a.y_row_ptr ? reinterpret_cast<uint8_t*>(__ldg(a.y_row_ptr + grow))
-                                  : reinterpret_cast<uint8_t*>(a.Y) +
-                                        (a.y_row_map ? (int64_t)__ldg(a.y_row_map + grow) : (int64_t)grow) * a.N *
-                                            (a.y_f32 ? 4 : 2);
-        uint32_t r[8];
-#pragma unroll
-        for (int cc = 0; cc < 8; ++cc) r[cc] = __float_as_uint(kFp8 ? sum[cc] * sc : sum[cc]);
-        if (a.y_f32) {
-          float* y = reinterpret_cast<float*>(yp) + c0;
-          *reinterpret_cast<uint4*>(y) = make_uint4(r[0], r[1], r[2], r[3]);
-          *reinterpret_cast<uint4*>(y + 4) = make_uint4(r[4], r[5], r[6], r[7]);
-        } else {
-          *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(yp) + c0) =
-              make_uint4(pack_bf16(r[0], r[1]), pack_bf16(r[2], r[3]), pack_bf16(r[4], r[5]), pack_bf16(r[6], r[7]));
-        }
-      }
-    }
-    __syncthreads();
-  }
-}
-
 // Pipeline geometry per CTA-group size: a CTA pair (cta_group::2) splits the B block across the
 // two CTAs, so a stage is 32 KB instead of 48 KB and six stages fit.  A wide pair tile (256 x 512,
 // kWide) stages 128 rows + 256 W columns per CTA: 48 KB, four stages.
@@ -721,24 +578,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     return v < total;
   };
 
-  // A GEMV launch (§6.9): no tiles, GEMV tasks -> every thread of the CTA streams W (gated plans never)
-  bool gemv_launch = false;
-  if constexpr (!kGated) {
-    if (total == 0 && a.gemv_q != nullptr) {
-      __shared__ int s_any_gemv;
-      if (threadIdx.x == 0) s_any_gemv = 0;
-      __syncthreads();
-      const int n_tasks = __ldg(a.plan + 9);
-      for (int i = threadIdx.x; i < n_tasks; i += blockDim.x)
-        if (__ldg(params + i * MOE_PLAN_TASK_WORDS + 3) == MOE_KIND_GEMV && __ldg(params + i * MOE_PLAN_TASK_WORDS + 2) > 0)
-          s_any_gemv = 1;
-      __syncthreads();
-      gemv_launch = s_any_gemv != 0;
-    }
-  }
-  if (gemv_launch) {
-    gemv_launch_body<kFp8>(a, params, smem);
-  } else if (warp < kAWarps) {
+  if (warp < kAWarps) {
     // ===================== A producers: this CTA's 128 token rows, 64 columns per stage =====================
     // Gathered straight from X through the token-index array: no gathered copy of X.
     // a_mode 0 (1-CTA only): TMA tile::gather4 — warp p stages rows [32p, 32p+32), 4 rows per lane.
@@ -2131,8 +1971,6 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
     int64_t words = 0;
     const int32_t* blob = moe::plan_blob_host(plan, &words);
     if (dev_planned) {
-      // a device plan may turn out a GEMV launch (§6.9) or hold catalog GEMV tasks (§6.8)
-      has_gemv = !(v.flags & MOE_NO_GEMV_LAUNCH) && v.bm != kDecRows;
       for (int i = 0; i < MOE_MAX_RULES; ++i) has_gemv |= blob[12 + 2 * i] == MOE_KIND_GEMV && blob[13 + 2 * i] > 0;
     } else {
       if (!moe::blob_view(blob, words, &v)) MOE_FAIL(MOE_ERR_INVALID, "moe_gemm: corrupt plan");
@@ -2239,10 +2077,8 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
   a.sched = dynamic ? moe::plan_sched_dev(plan) : nullptr;
   a.light_merge = dynamic && (v.flags & MOE_ORDER_LIGHT_LAST) ? 1 : 0;
   a.gemv_q = has_gemv ? moe::plan_sched_dev(plan) + 2 : nullptr;
-  if (gated && has_gemv)
-    MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_gemm_swiglu: the plan may hold GEMV tasks (create it with MOE_NO_GEMV_LAUNCH)");
-  if (has_gemv && !dev_planned && v.total > 0 && !wide)
-    MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_gemm: GEMV tasks next to tiles need a wide pair tile plan (bm 256, bn > 256)");
+  if (has_gemv && !(wide && !gated))
+    MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_gemm: MOE_KIND_GEMV tasks need a wide pair tile plan (bm 256, bn > 256)");
   a.W = reinterpret_cast<const uint8_t*>(W);
   a.pf_dist = (v.flags & MOE_L2_PREFETCH) && v.N % 64 == 0 ? kL2Pf : 0;
   a.balance = a.sched ? 0 : (v.flags & MOE_GRID_BALANCED) ? 1 : (v.flags & MOE_GRID_STATIC) ? 0 : v.bm == 128;
@@ -2333,7 +2169,7 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
     if (le != cudaSuccess) MOE_FAIL(MOE_ERR_CUDA, "moe_gemm pair launch: %s", cudaGetErrorString(le));
   } else {
     // one CTA per SM when the kernel may choose stream-K (it spreads the K blocks over every CTA)
-    const int grid = v.total < 0 || a.sk_ws || has_gemv ? sm_count_cached() : std::min(v.total, sm_count_cached());
+    const int grid = v.total < 0 || a.sk_ws ? sm_count_cached() : std::min(v.total, sm_count_cached());
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kThreads);

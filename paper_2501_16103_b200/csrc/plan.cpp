@@ -112,8 +112,7 @@ moe_status moe_plan_build_catalog(const int32_t* counts, int32_t E, int64_t H, i
              "moe_plan_build: bn=%d must be a multiple of %d in [16, 256] (or of 32 in (256, 512] with bm=256)", bn,
              bm == 256 ? 32 : 16);
   if (flags & ~(MOE_PAD_REPEAT | MOE_SPLIT_TAIL | MOE_ORDER_ALTERNATING | MOE_ORDER_HALF_INTERVAL | MOE_ORDER_LIGHT_LAST | MOE_GRID_BALANCED |
-                MOE_GRID_STATIC | MOE_A_GATHER4 | MOE_EPI_REGISTER | MOE_SCHED_DYNAMIC | MOE_L2_PREFETCH | MOE_SPLIT_K |
-                MOE_NO_GEMV_LAUNCH))
+                MOE_GRID_STATIC | MOE_A_GATHER4 | MOE_EPI_REGISTER | MOE_SCHED_DYNAMIC | MOE_L2_PREFETCH | MOE_SPLIT_K))
     MOE_FAIL(MOE_ERR_INVALID, "moe_plan_build: unknown flags 0x%x", flags);
   if ((flags & MOE_GRID_BALANCED) && (flags & MOE_GRID_STATIC))
     MOE_FAIL(MOE_ERR_INVALID, "moe_plan_build: MOE_GRID_BALANCED and MOE_GRID_STATIC are exclusive");
@@ -173,21 +172,7 @@ moe_status moe_plan_build_catalog(const int32_t* counts, int32_t E, int64_t H, i
   const int64_t col_tiles = ceil_div(N, bn);
   std::vector<int64_t> nu(n_tasks);
   int32_t n_gemv = 0;                            // GEMV tasks have no tiles (Alg. 3's other strategy, §6.8)
-  // A GEMV launch (§6.9): every non-empty task has <= MOE_GEMV_MAX_ROWS rows -> all of them GEMV.
-  bool gemv_launch = false;
-  if (!(flags & MOE_NO_GEMV_LAUNCH) && bm != 64) {       // (the bm = 64 decode kernel has no GEMV path)
-    int32_t ne = 0, small = 0;
-    for (int32_t i = 0; i < n_tasks; ++i) {
-      ne += counts[i] > 0;
-      small += counts[i] > 0 && counts[i] <= MOE_GEMV_MAX_ROWS;
-    }
-    gemv_launch = ne > 0 && small == ne;
-  }
-  if (gemv_launch) {
-    for (int32_t i = 0; i < n_tasks; ++i) nu[i] = 0;
-    n_gemv = 1;
-  }
-  for (int pass = 0; pass < 2 && !gemv_launch; ++pass) {
+  for (int pass = 0; pass < 2; ++pass) {
     n_gemv = 0;
     int64_t other_tiles = 0;
     for (int32_t i = 0; i < n_tasks; ++i) {
@@ -280,7 +265,7 @@ moe_status moe_plan_build_catalog(const int32_t* counts, int32_t E, int64_t H, i
     p[0] = i;                                   // expert
     p[1] = (int32_t)row_off[i];                 // first CSR row of the task
     p[2] = counts[i];                           // rows
-    p[3] = gemv_launch && counts[i] > 0 ? MOE_KIND_GEMV : kind_of(counts[i]);   // the catalog's strategy
+    p[3] = kind_of(counts[i]);                  // kind of the last row tile (1: swap-AB, the catalog)
     p[4] = bm;
     p[5] = bn;
     p[6] = (int32_t)ceil_div(counts[i], bm);    // row tiles
@@ -500,12 +485,7 @@ moe_status moe_plan_sync(moe_plan* p, void* stream) {
   p->device_mode = false;
   if (p->blob[11] != 0)
     MOE_FAIL(MOE_ERR_CAPACITY, "moe_plan_device: rows or tiles >= 2^31 (device planner status %d)", p->blob[11]);
-  if (p->blob[1] > 0) return MOE_OK;
-  for (int32_t i = 0; i < v.n_tasks; ++i) {              // GEMV tasks have no tiles but are work
-    const int32_t* q = p->blob.data() + v.off_params + (int64_t)MOE_PLAN_TASK_WORDS * i;
-    if (q[3] == MOE_KIND_GEMV && q[2] > 0) return MOE_OK;
-  }
-  return MOE_OK_EMPTY;
+  return p->blob[1] == 0 ? MOE_OK_EMPTY : MOE_OK;
 }
 
 moe_status moe_plan_query(const moe_plan* p, int32_t* M, int32_t* total, int32_t* M_pad) {

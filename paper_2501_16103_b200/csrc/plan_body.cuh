@@ -61,14 +61,10 @@ __device__ __forceinline__ void plan_body(long long m, int E, int H, int N, int 
   const long long row_tiles = (m + bm - 1) / bm;
   {
     // GEMV only when the other tasks' tiles cover the GEMV streams (MOE_GEMV_MIN_TILES; plan.cpp)
-    long long other_tiles, gemv_any, ne_all, small_all;
+    long long other_tiles, gemv_any;
     block_scan_incl(m > 0 && kind != MOE_KIND_GEMV ? row_tiles * col_tiles : 0, s_warp, &other_tiles);
     block_scan_incl(m > 0 && kind == MOE_KIND_GEMV ? 1 : 0, s_warp, &gemv_any);
     if (gemv_any > 0 && other_tiles < MOE_GEMV_MIN_TILES) kind = kind_nogemv;
-    // a GEMV launch: every non-empty task has <= MOE_GEMV_MAX_ROWS rows (§6.9)
-    block_scan_incl(m > 0 ? 1 : 0, s_warp, &ne_all);
-    block_scan_incl(m > 0 && m <= MOE_GEMV_MAX_ROWS ? 1 : 0, s_warp, &small_all);
-    if (!(flags & MOE_NO_GEMV_LAUNCH) && bm != 64 && ne_all > 0 && small_all == ne_all && m > 0) kind = MOE_KIND_GEMV;
   }
   const long long nu = m > 0 && kind != MOE_KIND_GEMV ? row_tiles * col_tiles : 0;   // nu(T_t); GEMV: no tiles
   long long rows_total, tiles_total, ne_total;

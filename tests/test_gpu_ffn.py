@@ -38,7 +38,7 @@ def test_gemm_swiglu_matches_oracle(T, E, k, H, I):
     (Wg, Wu, _), (Wgd, Wud, _) = _weights(T, E, H, I, 64)
     Xd = torch.from_numpy(X).to(torch.bfloat16).cuda()
     counts, row_off, tok, slot, _ = M.moe_route(torch.from_numpy(ids).cuda(), E)
-    plan = M.Plan(counts.cpu().numpy(), H, I, 256, 256, M.MOE_NO_GEMV_LAUNCH)   # the gated GEMM has no GEMV path
+    plan = M.Plan(counts.cpu().numpy(), H, I, 256, 256)
     Y = torch.full((tok.numel(), I), float("nan"), dtype=torch.bfloat16, device="cuda")
     M.moe_gemm_swiglu(plan, Xd, tok, Wgd, Wud, Y=Y)
     torch.cuda.synchronize()

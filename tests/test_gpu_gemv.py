@@ -5,9 +5,7 @@ GEMVs between their accumulator drains, from a global unit queue.
 Checks against the fp64 oracle: integer inputs bit-exact (host- and device-planned, bf16 and
 fp32 Y, with swap-AB tails and whole tiles in the same launch, a plan of GEMV tasks only, three launches on
 one plan: the unit queue resets), FP8 codes bit-exact, the paper's §5 worst case at full size sampled within
-the north-star tolerance, and the EP row-pointer epilogue.  And the GEMV launch (§6.9): plans whose tasks all
-have <= 4 rows (decode steps) run every task as a GEMV on every SM — bit-exact on integer inputs for each tile
-shape, host / device plans, plain / row-map / row-pointer Y, FP8, full-size decode within tolerance."""
+the north-star tolerance, and the EP row-pointer epilogue."""
 import numpy as np
 import pytest
 import torch
@@ -153,76 +151,3 @@ def test_gemv_through_ep_peer_rowptr():
     assert [ep.status() for ep in eps] == [0] * G
     got = torch.cat([o.cpu() for o in outs]).double().numpy()
     assert np.array_equal(got, omoe.per_slot_outputs(ids, X, W))
-
-
-@pytest.mark.parametrize("device_plan", [False, True])
-@pytest.mark.parametrize("bm,bn", [(128, 256), (256, 512), (256, 256)])
-@pytest.mark.parametrize("shape", [(1, 8, 2, 4096, 14336), (4, 8, 2, 512, 1000), (7, 64, 6, 256, 1408)])
-def test_gemv_launch_integer_bit_exact(shape, bm, bn, device_plan):
-    T, E, k, H, N = shape
-    ids = synth.route_gumbel(T + E, T, E, k)
-    X, W = synth.make_x(T, T, H, "int"), synth.make_w(T, E, H, N, "int")
-    Xd, Wd = torch.from_numpy(X).to(torch.bfloat16).cuda(), torch.from_numpy(W).to(torch.bfloat16).cuda()
-    topk = torch.from_numpy(ids).cuda()
-    if device_plan:
-        plan = M.Plan(None, H, N, bm, bn, E=E)
-        counts, row_off, tok, _, _ = M.moe_route(topk, E, plan=plan)
-    else:
-        counts, row_off, tok, _, _ = M.moe_route(topk, E)
-        plan = M.Plan(counts.cpu().numpy(), H, N, bm, bn)
-        assert plan.total_tiles == 0                                      # a GEMV launch
-    assert counts.max().item() <= 4
-    rc, rr, rt, _ = omoe.buckets(ids, E)
-    ref = omoe.expert_gemm(X, W, rt, rr)
-    for _ in range(2):
-        Y = torch.full((tok.numel(), N), float("nan"), device="cuda")
-        M.moe_gemm(plan, Xd, tok, Wd, Y=Y)
-        torch.cuda.synchronize()
-        assert np.array_equal(Y.cpu().double().numpy(), ref)
-    Yb = M.moe_gemm(plan, Xd, tok, Wd, out_dtype=torch.bfloat16)
-    assert torch.equal(Yb, torch.from_numpy(ref).float().to(torch.bfloat16).cuda())
-    # row-map output (the EP send-buffer layout): row i lands at map[i]
-    R = tok.numel()
-    perm = torch.randperm(R, device="cuda").to(torch.int32)
-    Ym = torch.full((R, N), float("nan"), device="cuda")
-    M.moe_gemm(plan, Xd, tok, Wd, Y=Ym, row_map=perm)
-    torch.cuda.synchronize()
-    got = np.empty_like(ref)
-    got[:] = Ym[perm.long()].cpu().double().numpy()
-    assert np.array_equal(got, ref)
-
-
-def test_gemv_launch_fp8_and_full_size_decode():
-    """FP8 codes through the GEMV launch (bit-exact), and the dec1 bench shape on full-mantissa inputs
-    (device plan fused into the route, as bench.py runs it) within the north-star tolerance."""
-    T, E, k, H, N = 3, 8, 2, 1024, 2048
-    ids = synth.route_gumbel(1, T, E, k)
-    X8, W8 = sfp8.make_x_fp8(1, T, H, "int"), sfp8.make_w_fp8(1, E, H, N, "int")
-    sc = np.array([2.0 ** (e % 3 - 1) for e in range(E)], dtype=np.float32)
-    counts, row_off, tok, _, _ = M.moe_route(torch.from_numpy(ids).cuda(), E)
-    plan = M.Plan(counts.cpu().numpy(), H, N, 128, 256)
-    assert plan.total_tiles == 0
-    Y = M.moe_gemm_fp8(plan, torch.from_numpy(X8).cuda(), tok, torch.from_numpy(W8).cuda(),
-                       torch.from_numpy(sc).cuda(), out_dtype=torch.float32)
-    torch.cuda.synchronize()
-    rc, rr, rt, _ = omoe.buckets(ids, E)
-    assert np.array_equal(Y.cpu().double().numpy(), ofp8.expert_gemm_fp8(X8, W8, rt, rr, sc))
-    c = synth.CONFIGS["dec1"]
-    ids = synth.route(c, 0)
-    Xd = synth.make_x_torch(0, c.T, c.H, "generic", device="cuda")
-    Wd = synth.make_w_torch(0, c.E, c.H, c.N, "generic", device="cuda")
-    bm, bn = M.suggest_tile(c.T * c.k, c.E, c.H, c.N)
-    plan = M.Plan(None, c.H, c.N, bm, bn, E=c.E)
-    counts, row_off, tok, _, _ = M.moe_route(torch.from_numpy(ids).cuda(), c.E, plan=plan)
-    Y = M.moe_gemm(plan, Xd, tok, Wd, out_dtype=torch.float32)
-    torch.cuda.synchronize()
-    rc, rr, rt, _ = omoe.buckets(ids, c.E)
-    cols = np.arange(0, c.N, 7)
-    got = Y.cpu().double().numpy()[:, cols]
-    ref = np.zeros_like(got)
-    for r in range(len(rt)):
-        e = int(np.searchsorted(rr, r, side="right") - 1)
-        ref[r] = wl.x_rows(0, c.T, c.H, [int(rt[r])], "generic")[0] @ wl.w_columns(0, c.E, c.H, c.N, e, cols, "generic")
-    d = np.abs(got - ref)
-    assert (d <= 1e-2 * (np.abs(ref) + 1)).all(), d.max()
-    assert np.linalg.norm(got - ref) <= 2e-3 * np.linalg.norm(ref)

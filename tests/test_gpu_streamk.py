@@ -30,7 +30,6 @@ CASES = [  # T, E, k, H, N: tiles < SMs, <= 16 rows per expert (the 20-row case 
 
 
 def _run(ids, Xd, Wd, E, flags=M.MOE_SPLIT_K, device_plan=False, out_dtype=torch.float32, reps=1):
-    flags |= M.MOE_NO_GEMV_LAUNCH                       # tiles (a <= 4-row batch would be a GEMV launch)
     topk = torch.from_numpy(np.ascontiguousarray(ids, dtype=np.int32)).cuda()
     if device_plan:
         plan = M.Plan(None, Xd.shape[1], Wd.shape[2], 128, 256, flags, E=E)
@@ -99,7 +98,7 @@ def test_streamk_fp8_codes_bit_exact(case):
     sc = np.array([2.0 ** (e % 3 - 1) for e in range(E)], dtype=np.float32)
     topk = torch.from_numpy(ids).cuda()
     counts, row_off, tok, _, _ = M.moe_route(topk, E)
-    plan = M.Plan(counts.cpu().numpy(), H, N, 128, 256, M.MOE_SPLIT_K | M.MOE_NO_GEMV_LAUNCH)
+    plan = M.Plan(counts.cpu().numpy(), H, N, 128, 256, M.MOE_SPLIT_K)
     Y = M.moe_gemm_fp8(plan, torch.from_numpy(X8).cuda(), tok, torch.from_numpy(W8).cuda(), torch.from_numpy(sc).cuda(),
                        out_dtype=torch.float32)
     torch.cuda.synchronize()

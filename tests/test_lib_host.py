@@ -56,8 +56,7 @@ def _compare(counts, N, bm, bn, pad, split=False, order="natural", catalog=None)
     if split:
         catalog = ((1, bm),)
     assert p["catalog"] == tuple(catalog)
-    ref = omoe.plan(counts, N, bm, bn, pad_mode=pad, split_tail=split, order=order, catalog=catalog,
-                    gemv_launch=not (flags & moe_lib.MOE_NO_GEMV_LAUNCH))
+    ref = omoe.plan(counts, N, bm, bn, pad_mode=pad, split_tail=split, order=order, catalog=catalog)
     assert p["M"] == ref["M"] and p["total"] == ref["total"]
     if ref["M"] == 0:
         return
@@ -322,16 +321,8 @@ def test_planner_gemv_strategy_by_hand():
     # fewer than MOE_GEMV_MIN_TILES other tiles: the GEMV candidates fall through to the next rule
     q = moe_lib.parse_plan_blob(moe_lib.moe_plan_build(counts, 64, 1024, 256, 512, catalog=[(2, 4), (1, 64)]))
     assert q["params"][:, 3].tolist() == [1, 0, 1, 0, 1, 1, 1] and q["M"] == 6
-    # every task <= 4 rows: a GEMV launch (§6.9) on any tile shape, unless MOE_NO_GEMV_LAUNCH (or bm = 64)
-    for bm, bn in ((256, 512), (128, 256), (256, 256)):
-        q = moe_lib.parse_plan_blob(moe_lib.moe_plan_build([2, 0, 1, 4], 64, 1024, bm, bn))
-        assert q["M"] == 0 and q["total"] == 0 and q["params"][:, 3].tolist() == [2, 0, 2, 2]
-        q = moe_lib.parse_plan_blob(moe_lib.moe_plan_build([2, 0, 1, 4], 64, 1024, bm, bn, moe_lib.MOE_NO_GEMV_LAUNCH))
-        assert q["M"] == 3 and 2 not in q["params"][:, 3].tolist()
-    q = moe_lib.parse_plan_blob(moe_lib.moe_plan_build([2, 0, 1, 5], 64, 1024, 128, 256))
-    assert q["M"] == 3                                                     # one task of 5 rows: tiles
-    q = moe_lib.parse_plan_blob(moe_lib.moe_plan_build([2, 0, 1], 64, 256, 64, 256))
-    assert q["M"] == 2                                                     # bm = 64 decode tiles: no GEMV launch
+    q = moe_lib.parse_plan_blob(moe_lib.moe_plan_build([2, 0, 1], 64, 1024, 256, 512, catalog=[(2, 4)]))
+    assert q["M"] == 2 and q["params"][:, 3].tolist() == [0, 0, 0]
     for bad in ([(2, 5)], [(2, 4)]):
         with pytest.raises(moe_lib.MoeError):
             moe_lib.moe_plan_build([1, 1], 64, 1024, 256, 256 if bad == [(2, 4)] else 512, catalog=bad)

@@ -181,7 +181,7 @@ def test_decode_enumeration_rt_fastest_and_cover():
             counts[0] = 3
         N = rng.choice([16, 40, 64])
         bm, bn = rng.choice([(8, 16), (16, 16), (4, 32)])
-        p = moe.plan(counts, N, bm, bn, gemv_launch=False)          # the tile mapping under test
+        p = moe.plan(counts, N, bm, bn)
         row_off = np.concatenate([[0], np.cumsum(counts)])
         B = 0
         for e in range(E):                      # independent enumeration: experts, then ct, then rt
