@@ -121,6 +121,8 @@ struct GemmArgs {
   int32_t* sk_cnt;           //           and per-tile arrival counters (zero between launches)
   int32_t light_merge;       // MOE_ORDER_LIGHT_LAST plan under the dynamic tile order: interleave the light
                              // (memory-bound) tail of the virtual tiles among the others in proportion
+  int32_t half_last;        // MOE_SCHED_HALF_LAST: dynamic order of wide tiles with each task's <= 128-row last
+                             // row tile (a half tile) after every full tile (LPT-like end)
   int32_t* gemv_q;           // nullable: the plan may hold MOE_KIND_GEMV tasks (wide pair kernels): [0] next
                              // GEMV unit, [1] epilogue warps done (both zero between launches)
 };
@@ -738,11 +740,67 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int before = (int)((long long)i * L / total), upto = (int)((long long)(i + 1) * L / total);
       return upto > before ? light0 + before : i - before;
     };
+    // Half tiles last: fetch positions [0, n_full) walk the full tiles in virtual order
+    // (each task's row tiles [0, R - f) of every column block, row tile fastest), [n_full, total) the half
+    // tiles (f = 1: the task's last row tile holds <= 128 rows).  All 32 lanes: per-lane task data, a warp
+    // scan of the per-task counts and a vote find the task holding position pos (Alg. 2's search on a
+    // derived prefix), then the tile's virtual index in the plan's own order.
+    const int mt = __ldg(a.plan + 1);               // tasks with tiles (sigma's length)
+    auto task_rf = [&](int hh, int& R, int& f, int& C) {
+      const int tk = s_sigma[hh];
+      const int4 pb = __ldg(reinterpret_cast<const int4*>(params + tk * MOE_PLAN_TASK_WORDS + 4));
+      const int rows = __ldg(params + tk * MOE_PLAN_TASK_WORDS + 2);
+      R = pb.z;
+      C = pb.w;
+      f = rows - (R - 1) * kPairRows <= kPairRows / 2 ? 1 : 0;
+    };
+    int n_full = total;
+    if (dyn && rank == 0 && a.half_last) {
+      int nh = 0;
+      for (int c = 0; c < mt; c += 32) {
+        int R = 0, f = 0, C = 0;
+        if (c + lane < mt) task_rf(c + lane, R, f, C);
+        nh += __reduce_add_sync(0xffffffffu, f * C);
+      }
+      n_full = total - nh;
+    }
+    auto half_reorder = [&](int pos) -> int {
+      if (pos >= total || n_full >= total) return pos;
+      const bool second = pos >= n_full;
+      const int q = second ? pos - n_full : pos;
+      int base = 0;
+      for (int c = 0; c < mt; c += 32) {
+        const int hh = c + lane;
+        int R = 1, f = 0, C = 0;
+        if (hh < mt) task_rf(hh, R, f, C);
+        int cnt = hh < mt ? (second ? f * C : (R - f) * C) : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, cnt, o);
+          if (lane >= o) cnt += y;
+        }
+        const int pref = base + cnt;                 // this kind's tiles through task hh
+        const unsigned before_mask = __ballot_sync(0xffffffffu, hh < mt && q >= pref);
+        const int nb = __popc(before_mask);
+        if (nb < 32) {
+          const int h = c + nb;
+          const int start = nb == 0 ? base : __shfl_sync(0xffffffffu, pref, nb - 1);
+          const int Rh = __shfl_sync(0xffffffffu, R, nb), fh = __shfl_sync(0xffffffffu, f, nb);
+          const int l = q - start;
+          const int first = h > 0 ? s_prefix[h - 1] : 0;
+          if (second) return first + l * Rh + (Rh - 1);            // column block l, last row tile
+          const int rf = Rh - fh;
+          return first + (l / rf) * Rh + (l % rf);
+        }
+        base = __shfl_sync(0xffffffffu, pref, 31);
+      }
+      return pos;
+    };
     for (uint32_t qi = 0;; ++qi) {
       int v, k0 = 0, k1 = a.num_kb;
       if (dyn && rank == 0) {                       // the producer of the pair's tile queue
         const int pos = __shfl_sync(0xffffffffu, v_next, 0);
-        v = merged(pos);
+        v = a.light_merge ? merged(pos) : a.half_last ? half_reorder(pos) : pos;
         const int sl = (int)(qi % kQ);
         mbar_wait(qempty_bar(sl), ((qi / kQ) & 1u) ^ 1u);
         if (lane == 0) {
@@ -2076,6 +2134,7 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
                        (!(v.flags & (MOE_GRID_STATIC | MOE_GRID_BALANCED)) && v.bm == 256);
   a.sched = dynamic ? moe::plan_sched_dev(plan) : nullptr;
   a.light_merge = dynamic && (v.flags & MOE_ORDER_LIGHT_LAST) ? 1 : 0;
+  a.half_last = dynamic && wide && !gated && !a.light_merge && (v.flags & MOE_SCHED_HALF_LAST) ? 1 : 0;
   a.gemv_q = has_gemv ? moe::plan_sched_dev(plan) + 2 : nullptr;
   if (has_gemv && !(wide && !gated))
     MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_gemm: MOE_KIND_GEMV tasks need a wide pair tile plan (bm 256, bn > 256)");

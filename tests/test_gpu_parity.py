@@ -733,3 +733,32 @@ def test_dynamic_order_full_size_graph(cfg):
     ref = omoe.expert_gemm_entries(lambda t: wl.x_rows(0, c.T, c.H, [t])[0],
                                    lambda e, cs: wl.w_columns(0, c.E, c.H, c.N, e, cs), rt, rr, rows, cols)
     tol_check(outs[0][torch.from_numpy(rows).cuda()][:, torch.from_numpy(cols).cuda()].cpu(), ref, cfg)
+
+
+@pytest.mark.parametrize("shape", [(700, 9, 3, 256, 1408), (2000, 16, 2, 128, 2560), (300, 5, 2, 512, 640),
+                                   (4096, 64, 6, 128, 1408)])
+@pytest.mark.parametrize("device_plan", [False, True])
+def test_half_tiles_last_order_is_invisible(shape, device_plan):
+    """MOE_SCHED_HALF_LAST: the dynamic order of wide tiles fetches each task's <= 128-row last row tile after
+    every full tile: Y is bit-identical to the plan-order launch and exact."""
+    T, E, k, H, N = shape
+    ids = synth.route_gumbel(T, T, E, k, s=1.1, n_empty=1)
+    X, W = synth.make_x(T, T, H, "int"), synth.make_w(T, E, H, N, "int")
+    Xd, Wd = torch.from_numpy(X).to(torch.bfloat16).cuda(), torch.from_numpy(W).to(torch.bfloat16).cuda()
+    topk = torch.from_numpy(ids).cuda()
+    outs = []
+    for flags in (M.MOE_SCHED_HALF_LAST, 0):
+        if device_plan:
+            plan = M.Plan(None, H, N, 256, 512, flags, E=E)
+            counts, row_off, tok, _, _ = M.moe_route(topk, E, plan=plan)
+        else:
+            counts, row_off, tok, _, _ = M.moe_route(topk, E)
+            plan = M.Plan(counts.cpu().numpy(), H, N, 256, 512, flags)
+        Y = torch.full((tok.numel(), N), float("nan"), device="cuda")
+        for _ in range(2):
+            M.moe_gemm(plan, Xd, tok, Wd, Y=Y)
+        outs.append(Y)
+    torch.cuda.synchronize()
+    rc, rr, rt, _ = omoe.buckets(ids, E)
+    assert np.array_equal(outs[0].cpu().double().numpy(), omoe.expert_gemm(X, W, rt, rr))
+    assert torch.equal(outs[0], outs[1])
