@@ -106,8 +106,10 @@ moe_status ep_peer_forward(moe_ep* ep, const int32_t* topk, int64_t T, int32_t k
   // 1. dispatch: per-destination deduplicated rows, stored into the owners' receive buffers
   PEER_TRY(moe_ep_dispatch_plan(topk, T, k, ep->E, G, P.counts2, P.send_off, P.send_tok, P.send_meta, s));
   PEER_CUDA(ep_peer_dispatch(X, x_row, P.send_off, P.send_tok, P.send_meta, G, k, ep->rank, P.T_max, P.peers_dev, s));
-  PEER_CUDA(ep_peer_signal(P.peers_dev, G, ep->rank, kDispatchWord, P.epoch_dev, true, s));
-  PEER_CUDA(ep_peer_wait(flags_mine, G, kDispatchWord, P.epoch_dev, P.status_dev, P.timeout_ns, s));
+  if (G > 1) {                                       // one rank: stream order is the whole protocol
+    PEER_CUDA(ep_peer_signal(P.peers_dev, G, ep->rank, kDispatchWord, P.epoch_dev, true, s));
+    PEER_CUDA(ep_peer_wait(flags_mine, G, kDispatchWord, P.epoch_dev, P.status_dev, P.timeout_ns, s));
+  }
   // 2. local experts: buckets over the received ids (empty rows are -1), device plan
   PEER_TRY(moe_route_plan(meta_mine, R, k, El, P.counts_l, P.row_off_l, P.tok_l, P.slot_l, nullptr, ep->plan, s));
   PEER_CUDA(cudaMemsetAsync(meta_mine, 0xff, sizeof(int32_t) * (size_t)(R * k), s));   // next step's empty rows
@@ -119,8 +121,10 @@ moe_status ep_peer_forward(moe_ep* ep, const int32_t* topk, int64_t T, int32_t k
   PEER_CUDA(cudaEventRecord(ep->gemm_ev[1], s));
   ep->gemm_timed = true;
   // 4. every peer's GEMM has stored this rank's rows
-  PEER_CUDA(ep_peer_signal(P.peers_dev, G, ep->rank, kCombineWord, P.epoch_dev, false, s));
-  PEER_CUDA(ep_peer_wait(flags_mine, G, kCombineWord, P.epoch_dev, P.status_dev, P.timeout_ns, s));
+  if (G > 1) {
+    PEER_CUDA(ep_peer_signal(P.peers_dev, G, ep->rank, kCombineWord, P.epoch_dev, false, s));
+    PEER_CUDA(ep_peer_wait(flags_mine, G, kCombineWord, P.epoch_dev, P.status_dev, P.timeout_ns, s));
+  }
   void* out_mine = mine + P.off_out;
   if (out && out != out_mine) PEER_CUDA(ep_peer_copy_out(out_mine, topk, T, k, y_row, out, s));
   P.last = s;

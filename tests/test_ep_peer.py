@@ -230,3 +230,37 @@ def test_ep_peer_multiprocess_one_gpu(world, fp8):
             if p.is_alive():  # pragma: no cover
                 p.kill()
     assert res == {r: [True, True, True] for r in range(world)}, res
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("T,E,G,k", [(5000, 16, 4, 3), (1025, 8, 2, 2), (4096, 8, 1, 2), (3000, 64, 8, 6)])
+def test_dispatch_plan_chunked_matches_definition(T, E, G, k):
+    """moe_ep_dispatch_plan over chunks x G blocks (T > 1024): per destination d the tokens with a slot
+    owned by d in ascending order, their d-local ids (-1: another rank's slot or a repeated id), the row /
+    slot totals and offsets — written out here from the definition (R8)."""
+    import paper_2501_16103_b200 as M
+    rng = np.random.default_rng(T)
+    ids = synth.route_gumbel(T, T, E, k, s=1.0, n_empty=1)
+    ids = np.where(rng.random((T, k)) < 0.1, -1, ids).astype(np.int32)
+    rep = np.nonzero(rng.random(T) < 0.05)[0]
+    ids[rep, k - 1] = ids[rep, 0]
+    counts2, send_off, send_tok, send_meta = M.moe_ep_dispatch_plan(torch.from_numpy(ids).cuda(), E, G)
+    torch.cuda.synchronize()
+    El = E // G
+    off = 0
+    for d in range(G):
+        toks, metas, slots = [], [], 0
+        for t in range(T):
+            row = ids[t].tolist()
+            meta = [row[j] - d * El if row[j] >= 0 and row[j] // El == d and row[j] not in row[:j] else -1
+                    for j in range(k)]
+            if any(r >= 0 and r // El == d for r in row):
+                toks.append(t)
+                metas.append(meta)
+            slots += sum(m >= 0 for m in meta)
+        assert counts2[d].tolist() == [len(toks), slots]
+        assert int(send_off[d]) == off
+        assert send_tok[off:off + len(toks)].tolist() == toks
+        assert send_meta[off:off + len(toks)].tolist() == metas
+        off += len(toks)
+    assert int(send_off[G]) == off
