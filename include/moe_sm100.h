@@ -83,6 +83,9 @@ typedef int32_t moe_status;
                                    and sum them in K order (opt-in: measured slower than whole tiles on the
                                    balanced grid)                                       */
 
+#define MOE_SCHED_PLAN_ORDER 16384u /* dynamic order of wide tiles strictly in the plan's order (default when N %
+                                   bn != 0: every task's narrower last column block after the full-width
+                                   ones)                                              */
 #define MOE_SCHED_HALF_LAST 2048u /* dynamic order of wide tiles: each task's <= 128-row last row tiles after
                                    all full tiles (LPT-like end of the launch; opt-in: 8x22B +3.4 %, Mix
                                    -1.9 % — a half tile moved away from its column block re-reads W from

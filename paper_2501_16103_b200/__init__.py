@@ -28,6 +28,7 @@ MOE_GRID_BALANCED, MOE_GRID_STATIC, MOE_A_GATHER4, MOE_EPI_REGISTER, MOE_SCHED_D
 MOE_L2_PREFETCH = 512
 MOE_SPLIT_K = 1024
 MOE_SCHED_HALF_LAST = 2048
+MOE_SCHED_PLAN_ORDER = 16384
 MOE_ROUTE_NO_SMALL, MOE_ROUTE_THREE_KERNELS = 1, 2
 MOE_KIND_WIDE, MOE_KIND_SWAP, MOE_MAX_RULES = 0, 1, 2
 MOE_DEFAULT_SWAP_MAX = 64                       # include/moe_sm100.h: the swap-AB rule of tests and A/B runs

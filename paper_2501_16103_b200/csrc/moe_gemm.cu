@@ -121,6 +121,8 @@ struct GemmArgs {
   int32_t* sk_cnt;           //           and per-tile arrival counters (zero between launches)
   int32_t light_merge;       // MOE_ORDER_LIGHT_LAST plan under the dynamic tile order: interleave the light
                              // (memory-bound) tail of the virtual tiles among the others in proportion
+  int32_t narrow_last;      // > 1: column tiles per task, the last (narrower) column block of every task is fetched
+                             // after the full-width ones (dynamic order of wide tiles)
   int32_t half_last;        // MOE_SCHED_HALF_LAST: dynamic order of wide tiles with each task's <= 128-row last
                              // row tile (a half tile) after every full tile (LPT-like end)
   int32_t* gemv_q;           // nullable: the plan may hold MOE_KIND_GEMV tasks (wide pair kernels): [0] next
@@ -764,6 +766,34 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       n_full = total - nh;
     }
+    // Narrow column block last: when N is not a multiple of bn the last column block of
+    // every task is narrower; fetch positions [0, total (C-1)/C) walk the full-width column blocks, the rest
+    // the narrow ones, each run in the plan's order.  Task h owns R_h (C-1) / R_h tiles of each run, i.e.
+    // TilePrefix x (C-1) / C and TilePrefix / C (exact: every task has R_h x C tiles): Alg. 2's vote on the
+    // scaled prefix finds the task, and the tile keeps its (rt, ct), so a column block stays together.
+    auto narrow_reorder = [&](int pos) -> int {
+      const int C = a.narrow_last;                     // column tiles per task (> 1)
+      const int n_wide = (int)((long long)total * (C - 1) / C);
+      if (pos >= total) return pos;
+      const bool second = pos >= n_wide;
+      const int q = second ? pos - n_wide : pos;
+      for (int c = 0; c < mt; c += 32) {
+        const int hh = c + lane;
+        const long long pf = hh < mt ? (long long)s_prefix[hh] : (long long)total;
+        const long long pref = second ? pf / C : pf * (C - 1) / C;
+        const unsigned mask = __ballot_sync(0xffffffffu, hh < mt && q >= pref);
+        const int nb = __popc(mask);
+        if (nb < 32) {
+          const int h = c + nb;
+          const int first = h > 0 ? s_prefix[h - 1] : 0;
+          const int start = second ? first / C : (int)((long long)first * (C - 1) / C);
+          const int l = q - start;
+          const int R = (s_prefix[h] - first) / C;
+          return second ? first + (C - 1) * R + l : first + l;
+        }
+      }
+      return pos;
+    };
     auto half_reorder = [&](int pos) -> int {
       if (pos >= total || n_full >= total) return pos;
       const bool second = pos >= n_full;
@@ -800,7 +830,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int v, k0 = 0, k1 = a.num_kb;
       if (dyn && rank == 0) {                       // the producer of the pair's tile queue
         const int pos = __shfl_sync(0xffffffffu, v_next, 0);
-        v = a.light_merge ? merged(pos) : a.half_last ? half_reorder(pos) : pos;
+        v = a.light_merge ? merged(pos) : a.half_last ? half_reorder(pos) : a.narrow_last > 1 ? narrow_reorder(pos) : pos;
         const int sl = (int)(qi % kQ);
         mbar_wait(qempty_bar(sl), ((qi / kQ) & 1u) ^ 1u);
         if (lane == 0) {
@@ -2135,6 +2165,10 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
   a.sched = dynamic ? moe::plan_sched_dev(plan) : nullptr;
   a.light_merge = dynamic && (v.flags & MOE_ORDER_LIGHT_LAST) ? 1 : 0;
   a.half_last = dynamic && wide && !gated && !a.light_merge && (v.flags & MOE_SCHED_HALF_LAST) ? 1 : 0;
+  a.narrow_last = dynamic && wide && !gated && !a.light_merge && !a.half_last && v.N % v.bn != 0 && v.N > v.bn &&
+                          !(v.flags & MOE_SCHED_PLAN_ORDER)
+                      ? (int)moe::ceil_div(v.N, v.bn)
+                      : 0;
   a.gemv_q = has_gemv ? moe::plan_sched_dev(plan) + 2 : nullptr;
   if (has_gemv && !(wide && !gated))
     MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_gemm: MOE_KIND_GEMV tasks need a wide pair tile plan (bm 256, bn > 256)");

@@ -113,7 +113,7 @@ moe_status moe_plan_build_catalog(const int32_t* counts, int32_t E, int64_t H, i
              bm == 256 ? 32 : 16);
   if (flags & ~(MOE_PAD_REPEAT | MOE_SPLIT_TAIL | MOE_ORDER_ALTERNATING | MOE_ORDER_HALF_INTERVAL | MOE_ORDER_LIGHT_LAST | MOE_GRID_BALANCED |
                 MOE_GRID_STATIC | MOE_A_GATHER4 | MOE_EPI_REGISTER | MOE_SCHED_DYNAMIC | MOE_L2_PREFETCH | MOE_SPLIT_K |
-                MOE_SCHED_HALF_LAST))
+                MOE_SCHED_HALF_LAST | MOE_SCHED_PLAN_ORDER))
     MOE_FAIL(MOE_ERR_INVALID, "moe_plan_build: unknown flags 0x%x", flags);
   if ((flags & MOE_GRID_BALANCED) && (flags & MOE_GRID_STATIC))
     MOE_FAIL(MOE_ERR_INVALID, "moe_plan_build: MOE_GRID_BALANCED and MOE_GRID_STATIC are exclusive");

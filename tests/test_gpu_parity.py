@@ -739,15 +739,16 @@ def test_dynamic_order_full_size_graph(cfg):
                                    (4096, 64, 6, 128, 1408)])
 @pytest.mark.parametrize("device_plan", [False, True])
 def test_half_tiles_last_order_is_invisible(shape, device_plan):
-    """MOE_SCHED_HALF_LAST: the dynamic order of wide tiles fetches each task's <= 128-row last row tile after
-    every full tile: Y is bit-identical to the plan-order launch and exact."""
+    """The dynamic fetch orders of wide tiles — MOE_SCHED_HALF_LAST (each task's <= 128-row
+    last row tile after every full tile), the default narrow-column-block-last order (N % 512 != 0 here for
+    two shapes) and MOE_SCHED_PLAN_ORDER — give bit-identical, exact Y."""
     T, E, k, H, N = shape
     ids = synth.route_gumbel(T, T, E, k, s=1.1, n_empty=1)
     X, W = synth.make_x(T, T, H, "int"), synth.make_w(T, E, H, N, "int")
     Xd, Wd = torch.from_numpy(X).to(torch.bfloat16).cuda(), torch.from_numpy(W).to(torch.bfloat16).cuda()
     topk = torch.from_numpy(ids).cuda()
     outs = []
-    for flags in (M.MOE_SCHED_HALF_LAST, 0):
+    for flags in (M.MOE_SCHED_HALF_LAST, 0, M.MOE_SCHED_PLAN_ORDER):       # 0: narrow column block last
         if device_plan:
             plan = M.Plan(None, H, N, 256, 512, flags, E=E)
             counts, row_off, tok, _, _ = M.moe_route(topk, E, plan=plan)
@@ -761,4 +762,4 @@ def test_half_tiles_last_order_is_invisible(shape, device_plan):
     torch.cuda.synchronize()
     rc, rr, rt, _ = omoe.buckets(ids, E)
     assert np.array_equal(outs[0].cpu().double().numpy(), omoe.expert_gemm(X, W, rt, rr))
-    assert torch.equal(outs[0], outs[1])
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
