@@ -207,7 +207,7 @@ def _proc_worker(rank, world, port, q, fp8):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world,fp8", [(2, False), (4, False), (2, True)])
+@pytest.mark.parametrize("world,fp8", [(2, False), (4, False), (2, True), (8, False)])
 def test_ep_peer_multiprocess_one_gpu(world, fp8):
     """`world` processes (one rank each, as under torchrun) on one GPU: CUDA IPC mappings of each
     other's regions, blobs all-gathered over gloo, three steps each, bit-exact per rank."""
