@@ -735,16 +735,32 @@ def run_ep(args, base):
     native = None
     peer = not args.ep_python and args.ep_transport == "peer"
     out_view = None
+    peer_fallback = None
     if peer:                                         # the library's moe_ep_* step over symmetric peer memory
-        def allgather(blob):
-            got = [None] * ws
-            dist.all_gather_object(got, blob)
-            return got
         y_bytes = cfg.N * (2 if out_dtype == torch.bfloat16 else 4)
-        native = M.PeerExpertParallel(rank, ws, cfg.E, W_l, max_tokens=T_l, k=cfg.k, allgather=allgather,
-                                      w_scale=w_scale, bm=args.bm, bn=args.bn, max_out_bytes=y_bytes)
-        out_view = native.output(T_l, cfg.N, out_dtype)          # zero copy: the rows stay in the output buffer
-    elif not args.ep_python:                         # the library's moe_ep_* step (NCCL from C++)
+        native, err = None, None
+        try:
+            native = M.PeerExpertParallel(rank, ws, cfg.E, W_l, max_tokens=T_l, k=cfg.k, w_scale=w_scale,
+                                          bm=args.bm, bn=args.bn, max_out_bytes=y_bytes, connect=False)
+        except Exception as e:  # pragma: no cover - region allocation failed
+            err = repr(e)[:200]
+        blobs = [None] * ws
+        dist.all_gather_object(blobs, native.blob if native is not None else None)
+        if native is not None and all(b is not None for b in blobs):
+            try:
+                native.connect(blobs)                # CUDA IPC mappings of every peer's region
+            except Exception as e:  # pragma: no cover - e.g. no P2P / IPC between these GPUs
+                err = repr(e)[:200]
+        ok = [None] * ws
+        dist.all_gather_object(ok, err)
+        if any(o is not None for o in ok) or any(b is None for b in blobs):
+            # every rank falls back together: the NCCL transport of the same library step
+            peer_fallback = next(o for o in ok if o is not None) if any(o is not None for o in ok) else "no blob"
+            native, peer = None, False
+            dist.barrier()
+        else:
+            out_view = native.output(T_l, cfg.N, out_dtype)      # zero copy: the rows stay in the output buffer
+    if not peer and not args.ep_python:              # the library's moe_ep_* step (NCCL from C++)
         uid = torch.zeros(128, dtype=torch.uint8, device=dev)
         if rank == 0:
             uid.copy_(torch.frombuffer(bytearray(M.moe_ep_unique_id()), dtype=torch.uint8))
@@ -882,6 +898,7 @@ def run_ep(args, base):
             "config": {**ep_config(base, ws, args),
                        **({"oversubscribed": f"{ws} ranks on {n_dev} GPU(s): functional run, not a scaling number"}
                           if shared else {}),
+                       **({"peer_transport_unavailable": peer_fallback} if peer_fallback else {}),
                        "collectives": ("none: symmetric peer memory (CUDA IPC) — dispatch rows stored into the "
                                        "owners' receive buffers, the GEMM epilogue storing result rows into the "
                                        "token owners' outputs, device-side epoch flags (moe_ep_peer_*)") if peer else
