@@ -919,9 +919,10 @@ def run_ep(args, base):
             "cpu_baseline": None,
             "e2e": e2e,
             # NCCL / torch paths: dispatch plan 2, gather 1, route (1-3, on the received rows), plan 1, combine
-            # map 1, GEMM 1, unpack 1.  Peer path: dispatch plan 2, dispatch 1, signal + wait 2, route (on the
-            # G * T_l receive rows), id reset 1, row pointers 1, GEMM 1, signal + wait 2.
-            "gpu_launches": ((10 + route_launches(ws * T_l, El, cfg.k)) if peer else
+            # map 1, GEMM 1, unpack 1.  Peer path: dispatch plan 2, dispatch 1, route (on the G * T_l receive
+            # rows), row pointers 1, GEMM 1, and with > 1 rank two signal + wait pairs (4); the id reset is a
+            # memset node.
+            "gpu_launches": ((5 + (4 if ws > 1 else 0) + route_launches(ws * T_l, El, cfg.k)) if peer else
                              (7 + route_launches(native.last_rows()["received"] if native is not None
                                                  else sum(moe.last["recv_rows"]), El, cfg.k))) * args.steps,
             "clocks": clk.summary(),
