@@ -323,6 +323,9 @@ __device__ __forceinline__ void wait_timed(uint32_t bar, uint32_t parity, long l
 // further ahead measured slower (paper worst 0.811 / 0.724 of peak at 6 / 16 rounds ahead vs 0.830 without).
 // ---------------------------------------------------------------------------
 constexpr int kGemvCols = 128;
+#ifndef MOE_GEMV_LOAD
+#define MOE_GEMV_LOAD 1   // W loads of GEMV units: 1 = ld.global.nc.L1::no_allocate (paper worst +2.4 %), 0 = ld.global.cs
+#endif
 #ifndef MOE_GEMV_BATCH
 #define MOE_GEMV_BATCH 1
 #endif
@@ -360,12 +363,27 @@ struct GemvUnit {
     }
   }
   __device__ __forceinline__ static uint4 load8(const uint8_t* p) {
+#if MOE_GEMV_LOAD == 1
+    // read-only path, no L1 allocation (the W stream is used once)
+    if constexpr (kFp8) {
+      uint32_t x, y;
+      asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0, %1}, [%2];" : "=r"(x), "=r"(y) : "l"(p));
+      return make_uint4(x, y, 0u, 0u);
+    } else {
+      uint4 v;
+      asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                   : "l"(p));
+      return v;
+    }
+#else
     if constexpr (kFp8) {
       const uint2 v = __ldcs(reinterpret_cast<const uint2*>(p));
       return make_uint4(v.x, v.y, 0u, 0u);
     } else {
       return __ldcs(reinterpret_cast<const uint4*>(p));
     }
+#endif
   }
 };
 
