@@ -37,10 +37,47 @@ __device__ __forceinline__ long long block_scan_incl(long long x, long long* s_w
   return x + off;
 }
 
+// Four inclusive block scans in one pass (the planner's latency is its barriers: one pass = 3 instead of 12).
+__device__ __forceinline__ void block_scan_incl4(long long (&x)[4], long long* s_warp4, long long (&total)[4]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long y = __shfl_up_sync(0xffffffffu, x[i], o);
+      if (lane >= o) x[i] += y;
+    }
+  }
+  if (lane == 31)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) s_warp4[4 * warp + i] = x[i];
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      long long w = s_warp4[4 * lane + i];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long y = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += y;
+      }
+      s_warp4[4 * lane + i] = w;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    x[i] += warp > 0 ? s_warp4[4 * (warp - 1) + i] : 0;
+    total[i] = s_warp4[4 * 31 + i];
+  }
+  __syncthreads();
+}
+
 // All kPlanThreads threads of the block call this; m = tokens of expert threadIdx.x (0 if >= E).
 __device__ __forceinline__ void plan_body(long long m, int E, int H, int N, int bm, int bn, uint32_t flags,
                                           int32_t* __restrict__ blob) {
   __shared__ long long s_warp[32];
+  __shared__ long long s_warp4[4 * 32];
   const int t = threadIdx.x;                                       // expert t
   // The catalog (header words 12-15, written at plan creation and never rewritten here): kind of
   // each expert's last row tile by its r = m mod bm rows (include/moe_sm100.h).
@@ -61,20 +98,20 @@ __device__ __forceinline__ void plan_body(long long m, int E, int H, int N, int 
   const long long row_tiles = (m + bm - 1) / bm;
   {
     // GEMV only when the other tasks' tiles cover the GEMV streams (MOE_GEMV_MIN_TILES; plan.cpp)
-    long long other_tiles, gemv_any;
-    block_scan_incl(m > 0 && kind != MOE_KIND_GEMV ? row_tiles * col_tiles : 0, s_warp, &other_tiles);
-    block_scan_incl(m > 0 && kind == MOE_KIND_GEMV ? 1 : 0, s_warp, &gemv_any);
+    long long v4[4] = {m > 0 && kind != MOE_KIND_GEMV ? row_tiles * col_tiles : 0, m > 0 && kind == MOE_KIND_GEMV ? 1 : 0,
+                       0, 0};
+    long long t4[4];
+    block_scan_incl4(v4, s_warp4, t4);
+    const long long other_tiles = t4[0], gemv_any = t4[1];
     if (gemv_any > 0 && other_tiles < MOE_GEMV_MIN_TILES) kind = kind_nogemv;
   }
   const long long nu = m > 0 && kind != MOE_KIND_GEMV ? row_tiles * col_tiles : 0;   // nu(T_t); GEMV: no tiles
-  long long rows_total, tiles_total, ne_total;
-  const long long rows_incl = block_scan_incl(m, s_warp, &rows_total);
-  block_scan_incl(nu, s_warp, &tiles_total);                       // total tiles
-  const long long ne_incl = block_scan_incl(nu > 0 ? 1 : 0, s_warp, &ne_total);
   // MOE_ORDER_LIGHT_LAST: heavy non-empty tasks first, then the light ones (both in expert order)
   const bool heavy = nu > 0 && m > MOE_LIGHT_ROWS;
-  long long heavy_total;
-  const long long heavy_incl = block_scan_incl(heavy ? 1 : 0, s_warp, &heavy_total);
+  long long sc4[4] = {m, nu, nu > 0 ? 1 : 0, heavy ? 1 : 0}, tot4[4];
+  block_scan_incl4(sc4, s_warp4, tot4);                            // rows, tiles, non-empty, heavy
+  const long long rows_incl = sc4[0], ne_incl = sc4[2], heavy_incl = sc4[3];
+  const long long rows_total = tot4[0], tiles_total = tot4[1], ne_total = tot4[2], heavy_total = tot4[3];
   const int M = (int)ne_total;                                      // |eta|
   const int M_pad = E <= 32 ? 32 : (E + 31) / 32 * 32;
   const bool overflow = rows_total >= INT_MAX || tiles_total >= INT_MAX;

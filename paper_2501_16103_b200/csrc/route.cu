@@ -210,6 +210,10 @@ __global__ void __launch_bounds__(kChunk)
   const int c = blockIdx.x, e = blockIdx.y;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int i = threadIdx.x;                         // thread = expert for the scan
+  // With a plan the grid has one more column (e == E): block (0, E) only plans, in parallel with the
+  // compaction blocks, instead of after block (0, 0)'s compaction (the planner reads counts only).
+  const bool planner = e == E;
+  if (planner && c != 0) return;
   long long tot = 0, before = 0;
   if (i < E) {
 #pragma unroll 8
@@ -221,6 +225,10 @@ __global__ void __launch_bounds__(kChunk)
   }
   long long all;
   const long long incl = moe::dplan::block_scan_incl(tot, s_warp, &all);
+  if (planner) {
+    moe::dplan::plan_body(i < E ? tot : 0, E, H, N, bm, bn, flags, blob);
+    return;
+  }
   if (i == e) s_base = (int)(incl - tot + before);
   const bool lead = c == 0 && e == 0;
   if (lead) {
@@ -252,7 +260,6 @@ __global__ void __launch_bounds__(kChunk)
     token_idx[pos] = t;
     if (slot) slot[pos] = hit;
   }
-  if (lead && blob) moe::dplan::plan_body(i < E ? tot : 0, E, H, N, bm, bn, flags, blob);
 }
 
 __global__ void __launch_bounds__(moe::dplan::kPlanThreads)
@@ -358,7 +365,7 @@ moe_status route_impl(const int32_t* topk, int64_t T, int32_t k, int32_t E, int3
   const bool force_split = (route_flags & MOE_ROUTE_THREE_KERNELS) != 0;
   if ((int64_t)n_chunks * E <= kPlaceMaxCells && T > 0 && !force_split) {
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(n_chunks, E);
+    cfg.gridDim = dim3(n_chunks, E + (blob ? 1 : 0));   // + the planner column
     cfg.blockDim = dim3(kChunk);
     cfg.dynamicSmemBytes = 0;
     cfg.stream = s;
