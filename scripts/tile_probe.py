@@ -66,6 +66,9 @@ def main():
     for case in args.cases.split(","):
         parts = case.split(":")
         cfg, bm, bn, flags, order = parts[:5]
+        seed = 0
+        if "@" in cfg:                              # cfg@seed: another routing draw of the same config
+            cfg, seed = cfg.split("@")[0], int(cfg.split("@")[1])
         cat = parts[5] if len(parts) > 5 else "default"
         catalog = None if cat == "default" else () if cat == "none" else tuple(
             tuple(int(x) for x in r.split(".")) for r in cat.split("+"))
@@ -76,15 +79,15 @@ def main():
         else:
             c = synth.CONFIGS[cfg]
             ids_np = None
-        if cfg not in cache:
+        if (cfg, seed) not in cache:
             cache.clear()
-            ids = torch.from_numpy(synth.route(c) if ids_np is None else ids_np).cuda()
+            ids = torch.from_numpy(synth.route(c, seed) if ids_np is None else ids_np).cuda()
             counts, row_off, tok, _, _ = M.moe_route(ids, c.E)
             X = synth.make_x_torch(0, c.T, c.H, device="cuda")
             W = synth.make_w_torch(0, c.E, c.H, c.N, device="cuda")
             Y = torch.empty((tok.numel(), c.N), dtype=torch.bfloat16, device="cuda")
-            cache[cfg] = (counts.cpu().numpy(), tok, X, W, Y)
-        counts_h, tok, X, W, Y = cache[cfg]
+            cache[(cfg, seed)] = (counts.cpu().numpy(), tok, X, W, Y)
+        counts_h, tok, X, W, Y = cache[(cfg, seed)]
         plan = M.Plan(counts_h, c.H, c.N, int(bm), int(bn), int(flags) | ORDER[order], catalog=catalog)
         ms, mn = time_gemm(plan, X, tok, W, Y, flush, args.reps)
         tf = c.flops / (ms * 1e-3) / 1e12
