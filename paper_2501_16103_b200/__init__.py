@@ -40,8 +40,29 @@ class _Rule(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_int32), ("m_max", ctypes.c_int32)]
 
 
+def parse_catalog(text: str):
+    """'kind.m_max+kind.m_max' (e.g. '2.4+1.64'), 'none' (one strategy) or 'default' -> a catalog argument."""
+    text = text.strip()
+    if text in ("", "default"):
+        return None
+    if text == "none":
+        return ()
+    rules = tuple(tuple(int(x) for x in r.split(".")) for r in text.split("+"))
+    if len(rules) > MOE_MAX_RULES or any(len(r) != 2 for r in rules):
+        raise ValueError(f"MOE_TILE_CATALOG: at most {MOE_MAX_RULES} 'kind.m_max' rules, got {text!r}")
+    return rules
+
+
+# SURVEY §5 config override: the tile-strategy catalog of plans built without an explicit one, read once at
+# import (the library itself reads no environment; the catalog reaches it as plan arguments).
+ENV_CATALOG = parse_catalog(os.environ.get("MOE_TILE_CATALOG", ""))
+
+
 def _rules(catalog):
-    """None -> built-in catalog (n_rules = -1); a sequence of (kind, m_max) -> the rule array."""
+    """None -> MOE_TILE_CATALOG if set, else the built-in catalog (n_rules = -1); a sequence of (kind, m_max)
+    -> the rule array."""
+    if catalog is None:
+        catalog = ENV_CATALOG
     if catalog is None:
         return None, -1
     arr = (_Rule * max(len(catalog), 1))(*[_Rule(int(k), int(m)) for k, m in catalog])

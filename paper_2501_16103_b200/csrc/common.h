@@ -6,6 +6,8 @@
 #include <cstdio>
 #include <string>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "moe_sm100.h"
 #include "moe_sm100_ep.h"
 #include "moe_sm100_ffn.h"
@@ -43,6 +45,16 @@ cudaError_t preload_gemm_kernels();
 cudaError_t preload_route_kernels();
 cudaError_t preload_ep_kernels();
 cudaError_t preload_plan_kernel();
+
+// NVTX range over a host entry point (route / plan / gemm / ep step / combine; SURVEY §5 tracing): nsys or
+// ncu --nvtx attribute the launches it encloses to it.  Header-only NVTX 3: without a tool attached a
+// push / pop is a call through a null-injection stub.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 }  // namespace moe
 

@@ -268,6 +268,7 @@ moe_status moe_ep_create(const void* unique_id, int32_t rank, int32_t world, int
 moe_status moe_ep_forward(moe_ep* ep, const int32_t* topk, int64_t T, int32_t k, const void* X, int64_t H,
                           int32_t x_dtype, const void* W, int64_t N, const float* w_scale, void* out,
                           int32_t out_dtype, void* stream) {
+  moe::NvtxRange nvtx("moe_ep_forward");
   moe::clear_error();
   if (!ep || (T > 0 && (!topk || !X || !out)) || !W) MOE_FAIL(MOE_ERR_INVALID, "moe_ep_forward: null argument");
   if (x_dtype != MOE_DTYPE_BF16 && x_dtype != MOE_DTYPE_E4M3)

@@ -67,6 +67,7 @@ inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 moe_status ep_peer_forward(moe_ep* ep, const int32_t* topk, int64_t T, int32_t k, const void* X, int64_t H,
                            int32_t x_dtype, const void* W, int64_t N, const float* w_scale, void* out,
                            int32_t out_dtype, cudaStream_t s) {
+  moe::NvtxRange nvtx("moe_ep_forward (peer)");
   PeerState& P = *ep->peer;
   if (!P.connected) MOE_FAIL(MOE_ERR_INVALID, "moe_ep_forward: peer handle not connected (moe_ep_peer_connect)");
   const int G = ep->world, El = ep->E / G;
@@ -104,11 +105,14 @@ moe_status ep_peer_forward(moe_ep* ep, const int32_t* topk, int64_t T, int32_t k
     ep->plan_N = N;
   }
   // 1. dispatch: per-destination deduplicated rows, stored into the owners' receive buffers
-  PEER_TRY(moe_ep_dispatch_plan(topk, T, k, ep->E, G, P.counts2, P.send_off, P.send_tok, P.send_meta, s));
-  PEER_CUDA(ep_peer_dispatch(X, x_row, P.send_off, P.send_tok, P.send_meta, G, k, ep->rank, P.T_max, P.peers_dev, s));
-  if (G > 1) {                                       // one rank: stream order is the whole protocol
-    PEER_CUDA(ep_peer_signal(P.peers_dev, G, ep->rank, kDispatchWord, P.epoch_dev, true, s));
-    PEER_CUDA(ep_peer_wait(flags_mine, G, kDispatchWord, P.epoch_dev, P.status_dev, P.timeout_ns, s));
+  {
+    moe::NvtxRange nvtx("ep_dispatch");
+    PEER_TRY(moe_ep_dispatch_plan(topk, T, k, ep->E, G, P.counts2, P.send_off, P.send_tok, P.send_meta, s));
+    PEER_CUDA(ep_peer_dispatch(X, x_row, P.send_off, P.send_tok, P.send_meta, G, k, ep->rank, P.T_max, P.peers_dev, s));
+    if (G > 1) {                                     // one rank: stream order is the whole protocol
+      PEER_CUDA(ep_peer_signal(P.peers_dev, G, ep->rank, kDispatchWord, P.epoch_dev, true, s));
+      PEER_CUDA(ep_peer_wait(flags_mine, G, kDispatchWord, P.epoch_dev, P.status_dev, P.timeout_ns, s));
+    }
   }
   // 2. local experts: buckets over the received ids (empty rows are -1), device plan
   PEER_TRY(moe_route_plan(meta_mine, R, k, El, P.counts_l, P.row_off_l, P.tok_l, P.slot_l, nullptr, ep->plan, s));
@@ -121,6 +125,7 @@ moe_status ep_peer_forward(moe_ep* ep, const int32_t* topk, int64_t T, int32_t k
   PEER_CUDA(cudaEventRecord(ep->gemm_ev[1], s));
   ep->gemm_timed = true;
   // 4. every peer's GEMM has stored this rank's rows
+  moe::NvtxRange nvtx_combine("ep_combine");
   if (G > 1) {
     PEER_CUDA(ep_peer_signal(P.peers_dev, G, ep->rank, kCombineWord, P.epoch_dev, false, s));
     PEER_CUDA(ep_peer_wait(flags_mine, G, kCombineWord, P.epoch_dev, P.status_dev, P.timeout_ns, s));

@@ -74,6 +74,7 @@ __global__ void __launch_bounds__(kCombineThreads)
 extern "C" moe_status moe_combine(const void* Y, int32_t y_dtype, int64_t T, int32_t k, int64_t N,
                                   const int32_t* token_idx, const int32_t* slot, const int32_t* row_off, int32_t E,
                                   const float* topk_w, void* out, int32_t out_dtype, void* stream) {
+  moe::NvtxRange nvtx("moe_combine");
   moe::clear_error();
   if (T < 0 || k < 1 || k > 32 || E < 1) MOE_FAIL(MOE_ERR_INVALID, "moe_combine: T=%lld k=%d E=%d", (long long)T, k, E);
   if (N <= 0 || N % 8) MOE_FAIL(MOE_ERR_INVALID, "moe_combine: N=%lld must be a positive multiple of 8", (long long)N);

@@ -2053,6 +2053,7 @@ static moe_status gemm_launch(const moe_plan* plan, const void* X, int64_t T, co
                               const void* W, void* Y, int32_t y_dtype, void* stream, long long* prof,
                               const int32_t* y_row_map = nullptr, const void* W2 = nullptr, bool fp8 = false,
                               const float* scale = nullptr, const unsigned long long* y_row_ptr = nullptr) {
+  moe::NvtxRange nvtx(W2 ? "moe_gemm_swiglu" : fp8 ? "moe_gemm_fp8" : "moe_gemm");
   moe::clear_error();
   if (!plan) MOE_FAIL(MOE_ERR_INVALID, "moe_gemm: null plan");
   moe::BlobView v;

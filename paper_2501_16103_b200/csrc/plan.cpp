@@ -355,6 +355,7 @@ moe_status moe_plan_create(const int32_t* counts, int32_t E, int64_t H, int64_t 
 moe_status moe_plan_create_catalog(const int32_t* counts, int32_t E, int64_t H, int64_t N, int32_t bm, int32_t bn,
                                    uint32_t flags, const moe_tile_rule* rules, int32_t n_rules, void* stream,
                                    moe_plan** out) {
+  moe::NvtxRange nvtx("moe_plan_create");
   moe::clear_error();
   if (!out) MOE_FAIL(MOE_ERR_INVALID, "moe_plan_create: null out");
   *out = nullptr;

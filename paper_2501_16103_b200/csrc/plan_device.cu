@@ -35,6 +35,7 @@ __global__ void __launch_bounds__(kPlanThreads)
 }  // namespace
 
 extern "C" moe_status moe_plan_device(moe_plan* plan, const int32_t* counts_dev, void* stream) {
+  moe::NvtxRange nvtx("moe_plan_device");
   moe::clear_error();
   if (!plan || !counts_dev) MOE_FAIL(MOE_ERR_INVALID, "moe_plan_device: null argument");
   int32_t E, H, N, bm, bn;

@@ -331,6 +331,7 @@ __global__ void __launch_bounds__(kChunk) route_scatter_kernel(const int32_t* __
 moe_status route_impl(const int32_t* topk, int64_t T, int32_t k, int32_t E, int32_t* counts, int32_t* row_off,
                       int32_t* token_idx, int32_t* slot, int32_t* status, moe_plan* plan, uint32_t route_flags,
                       void* stream) {
+  moe::NvtxRange nvtx(plan ? "moe_route_plan" : "moe_route");
   moe::clear_error();
   if (T < 0 || k < 1 || k > 32 || E < 1 || E > kMaxE)
     MOE_FAIL(MOE_ERR_INVALID, "moe_route: T=%lld k=%d E=%d outside T>=0, 1<=k<=32, 1<=E<=1024", (long long)T, k, E);

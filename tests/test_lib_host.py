@@ -326,3 +326,26 @@ def test_planner_gemv_strategy_by_hand():
     for bad in ([(2, 5)], [(2, 4)]):
         with pytest.raises(moe_lib.MoeError):
             moe_lib.moe_plan_build([1, 1], 64, 1024, 256, 256 if bad == [(2, 4)] else 512, catalog=bad)
+
+
+def test_tile_catalog_env_override():
+    """MOE_TILE_CATALOG overrides the catalog of plans built without an explicit one (read by the
+    binding at import; the library reads no environment)."""
+    import subprocess
+    import sys
+    M = moe_lib
+    assert M.parse_catalog("default") is None and M.parse_catalog("none") == ()
+    assert M.parse_catalog("2.4+1.64") == ((2, 4), (1, 64))
+    with pytest.raises(ValueError):
+        M.parse_catalog("1.16+1.32+2.4")
+    code = ("import sys; sys.path.insert(0, %r); import paper_2501_16103_b200 as M; "
+            "b = M.parse_plan_blob(M.moe_plan_build([1029, 1009, 1020, 1047, 1026, 1000, 1032, 1029], 4096, 14336, "
+            "256, 512)); print(b['catalog'])") % ROOT
+    out = {}
+    for env in ("none", "1.64", ""):
+        e = dict(os.environ, MOE_TILE_CATALOG=env)
+        out[env] = subprocess.run([sys.executable, "-c", code], env=e, capture_output=True, text=True,
+                                  check=True).stdout.strip()
+    assert out["none"] == "()"
+    assert out["1.64"] == "((1, 64),)"
+    assert out[""] == str(M.DEFAULT_CATALOG)
