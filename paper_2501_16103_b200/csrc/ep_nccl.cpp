@@ -242,8 +242,9 @@ moe_status moe_ep_create(const void* unique_id, int32_t rank, int32_t world, int
   ep->bm = bm;
   ep->bn = bn;
   // With one rank the combine never leaves the device: fuse it into the GEMM epilogue (moe_gemm_rowptr,
-  // which has no bm = 64 decode-tile form: those tiles keep the send buffer + exchange).  Between
-  // GPUs the same path needs the peers' buffers mapped (CUDA IPC), not built yet: NCCL exchange.
+  // which has no bm = 64 decode-tile form: those tiles keep the send buffer + exchange).  Between GPUs
+  // this NCCL transport exchanges result rows; the peer transport (ep_peer.cpp) maps the peers' buffers
+  // and fuses the combine at every world size.
   ep->fused = world == 1 && !(flags & MOE_EP_UNFUSED) && bm != 64;
   ncclUniqueId id;
   std::memcpy(&id, unique_id, sizeof(id));

@@ -188,6 +188,9 @@ moe_status moe_ep_peer_create(int32_t rank, int32_t world, int32_t E, int32_t bm
       max_y_row_bytes % 16 || world * max_tokens * k >= INT32_MAX)
     MOE_FAIL(MOE_ERR_INVALID, "moe_ep_peer_create: max_tokens %lld, k %d, row bytes %lld / %lld", (long long)max_tokens,
              k, (long long)max_x_row_bytes, (long long)max_y_row_bytes);
+  // the step's GEMM stores through row pointers (moe_gemm_rowptr): no bm = 64 decode-tile form; failing here
+  // keeps every rank out of a step whose GEMM would fail after the dispatch (the peers would time out)
+  if (bm == 64) MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_ep_peer_create: bm = 64 tiles have no row-pointer epilogue");
   auto P = std::make_shared<PeerState>();
   P->T_max = max_tokens;
   P->k = k;

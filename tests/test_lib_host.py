@@ -349,3 +349,14 @@ def test_tile_catalog_env_override():
     assert out["none"] == "()"
     assert out["1.64"] == "((1, 64),)"
     assert out[""] == str(M.DEFAULT_CATALOG)
+
+
+def test_ep_peer_create_rejects_decode_tiles_before_touching_the_device():
+    """ADVICE (round 1, low): the peer step's GEMM stores through row pointers, which have no bm = 64 form —
+    moe_ep_peer_create refuses it up front (argument checks run before any CUDA call, so this runs on CPU)."""
+    L = moe_lib.lib()
+    out = ctypes.c_void_p()
+    blob = (ctypes.c_uint8 * 4096)()
+    st = L.moe_ep_peer_create(0, 2, 8, 64, 256, 16, 2, 8192, 8192, ctypes.byref(out), blob)
+    assert moe_lib.MOE_ERR[st] == "UNSUPPORTED" and not out.value
+    assert b"bm = 64" in L.moe_last_error()
