@@ -72,7 +72,11 @@ def main():
         cat = parts[5] if len(parts) > 5 else "default"
         catalog = None if cat == "default" else () if cat == "none" else tuple(
             tuple(int(x) for x in r.split(".")) for r in cat.split("+"))
-        if cfg.startswith("light"):                 # lightN: N experts of the paper §5 shape, one token each
+        if cfg.startswith("rows"):                  # rowsR_E: E experts of R rows each, Mixtral H / N (tile-kind cost)
+            r_, e_ = (int(x) for x in cfg[4:].split("_"))
+            c = synth.Config(cfg, E=e_, k=1, T=r_ * e_, H=4096, N=14336, routing="custom")
+            ids_np = (np.arange(r_ * e_, dtype=np.int32) // r_)[:, None]
+        elif cfg.startswith("light"):               # lightN: N experts of the paper §5 shape, one token each
             n = int(cfg[5:])
             c = synth.Config(cfg, E=64, k=1, T=n, H=3584, N=2560, routing="custom")
             ids_np = np.arange(n, dtype=np.int32)[:, None]
