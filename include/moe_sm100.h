@@ -154,6 +154,17 @@ typedef struct { int32_t kind; int32_t m_max; } moe_tile_rule;
                                      their accumulator drains (wide pair tiles only): the task has no tiles
                                      (nu = 0, outside TilePrefix and sigma), its W streams while the tensor
                                      cores work on the other tasks                       */
+#define MOE_KIND_RIDE 3           /* an expert of m = 256 R + r rows (R >= 1, 1 <= r <= m_max <= MOE_RIDE_MAX_ROWS)
+                                     in a plan of 256 x 512 pair tiles with N % 512 == 0: its last two row-tile
+                                     slots of each column block are the two 256-column halves of its last full
+                                     row tile, and each also computes the r tail rows x its 256 columns with a
+                                     swap-AB MMA (the staged W block as the M = 256 operand, the tail tokens as
+                                     N = r rounded up to 16) on the same staged K blocks — the tail needs no
+                                     W stream of its own.  Same tile count (ceil(m / 256) per column block),
+                                     same mapping; kernels without the strategy (FP8, gated, contiguous-row A)
+                                     run those slots as the plain wide tiles.  Elsewhere the
+                                     rule does not match (the catalog's next rule applies).            */
+#define MOE_RIDE_MAX_ROWS 32
 #define MOE_GEMV_MAX_ROWS 4
 #define MOE_GEMV_MIN_TILES 128    /* GEMV rules apply only when the plan's other tasks have >= this many tiles
                                      (their tensor work must cover the GEMV streams); otherwise those tasks

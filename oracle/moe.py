@@ -71,25 +71,31 @@ def tiles_of(rows: int, N: int, bm: int, bn: int) -> int:
 
 KIND_GEMV = 2   # a whole task of <= m_max rows computed as a CUDA-core GEMV, outside the tile space
 GEMV_MIN_TILES = 128
+KIND_RIDE = 3   # the tail rows ride on the two 256-column halves of the expert's last full row tile
 
 
-def tail_kind(m: int, bm: int, catalog) -> int:
+def tail_kind(m: int, bm: int, catalog, bn: int | None = None, N: int | None = None) -> int:
     """The tiling strategy of an expert's last row tile ("categorized into several
     pre-defined tiling strategies"; R6): r = m mod bm rows (0: no partial tile); the first
     catalog rule (kind, m_max) with r <= m_max gives the kind, else kind 0.  A GEMV rule (kind 2) applies
-    only to a task that is a single partial row tile (m < bm): the whole task is then that strategy."""
+    only to a task that is a single partial row tile (m < bm): the whole task is then that strategy.  A
+    RIDE rule (kind 3) applies only to a task with a full row tile (m > bm) in a plan of 256 x 512 tiles
+    whose column tiles all lie inside N."""
     r = int(m) % bm
     if int(m) <= 0 or r == 0:
         return 0
     for kind, m_max in catalog:
         if int(kind) == KIND_GEMV and int(m) >= bm:
             continue
+        if int(kind) == KIND_RIDE and not (int(m) > bm and bm == 256 and bn == 512 and N is not None
+                                           and int(N) % 512 == 0):
+            continue
         if r <= m_max:
             return int(kind)
     return 0
 
 
-def make_tasks(counts, bm: int, bn: int, split_tail: bool = False, catalog=()) -> list[dict]:
+def make_tasks(counts, bm: int, bn: int, split_tail: bool = False, catalog=(), N: int | None = None) -> list[dict]:
     """One task per expert with tile bm x bn.
 
     The mapping is unchanged by the catalog, but an expert's LAST row tile (rows
@@ -98,7 +104,7 @@ def make_tasks(counts, bm: int, bn: int, split_tail: bool = False, catalog=()) -
     rounded up to 16.  split_tail = the catalog ((1, bm),).  The tile partition, hence Y, is identical."""
     if split_tail:
         catalog = ((1, bm),)
-    return [dict(expert=e, row_begin=0, rows=int(m), bm=bm, bn=bn, kind=tail_kind(m, bm, catalog))
+    return [dict(expert=e, row_begin=0, rows=int(m), bm=bm, bn=bn, kind=tail_kind(m, bm, catalog, bn, N))
             for e, m in enumerate(counts)]
 
 
@@ -150,12 +156,12 @@ def plan(counts, N: int, bm: int, bn: int, pad_mode: str = "max", warp_size: int
     """Host-side plan: nu per task, sigma (non-empty tasks, natural order or a §4.2
     ordering), TilePrefix (Alg. 1 over eta in sigma's order), padded per P:203."""
     if tasks is None:
-        tasks = make_tasks(counts, bm, bn, split_tail, catalog)
+        tasks = make_tasks(counts, bm, bn, split_tail, catalog, N)
         # GEMV rules apply only when the other tasks have >= GEMV_MIN_TILES tiles (their tensor work must
         # cover the GEMV streams, DESIGN.md §6.8); otherwise those tasks take the next rule.
         other = sum(tiles_of(t["rows"], N, t["bm"], t["bn"]) for t in tasks if t["kind"] != KIND_GEMV)
         if any(t["kind"] == KIND_GEMV for t in tasks) and other < GEMV_MIN_TILES:
-            tasks = make_tasks(counts, bm, bn, split_tail, [r for r in catalog if int(r[0]) != KIND_GEMV])
+            tasks = make_tasks(counts, bm, bn, split_tail, [r for r in catalog if int(r[0]) != KIND_GEMV], N)
     # Alg. 3's per-task strategies: a GEMV task has no tiles (nu = 0, so the non-empty stage leaves it out
     # of sigma / TilePrefix); its rows are computed by the GEMV strategy (DESIGN.md R6, §6.8).
     nu = [0 if t.get("kind", 0) == KIND_GEMV else tiles_of(t["rows"], N, t["bm"], t["bn"]) for t in tasks]
@@ -185,6 +191,17 @@ def decode(pl: dict, row_off, B: int) -> dict:
     c0 = ct * task["bn"]
     c1 = min(c0 + task["bn"], pl["N"])
     kind = 1 if (task["kind"] == 1 and rt == R - 1) else 0          # the tail tile of a split task
+    if task["kind"] == KIND_RIDE and rt >= R - 2:
+        # RIDE: slots R-2 / R-1 of the column block are its two 256-column halves, each computing the body
+        # rows of row tile R-2 and the tail rows [(R-1) bm, m) — together the rows and columns of slots R-2
+        # and R-1 of the plain partition
+        half = rt - (R - 2)
+        r0 = int(row_off[e]) + task["row_begin"] + (R - 2) * task["bm"]
+        r1 = int(row_off[e]) + task["row_begin"] + task["rows"]
+        c0, c1 = c0 + half * (task["bn"] // 2), min(c0 + (half + 1) * (task["bn"] // 2), pl["N"])
+        tail = task["rows"] - (R - 1) * task["bm"]
+        return dict(h=h, task=j, expert=e, l=l, rt=rt, ct=ct, rows=(r0, r1), cols=(c0, c1), kind=KIND_RIDE,
+                    half=half, height=-(-tail // 16) * 16)
     return dict(h=h, task=j, expert=e, l=l, rt=rt, ct=ct, rows=(r0, r1), cols=(c0, c1), kind=kind,
                 height=-(-(r1 - r0) // 16) * 16 if kind == 1 else task["bm"])
 

@@ -33,6 +33,7 @@ MOE_ROUTE_NO_SMALL, MOE_ROUTE_THREE_KERNELS = 1, 2
 MOE_KIND_WIDE, MOE_KIND_SWAP, MOE_MAX_RULES = 0, 1, 2
 MOE_DEFAULT_SWAP_MAX = 64                       # include/moe_sm100.h: the swap-AB rule of tests and A/B runs
 MOE_KIND_GEMV, MOE_DEFAULT_GEMV_MAX, MOE_GEMV_MIN_TILES = 2, 4, 128
+MOE_KIND_RIDE, MOE_RIDE_MAX_ROWS = 3, 32
 DEFAULT_CATALOG = ((MOE_KIND_GEMV, MOE_DEFAULT_GEMV_MAX),)   # the built-in catalog of wide pair plans
 
 

@@ -137,8 +137,12 @@ moe_status moe_plan_build_catalog(const int32_t* counts, int32_t E, int64_t H, i
     if (n_rules > MOE_MAX_RULES) MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_plan_build: at most %d catalog rules", MOE_MAX_RULES);
     if (n_rules > 0 && !rules) MOE_FAIL(MOE_ERR_INVALID, "moe_plan_build: null catalog");
     for (int32_t i = 0; i < n_rules; ++i) {
-      if (rules[i].kind != MOE_KIND_WIDE && rules[i].kind != MOE_KIND_SWAP && rules[i].kind != MOE_KIND_GEMV)
+      if (rules[i].kind != MOE_KIND_WIDE && rules[i].kind != MOE_KIND_SWAP && rules[i].kind != MOE_KIND_GEMV &&
+          rules[i].kind != MOE_KIND_RIDE)
         MOE_FAIL(MOE_ERR_INVALID, "moe_plan_build: catalog rule %d: kind %d", i, rules[i].kind);
+      if (rules[i].kind == MOE_KIND_RIDE && (!(bm == 256 && bn > 256) || rules[i].m_max > MOE_RIDE_MAX_ROWS))
+        MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_plan_build: MOE_KIND_RIDE needs wide pair tiles (bm = 256, bn > 256) and "
+                 "m_max <= %d (got %d x %d, m_max %d)", MOE_RIDE_MAX_ROWS, bm, bn, rules[i].m_max);
       if (rules[i].kind == MOE_KIND_SWAP && !pair_blocks)
         MOE_FAIL(MOE_ERR_UNSUPPORTED, "moe_plan_build: MOE_KIND_SWAP needs bm = 256 and bn >= 256 (got %d x %d)", bm, bn);
       if (rules[i].kind == MOE_KIND_GEMV && (!(bm == 256 && bn > 256) || rules[i].m_max > MOE_GEMV_MAX_ROWS))
@@ -148,12 +152,15 @@ moe_status moe_plan_build_catalog(const int32_t* counts, int32_t E, int64_t H, i
     }
   }
   bool allow_gemv = true;
+  // RIDE: a full row tile to ride on (m > bm), 512-column tiles that all lie inside N (two 256-column halves)
+  const bool ride_shape = bm == 256 && bn == 512 && N % bn == 0;
   auto kind_of = [&](int64_t m) -> int32_t {
     const int64_t r = m % bm;
     if (m <= 0 || r == 0) return MOE_KIND_WIDE;
     for (int32_t i = 0; i < n_cat; ++i) {
       // GEMV: whole single-row-tile tasks only, and only when the other tasks' tiles cover it
       if (cat[i].kind == MOE_KIND_GEMV && (m >= bm || !allow_gemv)) continue;
+      if (cat[i].kind == MOE_KIND_RIDE && (m < bm || !ride_shape)) continue;
       if (r <= cat[i].m_max) return cat[i].kind;
     }
     return MOE_KIND_WIDE;
@@ -330,10 +337,11 @@ float* plan_sk_ws(const moe_plan* p, int32_t** cnt, int32_t* ctas) {
   *ctas = p->sk_ctas;
   return p->sk_ws;
 }
-// The catalog (header words 12-15) holds a swap-AB rule: the launch needs the two-strategy kernel.
+// The catalog (header words 12-15) holds a swap-AB or ride rule: the launch needs the two-strategy kernel.
 bool plan_has_swap(const moe_plan* p) {
   for (int i = 0; i < MOE_MAX_RULES; ++i)
-    if (p->blob[12 + 2 * i] == MOE_KIND_SWAP && p->blob[13 + 2 * i] > 0) return true;
+    if ((p->blob[12 + 2 * i] == MOE_KIND_SWAP || p->blob[12 + 2 * i] == MOE_KIND_RIDE) && p->blob[13 + 2 * i] > 0)
+      return true;
   return false;
 }
 }  // namespace moe

@@ -85,9 +85,11 @@ __device__ __forceinline__ void plan_body(long long m, int E, int H, int N, int 
   {
     const long long r = m % bm;
     if (m > 0 && r > 0) {
+      const bool ride_shape = bm == 256 && bn == 512 && N % bn == 0;   // MOE_KIND_RIDE's tiles (plan.cpp)
       for (int i = MOE_MAX_RULES - 1; i >= 0; --i) {               // the first matching rule wins
         const int32_t ki = blob[12 + 2 * i];
         if (r > blob[13 + 2 * i]) continue;
+        if (ki == MOE_KIND_RIDE && (m < bm || !ride_shape)) continue;   // needs a full row tile to ride on
         if (ki != MOE_KIND_GEMV) kind_nogemv = ki;
         if (ki != MOE_KIND_GEMV || m < bm) kind = ki;              // GEMV: whole single-tile tasks only
       }

@@ -285,12 +285,14 @@ def test_planner_catalog_matches_oracle():
         E = rng.randint(1, 200)
         counts = np.array([0 if rng.random() < 0.3 else rng.randint(1, 3000) for _ in range(E)])
         bn = rng.choice([256, 512])
-        kinds = [0, 1, 2] if bn == 512 else [0, 1]
-        rules = [(k_, rng.randint(0, 4) if k_ == 2 else rng.randint(0, 256))
+        kinds = [0, 1, 2, 3] if bn == 512 else [0, 1]
+        rules = [(k_, rng.randint(0, 4) if k_ == 2 else rng.randint(0, 32) if k_ == 3 else rng.randint(0, 256))
                  for k_ in (rng.choice(kinds) for _ in range(rng.randint(0, 2)))]
         if rng.random() < 0.3:
             counts = np.where(counts > 0, counts % 7, 0)                   # many 1-6 row experts
-        N = 8 * rng.randint(1, 3000)
+        elif rng.random() < 0.3:
+            counts = np.where(counts > 0, 256 * rng.randint(1, 5) + counts % 40, 0)   # short tails on full tiles
+        N = 8 * rng.randint(1, 3000) if rng.random() < 0.5 else 512 * rng.randint(1, 30)
         _compare(counts, N, 256, bn, rng.choice(["max", "repeat"]), catalog=rules,
                  order=rng.choice(["natural", "half_interval", "light_last"]))
         if all(k_ != 2 for k_, _ in rules):                                # swap / wide: mapping unchanged
@@ -306,6 +308,19 @@ def test_planner_catalog_matches_oracle():
         moe_lib.moe_plan_build([5, 5], 64, 1024, 256, 512, catalog=[(1, 64), (0, 9), (1, 200)])
     with pytest.raises(moe_lib.MoeError):
         moe_lib.moe_plan_build([5, 5], 64, 1024, 256, 512, catalog=[(7, 64)])
+    # RIDE: tails of <= m_max rows on experts with a full row tile, 512-column tiles inside N
+    cnt = [1029, 1009, 256, 300, 257, 20, 0]
+    p = moe_lib.parse_plan_blob(moe_lib.moe_plan_build(cnt, 64, 14336, 256, 512, catalog=[(2, 4), (3, 32)]))
+    assert p["params"][:, 3].tolist() == [3, 0, 0, 0, 3, 0, 0]
+    base = moe_lib.parse_plan_blob(moe_lib.moe_plan_build(cnt, 64, 14336, 256, 512, catalog=()))
+    assert np.array_equal(base["prefix"], p["prefix"]) and np.array_equal(base["params"][:, 6:], p["params"][:, 6:])
+    p = moe_lib.parse_plan_blob(moe_lib.moe_plan_build(cnt, 64, 1408, 256, 512, catalog=[(3, 32)]))
+    assert p["params"][:, 3].tolist() == [0] * 7                       # N % 512 != 0: no ride
+    for bad in ([(3, 33)],):
+        with pytest.raises(moe_lib.MoeError):
+            moe_lib.moe_plan_build(cnt, 64, 14336, 256, 512, catalog=bad)
+    with pytest.raises(moe_lib.MoeError):
+        moe_lib.moe_plan_build(cnt, 64, 14336, 256, 256, catalog=[(3, 32)])
 
 
 def test_planner_gemv_strategy_by_hand():

@@ -223,6 +223,35 @@ def test_split_tail_tasks_cover_exactly_once():
                 assert d["rows"][1] - d["rows"][0] == 256 or m % 256 == 0 or d["rt"] < m // 256
 
 
+def test_ride_tasks_cover_exactly_once():
+    """MOE_KIND_RIDE: an expert of 256 R + r rows (r <= 32) keeps its ceil(m/256) tile slots
+    per column block; slots R-2 / R-1 are the two 256-column halves of row tile R-2 plus the tail rows, and Y is
+    still tiled exactly once.  Experts without a full row tile, or N % 512 != 0, do not ride."""
+    rng = random.Random(11)
+    for _ in range(25):
+        E = rng.randint(1, 6)
+        counts = [0 if rng.random() < 0.2 else rng.choice([rng.randint(1, 700), 256 * rng.randint(1, 3) +
+                                                           rng.randint(1, 40)]) for _ in range(E)]
+        if sum(counts) == 0:
+            counts[0] = 300
+        N = rng.choice([512, 1024, 1536])
+        p = moe.plan(counts, N, 256, 512, catalog=((3, 32),))
+        assert p["total"] == moe.plan(counts, N, 256, 512)["total"] and p["prefix"] == moe.plan(counts, N, 256, 512)["prefix"]
+        row_off = np.concatenate([[0], np.cumsum(counts)])
+        assert (moe.tile_cover(p, row_off, sum(counts)) == 1).all()
+        for t in p["tasks"]:
+            m = t["rows"]
+            assert (t["kind"] == 3) == (m > 256 and 0 < m % 256 <= 32)
+        for B in range(p["total"]):
+            d = moe.decode(p, row_off, B)
+            m = counts[d["expert"]]
+            if d["kind"] == 3:
+                assert d["rows"] == (row_off[d["expert"]] + (m // 256 - 1) * 256, row_off[d["expert"]] + m)
+                assert d["cols"] == (d["ct"] * 512 + 256 * d["half"], d["ct"] * 512 + 256 * d["half"] + 256)
+                assert d["height"] in (16, 32) and d["height"] - 16 < m % 256 <= d["height"]
+    assert all(t["kind"] == 0 for t in moe.plan([300, 260, 20], 1408, 256, 512, catalog=((3, 32),))["tasks"])
+
+
 # ---- c4 GEMM -----------------------------------------------------------------
 def _route(T, E, k, seed):
     return synth.route_gumbel(seed, T, E, k)
