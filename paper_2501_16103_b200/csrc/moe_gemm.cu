@@ -196,12 +196,14 @@ __device__ __forceinline__ int sk_parts(int total, int grid, int num_kb) {
 
 struct Tile {
   int expert, row0, rows, bn, rt, ct;
-  int kind;     // of THIS tile: 0 = bm rows x bn cols (MOE_KIND_WIDE); 1 = swap-AB tile (MOE_KIND_SWAP)
-  int height;   // kind 1: tail rows rounded up to 16 (the MMA's N)
+  int kind;     // of THIS tile: 0 = bm rows x bn cols (MOE_KIND_WIDE); 1 = swap-AB tile (MOE_KIND_SWAP);
+                // 3 = ride tile (MOE_KIND_RIDE): body row tile rt, 256-column half hh, plus the tail rows
+  int height;   // kind 1 / 3: tail rows rounded up to 16 (the swap MMA's N)
+  int hh, trow0, trows;   // kind 3: the half, the tail's first CSR row and its row count
 };
 
 template <bool kSplit = false>
-__device__ __forceinline__ Tile load_tile(const int32_t* params, int task, int l) {
+__device__ __forceinline__ Tile load_tile(const int32_t* params, int task, int l, bool ride_ok = false) {
   const int4 pa = __ldg(reinterpret_cast<const int4*>(params + task * MOE_PLAN_TASK_WORDS));
   const int4 pb = __ldg(reinterpret_cast<const int4*>(params + task * MOE_PLAN_TASK_WORDS + 4));
   Tile t;
@@ -213,6 +215,7 @@ __device__ __forceinline__ Tile load_tile(const int32_t* params, int task, int l
   t.ct = l / pb.z;
   t.kind = 0;
   t.height = pb.x;
+  t.hh = t.trow0 = t.trows = 0;
   if constexpr (kSplit) {
     // The catalog: a kind-1 task runs its last row tile (rows [rt*bm, rows)) swap-AB.
     if (pa.w == 1 && t.rt == pb.z - 1) {
@@ -221,6 +224,15 @@ __device__ __forceinline__ Tile load_tile(const int32_t* params, int task, int l
       t.height = (tail + 15) / 16 * 16;
       t.row0 += t.rt * pb.x;                       // kind 1: row0 / rows are the tail's
       t.rows = tail;
+    } else if (pa.w == MOE_KIND_RIDE && ride_ok && t.rt >= pb.z - 2) {
+      // The catalog's ride strategy: slots R-2 / R-1 are the two 256-column halves of row
+      // tile R-2; each also computes the r = rows - 256 (R-1) tail rows x its columns (swap-AB MMA).
+      t.kind = 3;
+      t.hh = t.rt - (pb.z - 2);
+      t.rt = pb.z - 2;
+      t.trow0 = t.row0 + (pb.z - 1) * pb.x;
+      t.trows = t.rows - (pb.z - 1) * pb.x;
+      t.height = (t.trows + 15) / 16 * 16;
     }
   }
   return t;
@@ -479,6 +491,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto leader = [&](uint32_t addr) { return kCta == 2 ? mapa_shared(addr, 0) : addr; };
 
   const int a_mode = a.a_mode == 2 ? 2 : kCta == 2 && !kWide ? 1 : a.a_mode;
+  // MOE_KIND_RIDE tiles need the gathered (cp.async) token rows: with contiguous-row A (a_mode 2) the plan's
+  // ride slots run as the plain wide tiles they partition (same rows, same columns).
+  const bool ride_ok = kSplit && kWide && !kGated && a_mode == 1;
   if (threadIdx.x == 0) {
     // full[s] arrivals: A stage done (gather4: one expect_tx per A warp; cp.async: one asynchronous
     // arrive per A thread; contiguous rows: the 1-CTA A thread's expect_tx, while in a pair the
@@ -621,7 +636,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (!next_unit(qi, v, k0, k1)) break;
       int h, task, l;
       map_tile(s_prefix, s_sigma, a.M_pad, v, h, task, l);
-      const Tile t = load_tile<kSplit>(params, task, l);
+      const Tile t = load_tile<kSplit>(params, task, l, ride_ok);
       // kind 0: this CTA's 128 rows of the tile; kind 1 (swap-AB tail): this CTA's half of the
       // tail's `height` token rows, which the MMA reads as its N operand.
       const bool hlf = half_tile<kWide, kGated>(t.rows, t.rt, kSplit && t.kind == 1);
@@ -672,6 +687,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           src[j] = reinterpret_cast<const uint8_t*>(a.X) + (int64_t)tok * row_bytes + ch * 16;
           rowok |= (r < nvalid ? 1u : 0u) << j;
         }
+        // Ride tile (kind 3): this CTA's half of the tail's `height` token rows (<= 16: one row per 16-row
+        // group thread), staged K-major SW128 in the half of the B slot the tile's W does not use; the swap
+        // MMA reads them as its N operand.
+        const bool ride = kSplit && t.kind == 3;
+        const int ride_n = ride ? t.height / kCta : 0;
+        const bool ride_row = rsub < ride_n && (int)rank * ride_n + rsub < (ride ? t.trows : 0);
+        const uint8_t* ride_src = reinterpret_cast<const uint8_t*>(a.X) + ch * 16;
+        if (ride_row) ride_src += (int64_t)__ldg(a.token_idx + t.trow0 + (int)rank * ride_n + rsub) * row_bytes;
+        const uint32_t ride_off = (uint32_t)(1 - t.hh) * (uint32_t)(kBSt / 2) + dst_off;
         // Memory-bound tiles: the A warps (idle but for a few token rows) also pull this CTA's W lines
         // of K block kb + pf_dist into L2 through the load/store path, so the ring's W boxes hit in L2
         // (TMA moves one box per ~330 ns per SM from HBM).
@@ -726,6 +750,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             const bool ok = colok && ((rowok >> j) & 1u);
 #endif
             cp_async_16(dst + j * 16 * 128, ok ? (const void*)(src[j] + kbyte) : (const void*)a.X, ok ? 16u : 0u);
+          }
+          if (kSplit && rsub < ride_n) {
+            const bool ok = colok && ride_row;
+            cp_async_16(sB + s * kBSt + ride_off, ok ? (const void*)(ride_src + kbyte) : (const void*)a.X, ok ? 16u : 0u);
           }
           cp_async_mbar_arrive_noinc(full_bar(s));
         }
@@ -868,12 +896,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (v >= total) break;
       int h, task, l;
       map_tile(s_prefix, s_sigma, a.M_pad, v, h, task, l);
-      const Tile t = load_tile<kSplit>(params, task, l);
+      const Tile t = load_tile<kSplit>(params, task, l, ride_ok);
       const int bnp = t.bn / kHalves;               // columns of one MMA block (gated: 128 gate + 128 up)
       const int bnc = kGated ? 128 : bnp / kCta;    // columns of an MMA block staged by this CTA
       const int n0 = kGated ? t.ct * t.bn : t.ct * t.bn + (int)rank * bnc;   // block h at n0 + h * bnp
       const int nbox = (bnc + (1 << kCS) - 1) >> kCS;
-      const bool one = kCta == 2 && one_box<kWide, kGated>(t.bn, t.ct, a.N, a.w4d, kSplit && t.kind == 1);
+      // (a ride tile stages only its half's block, in the two-box layout: block hh at offset hh * kBSt / 2)
+      const bool one = kCta == 2 && !(kSplit && t.kind == 3) &&
+                       one_box<kWide, kGated>(t.bn, t.ct, a.N, a.w4d, kSplit && t.kind == 1);
       const int n_one = t.ct * t.bn + (int)rank * 256;   // one box: this CTA's 256 columns
       for (int kb = k0; kb < k1; ++kb, ++g) {
         const int s = g % kSt;
@@ -916,6 +946,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                   const int nc = wide_block_cols<kFp8>(t.bn, t.ct, a.N, hf);
                   nh[hf] = t.ct * t.bn + hf * bnp + (int)rank * (nc / 2);
                   nbx[hf] = nc == 0 ? 0 : a.w4d ? nbox : (nc / 2 + (1 << kCS) - 1) >> kCS;
+                  if (kSplit && t.kind == 3 && hf != t.hh) nbx[hf] = 0;   // ride: the tile's half only
                 }
               }
               bytes += kCta * nbx[hf] * kBox;
@@ -982,7 +1013,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++n_tiles;
         int h, task, l;
         map_tile(s_prefix, s_sigma, a.M_pad, v, h, task, l);
-        const Tile t = load_tile<kSplit>(params, task, l);
+        const Tile t = load_tile<kSplit>(params, task, l, ride_ok);
         const bool swap = kSplit && t.kind == 1;
         // kind 0: D[tokens, cols] = A[tokens (K-major)] * B[W block (MN-major)], N = bn.
         // kind 1: D[cols, tokens] = A[W block as MN-major M-operand] * B[tail tokens (K-major)],
@@ -1004,6 +1035,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
+        // Ride tile (kind 3): block 0 = the body (M = 256 rows x the half's 256 columns), block 1 = the tail
+        // (swap-AB: the same staged W as the M = 256 operand, the tail tokens as N = height) in TMEM
+        // columns [256, 256 + height).
+        const bool ride = kSplit && t.kind == 3;
+        if (ride) idesc_blk[1] = idesc_bf16_f32(kPairRows, t.height, /*A MN-major*/ 1, /*B K-major*/ 0);
         if constexpr (kWide) {
           // Wide tiles (TMEM holds one accumulator: block 0 = columns [0,256), block 1 = [256,512)).
           // Block-staggered order so the epilogue drains one block while the other is still
@@ -1043,6 +1079,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int kk = 0; kk < kBK / 16; ++kk)
                   mma_bf16_pair(d, smem_desc_sw128(b0 + kk * 2048, kBBoxBytes, 1024),
                                 smem_desc_sw128(a0 + kk * 32, 16, 1024), idesc, (kb | kk) != 0);
+              } else if (kSplit && ride) {
+                const uint32_t wB = sB + slot(kb) * kBSt + t.hh * (kBSt / 2);         // the half's staged W
+                if (hf == 0) {
+#pragma unroll
+                  for (int kk = 0; kk < kBK / 16; ++kk)
+                    mma_issue<kFp8, 2>(d, smem_desc_sw128(a0 + kk * 32, 16, 1024),
+                                       smem_desc_sw128(wB + kk * kKStep, kBox, 1024), idesc_blk[0], (kb | kk) != 0);
+                } else {
+                  const uint32_t tok = sB + slot(kb) * kBSt + (1 - t.hh) * (kBSt / 2);   // the tail tokens
+#pragma unroll
+                  for (int kk = 0; kk < kBK / 16; ++kk)
+                    mma_bf16_pair(d, smem_desc_sw128(wB + kk * 2048, kBBoxBytes, 1024),
+                                  smem_desc_sw128(tok + kk * 32, 16, 1024), idesc_blk[1], (kb | kk) != 0);
+                }
               } else if (ncol_blk[hf] > 0) {
 #pragma unroll
                 for (int kk = 0; kk < kBK / 16; ++kk)
@@ -1371,7 +1421,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (!next_unit(qi, v, k0, k1)) break;
       int h, task, l;
       map_tile(s_prefix, s_sigma, a.M_pad, v, h, task, l);
-      const Tile t = load_tile<kSplit>(params, task, l);
+      const Tile t = load_tile<kSplit>(params, task, l, ride_ok);
       wait_acc(tfull_bar(acc), acc_phase);
       const long long w0 = kProf ? clock64() : 0;
       tc_fence_after();
@@ -1578,13 +1628,48 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       } else {
         const int bnp = t.bn / kHalves;             // columns of one accumulator block
-        const bool one = kCta == 2 && one_box<kWide, kGated>(t.bn, t.ct, a.N, a.w4d, false);
+        const bool ride = kSplit && t.kind == 3;
+        const bool one = kCta == 2 && !ride && one_box<kWide, kGated>(t.bn, t.ct, a.N, a.w4d, false);
 #pragma unroll 1
         for (int hf = 0; hf < kHalves; ++hf) {
           wait_block1(hf);
+          if (kSplit && ride && hf == 1) {
+            // Ride tile, the tail (TMEM block 1, swap-AB): lane = output column (this CTA's 128 of the half's
+            // 256: t.ct * bn + 256 hh + 128 rank + lane), TMEM column = tail token; as on kind-1 tiles, each
+            // warp stores, token by token, 32 consecutive columns of the token's Y row.
+            const int esz = a.y_f32 ? 4 : 2;
+            const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + kAccCols;
+            const int col = t.ct * t.bn + t.hh * bnp + (int)rank * (bnp / kCta) + q * 32 + lane;
+            const bool col_ok = col < a.N;
+            for (int c = 32 * cg; c < t.height; c += 32 * kEpiGroups) {
+              uint32_t r[32];
+              tmem_ld32(taddr + c, r);
+              const int tk = min(c + lane, t.trows - 1);
+              uint8_t* rp = a.y_row_ptr ? reinterpret_cast<uint8_t*>(__ldg(a.y_row_ptr + t.trow0 + tk))
+                                        : reinterpret_cast<uint8_t*>(a.Y) +
+                                              (a.y_row_map ? (int64_t)__ldg(a.y_row_map + t.trow0 + tk)
+                                                           : (int64_t)t.trow0 + tk) * a.N * esz;
+              tmem_wait_ld();
+              const int ntok = min(32, t.trows - c);
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                uint8_t* row = reinterpret_cast<uint8_t*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(rp), j));
+                if (j < ntok && col_ok) {
+                  if (a.y_f32)
+                    reinterpret_cast<float*>(row)[col] = __uint_as_float(r[j]);
+                  else
+                    reinterpret_cast<__nv_bfloat16*>(row)[col] = __float2bfloat16_rn(__uint_as_float(r[j]));
+                }
+              }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(leader(tempty_bar(1)));
+            continue;
+          }
           // columns of this warp's lanes: the whole block, or (half tile) its first / second half
           const int hw = hlf ? wide_block_cols<kFp8>(t.bn, t.ct, a.N, hf) / 2 : bnp;
-          const int n0 = t.ct * t.bn + hf * bnp + (hlf ? (q >> 1) * hw : 0);
+          const int n0 = t.ct * t.bn + (ride ? t.hh : hf) * bnp + (hlf ? (q >> 1) * hw : 0);
           const int slot = kWide ? hf : acc;        // TMEM block and its tmem-empty barrier
           const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + slot * kAccCols;
           for (int c = 32 * cg; c < hw && (!tma_rows || n0 + c < a.N); c += 32 * kEpiGroups) {
