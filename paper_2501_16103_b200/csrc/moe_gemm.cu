@@ -499,8 +499,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     // arrive per A thread; contiguous rows: the 1-CTA A thread's expect_tx, while in a pair the
     // A tile TMAs of both CTAs complete on the leader's barrier under the B warp's expect_tx), the
     // B warp's expect_tx (leader), and in a pair the peer's relay (leader; not in a_mode 2).
-    const uint32_t a_arrivals = a_mode == 2 ? (kCta == 1 ? 1u : 0u) : a_mode == 0 ? kAWarps : 32 * kAWarps;
-    const uint32_t relay = kCta == 2 && a_mode != 2 ? 1u : 0u;
+    // (a CTA pair's gather4 rows complete on the leader's barrier under the B warp's expect_tx, like a_mode 2)
+    const uint32_t a_arrivals = a_mode == 2 ? (kCta == 1 ? 1u : 0u) : a_mode == 0 ? (kCta == 1 ? kAWarps : 0u)
+                                                                                  : 32 * kAWarps;
+    const uint32_t relay = kCta == 2 && a_mode == 1 ? 1u : 0u;
     const uint32_t full_count = a_arrivals + (rank == 0 ? 1u + relay : 0u);
     for (int s = 0; s < kSt; ++s) {
       mbar_init(full_bar(s), full_count > 0 ? full_count : 1u);   // a pair peer's are unused in a_mode 2
@@ -512,7 +514,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     // queue consumers (one arrival per warp, on the leader's qempty): A warps, MMA warp (leader) or
     // relay lane (peer, unless rows are contiguous), the peer's B warp, epilogue warps
-    const uint32_t q_consumers = kCta == 2 ? 2 * (kAWarps + kEpiWarps) + 2 + (a_mode != 2 ? 1u : 0u)
+    const uint32_t q_consumers = kCta == 2 ? 2 * (kAWarps + kEpiWarps) + 2 + (a_mode == 1 ? 1u : 0u)
                                            : kAWarps + 1 + kEpiWarps;
     for (int i = 0; i < kQ; ++i) {
       mbar_init(qfull_bar(i), 1);
@@ -670,9 +672,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = k0; kb < k1; ++kb, ++g) {
           const int s = g % kSt;
           wait_timed<kProf>(empty_bar(s), ((g / kSt) & 1u) ^ 1u, c_wait);
-          if (lane == 0) mbar_arrive_expect_tx(full_bar(s), kABytes / kAWarps);
-          __syncwarp();
-          if (lane < 8) tma_gather4(&tmX, full_bar(s), sA + s * kABytes + rr * 128, kb * kKB, r0, r1, r2, r3, pol_x);
+          if constexpr (kCta == 2) {
+            if (lane < 8)
+              tma_gather4_pair(&tmX, leader(full_bar(s)), sA + s * kABytes + rr * 128, kb * kKB, r0, r1, r2, r3, pol_x);
+          } else {
+            if (lane == 0) mbar_arrive_expect_tx(full_bar(s), kABytes / kAWarps);
+            __syncwarp();
+            if (lane < 8) tma_gather4(&tmX, full_bar(s), sA + s * kABytes + rr * 128, kb * kKB, r0, r1, r2, r3, pol_x);
+          }
         }
       } else {
         // Byte addressing: a row of X is H * (1 or 2) bytes; thread ch copies bytes [16 ch, 16 ch + 16)
@@ -928,7 +935,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             // both blocks' W columns of this CTA in one box (tmW2 has the 2 x nbox-chunk box)
             const uint32_t fb = leader(full_bar(s));
             uint32_t bytes = (uint32_t)(kCta * 2 * nbox * kBox);
-            if (a_mode == 2) bytes += kCta * kABytes;
+            if (a_mode == 2 || a_mode == 0) bytes += kCta * kABytes;
             if (rank == 0) mbar_arrive_expect_tx(full_bar(s), bytes);
             tma_load_4d_pair(&tmW2, fb, dstB, 0, kb * kKB, n_one >> kCS, t.expert, pol_w);
           } else if constexpr (kCta == 2) {
@@ -951,7 +958,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
               bytes += kCta * nbx[hf] * kBox;
             }
-            if (a_mode == 2) bytes += kCta * kABytes;   // both CTAs' contiguous-row A tiles
+            if (a_mode == 2 || a_mode == 0) bytes += kCta * kABytes;   // both CTAs' contiguous-row A tiles
 #ifdef MOE_EXPERIMENTS
             if (rank == 0) mbar_arrive_expect_tx(full_bar(s), bytes + ((a.experiment & 4) ? kCta * kABytes : 0));
 #else
@@ -1248,7 +1255,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           o[kProfMmaTileGap] = c_gap;
         }
       }
-    } else if (lane == 0 && a_mode != 2) {
+    } else if (lane == 0 && a_mode == 1) {
       // Pair peer: relay "my A stage landed" (local full barrier, fed by cp.async arrivals) to the
       // leader's full barrier, where the MMA issuer waits for both CTAs' bytes.
       uint32_t g = 0;

@@ -189,6 +189,16 @@ __device__ __forceinline__ void tma_gather4(const void* tmap, uint32_t bar, uint
       "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "l"(policy)
       : "memory");
 }
+// The same, for a CTA pair: the bytes complete on the barrier at a cluster address (the leader's full
+// barrier), so the peer's token rows need no relay (cta_group::2 TMA, as the pair's W boxes).
+__device__ __forceinline__ void tma_gather4_pair(const void* tmap, uint32_t bar_cluster, uint32_t dst, int32_t c0,
+                                                 int32_t r0, int32_t r1, int32_t r2, int32_t r3, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2], %8;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar_cluster), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "l"(policy)
+      : "memory");
+}
 __device__ __forceinline__ uint64_t policy_evict_last() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
