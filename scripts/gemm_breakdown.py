@@ -105,6 +105,10 @@ def main():
         "fill_latency_a_cycles": float((p[:, 13] / p[:, 15]).mean()),
         "release_to_reissue_cycles": float((p[:, 14] / p[:, 15]).mean()),
         "mma_cycles_per_stage": float((tot / p[:, 15]).mean()),
+        # finish spread of the persistent CTA pairs (the launch ends with the slowest one)
+        "mma_loop_cycles_quantiles": [float(torch.quantile(tot, q_)) for q_ in (0.0, 0.1, 0.5, 0.9, 1.0)],
+        "mma_loop_cycles_mean": float(tot.mean()),
+        "tiles_per_cta_hist": {int(k_): int(v_) for k_, v_ in zip(*torch.unique(p[:, 6], return_counts=True))},
     }
     if bm == 256:
         q = pall[1::2]
