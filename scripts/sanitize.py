@@ -116,7 +116,20 @@ def main():
     torch.cuda.synchronize()
     assert [p_.status() for p_ in peers] == [0] * G
     assert np.array_equal(torch.cat([o.cpu() for o in pouts]).double().numpy(), omoe.per_slot_outputs(ide, Xe, We))
-    print(f"sanitize workload ok: {n} GEMM variants + CSR rows + both route paths + FFN layer + balanced decode "
+    # round 2, late: ride tiles (tails on the last full row tile) and the pair gather4 A path
+    rng = np.random.default_rng(8)
+    cr = [261, 520, 300, 280, 0, 259]
+    idr = np.repeat(np.arange(len(cr), dtype=np.int32), cr)[:, None]
+    rng.shuffle(idr)
+    Xr, Wr = synth.make_x(8, idr.shape[0], 128, "int"), synth.make_w(8, len(cr), 128, 1024, "int")
+    crr, rrr, trr, _ = omoe.buckets(idr, len(cr))
+    for cat, fl in ((((M.MOE_KIND_RIDE, 32),), 0), (None, M.MOE_A_GATHER4)):
+        Yr, *_ = M.moe_forward(torch.from_numpy(idr).cuda(), torch.from_numpy(Xr).to(torch.bfloat16).cuda(),
+                               torch.from_numpy(Wr).to(torch.bfloat16).cuda(), len(cr),
+                               plan=M.Plan(None, 128, 1024, 256, 512, fl, E=len(cr), catalog=cat), out_dtype=torch.float32)
+        torch.cuda.synchronize()
+        assert np.array_equal(Yr.cpu().double().numpy(), omoe.expert_gemm(Xr, Wr, trr, rrr)), (cat, fl)
+    print(f"sanitize workload ok: {n} GEMM variants + ride tiles + pair gather4 + CSR rows + both route paths + FFN layer + balanced decode "
           f"grid + EP step (loopback, fused combine) + GEMV tasks (natural, light-last) + split-K decode tiles + "
           f"peer-memory EP step")
 
