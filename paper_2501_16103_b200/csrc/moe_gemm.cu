@@ -80,6 +80,22 @@ constexpr int kDefaultAMode = 1;                // A staging: cp.async (see the 
 constexpr uint32_t kTmemCols = 512;             // 2 accumulators x 256 fp32 columns
 constexpr uint32_t kAccCols = 256;
 constexpr int kMaxMPad = 1024;
+#ifndef MOE_TIMELINE
+#define MOE_TIMELINE 0      // 1: %globaltimer stamps per CTA at the kernel's phase boundaries (study builds,
+#endif                      //    scripts/timeline.py)
+#if MOE_TIMELINE
+__device__ unsigned long long g_moe_tl[1024 * 8];
+#define MOE_TL(i)                                                              \
+  do {                                                                         \
+    unsigned long long t_;                                                     \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)::"memory");          \
+    g_moe_tl[blockIdx.x * 8 + (i)] = t_;                                       \
+  } while (0)
+#else
+#define MOE_TL(i) \
+  do {            \
+  } while (0)
+#endif
 #ifndef MOE_L2_PREFETCH
 #define MOE_L2_PREFETCH 8
 #endif
@@ -480,6 +496,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) MOE_TL(0);                   // kernel entry
   // Everything up to the TMEM allocation overlaps the previous kernel (PDL); the plan, the
   // token-index array and X are only touched after griddepcontrol.wait.
   int total = a.total;
@@ -530,6 +547,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   if (warp == kMmaWarp) tmem_alloc<kTmemCols, kCta>(smem_u32(tmem_holder));
   pdl_wait();                                        // routing / plan of this step are complete
+  if (threadIdx.x == 0) MOE_TL(1);                   // after the PDL wait
   // TilePrefix and sigma are adjacent in the blob: one copy into shared memory.
   for (int i = threadIdx.x; i < 2 * a.M_pad; i += blockDim.x) s_prefix[i] = a.plan[MOE_PLAN_HEADER + i];
   if (total < 0) total = __ldg(a.plan + 2);
@@ -568,6 +586,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if constexpr (kCta == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  if (threadIdx.x == 0) MOE_TL(2);                   // prologue done (plan in shared memory, TMEM allocated)
   const int32_t* params = a.plan + a.off_params;
   constexpr int kPairRows = kBM * kCta;                     // rows of a virtual tile
 
@@ -1176,6 +1195,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (kb == k0 && n_tiles > 1) c_gap += clock64() - t_end;  // decode + accumulator hand-off
             }
             wait_timed<kProf>(full_bar(s), par, c_full);                   // both CTAs' bytes landed
+            if (g == 0 && lane == 0) MOE_TL(3);                             // first stage landed (1-CTA / pair)
             long long t_i = 0;
             if constexpr (kProf) {
               const long long now = clock64();
@@ -1241,6 +1261,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           acc_phase ^= 1u;
         }
       }
+      if (lane == 0) MOE_TL(4);                             // last MMA issued
       if constexpr (kProf) {
         if (lane == 0) {
           long long* o = a.prof + blockIdx.x * kProfSlots;
@@ -1713,7 +1734,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     while (gemv_round()) {
     }                                                         // the GEMV units left after the last tile
+    if (ew == 0 && lane == 0) MOE_TL(5);                      // epilogue done, stores in flight
     if (lane == 0) bulk_wait_group<0>();                      // TMA stores complete before exit
+    if (ew == 0 && lane == 0) MOE_TL(6);
     if constexpr (kProf) {
       if (q == 0 && lane == 0) {
         a.prof[blockIdx.x * kProfSlots + kProfEpiWaitFull] = c_wait;
@@ -2086,6 +2109,12 @@ int sm_count_cached() {
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 }  // namespace
+
+#if MOE_TIMELINE
+extern "C" int moe_debug_timeline(unsigned long long* out, int n) {   // study builds only
+  return (int)cudaMemcpyFromSymbol(out, g_moe_tl, sizeof(unsigned long long) * (size_t)n);
+}
+#endif
 
 extern "C" moe_status moe_device_info(int32_t* sm_count, int32_t* cc_major, int32_t* cc_minor) {
   moe::clear_error();
