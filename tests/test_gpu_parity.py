@@ -256,6 +256,8 @@ RAGGED_WIDE_BN = [                  # wide tiles narrower than 512: blocks of bn
                          + [c + (256, 256, "1", M.MOE_SPLIT_TAIL) for c in RAGGED_SPLIT]
                          + [c + (512, 256, a, 0) for c in RAGGED_WIDE for a in ("0", "1")]
                          + [c + (512, 256, "1", M.MOE_SPLIT_TAIL) for c in RAGGED_SPLIT]
+                         + [c + (512, 256, "0", M.MOE_SPLIT_TAIL) for c in RAGGED_SPLIT]   # pair gather4 + swap tails
+                         + [c + (512, 256, "0", M.MOE_SCHED_DYNAMIC | M.MOE_ORDER_HALF_INTERVAL) for c in RAGGED_WIDE]
                          + [c[:5] + (c[5], 256, "1", f) for c in RAGGED_WIDE_BN for f in (0, M.MOE_SPLIT_TAIL)]
                          + [c + (256, 64, "1", 0) for c in RAGGED_DECODE])
 @pytest.mark.parametrize("mode", ["int", "int_bf16", "normal"])

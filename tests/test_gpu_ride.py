@@ -162,3 +162,25 @@ def test_ride_full_size_mixtral_generic(out_dtype):
     d = np.abs(got - ref)
     assert (d <= 1e-2 * (np.abs(ref) + 1)).all(), d.max()
     assert np.linalg.norm(got - ref) / np.linalg.norm(ref) <= 2e-3
+
+
+@pytest.mark.parametrize("flags", [0, M.MOE_A_GATHER4])
+def test_ride_with_gemv_tasks_fp32_and_row_map(flags):
+    """A plan holding GEMV tasks (one-row experts), ride tasks and plain tasks in one launch; gather4 A makes
+    the ride slots run as wide tiles (ride needs the cp.async rows): the same exact Y either way."""
+    rng = np.random.default_rng(77)
+    counts = [1, 2, 300, 1, 513, 777, 256, 4, 280, 3] + [600] * 8         # >= 128 other tiles: GEMV applies
+    ids = _ids_from_counts(counts, 1, rng)
+    T, E, H, N = ids.shape[0], len(counts), 128, 2048
+    rc, rr, rt, _ = omoe.buckets(ids, E)
+    plan = M.Plan(rc, H, N, 256, 512, flags, catalog=RIDE)
+    kinds = M.parse_plan_blob(plan.blob())["params"][:, 3].tolist()
+    assert kinds.count(M.MOE_KIND_GEMV) == 5 and kinds.count(M.MOE_KIND_RIDE) == 3
+    X, W = synth.make_x(77, T, H, "int"), synth.make_w(77, E, H, N, "int")
+    _, _, tok, _, _ = M.moe_route(torch.from_numpy(ids).cuda(), E)
+    perm = torch.from_numpy(rng.permutation(T).astype(np.int32)).cuda()
+    Y = torch.full((T, N), float("nan"), dtype=torch.float32, device="cuda")
+    M.moe_gemm(plan, torch.from_numpy(X).to(torch.bfloat16).cuda(), tok, torch.from_numpy(W).to(torch.bfloat16).cuda(),
+               Y=Y, row_map=perm)
+    torch.cuda.synchronize()
+    assert np.array_equal(Y.cpu().double().numpy()[perm.cpu().numpy()], omoe.expert_gemm(X, W, rt, rr))
