@@ -925,6 +925,12 @@ def run_ep(args, base):
                                        "combine rows")},
             "pct_of_peak": value / (peak * ws),
             "exchange_bytes_per_step_rank0": exch_bytes,
+            # exchange rate per GPU against NVLink's ~900 GB/s per direction.  The combine rides in
+            # the GEMM's epilogue, so the step's time outside the GEMM bounds the dispatch side: this is its rate
+            # over that time (a lower bound; oversubscribed shared-GPU runs say nothing about NVLink)
+            "dispatch_gbs_per_gpu_lower_bound": (
+                exch_bytes["dispatch_bytes"] / max(float(gathered[0][0]) - float(gathered[0][1]), 1e-6) / 1e6
+                if isinstance(exch_bytes, dict) and "dispatch_bytes" in exch_bytes else None),
             "per_rank": [{"ms_per_step": float(g[0]), "gemm_ms": float(g[1]), "gemm_tflops": float(g[2])}
                          for g in gathered],
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
