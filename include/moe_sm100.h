@@ -166,6 +166,10 @@ typedef struct { int32_t kind; int32_t m_max; } moe_tile_rule;
                                      rule does not match (the catalog's next rule applies).            */
 #define MOE_RIDE_MAX_ROWS 32
 #define MOE_GEMV_MAX_ROWS 4
+#define MOE_GEMV_MIN_SHARE 10     /* ... and only when the GEMV candidates would otherwise take >= this many
+                                     percent as many tiles (count x column tiles) as the other tasks have: a
+                                     GEMV unit streams all of K for 128 columns on one warp, a tail that a
+                                     handful of candidates does not repay              */
 #define MOE_GEMV_MIN_TILES 128    /* GEMV rules apply only when the plan's other tasks have >= this many tiles
                                      (their tensor work must cover the GEMV streams); otherwise those tasks
                                      fall through to the catalog's next rule                              */

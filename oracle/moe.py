@@ -71,6 +71,7 @@ def tiles_of(rows: int, N: int, bm: int, bn: int) -> int:
 
 KIND_GEMV = 2   # a whole task of <= m_max rows computed as a CUDA-core GEMV, outside the tile space
 GEMV_MIN_TILES = 128
+GEMV_MIN_SHARE = 10   # percent: the candidates' would-be tiles against the other tasks'
 KIND_RIDE = 3   # the tail rows ride on the two 256-column halves of the expert's last full row tile
 
 
@@ -158,9 +159,11 @@ def plan(counts, N: int, bm: int, bn: int, pad_mode: str = "max", warp_size: int
     if tasks is None:
         tasks = make_tasks(counts, bm, bn, split_tail, catalog, N)
         # GEMV rules apply only when the other tasks have >= GEMV_MIN_TILES tiles (their tensor work must
-        # cover the GEMV streams); otherwise those tasks take the next rule.
+        # cover the GEMV streams) and the candidates are >= GEMV_MIN_SHARE % of the launch's tiles (a handful
+        # does not repay the GEMV units' serial streams); otherwise they take the next rule.
         other = sum(tiles_of(t["rows"], N, t["bm"], t["bn"]) for t in tasks if t["kind"] != KIND_GEMV)
-        if any(t["kind"] == KIND_GEMV for t in tasks) and other < GEMV_MIN_TILES:
+        n_gemv = sum(1 for t in tasks if t["kind"] == KIND_GEMV and t["rows"] > 0)
+        if n_gemv and (other < GEMV_MIN_TILES or n_gemv * ceil_div(N, bn) * 100 < GEMV_MIN_SHARE * other):
             tasks = make_tasks(counts, bm, bn, split_tail, [r for r in catalog if int(r[0]) != KIND_GEMV], N)
     # Alg. 3's per-task strategies: a GEMV task has no tiles (nu = 0, so the non-empty stage leaves it out
     # of sigma / TilePrefix); its rows are computed by the GEMV strategy (R6, §6.8).

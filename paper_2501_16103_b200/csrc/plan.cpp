@@ -189,7 +189,9 @@ moe_status moe_plan_build_catalog(const int32_t* counts, int32_t E, int64_t H, i
       nu[i] = counts[i] == 0 || gemv ? 0 : ceil_div(counts[i], bm) * col_tiles;
       other_tiles += nu[i];
     }
-    if (n_gemv == 0 || other_tiles >= MOE_GEMV_MIN_TILES) break;
+    if (n_gemv == 0 || (other_tiles >= MOE_GEMV_MIN_TILES &&
+                        (int64_t)n_gemv * col_tiles * 100 >= (int64_t)MOE_GEMV_MIN_SHARE * other_tiles))
+      break;
     allow_gemv = false;                          // too little tensor work to hide the GEMV streams
   }
 

@@ -99,13 +99,16 @@ __device__ __forceinline__ void plan_body(long long m, int E, int H, int N, int 
   const long long col_tiles = (N + bn - 1) / bn;
   const long long row_tiles = (m + bm - 1) / bm;
   {
-    // GEMV only when the other tasks' tiles cover the GEMV streams (MOE_GEMV_MIN_TILES; plan.cpp)
+    // GEMV only when the other tasks' tiles cover the GEMV streams and the candidates are a real share of the
+    // launch (MOE_GEMV_MIN_TILES, MOE_GEMV_MIN_SHARE; plan.cpp)
     long long v4[4] = {m > 0 && kind != MOE_KIND_GEMV ? row_tiles * col_tiles : 0, m > 0 && kind == MOE_KIND_GEMV ? 1 : 0,
                        0, 0};
     long long t4[4];
     block_scan_incl4(v4, s_warp4, t4);
     const long long other_tiles = t4[0], gemv_any = t4[1];
-    if (gemv_any > 0 && other_tiles < MOE_GEMV_MIN_TILES) kind = kind_nogemv;
+    if (gemv_any > 0 && (other_tiles < MOE_GEMV_MIN_TILES ||
+                         gemv_any * col_tiles * 100 < (long long)MOE_GEMV_MIN_SHARE * other_tiles))
+      kind = kind_nogemv;
   }
   const long long nu = m > 0 && kind != MOE_KIND_GEMV ? row_tiles * col_tiles : 0;   // nu(T_t); GEMV: no tiles
   // MOE_ORDER_LIGHT_LAST: heavy non-empty tasks first, then the light ones (both in expert order)

@@ -72,9 +72,13 @@ def main():
         cat = parts[5] if len(parts) > 5 else "default"
         catalog = None if cat == "default" else () if cat == "none" else tuple(
             tuple(int(x) for x in r.split(".")) for r in cat.split("+"))
-        if cfg.startswith("counts"):                # countsA-B-C...: one expert per count (k = 1), Mixtral H / N
-            cnt = [int(x) for x in cfg[6:].split("-")]
-            c = synth.Config(cfg, E=len(cnt), k=1, T=sum(cnt), H=4096, N=14336, routing="custom")
+        if cfg.startswith("counts"):                # counts[H<h>N<n>_]A-B-C...: one expert per count (k = 1)
+            body, hh, nn = cfg[6:], 4096, 14336     # (default: Mixtral H / N)
+            if body.startswith("H"):
+                dims, body = body.split("_", 1)
+                hh, nn = (int(x) for x in dims[1:].split("N"))
+            cnt = [int(x) for x in body.split("-")]
+            c = synth.Config(cfg, E=len(cnt), k=1, T=sum(cnt), H=hh, N=nn, routing="custom")
             ids_np = np.repeat(np.arange(len(cnt), dtype=np.int32), cnt)[:, None]
         elif cfg.startswith("rows"):                  # rowsR_E: E experts of R rows each, Mixtral H / N (tile-kind cost)
             r_, e_ = (int(x) for x in cfg[4:].split("_"))

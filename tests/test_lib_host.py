@@ -375,3 +375,19 @@ def test_ep_peer_create_rejects_decode_tiles_before_touching_the_device():
     st = L.moe_ep_peer_create(0, 2, 8, 64, 256, 16, 2, 8192, 8192, ctypes.byref(out), blob)
     assert moe_lib.MOE_ERR[st] == "UNSUPPORTED" and not out.value
     assert b"bm = 64" in L.moe_last_error()
+
+
+def test_gemv_share_rule():
+    """MOE_GEMV_MIN_SHARE: a handful of <= 4-row experts next to a long launch stay tiles (their
+    GEMV units' serial K streams outlast the launch: measured 223 -> 343 us on the DeepSeek shape with four such
+    experts), many of them (the paper's worst case) become GEMV units; host planner = oracle."""
+    ds = synth.CONFIGS["ds"]
+    cnt = [int(x) for x in np.bincount(synth.route(ds, 0).ravel(), minlength=ds.E) if x > 0] + [1, 2, 3, 4]
+    p = moe_lib.parse_plan_blob(moe_lib.moe_plan_build(cnt, ds.H, ds.N, 256, 512))
+    assert (p["params"][:, 3] == moe_lib.MOE_KIND_GEMV).sum() == 0
+    assert [t["kind"] for t in omoe.plan(cnt, ds.N, 256, 512, catalog=moe_lib.DEFAULT_CATALOG)["tasks"]] == \
+        p["params"][:, 3].tolist()
+    pw = synth.CONFIGS["paper_worst"]
+    cw = np.bincount(synth.route(pw, 0).ravel(), minlength=pw.E)
+    q = moe_lib.parse_plan_blob(moe_lib.moe_plan_build(cw, pw.H, pw.N, 256, 512))
+    assert (q["params"][:, 3] == moe_lib.MOE_KIND_GEMV).sum() == 56
